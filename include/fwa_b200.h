@@ -1,0 +1,171 @@
+/*
+ * fwa_b200.h — C ABI of the B200-native FlatFormer backbone (flattened window
+ * attention) hot path.  Plain pointers and sizes only; no torch types.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/proj):
+ *
+ *   fwa_b200_backbone_forward        fwa::backbone::run_backbone(PillarSet, FwaConfig,
+ *                                    BackboneParams, n_threads)   include/fwa/backbone.hpp:159-325
+ *   fwa_b200_backbone_forward_device the same, inputs/outputs already in HBM
+ *   fwa_b200_backbone_forward_batch  the same over F independent frames (one model), frame-
+ *                                    parallel inside one GPU (BASELINE config 3)
+ *   fwa_b200_sort_plan               fwa::flatten::sort(coords, WindowSpec)  include/fwa/flatten.hpp:97-120
+ *   fwa_b200_block_forward           fwa::kernels::fwa_block_forward(f, pe, params, n_groups)
+ *                                    include/fwa/kernels.hpp:636-650
+ *   fwa_b200_positional_embedding    fwa::kernels::positional_embedding  include/fwa/kernels.hpp:364-393
+ *   fwa_b200_load_params             fwa::kernels::load_params (FWAP records)  include/fwa/kernels.hpp:177-206
+ *                                    + fwa::kernels::validate  kernels.hpp:75-90
+ *   fwa_b200_generate_pillars        fwa::geometry::generate_synthetic + pillarize +
+ *                                    random_pillar_params  include/fwa/geometry.hpp:355-386, 246-300, 71-79
+ *   fwa_b200_init_params             fwa::backbone::init_backbone_params  include/fwa/backbone.hpp:83-102
+ *
+ * Status codes mirror the reference exception taxonomy (include/fwa/error.hpp:11-33),
+ * which the reference CLI maps to exit codes 2 (config/parse/schema/shape) and
+ * 3 (numeric/contract/other) (tools/fwa_cli.cpp:514-529).
+ */
+#ifndef FWA_B200_H
+#define FWA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum fwa_status {
+    FWA_OK = 0,
+    FWA_ERR_CONFIG = 1,   /* fwa::config_error   */
+    FWA_ERR_PARSE = 2,    /* fwa::parse_error    */
+    FWA_ERR_SCHEMA = 3,   /* fwa::schema_error   */
+    FWA_ERR_SHAPE = 4,    /* fwa::shape_error    */
+    FWA_ERR_NUMERIC = 5,  /* fwa::numeric_error  */
+    FWA_ERR_CONTRACT = 6, /* fwa::contract_error */
+    FWA_ERR_INTERNAL = 7,
+    FWA_ERR_CUDA = 8      /* CUDA runtime / launch failure (no reference analogue) */
+};
+
+/* Arithmetic mode of the feature path.  Integer outputs (sort, groups, drops,
+ * kept set, cache stats) are bit-exact in both modes. */
+enum fwa_precision {
+    FWA_PREC_BF16 = 0, /* tcgen05/TMEM GEMMs + mma.sync attention, bf16 operands, fp32
+                          accumulate / LN / softmax / residual (default) */
+    FWA_PREC_FP32 = 1  /* fp32 FFMA check mode (tolerance 1e-4) */
+};
+
+/* fwa::backbone::FwaConfig (backbone.hpp:22-34).  Window metres are
+ * window_p{x,y} * resolution computed in fp64, exactly as window_x_m(). */
+typedef struct fwa_config {
+    double resolution;
+    int32_t window_px, window_py;
+    int32_t group_size;
+    int32_t n_blocks;
+    int32_t d_model, n_heads, d_ff;
+} fwa_config_t;
+
+/* fwa::backbone::BackboneOutput (backbone.hpp:128-135); caller-allocated.
+ * features: capacity N*d_model (rows in ascending-id "active" order);
+ * kept_indices: capacity N; dropped_ids: capacity N (per block, in sorted
+ * tail order, blocks concatenated); dropped_per_block: n_blocks;
+ * block_perms (optional, may be NULL; single-frame calls only): n_blocks x N,
+ * row b holds block b's permutation as local indices into that block's
+ * active list (the parity hook for flatten::sort/group). */
+typedef struct fwa_output {
+    float* features;
+    int32_t* kept_indices;
+    int32_t* dropped_ids;
+    int32_t* dropped_per_block;
+    int32_t* block_perms;
+    int64_t n_kept;
+    int32_t cache_computed; /* SortStats::sorts_computed (flatten.hpp:82-86) */
+    int32_t cache_hits;     /* SortStats::cache_hits */
+} fwa_output_t;
+
+typedef struct fwa_b200_ctx fwa_b200_ctx;
+
+/* One context per device; all work is enqueued on `cuda_stream` (a
+ * cudaStream_t; NULL = the context creates its own).  Calls on one context are
+ * serialised on that stream; contexts on different devices run concurrently. */
+int fwa_b200_ctx_create(int device, void* cuda_stream, fwa_b200_ctx** out);
+void fwa_b200_ctx_destroy(fwa_b200_ctx* ctx);
+const char* fwa_b200_last_error(const fwa_b200_ctx* ctx);
+int fwa_b200_set_precision(fwa_b200_ctx* ctx, int precision);
+/* Number of CUDA kernels this context has launched so far (telemetry). */
+int64_t fwa_b200_kernel_launches(const fwa_b200_ctx* ctx);
+/* 1 if the tcgen05 bf16 path serves `cfg`, 0 if the fp32 SIMT kernels do. */
+int fwa_b200_fast_path(const fwa_b200_ctx* ctx, const fwa_config_t* cfg);
+
+/* Parse n_blocks back-to-back FWAP records (kernels.hpp:149-206), validate
+ * shapes against cfg (config_error / shape_error / parse_error as the
+ * reference), upload fp32 + bf16 copies to HBM.  Params stay resident. */
+int fwa_b200_load_params(fwa_b200_ctx* ctx, const fwa_config_t* cfg, const void* fwap_blob,
+                         size_t blob_len);
+
+/* run_backbone with HOST buffers: coords N x 2 f64 (pillar centres),
+ * feats N x d_model, f64 if feats_is_f64 (cast to f32 on device exactly as
+ * backbone.hpp:195-196) else f32.  Blocks until `out` is filled. */
+int fwa_b200_backbone_forward(fwa_b200_ctx* ctx, const double* coords, const void* feats,
+                              int feats_is_f64, int64_t n, const fwa_config_t* cfg,
+                              fwa_output_t* out);
+
+/* Same over F frames concatenated along rows: frame f owns rows
+ * [frame_offsets[f], frame_offsets[f+1]).  Each frame is an independent
+ * run_backbone (own sort, groups, drops); outputs are concatenated per frame
+ * (kept ids are global row ids); out->n_kept is the total, kept_per_frame
+ * (optional, capacity F) receives per-frame counts. cache stats are per frame
+ * (identical for every frame). */
+int fwa_b200_backbone_forward_batch(fwa_b200_ctx* ctx, const double* coords, const void* feats,
+                                    int feats_is_f64, const int64_t* frame_offsets, int n_frames,
+                                    const fwa_config_t* cfg, fwa_output_t* out,
+                                    int64_t* kept_per_frame);
+
+/* Device-resident variant (inputs already in HBM, outputs written to HBM,
+ * enqueued on the context stream without a trailing host sync).  d_feats is
+ * f32.  d_out_features: capacity N*d_model; d_out_kept: capacity N (may be
+ * NULL).  *n_kept_out is known on the host before the call returns (it depends
+ * only on N and group_size).  Single frame, or batch when frame_offsets != NULL. */
+int fwa_b200_backbone_forward_device(fwa_b200_ctx* ctx, const double* d_coords,
+                                     const float* d_feats, const int64_t* frame_offsets,
+                                     int n_frames, const fwa_config_t* cfg,
+                                     float* d_out_features, int32_t* d_out_kept,
+                                     int64_t* n_kept_out);
+
+/* flatten::sort (minimum slice): host coords in, host permutation out. */
+int fwa_b200_sort_plan(fwa_b200_ctx* ctx, const double* coords, int64_t n, double w_x,
+                       double w_y, int shift, int major_axis_y, int32_t* perm_out);
+
+/* fwa_block_forward on pre-grouped host rows f, pe (rows x D f32; rows =
+ * n_groups * G) with ONE FWAP record.  Uses the context precision. */
+int fwa_b200_block_forward(fwa_b200_ctx* ctx, const float* f, const float* pe, int64_t rows,
+                           int32_t n_groups, const void* fwap_record, size_t record_len,
+                           float* out);
+
+/* positional_embedding: host coords N x 2 f64 -> host N x d f32. */
+int fwa_b200_positional_embedding(fwa_b200_ctx* ctx, const double* coords, int64_t n,
+                                  int32_t d_model, float* out);
+
+/* ---- host-side input generators (bit-identical to the reference's) ---- */
+
+/* geometry::SceneSpec (geometry.hpp:310-319). */
+typedef struct fwa_scene_spec {
+    int32_t n_clusters, points_per_cluster_min, points_per_cluster_max;
+    double cluster_sigma, extent_x, extent_y;
+    int32_t n_background, f_in;
+} fwa_scene_spec_t;
+
+/* generate_synthetic(spec, seed) -> pillarize(cloud, resolution,
+ * random_pillar_params(f_in, d_out, param_seed)).  Two-phase: call with
+ * coords == NULL to get the pillar count, then again with buffers
+ * (coords N x 2 f64, feats N x d_out f64).  Returns N or -status. */
+int64_t fwa_b200_generate_pillars(const fwa_scene_spec_t* spec, uint64_t seed, double resolution,
+                                  int32_t d_out, uint64_t param_seed, double* coords,
+                                  double* feats);
+
+/* init_backbone_params(cfg, f_in == d_model, seed) as FWAP records.  Returns
+ * the blob length (out may be NULL to size) or -status. */
+int64_t fwa_b200_init_params(const fwa_config_t* cfg, uint64_t seed, void* out, size_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FWA_B200_H */
