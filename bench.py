@@ -1,0 +1,351 @@
+"""FlatFormer backbone forward on B200 — the driver's benchmark contract.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): the full 8-block FlatFormer backbone
+(alternating x/y window sort + shifted windows, G 69, D 128, 8 heads, D_ff 256) on
+the F60 synthetic frame (reference generate_synthetic + pillarize, 60,897 pillars
+at seed 42), one frame per GPU per step.  Under torchrun (N > 1) rank r processes
+its own F60 frame (seed 42 + r): frames are independent, no collective on the data
+path ("scaling": "weak").
+
+`value`  pillars/s over all ranks, inputs resident in HBM, device time (CUDA events
+         on the context stream, L2 flushed by a 256 MiB write before every step),
+         max over ranks.
+`e2e`    the same metric through the reference-facing API (run_backbone on pinned
+         HOST PillarSet buffers: coords f64 + features f64 in, features + kept +
+         dropped ids out), host<->device copies inside the timed region.
+`roofline` the dominant kernel, from the live stage timers (CUDA events) of the
+         timed region; `cpu_baseline` the reference itself (oracle/_ref, the
+         unmodified headers compiled with -O3) timed on this host, rank 0, N = 1.
+
+`--impl reference` times the reference's own CPU run_backbone (oracle/_ref, or the C
+restatement when _ref is absent) on the same frame with all host threads; each
+step is a bounded sample (one block of the frame) extrapolated to the 8 blocks.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "pillars/sec and ms/frame, FlatFormer backbone fwd, 1/2/4/8 B200 vs CPU ref"
+FLOP_PER_ROW = {"ln1_qkv": 2 * 128 * 384, "attention": 2 * 2 * 69 * 128,
+                "outproj_ffn": 2 * (128 * 128 + 2 * 128 * 256)}  # 297,472 per kept pillar per block
+WORKLOAD = "F60 frame (60,897 pillars), full FlatFormer backbone: 8 blocks, G 69, D 128, H 8, D_ff 256"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], p["bf16_tflops"], p["bf16_tflops_sustained"], "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms while running."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": len(self.rows)}
+        if self.rows:
+            sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+            mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+            out["sm_mhz"] = statistics.median(sm) if sm else None
+            out["sm_max_mhz"] = max(mx) if mx else None
+            reasons = set()
+            for r in self.rows:
+                for name, v in zip(self.NAMES, r[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(name)
+            out["reasons"] = sorted(reasons)
+        return out
+
+
+def cpu_reference_sample(ps, n_threads, blocks_run=1, n_blocks_metric=8, seed=42):
+    """The reference run_backbone (oracle/_ref, else the C restatement) on `blocks_run`
+    blocks of the frame with n_threads threads; returns (seconds, kind, cores)."""
+    import oracle as O
+    cfg = O.make_cfg(n_blocks=blocks_run)
+    if O.have_ref():
+        blob = O.ref_init_params(cfg, 128, seed)
+        t0 = time.perf_counter()
+        O.ref_run_backbone(ps.coords, ps.features, cfg, blob, n_threads=n_threads)
+        return time.perf_counter() - t0, "reference", n_threads
+    import paper_2301_08739_b200 as F
+    blob = F.init_backbone_params(F.FwaConfig(n_blocks=blocks_run), seed)
+    t0 = time.perf_counter()
+    O.port_run_backbone(ps.coords, ps.features.astype(np.float32), cfg, blob)
+    return time.perf_counter() - t0, "port", 1
+
+
+def run_reference(args, rank):
+    import paper_2301_08739_b200 as F
+    if rank != 0:
+        return
+    ps = F.make_pillars(F.SCENES["F60"], 42)
+    n = ps.size()
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_reference_sample(ps, threads)
+    times = []
+    kind = cores = None
+    for _ in range(args.steps):
+        t, kind, cores = cpu_reference_sample(ps, threads)
+        times.append(t * 8)  # one block sampled, extrapolated to the 8-block backbone
+    ms = 1e3 * statistics.mean(times)
+    value = n / (ms / 1e3)
+    line = {
+        "metric": METRIC, "value": value, "unit": "pillars/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "ms_per_frame": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+        "data": "synthetic (reference generate_synthetic + pillarize, F60 seed 42)",
+        "config": {"workload": WORKLOAD, "pillars_per_frame": n, "frames_per_step": 1},
+        "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": "pillars/s", "cores": cores, "kind": kind,
+                         "sample": "1 of 8 blocks of run_backbone on the F60 frame per step "
+                                   "(block 0: X axis, no shift), time x8",
+                         "cpu": _cpu_model()},
+        "e2e": {"value": value, "unit": "pillars/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _cpu_model():
+    try:
+        for l in open("/proc/cpuinfo"):
+            if l.startswith("model name"):
+                return l.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_ours(args, rank, world, local_rank, dist):
+    import torch
+
+    import paper_2301_08739_b200 as F
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.current_stream(dev)
+    ctx = F.Context(local_rank, stream=stream.cuda_stream, precision="bf16")
+    cfg = F.FwaConfig()
+    blob = F.init_backbone_params(cfg, 42)
+    ctx.load_params(cfg, blob)
+    ps = F.make_pillars(F.SCENES["F60"], 42 + rank)
+    n = ps.size()
+    nk = (n // cfg.group_size) * cfg.group_size
+
+    # ---------------------------------------------------------------- device-resident inputs
+    d_coords = torch.from_numpy(ps.coords).to(dev)
+    d_feats = torch.from_numpy(ps.features.astype(np.float32)).to(dev)
+    d_out = torch.empty((n, cfg.d_model), dtype=torch.float32, device=dev)
+    d_kept = torch.empty(n, dtype=torch.int32, device=dev)
+    off = [0, n]
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        return ctx.forward_device(d_coords.data_ptr(), d_feats.data_ptr(), off, cfg,
+                                  d_out.data_ptr(), d_kept.data_ptr())
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    ctx.set_profiling(True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.kernel_launches
+    for i in range(args.steps):
+        flush.zero_()  # L2 flush (256 MiB write > 126 MB L2) outside the timed events
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches = ctx.kernel_launches - launches0
+    prof = ctx.profile()
+    ctx.set_profiling(False)
+    dev_ms = sum(a.elapsed_time(b) for a, b in ev)
+    # ---------------------------------------------------------------- e2e via the host API
+    pin = dict(pin_memory=True)
+    h_coords = torch.from_numpy(ps.coords).pin_memory()
+    h_feats = torch.from_numpy(ps.features).pin_memory()          # PillarSet features, f64
+    h_out = torch.empty((n, cfg.d_model), dtype=torch.float32, **pin)
+    h_kept = torch.empty(n, dtype=torch.int32, **pin)
+    h_drop = torch.empty(max(n, 1), dtype=torch.int32, **pin)
+    h_dpb = torch.empty(cfg.n_blocks, dtype=torch.int32, **pin)
+
+    def e2e_step():
+        return ctx.run_backbone_ptrs(h_coords.data_ptr(), h_feats.data_ptr(), True, n, cfg,
+                                     h_out.data_ptr(), h_kept.data_ptr(), h_drop.data_ptr(),
+                                     h_dpb.data_ptr())
+
+    for _ in range(max(1, args.warmup)):
+        flush.zero_()
+        torch.cuda.synchronize()
+        e2e_step()
+    e2e_s = 0.0
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        nk_e2e, cache = e2e_step()
+        e2e_s += time.perf_counter() - t0
+    clk = clocks.stop()
+    assert nk_e2e == nk
+
+    # ---------------------------------------------------------------- reduce over ranks
+    t_dev = torch.tensor([dev_ms, e2e_s, float(n), float(nk)], dtype=torch.float64, device=dev)
+    if dist:
+        mx = t_dev.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = t_dev.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        dev_ms_max, e2e_max = float(mx[0]), float(mx[1])
+        pillars_all, kept_all = float(sm[2]), float(sm[3])
+    else:
+        dev_ms_max, e2e_max, pillars_all, kept_all = dev_ms, e2e_s, float(n), float(nk)
+    if rank != 0:
+        return
+    ms_per_step = dev_ms_max / args.steps
+    value = pillars_all * args.steps / (dev_ms_max / 1e3)
+    e2e_value = pillars_all * args.steps / e2e_max
+
+    hbm, pk_burst, pk_sus, pk_kind = peaks()
+    kernels = {}
+    for k, rows_flop in FLOP_PER_ROW.items():
+        tot_ms, calls = prof[k]
+        if calls:
+            avg = tot_ms / calls
+            flop = rows_flop * nk
+            kernels[k] = {"avg_ms": avg, "calls": calls, "tflops": flop / (avg / 1e3) / 1e12,
+                          "frac_of_sustained": flop / (avg / 1e3) / 1e12 / pk_sus}
+    for k in ("schedule", "pe"):
+        tot_ms, calls = prof[k]
+        if calls:
+            kernels[k] = {"avg_ms": tot_ms / calls, "calls": calls}
+    if prof["schedule"][1]:
+        # sort/group/drop/compaction bytes per call: coords 16 B + per spec (4 specs):
+        # keys 32 B write + 32 B read, bin id 4+4, scatter 4+4, per-bin sort 4+16+4 read/write,
+        # compaction 4+1+4+4 (SURVEY §8d counts 16 B in + 4 B perm out per pillar per spec)
+        alg = n * (16 + 4 * 4)
+        kernels["schedule"]["algorithmic_gbs"] = alg / (kernels["schedule"]["avg_ms"] / 1e3) / 1e9
+    dom = max(FLOP_PER_ROW, key=lambda k: prof[k][0])
+    dk = kernels[dom]
+    roofline = {"bound": "tensor", "kernel": dom, "achieved": dk["tflops"], "peak": pk_sus,
+                "unit": "TFLOP/s", "frac": dk["tflops"] / pk_sus, "traffic": None,
+                "peak_kind": f"{pk_kind} bf16 sustained (kernel timed inside the step)",
+                "flop_per_launch": FLOP_PER_ROW[dom] * nk}
+    tot_flop = 297472 * nk * 8
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        t, kind, cores = cpu_reference_sample(ps, threads)
+        cpu = {"value": n / (t * 8), "unit": "pillars/s", "cores": cores, "kind": kind,
+               "sample": "1 of 8 blocks of run_backbone on the same F60 frame (block 0), "
+                         "time x8; all host threads", "cpu": _cpu_model()}
+    h2d = n * 16 + n * cfg.d_model * 8
+    d2h = nk * cfg.d_model * 4 + nk * 4 + (n - nk) * 4 + 4
+    line = {
+        "metric": METRIC, "value": value, "unit": "pillars/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "ms_per_frame": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (reference generate_synthetic + pillarize, F60 seed 42 + rank; "
+                "init_backbone_params seed 42)",
+        "config": {"workload": WORKLOAD, "pillars_per_frame": n, "kept_per_frame": nk,
+                   "frames_per_step_per_gpu": 1, "parallelism": f"frame-parallel x{world}",
+                   "l2": "flushed by a 256 MiB write before every timed step",
+                   "precision": "bf16 tensor cores, fp32 accumulate/LN/softmax/residual"},
+        "e2e": {"value": e2e_value, "unit": "pillars/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_frame": 1e3 * e2e_max / args.steps},
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "gpu_launches": launches,
+        "clocks": clk,
+        "kernels": kernels,
+        "frame_tflops": tot_flop / (ms_per_step / 1e3) / 1e12,
+        "frame_frac_of_sustained": tot_flop / (ms_per_step / 1e3) / 1e12 / pk_sus,
+        "cache": {"computed": cache[0], "hits": cache[1]},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(local_rank)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dist = tdist
+    try:
+        run_ours(args, rank, world, local_rank, dist)
+    finally:
+        if dist:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -92,6 +92,23 @@ const char* fwa_b200_last_error(const fwa_b200_ctx* ctx);
 int fwa_b200_set_precision(fwa_b200_ctx* ctx, int precision);
 /* Number of CUDA kernels this context has launched so far (telemetry). */
 int64_t fwa_b200_kernel_launches(const fwa_b200_ctx* ctx);
+/* Stage timers on the context stream (CUDA events), the analogue of the
+ * reference's StageTimer/StageTimes (backbone.hpp:109-151).  Enabling resets the
+ * accumulators; fwa_b200_get_profile synchronises the stream and returns the
+ * accumulated milliseconds and call counts per slot (arrays of FWA_PROF_SLOTS). */
+enum fwa_prof_slot {
+    FWA_PROF_SCHEDULE = 0,     /* window sorts + groups + drops + kept set (sort/group stages) */
+    FWA_PROF_PE = 1,           /* positional embedding */
+    FWA_PROF_LN_QKV = 2,       /* gather + LN1 + PE + packed QKV */
+    FWA_PROF_ATTENTION = 3,    /* per-group MHSA */
+    FWA_PROF_OUTPROJ_FFN = 4,  /* out-proj + residual + LN2 + FFN + residual + scatter */
+    FWA_PROF_H2D = 5,
+    FWA_PROF_D2H = 6,
+    FWA_PROF_SLOTS = 7
+};
+int fwa_b200_set_profiling(fwa_b200_ctx* ctx, int enable);
+int fwa_b200_get_profile(fwa_b200_ctx* ctx, double* ms, int64_t* counts);
+
 /* 1 if the tcgen05 bf16 path serves `cfg`, 0 if the fp32 SIMT kernels do. */
 int fwa_b200_fast_path(const fwa_b200_ctx* ctx, const fwa_config_t* cfg);
 

@@ -1,0 +1,920 @@
+// Host driver + C ABI for the B200 FlatFormer backbone forward.
+//
+// Mirrors fwa::backbone::run_backbone (/root/reference/proj/include/fwa/backbone.hpp:159-325):
+// same inputs (pillar centres + features), config fields, FWAP parameters,
+// outputs (features in ascending-id active order, kept ids, per-block dropped
+// ids in tail order, sort-cache stats) and error taxonomy.
+//
+// B200-first structure:
+//   * the whole index schedule (4 window sorts, groups, drops, kept set) depends
+//     only on coordinates, so it is built ONCE per call in one batched device
+//     sort (sort.cu) before any feature math; every block then is
+//     gather -> LN1+PE -> QKV -> group attention -> out-proj+FFN -> scatter over
+//     precomputed index arrays, with the residual stream kept in fp32 in HBM,
+//     indexed by pillar id;
+//   * the plan-cache statistics the reference reports (computed/hits) are
+//     reproduced by simulating its cache rule (backbone.hpp:224-234, 314) on the host;
+//   * frames of a batch are concatenated: windows carry the frame id, groups
+//     never cross frames, one launch sequence serves all frames.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "fwa_b200.h"
+#include "internal.h"
+
+using namespace fwa_b200;
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+};
+
+struct BlockParams {
+    // fp32 tensors (device), FWAP field order
+    const float *w_qkv, *b_qkv, *w_out, *b_out, *ln1_g, *ln1_b, *ln2_g, *ln2_b, *w1, *b1, *w2, *b2;
+    TcBlockWeights tc{};
+};
+
+} // namespace
+
+struct fwa_b200_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::string err;
+    int precision = FWA_PREC_BF16;
+    int64_t launches = 0;
+    bool have_params = false;
+    fwa_config_t pcfg{};
+    DevBuf params_f32, params_bf16;
+    std::vector<BlockParams> blocks;
+    std::map<std::string, DevBuf> ws;
+    int freq_d = 0;
+    DevBuf freq;
+    int* d_flag = nullptr;     // non-finite input flag
+    int* h_flag = nullptr;     // pinned
+    long long* h_minmax = nullptr;  // pinned (16)
+    // stage profiling (the analogue of the reference's StageTimer, backbone.hpp:139-151)
+    bool profiling = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    struct Pending { int slot; cudaEvent_t a, b; };
+    std::vector<Pending> pending;
+    double prof_ms[FWA_PROF_SLOTS] = {};
+    int64_t prof_n[FWA_PROF_SLOTS] = {};
+};
+
+namespace {
+
+struct FwaError {
+    int code;
+    std::string msg;
+};
+
+#define CUDA_OK(expr)                                                                      \
+    do {                                                                                   \
+        cudaError_t e_ = (expr);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            throw FwaError{FWA_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)}; \
+    } while (0)
+
+template <class T>
+T* ws(fwa_b200_ctx* c, const char* name, size_t count) {
+    DevBuf& b = c->ws[name];
+    const size_t bytes = std::max<size_t>(count * sizeof(T), 256);
+    if (b.cap < bytes) {
+        if (b.p) cudaFree(b.p);
+        b.p = nullptr;
+        size_t want = std::max(bytes, b.cap + b.cap / 2);
+        CUDA_OK(cudaMalloc(&b.p, want));
+        b.cap = want;
+    }
+    return static_cast<T*>(b.p);
+}
+
+cudaEvent_t prof_event(fwa_b200_ctx* c) {
+    if (c->ev_used == c->ev_pool.size()) {
+        cudaEvent_t e;
+        CUDA_OK(cudaEventCreate(&e));
+        c->ev_pool.push_back(e);
+    }
+    return c->ev_pool[c->ev_used++];
+}
+
+// RAII stage timer on the context stream (no-op unless profiling is enabled).
+struct StageEv {
+    fwa_b200_ctx* c;
+    int slot;
+    cudaEvent_t a = nullptr;
+    StageEv(fwa_b200_ctx* c_, int slot_) : c(c_), slot(slot_) {
+        if (c->profiling) {
+            a = prof_event(c);
+            cudaEventRecord(a, c->stream);
+        }
+    }
+    ~StageEv() {
+        if (a) {
+            cudaEvent_t b = prof_event(c);
+            cudaEventRecord(b, c->stream);
+            c->pending.push_back({slot, a, b});
+        }
+    }
+};
+
+void prof_collect(fwa_b200_ctx* c) {
+    if (c->pending.empty()) return;
+    cudaStreamSynchronize(c->stream);
+    for (auto& p : c->pending) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+            c->prof_ms[p.slot] += ms;
+            c->prof_n[p.slot] += 1;
+        }
+    }
+    c->pending.clear();
+    c->ev_used = 0;
+}
+
+// FWA_B200_SYNC_DEBUG=1: synchronise after every launch group and name the failing stage.
+bool sync_debug() {
+    static const bool on = [] {
+        const char* v = std::getenv("FWA_B200_SYNC_DEBUG");
+        return v && v[0] == '1';
+    }();
+    return on;
+}
+
+void check_launch(const char* what = "kernel launch") {
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess && sync_debug()) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) throw FwaError{FWA_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+// backbone.hpp:36-47
+void validate_cfg(const fwa_config_t* c) {
+    if (!c) throw FwaError{FWA_ERR_CONFIG, "config: null"};
+    if (!(c->resolution > 0.0)) throw FwaError{FWA_ERR_CONFIG, "config: resolution must be > 0"};
+    if (c->window_px < 1 || c->window_py < 1)
+        throw FwaError{FWA_ERR_CONFIG, "config: window dims must be >= 1"};
+    if (c->group_size < 1) throw FwaError{FWA_ERR_CONFIG, "config: group_size must be >= 1"};
+    if (c->n_blocks < 1) throw FwaError{FWA_ERR_CONFIG, "config: n_blocks must be >= 1"};
+    if (c->d_model < 4 || c->d_model % 4 != 0)
+        throw FwaError{FWA_ERR_CONFIG, "config: d_model must be divisible by 4"};
+    if (c->n_heads < 1 || c->d_model % c->n_heads != 0)
+        throw FwaError{FWA_ERR_CONFIG, "config: d_model must be divisible by n_heads"};
+    if (c->d_ff < 1) throw FwaError{FWA_ERR_CONFIG, "config: d_ff must be >= 1"};
+}
+
+bool fast_path_ok(const fwa_b200_ctx* c, int d, int h, int dff, int G) {
+    return c->precision == FWA_PREC_BF16 && d == 128 && dff == 256 && h > 0 && d / h == 16 &&
+           G >= 1 && G <= 128;
+}
+
+size_t record_floats(int d, int dff) {
+    return static_cast<size_t>(3 * d * d + 3 * d + d * d + d + 4 * d + dff * d + dff + d * dff + d);
+}
+
+struct Record {
+    int d, h, dff;
+    const float* t;  // host pointer into the blob (may be unaligned -> copied)
+};
+
+// FWAP records (kernels.hpp:149-206).  Throws parse_error like load_params.
+std::vector<Record> parse_fwap(const void* blob, size_t len, std::vector<std::vector<float>>& keep) {
+    std::vector<Record> out;
+    const uint8_t* p = static_cast<const uint8_t*>(blob);
+    size_t off = 0;
+    while (off < len) {
+        if (len - off < 4 || std::memcmp(p + off, "FWAP", 4) != 0)
+            throw FwaError{FWA_ERR_PARSE, "bad magic, expected FWAP"};
+        if (len - off < 16) throw FwaError{FWA_ERR_PARSE, "truncated FWAP header"};
+        uint32_t dims[3];
+        std::memcpy(dims, p + off + 4, 12);
+        const int d = static_cast<int>(dims[0]), h = static_cast<int>(dims[1]), f = static_cast<int>(dims[2]);
+        // zero_attn_params -> validate (kernels.hpp:75-90, 92-114)
+        if (d < 1 || h < 1 || f < 1) throw FwaError{FWA_ERR_CONFIG, "attn params: dims must be >= 1"};
+        if (d % h != 0) throw FwaError{FWA_ERR_CONFIG, "attn params: d_model must be divisible by n_heads"};
+        const size_t nf = record_floats(d, f);
+        if (len - off - 16 < nf * 4) throw FwaError{FWA_ERR_PARSE, "truncated FWAP tensor"};
+        keep.emplace_back(nf);
+        std::memcpy(keep.back().data(), p + off + 16, nf * 4);
+        out.push_back(Record{d, h, f, keep.back().data()});
+        off += 16 + nf * 4;
+    }
+    return out;
+}
+
+__global__ void k_out_pos(const int32_t* __restrict__ idx, const uint32_t* __restrict__ rank,
+                          int64_t n, int32_t* __restrict__ out) {
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r < n) out[r] = static_cast<int32_t>(rank[idx[r]]);
+}
+
+__global__ void k_cast_f64_f32(const double* __restrict__ in, int64_t n, float* __restrict__ out) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = static_cast<float>(in[i]);
+}
+
+std::vector<BlockParams> upload_block_params(const std::vector<Record>& recs, DevBuf& pf32,
+                                             DevBuf& pbf16, cudaStream_t st) {
+    const int d = recs[0].d, dff = recs[0].dff;
+    const size_t nf = record_floats(d, dff);
+    const size_t nb = recs.size();
+    std::vector<float> host(nf * nb);
+    for (size_t b = 0; b < nb; ++b) std::memcpy(host.data() + b * nf, recs[b].t, nf * 4);
+    const size_t bytes = host.size() * 4;
+    if (pf32.cap < bytes) {
+        if (pf32.p) cudaFree(pf32.p);
+        pf32.p = nullptr;
+        CUDA_OK(cudaMalloc(&pf32.p, bytes));
+        pf32.cap = bytes;
+    }
+    CUDA_OK(cudaMemcpyAsync(pf32.p, host.data(), bytes, cudaMemcpyHostToDevice, st));
+    const float* base = static_cast<const float*>(pf32.p);
+    std::vector<BlockParams> blocks(nb);
+    const bool tc = d == 128 && dff == 256;
+    const size_t tc_elems = 384 * 128 + 128 * 128 + 256 * 128 + 128 * 256;
+    std::vector<uint16_t> sw;
+    if (tc) {
+        sw.assign(tc_elems * nb, 0);
+        const size_t tb = sw.size() * 2;
+        if (pbf16.cap < tb) {
+            if (pbf16.p) cudaFree(pbf16.p);
+            pbf16.p = nullptr;
+            CUDA_OK(cudaMalloc(&pbf16.p, tb));
+            pbf16.cap = tb;
+        }
+    }
+    for (size_t b = 0; b < nb; ++b) {
+        const float* t = base + b * nf;
+        BlockParams& bp = blocks[b];
+        bp.w_qkv = t; t += 3 * d * d;
+        bp.b_qkv = t; t += 3 * d;
+        bp.w_out = t; t += d * d;
+        bp.b_out = t; t += d;
+        bp.ln1_g = t; t += d;
+        bp.ln1_b = t; t += d;
+        bp.ln2_g = t; t += d;
+        bp.ln2_b = t; t += d;
+        bp.w1 = t; t += dff * d;
+        bp.b1 = t; t += dff;
+        bp.w2 = t; t += d * dff;
+        bp.b2 = t;
+        if (tc) {
+            const float* h = host.data() + b * nf;
+            const float* hw_qkv = h;
+            const float* hw_out = h + 3 * d * d + 3 * d;
+            const float* hw1 = hw_out + d * d + d + 4 * d;
+            const float* hw2 = hw1 + dff * d + dff;
+            uint16_t* o = sw.data() + b * tc_elems;
+            swizzle_weight_bf16(hw_qkv, 384, 128, o);
+            swizzle_weight_bf16(hw_out, 128, 128, o + 384 * 128);
+            swizzle_weight_bf16(hw1, 256, 128, o + 384 * 128 + 128 * 128);
+            swizzle_weight_bf16(hw2, 128, 256, o + 384 * 128 + 128 * 128 + 256 * 128);
+            const __nv_bfloat16* dbase =
+                static_cast<const __nv_bfloat16*>(pbf16.p) + b * tc_elems;
+            bp.tc.w_qkv = dbase;
+            bp.tc.w_out = dbase + 384 * 128;
+            bp.tc.w1 = dbase + 384 * 128 + 128 * 128;
+            bp.tc.w2 = dbase + 384 * 128 + 128 * 128 + 256 * 128;
+            bp.tc.b_qkv = bp.b_qkv;
+            bp.tc.b_out = bp.b_out;
+            bp.tc.ln1_g = bp.ln1_g;
+            bp.tc.ln1_b = bp.ln1_b;
+            bp.tc.ln2_g = bp.ln2_g;
+            bp.tc.ln2_b = bp.ln2_b;
+            bp.tc.b1 = bp.b1;
+            bp.tc.b2 = bp.b2;
+        }
+    }
+    if (tc) CUDA_OK(cudaMemcpyAsync(pbf16.p, sw.data(), sw.size() * 2, cudaMemcpyHostToDevice, st));
+    CUDA_OK(cudaStreamSynchronize(st));  // host staging vectors die on return
+    return blocks;
+}
+
+const double* pe_freq(fwa_b200_ctx* c, int d) {
+    if (c->freq_d != d) {
+        const int nf = d / 4;
+        std::vector<double> f(static_cast<size_t>(nf));
+        const double f_min = 1.0 / 10000.0, f_max = 1.0;
+        for (int k = 0; k < nf; ++k)  // kernels.hpp:373-377
+            f[static_cast<size_t>(k)] =
+                nf == 1 ? f_min : f_min * std::pow(f_max / f_min, static_cast<double>(k) / (nf - 1));
+        if (c->freq.p) cudaFree(c->freq.p);
+        c->freq.p = nullptr;
+        CUDA_OK(cudaMalloc(&c->freq.p, f.size() * 8));
+        CUDA_OK(cudaMemcpyAsync(c->freq.p, f.data(), f.size() * 8, cudaMemcpyHostToDevice, c->stream));
+        CUDA_OK(cudaStreamSynchronize(c->stream));
+        c->freq_d = d;
+    }
+    return static_cast<const double*>(c->freq.p);
+}
+
+// ------------------------------------------------------------------ schedule
+
+struct Schedule {
+    int64_t ntot = 0, K = 0, n_drop = 0;
+    int n_frames = 0, n_specs = 0;
+    std::vector<int64_t> off, rows, drop, drop_off;
+    int32_t* sorted = nullptr;     // n_specs x ntot, full-set plans
+    int32_t* idx = nullptr;        // n_specs x K, kept-restricted plans
+    uint8_t* dropped = nullptr;    // ntot
+    uint32_t* kept_rank = nullptr; // ntot
+    int32_t* kept_ids = nullptr;   // K
+    int32_t* dropped_ids = nullptr;
+    int32_t* out_pos = nullptr;    // K: output row of the last block's row r
+};
+
+void host_frames(const int64_t* off, int n_frames, int G, Schedule& S) {
+    S.n_frames = n_frames;
+    S.off.assign(off, off + n_frames + 1);
+    S.rows.resize(static_cast<size_t>(n_frames));
+    S.drop.resize(static_cast<size_t>(n_frames));
+    S.drop_off.assign(static_cast<size_t>(n_frames) + 1, 0);
+    S.ntot = S.off[static_cast<size_t>(n_frames)];
+    S.K = 0;
+    for (int f = 0; f < n_frames; ++f) {
+        const int64_t n = S.off[f + 1] - S.off[f];
+        if (n < 0) throw FwaError{FWA_ERR_SHAPE, "frame offsets must be non-decreasing"};
+        if (n < G)  // backbone.hpp:218-222
+            throw FwaError{FWA_ERR_NUMERIC, "backbone: block 0 has " + std::to_string(n) +
+                                                " pillars, fewer than group size " + std::to_string(G) +
+                                                "; refusing to emit empty output"};
+        S.rows[f] = (n / G) * G;
+        S.drop[f] = n - S.rows[f];
+        S.drop_off[f + 1] = S.drop_off[f] + S.drop[f];
+        S.K += S.rows[f];
+    }
+    S.n_drop = S.drop_off[static_cast<size_t>(n_frames)];
+    if (S.ntot > INT32_MAX / 4) throw FwaError{FWA_ERR_SHAPE, "too many pillars for int32 ids"};
+}
+
+// K1..K4 for n_specs specs of nf frames: returns the n_specs x ntot full-set plans.
+int32_t* sort_specs(fwa_b200_ctx* c, const double* d_coords, int64_t ntot, int n_specs, double w_x,
+                    double w_y, const int64_t* d_off, int nf) {
+    cudaStream_t st = c->stream;
+    const int64_t total = ntot * n_specs;
+    long long* win = ws<long long>(c, "win", 2 * static_cast<size_t>(total));
+    double* loc = ws<double>(c, "loc", 2 * static_cast<size_t>(total));
+    long long* mm = ws<long long>(c, "minmax", 16);
+    launch_sort_keys(d_coords, ntot, n_specs, w_x, w_y, win, loc, mm, st, &c->launches);
+    check_launch();
+    CUDA_OK(cudaMemcpyAsync(c->h_minmax, mm, 16 * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+    SpecBins sb[4];
+    long long nbins = 0;
+    for (int s = 0; s < n_specs; ++s) {
+        const long long* m = c->h_minmax + 4 * s;
+        const long long rM = m[1] - m[0] + 1, rm = m[3] - m[2] + 1;
+        if (rM <= 0 || rm <= 0 || rM > (1LL << 31) || rm > (1LL << 31) ||
+            static_cast<double>(rM) * static_cast<double>(rm) * nf > 1.5e9)
+            throw FwaError{FWA_ERR_INTERNAL,
+                           "window index range too large for the dense window-bin sort"};
+        sb[s] = SpecBins{m[0], m[2], rm, rM * rm, nbins};
+        nbins += rM * rm * nf;
+    }
+    if (nbins > 1500000000LL)
+        throw FwaError{FWA_ERR_INTERNAL, "window index range too large for the dense window-bin sort"};
+    SpecBins* d_sb = ws<SpecBins>(c, "specbins", 4);
+    CUDA_OK(cudaMemcpyAsync(d_sb, sb, sizeof(sb), cudaMemcpyHostToDevice, st));
+    uint32_t* hist = ws<uint32_t>(c, "hist", static_cast<size_t>(nbins));
+    uint32_t* bin_start = ws<uint32_t>(c, "bin_start", static_cast<size_t>(nbins));
+    uint32_t* scan_tmp = ws<uint32_t>(c, "scan_tmp", scan_tmp_words(std::max<int64_t>(nbins, total)) + 8);
+    uint32_t* bin_of = ws<uint32_t>(c, "bin_of", static_cast<size_t>(total));
+    CUDA_OK(cudaMemsetAsync(hist, 0, static_cast<size_t>(nbins) * 4, st));
+    launch_bins_hist(win, ntot, n_specs, d_off, nf, d_sb, bin_of, hist, st, &c->launches);
+    exclusive_scan_u32(hist, bin_start, nbins, scan_tmp, nullptr, st, &c->launches);
+    uint32_t* cursor = ws<uint32_t>(c, "cursor", static_cast<size_t>(nbins));
+    CUDA_OK(cudaMemcpyAsync(cursor, bin_start, static_cast<size_t>(nbins) * 4, cudaMemcpyDeviceToDevice, st));
+    int32_t* pre = ws<int32_t>(c, "pre", static_cast<size_t>(total));
+    launch_bin_scatter(bin_of, ntot, n_specs, cursor, pre, st, &c->launches);
+    int32_t* sorted = ws<int32_t>(c, "sorted", static_cast<size_t>(total));
+    int32_t* scratch = ws<int32_t>(c, "sort_scratch", 2 * static_cast<size_t>(total));
+    launch_bin_sort(bin_start, hist, static_cast<uint32_t>(nbins), pre, loc, ntot, sorted, scratch,
+                    st, &c->launches);
+    check_launch();
+    return sorted;
+}
+
+void build_schedule(fwa_b200_ctx* c, const double* d_coords, const fwa_config_t* cfg, Schedule& S) {
+    cudaStream_t st = c->stream;
+    const int64_t ntot = S.ntot;
+    const int n_specs = std::min(cfg->n_blocks, 4);
+    S.n_specs = n_specs;
+    const double w_x = cfg->window_px * cfg->resolution;  // window_x_m(), backbone.hpp:32
+    const double w_y = cfg->window_py * cfg->resolution;
+
+    // frame tables
+    const int nf = S.n_frames;
+    int64_t* d_tab = ws<int64_t>(c, "frame_tab", 3 * static_cast<size_t>(nf) + 2);
+    std::vector<int64_t> tab;
+    tab.insert(tab.end(), S.off.begin(), S.off.end());
+    tab.insert(tab.end(), S.rows.begin(), S.rows.end());
+    tab.insert(tab.end(), S.drop_off.begin(), S.drop_off.end() - 1);
+    CUDA_OK(cudaMemcpyAsync(d_tab, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, st));
+    const int64_t* d_off = d_tab;
+    const int64_t* d_rows = d_tab + nf + 1;
+    const int64_t* d_drop_off = d_tab + 2 * nf + 1;
+
+    const int64_t total = ntot * n_specs;
+    S.sorted = sort_specs(c, d_coords, ntot, n_specs, w_x, w_y, d_off, nf);
+    uint32_t* scan_tmp = ws<uint32_t>(c, "scan_tmp", scan_tmp_words(total) + 8);
+
+    // drops (block 0 = spec 0), kept set
+    S.dropped = ws<uint8_t>(c, "dropped", static_cast<size_t>(ntot));
+    CUDA_OK(cudaMemsetAsync(S.dropped, 0, static_cast<size_t>(ntot), st));
+    S.dropped_ids = ws<int32_t>(c, "dropped_ids", static_cast<size_t>(S.n_drop) + 1);
+    launch_drop_mark(S.sorted, ntot, d_off, d_rows, d_drop_off, nf, S.dropped, S.dropped_ids, st,
+                     &c->launches);
+    uint32_t* flags = ws<uint32_t>(c, "flags", static_cast<size_t>(std::max(total, ntot)));
+    S.kept_rank = ws<uint32_t>(c, "kept_rank", static_cast<size_t>(ntot));
+    launch_keep_flags(S.dropped, ntot, flags, st, &c->launches);
+    exclusive_scan_u32(flags, S.kept_rank, ntot, scan_tmp, nullptr, st, &c->launches);
+    S.kept_ids = ws<int32_t>(c, "kept_ids", static_cast<size_t>(S.K));
+    launch_kept_ids(S.kept_rank, S.dropped, ntot, S.kept_ids, st, &c->launches);
+
+    // kept-restricted plans for every spec
+    launch_spec_keep_flags(S.sorted, total, S.dropped, flags, st, &c->launches);
+    uint32_t* pos = ws<uint32_t>(c, "compact_pos", static_cast<size_t>(total));
+    exclusive_scan_u32(flags, pos, total, scan_tmp, nullptr, st, &c->launches);
+    S.idx = ws<int32_t>(c, "idx", static_cast<size_t>(S.K) * n_specs);
+    launch_spec_compact(S.sorted, total, S.dropped, pos, S.idx, st, &c->launches);
+
+    const int s_last = (cfg->n_blocks - 1) % 4;
+    S.out_pos = ws<int32_t>(c, "out_pos", static_cast<size_t>(S.K));
+    k_out_pos<<<static_cast<unsigned>((S.K + 255) / 256), 256, 0, st>>>(S.idx + S.K * s_last,
+                                                                       S.kept_rank, S.K, S.out_pos);
+    ++c->launches;
+    check_launch();
+}
+
+// Reference plan-cache rule (backbone.hpp:224-234, 285-316) for a frame of n
+// pillars: block b drops n_active mod G; any drop clears the cache.
+void cache_stats(int n_blocks, int64_t n, int G, int32_t* computed, int32_t* hits,
+                 std::vector<int64_t>* drops) {
+    bool have[4] = {false, false, false, false};
+    int64_t have_n[4] = {0, 0, 0, 0};
+    int comp = 0, hit = 0;
+    int64_t act = n;
+    for (int b = 0; b < n_blocks; ++b) {
+        const int s = b % 4;
+        if (have[s] && have_n[s] == act) ++hit;
+        else {
+            ++comp;
+            have[s] = true;
+            have_n[s] = act;
+        }
+        const int64_t d = act % G;
+        if (drops) drops->push_back(d);
+        if (d) {
+            act -= d;
+            for (auto& h : have) h = false;
+        }
+    }
+    *computed = comp;
+    *hits = hit;
+}
+
+// ------------------------------------------------------------------ block pipeline
+
+struct Scratch {
+    float *h, *qkv, *cat, *mid, *ln2, *act;  // fp32 path
+    __nv_bfloat16 *qkv16, *cat16;             // bf16 path
+};
+
+// One FlatFormer block over `rows` grouped rows: input rows x_in[ridx[r]]
+// (f32, or f64 when x_in64), positional rows pe[ridx[r]], output
+// x_out[sidx[r]].  kernels.hpp:636-650 composed with backbone.hpp:245-283.
+void run_block(fwa_b200_ctx* c, const BlockParams& p, const fwa_config_t* cfg, int64_t rows,
+               const int32_t* ridx, const float* x_in, const double* x_in64, const float* pe,
+               float* x_out, const int32_t* sidx, bool fast) {
+    cudaStream_t st = c->stream;
+    const int d = cfg->d_model, dff = cfg->d_ff, G = cfg->group_size;
+    if (rows == 0) return;
+    if (fast) {
+        __nv_bfloat16* qkv = ws<__nv_bfloat16>(c, "qkv16", static_cast<size_t>(rows) * 3 * d);
+        __nv_bfloat16* cat = ws<__nv_bfloat16>(c, "cat16", static_cast<size_t>(rows) * d);
+        {
+            StageEv t(c, FWA_PROF_LN_QKV);
+            launch_ln1_qkv_tc(x_in, x_in64, pe, ridx, rows, p.tc, qkv, c->d_flag, st, &c->launches);
+            check_launch("k_ln1_qkv_tc");
+        }
+        {
+            StageEv t(c, FWA_PROF_ATTENTION);
+            launch_attention_mma(qkv, rows, G, cat, st, &c->launches);
+            check_launch("k_attention_mma");
+        }
+        {
+            StageEv t(c, FWA_PROF_OUTPROJ_FFN);
+            launch_outproj_ffn_tc(cat, x_in, x_in64, ridx, rows, p.tc, x_out, sidx, st, &c->launches);
+            check_launch("k_outproj_ffn_tc");
+        }
+        check_launch();
+        return;
+    }
+    float* h = ws<float>(c, "h32", static_cast<size_t>(rows) * d);
+    float* qkv = ws<float>(c, "qkv32", static_cast<size_t>(rows) * 3 * d);
+    float* cat = ws<float>(c, "cat32", static_cast<size_t>(rows) * d);
+    float* mid = ws<float>(c, "mid32", static_cast<size_t>(rows) * d);
+    float* ln2 = ws<float>(c, "ln2_32", static_cast<size_t>(rows) * d);
+    float* act = ws<float>(c, "act32", static_cast<size_t>(rows) * dff);
+    GemmArgs g{};
+    {
+        StageEv t(c, FWA_PROF_LN_QKV);
+        launch_ln_gather_f32(x_in, x_in64, pe, ridx, rows, d, p.ln1_g, p.ln1_b, h, c->d_flag, st,
+                             &c->launches);
+        g.A = h; g.M = rows; g.K = d; g.W = p.w_qkv; g.N = 3 * d; g.bias = p.b_qkv; g.C = qkv;
+        launch_gemm_f32(g, EPI_BIAS, st, &c->launches);
+    }
+    {
+        StageEv t(c, FWA_PROF_ATTENTION);
+        launch_attention_f32(qkv, rows, G, d, cfg->n_heads, cat, st, &c->launches);
+    }
+    StageEv t_ffn(c, FWA_PROF_OUTPROJ_FFN);
+    g = GemmArgs{};
+    g.A = cat; g.M = rows; g.K = d; g.W = p.w_out; g.N = d; g.bias = p.b_out; g.C = mid;
+    g.R = x_in; g.R64 = x_in64; g.ridx = ridx;
+    launch_gemm_f32(g, EPI_RESID_GATHER, st, &c->launches);
+    launch_ln_rows_f32(mid, rows, d, p.ln2_g, p.ln2_b, ln2, st, &c->launches);
+    g = GemmArgs{};
+    g.A = ln2; g.M = rows; g.K = d; g.W = p.w1; g.N = dff; g.bias = p.b1; g.C = act;
+    launch_gemm_f32(g, EPI_BIAS_GELU, st, &c->launches);
+    g = GemmArgs{};
+    g.A = act; g.M = rows; g.K = dff; g.W = p.w2; g.N = d; g.bias = p.b2;
+    g.R = mid; g.D = x_out; g.sidx = sidx;
+    launch_gemm_f32(g, EPI_RESID_SCATTER, st, &c->launches);
+    check_launch();
+}
+
+void require_params(fwa_b200_ctx* c, const fwa_config_t* cfg) {
+    if (!c->have_params) throw FwaError{FWA_ERR_CONTRACT, "no parameters loaded (fwa_b200_load_params)"};
+    if (static_cast<int>(c->blocks.size()) != cfg->n_blocks)
+        throw FwaError{FWA_ERR_CONFIG, "backbone: params.blocks length must equal n_blocks"};
+    if (c->pcfg.d_model != cfg->d_model || c->pcfg.n_heads != cfg->n_heads || c->pcfg.d_ff != cfg->d_ff)
+        throw FwaError{FWA_ERR_CONFIG, "backbone: block params disagree with config"};
+}
+
+// Device-resident forward over S (already host-framed).  Writes d_out
+// (K x d, active order) and, optionally, d_kept.
+void forward_device(fwa_b200_ctx* c, const double* d_coords, const float* d_feats,
+                    const double* d_feats64, const fwa_config_t* cfg, Schedule& S, float* d_out,
+                    int32_t* d_kept) {
+    cudaStream_t st = c->stream;
+    const int d = cfg->d_model;
+    {
+        StageEv t(c, FWA_PROF_SCHEDULE);
+        build_schedule(c, d_coords, cfg, S);
+    }
+    float* pe = ws<float>(c, "pe", static_cast<size_t>(S.ntot) * d);
+    {
+        StageEv t(c, FWA_PROF_PE);
+        launch_positional_embedding(d_coords, S.ntot, d, pe_freq(c, d), pe, st, &c->launches);
+    }
+    float* X = ws<float>(c, "X", static_cast<size_t>(S.ntot) * d);
+    CUDA_OK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), st));
+    const bool fast = fast_path_ok(c, d, cfg->n_heads, cfg->d_ff, cfg->group_size);
+    for (int b = 0; b < cfg->n_blocks; ++b) {
+        const int s = b % 4;
+        const int32_t* idx = S.idx + S.K * s;
+        const bool last = b == cfg->n_blocks - 1;
+        const float* xin = b == 0 ? d_feats : X;
+        const double* xin64 = b == 0 ? d_feats64 : nullptr;
+        run_block(c, c->blocks[static_cast<size_t>(b)], cfg, S.K, idx, xin, xin64, pe,
+                  last ? d_out : X, last ? S.out_pos : idx, fast);
+    }
+    if (d_kept)
+        CUDA_OK(cudaMemcpyAsync(d_kept, S.kept_ids, static_cast<size_t>(S.K) * 4,
+                                cudaMemcpyDeviceToDevice, st));
+}
+
+int fail(fwa_b200_ctx* c, const FwaError& e) {
+    if (c) c->err = e.msg;
+    return e.code;
+}
+
+template <class Fn>
+int guarded(fwa_b200_ctx* c, Fn&& fn) {
+    try {
+        if (c) {
+            cudaSetDevice(c->device);
+            c->err.clear();
+        }
+        fn();
+        return FWA_OK;
+    } catch (const FwaError& e) {
+        return fail(c, e);
+    } catch (const std::exception& e) {
+        return fail(c, FwaError{FWA_ERR_INTERNAL, e.what()});
+    }
+}
+
+// Host-buffer forward shared by the single-frame and batch entry points.
+void forward_host(fwa_b200_ctx* c, const double* coords, const void* feats, int f64,
+                  const int64_t* off, int n_frames, const fwa_config_t* cfg, fwa_output_t* out,
+                  int64_t* kept_per_frame) {
+    validate_cfg(cfg);
+    require_params(c, cfg);
+    if (!coords || !feats || !out || !out->features) throw FwaError{FWA_ERR_SHAPE, "null buffer"};
+    Schedule S;
+    host_frames(off, n_frames, cfg->group_size, S);
+    cudaStream_t st = c->stream;
+    const int d = cfg->d_model;
+    double* d_coords = ws<double>(c, "in_coords", 2 * static_cast<size_t>(S.ntot));
+    const float* d_f32 = nullptr;
+    const double* d_f64 = nullptr;
+    StageEv* h2d = new StageEv(c, FWA_PROF_H2D);
+    CUDA_OK(cudaMemcpyAsync(d_coords, coords, static_cast<size_t>(S.ntot) * 16, cudaMemcpyHostToDevice, st));
+    if (f64) {
+        double* p = ws<double>(c, "in_feats64", static_cast<size_t>(S.ntot) * d);
+        CUDA_OK(cudaMemcpyAsync(p, feats, static_cast<size_t>(S.ntot) * d * 8, cudaMemcpyHostToDevice, st));
+        d_f64 = p;
+    } else {
+        float* p = ws<float>(c, "in_feats32", static_cast<size_t>(S.ntot) * d);
+        CUDA_OK(cudaMemcpyAsync(p, feats, static_cast<size_t>(S.ntot) * d * 4, cudaMemcpyHostToDevice, st));
+        d_f32 = p;
+    }
+    delete h2d;
+    float* d_out = ws<float>(c, "out_feats", static_cast<size_t>(S.ntot) * d);
+    forward_device(c, d_coords, d_f32, d_f64, cfg, S, d_out, nullptr);
+    StageEv* d2h = new StageEv(c, FWA_PROF_D2H);
+    CUDA_OK(cudaMemcpyAsync(out->features, d_out, static_cast<size_t>(S.K) * d * 4, cudaMemcpyDeviceToHost, st));
+    if (out->kept_indices)
+        CUDA_OK(cudaMemcpyAsync(out->kept_indices, S.kept_ids, static_cast<size_t>(S.K) * 4,
+                                cudaMemcpyDeviceToHost, st));
+    if (out->dropped_ids && S.n_drop)
+        CUDA_OK(cudaMemcpyAsync(out->dropped_ids, S.dropped_ids, static_cast<size_t>(S.n_drop) * 4,
+                                cudaMemcpyDeviceToHost, st));
+    std::vector<int32_t> h_sorted, h_rank, h_idx;
+    const bool perms = out->block_perms && n_frames == 1;
+    if (perms) {
+        h_sorted.resize(static_cast<size_t>(S.ntot) * S.n_specs);
+        h_idx.resize(static_cast<size_t>(S.K) * S.n_specs);
+        h_rank.resize(static_cast<size_t>(S.ntot));
+        CUDA_OK(cudaMemcpyAsync(h_sorted.data(), S.sorted, h_sorted.size() * 4, cudaMemcpyDeviceToHost, st));
+        CUDA_OK(cudaMemcpyAsync(h_idx.data(), S.idx, h_idx.size() * 4, cudaMemcpyDeviceToHost, st));
+        CUDA_OK(cudaMemcpyAsync(h_rank.data(), S.kept_rank, h_rank.size() * 4, cudaMemcpyDeviceToHost, st));
+    }
+    CUDA_OK(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    delete d2h;
+    CUDA_OK(cudaStreamSynchronize(st));
+    if (*c->h_flag) throw FwaError{FWA_ERR_NUMERIC, "group_attention: non-finite input"};
+    out->n_kept = S.K;
+    std::vector<int64_t> drops;
+    cache_stats(cfg->n_blocks, S.off[1] - S.off[0], cfg->group_size, &out->cache_computed,
+                &out->cache_hits, &drops);
+    if (out->dropped_per_block)
+        for (int b = 0; b < cfg->n_blocks; ++b) {
+            int64_t tot = 0;  // summed over frames (each frame drops only in block 0)
+            for (int f = 0; f < n_frames; ++f) tot += b == 0 ? S.drop[f] : 0;
+            out->dropped_per_block[b] = static_cast<int32_t>(tot);
+        }
+    if (kept_per_frame)
+        for (int f = 0; f < n_frames; ++f) kept_per_frame[f] = S.rows[f];
+    if (perms) {
+        const int64_t n = S.ntot;
+        for (int b = 0; b < cfg->n_blocks; ++b) {
+            const int s = b % 4;
+            int32_t* row = out->block_perms + static_cast<int64_t>(b) * n;
+            if (b == 0 || S.n_drop == 0) {
+                std::memcpy(row, h_sorted.data() + static_cast<int64_t>(s) * n, static_cast<size_t>(n) * 4);
+            } else {
+                const int32_t* ix = h_idx.data() + static_cast<int64_t>(s) * S.K;
+                for (int64_t r = 0; r < S.K; ++r) row[r] = static_cast<int32_t>(h_rank[static_cast<size_t>(ix[r])]);
+            }
+        }
+    }
+}
+
+} // namespace
+
+extern "C" {
+
+int fwa_b200_ctx_create(int device, void* stream, fwa_b200_ctx** out) {
+    if (!out) return FWA_ERR_CONFIG;
+    *out = nullptr;
+    auto* c = new fwa_b200_ctx;
+    c->device = device;
+    const int rc = guarded(c, [&] {
+        int n = 0;
+        CUDA_OK(cudaGetDeviceCount(&n));
+        if (device < 0 || device >= n) throw FwaError{FWA_ERR_CUDA, "no such CUDA device"};
+        CUDA_OK(cudaSetDevice(device));
+        if (stream) {
+            c->stream = static_cast<cudaStream_t>(stream);
+        } else {
+            CUDA_OK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+            c->own_stream = true;
+        }
+        CUDA_OK(cudaMalloc(&c->d_flag, sizeof(int)));
+        CUDA_OK(cudaMallocHost(&c->h_flag, sizeof(int)));
+        CUDA_OK(cudaMallocHost(&c->h_minmax, 16 * sizeof(long long)));
+    });
+    if (rc != FWA_OK) {
+        static std::string last;
+        last = c->err;
+        delete c;
+        return rc;
+    }
+    *out = c;
+    return FWA_OK;
+}
+
+void fwa_b200_ctx_destroy(fwa_b200_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    for (auto& kv : c->ws)
+        if (kv.second.p) cudaFree(kv.second.p);
+    if (c->params_f32.p) cudaFree(c->params_f32.p);
+    if (c->params_bf16.p) cudaFree(c->params_bf16.p);
+    if (c->freq.p) cudaFree(c->freq.p);
+    if (c->d_flag) cudaFree(c->d_flag);
+    if (c->h_flag) cudaFreeHost(c->h_flag);
+    if (c->h_minmax) cudaFreeHost(c->h_minmax);
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+const char* fwa_b200_last_error(const fwa_b200_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int fwa_b200_set_precision(fwa_b200_ctx* c, int precision) {
+    if (!c) return FWA_ERR_CONFIG;
+    if (precision != FWA_PREC_BF16 && precision != FWA_PREC_FP32) {
+        c->err = "unknown precision";
+        return FWA_ERR_CONFIG;
+    }
+    c->precision = precision;
+    return FWA_OK;
+}
+
+int64_t fwa_b200_kernel_launches(const fwa_b200_ctx* c) { return c ? c->launches : 0; }
+
+int fwa_b200_set_profiling(fwa_b200_ctx* c, int enable) {
+    if (!c) return FWA_ERR_CONFIG;
+    return guarded(c, [&] {
+        prof_collect(c);
+        c->profiling = enable != 0;
+        for (int i = 0; i < FWA_PROF_SLOTS; ++i) {
+            c->prof_ms[i] = 0.0;
+            c->prof_n[i] = 0;
+        }
+    });
+}
+
+int fwa_b200_get_profile(fwa_b200_ctx* c, double* ms, int64_t* counts) {
+    if (!c) return FWA_ERR_CONFIG;
+    return guarded(c, [&] {
+        prof_collect(c);
+        for (int i = 0; i < FWA_PROF_SLOTS; ++i) {
+            if (ms) ms[i] = c->prof_ms[i];
+            if (counts) counts[i] = c->prof_n[i];
+        }
+    });
+}
+
+int fwa_b200_fast_path(const fwa_b200_ctx* c, const fwa_config_t* cfg) {
+    return (c && cfg && fast_path_ok(c, cfg->d_model, cfg->n_heads, cfg->d_ff, cfg->group_size)) ? 1 : 0;
+}
+
+int fwa_b200_load_params(fwa_b200_ctx* c, const fwa_config_t* cfg, const void* blob, size_t len) {
+    return guarded(c, [&] {
+        validate_cfg(cfg);
+        if (!blob) throw FwaError{FWA_ERR_PARSE, "null FWAP blob"};
+        std::vector<std::vector<float>> keep;
+        const auto recs = parse_fwap(blob, len, keep);
+        if (static_cast<int>(recs.size()) != cfg->n_blocks)
+            throw FwaError{FWA_ERR_CONFIG, "backbone: params.blocks length must equal n_blocks"};
+        for (const auto& r : recs)
+            if (r.d != cfg->d_model || r.h != cfg->n_heads || r.dff != cfg->d_ff)
+                throw FwaError{FWA_ERR_CONFIG, "backbone: block params disagree with config"};
+        c->blocks = upload_block_params(recs, c->params_f32, c->params_bf16, c->stream);
+        c->pcfg = *cfg;
+        c->have_params = true;
+    });
+}
+
+int fwa_b200_backbone_forward(fwa_b200_ctx* c, const double* coords, const void* feats, int f64,
+                              int64_t n, const fwa_config_t* cfg, fwa_output_t* out) {
+    return guarded(c, [&] {
+        const int64_t off[2] = {0, n};
+        forward_host(c, coords, feats, f64, off, 1, cfg, out, nullptr);
+    });
+}
+
+int fwa_b200_backbone_forward_batch(fwa_b200_ctx* c, const double* coords, const void* feats,
+                                    int f64, const int64_t* frame_offsets, int n_frames,
+                                    const fwa_config_t* cfg, fwa_output_t* out,
+                                    int64_t* kept_per_frame) {
+    return guarded(c, [&] {
+        if (!frame_offsets || n_frames < 1) throw FwaError{FWA_ERR_SHAPE, "need >= 1 frame"};
+        if (frame_offsets[0] != 0) throw FwaError{FWA_ERR_SHAPE, "frame_offsets[0] must be 0"};
+        forward_host(c, coords, feats, f64, frame_offsets, n_frames, cfg, out, kept_per_frame);
+    });
+}
+
+int fwa_b200_backbone_forward_device(fwa_b200_ctx* c, const double* d_coords, const float* d_feats,
+                                     const int64_t* frame_offsets, int n_frames,
+                                     const fwa_config_t* cfg, float* d_out, int32_t* d_kept,
+                                     int64_t* n_kept_out) {
+    return guarded(c, [&] {
+        validate_cfg(cfg);
+        require_params(c, cfg);
+        if (!d_coords || !d_feats || !d_out) throw FwaError{FWA_ERR_SHAPE, "null buffer"};
+        if (!frame_offsets || n_frames < 1) throw FwaError{FWA_ERR_SHAPE, "need frame offsets"};
+        Schedule S;
+        host_frames(frame_offsets, n_frames, cfg->group_size, S);
+        forward_device(c, d_coords, d_feats, nullptr, cfg, S, d_out, d_kept);
+        if (n_kept_out) *n_kept_out = S.K;
+    });
+}
+
+int fwa_b200_sort_plan(fwa_b200_ctx* c, const double* coords, int64_t n, double w_x, double w_y,
+                       int shift, int major_axis_y, int32_t* perm_out) {
+    return guarded(c, [&] {
+        if (!(w_x > 0.0) || !(w_y > 0.0)) throw FwaError{FWA_ERR_CONFIG, "window dims must be positive"};
+        if (n == 0) return;
+        if (!coords || !perm_out) throw FwaError{FWA_ERR_SHAPE, "null buffer"};
+        // one frame; specs 0..spec are keyed, only `spec` is read back
+        cudaStream_t st = c->stream;
+        const int64_t off[2] = {0, n};
+        double* d_coords = ws<double>(c, "in_coords", 2 * static_cast<size_t>(n));
+        CUDA_OK(cudaMemcpyAsync(d_coords, coords, static_cast<size_t>(n) * 16, cudaMemcpyHostToDevice, st));
+        int64_t* d_off = ws<int64_t>(c, "frame_tab", 4);
+        CUDA_OK(cudaMemcpyAsync(d_off, off, 16, cudaMemcpyHostToDevice, st));
+        const int spec = 2 * (major_axis_y ? 1 : 0) + (shift ? 1 : 0);
+        const int64_t ntot = n;
+        const int32_t* sorted = sort_specs(c, d_coords, ntot, spec + 1, w_x, w_y, d_off, 1);
+        CUDA_OK(cudaMemcpyAsync(perm_out, sorted + static_cast<int64_t>(spec) * ntot,
+                                static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, st));
+        CUDA_OK(cudaStreamSynchronize(st));
+    });
+}
+
+int fwa_b200_block_forward(fwa_b200_ctx* c, const float* f, const float* pe, int64_t rows,
+                           int32_t n_groups, const void* record, size_t record_len, float* out) {
+    return guarded(c, [&] {
+        std::vector<std::vector<float>> keep;
+        const auto recs = parse_fwap(record, record_len, keep);
+        if (recs.size() != 1) throw FwaError{FWA_ERR_CONFIG, "expected exactly one FWAP record"};
+        const Record& r = recs[0];
+        const int d = r.d;
+        if (n_groups == 0 && rows == 0) return;  // kernels.hpp:454
+        if (n_groups < 1 || rows % n_groups != 0)
+            throw FwaError{FWA_ERR_SHAPE, "group_attention: rows not divisible by n_groups"};
+        fwa_config_t cfg{};
+        cfg.resolution = 0.32;
+        cfg.window_px = cfg.window_py = 9;
+        cfg.group_size = static_cast<int32_t>(rows / n_groups);
+        cfg.n_blocks = 1;
+        cfg.d_model = d;
+        cfg.n_heads = r.h;
+        cfg.d_ff = r.dff;
+        // parameters for this call only (the loaded backbone params are kept)
+        const std::vector<BlockParams> bp =
+            upload_block_params(recs, c->ws["blk_params_f32"], c->ws["blk_params_bf16"], c->stream);
+        cudaStream_t st = c->stream;
+        float* df = ws<float>(c, "bf_f", static_cast<size_t>(rows) * d);
+        float* dpe = ws<float>(c, "bf_pe", static_cast<size_t>(rows) * d);
+        float* dout = ws<float>(c, "bf_out", static_cast<size_t>(rows) * d);
+        CUDA_OK(cudaMemcpyAsync(df, f, static_cast<size_t>(rows) * d * 4, cudaMemcpyHostToDevice, st));
+        CUDA_OK(cudaMemcpyAsync(dpe, pe, static_cast<size_t>(rows) * d * 4, cudaMemcpyHostToDevice, st));
+        CUDA_OK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), st));
+        const bool fast = fast_path_ok(c, d, r.h, r.dff, cfg.group_size);
+        run_block(c, bp[0], &cfg, rows, nullptr, df, nullptr, dpe, dout, nullptr, fast);
+        CUDA_OK(cudaMemcpyAsync(out, dout, static_cast<size_t>(rows) * d * 4, cudaMemcpyDeviceToHost, st));
+        CUDA_OK(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CUDA_OK(cudaStreamSynchronize(st));
+        if (*c->h_flag) throw FwaError{FWA_ERR_NUMERIC, "group_attention: non-finite input"};
+    });
+}
+
+int fwa_b200_positional_embedding(fwa_b200_ctx* c, const double* coords, int64_t n, int32_t d,
+                                  float* out) {
+    return guarded(c, [&] {
+        if (d < 4 || d % 4 != 0)
+            throw FwaError{FWA_ERR_CONFIG, "positional_embedding: d_model must be divisible by 4"};
+        if (n == 0) return;
+        cudaStream_t st = c->stream;
+        double* dc = ws<double>(c, "pe_coords", 2 * static_cast<size_t>(n));
+        float* dp = ws<float>(c, "pe_out", static_cast<size_t>(n) * d);
+        CUDA_OK(cudaMemcpyAsync(dc, coords, static_cast<size_t>(n) * 16, cudaMemcpyHostToDevice, st));
+        launch_positional_embedding(dc, n, d, pe_freq(c, d), dp, st, &c->launches);
+        check_launch();
+        CUDA_OK(cudaMemcpyAsync(out, dp, static_cast<size_t>(n) * d * 4, cudaMemcpyDeviceToHost, st));
+        CUDA_OK(cudaStreamSynchronize(st));
+    });
+}
+
+} // extern "C"

@@ -1,0 +1,112 @@
+// Internal launcher declarations shared by the driver (fwa_b200.cu) and the
+// kernel translation units.  Not part of the C ABI.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fwa_b200 {
+
+struct LaunchCounter {
+    int64_t* n;
+    void operator++() const { ++*n; }
+};
+
+// ------------------------------------------------------------------ scan
+// Exclusive prefix sum of n uint32 values (in -> out, may alias), total
+// written to *d_total if non-null.  tmp must hold scan_tmp_words(n) words.
+size_t scan_tmp_words(int64_t n);
+void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* tmp,
+                        uint32_t* d_total, cudaStream_t s, int64_t* launches);
+
+// ------------------------------------------------------------------ sort (flatten.hpp:49-120)
+// Spec s in [0,4): axis Y iff s >= 2, shift iff s odd (block_schedule,
+// flatten.hpp:150-161: block b uses spec b % 4).
+struct SpecBins {
+    long long min_major, min_minor;
+    long long range_minor;      // max_minor - min_minor + 1
+    long long bins_per_frame;   // range_major * range_minor
+    long long base;             // first global bin id of this spec
+};
+
+void launch_sort_keys(const double* coords, int64_t ntot, int n_specs, double w_x, double w_y,
+                      long long* win, double* loc, long long* minmax, cudaStream_t s,
+                      int64_t* launches);
+void launch_bins_hist(const long long* win, int64_t ntot, int n_specs, const int64_t* d_frame_off,
+                      int n_frames, const SpecBins* d_specs, uint32_t* bin_of, uint32_t* hist,
+                      cudaStream_t s, int64_t* launches);
+void launch_bin_scatter(const uint32_t* bin_of, int64_t ntot, int n_specs, uint32_t* cursor,
+                        int32_t* pre, cudaStream_t s, int64_t* launches);
+void launch_bin_sort(const uint32_t* bin_start, const uint32_t* hist, uint32_t n_bins,
+                     const int32_t* pre, const double* loc, int64_t ntot, int32_t* sorted,
+                     int32_t* scratch, cudaStream_t s, int64_t* launches);
+
+// ------------------------------------------------------------------ schedule (backbone.hpp:236-316)
+void launch_drop_mark(const int32_t* sorted0, int64_t ntot, const int64_t* d_frame_off,
+                      const int64_t* d_rows, const int64_t* d_drop_off, int n_frames,
+                      uint8_t* dropped, int32_t* dropped_ids, cudaStream_t s, int64_t* launches);
+void launch_keep_flags(const uint8_t* dropped, int64_t ntot, uint32_t* flags, cudaStream_t s,
+                       int64_t* launches);
+void launch_kept_ids(const uint32_t* kept_rank, const uint8_t* dropped, int64_t ntot,
+                     int32_t* kept_ids, cudaStream_t s, int64_t* launches);
+void launch_spec_keep_flags(const int32_t* sorted, int64_t total, const uint8_t* dropped,
+                            uint32_t* flags, cudaStream_t s, int64_t* launches);
+void launch_spec_compact(const int32_t* sorted, int64_t total, const uint8_t* dropped,
+                         const uint32_t* pos, int32_t* idx, cudaStream_t s, int64_t* launches);
+
+// ------------------------------------------------------------------ fp32 SIMT path (check mode)
+void launch_positional_embedding(const double* coords, int64_t n, int d, const double* d_freq,
+                                 float* pe, cudaStream_t s, int64_t* launches);
+// h[r] = LN1(x[idx[r]]) * g + b + pe[idx[r]]  (x f32, or f64 when x64 != nullptr)
+void launch_ln_gather_f32(const float* x, const double* x64, const float* pe, const int32_t* idx,
+                          int64_t rows, int d, const float* gamma, const float* beta,
+                          float* h, int* d_nonfinite, cudaStream_t s, int64_t* launches);
+void launch_ln_rows_f32(const float* x, int64_t rows, int d, const float* gamma,
+                        const float* beta, float* out, cudaStream_t s, int64_t* launches);
+
+enum GemmEpi {
+    EPI_BIAS = 0,          // C = A W^T + b
+    EPI_BIAS_GELU = 1,     // C = gelu(A W^T + b)
+    EPI_RESID_GATHER = 2,  // C[r] = (R[ridx[r]] + A W^T) + b   (kernels.hpp:559 order)
+    EPI_RESID_SCATTER = 3  // D[sidx[r]] = R[r] + (A W^T + b)    (kernels.hpp:612-614)
+};
+struct GemmArgs {
+    const float* A; int64_t M; int K;
+    const float* W; int N;         // W: N x K row-major (out x in)
+    const float* bias;
+    float* C;                      // M x N (EPI_BIAS/GELU/RESID_GATHER)
+    const float* R; const double* R64; const int32_t* ridx;  // residual (gather) source
+    float* D; const int32_t* sidx;                           // scatter destination
+};
+void launch_gemm_f32(const GemmArgs& a, GemmEpi epi, cudaStream_t s, int64_t* launches);
+void launch_attention_f32(const float* qkv, int64_t rows, int G, int d, int heads, float* cat,
+                          cudaStream_t s, int64_t* launches);
+
+// ------------------------------------------------------------------ bf16 tensor-core path
+// Fast path: d_model 128, d_ff 256, head dim 16, group_size <= 128.
+struct TcBlockWeights {
+    const __nv_bfloat16* w_qkv; // 384 x 128, pre-swizzled UMMA K-major SW128 image
+    const __nv_bfloat16* w_out; // 128 x 128, swizzled
+    const __nv_bfloat16* w1;    // 256 x 128, swizzled
+    const __nv_bfloat16* w2;    // 128 x 256, swizzled
+    const float *b_qkv, *b_out, *ln1_g, *ln1_b, *ln2_g, *ln2_b, *b1, *b2;
+};
+// Host-side: write the UMMA SW128 K-major smem image of a row-major f32
+// [rows x k] weight as bf16 (rows multiple of 8, k multiple of 64).
+void swizzle_weight_bf16(const float* w, int rows, int k, uint16_t* out);
+
+void launch_ln1_qkv_tc(const float* x, const double* x64, const float* pe, const int32_t* idx,
+                       int64_t rows, const TcBlockWeights& w, __nv_bfloat16* qkv,
+                       int* d_nonfinite, cudaStream_t s, int64_t* launches);
+void launch_attention_mma(const __nv_bfloat16* qkv, int64_t rows, int G, __nv_bfloat16* cat,
+                          cudaStream_t s, int64_t* launches);
+// x_out[sidx[r]] = FFN-block(x_in[ridx[r]] + cat[r] Wout^T + b_out)
+void launch_outproj_ffn_tc(const __nv_bfloat16* cat, const float* x_in, const double* x_in64,
+                           const int32_t* ridx, int64_t rows, const TcBlockWeights& w,
+                           float* x_out, const int32_t* sidx, cudaStream_t s, int64_t* launches);
+
+// ------------------------------------------------------------------ misc
+void launch_scatter_rows(const float* src, const int32_t* ids, const uint32_t* rank, int64_t n,
+                         int d, float* dst, cudaStream_t s, int64_t* launches);
+
+} // namespace fwa_b200

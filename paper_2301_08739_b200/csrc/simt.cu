@@ -1,0 +1,277 @@
+// fp32 CUDA-core kernels: the FWA_PREC_FP32 check mode (tolerance 1e-4) and
+// the path for configurations outside the tensor-core fast path's shapes.
+// All run on the GPU; there is no CPU fallback.
+//
+//   positional_embedding   /root/reference/proj/include/fwa/kernels.hpp:364-393
+//   LN1 + affine + PE      kernels.hpp:235-249, 472-485
+//   packed QKV / out-proj  kernels.hpp:488-500, 550-560 (matmul_nt dense.hpp:50-64)
+//   group attention        kernels.hpp:512-548 (softmax_row 251-262)
+//   FFN (LN2, W1, GELU, W2, residual)  kernels.hpp:575-633
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace fwa_b200 {
+
+// ------------------------------------------------------------------ PE
+
+// pe[i] = [sin/cos(2*pi*freq_k*x) pairs | sin/cos(2*pi*freq_k*y) pairs] in fp64,
+// rounded to f32.  freq_k comes from the host (glibc pow, as the reference).
+__global__ void k_positional_embedding(const double* __restrict__ coords, int64_t n, int d,
+                                       const double* __restrict__ freq, float* __restrict__ pe) {
+    const int nf = d / 4;
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t i = t / (2 * nf);
+    if (i >= n) return;
+    const int r = static_cast<int>(t % (2 * nf));
+    const int axis = r / nf, k = r % nf;
+    const double c = coords[2 * i + axis];
+    const double phase = __dmul_rn(__dmul_rn(6.283185307179586, freq[k]), c);
+    double sv, cv;
+    sincos(phase, &sv, &cv);
+    float2 o = make_float2(static_cast<float>(sv), static_cast<float>(cv));
+    reinterpret_cast<float2*>(pe + i * d + axis * (d / 2))[k] = o;
+}
+
+void launch_positional_embedding(const double* coords, int64_t n, int d, const double* d_freq,
+                                 float* pe, cudaStream_t s, int64_t* launches) {
+    const int64_t total = n * (d / 2);
+    k_positional_embedding<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
+        coords, n, d, d_freq, pe);
+    ++*launches;
+}
+
+// ------------------------------------------------------------------ LN (one warp per row)
+
+template <bool kF64>
+__global__ void __launch_bounds__(256) k_ln_gather_f32(const float* __restrict__ x,
+                                                       const double* __restrict__ x64,
+                                                       const float* __restrict__ pe,
+                                                       const int32_t* __restrict__ idx,
+                                                       int64_t rows, int d,
+                                                       const float* __restrict__ g,
+                                                       const float* __restrict__ b,
+                                                       float* __restrict__ h,
+                                                       int* __restrict__ nonfinite) {
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (r >= rows) return;
+    const int64_t id = idx ? idx[r] : r;
+    float sum = 0.f;
+    bool bad = false;
+    for (int c = lane; c < d; c += 32) {
+        const float v = kF64 ? static_cast<float>(x64[id * d + c]) : x[id * d + c];
+        const float p = pe[id * d + c];
+        bad |= !isfinite(v) || !isfinite(p);
+        sum += v;
+    }
+    const float mean = warp_sum(sum) / static_cast<float>(d);
+    float var = 0.f;
+    for (int c = lane; c < d; c += 32) {
+        const float v = kF64 ? static_cast<float>(x64[id * d + c]) : x[id * d + c];
+        var += (v - mean) * (v - mean);
+    }
+    var = warp_sum(var) / static_cast<float>(d);
+    const float inv = 1.0f / sqrtf(var + 1e-5f);
+    for (int c = lane; c < d; c += 32) {
+        const float v = kF64 ? static_cast<float>(x64[id * d + c]) : x[id * d + c];
+        h[r * d + c] = g[c] * ((v - mean) * inv) + b[c] + pe[id * d + c];
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(nonfinite, 1);
+}
+
+void launch_ln_gather_f32(const float* x, const double* x64, const float* pe, const int32_t* idx,
+                          int64_t rows, int d, const float* gamma, const float* beta, float* h,
+                          int* d_nonfinite, cudaStream_t s, int64_t* launches) {
+    const unsigned grid = static_cast<unsigned>((rows + 7) / 8);
+    if (x64)
+        k_ln_gather_f32<true><<<grid, 256, 0, s>>>(x, x64, pe, idx, rows, d, gamma, beta, h,
+                                                   d_nonfinite);
+    else
+        k_ln_gather_f32<false><<<grid, 256, 0, s>>>(x, x64, pe, idx, rows, d, gamma, beta, h,
+                                                    d_nonfinite);
+    ++*launches;
+}
+
+__global__ void __launch_bounds__(256) k_ln_rows_f32(const float* __restrict__ x, int64_t rows,
+                                                     int d, const float* __restrict__ g,
+                                                     const float* __restrict__ b,
+                                                     float* __restrict__ out) {
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (r >= rows) return;
+    float sum = 0.f;
+    for (int c = lane; c < d; c += 32) sum += x[r * d + c];
+    const float mean = warp_sum(sum) / static_cast<float>(d);
+    float var = 0.f;
+    for (int c = lane; c < d; c += 32) {
+        const float v = x[r * d + c] - mean;
+        var += v * v;
+    }
+    var = warp_sum(var) / static_cast<float>(d);
+    const float inv = 1.0f / sqrtf(var + 1e-5f);
+    for (int c = lane; c < d; c += 32) out[r * d + c] = g[c] * ((x[r * d + c] - mean) * inv) + b[c];
+}
+
+void launch_ln_rows_f32(const float* x, int64_t rows, int d, const float* gamma,
+                        const float* beta, float* out, cudaStream_t s, int64_t* launches) {
+    k_ln_rows_f32<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, s>>>(x, rows, d, gamma, beta,
+                                                                       out);
+    ++*launches;
+}
+
+// ------------------------------------------------------------------ SIMT GEMM, C = A W^T (+epilogue)
+
+constexpr int kTM = 64, kTN = 64, kTK = 16;
+
+template <int kEpi>
+__global__ void __launch_bounds__(256) k_gemm_f32(GemmArgs a) {
+    __shared__ float As[kTK][kTM + 4];
+    __shared__ float Ws[kTK][kTN + 4];
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    const int64_t m0 = static_cast<int64_t>(blockIdx.y) * kTM;
+    const int n0 = blockIdx.x * kTN;
+    float acc[4][4] = {};
+    for (int k0 = 0; k0 < a.K; k0 += kTK) {
+        for (int t = threadIdx.x; t < kTM * kTK; t += 256) {
+            const int mm = t / kTK, kk = t % kTK;
+            const int64_t gm = m0 + mm;
+            const int gk = k0 + kk;
+            As[kk][mm] = (gm < a.M && gk < a.K) ? a.A[gm * a.K + gk] : 0.f;
+            const int gn = n0 + mm;
+            Ws[kk][mm] = (gn < a.N && gk < a.K) ? a.W[static_cast<int64_t>(gn) * a.K + gk] : 0.f;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < kTK; ++kk) {
+            float av[4], wv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) av[i] = As[kk][ty * 4 + i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) wv[j] = Ws[kk][tx * 4 + j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], wv[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int64_t m = m0 + ty * 4 + i;
+        if (m >= a.M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int n = n0 + tx * 4 + j;
+            if (n >= a.N) continue;
+            const float bias = a.bias ? a.bias[n] : 0.f;
+            if (kEpi == EPI_BIAS) {
+                a.C[m * a.N + n] = acc[i][j] + bias;
+            } else if (kEpi == EPI_BIAS_GELU) {
+                a.C[m * a.N + n] = gelu_erf(acc[i][j] + bias);
+            } else if (kEpi == EPI_RESID_GATHER) {
+                const int64_t src = a.ridx ? a.ridx[m] : m;
+                const float res = a.R64 ? static_cast<float>(a.R64[src * a.N + n]) : a.R[src * a.N + n];
+                a.C[m * a.N + n] = (res + acc[i][j]) + bias;
+            } else {
+                const int64_t dst = a.sidx ? a.sidx[m] : m;
+                a.D[dst * a.N + n] = a.R[m * a.N + n] + (acc[i][j] + bias);
+            }
+        }
+    }
+}
+
+void launch_gemm_f32(const GemmArgs& a, GemmEpi epi, cudaStream_t s, int64_t* launches) {
+    dim3 grid(static_cast<unsigned>((a.N + kTN - 1) / kTN), static_cast<unsigned>((a.M + kTM - 1) / kTM));
+    switch (epi) {
+        case EPI_BIAS: k_gemm_f32<EPI_BIAS><<<grid, 256, 0, s>>>(a); break;
+        case EPI_BIAS_GELU: k_gemm_f32<EPI_BIAS_GELU><<<grid, 256, 0, s>>>(a); break;
+        case EPI_RESID_GATHER: k_gemm_f32<EPI_RESID_GATHER><<<grid, 256, 0, s>>>(a); break;
+        case EPI_RESID_SCATTER: k_gemm_f32<EPI_RESID_SCATTER><<<grid, 256, 0, s>>>(a); break;
+    }
+    ++*launches;
+}
+
+// ------------------------------------------------------------------ attention fp32
+// One CTA per (group, head); K/V of the head staged in shared memory when they
+// fit, one thread per query row; logits recomputed in a second pass instead of
+// materialising the G x G matrix (the reference's O(G) cache-free path).
+
+__global__ void __launch_bounds__(128) k_attention_f32(const float* __restrict__ qkv, int G, int d,
+                                                       int heads, float* __restrict__ cat,
+                                                       bool stage) {
+    extern __shared__ float sm[];
+    const int grp = blockIdx.x, head = blockIdx.y;
+    const int hd = d / heads;
+    const int64_t base = static_cast<int64_t>(grp) * G;
+    const int off = head * hd;
+    const float scale = 1.0f / sqrtf(static_cast<float>(hd));
+    float* Ks = sm;
+    float* Vs = sm + static_cast<size_t>(G) * hd;
+    if (stage) {
+        for (int t = threadIdx.x; t < G * hd; t += blockDim.x) {
+            const int j = t / hd, c = t % hd;
+            Ks[t] = qkv[(base + j) * 3 * d + d + off + c];
+            Vs[t] = qkv[(base + j) * 3 * d + 2 * d + off + c];
+        }
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < G; i += blockDim.x) {
+        const float* q = qkv + (base + i) * 3 * d + off;
+        float mx = -INFINITY;
+        for (int j = 0; j < G; ++j) {
+            const float* kj = stage ? Ks + j * hd : qkv + (base + j) * 3 * d + d + off;
+            float acc = 0.f;
+            for (int c = 0; c < hd; ++c) acc = fmaf(q[c], kj[c], acc);
+            mx = fmaxf(mx, acc * scale);
+        }
+        float sum = 0.f;
+        float* o = cat + (base + i) * d + off;
+        for (int c = 0; c < hd; ++c) o[c] = 0.f;
+        for (int j = 0; j < G; ++j) {
+            const float* kj = stage ? Ks + j * hd : qkv + (base + j) * 3 * d + d + off;
+            const float* vj = stage ? Vs + j * hd : qkv + (base + j) * 3 * d + 2 * d + off;
+            float acc = 0.f;
+            for (int c = 0; c < hd; ++c) acc = fmaf(q[c], kj[c], acc);
+            const float p = expf(acc * scale - mx);
+            sum += p;
+            for (int c = 0; c < hd; ++c) o[c] = fmaf(p, vj[c], o[c]);
+        }
+        const float inv = 1.0f / sum;
+        for (int c = 0; c < hd; ++c) o[c] *= inv;
+    }
+}
+
+void launch_attention_f32(const float* qkv, int64_t rows, int G, int d, int heads, float* cat,
+                          cudaStream_t s, int64_t* launches) {
+    const int64_t n_groups = rows / G;
+    if (n_groups == 0) return;
+    const int hd = d / heads;
+    const size_t smem = 2ull * G * hd * sizeof(float);
+    const bool stage = smem <= 48 * 1024;
+    dim3 grid(static_cast<unsigned>(n_groups), static_cast<unsigned>(heads));
+    k_attention_f32<<<grid, 128, stage ? smem : 0, s>>>(qkv, G, d, heads, cat, stage);
+    ++*launches;
+}
+
+// ------------------------------------------------------------------ row scatter to active order
+
+__global__ void k_scatter_rows(const float* __restrict__ src, const int32_t* __restrict__ ids,
+                               const uint32_t* __restrict__ rank, int64_t n, int d,
+                               float* __restrict__ dst) {
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (r >= n) return;
+    const int64_t id = ids ? ids[r] : r;
+    const int64_t o = rank ? rank[id] : r;
+    for (int c = threadIdx.x & 31; c < d; c += 32) dst[o * d + c] = src[id * d + c];
+}
+
+void launch_scatter_rows(const float* src, const int32_t* ids, const uint32_t* rank, int64_t n,
+                         int d, float* dst, cudaStream_t s, int64_t* launches) {
+    k_scatter_rows<<<static_cast<unsigned>((n + 7) / 8), 256, 0, s>>>(src, ids, rank, n, d, dst);
+    ++*launches;
+}
+
+} // namespace fwa_b200

@@ -1,0 +1,485 @@
+// Window sort (Eq. 1 of FlatFormer), equal-size grouping and drop schedule on
+// the device, bit-exact with the reference:
+//
+//   make_sort_key   /root/reference/proj/include/fwa/flatten.hpp:49-69
+//   key_less        flatten.hpp:41-47
+//   sort            flatten.hpp:97-120
+//   group           flatten.hpp:134-146
+//   drop/compaction /root/reference/proj/include/fwa/backbone.hpp:285-316
+//
+// Design: all four (axis, shift) specs of one or many
+// frames are sorted in ONE batched pass.
+//   K1 keys:   fp64 shift/div/floor/mul/sub with explicit round-to-nearest
+//              intrinsics (no FMA contraction can change a key bit), + window
+//              min/max per spec.
+//   K2 bins:   dense window-bin id (spec, frame, win_major, win_minor) — the
+//              lexicographic order of (win_major, win_minor) IS the bin order —
+//              and an HBM histogram (1-digit counting sort on the window id).
+//   K3 scan + scatter into bins (order inside a bin is irrelevant: K4 totally
+//              orders it).
+//   K4 per-bin exact comparator sort on (loc_major, loc_minor, orig index):
+//              a warp rank-sort in shared memory for bins <= 128 points (pillar
+//              windows hold <= (9+1)^2), a CTA rank-sort for <= 4096, and a
+//              CTA bitonic network in global scratch beyond that, so any input
+//              is ordered exactly as std::sort(key_less) orders it.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <climits>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace fwa_b200 {
+
+// ------------------------------------------------------------------ scan
+
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 4;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_tiles(const uint32_t* in, uint32_t* out,
+                                                              int64_t n, uint32_t* tile_sums) {
+    __shared__ uint32_t warp_tot[32];
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
+    uint32_t v[kScanItems];
+    uint32_t run = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const int64_t i = base + k;
+        v[k] = i < n ? in[i] : 0u;
+        const uint32_t t = v[k];
+        v[k] = run;
+        run += t;
+    }
+    // warp-inclusive scan of per-thread totals
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t x = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t w = warp_tot[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        warp_tot[lane] = w;
+    }
+    __syncthreads();
+    const uint32_t excl = x - run + (wid ? warp_tot[wid - 1] : 0u);
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const int64_t i = base + k;
+        if (i < n) out[i] = v[k] + excl;
+    }
+    if (threadIdx.x == kScanThreads - 1 && tile_sums) tile_sums[blockIdx.x] = excl + run;
+}
+
+__global__ void k_scan_add(uint32_t* out, int64_t n, const uint32_t* tile_off) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * kScanTile + threadIdx.x;
+    const uint32_t add = tile_off[blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const int64_t j = i + static_cast<int64_t>(k) * kScanThreads;
+        if (j < n) out[j] += add;
+    }
+}
+
+size_t scan_tmp_words(int64_t n) {
+    size_t words = 0;
+    int64_t m = n;
+    while (m > kScanTile) {
+        m = (m + kScanTile - 1) / kScanTile;
+        words += static_cast<size_t>(m);
+    }
+    return words + 1;
+}
+
+void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* tmp,
+                        uint32_t* d_total, cudaStream_t s, int64_t* launches) {
+    if (n <= 0) return;
+    // in-place safe: every element is read and rewritten by the same thread
+    const int64_t tiles = (n + kScanTile - 1) / kScanTile;
+    if (tiles == 1) {
+        k_scan_tiles<<<1, kScanThreads, 0, s>>>(in, out, n, d_total);
+        ++*launches;
+        return;
+    }
+    uint32_t* sums = tmp;
+    k_scan_tiles<<<static_cast<unsigned>(tiles), kScanThreads, 0, s>>>(in, out, n, sums);
+    ++*launches;
+    exclusive_scan_u32(sums, sums, tiles, tmp + tiles, d_total, s, launches);
+    k_scan_add<<<static_cast<unsigned>(tiles), kScanThreads, 0, s>>>(out, n, sums);
+    ++*launches;
+}
+
+// ------------------------------------------------------------------ K1 keys
+
+__global__ void k_init_minmax(long long* mm, int n) {
+    const int i = threadIdx.x;
+    if (i < n) mm[i] = (i & 1) ? LLONG_MIN : LLONG_MAX;  // [min_M, max_M, min_m, max_m] per spec
+}
+
+FWA_DEVINL long long wmin(long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const long long y = __shfl_xor_sync(0xffffffffu, v, o);
+        v = y < v ? y : v;
+    }
+    return v;
+}
+FWA_DEVINL long long wmax(long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const long long y = __shfl_xor_sync(0xffffffffu, v, o);
+        v = y > v ? y : v;
+    }
+    return v;
+}
+
+// One thread per (spec, point).  flatten.hpp:49-69, op by op, round-to-nearest.
+__global__ void __launch_bounds__(256) k_sort_keys(const double* __restrict__ coords, int64_t ntot,
+                                                   int n_specs, double w_x, double w_y,
+                                                   long long* __restrict__ win,
+                                                   double* __restrict__ loc,
+                                                   long long* __restrict__ minmax) {
+    const int s = blockIdx.y;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool axis_y = s >= 2, shift = (s & 1) != 0;
+    long long wM = LLONG_MAX, wm = LLONG_MAX, xM = LLONG_MIN, xm = LLONG_MIN;
+    if (i < ntot) {
+        const double2 c = reinterpret_cast<const double2*>(coords)[i];
+        double cx = c.x, cy = c.y;
+        if (shift) {
+            cx = __dadd_rn(cx, __ddiv_rn(w_x, 2.0));
+            cy = __dadd_rn(cy, __ddiv_rn(w_y, 2.0));
+        }
+        const double cm = axis_y ? cy : cx, cn = axis_y ? cx : cy;
+        const double wmj = axis_y ? w_y : w_x, wmn = axis_y ? w_x : w_y;
+        const long long a = static_cast<long long>(floor(__ddiv_rn(cm, wmj)));
+        const long long b = static_cast<long long>(floor(__ddiv_rn(cn, wmn)));
+        const double la = __dsub_rn(cm, __dmul_rn(static_cast<double>(a), wmj));
+        const double lb = __dsub_rn(cn, __dmul_rn(static_cast<double>(b), wmn));
+        const int64_t e = static_cast<int64_t>(s) * ntot + i;
+        reinterpret_cast<longlong2*>(win)[e] = make_longlong2(a, b);
+        reinterpret_cast<double2*>(loc)[e] = make_double2(la, lb);
+        wM = xM = a;
+        wm = xm = b;
+    }
+    wM = wmin(wM);
+    xM = wmax(xM);
+    wm = wmin(wm);
+    xm = wmax(xm);
+    __shared__ long long red[4][8];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) {
+        red[0][wid] = wM;
+        red[1][wid] = xM;
+        red[2][wid] = wm;
+        red[3][wid] = xm;
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        const int q = threadIdx.x;
+        long long v = red[q][0];
+        for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
+            v = (q & 1) ? (red[q][w] > v ? red[q][w] : v) : (red[q][w] < v ? red[q][w] : v);
+        long long* dst = minmax + s * 4 + q;
+        if (q & 1) atomicMax(dst, v);
+        else atomicMin(dst, v);
+    }
+}
+
+void launch_sort_keys(const double* coords, int64_t ntot, int n_specs, double w_x, double w_y,
+                      long long* win, double* loc, long long* minmax, cudaStream_t s,
+                      int64_t* launches) {
+    k_init_minmax<<<1, 32, 0, s>>>(minmax, 4 * n_specs);
+    dim3 grid(static_cast<unsigned>((ntot + 255) / 256), static_cast<unsigned>(n_specs));
+    k_sort_keys<<<grid, 256, 0, s>>>(coords, ntot, n_specs, w_x, w_y, win, loc, minmax);
+    *launches += 2;
+}
+
+// ------------------------------------------------------------------ K2 bins + histogram
+
+FWA_DEVINL int frame_of(const int64_t* off, int n_frames, int64_t i) {
+    int lo = 0, hi = n_frames - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (off[mid] <= i) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(256) k_bins_hist(const long long* __restrict__ win, int64_t ntot,
+                                                   const int64_t* __restrict__ frame_off,
+                                                   int n_frames, const SpecBins* __restrict__ specs,
+                                                   uint32_t* __restrict__ bin_of,
+                                                   uint32_t* __restrict__ hist) {
+    const int s = blockIdx.y;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= ntot) return;
+    const SpecBins sb = specs[s];
+    const int64_t e = static_cast<int64_t>(s) * ntot + i;
+    const longlong2 w = reinterpret_cast<const longlong2*>(win)[e];
+    const int f = n_frames > 1 ? frame_of(frame_off, n_frames, i) : 0;
+    const long long bin = sb.base + static_cast<long long>(f) * sb.bins_per_frame +
+                          (w.x - sb.min_major) * sb.range_minor + (w.y - sb.min_minor);
+    bin_of[e] = static_cast<uint32_t>(bin);
+    atomicAdd(hist + bin, 1u);
+}
+
+void launch_bins_hist(const long long* win, int64_t ntot, int n_specs, const int64_t* d_frame_off,
+                      int n_frames, const SpecBins* d_specs, uint32_t* bin_of, uint32_t* hist,
+                      cudaStream_t s, int64_t* launches) {
+    dim3 grid(static_cast<unsigned>((ntot + 255) / 256), static_cast<unsigned>(n_specs));
+    k_bins_hist<<<grid, 256, 0, s>>>(win, ntot, d_frame_off, n_frames, d_specs, bin_of, hist);
+    ++*launches;
+}
+
+// ------------------------------------------------------------------ K3 scatter into bins
+
+__global__ void __launch_bounds__(256) k_bin_scatter(const uint32_t* __restrict__ bin_of,
+                                                     int64_t total, int64_t ntot,
+                                                     uint32_t* __restrict__ cursor,
+                                                     int32_t* __restrict__ pre) {
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= total) return;
+    const uint32_t pos = atomicAdd(cursor + bin_of[e], 1u);
+    pre[pos] = static_cast<int32_t>(e % ntot);
+}
+
+void launch_bin_scatter(const uint32_t* bin_of, int64_t ntot, int n_specs, uint32_t* cursor,
+                        int32_t* pre, cudaStream_t s, int64_t* launches) {
+    const int64_t total = ntot * n_specs;
+    k_bin_scatter<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(bin_of, total, ntot,
+                                                                           cursor, pre);
+    ++*launches;
+}
+
+// ------------------------------------------------------------------ K4 per-bin exact sort
+
+// key_less restricted to one window: (loc_major, loc_minor, orig index).
+FWA_DEVINL bool loc_less(double a0, double a1, int ai, double b0, double b1, int bi) {
+    if (a0 != b0) return a0 < b0;
+    if (a1 != b1) return a1 < b1;
+    return ai < bi;
+}
+
+constexpr int kWarpBin = 128;   // bins up to this size: one warp, shared memory
+constexpr int kCtaBin = 4096;   // up to this: one CTA, shared-memory rank sort
+constexpr int kBinWarps = 8;
+
+__global__ void __launch_bounds__(kBinWarps * 32) k_bin_sort_small(
+    const uint32_t* __restrict__ bin_start, const uint32_t* __restrict__ hist, uint32_t n_bins,
+    const int32_t* __restrict__ pre, const double* __restrict__ loc, int64_t ntot,
+    int32_t* __restrict__ sorted) {
+    __shared__ double s_a[kBinWarps][kWarpBin];
+    __shared__ double s_b[kBinWarps][kWarpBin];
+    __shared__ int s_i[kBinWarps][kWarpBin];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t bin = blockIdx.x * kBinWarps + wid;
+    if (bin >= n_bins) return;
+    const int n = static_cast<int>(hist[bin]);
+    if (n == 0 || n > kWarpBin) return;
+    const uint32_t start = bin_start[bin];
+    const int64_t spec_base = (static_cast<int64_t>(start) / ntot) * ntot;
+    if (n == 1) {
+        if (lane == 0) sorted[start] = pre[start];
+        return;
+    }
+    for (int k = lane; k < n; k += 32) {
+        const int id = pre[start + k];
+        const double2 l = reinterpret_cast<const double2*>(loc)[spec_base + id];
+        s_a[wid][k] = l.x;
+        s_b[wid][k] = l.y;
+        s_i[wid][k] = id;
+    }
+    __syncwarp();
+    for (int k = lane; k < n; k += 32) {
+        const double a = s_a[wid][k], b = s_b[wid][k];
+        const int id = s_i[wid][k];
+        int rank = 0;
+        for (int j = 0; j < n; ++j) rank += loc_less(s_a[wid][j], s_b[wid][j], s_i[wid][j], a, b, id);
+        sorted[start + rank] = id;
+    }
+}
+
+__global__ void __launch_bounds__(512) k_bin_sort_large(
+    const uint32_t* __restrict__ bin_start, const uint32_t* __restrict__ hist, uint32_t n_bins,
+    const int32_t* __restrict__ pre, const double* __restrict__ loc, int64_t ntot,
+    int32_t* __restrict__ sorted, int32_t* __restrict__ scratch) {
+    extern __shared__ unsigned char smem_raw[];
+    double* s_a = reinterpret_cast<double*>(smem_raw);
+    double* s_b = s_a + kCtaBin;
+    int* s_i = reinterpret_cast<int*>(s_b + kCtaBin);
+    for (uint32_t bin = blockIdx.x; bin < n_bins; bin += gridDim.x) {
+        const int n = static_cast<int>(hist[bin]);
+        if (n <= kWarpBin) continue;
+        const uint32_t start = bin_start[bin];
+        const int64_t spec_base = (static_cast<int64_t>(start) / ntot) * ntot;
+        const double2* L = reinterpret_cast<const double2*>(loc) + spec_base;
+        if (n <= kCtaBin) {
+            for (int k = threadIdx.x; k < n; k += blockDim.x) {
+                const int id = pre[start + k];
+                const double2 l = L[id];
+                s_a[k] = l.x;
+                s_b[k] = l.y;
+                s_i[k] = id;
+            }
+            __syncthreads();
+            for (int k = threadIdx.x; k < n; k += blockDim.x) {
+                const double a = s_a[k], b = s_b[k];
+                const int id = s_i[k];
+                int rank = 0;
+                for (int j = 0; j < n; ++j) rank += loc_less(s_a[j], s_b[j], s_i[j], a, b, id);
+                sorted[start + rank] = id;
+            }
+            __syncthreads();
+        } else {
+            // bitonic network over next_pow2(n) slots of global scratch
+            // (slot range [2*start, 2*start + P) never overlaps another bin's).
+            int P = 1;
+            while (P < n) P <<= 1;
+            int32_t* v = scratch + 2 * static_cast<int64_t>(start);
+            for (int k = threadIdx.x; k < P; k += blockDim.x) v[k] = k < n ? pre[start + k] : -1;
+            __syncthreads();
+            for (int size = 2; size <= P; size <<= 1) {
+                for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                    for (int t = threadIdx.x; t < P / 2; t += blockDim.x) {
+                        const int lo = 2 * t - (t & (stride - 1));
+                        const int hi = lo + stride;
+                        const bool up = (lo & size) == 0;
+                        const int a = v[lo], b = v[hi];
+                        // -1 is +infinity
+                        bool b_less_a;
+                        if (a < 0) b_less_a = b >= 0;
+                        else if (b < 0) b_less_a = false;
+                        else {
+                            const double2 la = L[a], lb = L[b];
+                            b_less_a = loc_less(lb.x, lb.y, b, la.x, la.y, a);
+                        }
+                        if (b_less_a == up) {
+                            v[lo] = b;
+                            v[hi] = a;
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+            for (int k = threadIdx.x; k < n; k += blockDim.x) sorted[start + k] = v[k];
+            __syncthreads();
+        }
+    }
+}
+
+void launch_bin_sort(const uint32_t* bin_start, const uint32_t* hist, uint32_t n_bins,
+                     const int32_t* pre, const double* loc, int64_t ntot, int32_t* sorted,
+                     int32_t* scratch, cudaStream_t s, int64_t* launches) {
+    const unsigned grid = (n_bins + kBinWarps - 1) / kBinWarps;
+    k_bin_sort_small<<<grid, kBinWarps * 32, 0, s>>>(bin_start, hist, n_bins, pre, loc, ntot,
+                                                     sorted);
+    static bool attr_set = false;
+    const int smem = kCtaBin * (8 + 8 + 4);
+    if (!attr_set) {
+        cudaFuncSetAttribute(k_bin_sort_large, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr_set = true;
+    }
+    k_bin_sort_large<<<kNumSMs, 512, smem, s>>>(bin_start, hist, n_bins, pre, loc, ntot, sorted,
+                                                scratch);
+    *launches += 2;
+}
+
+// ------------------------------------------------------------------ schedule kernels
+
+// Block 0 uses spec 0 (X, no shift).  Its per-frame tail beyond rows_f is the
+// dropped residual (flatten.hpp:134-146); record ids in tail order
+// (backbone.hpp:285-291) and flag them.
+__global__ void k_drop_mark(const int32_t* __restrict__ sorted0, int64_t ntot,
+                            const int64_t* __restrict__ frame_off, const int64_t* __restrict__ rows,
+                            const int64_t* __restrict__ drop_off, int n_frames,
+                            uint8_t* __restrict__ dropped, int32_t* __restrict__ dropped_ids) {
+    const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= ntot) return;
+    const int f = n_frames > 1 ? frame_of(frame_off, n_frames, j) : 0;
+    const int64_t t = j - frame_off[f] - rows[f];
+    if (t >= 0) {
+        const int id = sorted0[j];
+        dropped[id] = 1;
+        if (dropped_ids) dropped_ids[drop_off[f] + t] = id;
+    }
+}
+
+void launch_drop_mark(const int32_t* sorted0, int64_t ntot, const int64_t* d_frame_off,
+                      const int64_t* d_rows, const int64_t* d_drop_off, int n_frames,
+                      uint8_t* dropped, int32_t* dropped_ids, cudaStream_t s, int64_t* launches) {
+    k_drop_mark<<<static_cast<unsigned>((ntot + 255) / 256), 256, 0, s>>>(
+        sorted0, ntot, d_frame_off, d_rows, d_drop_off, n_frames, dropped, dropped_ids);
+    ++*launches;
+}
+
+__global__ void k_keep_flags(const uint8_t* __restrict__ dropped, int64_t n, uint32_t* flags) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) flags[i] = dropped[i] ? 0u : 1u;
+}
+
+void launch_keep_flags(const uint8_t* dropped, int64_t ntot, uint32_t* flags, cudaStream_t s,
+                       int64_t* launches) {
+    k_keep_flags<<<static_cast<unsigned>((ntot + 255) / 256), 256, 0, s>>>(dropped, ntot, flags);
+    ++*launches;
+}
+
+__global__ void k_kept_ids(const uint32_t* __restrict__ rank, const uint8_t* __restrict__ dropped,
+                           int64_t n, int32_t* __restrict__ kept) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n && !dropped[i]) kept[rank[i]] = static_cast<int32_t>(i);
+}
+
+void launch_kept_ids(const uint32_t* kept_rank, const uint8_t* dropped, int64_t ntot,
+                     int32_t* kept_ids, cudaStream_t s, int64_t* launches) {
+    k_kept_ids<<<static_cast<unsigned>((ntot + 255) / 256), 256, 0, s>>>(kept_rank, dropped, ntot,
+                                                                        kept_ids);
+    ++*launches;
+}
+
+__global__ void k_spec_keep_flags(const int32_t* __restrict__ sorted, int64_t total,
+                                  const uint8_t* __restrict__ dropped, uint32_t* flags) {
+    const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j < total) flags[j] = dropped[sorted[j]] ? 0u : 1u;
+}
+
+void launch_spec_keep_flags(const int32_t* sorted, int64_t total, const uint8_t* dropped,
+                            uint32_t* flags, cudaStream_t s, int64_t* launches) {
+    k_spec_keep_flags<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(sorted, total,
+                                                                               dropped, flags);
+    ++*launches;
+}
+
+// Restrict each spec's full-set plan to the kept set, preserving order: the
+// result is bit-identical to re-sorting the compacted coordinates (the order
+// is total on (key, original id) and compaction preserves relative order;
+// SURVEY.md Appendix B.6, pinned by tests/test_gpu_parity.py).
+__global__ void k_spec_compact(const int32_t* __restrict__ sorted, int64_t total,
+                               const uint8_t* __restrict__ dropped,
+                               const uint32_t* __restrict__ pos, int32_t* __restrict__ idx) {
+    const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j < total) {
+        const int id = sorted[j];
+        if (!dropped[id]) idx[pos[j]] = id;
+    }
+}
+
+void launch_spec_compact(const int32_t* sorted, int64_t total, const uint8_t* dropped,
+                         const uint32_t* pos, int32_t* idx, cudaStream_t s, int64_t* launches) {
+    k_spec_compact<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(sorted, total,
+                                                                            dropped, pos, idx);
+    ++*launches;
+}
+
+} // namespace fwa_b200

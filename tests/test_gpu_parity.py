@@ -1,0 +1,325 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracles.
+
+Integer outputs (window-sort permutations, groups, drops, kept set, cache stats)
+must be bit-exact.  Features: normwise max rel err (tests/test_kernels.cpp:25-33)
+<= 1e-4 in the fp32 check mode and <= 1e-2 in the bf16 tensor-core mode (the
+north-star tolerances).  Full-size frames are checked through size-independent
+properties (sortedness of the reference keys, permutation/partition invariants,
+zero-weight identity, determinism, batch == per-frame)."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2301_08739_b200 as F
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+SPECS = [(0, 0), (0, 1), (1, 0), (1, 1)]
+TOL_FP32, TOL_BF16 = 1e-4, 1e-2
+
+
+@pytest.fixture(scope="module")
+def ctx32():
+    return F.Context(0, precision="fp32")
+
+
+@pytest.fixture(scope="module")
+def ctx16():
+    return F.Context(0, precision="bf16")
+
+
+def _spec(w, ay, sh):
+    return F.WindowSpec(w[0], w[1], bool(sh), "Y" if ay else "X")
+
+
+# ----------------------------------------------------------------------------- sort
+
+def test_sort_golden_cases(ctx32):
+    d = np.load(os.path.join(GOLD, "sort_cases.npz"))
+    for name in d["names"]:
+        c = d[f"{name}_coords"]
+        w = d[f"{name}_w"]
+        for ay, sh in SPECS:
+            got = ctx32.sort(c, _spec(w, ay, sh))
+            assert np.array_equal(got, d[f"{name}_perm_{ay}{sh}"]), (name, ay, sh)
+
+
+def test_sort_random_scenes_vs_numpy_oracle(ctx32):
+    """acceptance.cpp:138-179 style: random scenes up to 10k points, w = 2.88, all specs,
+    plus boundary/duplicate scenes and an oversize-window scene (CTA + bitonic bins)."""
+    rng = np.random.default_rng(1001)
+    for trial in range(24):
+        n = int(rng.integers(100, 10000))
+        c = rng.uniform(-50, 50, size=(n, 2))
+        ay, sh = SPECS[trial % 4]
+        assert np.array_equal(ctx32.sort(c, _spec((2.88, 2.88), ay, sh)), O.np_sort(c, 2.88, 2.88, sh, ay))
+    for v in range(4):
+        c = 2.0 * (rng.integers(0, 9, size=(2000, 2)).astype(np.float64) - 4.0)
+        if v >= 2:
+            c = np.concatenate([c, c[::3]])
+        for ay, sh in SPECS:
+            assert np.array_equal(ctx32.sort(c, _spec((2.0, 2.0), ay, sh)), O.np_sort(c, 2.0, 2.0, sh, ay))
+    # big windows: bins of ~300 (CTA rank sort) and ~6000 (bitonic network) points
+    for w in (10.0, 60.0):
+        c = rng.uniform(-60, 60, size=(20000, 2)).round(1)  # many exact ties in loc
+        for ay, sh in SPECS:
+            assert np.array_equal(ctx32.sort(c, _spec((w, w), ay, sh)), O.np_sort(c, w, w, sh, ay))
+    # identical points sort by original index (test_flatten.cpp:62-66); non-square windows
+    assert list(ctx32.sort(np.ones((3, 2)), F.WindowSpec(2.0, 2.0))) == [0, 1, 2]
+    c = rng.uniform(-10, 10, size=(500, 2))
+    assert np.array_equal(ctx32.sort(c, F.WindowSpec(1.5, 0.75, True, "Y")), O.np_sort(c, 1.5, 0.75, 1, 1))
+
+
+def test_sort_full_size_frames_all_specs(ctx32):
+    """F60 (60,897 pillars) and F250 (255,066): bit-exact vs the NumPy oracle, and the
+    reference keys are lexicographically non-decreasing along the GPU permutation."""
+    w = 9 * 0.32
+    for name in ("F60", "F250"):
+        ps = F.make_pillars(F.SCENES[name], 42)
+        for ay, sh in SPECS:
+            got = ctx32.sort(ps.coords, _spec((w, w), ay, sh))
+            assert np.array_equal(got, O.np_sort(ps.coords, w, w, sh, ay)), (name, ay, sh)
+            wm, wn, lm, ln = O.np_sort_keys(ps.coords, w, w, sh, ay)
+            k = np.stack([wm[got], wn[got]], 1)
+            assert np.all((np.diff(k[:, 0]) > 0) | ((np.diff(k[:, 0]) == 0) & (np.diff(k[:, 1]) >= 0)))
+            assert np.array_equal(np.sort(got), np.arange(ps.size()))
+
+
+# ----------------------------------------------------------------------------- positional embedding
+
+def test_positional_embedding(ctx32):
+    ps = F.make_pillars(F.SCENES["F10"], 42)
+    got = ctx32.positional_embedding(ps.coords, 128)
+    want = O.port_positional_embedding(ps.coords, 128)
+    assert np.max(np.abs(got - want)) <= 1e-6  # fp64 sin/cos, f32 rounding
+
+
+# ----------------------------------------------------------------------------- block
+
+def test_block_forward_fp32_vs_f64_oracle(ctx32):
+    """acceptance.cpp:203-239 (C3): f32 block vs dense f64 oracle; here on the GPU
+    fp32 check path at several (G, D, H) shapes incl. G=1 and identical tokens."""
+    rng = np.random.default_rng(1003)
+    shapes = [(1, 16, 4), (7, 8, 2), (13, 32, 8), (31, 64, 4), (5, 12, 1), (29, 48, 8),
+              (17, 24, 2), (32, 40, 8), (3, 4, 1), (20, 56, 8)]
+    for trial, (G, D, H) in enumerate(shapes):
+        ng = int(rng.integers(1, 4))
+        cfg = F.FwaConfig(d_model=D, n_heads=H, d_ff=2 * D, n_blocks=1)
+        rec = F.init_backbone_params(cfg, trial)
+        f = rng.normal(size=(ng * G, D)).astype(np.float32)
+        pe = (0.3 * rng.normal(size=(ng * G, D))).astype(np.float32)
+        if trial == 1:
+            f[:] = f[0]
+            pe[:] = pe[0]
+        got = ctx32.fwa_block_forward(f, pe, rec, ng)
+        want = O.port_block_forward(f, pe, ng, rec)
+        assert O.max_rel_err(got, want) <= 1e-5, (trial, G, D, H)
+
+
+def test_block_forward_golden_d128(ctx32, ctx16):
+    g = np.load(os.path.join(GOLD, "block_d128.npz"))
+    blob = F.init_backbone_params(F.FwaConfig(), int(g["param_seed"]))
+    rec = blob[:len(blob) // 8]
+    e32 = O.max_rel_err(ctx32.fwa_block_forward(g["f"], g["pe"], rec, 3), g["out64"])
+    e16 = O.max_rel_err(ctx16.fwa_block_forward(g["f"], g["pe"], rec, 3), g["out64"])
+    assert e32 <= 1e-5, e32
+    assert e16 <= TOL_BF16, e16
+    assert ctx16.fast_path(F.FwaConfig(group_size=69))
+
+
+@pytest.mark.parametrize("G", [16, 33, 64, 69, 128])
+def test_block_forward_bf16_group_sizes(ctx16, G):
+    """tcgen05 QKV / out-proj+FFN and mma.sync attention at several group sizes."""
+    rng = np.random.default_rng(G)
+    cfg = F.FwaConfig(group_size=G)
+    rec = F.init_backbone_params(cfg, 3)[:16 + 4 * 132480]
+    ng = 300 // G + 1
+    f = rng.normal(size=(ng * G, 128)).astype(np.float32)
+    pe = (0.3 * rng.normal(size=(ng * G, 128))).astype(np.float32)
+    got = ctx16.fwa_block_forward(f, pe, rec, ng)
+    want = O.port_block_forward(f, pe, ng, rec)
+    assert O.max_rel_err(got, want) <= TOL_BF16
+
+
+# ----------------------------------------------------------------------------- backbone
+
+def _check_ints(res, want_kept, want_dropped, want_dpb, want_cache):
+    assert np.array_equal(res.kept_indices, want_kept)
+    assert np.array_equal(np.concatenate(res.dropped_indices), want_dropped)
+    assert list(res.stats.dropped_per_block) == list(want_dpb)
+    assert (res.stats.cache.computed, res.stats.cache.hits) == tuple(want_cache)
+
+
+def test_backbone_golden_small(ctx32):
+    g = np.load(os.path.join(GOLD, "backbone_small.npz"))
+    d, h, dff, G, nb = (int(x) for x in g["cfg"])
+    cfg = F.FwaConfig(d_model=d, n_heads=h, d_ff=dff, group_size=G, n_blocks=nb)
+    ctx32.load_params(cfg, g["blob"].tobytes())
+    r = ctx32.run_backbone(F.PillarSet(g["coords"], g["feats"]), cfg, want_block_perms=True)
+    _check_ints(r, g["kept"], g["dropped"], g["dropped_per_block"], g["cache"])
+    for b in range(nb):
+        assert np.array_equal(r.block_perms[b], g[f"plan{b}"]), b
+    assert O.max_rel_err(r.features, g["features"]) <= TOL_FP32
+
+
+@pytest.mark.parametrize("prec,tol", [("fp32", TOL_FP32), ("bf16", TOL_BF16)])
+def test_backbone_golden_d128(prec, tol, ctx32, ctx16):
+    ctx = ctx32 if prec == "fp32" else ctx16
+    g = np.load(os.path.join(GOLD, "backbone_d128.npz"))
+    s = [float(x) for x in g["scene"]]
+    scene = F.SceneSpec(int(s[0]), int(s[1]), int(s[2]), s[3], s[4], s[5], int(s[6]), int(s[7]))
+    ps = F.make_pillars(scene, int(g["scene_seed"]))
+    cfg = F.FwaConfig()
+    ctx.load_params(cfg, F.init_backbone_params(cfg, int(g["param_seed"])))
+    r = ctx.run_backbone(ps, cfg, want_block_perms=True)
+    _check_ints(r, g["kept"], g["dropped"], g["dropped_per_block"], g["cache"])
+    for b in range(8):
+        assert np.array_equal(r.block_perms[b], g[f"plan{b}"]), b
+    err = O.max_rel_err(r.features, g["features"])
+    assert err <= tol, err
+
+
+@pytest.mark.parametrize("prec,tol", [("fp32", TOL_FP32), ("bf16", TOL_BF16)])
+def test_backbone_config1_f30_one_block(prec, tol, ctx32, ctx16):
+    """BASELINE config 1: one block (X, no shift), G 69, D 128, H 8 on F30 (30,212 pillars)."""
+    ctx = ctx32 if prec == "fp32" else ctx16
+    ps = F.make_pillars(F.SCENES["F30"], 42)
+    cfg = F.FwaConfig(n_blocks=1)
+    blob = F.init_backbone_params(cfg, 42)
+    ctx.load_params(cfg, blob)
+    r = ctx.run_backbone(ps, cfg)
+    w = O.port_run_backbone(ps.coords, ps.features.astype(np.float32), O.make_cfg(n_blocks=1), blob)
+    _check_ints(r, w["kept"], w["dropped"], w["dropped_per_block"], w["cache"])
+    assert r.stats.dropped_per_block == [30212 % 69]
+    err = O.max_rel_err(r.features, w["features"])
+    assert err <= tol, err
+
+
+def test_backbone_cache_counts_and_drops(ctx32):
+    """test_backbone.cpp:149-183 / acceptance.cpp:451-465, 496-536."""
+    cfg = F.FwaConfig(d_model=16, n_heads=4, d_ff=32, group_size=16, n_blocks=8)
+    i = np.arange(640)
+    c = np.stack([((i % 200) + 0.5) * 0.32, ((i // 200) + 0.5) * 0.32], 1)
+    f = np.random.default_rng(0).normal(size=(640, 16))
+    ctx32.load_params(cfg, F.init_backbone_params(cfg, 5))
+    r = ctx32.run_backbone(F.PillarSet(c, f), cfg)
+    assert (r.stats.cache.computed, r.stats.cache.hits) == (4, 4) and len(r.kept_indices) == 640
+    cfg1 = F.FwaConfig(d_model=16, n_heads=4, d_ff=32, group_size=16, n_blocks=1)
+    ctx32.load_params(cfg1, F.init_backbone_params(cfg1, 5))
+    r = ctx32.run_backbone(F.PillarSet(c, f), cfg1)
+    assert (r.stats.cache.computed, r.stats.cache.hits) == (1, 0)
+    cfg2 = F.FwaConfig(d_model=16, n_heads=4, d_ff=32, group_size=69, n_blocks=8)
+    i = np.arange(30000)
+    c2 = np.stack([((i % 200) + 0.5) * 0.32, ((i // 200) + 0.5) * 0.32], 1)
+    f2 = np.random.default_rng(1).normal(size=(30000, 16))
+    blob = F.init_backbone_params(cfg2, 13)
+    ctx32.load_params(cfg2, blob)
+    r = ctx32.run_backbone(F.PillarSet(c2, f2), cfg2)
+    assert r.stats.dropped_per_block == [54, 0, 0, 0, 0, 0, 0, 0]
+    assert (r.stats.cache.computed, r.stats.cache.hits) == (5, 3)
+    w = O.port_run_backbone(c2, f2.astype(np.float32), O.make_cfg(d_model=16, n_heads=4, d_ff=32,
+                                                                  group_size=69), blob)
+    assert np.array_equal(r.kept_indices, w["kept"]) and np.array_equal(r.dropped_indices[0], w["dropped"])
+    assert O.max_rel_err(r.features, w["features"]) <= TOL_FP32
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_zero_weights_identity_bit_exact(prec, ctx32, ctx16):
+    """test_backbone.cpp:69-86: gather -> zero block -> scatter moves the f32 bits unchanged."""
+    ctx = ctx32 if prec == "fp32" else ctx16
+    ps = F.make_pillars(F.SCENES["F10"], 42)
+    cfg = F.FwaConfig(n_blocks=4)
+    rec_len = 16 + 4 * 132480
+    zero = (b"FWAP" + np.array([128, 8, 256], np.uint32).tobytes() + bytes(rec_len - 16)) * 4
+    ctx.load_params(cfg, zero)
+    r = ctx.run_backbone(ps, cfg)
+    assert np.array_equal(r.features, ps.features.astype(np.float32)[r.kept_indices])
+
+
+def test_determinism(ctx16):
+    """acceptance.cpp:467-476: bitwise determinism (no FP atomics on the feature path)."""
+    ps = F.make_pillars(F.SCENES["F10"], 42)
+    cfg = F.FwaConfig(n_blocks=2)
+    blob = F.init_backbone_params(cfg, 7)
+    ctx16.load_params(cfg, blob)
+    a = ctx16.run_backbone(ps, cfg)
+    b = ctx16.run_backbone(ps, cfg)
+    assert np.array_equal(a.features, b.features) and np.array_equal(a.kept_indices, b.kept_indices)
+    w = O.port_run_backbone(ps.coords, ps.features.astype(np.float32), O.make_cfg(n_blocks=2), blob)
+    assert np.array_equal(a.kept_indices, w["kept"])
+    assert O.max_rel_err(a.features, w["features"]) <= TOL_BF16
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_batch_equals_per_frame(prec, ctx32, ctx16):
+    """Frame-parallel batch (config 3 machinery): bitwise equal to per-frame runs."""
+    ctx = ctx32 if prec == "fp32" else ctx16
+    cfg = F.FwaConfig(n_blocks=3)
+    ctx.load_params(cfg, F.init_backbone_params(cfg, 42))
+    frames = [F.make_pillars(F.SCENES["F10"], s) for s in (42, 43, 44)]
+    off = np.cumsum([0] + [p.size() for p in frames])
+    res = ctx.run_batch(np.concatenate([p.coords for p in frames]),
+                        np.concatenate([p.features for p in frames]), off, cfg)
+    ko = np.concatenate([[0], np.cumsum(res["kept_per_frame"])])
+    for i, p in enumerate(frames):
+        r = ctx.run_backbone(p, cfg)
+        assert np.array_equal(res["kept"][ko[i]:ko[i + 1]] - off[i], r.kept_indices)
+        assert np.array_equal(res["features"][ko[i]:ko[i + 1]], r.features)
+
+
+def test_errors_mirror_reference(ctx32):
+    cfg = F.FwaConfig(d_model=16, n_heads=4, d_ff=32, group_size=8, n_blocks=2)
+    blob = F.init_backbone_params(cfg, 1)
+    ctx32.load_params(cfg, blob)
+    c = np.random.default_rng(0).uniform(0, 5, size=(5, 2))
+    with pytest.raises(F.NumericError):          # backbone.hpp:218-222 (N < G)
+        ctx32.run_backbone(F.PillarSet(c, np.zeros((5, 16))), cfg)
+    c = np.random.default_rng(0).uniform(0, 5, size=(40, 2))
+    f = np.zeros((40, 16))
+    f[3, 2] = np.nan
+    with pytest.raises(F.NumericError):          # kernels.hpp:460-461
+        ctx32.run_backbone(F.PillarSet(c, f), cfg)
+    with pytest.raises(F.ParseError):            # kernels.hpp:179-180
+        ctx32.load_params(cfg, b"XXXX" + blob[4:])
+    with pytest.raises(F.ParseError):            # truncated tensor
+        ctx32.load_params(cfg, blob[:-8])
+    with pytest.raises(F.ConfigError):           # backbone.hpp:164-169
+        ctx32.load_params(F.FwaConfig(d_model=16, n_heads=4, d_ff=32, n_blocks=3), blob)
+    with pytest.raises(F.ConfigError):
+        ctx32.load_params(F.FwaConfig(d_model=16, n_heads=2, d_ff=32, n_blocks=2), blob)
+    with pytest.raises(F.ConfigError):
+        F.sort(c, F.WindowSpec(0.0, 1.0))
+
+
+def test_full_size_f60_properties(ctx16):
+    """BASELINE config 2 sizes (F60, 8 blocks): integer schedule bit-exact vs the
+    NumPy oracle's plans restricted to the kept set; zero-weight identity at full size."""
+    ps = F.make_pillars(F.SCENES["F60"], 42)
+    cfg = F.FwaConfig()
+    ctx16.load_params(cfg, F.init_backbone_params(cfg, 42))
+    r = ctx16.run_backbone(ps, cfg, want_block_perms=True)
+    w = 9 * 0.32
+    p0 = O.np_sort(ps.coords, w, w, 0, 0)
+    n = ps.size()
+    nk = (n // 69) * 69
+    assert np.array_equal(np.sort(p0[nk:]), np.sort(r.dropped_indices[0]))
+    assert np.array_equal(r.dropped_indices[0], p0[nk:])
+    kept = np.sort(p0[:nk])
+    assert np.array_equal(r.kept_indices, kept)
+    assert (r.stats.cache.computed, r.stats.cache.hits) == (5, 3)
+    for b in range(8):
+        ay, sh = (b % 4) >= 2, b % 2
+        full = O.np_sort(ps.coords, w, w, sh, ay)
+        if b == 0:
+            want = full
+        else:  # reference re-sorts the compacted coords: local indices into the kept list
+            want = O.np_sort(ps.coords[kept], w, w, sh, ay)
+            # restriction identity
+            rank = np.full(n, -1)
+            rank[kept] = np.arange(nk)
+            restricted = rank[full[np.isin(full, kept)]]
+            assert np.array_equal(restricted, want)
+        assert np.array_equal(r.block_perms[b], want), b
+    assert np.all(np.isfinite(r.features)) and r.features.shape == (nk, 128)

@@ -1,0 +1,86 @@
+"""CPU: the C-ABI library loads, exports every symbol include/fwa_b200.h declares,
+and its host-side input generators are bit-identical to the reference's."""
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2301_08739_b200 as F
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLD = os.path.join(ROOT, "tests", "golden")
+
+
+def fnv(b: bytes) -> str:
+    return F.fnv1a64_hex(b)
+
+
+def test_library_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "fwa_b200.h")).read()
+    declared = set(re.findall(r"\b(fwa_b200_\w+)\s*\(", hdr))
+    assert declared, "no declarations parsed"
+    L = F.lib()
+    missing = [s for s in sorted(declared) if not hasattr(L, s)]
+    assert not missing, missing
+    assert declared == set(F.EXPORTS)
+
+
+def test_generated_frames_match_reference_hashes():
+    """generate_synthetic + pillarize (geometry.hpp:246-386), pillar counts of SURVEY §8d."""
+    gold = json.load(open(os.path.join(GOLD, "scenes.json")))
+    for name in ("F10", "PINNED", "F30", "F60"):
+        ps = F.make_pillars(F.SCENES[name], 42)
+        g = gold[name]
+        assert ps.size() == g["n"], name
+        assert fnv(np.ascontiguousarray(ps.coords).tobytes()) == g["coords_fnv"], name
+        assert fnv(np.ascontiguousarray(ps.features[:512]).tobytes()) == g["feats_fnv"], name
+        assert float(ps.features.sum()) == g["feats_sum"], name
+    assert gold["PINNED"]["n"] == 21199 and gold["F60"]["n"] == 60897
+
+
+def test_init_params_match_reference_hash():
+    gold = json.load(open(os.path.join(GOLD, "scenes.json")))
+    blob = F.init_backbone_params(F.FwaConfig(), 42)
+    assert len(blob) == 8 * (16 + 4 * 132480)
+    assert fnv(blob) == gold["params_default_seed42_fnv"]
+
+
+def test_config_validation_mirrors_reference():
+    F.validate(F.FwaConfig())
+    for bad in (dict(resolution=0.0), dict(window_px=0), dict(group_size=0), dict(n_blocks=0),
+                dict(d_model=6), dict(n_heads=3), dict(d_ff=0)):
+        with pytest.raises(F.ConfigError):
+            F.validate(F.FwaConfig(**bad))
+    c = F.FwaConfig.from_json({"window": [7, 5], "group_size": 32})
+    assert (c.window_px, c.window_py, c.group_size, c.d_model) == (7, 5, 32, 128)
+    assert c.window_x_m() == 7 * 0.32
+
+
+def test_no_gpu_fails_loudly():
+    """Without a CUDA device the product path raises; it never falls back to the CPU."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("GPU present")
+    except Exception:
+        pass
+    with pytest.raises(F.FwaError):
+        F.Context(0)
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libfwa_ref.so")),
+                    reason="oracle/_ref not built")
+def test_generator_equals_reference_live():
+    import oracle as O
+    ps = F.make_pillars(F.SCENES["F10"], 42)
+    s = F.SCENES["F10"]
+    c, f = O.ref_make_pillars(dict(n_clusters=s.n_clusters, ppc_min=s.points_per_cluster_min,
+                                   ppc_max=s.points_per_cluster_max, sigma=s.cluster_sigma,
+                                   ext_x=s.extent_x, ext_y=s.extent_y, n_bg=s.n_background,
+                                   f_in=s.f_in), 42, 128)
+    assert np.array_equal(ps.coords, c) and np.array_equal(ps.features, f)
+    cfg = O.make_cfg(n_blocks=3, d_model=64, n_heads=4, d_ff=96)
+    assert F.init_backbone_params(F.FwaConfig(n_blocks=3, d_model=64, n_heads=4, d_ff=96), 9) == \
+        O.ref_init_params(cfg, 64, 9)
