@@ -22,6 +22,12 @@ namespace fwa_b200 {
 
 constexpr int kPitch = 768 + 16;  // bytes per staged row
 
+// element (row, col) of a 128-row K-major SW128 bf16 image (see tcgen05.cuh sw128_offset)
+FWA_DEVINL uint32_t tc_sw128_offset(int row, int col) {
+    return static_cast<uint32_t>((col >> 6) * 16384 + row * 128 + ((((col & 63) >> 3) ^ (row & 7)) << 4) +
+                                 (col & 7) * 2);
+}
+
 FWA_DEVINL void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                  : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
@@ -43,19 +49,27 @@ FWA_DEVINL void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, u
 
 // NT = padded group / 8 (even); MT = NT / 2 query tiles; KT = NT / 2 key tiles.
 template <int NT>
-__global__ void __launch_bounds__(256) k_attention_mma(const __nv_bfloat16* __restrict__ qkv, int G,
-                                                       __nv_bfloat16* __restrict__ cat) {
-    extern __shared__ uint8_t sm[];
+__global__ void __launch_bounds__(256) k_attention_mma(const __nv_bfloat16* __restrict__ qkv,
+                                                       int64_t rows, int G,
+                                                       uint8_t* __restrict__ cat) {
+    extern __shared__ __align__(16) uint8_t sm[];
     constexpr int Gp = NT * 8;
     const int64_t base = static_cast<int64_t>(blockIdx.x) * G;
-    // ---- stage q|k|v rows (48 x 16 B per row), zero the padding rows
-    const uint4* src = reinterpret_cast<const uint4*>(qkv + base * 384);
-    for (int t = threadIdx.x; t < Gp * 48; t += 256) {
-        const int r = t / 48, c = t % 48;
-        uint4 v = make_uint4(0u, 0u, 0u, 0u);
-        if (r < G) v = src[r * 48 + c];
-        *reinterpret_cast<uint4*>(sm + r * kPitch + c * 16) = v;
+    // ---- stage q|k|v rows: the QKV kernel writes 12 column chunks of [rows x 32]
+    // bf16, so each chunk of this group is one contiguous 64*G-byte run; cp.async
+    // (16 B, L1-bypassing) into a 784 B row pitch; padding rows zeroed.
+    const uint32_t s_base = smem_u32(sm);
+    for (int t = threadIdx.x; t < 12 * Gp * 4; t += 256) {
+        const int c = t / (Gp * 4), rem = t % (Gp * 4), r = rem >> 2, pp = rem & 3;
+        const uint32_t dst = s_base + r * kPitch + c * 64 + pp * 16;
+        if (r < G) {
+            const __nv_bfloat16* src = qkv + (static_cast<int64_t>(c) * rows + base + r) * 32 + pp * 8;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+        } else {
+            asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(dst), "r"(0u) : "memory");
+        }
     }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
     __syncthreads();
     const int head = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t4 = lane & 3;
@@ -134,21 +148,27 @@ __global__ void __launch_bounds__(256) k_attention_mma(const __nv_bfloat16* __re
         }
         const float i0 = 1.0f / l0, i1 = 1.0f / l1;
         const int r0 = mt * 16 + g, r1 = r0 + 8;
+        // output rows go straight into the out-proj kernel's A-operand images: per
+        // 128-row tile, a K-major SW128 [128 x 128] bf16 image (one TMA bulk load there)
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) {
             const int col = head * 16 + nt * 8 + 2 * t4;
-            if (r0 < G)
-                *reinterpret_cast<uint32_t*>(cat + (base + r0) * 128 + col) =
+            if (r0 < G) {
+                const int64_t gr = base + r0;
+                *reinterpret_cast<uint32_t*>(cat + (gr >> 7) * 32768 + tc_sw128_offset(static_cast<int>(gr & 127), col)) =
                     pack_bf16x2(o[nt][0] * i0, o[nt][1] * i0);
-            if (r1 < G)
-                *reinterpret_cast<uint32_t*>(cat + (base + r1) * 128 + col) =
+            }
+            if (r1 < G) {
+                const int64_t gr = base + r1;
+                *reinterpret_cast<uint32_t*>(cat + (gr >> 7) * 32768 + tc_sw128_offset(static_cast<int>(gr & 127), col)) =
                     pack_bf16x2(o[nt][2] * i1, o[nt][3] * i1);
+            }
         }
     }
 }
 
 template <int NT>
-static void launch_nt(const __nv_bfloat16* qkv, int64_t n_groups, int G, __nv_bfloat16* cat,
+static void launch_nt(const __nv_bfloat16* qkv, int64_t rows, int64_t n_groups, int G, uint8_t* cat,
                       cudaStream_t s) {
     const int smem = NT * 8 * kPitch;
     static bool init = false;
@@ -156,23 +176,24 @@ static void launch_nt(const __nv_bfloat16* qkv, int64_t n_groups, int G, __nv_bf
         cudaFuncSetAttribute(k_attention_mma<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         init = true;
     }
-    k_attention_mma<NT><<<static_cast<unsigned>(n_groups), 256, smem, s>>>(qkv, G, cat);
+    k_attention_mma<NT><<<static_cast<unsigned>(n_groups), 256, smem, s>>>(qkv, rows, G, cat);
 }
 
-void launch_attention_mma(const __nv_bfloat16* qkv, int64_t rows, int G, __nv_bfloat16* cat,
+void launch_attention_mma(const __nv_bfloat16* qkv, int64_t rows, int G, __nv_bfloat16* cat_img,
                           cudaStream_t s, int64_t* launches) {
+    uint8_t* cat = reinterpret_cast<uint8_t*>(cat_img);
     const int64_t n_groups = rows / G;
     if (n_groups == 0) return;
     const int nt = ((G + 15) / 16) * 2;
     switch (nt) {
-        case 2: launch_nt<2>(qkv, n_groups, G, cat, s); break;
-        case 4: launch_nt<4>(qkv, n_groups, G, cat, s); break;
-        case 6: launch_nt<6>(qkv, n_groups, G, cat, s); break;
-        case 8: launch_nt<8>(qkv, n_groups, G, cat, s); break;
-        case 10: launch_nt<10>(qkv, n_groups, G, cat, s); break;
-        case 12: launch_nt<12>(qkv, n_groups, G, cat, s); break;
-        case 14: launch_nt<14>(qkv, n_groups, G, cat, s); break;
-        default: launch_nt<16>(qkv, n_groups, G, cat, s); break;
+        case 2: launch_nt<2>(qkv, rows, n_groups, G, cat, s); break;
+        case 4: launch_nt<4>(qkv, rows, n_groups, G, cat, s); break;
+        case 6: launch_nt<6>(qkv, rows, n_groups, G, cat, s); break;
+        case 8: launch_nt<8>(qkv, rows, n_groups, G, cat, s); break;
+        case 10: launch_nt<10>(qkv, rows, n_groups, G, cat, s); break;
+        case 12: launch_nt<12>(qkv, rows, n_groups, G, cat, s); break;
+        case 14: launch_nt<14>(qkv, rows, n_groups, G, cat, s); break;
+        default: launch_nt<16>(qkv, rows, n_groups, G, cat, s); break;
     }
     ++*launches;
 }

@@ -17,6 +17,7 @@
 //   * frames of a batch are concatenated: windows carry the frame id, groups
 //     never cross frames, one launch sequence serves all frames.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -221,10 +222,6 @@ __global__ void k_out_pos(const int32_t* __restrict__ idx, const uint32_t* __res
     if (r < n) out[r] = static_cast<int32_t>(rank[idx[r]]);
 }
 
-__global__ void k_cast_f64_f32(const double* __restrict__ in, int64_t n, float* __restrict__ out) {
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i < n) out[i] = static_cast<float>(in[i]);
-}
 
 std::vector<BlockParams> upload_block_params(const std::vector<Record>& recs, DevBuf& pf32,
                                              DevBuf& pbf16, cudaStream_t st) {
@@ -401,8 +398,9 @@ int32_t* sort_specs(fwa_b200_ctx* c, const double* d_coords, int64_t ntot, int n
     launch_bin_scatter(bin_of, ntot, n_specs, cursor, pre, st, &c->launches);
     int32_t* sorted = ws<int32_t>(c, "sorted", static_cast<size_t>(total));
     int32_t* scratch = ws<int32_t>(c, "sort_scratch", 2 * static_cast<size_t>(total));
+    uint32_t* large = ws<uint32_t>(c, "large_bins", static_cast<size_t>(nbins) + 1);
     launch_bin_sort(bin_start, hist, static_cast<uint32_t>(nbins), pre, loc, ntot, sorted, scratch,
-                    st, &c->launches);
+                    large, st, &c->launches);
     check_launch();
     return sorted;
 }
@@ -498,16 +496,17 @@ struct Scratch {
 // x_out[sidx[r]].  kernels.hpp:636-650 composed with backbone.hpp:245-283.
 void run_block(fwa_b200_ctx* c, const BlockParams& p, const fwa_config_t* cfg, int64_t rows,
                const int32_t* ridx, const float* x_in, const double* x_in64, const float* pe,
-               float* x_out, const int32_t* sidx, bool fast) {
+               const __half* pe16, float* x_out, const int32_t* sidx, bool fast) {
     cudaStream_t st = c->stream;
     const int d = cfg->d_model, dff = cfg->d_ff, G = cfg->group_size;
     if (rows == 0) return;
     if (fast) {
         __nv_bfloat16* qkv = ws<__nv_bfloat16>(c, "qkv16", static_cast<size_t>(rows) * 3 * d);
-        __nv_bfloat16* cat = ws<__nv_bfloat16>(c, "cat16", static_cast<size_t>(rows) * d);
+        // attention output as per-128-row-tile SW128 images (the out-proj A operand)
+        __nv_bfloat16* cat = ws<__nv_bfloat16>(c, "cat16", static_cast<size_t>((rows + 127) / 128) * 128 * d);
         {
             StageEv t(c, FWA_PROF_LN_QKV);
-            launch_ln1_qkv_tc(x_in, x_in64, pe, ridx, rows, p.tc, qkv, c->d_flag, st, &c->launches);
+            launch_ln1_qkv_tc(x_in, x_in64, pe16, ridx, rows, p.tc, qkv, c->d_flag, st, &c->launches);
             check_launch("k_ln1_qkv_tc");
         }
         {
@@ -576,21 +575,24 @@ void forward_device(fwa_b200_ctx* c, const double* d_coords, const float* d_feat
         StageEv t(c, FWA_PROF_SCHEDULE);
         build_schedule(c, d_coords, cfg, S);
     }
-    float* pe = ws<float>(c, "pe", static_cast<size_t>(S.ntot) * d);
+    const bool fast = fast_path_ok(c, d, cfg->n_heads, cfg->d_ff, cfg->group_size);
+    // fast path: fp16 PE rows (|PE| <= 1, abs err <= 2^-12, below the bf16 rounding of
+    // LN1 + PE that follows); check mode: fp32 rows
+    float* pe = fast ? nullptr : ws<float>(c, "pe", static_cast<size_t>(S.ntot) * d);
+    __half* pe16 = fast ? ws<__half>(c, "pe16", static_cast<size_t>(S.ntot) * d) : nullptr;
     {
         StageEv t(c, FWA_PROF_PE);
-        launch_positional_embedding(d_coords, S.ntot, d, pe_freq(c, d), pe, st, &c->launches);
+        launch_positional_embedding(d_coords, S.ntot, d, pe_freq(c, d), pe, pe16, st, &c->launches);
     }
     float* X = ws<float>(c, "X", static_cast<size_t>(S.ntot) * d);
     CUDA_OK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), st));
-    const bool fast = fast_path_ok(c, d, cfg->n_heads, cfg->d_ff, cfg->group_size);
     for (int b = 0; b < cfg->n_blocks; ++b) {
         const int s = b % 4;
         const int32_t* idx = S.idx + S.K * s;
         const bool last = b == cfg->n_blocks - 1;
         const float* xin = b == 0 ? d_feats : X;
         const double* xin64 = b == 0 ? d_feats64 : nullptr;
-        run_block(c, c->blocks[static_cast<size_t>(b)], cfg, S.K, idx, xin, xin64, pe,
+        run_block(c, c->blocks[static_cast<size_t>(b)], cfg, S.K, idx, xin, xin64, pe, pe16,
                   last ? d_out : X, last ? S.out_pos : idx, fast);
     }
     if (d_kept)
@@ -892,7 +894,12 @@ int fwa_b200_block_forward(fwa_b200_ctx* c, const float* f, const float* pe, int
         CUDA_OK(cudaMemcpyAsync(dpe, pe, static_cast<size_t>(rows) * d * 4, cudaMemcpyHostToDevice, st));
         CUDA_OK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), st));
         const bool fast = fast_path_ok(c, d, r.h, r.dff, cfg.group_size);
-        run_block(c, bp[0], &cfg, rows, nullptr, df, nullptr, dpe, dout, nullptr, fast);
+        __half* dpe16 = nullptr;
+        if (fast) {
+            dpe16 = ws<__half>(c, "bf_pe16", static_cast<size_t>(rows) * d);
+            launch_f32_to_f16(dpe, rows * d, dpe16, st, &c->launches);
+        }
+        run_block(c, bp[0], &cfg, rows, nullptr, df, nullptr, dpe, dpe16, dout, nullptr, fast);
         CUDA_OK(cudaMemcpyAsync(out, dout, static_cast<size_t>(rows) * d * 4, cudaMemcpyDeviceToHost, st));
         CUDA_OK(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
         CUDA_OK(cudaStreamSynchronize(st));
@@ -910,7 +917,7 @@ int fwa_b200_positional_embedding(fwa_b200_ctx* c, const double* coords, int64_t
         double* dc = ws<double>(c, "pe_coords", 2 * static_cast<size_t>(n));
         float* dp = ws<float>(c, "pe_out", static_cast<size_t>(n) * d);
         CUDA_OK(cudaMemcpyAsync(dc, coords, static_cast<size_t>(n) * 16, cudaMemcpyHostToDevice, st));
-        launch_positional_embedding(dc, n, d, pe_freq(c, d), dp, st, &c->launches);
+        launch_positional_embedding(dc, n, d, pe_freq(c, d), dp, nullptr, st, &c->launches);
         check_launch();
         CUDA_OK(cudaMemcpyAsync(out, dp, static_cast<size_t>(n) * d * 4, cudaMemcpyDeviceToHost, st));
         CUDA_OK(cudaStreamSynchronize(st));

@@ -2,6 +2,7 @@
 // kernel translation units.  Not part of the C ABI.
 #pragma once
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -39,7 +40,8 @@ void launch_bin_scatter(const uint32_t* bin_of, int64_t ntot, int n_specs, uint3
                         int32_t* pre, cudaStream_t s, int64_t* launches);
 void launch_bin_sort(const uint32_t* bin_start, const uint32_t* hist, uint32_t n_bins,
                      const int32_t* pre, const double* loc, int64_t ntot, int32_t* sorted,
-                     int32_t* scratch, cudaStream_t s, int64_t* launches);
+                     int32_t* scratch, uint32_t* large /* 1 + n_bins words */, cudaStream_t s,
+                     int64_t* launches);
 
 // ------------------------------------------------------------------ schedule (backbone.hpp:236-316)
 void launch_drop_mark(const int32_t* sorted0, int64_t ntot, const int64_t* d_frame_off,
@@ -55,8 +57,10 @@ void launch_spec_compact(const int32_t* sorted, int64_t total, const uint8_t* dr
                          const uint32_t* pos, int32_t* idx, cudaStream_t s, int64_t* launches);
 
 // ------------------------------------------------------------------ fp32 SIMT path (check mode)
+// f32 PE (pe != nullptr) and/or fp16 PE rows (pe16 != nullptr, the bf16 fast path's copy)
 void launch_positional_embedding(const double* coords, int64_t n, int d, const double* d_freq,
-                                 float* pe, cudaStream_t s, int64_t* launches);
+                                 float* pe, __half* pe16, cudaStream_t s, int64_t* launches);
+void launch_f32_to_f16(const float* in, int64_t n, __half* out, cudaStream_t s, int64_t* launches);
 // h[r] = LN1(x[idx[r]]) * g + b + pe[idx[r]]  (x f32, or f64 when x64 != nullptr)
 void launch_ln_gather_f32(const float* x, const double* x64, const float* pe, const int32_t* idx,
                           int64_t rows, int d, const float* gamma, const float* beta,
@@ -95,7 +99,7 @@ struct TcBlockWeights {
 // [rows x k] weight as bf16 (rows multiple of 8, k multiple of 64).
 void swizzle_weight_bf16(const float* w, int rows, int k, uint16_t* out);
 
-void launch_ln1_qkv_tc(const float* x, const double* x64, const float* pe, const int32_t* idx,
+void launch_ln1_qkv_tc(const float* x, const double* x64, const __half* pe16, const int32_t* idx,
                        int64_t rows, const TcBlockWeights& w, __nv_bfloat16* qkv,
                        int* d_nonfinite, cudaStream_t s, int64_t* launches);
 void launch_attention_mma(const __nv_bfloat16* qkv, int64_t rows, int G, __nv_bfloat16* cat,

@@ -7,6 +7,7 @@
 //   packed QKV / out-proj  kernels.hpp:488-500, 550-560 (matmul_nt dense.hpp:50-64)
 //   group attention        kernels.hpp:512-548 (softmax_row 251-262)
 //   FFN (LN2, W1, GELU, W2, residual)  kernels.hpp:575-633
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -20,7 +21,8 @@ namespace fwa_b200 {
 // pe[i] = [sin/cos(2*pi*freq_k*x) pairs | sin/cos(2*pi*freq_k*y) pairs] in fp64,
 // rounded to f32.  freq_k comes from the host (glibc pow, as the reference).
 __global__ void k_positional_embedding(const double* __restrict__ coords, int64_t n, int d,
-                                       const double* __restrict__ freq, float* __restrict__ pe) {
+                                       const double* __restrict__ freq, float* __restrict__ pe,
+                                       __half* __restrict__ pe16) {
     const int nf = d / 4;
     const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t i = t / (2 * nf);
@@ -31,15 +33,16 @@ __global__ void k_positional_embedding(const double* __restrict__ coords, int64_
     const double phase = __dmul_rn(__dmul_rn(6.283185307179586, freq[k]), c);
     double sv, cv;
     sincos(phase, &sv, &cv);
-    float2 o = make_float2(static_cast<float>(sv), static_cast<float>(cv));
-    reinterpret_cast<float2*>(pe + i * d + axis * (d / 2))[k] = o;
+    const float2 o = make_float2(static_cast<float>(sv), static_cast<float>(cv));
+    if (pe) reinterpret_cast<float2*>(pe + i * d + axis * (d / 2))[k] = o;
+    if (pe16) reinterpret_cast<__half2*>(pe16 + i * d + axis * (d / 2))[k] = __floats2half2_rn(o.x, o.y);
 }
 
 void launch_positional_embedding(const double* coords, int64_t n, int d, const double* d_freq,
-                                 float* pe, cudaStream_t s, int64_t* launches) {
+                                 float* pe, __half* pe16, cudaStream_t s, int64_t* launches) {
     const int64_t total = n * (d / 2);
     k_positional_embedding<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
-        coords, n, d, d_freq, pe);
+        coords, n, d, d_freq, pe, pe16);
     ++*launches;
 }
 
@@ -266,6 +269,16 @@ __global__ void k_scatter_rows(const float* __restrict__ src, const int32_t* __r
     const int64_t id = ids ? ids[r] : r;
     const int64_t o = rank ? rank[id] : r;
     for (int c = threadIdx.x & 31; c < d; c += 32) dst[o * d + c] = src[id * d + c];
+}
+
+__global__ void k_f32_to_f16(const float* __restrict__ in, int64_t n, __half* __restrict__ out) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = __float2half_rn(in[i]);
+}
+
+void launch_f32_to_f16(const float* in, int64_t n, __half* out, cudaStream_t s, int64_t* launches) {
+    k_f32_to_f16<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(in, n, out);
+    ++*launches;
 }
 
 void launch_scatter_rows(const float* src, const int32_t* ids, const uint32_t* rank, int64_t n,

@@ -279,7 +279,7 @@ constexpr int kBinWarps = 8;
 __global__ void __launch_bounds__(kBinWarps * 32) k_bin_sort_small(
     const uint32_t* __restrict__ bin_start, const uint32_t* __restrict__ hist, uint32_t n_bins,
     const int32_t* __restrict__ pre, const double* __restrict__ loc, int64_t ntot,
-    int32_t* __restrict__ sorted) {
+    int32_t* __restrict__ sorted, uint32_t* __restrict__ large) {
     __shared__ double s_a[kBinWarps][kWarpBin];
     __shared__ double s_b[kBinWarps][kWarpBin];
     __shared__ int s_i[kBinWarps][kWarpBin];
@@ -287,7 +287,11 @@ __global__ void __launch_bounds__(kBinWarps * 32) k_bin_sort_small(
     const uint32_t bin = blockIdx.x * kBinWarps + wid;
     if (bin >= n_bins) return;
     const int n = static_cast<int>(hist[bin]);
-    if (n == 0 || n > kWarpBin) return;
+    if (n > kWarpBin) {  // queue for the CTA-level kernel; large[0] = count
+        if (lane == 0) large[1 + atomicAdd(large, 1u)] = bin;
+        return;
+    }
+    if (n == 0) return;
     const uint32_t start = bin_start[bin];
     const int64_t spec_base = (static_cast<int64_t>(start) / ntot) * ntot;
     if (n == 1) {
@@ -312,16 +316,18 @@ __global__ void __launch_bounds__(kBinWarps * 32) k_bin_sort_small(
 }
 
 __global__ void __launch_bounds__(512) k_bin_sort_large(
-    const uint32_t* __restrict__ bin_start, const uint32_t* __restrict__ hist, uint32_t n_bins,
-    const int32_t* __restrict__ pre, const double* __restrict__ loc, int64_t ntot,
-    int32_t* __restrict__ sorted, int32_t* __restrict__ scratch) {
+    const uint32_t* __restrict__ bin_start, const uint32_t* __restrict__ hist,
+    const uint32_t* __restrict__ large, const int32_t* __restrict__ pre,
+    const double* __restrict__ loc, int64_t ntot, int32_t* __restrict__ sorted,
+    int32_t* __restrict__ scratch) {
     extern __shared__ unsigned char smem_raw[];
     double* s_a = reinterpret_cast<double*>(smem_raw);
     double* s_b = s_a + kCtaBin;
     int* s_i = reinterpret_cast<int*>(s_b + kCtaBin);
-    for (uint32_t bin = blockIdx.x; bin < n_bins; bin += gridDim.x) {
+    const uint32_t n_large = large[0];
+    for (uint32_t li = blockIdx.x; li < n_large; li += gridDim.x) {
+        const uint32_t bin = large[1 + li];
         const int n = static_cast<int>(hist[bin]);
-        if (n <= kWarpBin) continue;
         const uint32_t start = bin_start[bin];
         const int64_t spec_base = (static_cast<int64_t>(start) / ntot) * ntot;
         const double2* L = reinterpret_cast<const double2*>(loc) + spec_base;
@@ -381,17 +387,18 @@ __global__ void __launch_bounds__(512) k_bin_sort_large(
 
 void launch_bin_sort(const uint32_t* bin_start, const uint32_t* hist, uint32_t n_bins,
                      const int32_t* pre, const double* loc, int64_t ntot, int32_t* sorted,
-                     int32_t* scratch, cudaStream_t s, int64_t* launches) {
+                     int32_t* scratch, uint32_t* large, cudaStream_t s, int64_t* launches) {
     const unsigned grid = (n_bins + kBinWarps - 1) / kBinWarps;
+    cudaMemsetAsync(large, 0, sizeof(uint32_t), s);
     k_bin_sort_small<<<grid, kBinWarps * 32, 0, s>>>(bin_start, hist, n_bins, pre, loc, ntot,
-                                                     sorted);
+                                                     sorted, large);
     static bool attr_set = false;
     const int smem = kCtaBin * (8 + 8 + 4);
     if (!attr_set) {
         cudaFuncSetAttribute(k_bin_sort_large, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr_set = true;
     }
-    k_bin_sort_large<<<kNumSMs, 512, smem, s>>>(bin_start, hist, n_bins, pre, loc, ntot, sorted,
+    k_bin_sort_large<<<kNumSMs, 512, smem, s>>>(bin_start, hist, large, pre, loc, ntot, sorted,
                                                 scratch);
     *launches += 2;
 }

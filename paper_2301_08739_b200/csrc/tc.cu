@@ -16,6 +16,7 @@
 // Persistent CTAs (one per SM, 128-row tiles), one elected thread issues the
 // MMAs, completion via tcgen05.commit -> mbarrier.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -46,145 +47,218 @@ void swizzle_weight_bf16(const float* w, int rows, int k, uint16_t* out) {
             out[sw128_offset(r, c, rows) / 2] = f32_to_bf16_rn(w[static_cast<size_t>(r) * k + c]);
 }
 
-FWA_DEVINL uint8_t* align1024(uint8_t* p) {
-    return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
-}
+// pointer arithmetic on the extern __shared__ array keeps the shared address space
+// visible to the compiler (STS/LDS instead of generic ST/LD)
+FWA_DEVINL uint8_t* align1024(uint8_t* p) { return p + ((1024u - (smem_u32(p) & 1023u)) & 1023u); }
 
 // ------------------------------------------------------------------ K_a: gather + LN1 + PE + QKV
+//
+// Warp-specialised persistent kernel, 12 warps:
+//   warps 0-7  producers: gather 16 rows each (pillar ids from the window-sort
+//              permutation), LN1 + affine + PE in fp32, bf16 -> SW128 A tile; A is
+//              double-buffered so tile t+1 is gathered while tile t is multiplied.
+//   warps 8-11 MMA issue (one elected thread) + epilogue: TMEM -> +bias -> bf16,
+//              written chunk-major (q|k|v as 12 column chunks of [rows x 32]) so
+//              each warp store is 2 KB contiguous and the attention kernel reads
+//              each group's rows as contiguous 4.4 KB runs.
+// mbarriers: full[s] (8 producer warps), empty[s] (tcgen05.commit), done (commit).
 
-constexpr int kQkvW = 384 * 128 * 2;   // 98304 B
-constexpr int kTileA = 128 * 128 * 2;  // 32768 B
-constexpr int kQkvSmem = kQkvW + kTileA + 64 + 1024;
+constexpr int kQkvW = 384 * 128 * 2;   // 98304 B weight image
+constexpr int kTileA = 128 * 128 * 2;  // 32768 B per A stage
+constexpr int kQkvThreads = 384;
+constexpr int kQkvSmem = kQkvW + 2 * kTileA + 384 * 4 /*bias*/ + 128 /*bars*/ + 1024 /*align*/;
 
 template <bool kF64>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kQkvThreads, 1)
     k_ln1_qkv_tc(const float* __restrict__ x, const double* __restrict__ x64,
-                 const float* __restrict__ pe, const int32_t* __restrict__ idx, int64_t rows,
+                 const __half* __restrict__ pe16, const int32_t* __restrict__ idx, int64_t rows,
                  TcBlockWeights w, __nv_bfloat16* __restrict__ qkv, int* __restrict__ nonfinite) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
     uint8_t* sW = smem;
-    uint8_t* sA = smem + kQkvW;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sA + kTileA);  // [0] weights, [1] mma
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
+    uint8_t* sA = smem + kQkvW;                                        // 2 stages
+    float* sBias = reinterpret_cast<float*>(sA + 2 * kTileA);          // 384
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sBias + 384);         // wbar, full[2], empty[2], done
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6);
+    uint64_t* wbar = bars;
+    uint64_t* full = bars + 1;
+    uint64_t* empty = bars + 3;
+    uint64_t* done = bars + 5;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
+        mbar_init(wbar, 1);
+        mbar_init(&full[0], 8);
+        mbar_init(&full[1], 8);
+        mbar_init(&empty[0], 1);
+        mbar_init(&empty[1], 1);
+        mbar_init(done, 1);
         fence_mbar_init();
     }
-    if (warp == 0) tmem_alloc(tmem_slot, 512);
+    for (int i = threadIdx.x; i < 384; i += blockDim.x) sBias[i] = w.b_qkv[i];
+    if (warp == 8) {
+        __syncwarp();
+        tmem_alloc(tmem_slot, 512);
+    }
     fence_before_sync();
     __syncthreads();
     fence_after_sync();
     const uint32_t tmem = *tmem_slot;
-    if (threadIdx.x == 0) {
-        mbar_arrive_expect_tx(&bars[0], kQkvW);
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-            bulk_g2s(sW + c * 32768, reinterpret_cast<const uint8_t*>(w.w_qkv) + c * 32768, 32768, &bars[0]);
-    }
-    constexpr uint32_t idesc = idesc_bf16_f32(128, 128);
-    uint32_t phase = 0;
-    bool w_ready = false;
-    bool bad = false;
     const int64_t ntiles = (rows + 127) / 128;
-    const float4 g4 = reinterpret_cast<const float4*>(w.ln1_g)[lane];
-    const float4 b4 = reinterpret_cast<const float4*>(w.ln1_b)[lane];
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        // ---- gather + LN1 + PE -> bf16 SW128 A tile (one warp per row, 4 channels per lane)
-        for (int rr = 0; rr < 16; ++rr) {
-            const int r = warp * 16 + rr;
-            const int64_t grow = tile * 128 + r;
-            uint2 packed = make_uint2(0u, 0u);
-            if (grow < rows) {
-                const int64_t id = idx ? idx[grow] : grow;
-                float4 xv;
-                if (kF64) {
-                    const double2* p = reinterpret_cast<const double2*>(x64 + id * 128 + lane * 4);
-                    const double2 a = p[0], b = p[1];
-                    xv = make_float4(static_cast<float>(a.x), static_cast<float>(a.y),
-                                     static_cast<float>(b.x), static_cast<float>(b.y));
-                } else {
-                    xv = reinterpret_cast<const float4*>(x + id * 128)[lane];
-                }
-                const float4 pv = reinterpret_cast<const float4*>(pe + id * 128)[lane];
-                bad |= !(isfinite(xv.x) && isfinite(xv.y) && isfinite(xv.z) && isfinite(xv.w) &&
-                         isfinite(pv.x) && isfinite(pv.y) && isfinite(pv.z) && isfinite(pv.w));
-                const float mean = warp_sum(xv.x + xv.y + xv.z + xv.w) * (1.0f / 128.0f);
-                const float dx = xv.x - mean, dy = xv.y - mean, dz = xv.z - mean, dw = xv.w - mean;
-                const float var = warp_sum(dx * dx + dy * dy + dz * dz + dw * dw) * (1.0f / 128.0f);
-                const float inv = 1.0f / sqrtf(var + 1e-5f);
-                const float h0 = g4.x * (dx * inv) + b4.x + pv.x;
-                const float h1 = g4.y * (dy * inv) + b4.y + pv.y;
-                const float h2 = g4.z * (dz * inv) + b4.z + pv.z;
-                const float h3 = g4.w * (dw * inv) + b4.w + pv.w;
-                packed = make_uint2(pack_bf16x2(h0, h1), pack_bf16x2(h2, h3));
-            }
-            *reinterpret_cast<uint2*>(sA + sw128_offset(r, lane * 4, 128)) = packed;
-        }
-        fence_proxy_async_smem();
-        fence_before_sync();
-        __syncthreads();
-        // ---- packed QKV GEMM: [128 x 128] x [384 x 128]^T -> TMEM cols [0, 384)
+
+    if (warp < 8) {
+        // ------------------------------------------------ producers
         if (threadIdx.x == 0) {
-            if (!w_ready) {
-                mbar_wait(&bars[0], 0);
-                w_ready = true;
-            }
-            fence_after_sync();
-            const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sW);
+            mbar_arrive_expect_tx(wbar, kQkvW);
 #pragma unroll
-            for (int ks = 0; ks < 8; ++ks) {
-                const uint64_t ad = sdesc_sw128(a0 + (ks >> 2) * 16384 + (ks & 3) * 32);
+            for (int c = 0; c < 3; ++c)
+                bulk_g2s(sW + c * 32768, reinterpret_cast<const uint8_t*>(w.w_qkv) + c * 32768, 32768, wbar);
+        }
+        // 4 lanes per row (32 channels each, 128 B contiguous per lane), 8 rows per pass
+        const int sub = lane & 3, rl = lane >> 2;
+        float gam[32], bet[32];
 #pragma unroll
-                for (int n = 0; n < 3; ++n) {
-                    const uint64_t bd = sdesc_sw128(b0 + (ks >> 2) * (384 * 128) + n * (128 * 128) + (ks & 3) * 32);
-                    mma_bf16(tmem + n * 128, ad, bd, idesc, ks > 0 ? 1u : 0u);
+        for (int j = 0; j < 32; j += 4) {
+            const float4 g = __ldg(reinterpret_cast<const float4*>(w.ln1_g + sub * 32 + j));
+            const float4 bb = __ldg(reinterpret_cast<const float4*>(w.ln1_b + sub * 32 + j));
+            gam[j] = g.x; gam[j + 1] = g.y; gam[j + 2] = g.z; gam[j + 3] = g.w;
+            bet[j] = bb.x; bet[j + 1] = bb.y; bet[j + 2] = bb.z; bet[j + 3] = bb.w;
+        }
+        bool bad = false;
+        int it = 0;
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+            const int s = it & 1;
+            if (it >= 2) mbar_wait(&empty[s], ((it >> 1) - 1) & 1);
+            uint8_t* A = sA + s * kTileA;
+#pragma unroll 1
+            for (int pass = 0; pass < 2; ++pass) {
+                const int r = warp * 16 + pass * 8 + rl;
+                const int64_t g = tile * 128 + r;
+                const bool valid = g < rows;
+                const int64_t id = valid ? (idx ? idx[g] : g) : 0;
+                float v[32];
+                uint4 ph[4];
+                if (valid) {
+                    if (kF64) {
+                        const double2* p = reinterpret_cast<const double2*>(x64 + id * 128 + sub * 32);
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const double2 d2 = __ldg(p + j);
+                            v[2 * j] = static_cast<float>(d2.x);
+                            v[2 * j + 1] = static_cast<float>(d2.y);
+                        }
+                    } else {
+                        const float4* p = reinterpret_cast<const float4*>(x + id * 128 + sub * 32);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const float4 f4 = __ldg(p + j);
+                            v[4 * j] = f4.x; v[4 * j + 1] = f4.y; v[4 * j + 2] = f4.z; v[4 * j + 3] = f4.w;
+                        }
+                    }
+                    const uint4* pp = reinterpret_cast<const uint4*>(pe16 + id * 128 + sub * 32);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) ph[j] = __ldg(pp + j);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = 0.f;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) ph[j] = make_uint4(0u, 0u, 0u, 0u);
+                }
+                float sm = 0.f;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) sm += v[j];
+                sm += __shfl_xor_sync(0xffffffffu, sm, 1);
+                sm += __shfl_xor_sync(0xffffffffu, sm, 2);
+                const float mean = sm * (1.0f / 128.0f);
+                float sq = 0.f;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    bad |= !isfinite(v[j]);
+                    sq += (v[j] - mean) * (v[j] - mean);
+                }
+                sq += __shfl_xor_sync(0xffffffffu, sq, 1);
+                sq += __shfl_xor_sync(0xffffffffu, sq, 2);
+                const float inv = 1.0f / sqrtf(sq * (1.0f / 128.0f) + 1e-5f);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {  // 8 channels = one 16 B chunk of the SW128 image
+                    const uint32_t hw[4] = {ph[c].x, ph[c].y, ph[c].z, ph[c].w};
+                    uint32_t o[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float2 pf = __half22float2(*reinterpret_cast<const __half2*>(&hw[e]));
+                        bad |= !(isfinite(pf.x) && isfinite(pf.y));
+                        const int j = c * 8 + 2 * e;
+                        o[e] = pack_bf16x2(gam[j] * ((v[j] - mean) * inv) + bet[j] + pf.x,
+                                           gam[j + 1] * ((v[j + 1] - mean) * inv) + bet[j + 1] + pf.y);
+                    }
+                    if (!valid) o[0] = o[1] = o[2] = o[3] = 0u;
+                    *reinterpret_cast<uint4*>(A + sw128_offset(r, sub * 32 + c * 8, 128)) =
+                        make_uint4(o[0], o[1], o[2], o[3]);
                 }
             }
-            mma_commit(&bars[1]);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[s]);
         }
-        mbar_wait(&bars[1], phase);
-        phase ^= 1;
-        fence_after_sync();
-        // ---- epilogue: TMEM -> +bias -> bf16 rows of q|k|v
-        {
-            const int q = warp & 3, half = warp >> 2;
-            const int row = q * 32 + lane;
-            const int64_t grow = tile * 128 + row;
+        if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(nonfinite, 1);
+        if (threadIdx.x == 0 && ntiles <= blockIdx.x) mbar_wait(wbar, 0);  // no tile: drain the TMA
+    } else {
+        // ------------------------------------------------ MMA issue + epilogue (warps 8..11)
+        const int q = warp - 8;
+        const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+        constexpr uint32_t idesc = idesc_bf16_f32(128, 128);
+        int it = 0;
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+            const int s = it & 1;
+            if (warp == 8 && lane == 0) {
+                if (it == 0) mbar_wait(wbar, 0);
+                mbar_wait(&full[s], (it >> 1) & 1);
+                fence_after_sync();
+                const uint32_t a0 = smem_u32(sA + s * kTileA), b0 = smem_u32(sW);
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks) {
+                    const uint64_t ad = sdesc_sw128(a0 + (ks >> 2) * 16384 + (ks & 3) * 32);
+#pragma unroll
+                    for (int n = 0; n < 3; ++n) {
+                        const uint64_t bd = sdesc_sw128(b0 + (ks >> 2) * (384 * 128) + n * (128 * 128) + (ks & 3) * 32);
+                        mma_bf16(tmem + n * 128, ad, bd, idesc, ks > 0 ? 1u : 0u);
+                    }
+                }
+                mma_commit(&empty[s]);
+                mma_commit(done);
+            }
+            __syncwarp();
+            mbar_wait(done, it & 1);
+            fence_after_sync();
+            const int64_t grow = tile * 128 + q * 32 + lane;
 #pragma unroll 1
-            for (int ch = 0; ch < 6; ++ch) {
-                const int col0 = half * 192 + ch * 32;
+            for (int ch = 0; ch < 12; ++ch) {
                 uint32_t v[32];
-                tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) + col0, v);
+                tmem_ld32(tmem + lane_off + ch * 32, v);
                 tmem_ld_wait();
                 if (grow < rows) {
                     uint32_t o[16];
 #pragma unroll
                     for (int j = 0; j < 16; ++j)
-                        o[j] = pack_bf16x2(__uint_as_float(v[2 * j]) + w.b_qkv[col0 + 2 * j],
-                                           __uint_as_float(v[2 * j + 1]) + w.b_qkv[col0 + 2 * j + 1]);
-                    uint4* dst = reinterpret_cast<uint4*>(qkv + grow * 384 + col0);
+                        o[j] = pack_bf16x2(__uint_as_float(v[2 * j]) + sBias[ch * 32 + 2 * j],
+                                           __uint_as_float(v[2 * j + 1]) + sBias[ch * 32 + 2 * j + 1]);
+                    uint4* dst = reinterpret_cast<uint4*>(qkv + (static_cast<int64_t>(ch) * rows + grow) * 32);
 #pragma unroll
                     for (int j = 0; j < 4; ++j) dst[j] = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
                 }
             }
+            fence_before_sync();
+            asm volatile("bar.sync 1, 128;" ::: "memory");  // TMEM drained before the next MMA
+            fence_after_sync();
         }
-        fence_before_sync();
-        __syncthreads();
     }
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(nonfinite, 1);
-    // drain the weight barrier if this CTA had no tile (bulk copy must land before exit)
-    if (threadIdx.x == 0 && !w_ready) mbar_wait(&bars[0], 0);
     fence_before_sync();
     __syncthreads();
     fence_after_sync();
-    if (warp == 0) tmem_dealloc(tmem, 512);
+    if (warp == 8) tmem_dealloc(tmem, 512);
 }
 
-void launch_ln1_qkv_tc(const float* x, const double* x64, const float* pe, const int32_t* idx,
+void launch_ln1_qkv_tc(const float* x, const double* x64, const __half* pe, const int32_t* idx,
                        int64_t rows, const TcBlockWeights& w, __nv_bfloat16* qkv, int* d_nonfinite,
                        cudaStream_t s, int64_t* launches) {
     static bool init = false;
@@ -196,23 +270,76 @@ void launch_ln1_qkv_tc(const float* x, const double* x64, const float* pe, const
     const int64_t ntiles = (rows + 127) / 128;
     const unsigned grid = static_cast<unsigned>(ntiles < kNumSMs ? ntiles : kNumSMs);
     if (x64)
-        k_ln1_qkv_tc<true><<<grid, 256, kQkvSmem, s>>>(x, x64, pe, idx, rows, w, qkv, d_nonfinite);
+        k_ln1_qkv_tc<true><<<grid, kQkvThreads, kQkvSmem, s>>>(x, x64, pe, idx, rows, w, qkv, d_nonfinite);
     else
-        k_ln1_qkv_tc<false><<<grid, 256, kQkvSmem, s>>>(x, x64, pe, idx, rows, w, qkv, d_nonfinite);
+        k_ln1_qkv_tc<false><<<grid, kQkvThreads, kQkvSmem, s>>>(x, x64, pe, idx, rows, w, qkv, d_nonfinite);
     ++*launches;
 }
 
 // ------------------------------------------------------------------ K_c: out-proj + LN2 + FFN + scatter
+//
+// Per 128-row tile (persistent, 1 CTA/SM, 16 warps: warp w owns TMEM lanes
+// 32*(w%4).. (= tile rows) and the column quarter w/4; thread 0 issues MMAs):
+//   1. the attention output tile arrives by ONE TMA bulk copy (it is written as a
+//      SW128 image by the attention kernel) -> R0;  P = A Wout^T -> TMEM[0,128)
+//   2. residual x[ridx[r]] (fp32, this thread's 32 channels = one 128 B line) is
+//      loaded into registers while MMA1 runs; x1 = (x + P) + b_out stays in registers
+//   3. LN2: the 4 column quarters of a row exchange partial sums through TMEM
+//      columns [384,392) (no shared memory left) -> bf16 SW128 image R1
+//   4. U_a = LN2 W1[0:128]^T, U_b = LN2 W1[128:256]^T issued back to back;
+//      GELU(U_a) -> act_a (R0) runs while U_b is computed, then O = act_a W2_a^T
+//      runs while GELU(U_b) -> act_b (R1), then O += act_b W2_b^T  (O reuses P's columns)
+//   5. out = x1 + (O + b2) -> swizzled f32 rows in R -> coalesced 512 B row stores
+//      to x_out[sidx[r]] (the scatter, backbone.hpp:278-283); R0 then receives the
+//      next tile's A by TMA.
 
 constexpr int kWout = 128 * 128 * 2;  // 32768
 constexpr int kW1 = 256 * 128 * 2;    // 65536
 constexpr int kW2 = 128 * 256 * 2;    // 65536
-constexpr int kRegion = 65536;        // A tile | LN2 tile, later the 128 x 256 GELU tile
-constexpr int kFfnSmem = kWout + kW1 + kW2 + kRegion + 1024 /*red*/ + 64 /*bars*/ + 1024 /*align*/;
+constexpr int kRegion = 65536;        // R0 | R1
+constexpr int kFfnThreads = 512;
+constexpr int kFfnSmem = kWout + kW1 + kW2 + kRegion + 64 /*bars*/ + 1024 /*align*/;
+
+// f32 row staging in R: row r (512 B) chunk c (16 B) at r*512 + ((c ^ (r & 7)) * 16)
+FWA_DEVINL uint32_t stage_off(int r, int c) { return static_cast<uint32_t>(r * 512 + ((c ^ (r & 7)) << 4)); }
+
+// exact-erf GELU of the reference (dense.hpp:67-72) with erf from Abramowitz-Stegun
+// 7.1.26 (|err| <= 1.5e-7), far below the bf16 rounding of the activation that follows
+FWA_DEVINL float gelu_fast(float x) {
+    const float z = x * 0.70710678118654752f;
+    const float az = fabsf(z);
+    const float t = __frcp_rn(fmaf(0.3275911f, az, 1.0f));
+    const float poly =
+        t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, 1.061405429f, -1.453152027f), 1.421413741f), -0.284496736f),
+                 0.254829592f);
+    const float e = exp2f(-az * az * 1.4426950408889634f);
+    const float erf_abs = fmaf(-poly, e, 1.0f);
+    const float erf_z = copysignf(erf_abs, z);
+    return 0.5f * x * (1.0f + erf_z);
+}
+
+FWA_DEVINL void tmem_st1(uint32_t taddr, float v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(__float_as_uint(v))
+                 : "memory");
+}
+FWA_DEVINL void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+FWA_DEVINL float4 tmem_ld4(uint32_t taddr) {
+    uint32_t a, b, c, d;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    return make_float4(__uint_as_float(a), __uint_as_float(b), __uint_as_float(c), __uint_as_float(d));
+}
+FWA_DEVINL void cta_sync_tc() {
+    fence_before_sync();
+    __syncthreads();
+    fence_after_sync();
+}
 
 template <bool kF64>
-__global__ void __launch_bounds__(256, 1)
-    k_outproj_ffn_tc(const __nv_bfloat16* __restrict__ cat, const float* __restrict__ x_in,
+__global__ void __launch_bounds__(kFfnThreads, 1)
+    k_outproj_ffn_tc(const uint8_t* __restrict__ cat_img, const float* __restrict__ x_in,
                      const double* __restrict__ x_in64, const int32_t* __restrict__ ridx,
                      int64_t rows, TcBlockWeights w, float* __restrict__ x_out,
                      const int32_t* __restrict__ sidx) {
@@ -221,25 +348,26 @@ __global__ void __launch_bounds__(256, 1)
     uint8_t* sWo = smem;
     uint8_t* sW1 = sWo + kWout;
     uint8_t* sW2 = sW1 + kW1;
-    uint8_t* sR = sW2 + kW2;        // R0 = sR (A tile), R1 = sR + 32768 (LN2 tile)
-    float* red = reinterpret_cast<float*>(sR + kRegion);  // [128][2]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(red + 256);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
+    uint8_t* sR = sW2 + kW2;
+    uint8_t* sR1 = sR + 32768;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sR + kRegion);  // w, a, p, ua, ub, o
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int q = warp & 3, half = warp >> 2;
+    const int q = warp & 3, cq = warp >> 2;
     const int row = q * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
 
     if (threadIdx.x == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
+        for (int i = 0; i < 6; ++i) mbar_init(&bars[i], 1);
         fence_mbar_init();
     }
-    if (warp == 0) tmem_alloc(tmem_slot, 512);
-    fence_before_sync();
-    __syncthreads();
-    fence_after_sync();
+    if (warp == 0) {
+        __syncwarp();
+        tmem_alloc(tmem_slot, 512);
+    }
+    cta_sync_tc();
     const uint32_t tmem = *tmem_slot;
+    const int64_t ntiles = (rows + 127) / 128;
     if (threadIdx.x == 0) {
         mbar_arrive_expect_tx(&bars[0], kWout + kW1 + kW2);
         bulk_g2s(sWo, w.w_out, kWout, &bars[0]);
@@ -247,188 +375,185 @@ __global__ void __launch_bounds__(256, 1)
         bulk_g2s(sW1 + 32768, reinterpret_cast<const uint8_t*>(w.w1) + 32768, 32768, &bars[0]);
         bulk_g2s(sW2, w.w2, 32768, &bars[0]);
         bulk_g2s(sW2 + 32768, reinterpret_cast<const uint8_t*>(w.w2) + 32768, 32768, &bars[0]);
+        if (blockIdx.x < ntiles) {
+            mbar_arrive_expect_tx(&bars[1], 32768);
+            bulk_g2s(sR, cat_img + static_cast<int64_t>(blockIdx.x) * 32768, 32768, &bars[1]);
+        }
     }
     constexpr uint32_t id128 = idesc_bf16_f32(128, 128);
-    constexpr uint32_t id256 = idesc_bf16_f32(128, 256);
-    const uint32_t TP = tmem, TU = tmem + 128, TO = tmem + 384;
-    uint32_t phase = 0;
-    bool w_ready = false;
-    const int64_t ntiles = (rows + 127) / 128;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint32_t TP = tmem, TUa = tmem + 128, TUb = tmem + 256, TS = tmem + 384;
+    const int c0 = cq * 32;  // this thread's 32 channels / hidden units
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const uint32_t ph = it & 1;
         const int64_t grow = tile * 128 + row;
         const bool valid = grow < rows;
-        // ---- 1. attention rows (bf16, 256 B each) -> SW128 A tile in R0
-        for (int t = threadIdx.x; t < 128 * 16; t += 256) {
-            const int r = t >> 4, c16 = t & 15;
-            const int64_t g = tile * 128 + r;
-            uint4 v = make_uint4(0u, 0u, 0u, 0u);
-            if (g < rows) v = reinterpret_cast<const uint4*>(cat + g * 128)[c16];
-            *reinterpret_cast<uint4*>(sR + sw128_offset(r, c16 * 8, 128)) = v;
-        }
-        fence_proxy_async_smem();
-        fence_before_sync();
-        __syncthreads();
-        // ---- 2. P = A Wout^T
+        // ---- 1. P = A Wout^T
         if (threadIdx.x == 0) {
-            if (!w_ready) {
-                mbar_wait(&bars[0], 0);
-                w_ready = true;
-            }
+            if (it == 0) mbar_wait(&bars[0], 0);
+            mbar_wait(&bars[1], ph);
             fence_after_sync();
             const uint32_t a0 = smem_u32(sR), b0 = smem_u32(sWo);
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks)
                 mma_bf16(TP, sdesc_sw128(a0 + (ks >> 2) * 16384 + (ks & 3) * 32),
                          sdesc_sw128(b0 + (ks >> 2) * 16384 + (ks & 3) * 32), id128, ks > 0);
-            mma_commit(&bars[1]);
+            mma_commit(&bars[2]);
         }
-        mbar_wait(&bars[1], phase);
-        phase ^= 1;
-        fence_after_sync();
-        // ---- 3. x1 = (x + P) + b_out in registers; LN2 -> bf16 R1 (K-block `half`)
-        float x1[64];
+        // ---- 2. residual (one 128 B line per thread) while MMA1 runs
+        float x1[32];
         {
             const int64_t src = valid ? (ridx ? ridx[grow] : grow) : 0;
+            if (valid) {
+                if (kF64) {
+                    const double2* p = reinterpret_cast<const double2*>(x_in64 + src * 128 + c0);
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                uint32_t v[32];
-                tmem_ld32(TP + lane_off + half * 64 + c * 32, v);
-                tmem_ld_wait();
-#pragma unroll
-                for (int j = 0; j < 32; j += 4) {
-                    const int col = half * 64 + c * 32 + j;
-                    float4 xr = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (valid) {
-                        if (kF64) {
-                            const double2* p = reinterpret_cast<const double2*>(x_in64 + src * 128 + col);
-                            const double2 a = p[0], b = p[1];
-                            xr = make_float4(static_cast<float>(a.x), static_cast<float>(a.y),
-                                             static_cast<float>(b.x), static_cast<float>(b.y));
-                        } else {
-                            xr = *reinterpret_cast<const float4*>(x_in + src * 128 + col);
-                        }
+                    for (int j = 0; j < 16; ++j) {
+                        const double2 d2 = __ldg(p + j);
+                        x1[2 * j] = static_cast<float>(d2.x);
+                        x1[2 * j + 1] = static_cast<float>(d2.y);
                     }
-                    const float4 bo = *reinterpret_cast<const float4*>(w.b_out + col);
-                    x1[c * 32 + j + 0] = (xr.x + __uint_as_float(v[j + 0])) + bo.x;
-                    x1[c * 32 + j + 1] = (xr.y + __uint_as_float(v[j + 1])) + bo.y;
-                    x1[c * 32 + j + 2] = (xr.z + __uint_as_float(v[j + 2])) + bo.z;
-                    x1[c * 32 + j + 3] = (xr.w + __uint_as_float(v[j + 3])) + bo.w;
+                } else {
+                    const float4* p = reinterpret_cast<const float4*>(x_in + src * 128 + c0);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const float4 f4 = __ldg(p + j);
+                        x1[4 * j] = f4.x; x1[4 * j + 1] = f4.y; x1[4 * j + 2] = f4.z; x1[4 * j + 3] = f4.w;
+                    }
                 }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) x1[j] = 0.f;
             }
         }
+        mbar_wait(&bars[2], ph);
+        fence_after_sync();
+        {
+            uint32_t v[32];
+            tmem_ld32(TP + lane_off + c0, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+                const float4 bo = __ldg(reinterpret_cast<const float4*>(w.b_out + c0 + j));
+                x1[j + 0] = (x1[j + 0] + __uint_as_float(v[j + 0])) + bo.x;
+                x1[j + 1] = (x1[j + 1] + __uint_as_float(v[j + 1])) + bo.y;
+                x1[j + 2] = (x1[j + 2] + __uint_as_float(v[j + 2])) + bo.z;
+                x1[j + 3] = (x1[j + 3] + __uint_as_float(v[j + 3])) + bo.w;
+            }
+        }
+        // ---- 3. LN2 (row statistics over the 4 column quarters via TMEM)
         float s = 0.f;
 #pragma unroll
-        for (int j = 0; j < 64; ++j) s += x1[j];
-        red[row * 2 + half] = s;
-        __syncthreads();
-        const float mean = (red[row * 2] + red[row * 2 + 1]) * (1.0f / 128.0f);
-        __syncthreads();
+        for (int j = 0; j < 32; ++j) s += x1[j];
+        tmem_st1(TS + lane_off + cq, s);
+        tmem_st_wait();
+        cta_sync_tc();
+        float4 ps = tmem_ld4(TS + lane_off);
+        const float mean = ((ps.x + ps.y) + (ps.z + ps.w)) * (1.0f / 128.0f);
         float v2 = 0.f;
 #pragma unroll
-        for (int j = 0; j < 64; ++j) v2 += (x1[j] - mean) * (x1[j] - mean);
-        red[row * 2 + half] = v2;
-        __syncthreads();
-        const float inv = 1.0f / sqrtf((red[row * 2] + red[row * 2 + 1]) * (1.0f / 128.0f) + 1e-5f);
-        {
-            uint8_t* r1 = sR + 32768;
+        for (int j = 0; j < 32; ++j) v2 += (x1[j] - mean) * (x1[j] - mean);
+        tmem_st1(TS + lane_off + 4 + cq, v2);
+        tmem_st_wait();
+        cta_sync_tc();
+        ps = tmem_ld4(TS + lane_off + 4);
+        const float inv = 1.0f / sqrtf(((ps.x + ps.y) + (ps.z + ps.w)) * (1.0f / 128.0f) + 1e-5f);
 #pragma unroll
-            for (int ch = 0; ch < 8; ++ch) {
-                uint32_t o[4];
+        for (int ch = 0; ch < 4; ++ch) {
+            uint32_t o[4];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int j = ch * 8 + 2 * e, col = half * 64 + j;
-                    const float l0 = w.ln2_g[col] * ((x1[j] - mean) * inv) + w.ln2_b[col];
-                    const float l1 = w.ln2_g[col + 1] * ((x1[j + 1] - mean) * inv) + w.ln2_b[col + 1];
-                    o[e] = pack_bf16x2(l0, l1);
-                }
-                // K-block 0 of R1 holds cols 0..63; the LN2 tile is its own 2-K-block image
-                *reinterpret_cast<uint4*>(r1 + sw128_offset(row, half * 64 + ch * 8, 128)) =
-                    make_uint4(o[0], o[1], o[2], o[3]);
+            for (int e = 0; e < 4; ++e) {
+                const int j = ch * 8 + 2 * e, col = c0 + j;
+                o[e] = pack_bf16x2(__ldg(w.ln2_g + col) * ((x1[j] - mean) * inv) + __ldg(w.ln2_b + col),
+                                   __ldg(w.ln2_g + col + 1) * ((x1[j + 1] - mean) * inv) + __ldg(w.ln2_b + col + 1));
             }
+            *reinterpret_cast<uint4*>(sR1 + sw128_offset(row, c0 + ch * 8, 128)) = make_uint4(o[0], o[1], o[2], o[3]);
         }
         fence_proxy_async_smem();
-        fence_before_sync();
-        __syncthreads();
-        // ---- 4. U = LN2 W1^T  (N = 256)
+        cta_sync_tc();
+        // ---- 4. U_a, U_b = LN2 W1^T halves (N = 128 each)
         if (threadIdx.x == 0) {
-            fence_after_sync();
-            const uint32_t a0 = smem_u32(sR + 32768), b0 = smem_u32(sW1);
+            const uint32_t a0 = smem_u32(sR1), b0 = smem_u32(sW1);
 #pragma unroll
-            for (int ks = 0; ks < 8; ++ks)
-                mma_bf16(TU, sdesc_sw128(a0 + (ks >> 2) * 16384 + (ks & 3) * 32),
-                         sdesc_sw128(b0 + (ks >> 2) * 32768 + (ks & 3) * 32), id256, ks > 0);
-            mma_commit(&bars[1]);
+            for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks)
+                    mma_bf16(hh ? TUb : TUa, sdesc_sw128(a0 + (ks >> 2) * 16384 + (ks & 3) * 32),
+                             sdesc_sw128(b0 + (ks >> 2) * 32768 + hh * 16384 + (ks & 3) * 32), id128, ks > 0);
+                mma_commit(&bars[3 + hh]);
+            }
         }
-        mbar_wait(&bars[1], phase);
-        phase ^= 1;
-        fence_after_sync();
-        // ---- 5. act = gelu(U + b1) -> bf16 128 x 256 SW128 image over R (4 K-blocks)
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-            const int h0 = half * 128 + c * 32;
+        for (int hh = 0; hh < 2; ++hh) {
+            mbar_wait(&bars[3 + hh], ph);
+            fence_after_sync();
+            uint8_t* act = hh ? sR1 : sR;  // [128 x 128] SW128 image (K-blocks 2hh, 2hh+1 of act)
             uint32_t v[32];
-            tmem_ld32(TU + lane_off + h0, v);
+            tmem_ld32((hh ? TUb : TUa) + lane_off + c0, v);
             tmem_ld_wait();
+            const float* b1 = w.b1 + hh * 128 + c0;
 #pragma unroll
             for (int ch = 0; ch < 4; ++ch) {
                 uint32_t o[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int j = ch * 8 + 2 * e;
-                    const float a0 = gelu_erf(__uint_as_float(v[j]) + w.b1[h0 + j]);
-                    const float a1 = gelu_erf(__uint_as_float(v[j + 1]) + w.b1[h0 + j + 1]);
-                    o[e] = pack_bf16x2(a0, a1);
+                    o[e] = pack_bf16x2(gelu_fast(__uint_as_float(v[j]) + __ldg(b1 + j)),
+                                       gelu_fast(__uint_as_float(v[j + 1]) + __ldg(b1 + j + 1)));
                 }
-                *reinterpret_cast<uint4*>(sR + sw128_offset(row, h0 + ch * 8, 128)) =
-                    make_uint4(o[0], o[1], o[2], o[3]);
+                *reinterpret_cast<uint4*>(act + sw128_offset(row, c0 + ch * 8, 128)) = make_uint4(o[0], o[1], o[2], o[3]);
+            }
+            fence_proxy_async_smem();
+            cta_sync_tc();
+            // ---- O (+)= act_hh W2[:, 128hh : 128hh+128]^T  (O reuses P's columns)
+            if (threadIdx.x == 0) {
+                const uint32_t a0 = smem_u32(act), b0 = smem_u32(sW2) + hh * 2 * 16384;
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks)
+                    mma_bf16(TP, sdesc_sw128(a0 + (ks >> 2) * 16384 + (ks & 3) * 32),
+                             sdesc_sw128(b0 + (ks >> 2) * 16384 + (ks & 3) * 32), id128, (hh | ks) > 0);
+                if (hh) mma_commit(&bars[5]);
             }
         }
-        fence_proxy_async_smem();
-        fence_before_sync();
-        __syncthreads();
-        // ---- 6. O = act W2^T  (K = 256)
-        if (threadIdx.x == 0) {
-            fence_after_sync();
-            const uint32_t a0 = smem_u32(sR), b0 = smem_u32(sW2);
-#pragma unroll
-            for (int ks = 0; ks < 16; ++ks)
-                mma_bf16(TO, sdesc_sw128(a0 + (ks >> 2) * 16384 + (ks & 3) * 32),
-                         sdesc_sw128(b0 + (ks >> 2) * 16384 + (ks & 3) * 32), id128, ks > 0);
-            mma_commit(&bars[1]);
-        }
-        mbar_wait(&bars[1], phase);
-        phase ^= 1;
+        // ---- 5. out = x1 + (O + b2) -> staged rows -> coalesced scatter
+        mbar_wait(&bars[5], ph);
         fence_after_sync();
-        // ---- 7. out = x1 + (O + b2) -> pillar-id row
         {
-            const int64_t dst = valid ? (sidx ? sidx[grow] : grow) : 0;
+            uint32_t v[32];
+            tmem_ld32(TP + lane_off + c0, v);
+            tmem_ld_wait();
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                uint32_t v[32];
-                tmem_ld32(TO + lane_off + half * 64 + c * 32, v);
-                tmem_ld_wait();
-                if (valid) {
-#pragma unroll
-                    for (int j = 0; j < 32; j += 4) {
-                        const int col = half * 64 + c * 32 + j;
-                        const float4 b2 = *reinterpret_cast<const float4*>(w.b2 + col);
-                        float4 o;
-                        o.x = x1[c * 32 + j + 0] + (__uint_as_float(v[j + 0]) + b2.x);
-                        o.y = x1[c * 32 + j + 1] + (__uint_as_float(v[j + 1]) + b2.y);
-                        o.z = x1[c * 32 + j + 2] + (__uint_as_float(v[j + 2]) + b2.z);
-                        o.w = x1[c * 32 + j + 3] + (__uint_as_float(v[j + 3]) + b2.w);
-                        *reinterpret_cast<float4*>(x_out + dst * 128 + col) = o;
-                    }
-                }
+            for (int j = 0; j < 32; j += 4) {
+                const float4 b2 = __ldg(reinterpret_cast<const float4*>(w.b2 + c0 + j));
+                float4 o;
+                o.x = x1[j + 0] + (__uint_as_float(v[j + 0]) + b2.x);
+                o.y = x1[j + 1] + (__uint_as_float(v[j + 1]) + b2.y);
+                o.z = x1[j + 2] + (__uint_as_float(v[j + 2]) + b2.z);
+                o.w = x1[j + 3] + (__uint_as_float(v[j + 3]) + b2.w);
+                *reinterpret_cast<float4*>(sR + stage_off(row, (c0 + j) >> 2)) = o;
             }
         }
-        fence_before_sync();
-        __syncthreads();
+        cta_sync_tc();
+        {
+            const int rbase = warp * 8;
+            int myid = 0;
+            const int64_t gl = tile * 128 + rbase + (lane & 7);
+            if (lane < 8 && gl < rows) myid = sidx ? sidx[gl] : static_cast<int>(gl);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int64_t id = __shfl_sync(0xffffffffu, myid, i);
+                const float4 o = *reinterpret_cast<const float4*>(sR + stage_off(rbase + i, lane));
+                if (tile * 128 + rbase + i < rows) reinterpret_cast<float4*>(x_out + id * 128)[lane] = o;
+            }
+        }
+        __syncthreads();  // R free: prefetch the next tile's attention rows
+        if (threadIdx.x == 0 && tile + gridDim.x < ntiles) {
+            mbar_arrive_expect_tx(&bars[1], 32768);
+            bulk_g2s(sR, cat_img + (tile + gridDim.x) * 32768, 32768, &bars[1]);
+        }
     }
-    if (threadIdx.x == 0 && !w_ready) mbar_wait(&bars[0], 0);
-    fence_before_sync();
-    __syncthreads();
-    fence_after_sync();
+    if (threadIdx.x == 0 && blockIdx.x >= ntiles) mbar_wait(&bars[0], 0);
+    cta_sync_tc();
     if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
@@ -443,10 +568,11 @@ void launch_outproj_ffn_tc(const __nv_bfloat16* cat, const float* x_in, const do
     }
     const int64_t ntiles = (rows + 127) / 128;
     const unsigned grid = static_cast<unsigned>(ntiles < kNumSMs ? ntiles : kNumSMs);
+    const uint8_t* img = reinterpret_cast<const uint8_t*>(cat);
     if (x_in64)
-        k_outproj_ffn_tc<true><<<grid, 256, kFfnSmem, s>>>(cat, x_in, x_in64, ridx, rows, w, x_out, sidx);
+        k_outproj_ffn_tc<true><<<grid, kFfnThreads, kFfnSmem, s>>>(img, x_in, x_in64, ridx, rows, w, x_out, sidx);
     else
-        k_outproj_ffn_tc<false><<<grid, 256, kFfnSmem, s>>>(cat, x_in, x_in64, ridx, rows, w, x_out, sidx);
+        k_outproj_ffn_tc<false><<<grid, kFfnThreads, kFfnSmem, s>>>(img, x_in, x_in64, ridx, rows, w, x_out, sidx);
     ++*launches;
 }
 
