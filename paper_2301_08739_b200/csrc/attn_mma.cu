@@ -28,6 +28,13 @@ FWA_DEVINL uint32_t tc_sw128_offset(int row, int col) {
                                  (col & 7) * 2);
 }
 
+// 2^x on the SFU (rel err 2^-22), -inf -> +0
+FWA_DEVINL float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 FWA_DEVINL void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                  : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
@@ -53,6 +60,8 @@ __global__ void __launch_bounds__(256) k_attention_mma(const __nv_bfloat16* __re
                                                        int64_t rows, int G,
                                                        uint8_t* __restrict__ cat) {
     extern __shared__ __align__(16) uint8_t sm[];
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // q|k|v come from the previous kernel
     constexpr int Gp = NT * 8;
     const int64_t base = static_cast<int64_t>(blockIdx.x) * G;
     // ---- stage q|k|v rows: the QKV kernel writes 12 column chunks of [rows x 32]
@@ -100,19 +109,24 @@ __global__ void __launch_bounds__(256) k_attention_mma(const __nv_bfloat16* __re
             const int qrow = mt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
             ldsm_x4(s0 + qrow * kPitch + qcol + (lane >> 4) * 16, a0, a1, a2, a3);
         }
+        // key tiles entirely beyond G carry P = 0: skip their QK^T, exp and PV work;
+        // only the boundary tile needs a mask (G is uniform across the CTA)
+        const int nt_live = (G + 7) >> 3;
         float s[NT][4];
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
             s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
-            mma16816(s[nt], a0, a1, a2, a3, kb[nt][0], kb[nt][1]);
+            if (nt < nt_live) mma16816(s[nt], a0, a1, a2, a3, kb[nt][0], kb[nt][1]);
         }
-        // mask padded keys, row max (rows g and g+8 of this tile)
         float m0 = -INFINITY, m1 = -INFINITY;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-            const int col = nt * 8 + 2 * t4;
-            if (col >= G) { s[nt][0] = -INFINITY; s[nt][2] = -INFINITY; }
-            if (col + 1 >= G) { s[nt][1] = -INFINITY; s[nt][3] = -INFINITY; }
+            if (nt >= nt_live) continue;
+            if (nt * 8 + 8 > G) {
+                const int col = nt * 8 + 2 * t4;
+                if (col >= G) { s[nt][0] = -INFINITY; s[nt][2] = -INFINITY; }
+                if (col + 1 >= G) { s[nt][1] = -INFINITY; s[nt][3] = -INFINITY; }
+            }
             m0 = fmaxf(m0, fmaxf(s[nt][0], s[nt][1]));
             m1 = fmaxf(m1, fmaxf(s[nt][2], s[nt][3]));
         }
@@ -124,10 +138,11 @@ __global__ void __launch_bounds__(256) k_attention_mma(const __nv_bfloat16* __re
         float l0 = 0.f, l1 = 0.f;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-            s[nt][0] = exp2f(s[nt][0] * kScaleLog2 - mb0);
-            s[nt][1] = exp2f(s[nt][1] * kScaleLog2 - mb0);
-            s[nt][2] = exp2f(s[nt][2] * kScaleLog2 - mb1);
-            s[nt][3] = exp2f(s[nt][3] * kScaleLog2 - mb1);
+            if (nt >= nt_live) continue;
+            s[nt][0] = ex2_approx(fmaf(s[nt][0], kScaleLog2, -mb0));
+            s[nt][1] = ex2_approx(fmaf(s[nt][1], kScaleLog2, -mb0));
+            s[nt][2] = ex2_approx(fmaf(s[nt][2], kScaleLog2, -mb1));
+            s[nt][3] = ex2_approx(fmaf(s[nt][3], kScaleLog2, -mb1));
             l0 += s[nt][0] + s[nt][1];
             l1 += s[nt][2] + s[nt][3];
         }
@@ -139,6 +154,7 @@ __global__ void __launch_bounds__(256) k_attention_mma(const __nv_bfloat16* __re
         float o[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
         for (int kt = 0; kt < NT / 2; ++kt) {
+            if (2 * kt >= nt_live) continue;
             const uint32_t p0 = pack_bf16x2(s[2 * kt][0], s[2 * kt][1]);
             const uint32_t p1 = pack_bf16x2(s[2 * kt][2], s[2 * kt][3]);
             const uint32_t p2 = pack_bf16x2(s[2 * kt + 1][0], s[2 * kt + 1][1]);
@@ -176,7 +192,7 @@ static void launch_nt(const __nv_bfloat16* qkv, int64_t rows, int64_t n_groups, 
         cudaFuncSetAttribute(k_attention_mma<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         init = true;
     }
-    k_attention_mma<NT><<<static_cast<unsigned>(n_groups), 256, smem, s>>>(qkv, rows, G, cat);
+    launch_pdl(k_attention_mma<NT>, dim3(static_cast<unsigned>(n_groups)), dim3(256), smem, s, qkv, rows, G, cat);
 }
 
 void launch_attention_mma(const __nv_bfloat16* qkv, int64_t rows, int G, __nv_bfloat16* cat_img,

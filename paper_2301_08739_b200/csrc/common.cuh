@@ -34,4 +34,23 @@ FWA_DEVINL uint32_t pack_bf16x2(float lo, float hi) {
 // Exact-erf GELU of the reference (dense.hpp:67-72) in fp32.
 FWA_DEVINL float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
 
+// Launch with programmatic stream serialization (PDL) so the kernel's prologue can
+// overlap the previous kernel's tail (kernels call griddepcontrol.wait before reading
+// the previous kernel's outputs).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 } // namespace fwa_b200

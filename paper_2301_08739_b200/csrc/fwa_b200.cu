@@ -242,9 +242,13 @@ std::vector<BlockParams> upload_block_params(const std::vector<Record>& recs, De
     std::vector<BlockParams> blocks(nb);
     const bool tc = d == 128 && dff == 256;
     const size_t tc_elems = 384 * 128 + 128 * 128 + 256 * 128 + 128 * 256;
+    // per block, after the bf16 images: f32 [b_qkv 384 | b_out 128 | b2 128 | b1' 256]
+    constexpr size_t kTcVec = 896;
     std::vector<uint16_t> sw;
+    std::vector<float> tcv;
     if (tc) {
-        sw.assign(tc_elems * nb, 0);
+        sw.assign(tc_elems * nb + kTcVec * 2 * nb, 0);
+        tcv.assign(kTcVec * nb, 0.f);
         const size_t tb = sw.size() * 2;
         if (pbf16.cap < tb) {
             if (pbf16.p) cudaFree(pbf16.p);
@@ -277,7 +281,24 @@ std::vector<BlockParams> upload_block_params(const std::vector<Record>& recs, De
             uint16_t* o = sw.data() + b * tc_elems;
             swizzle_weight_bf16(hw_qkv, 384, 128, o);
             swizzle_weight_bf16(hw_out, 128, 128, o + 384 * 128);
-            swizzle_weight_bf16(hw1, 256, 128, o + 384 * 128 + 128 * 128);
+            // LN2's affine folded into FFN1 (bf16 fast path only): U = (g*xhat + b) W1^T + b1
+            //   = xhat (W1 diag g)^T + (b1 + W1 b)   -- exact in real arithmetic
+            const float* hln2g = hw_out + d * d + d + 2 * d;
+            const float* hln2b = hln2g + d;
+            const float* hb1 = hw1 + dff * d;
+            std::vector<float> w1f(static_cast<size_t>(dff) * d);
+            for (int j = 0; j < dff; ++j) {
+                double acc = hb1[j];
+                for (int i = 0; i < d; ++i) {
+                    w1f[static_cast<size_t>(j) * d + i] = hw1[static_cast<size_t>(j) * d + i] * hln2g[i];
+                    acc += static_cast<double>(hw1[static_cast<size_t>(j) * d + i]) * hln2b[i];
+                }
+                tcv[b * kTcVec + 640 + j] = static_cast<float>(acc);
+            }
+            swizzle_weight_bf16(w1f.data(), 256, 128, o + 384 * 128 + 128 * 128);
+            for (int i = 0; i < 384; ++i) tcv[b * kTcVec + i] = hw_qkv[3 * d * d + i];           // b_qkv
+            for (int i = 0; i < 128; ++i) tcv[b * kTcVec + 384 + i] = hw_out[d * d + i];          // b_out
+            for (int i = 0; i < 128; ++i) tcv[b * kTcVec + 512 + i] = hw2[static_cast<size_t>(d) * dff + i];  // b2
             swizzle_weight_bf16(hw2, 128, 256, o + 384 * 128 + 128 * 128 + 256 * 128);
             const __nv_bfloat16* dbase =
                 static_cast<const __nv_bfloat16*>(pbf16.p) + b * tc_elems;
@@ -285,17 +306,18 @@ std::vector<BlockParams> upload_block_params(const std::vector<Record>& recs, De
             bp.tc.w_out = dbase + 384 * 128;
             bp.tc.w1 = dbase + 384 * 128 + 128 * 128;
             bp.tc.w2 = dbase + 384 * 128 + 128 * 128 + 256 * 128;
-            bp.tc.b_qkv = bp.b_qkv;
-            bp.tc.b_out = bp.b_out;
+            const float* vbase = reinterpret_cast<const float*>(
+                                     static_cast<const __nv_bfloat16*>(pbf16.p) + tc_elems * nb) +
+                                 b * kTcVec;
+            bp.tc.vec = vbase;  // b_qkv | b_out | b2 | b1 (LN2-folded)
             bp.tc.ln1_g = bp.ln1_g;
             bp.tc.ln1_b = bp.ln1_b;
-            bp.tc.ln2_g = bp.ln2_g;
-            bp.tc.ln2_b = bp.ln2_b;
-            bp.tc.b1 = bp.b1;
-            bp.tc.b2 = bp.b2;
         }
     }
-    if (tc) CUDA_OK(cudaMemcpyAsync(pbf16.p, sw.data(), sw.size() * 2, cudaMemcpyHostToDevice, st));
+    if (tc) {
+        std::memcpy(sw.data() + tc_elems * nb, tcv.data(), tcv.size() * 4);
+        CUDA_OK(cudaMemcpyAsync(pbf16.p, sw.data(), sw.size() * 2, cudaMemcpyHostToDevice, st));
+    }
     CUDA_OK(cudaStreamSynchronize(st));  // host staging vectors die on return
     return blocks;
 }
@@ -504,9 +526,15 @@ void run_block(fwa_b200_ctx* c, const BlockParams& p, const fwa_config_t* cfg, i
         __nv_bfloat16* qkv = ws<__nv_bfloat16>(c, "qkv16", static_cast<size_t>(rows) * 3 * d);
         // attention output as per-128-row-tile SW128 images (the out-proj A operand)
         __nv_bfloat16* cat = ws<__nv_bfloat16>(c, "cat16", static_cast<size_t>((rows + 127) / 128) * 128 * d);
+        // FWA_B200_TRACE=1: phase clocks of the f32-input blocks' tcgen05 kernels (last call wins)
+        static const bool trace_on = [] {
+            const char* v = std::getenv("FWA_B200_TRACE");
+            return v && v[0] == '1';
+        }();
+        unsigned long long* tr = trace_on && !x_in64 ? ws<unsigned long long>(c, "trace", 2 * 148 * 64) : nullptr;
         {
             StageEv t(c, FWA_PROF_LN_QKV);
-            launch_ln1_qkv_tc(x_in, x_in64, pe16, ridx, rows, p.tc, qkv, c->d_flag, st, &c->launches);
+            launch_ln1_qkv_tc(x_in, x_in64, pe16, ridx, rows, p.tc, qkv, c->d_flag, st, &c->launches, tr);
             check_launch("k_ln1_qkv_tc");
         }
         {
@@ -516,7 +544,8 @@ void run_block(fwa_b200_ctx* c, const BlockParams& p, const fwa_config_t* cfg, i
         }
         {
             StageEv t(c, FWA_PROF_OUTPROJ_FFN);
-            launch_outproj_ffn_tc(cat, x_in, x_in64, ridx, rows, p.tc, x_out, sidx, st, &c->launches);
+            launch_outproj_ffn_tc(cat, x_in, x_in64, ridx, rows, p.tc, x_out, sidx, st, &c->launches,
+                                  tr ? tr + 148 * 64 : nullptr);
             check_launch("k_outproj_ffn_tc");
         }
         check_launch();
@@ -762,6 +791,16 @@ int fwa_b200_set_precision(fwa_b200_ctx* c, int precision) {
 }
 
 int64_t fwa_b200_kernel_launches(const fwa_b200_ctx* c) { return c ? c->launches : 0; }
+
+// Debug: copy the phase-trace buffer (2 x 148 x 64 u64 clocks) to the host.
+int fwa_b200_debug_trace(fwa_b200_ctx* c, unsigned long long* out) {
+    return guarded(c, [&] {
+        auto it = c->ws.find("trace");
+        if (it == c->ws.end() || !it->second.p) throw FwaError{FWA_ERR_CONTRACT, "no trace (FWA_B200_TRACE=1)"};
+        CUDA_OK(cudaStreamSynchronize(c->stream));
+        CUDA_OK(cudaMemcpy(out, it->second.p, 2 * 148 * 64 * 8, cudaMemcpyDeviceToHost));
+    });
+}
 
 int fwa_b200_set_profiling(fwa_b200_ctx* c, int enable) {
     if (!c) return FWA_ERR_CONFIG;

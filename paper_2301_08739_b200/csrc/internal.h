@@ -91,9 +91,10 @@ void launch_attention_f32(const float* qkv, int64_t rows, int G, int d, int head
 struct TcBlockWeights {
     const __nv_bfloat16* w_qkv; // 384 x 128, pre-swizzled UMMA K-major SW128 image
     const __nv_bfloat16* w_out; // 128 x 128, swizzled
-    const __nv_bfloat16* w1;    // 256 x 128, swizzled
+    const __nv_bfloat16* w1;    // 256 x 128, swizzled, LN2 gamma folded in (W1 diag(g2))
     const __nv_bfloat16* w2;    // 128 x 256, swizzled
-    const float *b_qkv, *b_out, *ln1_g, *ln1_b, *ln2_g, *ln2_b, *b1, *b2;
+    const float* vec;           // [b_qkv 384 | b_out 128 | b2 128 | b1 + W1 b2ln 256]
+    const float *ln1_g, *ln1_b;
 };
 // Host-side: write the UMMA SW128 K-major smem image of a row-major f32
 // [rows x k] weight as bf16 (rows multiple of 8, k multiple of 64).
@@ -101,13 +102,15 @@ void swizzle_weight_bf16(const float* w, int rows, int k, uint16_t* out);
 
 void launch_ln1_qkv_tc(const float* x, const double* x64, const __half* pe16, const int32_t* idx,
                        int64_t rows, const TcBlockWeights& w, __nv_bfloat16* qkv,
-                       int* d_nonfinite, cudaStream_t s, int64_t* launches);
+                       int* d_nonfinite, cudaStream_t s, int64_t* launches,
+                       unsigned long long* trace = nullptr);
 void launch_attention_mma(const __nv_bfloat16* qkv, int64_t rows, int G, __nv_bfloat16* cat,
                           cudaStream_t s, int64_t* launches);
 // x_out[sidx[r]] = FFN-block(x_in[ridx[r]] + cat[r] Wout^T + b_out)
 void launch_outproj_ffn_tc(const __nv_bfloat16* cat, const float* x_in, const double* x_in64,
                            const int32_t* ridx, int64_t rows, const TcBlockWeights& w,
-                           float* x_out, const int32_t* sidx, cudaStream_t s, int64_t* launches);
+                           float* x_out, const int32_t* sidx, cudaStream_t s, int64_t* launches,
+                           unsigned long long* trace = nullptr);
 
 // ------------------------------------------------------------------ misc
 void launch_scatter_rows(const float* src, const int32_t* ids, const uint32_t* rank, int64_t n,

@@ -47,6 +47,12 @@ void swizzle_weight_bf16(const float* w, int rows, int k, uint16_t* out) {
             out[sw128_offset(r, c, rows) / 2] = f32_to_bf16_rn(w[static_cast<size_t>(r) * k + c]);
 }
 
+// Phase tracing (FWA_B200_TRACE=1): SM clock at phase boundaries, 64 slots per CTA.
+#define FWA_TR(k)                                                                         \
+    do {                                                                                  \
+        if (trace) trace[blockIdx.x * 64 + (k)] = static_cast<unsigned long long>(clock64()); \
+    } while (0)
+
 // pointer arithmetic on the extern __shared__ array keeps the shared address space
 // visible to the compiler (STS/LDS instead of generic ST/LD)
 FWA_DEVINL uint8_t* align1024(uint8_t* p) { return p + ((1024u - (smem_u32(p) & 1023u)) & 1023u); }
@@ -54,31 +60,112 @@ FWA_DEVINL uint8_t* align1024(uint8_t* p) { return p + ((1024u - (smem_u32(p) & 
 // ------------------------------------------------------------------ K_a: gather + LN1 + PE + QKV
 //
 // Warp-specialised persistent kernel, 12 warps:
-//   warps 0-7  producers: gather 16 rows each (pillar ids from the window-sort
-//              permutation), LN1 + affine + PE in fp32, bf16 -> SW128 A tile; A is
-//              double-buffered so tile t+1 is gathered while tile t is multiplied.
-//   warps 8-11 MMA issue (one elected thread) + epilogue: TMEM -> +bias -> bf16,
-//              written chunk-major (q|k|v as 12 column chunks of [rows x 32]) so
-//              each warp store is 2 KB contiguous and the attention kernel reads
-//              each group's rows as contiguous 4.4 KB runs.
+//   warps 0-7  producers: 16 rows each per 128-row tile, 8 lanes per row (16 channels:
+//              64 B of the fp32 row + 32 B of the fp16 PE row per lane), 4-row passes
+//              software-pipelined (pass p+1 in flight while pass p is reduced), the
+//              pillar ids of the NEXT tile prefetched; LN1 + affine + PE in fp32 -> bf16
+//              SW128 A tile.  A is double-buffered so tile t+1 is gathered while tile t
+//              is multiplied.
+//   warps 8-15 MMA issue (one elected thread) + epilogue (lane quarter x column half):
+//              TMEM -> +bias -> bf16,
+//              written chunk-major (q|k|v as 12 column chunks of [rows x 32]) so each
+//              warp store is 2 KB contiguous and the attention kernel reads each
+//              group's rows as contiguous runs.
 // mbarriers: full[s] (8 producer warps), empty[s] (tcgen05.commit), done (commit).
 
 constexpr int kQkvW = 384 * 128 * 2;   // 98304 B weight image
 constexpr int kTileA = 128 * 128 * 2;  // 32768 B per A stage
-constexpr int kQkvThreads = 384;
-constexpr int kQkvSmem = kQkvW + 2 * kTileA + 384 * 4 /*bias*/ + 128 /*bars*/ + 1024 /*align*/;
+constexpr int kQkvThreads = 512;
+constexpr int kQkvSmem = kQkvW + 2 * kTileA + (384 + 256) * 4 /*bias, ln1 g|b*/ + 128 /*bars*/ + 1024;
+
+// One lane's 16 channels (an eighth of a row): 64 B of the fp32 row, 32 B of the fp16 PE row.
+template <bool kF64>
+FWA_DEVINL void load_row_eighth(const float* x, const double* x64, const __half* pe16, int64_t id,
+                                int sub, bool valid, float (&v)[16], uint4 (&ph)[2]) {
+    if (!valid) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = 0.f;
+        ph[0] = ph[1] = make_uint4(0u, 0u, 0u, 0u);
+        return;
+    }
+    if (kF64) {
+        const double2* p = reinterpret_cast<const double2*>(x64 + id * 128 + sub * 16);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const double2 d2 = __ldg(p + j);
+            v[2 * j] = static_cast<float>(d2.x);
+            v[2 * j + 1] = static_cast<float>(d2.y);
+        }
+    } else {
+        const float4* p = reinterpret_cast<const float4*>(x + id * 128 + sub * 16);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float4 f4 = __ldg(p + j);
+            v[4 * j] = f4.x; v[4 * j + 1] = f4.y; v[4 * j + 2] = f4.z; v[4 * j + 3] = f4.w;
+        }
+    }
+    const uint4* pp = reinterpret_cast<const uint4*>(pe16 + id * 128 + sub * 16);
+    ph[0] = __ldg(pp);
+    ph[1] = __ldg(pp + 1);
+}
+
+// LN1 (two-pass, 8 lanes per row) + affine + PE -> 2 bf16 chunks of the A image.
+FWA_DEVINL void ln1_row_to_tile(const float (&v)[16], const uint4 (&ph)[2], bool valid, int r, int sub,
+                                const float* sG, const float* sB, uint8_t* A, bool& bad) {
+    float sm = 0.f;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) sm += v[j];
+    sm += __shfl_xor_sync(0xffffffffu, sm, 1);
+    sm += __shfl_xor_sync(0xffffffffu, sm, 2);
+    sm += __shfl_xor_sync(0xffffffffu, sm, 4);
+    const float mean = sm * (1.0f / 128.0f);
+    float sq = 0.f;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        bad |= !isfinite(v[j]);
+        sq += (v[j] - mean) * (v[j] - mean);
+    }
+    sq += __shfl_xor_sync(0xffffffffu, sq, 1);
+    sq += __shfl_xor_sync(0xffffffffu, sq, 2);
+    sq += __shfl_xor_sync(0xffffffffu, sq, 4);
+    const float inv = 1.0f / sqrtf(sq * (1.0f / 128.0f) + 1e-5f);
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {  // 8 channels = one 16 B chunk of the SW128 image
+        const float4 g0 = *reinterpret_cast<const float4*>(sG + sub * 16 + c * 8);
+        const float4 g1 = *reinterpret_cast<const float4*>(sG + sub * 16 + c * 8 + 4);
+        const float4 b0 = *reinterpret_cast<const float4*>(sB + sub * 16 + c * 8);
+        const float4 b1 = *reinterpret_cast<const float4*>(sB + sub * 16 + c * 8 + 4);
+        const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+        const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+        const uint32_t hw[4] = {ph[c].x, ph[c].y, ph[c].z, ph[c].w};
+        uint32_t o[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float2 pf = __half22float2(*reinterpret_cast<const __half2*>(&hw[e]));
+            bad |= !(isfinite(pf.x) && isfinite(pf.y));
+            const int j = c * 8 + 2 * e;
+            o[e] = pack_bf16x2(gg[2 * e] * ((v[j] - mean) * inv) + bb[2 * e] + pf.x,
+                               gg[2 * e + 1] * ((v[j + 1] - mean) * inv) + bb[2 * e + 1] + pf.y);
+        }
+        if (!valid) o[0] = o[1] = o[2] = o[3] = 0u;
+        *reinterpret_cast<uint4*>(A + sw128_offset(r, sub * 16 + c * 8, 128)) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+}
 
 template <bool kF64>
 __global__ void __launch_bounds__(kQkvThreads, 1)
     k_ln1_qkv_tc(const float* __restrict__ x, const double* __restrict__ x64,
                  const __half* __restrict__ pe16, const int32_t* __restrict__ idx, int64_t rows,
-                 TcBlockWeights w, __nv_bfloat16* __restrict__ qkv, int* __restrict__ nonfinite) {
+                 TcBlockWeights w, __nv_bfloat16* __restrict__ qkv, int* __restrict__ nonfinite,
+                 unsigned long long* __restrict__ trace) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
     uint8_t* sW = smem;
     uint8_t* sA = smem + kQkvW;                                        // 2 stages
     float* sBias = reinterpret_cast<float*>(sA + 2 * kTileA);          // 384
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sBias + 384);         // wbar, full[2], empty[2], done
+    float* sG = sBias + 384;                                           // 128
+    float* sB = sG + 128;                                              // 128
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + 128);            // wbar, full[2], empty[2], done
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6);
     uint64_t* wbar = bars;
     uint64_t* full = bars + 1;
@@ -86,6 +173,7 @@ __global__ void __launch_bounds__(kQkvThreads, 1)
     uint64_t* done = bars + 5;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
+    griddep_launch_dependents();
     if (threadIdx.x == 0) {
         mbar_init(wbar, 1);
         mbar_init(&full[0], 8);
@@ -95,7 +183,11 @@ __global__ void __launch_bounds__(kQkvThreads, 1)
         mbar_init(done, 1);
         fence_mbar_init();
     }
-    for (int i = threadIdx.x; i < 384; i += blockDim.x) sBias[i] = w.b_qkv[i];
+    for (int i = threadIdx.x; i < 384; i += blockDim.x) sBias[i] = w.vec[i];
+    for (int i = threadIdx.x; i < 128; i += blockDim.x) {
+        sG[i] = w.ln1_g[i];
+        sB[i] = w.ln1_b[i];
+    }
     if (warp == 8) {
         __syncwarp();
         tmem_alloc(tmem_slot, 512);
@@ -114,97 +206,47 @@ __global__ void __launch_bounds__(kQkvThreads, 1)
             for (int c = 0; c < 3; ++c)
                 bulk_g2s(sW + c * 32768, reinterpret_cast<const uint8_t*>(w.w_qkv) + c * 32768, 32768, wbar);
         }
-        // 4 lanes per row (32 channels each, 128 B contiguous per lane), 8 rows per pass
-        const int sub = lane & 3, rl = lane >> 2;
-        float gam[32], bet[32];
-#pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-            const float4 g = __ldg(reinterpret_cast<const float4*>(w.ln1_g + sub * 32 + j));
-            const float4 bb = __ldg(reinterpret_cast<const float4*>(w.ln1_b + sub * 32 + j));
-            gam[j] = g.x; gam[j + 1] = g.y; gam[j + 2] = g.z; gam[j + 3] = g.w;
-            bet[j] = bb.x; bet[j + 1] = bb.y; bet[j + 2] = bb.z; bet[j + 3] = bb.w;
-        }
+        auto tile_ids = [&](int64_t tile) {  // lane l < 16 holds the id of row warp*16 + l
+            const int64_t g = tile * 128 + warp * 16 + (lane & 15);
+            return (tile < ntiles && g < rows) ? (idx ? idx[g] : static_cast<int>(g)) : 0;
+        };
         bool bad = false;
+        if (threadIdx.x == 0) FWA_TR(0);
+        griddep_wait();  // x / PE / ids come from earlier kernels
+        const int sub = lane & 7, rl = lane >> 3;  // 8 lanes per row, 4 rows per pass
+        int ids = tile_ids(blockIdx.x);
         int it = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
             const int s = it & 1;
+            float v[2][16];
+            uint4 ph[2][2];
+            int64_t id[4];
+            bool ok[4];
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                id[p] = __shfl_sync(0xffffffffu, ids, p * 4 + rl);
+                ok[p] = tile * 128 + warp * 16 + p * 4 + rl < rows;
+            }
+            ids = tile_ids(tile + gridDim.x);  // prefetch the next tile's pillar ids
+            load_row_eighth<kF64>(x, x64, pe16, id[0], sub, ok[0], v[0], ph[0]);
+            if (threadIdx.x == 0 && it < 6) FWA_TR(1 + 4 * it);
             if (it >= 2) mbar_wait(&empty[s], ((it >> 1) - 1) & 1);
+            if (threadIdx.x == 0 && it < 6) FWA_TR(2 + 4 * it);
             uint8_t* A = sA + s * kTileA;
-#pragma unroll 1
-            for (int pass = 0; pass < 2; ++pass) {
-                const int r = warp * 16 + pass * 8 + rl;
-                const int64_t g = tile * 128 + r;
-                const bool valid = g < rows;
-                const int64_t id = valid ? (idx ? idx[g] : g) : 0;
-                float v[32];
-                uint4 ph[4];
-                if (valid) {
-                    if (kF64) {
-                        const double2* p = reinterpret_cast<const double2*>(x64 + id * 128 + sub * 32);
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            const double2 d2 = __ldg(p + j);
-                            v[2 * j] = static_cast<float>(d2.x);
-                            v[2 * j + 1] = static_cast<float>(d2.y);
-                        }
-                    } else {
-                        const float4* p = reinterpret_cast<const float4*>(x + id * 128 + sub * 32);
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            const float4 f4 = __ldg(p + j);
-                            v[4 * j] = f4.x; v[4 * j + 1] = f4.y; v[4 * j + 2] = f4.z; v[4 * j + 3] = f4.w;
-                        }
-                    }
-                    const uint4* pp = reinterpret_cast<const uint4*>(pe16 + id * 128 + sub * 32);
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) ph[j] = __ldg(pp + j);
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) v[j] = 0.f;
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) ph[j] = make_uint4(0u, 0u, 0u, 0u);
-                }
-                float sm = 0.f;
-#pragma unroll
-                for (int j = 0; j < 32; ++j) sm += v[j];
-                sm += __shfl_xor_sync(0xffffffffu, sm, 1);
-                sm += __shfl_xor_sync(0xffffffffu, sm, 2);
-                const float mean = sm * (1.0f / 128.0f);
-                float sq = 0.f;
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    bad |= !isfinite(v[j]);
-                    sq += (v[j] - mean) * (v[j] - mean);
-                }
-                sq += __shfl_xor_sync(0xffffffffu, sq, 1);
-                sq += __shfl_xor_sync(0xffffffffu, sq, 2);
-                const float inv = 1.0f / sqrtf(sq * (1.0f / 128.0f) + 1e-5f);
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {  // 8 channels = one 16 B chunk of the SW128 image
-                    const uint32_t hw[4] = {ph[c].x, ph[c].y, ph[c].z, ph[c].w};
-                    uint32_t o[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float2 pf = __half22float2(*reinterpret_cast<const __half2*>(&hw[e]));
-                        bad |= !(isfinite(pf.x) && isfinite(pf.y));
-                        const int j = c * 8 + 2 * e;
-                        o[e] = pack_bf16x2(gam[j] * ((v[j] - mean) * inv) + bet[j] + pf.x,
-                                           gam[j + 1] * ((v[j + 1] - mean) * inv) + bet[j + 1] + pf.y);
-                    }
-                    if (!valid) o[0] = o[1] = o[2] = o[3] = 0u;
-                    *reinterpret_cast<uint4*>(A + sw128_offset(r, sub * 32 + c * 8, 128)) =
-                        make_uint4(o[0], o[1], o[2], o[3]);
-                }
+            for (int p = 0; p < 4; ++p) {  // rows of pass p+1 in flight while pass p is reduced
+                if (p + 1 < 4) load_row_eighth<kF64>(x, x64, pe16, id[p + 1], sub, ok[p + 1], v[(p + 1) & 1], ph[(p + 1) & 1]);
+                ln1_row_to_tile(v[p & 1], ph[p & 1], ok[p], warp * 16 + p * 4 + rl, sub, sG, sB, A, bad);
             }
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(&full[s]);
+            if (threadIdx.x == 0 && it < 6) FWA_TR(3 + 4 * it);
         }
         if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(nonfinite, 1);
-        if (threadIdx.x == 0 && ntiles <= blockIdx.x) mbar_wait(wbar, 0);  // no tile: drain the TMA
     } else {
-        // ------------------------------------------------ MMA issue + epilogue (warps 8..11)
-        const int q = warp - 8;
+        // ------------------------------------------------ MMA issue + epilogue (warps 8..15)
+        const int q = (warp - 8) & 3, half = (warp - 8) >> 2;  // lane quarter, column half
         const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
         constexpr uint32_t idesc = idesc_bf16_f32(128, 128);
         int it = 0;
@@ -226,31 +268,41 @@ __global__ void __launch_bounds__(kQkvThreads, 1)
                 }
                 mma_commit(&empty[s]);
                 mma_commit(done);
+                if (it < 6) FWA_TR(30 + 4 * it);
             }
             __syncwarp();
             mbar_wait(done, it & 1);
             fence_after_sync();
+            if (warp == 8 && lane == 0 && it < 6) FWA_TR(31 + 4 * it);
             const int64_t grow = tile * 128 + q * 32 + lane;
 #pragma unroll 1
-            for (int ch = 0; ch < 12; ++ch) {
-                uint32_t v[32];
+            for (int ch = half * 6; ch < half * 6 + 6; ch += 2) {
+                uint32_t v[32], u[32];
                 tmem_ld32(tmem + lane_off + ch * 32, v);
+                tmem_ld32(tmem + lane_off + ch * 32 + 32, u);
                 tmem_ld_wait();
                 if (grow < rows) {
-                    uint32_t o[16];
 #pragma unroll
-                    for (int j = 0; j < 16; ++j)
-                        o[j] = pack_bf16x2(__uint_as_float(v[2 * j]) + sBias[ch * 32 + 2 * j],
-                                           __uint_as_float(v[2 * j + 1]) + sBias[ch * 32 + 2 * j + 1]);
-                    uint4* dst = reinterpret_cast<uint4*>(qkv + (static_cast<int64_t>(ch) * rows + grow) * 32);
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const uint32_t* src = hh ? u : v;
+                        const float* bias = sBias + (ch + hh) * 32;
+                        uint32_t o[16];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) dst[j] = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+                        for (int j = 0; j < 16; ++j)
+                            o[j] = pack_bf16x2(__uint_as_float(src[2 * j]) + bias[2 * j],
+                                               __uint_as_float(src[2 * j + 1]) + bias[2 * j + 1]);
+                        uint4* dst = reinterpret_cast<uint4*>(qkv + (static_cast<int64_t>(ch + hh) * rows + grow) * 32);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) dst[j] = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+                    }
                 }
             }
             fence_before_sync();
-            asm volatile("bar.sync 1, 128;" ::: "memory");  // TMEM drained before the next MMA
+            asm volatile("bar.sync 1, 256;" ::: "memory");  // TMEM drained before the next MMA
             fence_after_sync();
+            if (warp == 8 && lane == 0 && it < 6) FWA_TR(32 + 4 * it);
         }
+        if (warp == 8 && lane == 0) FWA_TR(60);
     }
     fence_before_sync();
     __syncthreads();
@@ -260,7 +312,7 @@ __global__ void __launch_bounds__(kQkvThreads, 1)
 
 void launch_ln1_qkv_tc(const float* x, const double* x64, const __half* pe, const int32_t* idx,
                        int64_t rows, const TcBlockWeights& w, __nv_bfloat16* qkv, int* d_nonfinite,
-                       cudaStream_t s, int64_t* launches) {
+                       cudaStream_t s, int64_t* launches, unsigned long long* trace) {
     static bool init = false;
     if (!init) {
         cudaFuncSetAttribute(k_ln1_qkv_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kQkvSmem);
@@ -270,9 +322,11 @@ void launch_ln1_qkv_tc(const float* x, const double* x64, const __half* pe, cons
     const int64_t ntiles = (rows + 127) / 128;
     const unsigned grid = static_cast<unsigned>(ntiles < kNumSMs ? ntiles : kNumSMs);
     if (x64)
-        k_ln1_qkv_tc<true><<<grid, kQkvThreads, kQkvSmem, s>>>(x, x64, pe, idx, rows, w, qkv, d_nonfinite);
+        launch_pdl(k_ln1_qkv_tc<true>, grid, kQkvThreads, kQkvSmem, s, x, x64, pe, idx, rows, w, qkv,
+                   d_nonfinite, trace);
     else
-        k_ln1_qkv_tc<false><<<grid, kQkvThreads, kQkvSmem, s>>>(x, x64, pe, idx, rows, w, qkv, d_nonfinite);
+        launch_pdl(k_ln1_qkv_tc<false>, grid, kQkvThreads, kQkvSmem, s, x, x64, pe, idx, rows, w, qkv,
+                   d_nonfinite, trace);
     ++*launches;
 }
 
@@ -298,24 +352,32 @@ constexpr int kW1 = 256 * 128 * 2;    // 65536
 constexpr int kW2 = 128 * 256 * 2;    // 65536
 constexpr int kRegion = 65536;        // R0 | R1
 constexpr int kFfnThreads = 512;
-constexpr int kFfnSmem = kWout + kW1 + kW2 + kRegion + 64 /*bars*/ + 1024 /*align*/;
+constexpr int kFfnVec = 512;           // b_out 128 | b2 128 | b1 (LN2-folded) 256, fp32
+constexpr int kFfnSmemUsed = kWout + kW1 + kW2 + kRegion + kFfnVec * 4 + 64 /*bars*/;
+constexpr int kFfnSmem = 232448;       // the sm_100 per-block maximum; slack absorbs base alignment
 
 // f32 row staging in R: row r (512 B) chunk c (16 B) at r*512 + ((c ^ (r & 7)) * 16)
 FWA_DEVINL uint32_t stage_off(int r, int c) { return static_cast<uint32_t>(r * 512 + ((c ^ (r & 7)) << 4)); }
 
-// exact-erf GELU of the reference (dense.hpp:67-72) with erf from Abramowitz-Stegun
-// 7.1.26 (|err| <= 1.5e-7), far below the bf16 rounding of the activation that follows
+// The reference's exact-erf GELU (dense.hpp:67-72), x * Phi(x), evaluated as
+// x * 0.5 * (1 + tanh(g(x))) with g an odd degree-7 polynomial fitted to
+// atanh(erf(x / sqrt 2)) on |x| <= 3.2 (|x| clamped to 6, where Phi is 1 to 1e-9) and
+// the hardware tanh.approx.f32 (rel 2^-11): |dGELU| <= 3.2e-5 from the fit plus
+// <= 2.5e-4 |x| from tanh.approx -- below the bf16 rounding (2^-9 rel) of the
+// activation it feeds.  9 FMA-pipe ops + 1 MUFU instead of ~20 + 2 for erff.
+FWA_DEVINL float tanh_approx(float x) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 FWA_DEVINL float gelu_fast(float x) {
-    const float z = x * 0.70710678118654752f;
-    const float az = fabsf(z);
-    const float t = __frcp_rn(fmaf(0.3275911f, az, 1.0f));
-    const float poly =
-        t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, 1.061405429f, -1.453152027f), 1.421413741f), -0.284496736f),
-                 0.254829592f);
-    const float e = exp2f(-az * az * 1.4426950408889634f);
-    const float erf_abs = fmaf(-poly, e, 1.0f);
-    const float erf_z = copysignf(erf_abs, z);
-    return 0.5f * x * (1.0f + erf_z);
+    const float xc = fminf(fmaxf(x, -6.0f), 6.0f);
+    const float x2 = xc * xc;
+    const float p = fmaf(fmaf(fmaf(-4.71338576e-06f, x2, -3.19044083e-04f), x2, 3.69914203e-02f), x2,
+                         7.97462955e-01f);
+    const float t = tanh_approx(xc * p);
+    const float hx = 0.5f * x;
+    return fmaf(hx, t, hx);
 }
 
 FWA_DEVINL void tmem_st1(uint32_t taddr, float v) {
@@ -342,25 +404,30 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
     k_outproj_ffn_tc(const uint8_t* __restrict__ cat_img, const float* __restrict__ x_in,
                      const double* __restrict__ x_in64, const int32_t* __restrict__ ridx,
                      int64_t rows, TcBlockWeights w, float* __restrict__ x_out,
-                     const int32_t* __restrict__ sidx) {
+                     const int32_t* __restrict__ sidx, unsigned long long* __restrict__ trace) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
     uint8_t* sWo = smem;
+    if (threadIdx.x == 0) FWA_TR(0);
     uint8_t* sW1 = sWo + kWout;
     uint8_t* sW2 = sW1 + kW1;
     uint8_t* sR = sW2 + kW2;
     uint8_t* sR1 = sR + 32768;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sR + kRegion);  // w, a, p, ua, ub, o
+    float* sVec = reinterpret_cast<float*>(sR + kRegion);        // b_out | b2 | b1'
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sVec + kFfnVec);  // w, a, p, ua, ub, o
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int q = warp & 3, cq = warp >> 2;
     const int row = q * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
 
+    if (smem - smem_raw > kFfnSmem - kFfnSmemUsed) __trap();  // dynamic smem base misaligned
+    griddep_launch_dependents();
     if (threadIdx.x == 0) {
         for (int i = 0; i < 6; ++i) mbar_init(&bars[i], 1);
         fence_mbar_init();
     }
+    for (int i = threadIdx.x; i < kFfnVec; i += blockDim.x) sVec[i] = w.vec[384 + i];
     if (warp == 0) {
         __syncwarp();
         tmem_alloc(tmem_slot, 512);
@@ -375,10 +442,11 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
         bulk_g2s(sW1 + 32768, reinterpret_cast<const uint8_t*>(w.w1) + 32768, 32768, &bars[0]);
         bulk_g2s(sW2, w.w2, 32768, &bars[0]);
         bulk_g2s(sW2 + 32768, reinterpret_cast<const uint8_t*>(w.w2) + 32768, 32768, &bars[0]);
-        if (blockIdx.x < ntiles) {
-            mbar_arrive_expect_tx(&bars[1], 32768);
-            bulk_g2s(sR, cat_img + static_cast<int64_t>(blockIdx.x) * 32768, 32768, &bars[1]);
-        }
+    }
+    griddep_wait();  // attention rows + residual come from earlier kernels
+    if (threadIdx.x == 0 && blockIdx.x < ntiles) {
+        mbar_arrive_expect_tx(&bars[1], 32768);
+        bulk_g2s(sR, cat_img + static_cast<int64_t>(blockIdx.x) * 32768, 32768, &bars[1]);
     }
     constexpr uint32_t id128 = idesc_bf16_f32(128, 128);
     const uint32_t TP = tmem, TUa = tmem + 128, TUb = tmem + 256, TS = tmem + 384;
@@ -391,7 +459,9 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
         // ---- 1. P = A Wout^T
         if (threadIdx.x == 0) {
             if (it == 0) mbar_wait(&bars[0], 0);
+            if (it < 4) FWA_TR(1 + 12 * it);
             mbar_wait(&bars[1], ph);
+            if (it < 4) FWA_TR(2 + 12 * it);
             fence_after_sync();
             const uint32_t a0 = smem_u32(sR), b0 = smem_u32(sWo);
 #pragma unroll
@@ -427,6 +497,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
             }
         }
         mbar_wait(&bars[2], ph);
+        if (threadIdx.x == 0 && it < 4) FWA_TR(3 + 12 * it);
         fence_after_sync();
         {
             uint32_t v[32];
@@ -434,7 +505,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
             tmem_ld_wait();
 #pragma unroll
             for (int j = 0; j < 32; j += 4) {
-                const float4 bo = __ldg(reinterpret_cast<const float4*>(w.b_out + c0 + j));
+                const float4 bo = *reinterpret_cast<const float4*>(sVec + c0 + j);
                 x1[j + 0] = (x1[j + 0] + __uint_as_float(v[j + 0])) + bo.x;
                 x1[j + 1] = (x1[j + 1] + __uint_as_float(v[j + 1])) + bo.y;
                 x1[j + 2] = (x1[j + 2] + __uint_as_float(v[j + 2])) + bo.z;
@@ -464,13 +535,14 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const int j = ch * 8 + 2 * e, col = c0 + j;
-                o[e] = pack_bf16x2(__ldg(w.ln2_g + col) * ((x1[j] - mean) * inv) + __ldg(w.ln2_b + col),
-                                   __ldg(w.ln2_g + col + 1) * ((x1[j + 1] - mean) * inv) + __ldg(w.ln2_b + col + 1));
+                (void)col;  // LN2 affine folded into W1 / b1 on the host
+                o[e] = pack_bf16x2((x1[j] - mean) * inv, (x1[j + 1] - mean) * inv);
             }
             *reinterpret_cast<uint4*>(sR1 + sw128_offset(row, c0 + ch * 8, 128)) = make_uint4(o[0], o[1], o[2], o[3]);
         }
         fence_proxy_async_smem();
         cta_sync_tc();
+        if (threadIdx.x == 0 && it < 4) FWA_TR(4 + 12 * it);
         // ---- 4. U_a, U_b = LN2 W1^T halves (N = 128 each)
         if (threadIdx.x == 0) {
             const uint32_t a0 = smem_u32(sR1), b0 = smem_u32(sW1);
@@ -486,25 +558,27 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
 #pragma unroll 1
         for (int hh = 0; hh < 2; ++hh) {
             mbar_wait(&bars[3 + hh], ph);
+            if (threadIdx.x == 0 && it < 4) FWA_TR(5 + 2 * hh + 12 * it);
             fence_after_sync();
             uint8_t* act = hh ? sR1 : sR;  // [128 x 128] SW128 image (K-blocks 2hh, 2hh+1 of act)
             uint32_t v[32];
             tmem_ld32((hh ? TUb : TUa) + lane_off + c0, v);
             tmem_ld_wait();
-            const float* b1 = w.b1 + hh * 128 + c0;
+            const float* b1 = sVec + 256 + hh * 128 + c0;
 #pragma unroll
             for (int ch = 0; ch < 4; ++ch) {
                 uint32_t o[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int j = ch * 8 + 2 * e;
-                    o[e] = pack_bf16x2(gelu_fast(__uint_as_float(v[j]) + __ldg(b1 + j)),
-                                       gelu_fast(__uint_as_float(v[j + 1]) + __ldg(b1 + j + 1)));
+                    o[e] = pack_bf16x2(gelu_fast(__uint_as_float(v[j]) + b1[j]),
+                                       gelu_fast(__uint_as_float(v[j + 1]) + b1[j + 1]));
                 }
                 *reinterpret_cast<uint4*>(act + sw128_offset(row, c0 + ch * 8, 128)) = make_uint4(o[0], o[1], o[2], o[3]);
             }
             fence_proxy_async_smem();
             cta_sync_tc();
+            if (threadIdx.x == 0 && it < 4) FWA_TR(6 + 2 * hh + 12 * it);
             // ---- O (+)= act_hh W2[:, 128hh : 128hh+128]^T  (O reuses P's columns)
             if (threadIdx.x == 0) {
                 const uint32_t a0 = smem_u32(act), b0 = smem_u32(sW2) + hh * 2 * 16384;
@@ -517,6 +591,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
         }
         // ---- 5. out = x1 + (O + b2) -> staged rows -> coalesced scatter
         mbar_wait(&bars[5], ph);
+        if (threadIdx.x == 0 && it < 4) FWA_TR(9 + 12 * it);
         fence_after_sync();
         {
             uint32_t v[32];
@@ -524,7 +599,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
             tmem_ld_wait();
 #pragma unroll
             for (int j = 0; j < 32; j += 4) {
-                const float4 b2 = __ldg(reinterpret_cast<const float4*>(w.b2 + c0 + j));
+                const float4 b2 = *reinterpret_cast<const float4*>(sVec + 128 + c0 + j);
                 float4 o;
                 o.x = x1[j + 0] + (__uint_as_float(v[j + 0]) + b2.x);
                 o.y = x1[j + 1] + (__uint_as_float(v[j + 1]) + b2.y);
@@ -547,6 +622,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
             }
         }
         __syncthreads();  // R free: prefetch the next tile's attention rows
+        if (threadIdx.x == 0 && it < 4) FWA_TR(10 + 12 * it);
         if (threadIdx.x == 0 && tile + gridDim.x < ntiles) {
             mbar_arrive_expect_tx(&bars[1], 32768);
             bulk_g2s(sR, cat_img + (tile + gridDim.x) * 32768, 32768, &bars[1]);
@@ -559,7 +635,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
 
 void launch_outproj_ffn_tc(const __nv_bfloat16* cat, const float* x_in, const double* x_in64,
                            const int32_t* ridx, int64_t rows, const TcBlockWeights& w, float* x_out,
-                           const int32_t* sidx, cudaStream_t s, int64_t* launches) {
+                           const int32_t* sidx, cudaStream_t s, int64_t* launches,
+                           unsigned long long* trace) {
     static bool init = false;
     if (!init) {
         cudaFuncSetAttribute(k_outproj_ffn_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFfnSmem);
@@ -570,9 +647,11 @@ void launch_outproj_ffn_tc(const __nv_bfloat16* cat, const float* x_in, const do
     const unsigned grid = static_cast<unsigned>(ntiles < kNumSMs ? ntiles : kNumSMs);
     const uint8_t* img = reinterpret_cast<const uint8_t*>(cat);
     if (x_in64)
-        k_outproj_ffn_tc<true><<<grid, kFfnThreads, kFfnSmem, s>>>(img, x_in, x_in64, ridx, rows, w, x_out, sidx);
+        launch_pdl(k_outproj_ffn_tc<true>, grid, kFfnThreads, kFfnSmem, s, img, x_in, x_in64, ridx, rows, w,
+                   x_out, sidx, trace);
     else
-        k_outproj_ffn_tc<false><<<grid, kFfnThreads, kFfnSmem, s>>>(img, x_in, x_in64, ridx, rows, w, x_out, sidx);
+        launch_pdl(k_outproj_ffn_tc<false>, grid, kFfnThreads, kFfnSmem, s, img, x_in, x_in64, ridx, rows, w,
+                   x_out, sidx, trace);
     ++*launches;
 }
 

@@ -40,6 +40,12 @@ FWA_DEVINL void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b
         : "memory");
 }
 
+// ---- programmatic dependent launch (PDL): the next kernel in the stream may start
+// its prologue (barrier init, TMEM alloc, weight TMA) while this one drains; data
+// produced by the previous kernel is read only after griddep_wait().
+FWA_DEVINL void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+FWA_DEVINL void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---- proxy / tcgen05 fences
 FWA_DEVINL void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 FWA_DEVINL void fence_before_sync() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
