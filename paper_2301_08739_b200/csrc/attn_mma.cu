@@ -55,10 +55,13 @@ FWA_DEVINL void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, u
 }
 
 // NT = padded group / 8 (even); MT = NT / 2 query tiles; KT = NT / 2 key tiles.
-template <int NT>
-__global__ void __launch_bounds__(256) k_attention_mma(const __nv_bfloat16* __restrict__ qkv,
-                                                       int64_t rows, int G,
-                                                       uint8_t* __restrict__ cat) {
+// GC > 0: the group size is a compile-time constant (the default config's 69) so the key
+// masking and the skipped all-padding tiles are resolved at compile time.
+template <int NT, int GC>
+__global__ void __launch_bounds__(256, 3) k_attention_mma(const __nv_bfloat16* __restrict__ qkv,
+                                                          int64_t rows, int G_rt,
+                                                          uint8_t* __restrict__ cat) {
+    const int G = GC > 0 ? GC : G_rt;
     extern __shared__ __align__(16) uint8_t sm[];
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");  // q|k|v come from the previous kernel
@@ -68,8 +71,9 @@ __global__ void __launch_bounds__(256) k_attention_mma(const __nv_bfloat16* __re
     // bf16, so each chunk of this group is one contiguous 64*G-byte run; cp.async
     // (16 B, L1-bypassing) into a 784 B row pitch; padding rows zeroed.
     const uint32_t s_base = smem_u32(sm);
+#pragma unroll 4
     for (int t = threadIdx.x; t < 12 * Gp * 4; t += 256) {
-        const int c = t / (Gp * 4), rem = t % (Gp * 4), r = rem >> 2, pp = rem & 3;
+        const int c = t / (Gp * 4), rem = t - c * (Gp * 4), r = rem >> 2, pp = rem & 3;  // Gp constexpr
         const uint32_t dst = s_base + r * kPitch + c * 64 + pp * 16;
         if (r < G) {
             const __nv_bfloat16* src = qkv + (static_cast<int64_t>(c) * rows + base + r) * 32 + pp * 8;
@@ -183,16 +187,18 @@ __global__ void __launch_bounds__(256) k_attention_mma(const __nv_bfloat16* __re
     }
 }
 
-template <int NT>
+template <int NT, int GC = 0>
 static void launch_nt(const __nv_bfloat16* qkv, int64_t rows, int64_t n_groups, int G, uint8_t* cat,
                       cudaStream_t s) {
     const int smem = NT * 8 * kPitch;
     static bool init = false;
     if (!init) {
-        cudaFuncSetAttribute(k_attention_mma<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_attention_mma<NT, GC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_attention_mma<NT, GC>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         init = true;
     }
-    launch_pdl(k_attention_mma<NT>, dim3(static_cast<unsigned>(n_groups)), dim3(256), smem, s, qkv, rows, G, cat);
+    launch_pdl(k_attention_mma<NT, GC>, dim3(static_cast<unsigned>(n_groups)), dim3(256), smem, s, qkv, rows, G,
+               cat);
 }
 
 void launch_attention_mma(const __nv_bfloat16* qkv, int64_t rows, int G, __nv_bfloat16* cat_img,
@@ -201,6 +207,11 @@ void launch_attention_mma(const __nv_bfloat16* qkv, int64_t rows, int G, __nv_bf
     const int64_t n_groups = rows / G;
     if (n_groups == 0) return;
     const int nt = ((G + 15) / 16) * 2;
+    if (G == 69) {  // FwaConfig default group size (backbone.hpp:26)
+        launch_nt<10, 69>(qkv, rows, n_groups, G, cat, s);
+        ++*launches;
+        return;
+    }
     switch (nt) {
         case 2: launch_nt<2>(qkv, rows, n_groups, G, cat, s); break;
         case 4: launch_nt<4>(qkv, rows, n_groups, G, cat, s); break;
