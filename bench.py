@@ -168,7 +168,12 @@ def run_ours(args, rank, world, local_rank, dist):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    stream = torch.cuda.current_stream(dev)
+    # ONE explicit stream for the flush, the CUDA events and the library (torch's default
+    # stream has handle 0, which the C ABI treats as "create your own": events on it would
+    # not order with the library's work)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    assert stream.cuda_stream != 0
     ctx = F.Context(local_rank, stream=stream.cuda_stream, precision="bf16")
     cfg = F.FwaConfig()
     blob = F.init_backbone_params(cfg, 42)
@@ -222,6 +227,7 @@ def run_ours(args, rank, world, local_rank, dist):
     # headline: no stage events between kernels (they would serialise the programmatic
     # dependent launches); the stage-timed pass right after gives the per-kernel split
     dev_ms, launches, _ = timed_loop(False)
+    ctx.sync_check()
     prof_ms, _, prof = timed_loop(True)
     # ---------------------------------------------------------------- e2e via the host API
     pin = dict(pin_memory=True)

@@ -92,6 +92,13 @@ const char* fwa_b200_last_error(const fwa_b200_ctx* ctx);
 int fwa_b200_set_precision(fwa_b200_ctx* ctx, int precision);
 /* Number of CUDA kernels this context has launched so far (telemetry). */
 int64_t fwa_b200_kernel_launches(const fwa_b200_ctx* ctx);
+/* Synchronise the context stream and report deferred device-side conditions of the
+ * last device-resident forward (fwa_b200_backbone_forward_device enqueues without a
+ * host round trip): FWA_ERR_NUMERIC for non-finite inputs (kernels.hpp:460-461),
+ * FWA_ERR_INTERNAL if the frame set's window range exceeded the fixed-capacity bin
+ * histogram (re-run through fwa_b200_backbone_forward, which falls back automatically). */
+int fwa_b200_sync_check(fwa_b200_ctx* ctx);
+
 /* Stage timers on the context stream (CUDA events), the analogue of the
  * reference's StageTimer/StageTimes (backbone.hpp:109-151).  Enabling resets the
  * accumulators; fwa_b200_get_profile synchronises the stream and returns the

@@ -32,7 +32,7 @@ LIB_PATH = os.path.join(HERE, "libfwa_b200.so")
 EXPORTS = [
     "fwa_b200_ctx_create", "fwa_b200_ctx_destroy", "fwa_b200_last_error", "fwa_b200_set_precision",
     "fwa_b200_kernel_launches", "fwa_b200_fast_path", "fwa_b200_load_params",
-    "fwa_b200_set_profiling", "fwa_b200_get_profile",
+    "fwa_b200_set_profiling", "fwa_b200_get_profile", "fwa_b200_sync_check",
     "fwa_b200_backbone_forward", "fwa_b200_backbone_forward_batch",
     "fwa_b200_backbone_forward_device", "fwa_b200_sort_plan", "fwa_b200_block_forward",
     "fwa_b200_positional_embedding", "fwa_b200_generate_pillars", "fwa_b200_init_params",
@@ -120,6 +120,7 @@ def lib():
         L.fwa_b200_kernel_launches.restype = i64
         L.fwa_b200_fast_path.argtypes = [vp, C.POINTER(_Cfg)]
         L.fwa_b200_set_profiling.argtypes = [vp, C.c_int]
+        L.fwa_b200_sync_check.argtypes = [vp]
         L.fwa_b200_get_profile.argtypes = [vp, vp, vp]
         L.fwa_b200_load_params.argtypes = [vp, C.POINTER(_Cfg), vp, C.c_size_t]
         L.fwa_b200_backbone_forward.argtypes = [vp, vp, vp, C.c_int, i64, C.POINTER(_Cfg),
@@ -394,6 +395,10 @@ class Context:
             self._h, C.c_void_p(d_coords), C.c_void_p(d_feats), _ptr(off), len(off) - 1,
             C.byref(c), C.c_void_p(d_out), C.c_void_p(d_kept) if d_kept else None, C.byref(nk)))
         return int(nk.value)
+
+    def sync_check(self):
+        """Wait for the stream; raise deferred device-side errors of forward_device."""
+        self._check(lib().fwa_b200_sync_check(self._h))
 
     def sort(self, coords: np.ndarray, spec: WindowSpec) -> np.ndarray:
         coords = np.ascontiguousarray(coords, np.float64)

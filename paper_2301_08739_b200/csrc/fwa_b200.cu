@@ -63,8 +63,35 @@ struct fwa_b200_ctx {
     std::map<std::string, DevBuf> ws;
     int freq_d = 0;
     DevBuf freq;
-    int* d_flag = nullptr;     // non-finite input flag
-    int* h_flag = nullptr;     // pinned
+    cudaStream_t side = nullptr;             // PE overlaps the schedule's host round trip
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    int* d_flag = nullptr;     // [0] non-finite input, [1] window-bin capacity overflow
+    int* h_flag = nullptr;     // pinned, 2 ints
+    bool exact_bins = false;   // set for one call after an overflow: host-sized bins
+    uint64_t ws_epoch = 0;     // bumped whenever a workspace buffer moves
+    uint64_t params_version = 0;
+    // CUDA graph of the device-resident forward (replayed while its key is unchanged)
+    struct GraphKey {
+        const void *coords = nullptr, *feats = nullptr, *out = nullptr, *kept = nullptr;
+        std::vector<int64_t> off;
+        fwa_config_t cfg{};
+        int precision = -1;
+        uint64_t params_version = 0, ws_epoch = 0;
+        bool operator==(const GraphKey& o) const {
+            return coords == o.coords && feats == o.feats && out == o.out && kept == o.kept && off == o.off &&
+                   std::memcmp(&cfg, &o.cfg, sizeof(cfg)) == 0 && precision == o.precision &&
+                   params_version == o.params_version && ws_epoch == o.ws_epoch;
+        }
+    };
+    GraphKey g_key, g_warm;
+    cudaGraphExec_t g_exec = nullptr;
+    int64_t g_launches = 0;
+    int64_t* g_tab = nullptr;  // frame table owned by the captured graph
+    bool g_disabled = false;
+    int64_t* h_tab = nullptr;  // pinned frame-table staging (2 slots)
+    size_t h_tab_cap = 0;
+    int h_tab_slot = 0;
+    cudaEvent_t ev_tab[2] = {nullptr, nullptr};
     long long* h_minmax = nullptr;  // pinned (16)
     // stage profiling (the analogue of the reference's StageTimer, backbone.hpp:139-151)
     bool profiling = false;
@@ -95,6 +122,7 @@ T* ws(fwa_b200_ctx* c, const char* name, size_t count) {
     DevBuf& b = c->ws[name];
     const size_t bytes = std::max<size_t>(count * sizeof(T), 256);
     if (b.cap < bytes) {
+        ++c->ws_epoch;  // captured graphs hold the old pointers
         if (b.p) cudaFree(b.p);
         b.p = nullptr;
         size_t want = std::max(bytes, b.cap + b.cap / 2);
@@ -347,6 +375,7 @@ struct Schedule {
     int n_frames = 0, n_specs = 0;
     std::vector<int64_t> off, rows, drop, drop_off;
     int32_t* sorted = nullptr;     // n_specs x ntot, full-set plans
+    int32_t* sorted_inv = nullptr; // n_specs x ntot, position of each pillar id in its plan
     int32_t* idx = nullptr;        // n_specs x K, kept-restricted plans
     uint8_t* dropped = nullptr;    // ntot
     uint32_t* kept_rank = nullptr; // ntot
@@ -379,9 +408,14 @@ void host_frames(const int64_t* off, int n_frames, int G, Schedule& S) {
     if (S.ntot > INT32_MAX / 4) throw FwaError{FWA_ERR_SHAPE, "too many pillars for int32 ids"};
 }
 
+constexpr long long kBinCap = 1LL << 22;  // sync-free histogram capacity (window bins)
+
 // K1..K4 for n_specs specs of nf frames: returns the n_specs x ntot full-set plans.
+// Default: fully enqueued (device-side bin ranges, fixed-capacity histogram); an
+// overflow sets d_flag[1] and the caller re-runs with exact = true (one host round trip
+// to size the histogram exactly).
 int32_t* sort_specs(fwa_b200_ctx* c, const double* d_coords, int64_t ntot, int n_specs, double w_x,
-                    double w_y, const int64_t* d_off, int nf) {
+                    double w_y, const int64_t* d_off, int nf, bool exact = true) {
     cudaStream_t st = c->stream;
     const int64_t total = ntot * n_specs;
     long long* win = ws<long long>(c, "win", 2 * static_cast<size_t>(total));
@@ -389,6 +423,30 @@ int32_t* sort_specs(fwa_b200_ctx* c, const double* d_coords, int64_t ntot, int n
     long long* mm = ws<long long>(c, "minmax", 16);
     launch_sort_keys(d_coords, ntot, n_specs, w_x, w_y, win, loc, mm, st, &c->launches);
     check_launch();
+    if (!exact) {
+        SpecBins* d_sb = ws<SpecBins>(c, "specbins", 4);
+        uint32_t* d_nbins = ws<uint32_t>(c, "nbins", 4);
+        uint32_t* hist = ws<uint32_t>(c, "hist", static_cast<size_t>(kBinCap));
+        uint32_t* bin_start = ws<uint32_t>(c, "bin_start", static_cast<size_t>(kBinCap));
+        uint32_t* cursor = ws<uint32_t>(c, "cursor", static_cast<size_t>(kBinCap));
+        uint32_t* tile_sums = ws<uint32_t>(c, "bin_tile_sums", 1024);
+        uint32_t* bin_of = ws<uint32_t>(c, "bin_of", static_cast<size_t>(total));
+        launch_bins_setup(mm, n_specs, nf, kBinCap, d_sb, d_nbins, c->d_flag + 1, st, &c->launches);
+        launch_zero_bins(hist, d_nbins, st, &c->launches);
+        launch_bins_hist(win, ntot, n_specs, d_off, nf, d_sb, bin_of, hist, d_nbins, st, &c->launches);
+        launch_scan_bins_dev(hist, bin_start, cursor, d_nbins, kBinCap, tile_sums, st, &c->launches);
+        int32_t* pre = ws<int32_t>(c, "pre", static_cast<size_t>(total));
+        double* pre_loc = ws<double>(c, "pre_loc", 2 * static_cast<size_t>(total));
+        launch_bin_scatter(bin_of, loc, ntot, n_specs, cursor, pre, pre_loc, d_nbins, st, &c->launches);
+        int32_t* sorted = ws<int32_t>(c, "sorted", static_cast<size_t>(total));
+        int32_t* inv = ws<int32_t>(c, "sorted_inv", static_cast<size_t>(total));
+        int32_t* scratch = ws<int32_t>(c, "sort_scratch", 2 * static_cast<size_t>(total));
+        uint32_t* large = ws<uint32_t>(c, "large_bins", static_cast<size_t>(kBinCap) + 1);
+        launch_bin_sort(bin_start, hist, 0u, pre, pre_loc, loc, ntot, sorted, inv, scratch, large, d_nbins, st,
+                        &c->launches);
+        check_launch();
+        return sorted;
+    }
     CUDA_OK(cudaMemcpyAsync(c->h_minmax, mm, 16 * 8, cudaMemcpyDeviceToHost, st));
     CUDA_OK(cudaStreamSynchronize(st));
     SpecBins sb[4];
@@ -412,22 +470,105 @@ int32_t* sort_specs(fwa_b200_ctx* c, const double* d_coords, int64_t ntot, int n
     uint32_t* scan_tmp = ws<uint32_t>(c, "scan_tmp", scan_tmp_words(std::max<int64_t>(nbins, total)) + 8);
     uint32_t* bin_of = ws<uint32_t>(c, "bin_of", static_cast<size_t>(total));
     CUDA_OK(cudaMemsetAsync(hist, 0, static_cast<size_t>(nbins) * 4, st));
-    launch_bins_hist(win, ntot, n_specs, d_off, nf, d_sb, bin_of, hist, st, &c->launches);
+    launch_bins_hist(win, ntot, n_specs, d_off, nf, d_sb, bin_of, hist, nullptr, st, &c->launches);
     exclusive_scan_u32(hist, bin_start, nbins, scan_tmp, nullptr, st, &c->launches);
     uint32_t* cursor = ws<uint32_t>(c, "cursor", static_cast<size_t>(nbins));
     CUDA_OK(cudaMemcpyAsync(cursor, bin_start, static_cast<size_t>(nbins) * 4, cudaMemcpyDeviceToDevice, st));
     int32_t* pre = ws<int32_t>(c, "pre", static_cast<size_t>(total));
-    launch_bin_scatter(bin_of, ntot, n_specs, cursor, pre, st, &c->launches);
+    double* pre_loc = ws<double>(c, "pre_loc", 2 * static_cast<size_t>(total));
+    launch_bin_scatter(bin_of, loc, ntot, n_specs, cursor, pre, pre_loc, nullptr, st, &c->launches);
     int32_t* sorted = ws<int32_t>(c, "sorted", static_cast<size_t>(total));
+    int32_t* inv = ws<int32_t>(c, "sorted_inv", static_cast<size_t>(total));
     int32_t* scratch = ws<int32_t>(c, "sort_scratch", 2 * static_cast<size_t>(total));
     uint32_t* large = ws<uint32_t>(c, "large_bins", static_cast<size_t>(nbins) + 1);
-    launch_bin_sort(bin_start, hist, static_cast<uint32_t>(nbins), pre, loc, ntot, sorted, scratch,
-                    large, st, &c->launches);
+    launch_bin_sort(bin_start, hist, static_cast<uint32_t>(nbins), pre, pre_loc, loc, ntot, sorted, inv,
+                    scratch, large, nullptr, st, &c->launches);
     check_launch();
     return sorted;
 }
 
-void build_schedule(fwa_b200_ctx* c, const double* d_coords, const fwa_config_t* cfg, Schedule& S) {
+std::vector<int64_t> frame_table(const Schedule& S) {
+    std::vector<int64_t> tab;
+    tab.insert(tab.end(), S.off.begin(), S.off.end());
+    tab.insert(tab.end(), S.rows.begin(), S.rows.end());
+    tab.insert(tab.end(), S.drop_off.begin(), S.drop_off.end() - 1);
+    return tab;
+}
+
+const int64_t* upload_frame_table(fwa_b200_ctx* c, const Schedule& S) {
+    cudaStream_t st = c->stream;
+    const int nf = S.n_frames;
+    int64_t* d_tab = ws<int64_t>(c, "frame_tab", 3 * static_cast<size_t>(nf) + 2);
+    std::vector<int64_t> tab = frame_table(S);
+    // pinned staging so the copy is truly asynchronous (ring: the previous call's copy
+    // may still be pending)
+    if (c->h_tab_cap < tab.size() * 2) {
+        if (c->h_tab) cudaFreeHost(c->h_tab);
+        c->h_tab = nullptr;
+        c->h_tab_cap = std::max<size_t>(tab.size() * 2, 64);
+        CUDA_OK(cudaMallocHost(&c->h_tab, c->h_tab_cap * 8));
+        c->h_tab_slot = 0;
+    }
+    CUDA_OK(cudaStreamSynchronize(c->side));  // previous call's PE done (cheap; usually idle)
+    int64_t* h = c->h_tab + (c->h_tab_slot ^= 1) * (c->h_tab_cap / 2);
+    CUDA_OK(cudaEventSynchronize(c->ev_tab[c->h_tab_slot]));
+    std::copy(tab.begin(), tab.end(), h);
+    CUDA_OK(cudaMemcpyAsync(d_tab, h, tab.size() * 8, cudaMemcpyHostToDevice, st));
+    CUDA_OK(cudaEventRecord(c->ev_tab[c->h_tab_slot], st));
+    return d_tab;
+}
+
+void build_schedule_body(fwa_b200_ctx* c, const double* d_coords, const fwa_config_t* cfg, Schedule& S,
+                         const int64_t* d_off, const int64_t* d_rows, const int64_t* d_drop_off, double w_x,
+                         double w_y, int64_t ntot, int n_specs, int nf) {
+    cudaStream_t st = c->stream;
+
+    const int64_t total = ntot * n_specs;
+    S.sorted = sort_specs(c, d_coords, ntot, n_specs, w_x, w_y, d_off, nf, c->exact_bins);
+    S.sorted_inv = ws<int32_t>(c, "sorted_inv", static_cast<size_t>(total));
+    uint32_t* scan_tmp = ws<uint32_t>(c, "scan_tmp", scan_tmp_words(total) + 8);
+
+    // drops (block 0 = spec 0), kept set
+    S.dropped = ws<uint8_t>(c, "dropped", static_cast<size_t>(ntot));
+    CUDA_OK(cudaMemsetAsync(S.dropped, 0, static_cast<size_t>(ntot), st));
+    S.dropped_ids = ws<int32_t>(c, "dropped_ids", static_cast<size_t>(S.n_drop) + 1);
+    launch_drop_mark(S.sorted, ntot, d_off, d_rows, d_drop_off, nf, S.dropped, S.dropped_ids, st,
+                     &c->launches);
+    S.kept_rank = ws<uint32_t>(c, "kept_rank", static_cast<size_t>(ntot));
+    S.kept_ids = ws<int32_t>(c, "kept_ids", static_cast<size_t>(S.K));
+    S.idx = ws<int32_t>(c, "idx", static_cast<size_t>(S.K) * n_specs);
+    S.out_pos = ws<int32_t>(c, "out_pos", static_cast<size_t>(S.K));
+    const int s_last = (cfg->n_blocks - 1) % 4;
+    if (S.n_drop <= kMaxDropTable) {
+        // few drops (<= G-1 per frame): binary-search compaction, no grid-wide scans
+        const int nd = static_cast<int>(S.n_drop);
+        int32_t* drop_sorted = ws<int32_t>(c, "drop_sorted", static_cast<size_t>(nd) + 1);
+        int32_t* drop_pos = ws<int32_t>(c, "drop_pos", static_cast<size_t>(nd + 1) * n_specs);
+        if (nd > 0)
+            launch_drop_tables(S.dropped_ids, nd, S.sorted_inv, ntot, n_specs, drop_sorted, drop_pos, st,
+                               &c->launches);
+        launch_compact_all(S.sorted, ntot, n_specs, S.dropped, drop_sorted, drop_pos, nd, S.K, s_last, S.idx,
+                           S.kept_rank, S.kept_ids, S.out_pos, st, &c->launches);
+        check_launch();
+        return;
+    }
+    // many drops (huge group sizes x many frames): flag scans
+    uint32_t* flags = ws<uint32_t>(c, "flags", static_cast<size_t>(std::max(total, ntot)));
+    launch_keep_flags(S.dropped, ntot, flags, st, &c->launches);
+    exclusive_scan_u32(flags, S.kept_rank, ntot, scan_tmp, nullptr, st, &c->launches);
+    launch_kept_ids(S.kept_rank, S.dropped, ntot, S.kept_ids, st, &c->launches);
+    launch_spec_keep_flags(S.sorted, total, S.dropped, flags, st, &c->launches);
+    uint32_t* pos = ws<uint32_t>(c, "compact_pos", static_cast<size_t>(total));
+    exclusive_scan_u32(flags, pos, total, scan_tmp, nullptr, st, &c->launches);
+    launch_spec_compact(S.sorted, total, S.dropped, pos, S.idx, st, &c->launches);
+    k_out_pos<<<static_cast<unsigned>((S.K + 255) / 256), 256, 0, st>>>(S.idx + S.K * s_last,
+                                                                       S.kept_rank, S.K, S.out_pos);
+    ++c->launches;
+    check_launch();
+}
+
+void build_schedule(fwa_b200_ctx* c, const double* d_coords, const fwa_config_t* cfg, Schedule& S,
+                    const int64_t* d_tab_fixed = nullptr) {
     cudaStream_t st = c->stream;
     const int64_t ntot = S.ntot;
     const int n_specs = std::min(cfg->n_blocks, 4);
@@ -437,46 +578,13 @@ void build_schedule(fwa_b200_ctx* c, const double* d_coords, const fwa_config_t*
 
     // frame tables
     const int nf = S.n_frames;
-    int64_t* d_tab = ws<int64_t>(c, "frame_tab", 3 * static_cast<size_t>(nf) + 2);
-    std::vector<int64_t> tab;
-    tab.insert(tab.end(), S.off.begin(), S.off.end());
-    tab.insert(tab.end(), S.rows.begin(), S.rows.end());
-    tab.insert(tab.end(), S.drop_off.begin(), S.drop_off.end() - 1);
-    CUDA_OK(cudaMemcpyAsync(d_tab, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, st));
+    const int64_t* d_tab = d_tab_fixed;
+    if (!d_tab) d_tab = upload_frame_table(c, S);
     const int64_t* d_off = d_tab;
     const int64_t* d_rows = d_tab + nf + 1;
     const int64_t* d_drop_off = d_tab + 2 * nf + 1;
-
-    const int64_t total = ntot * n_specs;
-    S.sorted = sort_specs(c, d_coords, ntot, n_specs, w_x, w_y, d_off, nf);
-    uint32_t* scan_tmp = ws<uint32_t>(c, "scan_tmp", scan_tmp_words(total) + 8);
-
-    // drops (block 0 = spec 0), kept set
-    S.dropped = ws<uint8_t>(c, "dropped", static_cast<size_t>(ntot));
-    CUDA_OK(cudaMemsetAsync(S.dropped, 0, static_cast<size_t>(ntot), st));
-    S.dropped_ids = ws<int32_t>(c, "dropped_ids", static_cast<size_t>(S.n_drop) + 1);
-    launch_drop_mark(S.sorted, ntot, d_off, d_rows, d_drop_off, nf, S.dropped, S.dropped_ids, st,
-                     &c->launches);
-    uint32_t* flags = ws<uint32_t>(c, "flags", static_cast<size_t>(std::max(total, ntot)));
-    S.kept_rank = ws<uint32_t>(c, "kept_rank", static_cast<size_t>(ntot));
-    launch_keep_flags(S.dropped, ntot, flags, st, &c->launches);
-    exclusive_scan_u32(flags, S.kept_rank, ntot, scan_tmp, nullptr, st, &c->launches);
-    S.kept_ids = ws<int32_t>(c, "kept_ids", static_cast<size_t>(S.K));
-    launch_kept_ids(S.kept_rank, S.dropped, ntot, S.kept_ids, st, &c->launches);
-
-    // kept-restricted plans for every spec
-    launch_spec_keep_flags(S.sorted, total, S.dropped, flags, st, &c->launches);
-    uint32_t* pos = ws<uint32_t>(c, "compact_pos", static_cast<size_t>(total));
-    exclusive_scan_u32(flags, pos, total, scan_tmp, nullptr, st, &c->launches);
-    S.idx = ws<int32_t>(c, "idx", static_cast<size_t>(S.K) * n_specs);
-    launch_spec_compact(S.sorted, total, S.dropped, pos, S.idx, st, &c->launches);
-
-    const int s_last = (cfg->n_blocks - 1) % 4;
-    S.out_pos = ws<int32_t>(c, "out_pos", static_cast<size_t>(S.K));
-    k_out_pos<<<static_cast<unsigned>((S.K + 255) / 256), 256, 0, st>>>(S.idx + S.K * s_last,
-                                                                       S.kept_rank, S.K, S.out_pos);
-    ++c->launches;
-    check_launch();
+    (void)st;
+    build_schedule_body(c, d_coords, cfg, S, d_off, d_rows, d_drop_off, w_x, w_y, ntot, n_specs, nf);
 }
 
 // Reference plan-cache rule (backbone.hpp:224-234, 285-316) for a frame of n
@@ -597,24 +705,27 @@ void require_params(fwa_b200_ctx* c, const fwa_config_t* cfg) {
 // (K x d, active order) and, optionally, d_kept.
 void forward_device(fwa_b200_ctx* c, const double* d_coords, const float* d_feats,
                     const double* d_feats64, const fwa_config_t* cfg, Schedule& S, float* d_out,
-                    int32_t* d_kept) {
+                    int32_t* d_kept, const int64_t* d_tab_fixed = nullptr) {
     cudaStream_t st = c->stream;
     const int d = cfg->d_model;
-    {
-        StageEv t(c, FWA_PROF_SCHEDULE);
-        build_schedule(c, d_coords, cfg, S);
-    }
+    CUDA_OK(cudaMemsetAsync(c->d_flag, 0, 2 * sizeof(int), st));
     const bool fast = fast_path_ok(c, d, cfg->n_heads, cfg->d_ff, cfg->group_size);
     // fast path: fp16 PE rows (|PE| <= 1, abs err <= 2^-12, below the bf16 rounding of
-    // LN1 + PE that follows); check mode: fp32 rows
+    // LN1 + PE that follows); check mode: fp32 rows.  PE depends only on coordinates:
+    // it runs on a side stream, overlapping the schedule (and its host round trip).
     float* pe = fast ? nullptr : ws<float>(c, "pe", static_cast<size_t>(S.ntot) * d);
     __half* pe16 = fast ? ws<__half>(c, "pe16", static_cast<size_t>(S.ntot) * d) : nullptr;
+    const double* freq = pe_freq(c, d);
+    CUDA_OK(cudaEventRecord(c->ev_fork, st));
+    CUDA_OK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    launch_positional_embedding(d_coords, S.ntot, d, freq, pe, pe16, c->side, &c->launches);
+    CUDA_OK(cudaEventRecord(c->ev_join, c->side));
     {
-        StageEv t(c, FWA_PROF_PE);
-        launch_positional_embedding(d_coords, S.ntot, d, pe_freq(c, d), pe, pe16, st, &c->launches);
+        StageEv t(c, FWA_PROF_SCHEDULE);
+        build_schedule(c, d_coords, cfg, S, d_tab_fixed);
     }
+    CUDA_OK(cudaStreamWaitEvent(st, c->ev_join, 0));
     float* X = ws<float>(c, "X", static_cast<size_t>(S.ntot) * d);
-    CUDA_OK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), st));
     for (int b = 0; b < cfg->n_blocks; ++b) {
         const int s = b % 4;
         const int32_t* idx = S.idx + S.K * s;
@@ -696,10 +807,19 @@ void forward_host(fwa_b200_ctx* c, const double* coords, const void* feats, int 
         CUDA_OK(cudaMemcpyAsync(h_idx.data(), S.idx, h_idx.size() * 4, cudaMemcpyDeviceToHost, st));
         CUDA_OK(cudaMemcpyAsync(h_rank.data(), S.kept_rank, h_rank.size() * 4, cudaMemcpyDeviceToHost, st));
     }
-    CUDA_OK(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaMemcpyAsync(c->h_flag, c->d_flag, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
     delete d2h;
     CUDA_OK(cudaStreamSynchronize(st));
-    if (*c->h_flag) throw FwaError{FWA_ERR_NUMERIC, "group_attention: non-finite input"};
+    if (c->h_flag[1]) {  // window-bin capacity overflow: redo with host-sized bins
+        c->exact_bins = true;
+        struct Reset {
+            fwa_b200_ctx* c;
+            ~Reset() { c->exact_bins = false; }
+        } reset{c};
+        forward_host(c, coords, feats, f64, off, n_frames, cfg, out, kept_per_frame);
+        return;
+    }
+    if (c->h_flag[0]) throw FwaError{FWA_ERR_NUMERIC, "group_attention: non-finite input"};
     out->n_kept = S.K;
     std::vector<int64_t> drops;
     cache_stats(cfg->n_blocks, S.off[1] - S.off[0], cfg->group_size, &out->cache_computed,
@@ -747,8 +867,13 @@ int fwa_b200_ctx_create(int device, void* stream, fwa_b200_ctx** out) {
             CUDA_OK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
             c->own_stream = true;
         }
-        CUDA_OK(cudaMalloc(&c->d_flag, sizeof(int)));
-        CUDA_OK(cudaMallocHost(&c->h_flag, sizeof(int)));
+        CUDA_OK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+        CUDA_OK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+        CUDA_OK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+        CUDA_OK(cudaEventCreateWithFlags(&c->ev_tab[0], cudaEventDisableTiming));
+        CUDA_OK(cudaEventCreateWithFlags(&c->ev_tab[1], cudaEventDisableTiming));
+        CUDA_OK(cudaMalloc(&c->d_flag, 2 * sizeof(int)));
+        CUDA_OK(cudaMallocHost(&c->h_flag, 2 * sizeof(int)));
         CUDA_OK(cudaMallocHost(&c->h_minmax, 16 * sizeof(long long)));
     });
     if (rc != FWA_OK) {
@@ -774,6 +899,17 @@ void fwa_b200_ctx_destroy(fwa_b200_ctx* c) {
     if (c->h_flag) cudaFreeHost(c->h_flag);
     if (c->h_minmax) cudaFreeHost(c->h_minmax);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
+    if (c->g_exec) cudaGraphExecDestroy(c->g_exec);
+    if (c->g_tab) cudaFree(c->g_tab);
+    if (c->side) {
+        cudaStreamSynchronize(c->side);
+        cudaStreamDestroy(c->side);
+    }
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    for (auto e : c->ev_tab)
+        if (e) cudaEventDestroy(e);
+    if (c->h_tab) cudaFreeHost(c->h_tab);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -799,6 +935,16 @@ int fwa_b200_debug_trace(fwa_b200_ctx* c, unsigned long long* out) {
         if (it == c->ws.end() || !it->second.p) throw FwaError{FWA_ERR_CONTRACT, "no trace (FWA_B200_TRACE=1)"};
         CUDA_OK(cudaStreamSynchronize(c->stream));
         CUDA_OK(cudaMemcpy(out, it->second.p, 2 * 148 * 64 * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+int fwa_b200_sync_check(fwa_b200_ctx* c) {
+    return guarded(c, [&] {
+        CUDA_OK(cudaMemcpyAsync(c->h_flag, c->d_flag, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        CUDA_OK(cudaStreamSynchronize(c->stream));
+        if (c->h_flag[1])
+            throw FwaError{FWA_ERR_INTERNAL, "window-bin capacity exceeded: re-run through the host API"};
+        if (c->h_flag[0]) throw FwaError{FWA_ERR_NUMERIC, "group_attention: non-finite input"};
     });
 }
 
@@ -841,6 +987,7 @@ int fwa_b200_load_params(fwa_b200_ctx* c, const fwa_config_t* cfg, const void* b
             if (r.d != cfg->d_model || r.h != cfg->n_heads || r.dff != cfg->d_ff)
                 throw FwaError{FWA_ERR_CONFIG, "backbone: block params disagree with config"};
         c->blocks = upload_block_params(recs, c->params_f32, c->params_bf16, c->stream);
+        ++c->params_version;
         c->pcfg = *cfg;
         c->have_params = true;
     });
@@ -876,8 +1023,73 @@ int fwa_b200_backbone_forward_device(fwa_b200_ctx* c, const double* d_coords, co
         if (!frame_offsets || n_frames < 1) throw FwaError{FWA_ERR_SHAPE, "need frame offsets"};
         Schedule S;
         host_frames(frame_offsets, n_frames, cfg->group_size, S);
-        forward_device(c, d_coords, d_feats, nullptr, cfg, S, d_out, d_kept);
         if (n_kept_out) *n_kept_out = S.K;
+        // CUDA graph: a repeated call (same buffers, frames, config, params, workspace)
+        // replays the captured launch sequence — no per-kernel host launch cost.
+        static const bool no_graph = [] {
+            const char* v = std::getenv("FWA_B200_NO_GRAPH");
+            return v && v[0] == '1';
+        }();
+        fwa_b200_ctx::GraphKey key;
+        key.coords = d_coords;
+        key.feats = d_feats;
+        key.out = d_out;
+        key.kept = d_kept;
+        key.off.assign(frame_offsets, frame_offsets + n_frames + 1);
+        key.cfg = *cfg;
+        key.precision = c->precision;
+        key.params_version = c->params_version;
+        key.ws_epoch = c->ws_epoch;
+        if (no_graph || c->g_disabled || c->profiling || c->exact_bins) {
+            forward_device(c, d_coords, d_feats, nullptr, cfg, S, d_out, d_kept);
+            return;
+        }
+        if (c->g_exec && c->g_key == key) {
+            CUDA_OK(cudaGraphLaunch(c->g_exec, c->stream));
+            c->launches += c->g_launches;
+            return;
+        }
+        if (!(c->g_warm == key)) {  // first sighting: run eagerly (sizes the workspace)
+            forward_device(c, d_coords, d_feats, nullptr, cfg, S, d_out, d_kept);
+            c->g_warm = key;
+            c->g_warm.ws_epoch = c->ws_epoch;
+            return;
+        }
+        // second sighting: capture
+        const std::vector<int64_t> tab = frame_table(S);
+        if (c->g_tab) cudaFree(c->g_tab);
+        c->g_tab = nullptr;
+        CUDA_OK(cudaMalloc(&c->g_tab, tab.size() * 8));
+        CUDA_OK(cudaMemcpy(c->g_tab, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice));
+        CUDA_OK(cudaStreamSynchronize(c->stream));
+        const int64_t l0 = c->launches;
+        cudaGraph_t graph = nullptr;
+        CUDA_OK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        try {
+            forward_device(c, d_coords, d_feats, nullptr, cfg, S, d_out, d_kept, c->g_tab);
+        } catch (...) {
+            cudaStreamEndCapture(c->stream, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            cudaGetLastError();
+            c->g_disabled = true;
+            throw;
+        }
+        const cudaError_t ec = cudaStreamEndCapture(c->stream, &graph);
+        cudaGraphExec_t exec = nullptr;
+        if (ec != cudaSuccess || !graph || cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+            if (graph) cudaGraphDestroy(graph);
+            cudaGetLastError();
+            c->g_disabled = true;  // not capturable here: stay eager
+            forward_device(c, d_coords, d_feats, nullptr, cfg, S, d_out, d_kept);
+            return;
+        }
+        cudaGraphDestroy(graph);
+        if (c->g_exec) cudaGraphExecDestroy(c->g_exec);
+        c->g_exec = exec;
+        c->g_launches = c->launches - l0;
+        c->g_key = key;
+        c->g_key.ws_epoch = c->ws_epoch;
+        CUDA_OK(cudaGraphLaunch(c->g_exec, c->stream));
     });
 }
 
@@ -931,7 +1143,7 @@ int fwa_b200_block_forward(fwa_b200_ctx* c, const float* f, const float* pe, int
         float* dout = ws<float>(c, "bf_out", static_cast<size_t>(rows) * d);
         CUDA_OK(cudaMemcpyAsync(df, f, static_cast<size_t>(rows) * d * 4, cudaMemcpyHostToDevice, st));
         CUDA_OK(cudaMemcpyAsync(dpe, pe, static_cast<size_t>(rows) * d * 4, cudaMemcpyHostToDevice, st));
-        CUDA_OK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), st));
+        CUDA_OK(cudaMemsetAsync(c->d_flag, 0, 2 * sizeof(int), st));
         const bool fast = fast_path_ok(c, d, r.h, r.dff, cfg.group_size);
         __half* dpe16 = nullptr;
         if (fast) {

@@ -33,15 +33,31 @@ struct SpecBins {
 void launch_sort_keys(const double* coords, int64_t ntot, int n_specs, double w_x, double w_y,
                       long long* win, double* loc, long long* minmax, cudaStream_t s,
                       int64_t* launches);
+// d_nbins (may be null): device-side bin count of the sync-free path; 0 disables
 void launch_bins_hist(const long long* win, int64_t ntot, int n_specs, const int64_t* d_frame_off,
                       int n_frames, const SpecBins* d_specs, uint32_t* bin_of, uint32_t* hist,
-                      cudaStream_t s, int64_t* launches);
-void launch_bin_scatter(const uint32_t* bin_of, int64_t ntot, int n_specs, uint32_t* cursor,
-                        int32_t* pre, cudaStream_t s, int64_t* launches);
+                      const uint32_t* d_nbins, cudaStream_t s, int64_t* launches);
+void launch_bins_setup(const long long* mm, int n_specs, int nf, long long cap, SpecBins* specs,
+                       uint32_t* d_nbins, int* overflow, cudaStream_t s, int64_t* launches);
+void launch_zero_bins(uint32_t* hist, const uint32_t* d_nbins, cudaStream_t s, int64_t* launches);
+void launch_scan_bins_dev(const uint32_t* hist, uint32_t* bin_start, uint32_t* cursor, const uint32_t* d_nbins,
+                          long long cap, uint32_t* tile_sums, cudaStream_t s, int64_t* launches);
+void launch_bin_scatter(const uint32_t* bin_of, const double* loc, int64_t ntot, int n_specs,
+                        uint32_t* cursor, int32_t* pre, double* pre_loc, const uint32_t* d_nbins,
+                        cudaStream_t s, int64_t* launches);
+// also writes the inverse permutation inv[s*ntot + id] = position in sorted
 void launch_bin_sort(const uint32_t* bin_start, const uint32_t* hist, uint32_t n_bins,
-                     const int32_t* pre, const double* loc, int64_t ntot, int32_t* sorted,
-                     int32_t* scratch, uint32_t* large /* 1 + n_bins words */, cudaStream_t s,
+                     const int32_t* pre, const double* pre_loc, const double* loc, int64_t ntot,
+                     int32_t* sorted, int32_t* inv, int32_t* scratch,
+                     uint32_t* large /* 1 + n_bins words */, const uint32_t* d_nbins, cudaStream_t s,
                      int64_t* launches);
+constexpr int kMaxDropTable = 8192;
+void launch_drop_tables(const int32_t* dropped_ids, int n, const int32_t* inv, int64_t ntot, int n_specs,
+                        int32_t* drop_sorted, int32_t* drop_pos, cudaStream_t s, int64_t* launches);
+void launch_compact_all(const int32_t* sorted, int64_t ntot, int n_specs, const uint8_t* dropped,
+                        const int32_t* drop_sorted, const int32_t* drop_pos, int n_drop, int64_t K,
+                        int s_last, int32_t* idx, uint32_t* kept_rank, int32_t* kept_ids, int32_t* out_pos,
+                        cudaStream_t s, int64_t* launches);
 
 // ------------------------------------------------------------------ schedule (backbone.hpp:236-316)
 void launch_drop_mark(const int32_t* sorted0, int64_t ntot, const int64_t* d_frame_off,

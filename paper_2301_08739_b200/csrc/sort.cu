@@ -221,10 +221,12 @@ __global__ void __launch_bounds__(256) k_bins_hist(const long long* __restrict__
                                                    const int64_t* __restrict__ frame_off,
                                                    int n_frames, const SpecBins* __restrict__ specs,
                                                    uint32_t* __restrict__ bin_of,
-                                                   uint32_t* __restrict__ hist) {
+                                                   uint32_t* __restrict__ hist,
+                                                   const uint32_t* __restrict__ d_nbins) {
     const int s = blockIdx.y;
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= ntot) return;
+    if (d_nbins && *d_nbins == 0u) return;  // bin capacity overflow: host falls back
     const SpecBins sb = specs[s];
     const int64_t e = static_cast<int64_t>(s) * ntot + i;
     const longlong2 w = reinterpret_cast<const longlong2*>(win)[e];
@@ -237,29 +239,35 @@ __global__ void __launch_bounds__(256) k_bins_hist(const long long* __restrict__
 
 void launch_bins_hist(const long long* win, int64_t ntot, int n_specs, const int64_t* d_frame_off,
                       int n_frames, const SpecBins* d_specs, uint32_t* bin_of, uint32_t* hist,
-                      cudaStream_t s, int64_t* launches) {
+                      const uint32_t* d_nbins, cudaStream_t s, int64_t* launches) {
     dim3 grid(static_cast<unsigned>((ntot + 255) / 256), static_cast<unsigned>(n_specs));
-    k_bins_hist<<<grid, 256, 0, s>>>(win, ntot, d_frame_off, n_frames, d_specs, bin_of, hist);
+    k_bins_hist<<<grid, 256, 0, s>>>(win, ntot, d_frame_off, n_frames, d_specs, bin_of, hist, d_nbins);
     ++*launches;
 }
 
 // ------------------------------------------------------------------ K3 scatter into bins
 
 __global__ void __launch_bounds__(256) k_bin_scatter(const uint32_t* __restrict__ bin_of,
-                                                     int64_t total, int64_t ntot,
-                                                     uint32_t* __restrict__ cursor,
-                                                     int32_t* __restrict__ pre) {
+                                                     const double* __restrict__ loc, int64_t total,
+                                                     int64_t ntot, uint32_t* __restrict__ cursor,
+                                                     int32_t* __restrict__ pre,
+                                                     double* __restrict__ pre_loc,
+                                                     const uint32_t* __restrict__ d_nbins) {
     const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (e >= total) return;
+    if (d_nbins && *d_nbins == 0u) return;
     const uint32_t pos = atomicAdd(cursor + bin_of[e], 1u);
     pre[pos] = static_cast<int32_t>(e % ntot);
+    // the window-local keys travel with the id: the per-bin sort reads them contiguously
+    reinterpret_cast<double2*>(pre_loc)[pos] = reinterpret_cast<const double2*>(loc)[e];
 }
 
-void launch_bin_scatter(const uint32_t* bin_of, int64_t ntot, int n_specs, uint32_t* cursor,
-                        int32_t* pre, cudaStream_t s, int64_t* launches) {
+void launch_bin_scatter(const uint32_t* bin_of, const double* loc, int64_t ntot, int n_specs,
+                        uint32_t* cursor, int32_t* pre, double* pre_loc, const uint32_t* d_nbins,
+                        cudaStream_t s, int64_t* launches) {
     const int64_t total = ntot * n_specs;
-    k_bin_scatter<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(bin_of, total, ntot,
-                                                                           cursor, pre);
+    k_bin_scatter<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(bin_of, loc, total, ntot,
+                                                                           cursor, pre, pre_loc, d_nbins);
     ++*launches;
 }
 
@@ -276,16 +284,13 @@ constexpr int kWarpBin = 128;   // bins up to this size: one warp, shared memory
 constexpr int kCtaBin = 4096;   // up to this: one CTA, shared-memory rank sort
 constexpr int kBinWarps = 8;
 
-__global__ void __launch_bounds__(kBinWarps * 32) k_bin_sort_small(
-    const uint32_t* __restrict__ bin_start, const uint32_t* __restrict__ hist, uint32_t n_bins,
-    const int32_t* __restrict__ pre, const double* __restrict__ loc, int64_t ntot,
-    int32_t* __restrict__ sorted, uint32_t* __restrict__ large) {
-    __shared__ double s_a[kBinWarps][kWarpBin];
-    __shared__ double s_b[kBinWarps][kWarpBin];
-    __shared__ int s_i[kBinWarps][kWarpBin];
-    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t bin = blockIdx.x * kBinWarps + wid;
-    if (bin >= n_bins) return;
+// One warp sorts one window bin (<= kWarpBin points) by rank counting in shared memory;
+// bigger bins are queued for k_bin_sort_large.  Writes sorted[] and the inverse inv[].
+FWA_DEVINL void sort_one_small_bin(uint32_t bin, const uint32_t* __restrict__ bin_start,
+                                   const uint32_t* __restrict__ hist, const int32_t* __restrict__ pre,
+                                   const double* __restrict__ ploc, int64_t ntot, int32_t* __restrict__ sorted,
+                                   int32_t* __restrict__ inv, uint32_t* __restrict__ large, double* sa,
+                                   double* sb, int* si, int lane) {
     const int n = static_cast<int>(hist[bin]);
     if (n > kWarpBin) {  // queue for the CTA-level kernel; large[0] = count
         if (lane == 0) large[1 + atomicAdd(large, 1u)] = bin;
@@ -295,31 +300,51 @@ __global__ void __launch_bounds__(kBinWarps * 32) k_bin_sort_small(
     const uint32_t start = bin_start[bin];
     const int64_t spec_base = (static_cast<int64_t>(start) / ntot) * ntot;
     if (n == 1) {
-        if (lane == 0) sorted[start] = pre[start];
+        if (lane == 0) {
+            const int id = pre[start];
+            sorted[start] = id;
+            inv[spec_base + id] = static_cast<int32_t>(start);
+        }
         return;
     }
     for (int k = lane; k < n; k += 32) {
-        const int id = pre[start + k];
-        const double2 l = reinterpret_cast<const double2*>(loc)[spec_base + id];
-        s_a[wid][k] = l.x;
-        s_b[wid][k] = l.y;
-        s_i[wid][k] = id;
+        const double2 l = reinterpret_cast<const double2*>(ploc)[start + k];
+        sa[k] = l.x;
+        sb[k] = l.y;
+        si[k] = pre[start + k];
     }
     __syncwarp();
     for (int k = lane; k < n; k += 32) {
-        const double a = s_a[wid][k], b = s_b[wid][k];
-        const int id = s_i[wid][k];
+        const double a = sa[k], b = sb[k];
+        const int id = si[k];
         int rank = 0;
-        for (int j = 0; j < n; ++j) rank += loc_less(s_a[wid][j], s_b[wid][j], s_i[wid][j], a, b, id);
+        for (int j = 0; j < n; ++j) rank += loc_less(sa[j], sb[j], si[j], a, b, id);
         sorted[start + rank] = id;
+        inv[spec_base + id] = static_cast<int32_t>(start + rank);
     }
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(kBinWarps * 32) k_bin_sort_small(
+    const uint32_t* __restrict__ bin_start, const uint32_t* __restrict__ hist, uint32_t n_bins,
+    const int32_t* __restrict__ pre, const double* __restrict__ ploc, int64_t ntot,
+    int32_t* __restrict__ sorted, int32_t* __restrict__ inv, uint32_t* __restrict__ large,
+    const uint32_t* __restrict__ d_nbins) {
+    __shared__ double s_a[kBinWarps][kWarpBin];
+    __shared__ double s_b[kBinWarps][kWarpBin];
+    __shared__ int s_i[kBinWarps][kWarpBin];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (d_nbins) n_bins = *d_nbins;  // sync-free path: grid-stride over the device-side count
+    for (uint32_t bin = blockIdx.x * kBinWarps + wid; bin < n_bins; bin += gridDim.x * kBinWarps)
+        sort_one_small_bin(bin, bin_start, hist, pre, ploc, ntot, sorted, inv, large, s_a[wid], s_b[wid],
+                           s_i[wid], lane);
 }
 
 __global__ void __launch_bounds__(512) k_bin_sort_large(
     const uint32_t* __restrict__ bin_start, const uint32_t* __restrict__ hist,
     const uint32_t* __restrict__ large, const int32_t* __restrict__ pre,
     const double* __restrict__ loc, int64_t ntot, int32_t* __restrict__ sorted,
-    int32_t* __restrict__ scratch) {
+    int32_t* __restrict__ inv, int32_t* __restrict__ scratch) {
     extern __shared__ unsigned char smem_raw[];
     double* s_a = reinterpret_cast<double*>(smem_raw);
     double* s_b = s_a + kCtaBin;
@@ -346,6 +371,7 @@ __global__ void __launch_bounds__(512) k_bin_sort_large(
                 int rank = 0;
                 for (int j = 0; j < n; ++j) rank += loc_less(s_a[j], s_b[j], s_i[j], a, b, id);
                 sorted[start + rank] = id;
+                inv[spec_base + id] = static_cast<int32_t>(start + rank);
             }
             __syncthreads();
         } else {
@@ -379,26 +405,31 @@ __global__ void __launch_bounds__(512) k_bin_sort_large(
                     __syncthreads();
                 }
             }
-            for (int k = threadIdx.x; k < n; k += blockDim.x) sorted[start + k] = v[k];
+            for (int k = threadIdx.x; k < n; k += blockDim.x) {
+                sorted[start + k] = v[k];
+                inv[spec_base + v[k]] = static_cast<int32_t>(start + k);
+            }
             __syncthreads();
         }
     }
 }
 
 void launch_bin_sort(const uint32_t* bin_start, const uint32_t* hist, uint32_t n_bins,
-                     const int32_t* pre, const double* loc, int64_t ntot, int32_t* sorted,
-                     int32_t* scratch, uint32_t* large, cudaStream_t s, int64_t* launches) {
-    const unsigned grid = (n_bins + kBinWarps - 1) / kBinWarps;
+                     const int32_t* pre, const double* pre_loc, const double* loc, int64_t ntot,
+                     int32_t* sorted, int32_t* inv, int32_t* scratch, uint32_t* large,
+                     const uint32_t* d_nbins, cudaStream_t s, int64_t* launches) {
+    // host-known n_bins: one warp per bin; device-side count: grid-stride
+    const unsigned grid = d_nbins ? kNumSMs * 16 : (n_bins + kBinWarps - 1) / kBinWarps;
     cudaMemsetAsync(large, 0, sizeof(uint32_t), s);
-    k_bin_sort_small<<<grid, kBinWarps * 32, 0, s>>>(bin_start, hist, n_bins, pre, loc, ntot,
-                                                     sorted, large);
+    k_bin_sort_small<<<grid, kBinWarps * 32, 0, s>>>(bin_start, hist, n_bins, pre, pre_loc, ntot,
+                                                     sorted, inv, large, d_nbins);
     static bool attr_set = false;
     const int smem = kCtaBin * (8 + 8 + 4);
     if (!attr_set) {
         cudaFuncSetAttribute(k_bin_sort_large, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr_set = true;
     }
-    k_bin_sort_large<<<kNumSMs, 512, smem, s>>>(bin_start, hist, large, pre, loc, ntot, sorted,
+    k_bin_sort_large<<<kNumSMs, 512, smem, s>>>(bin_start, hist, large, pre, loc, ntot, sorted, inv,
                                                 scratch);
     *launches += 2;
 }
@@ -487,6 +518,257 @@ void launch_spec_compact(const int32_t* sorted, int64_t total, const uint8_t* dr
     k_spec_compact<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(sorted, total,
                                                                             dropped, pos, idx);
     ++*launches;
+}
+
+
+// ------------------------------------------------------------------ small-drop schedule (no scans)
+//
+// Block 0 drops at most G-1 pillars per frame.  With the dropped ids sorted ascending
+// and, per spec, their positions in that spec's full-set plan sorted ascending, every
+// compaction index is a binary search instead of a grid-wide scan:
+//   kept_rank(id)        = id - #{dropped ids < id}
+//   compact position(j)  = j  - #{dropped positions < j}   (per spec)
+
+FWA_DEVINL int count_less(const int32_t* a, int n, int32_t v) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] < v) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// One CTA: sort the dropped ids, then (per spec) the positions of those ids in the
+// spec's full-set plan (inv[s][id]).  Bitonic sort in shared memory, n <= kMaxDrop.
+constexpr int kMaxDrop = 8192;
+
+__global__ void __launch_bounds__(1024) k_drop_tables(const int32_t* __restrict__ dropped_ids, int n,
+                                                      const int32_t* __restrict__ inv, int64_t ntot,
+                                                      int n_specs, int32_t* __restrict__ drop_sorted,
+                                                      int32_t* __restrict__ drop_pos) {
+    __shared__ int32_t v[kMaxDrop];
+    int P = 1;
+    while (P < n) P <<= 1;
+    {  // one CTA per table: blockIdx.x 0 = dropped ids, 1 + s = positions in spec s
+        const int pass = static_cast<int>(blockIdx.x) - 1;
+        for (int k = threadIdx.x; k < P; k += blockDim.x) {
+            int32_t x = INT32_MAX;
+            if (k < n) {
+                const int32_t id = dropped_ids[k];
+                x = pass < 0 ? id : inv[static_cast<int64_t>(pass) * ntot + id];
+            }
+            v[k] = x;
+        }
+        __syncthreads();
+        for (int size = 2; size <= P; size <<= 1)
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int t = threadIdx.x; t < P / 2; t += blockDim.x) {
+                    const int lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
+                    const bool up = (lo & size) == 0;
+                    const int32_t a = v[lo], b = v[hi];
+                    if ((b < a) == up) {
+                        v[lo] = b;
+                        v[hi] = a;
+                    }
+                }
+                __syncthreads();
+            }
+        int32_t* dst = pass < 0 ? drop_sorted : drop_pos + static_cast<int64_t>(pass) * (n > 0 ? n : 1);
+        for (int k = threadIdx.x; k < n; k += blockDim.x) dst[k] = v[k];
+    }
+}
+
+// Grid over n_specs * ntot plan entries + ntot pillar ids:
+//   plan entry (s, j): kept id -> idx[s][j - #drop_pos[s] < j]; for the last block's
+//   spec also out_pos[that] = kept_rank(id)
+//   pillar id i: kept_rank[i] = i - #drop_sorted < i; kept_ids[kept_rank] = i
+__global__ void k_compact_all(const int32_t* __restrict__ sorted, int64_t ntot, int n_specs,
+                              const uint8_t* __restrict__ dropped, const int32_t* __restrict__ drop_sorted,
+                              const int32_t* __restrict__ drop_pos, int n_drop, int64_t K, int s_last,
+                              int32_t* __restrict__ idx, uint32_t* __restrict__ kept_rank,
+                              int32_t* __restrict__ kept_ids, int32_t* __restrict__ out_pos) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t total = ntot * n_specs;
+    if (t < total) {
+        const int s = static_cast<int>(t / ntot);
+        const int32_t id = sorted[t];
+        if (dropped[id]) return;
+        const int64_t j = t - static_cast<int64_t>(s) * ntot;
+        const int64_t c = j - count_less(drop_pos + static_cast<int64_t>(s) * (n_drop > 0 ? n_drop : 1), n_drop,
+                                         static_cast<int32_t>(t));
+        idx[static_cast<int64_t>(s) * K + c] = id;
+        if (s == s_last) out_pos[c] = id - count_less(drop_sorted, n_drop, id);
+    } else if (t < total + ntot) {
+        const int32_t i = static_cast<int32_t>(t - total);
+        if (dropped[i]) return;
+        const int32_t r = i - count_less(drop_sorted, n_drop, i);
+        kept_rank[i] = static_cast<uint32_t>(r);
+        kept_ids[r] = i;
+    }
+}
+
+void launch_drop_tables(const int32_t* dropped_ids, int n, const int32_t* inv, int64_t ntot, int n_specs,
+                        int32_t* drop_sorted, int32_t* drop_pos, cudaStream_t s, int64_t* launches) {
+    k_drop_tables<<<1 + n_specs, 1024, 0, s>>>(dropped_ids, n, inv, ntot, n_specs, drop_sorted, drop_pos);
+    ++*launches;
+}
+
+void launch_compact_all(const int32_t* sorted, int64_t ntot, int n_specs, const uint8_t* dropped,
+                        const int32_t* drop_sorted, const int32_t* drop_pos, int n_drop, int64_t K,
+                        int s_last, int32_t* idx, uint32_t* kept_rank, int32_t* kept_ids, int32_t* out_pos,
+                        cudaStream_t s, int64_t* launches) {
+    const int64_t total = ntot * (n_specs + 1);
+    k_compact_all<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
+        sorted, ntot, n_specs, dropped, drop_sorted, drop_pos, n_drop, K, s_last, idx, kept_rank, kept_ids,
+        out_pos);
+    ++*launches;
+}
+
+
+// ------------------------------------------------------------------ sync-free bin setup
+//
+// The window-bin ranges are computed on the device from the key kernel's min/max, so the
+// whole schedule is enqueued without a host round trip.  The histogram has a fixed
+// capacity; a frame set whose dense window range exceeds it raises *overflow (nbins = 0
+// disables every bin kernel) and the host re-runs the exact-size path.
+
+__global__ void k_bins_setup(const long long* __restrict__ mm, int n_specs, int nf, long long cap,
+                             SpecBins* __restrict__ specs, uint32_t* __restrict__ d_nbins,
+                             int* __restrict__ overflow) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    long long nbins = 0;
+    bool bad = false;
+    for (int s = 0; s < n_specs; ++s) {
+        const long long rM = mm[4 * s + 1] - mm[4 * s + 0] + 1, rm = mm[4 * s + 3] - mm[4 * s + 2] + 1;
+        if (rM <= 0 || rm <= 0 || rM > (1LL << 31) || rm > (1LL << 31) ||
+            static_cast<double>(rM) * static_cast<double>(rm) * nf > 1.5e9) {
+            bad = true;
+            break;
+        }
+        specs[s] = SpecBins{mm[4 * s + 0], mm[4 * s + 2], rm, rM * rm, nbins};
+        nbins += rM * rm * nf;
+    }
+    if (bad || nbins > cap) {
+        *d_nbins = 0u;
+        *overflow = 1;
+    } else {
+        *d_nbins = static_cast<uint32_t>(nbins);
+    }
+}
+
+__global__ void k_zero_bins(uint32_t* __restrict__ a, const uint32_t* __restrict__ d_n) {
+    const uint32_t n = *d_n;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = 0u;
+}
+
+// exclusive scan of hist[0, *d_n) into bin_start and cursor (<= 1024 tiles of 4096)
+__global__ void __launch_bounds__(kScanThreads) k_scan_tiles_dev(const uint32_t* __restrict__ in,
+                                                                   uint32_t* __restrict__ out,
+                                                                   const uint32_t* __restrict__ d_n,
+                                                                   uint32_t* __restrict__ tile_sums) {
+    const int64_t n = *d_n;
+    if (static_cast<int64_t>(blockIdx.x) * kScanTile >= n) return;
+    __shared__ uint32_t warp_tot[32];
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
+    uint32_t v[kScanItems];
+    uint32_t run = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const int64_t i = base + k;
+        const uint32_t t = i < n ? in[i] : 0u;
+        v[k] = run;
+        run += t;
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t x = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t w = warp_tot[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        warp_tot[lane] = w;
+    }
+    __syncthreads();
+    const uint32_t excl = x - run + (wid ? warp_tot[wid - 1] : 0u);
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const int64_t i = base + k;
+        if (i < n) out[i] = v[k] + excl;
+    }
+    if (threadIdx.x == kScanThreads - 1) tile_sums[blockIdx.x] = excl + run;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_sums_dev(uint32_t* __restrict__ sums, const uint32_t* __restrict__ d_n) {
+    const int tiles = static_cast<int>((static_cast<int64_t>(*d_n) + kScanTile - 1) / kScanTile);
+    __shared__ uint32_t warp_tot[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t v = threadIdx.x < tiles ? sums[threadIdx.x] : 0u;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t w = warp_tot[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        warp_tot[lane] = w;
+    }
+    __syncthreads();
+    if (threadIdx.x < tiles) sums[threadIdx.x] = x - v + (wid ? warp_tot[wid - 1] : 0u);
+}
+
+__global__ void k_scan_add_dev(uint32_t* __restrict__ out, uint32_t* __restrict__ cursor,
+                               const uint32_t* __restrict__ d_n, const uint32_t* __restrict__ tile_off) {
+    const int64_t n = *d_n;
+    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kScanTile;
+    if (i0 >= n) return;
+    const uint32_t add = tile_off[blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const int64_t j = i0 + threadIdx.x + static_cast<int64_t>(k) * kScanThreads;
+        if (j < n) {
+            const uint32_t v = out[j] + add;
+            out[j] = v;
+            cursor[j] = v;
+        }
+    }
+}
+
+void launch_bins_setup(const long long* mm, int n_specs, int nf, long long cap, SpecBins* specs,
+                       uint32_t* d_nbins, int* overflow, cudaStream_t s, int64_t* launches) {
+    k_bins_setup<<<1, 32, 0, s>>>(mm, n_specs, nf, cap, specs, d_nbins, overflow);
+    ++*launches;
+}
+
+void launch_zero_bins(uint32_t* hist, const uint32_t* d_nbins, cudaStream_t s, int64_t* launches) {
+    k_zero_bins<<<kNumSMs * 4, 256, 0, s>>>(hist, d_nbins);
+    ++*launches;
+}
+
+void launch_scan_bins_dev(const uint32_t* hist, uint32_t* bin_start, uint32_t* cursor, const uint32_t* d_nbins,
+                          long long cap, uint32_t* tile_sums, cudaStream_t s, int64_t* launches) {
+    const unsigned tiles = static_cast<unsigned>((cap + kScanTile - 1) / kScanTile);
+    k_scan_tiles_dev<<<tiles, kScanThreads, 0, s>>>(hist, bin_start, d_nbins, tile_sums);
+    k_scan_sums_dev<<<1, 1024, 0, s>>>(tile_sums, d_nbins);
+    k_scan_add_dev<<<tiles, kScanThreads, 0, s>>>(bin_start, cursor, d_nbins, tile_sums);
+    *launches += 3;
 }
 
 } // namespace fwa_b200

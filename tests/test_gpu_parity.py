@@ -323,3 +323,46 @@ def test_full_size_f60_properties(ctx16):
             assert np.array_equal(restricted, want)
         assert np.array_equal(r.block_perms[b], want), b
     assert np.all(np.isfinite(r.features)) and r.features.shape == (nk, 128)
+
+
+def test_sparse_wide_scene_bin_overflow_fallback(ctx32):
+    """A frame whose dense window range (~12M windows) exceeds the sync-free histogram
+    capacity: the host API detects the overflow flag and re-runs with exact bins."""
+    rng = np.random.default_rng(77)
+    c = rng.uniform(-5000, 5000, size=(3000, 2))
+    f = rng.normal(size=(3000, 16))
+    cfg = F.FwaConfig(d_model=16, n_heads=4, d_ff=32, group_size=16, n_blocks=4)
+    blob = F.init_backbone_params(cfg, 3)
+    ctx32.load_params(cfg, blob)
+    r = ctx32.run_backbone(F.PillarSet(c, f), cfg, want_block_perms=True)
+    w = O.port_run_backbone(c, f.astype(np.float32), O.make_cfg(d_model=16, n_heads=4, d_ff=32,
+                                                                group_size=16, n_blocks=4), blob,
+                            want_perms=True)
+    assert np.array_equal(r.kept_indices, w["kept"])
+    for b in range(4):
+        assert np.array_equal(r.block_perms[b], w["block_perms"][b, :len(r.block_perms[b])])
+    assert O.max_rel_err(r.features, w["features"]) <= TOL_FP32
+
+
+def test_device_api_graph_replay_matches_host_api(ctx16):
+    """Device-resident forward: eager on first sighting, captured into a CUDA graph on
+    the second, replayed after -- bitwise equal to the host-buffer API every time."""
+    import torch
+    ps = F.make_pillars(F.SCENES["F10"], 42)
+    cfg = F.FwaConfig()
+    ctx16.load_params(cfg, F.init_backbone_params(cfg, 42))
+    want = ctx16.run_backbone(F.PillarSet(ps.coords, ps.features.astype(np.float32)), cfg)
+    dev = torch.device("cuda", 0)
+    dc = torch.from_numpy(ps.coords).to(dev)
+    df = torch.from_numpy(ps.features.astype(np.float32)).to(dev)
+    out = torch.empty((ps.size(), 128), dtype=torch.float32, device=dev)
+    kept = torch.empty(ps.size(), dtype=torch.int32, device=dev)
+    for i in range(4):
+        out.zero_()
+        torch.cuda.synchronize()
+        nk = ctx16.forward_device(dc.data_ptr(), df.data_ptr(), [0, ps.size()], cfg, out.data_ptr(),
+                                  kept.data_ptr())
+        ctx16.sync_check()
+        assert nk == len(want.kept_indices)
+        assert np.array_equal(kept[:nk].cpu().numpy(), want.kept_indices), i
+        assert np.array_equal(out[:nk].cpu().numpy(), want.features), i
