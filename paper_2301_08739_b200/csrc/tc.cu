@@ -400,6 +400,33 @@ FWA_DEVINL void cta_sync_tc() {
 }
 
 template <bool kF64>
+FWA_DEVINL void load_residual(const float* x_in, const double* x_in64, const int32_t* ridx, int64_t rows,
+                              int64_t grow, int c0, float (&x1)[32]) {
+    if (grow < rows) {
+        const int64_t src = ridx ? ridx[grow] : grow;
+        if (kF64) {
+            const double2* p = reinterpret_cast<const double2*>(x_in64 + src * 128 + c0);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const double2 d2 = __ldg(p + j);
+                x1[2 * j] = static_cast<float>(d2.x);
+                x1[2 * j + 1] = static_cast<float>(d2.y);
+            }
+        } else {
+            const float4* p = reinterpret_cast<const float4*>(x_in + src * 128 + c0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float4 f4 = __ldg(p + j);
+                x1[4 * j] = f4.x; x1[4 * j + 1] = f4.y; x1[4 * j + 2] = f4.z; x1[4 * j + 3] = f4.w;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) x1[j] = 0.f;
+    }
+}
+
+template <bool kF64>
 __global__ void __launch_bounds__(kFfnThreads, 1)
     k_outproj_ffn_tc(const uint8_t* __restrict__ cat_img, const float* __restrict__ x_in,
                      const double* __restrict__ x_in64, const int32_t* __restrict__ ridx,
@@ -451,11 +478,16 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
     constexpr uint32_t id128 = idesc_bf16_f32(128, 128);
     const uint32_t TP = tmem, TUa = tmem + 128, TUb = tmem + 256, TS = tmem + 384;
     const int c0 = cq * 32;  // this thread's 32 channels / hidden units
+    // x1 holds the residual row of the CURRENT tile on loop entry (prefetched while the
+    // previous tile's output was being stored)
+    float x1[32];
+    load_residual<kF64>(x_in, x_in64, ridx, rows, static_cast<int64_t>(blockIdx.x) * 128 + row, c0, x1);
     int it = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const uint32_t ph = it & 1;
         const int64_t grow = tile * 128 + row;
         const bool valid = grow < rows;
+        (void)valid;
         // ---- 1. P = A Wout^T
         if (threadIdx.x == 0) {
             if (it == 0) mbar_wait(&bars[0], 0);
@@ -469,32 +501,6 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
                 mma_bf16(TP, sdesc_sw128(a0 + (ks >> 2) * 16384 + (ks & 3) * 32),
                          sdesc_sw128(b0 + (ks >> 2) * 16384 + (ks & 3) * 32), id128, ks > 0);
             mma_commit(&bars[2]);
-        }
-        // ---- 2. residual (one 128 B line per thread) while MMA1 runs
-        float x1[32];
-        {
-            const int64_t src = valid ? (ridx ? ridx[grow] : grow) : 0;
-            if (valid) {
-                if (kF64) {
-                    const double2* p = reinterpret_cast<const double2*>(x_in64 + src * 128 + c0);
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const double2 d2 = __ldg(p + j);
-                        x1[2 * j] = static_cast<float>(d2.x);
-                        x1[2 * j + 1] = static_cast<float>(d2.y);
-                    }
-                } else {
-                    const float4* p = reinterpret_cast<const float4*>(x_in + src * 128 + c0);
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const float4 f4 = __ldg(p + j);
-                        x1[4 * j] = f4.x; x1[4 * j + 1] = f4.y; x1[4 * j + 2] = f4.z; x1[4 * j + 3] = f4.w;
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int j = 0; j < 32; ++j) x1[j] = 0.f;
-            }
         }
         mbar_wait(&bars[2], ph);
         if (threadIdx.x == 0 && it < 4) FWA_TR(3 + 12 * it);
@@ -589,10 +595,17 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
                 if (hh) mma_commit(&bars[5]);
             }
         }
-        // ---- 5. out = x1 + (O + b2) -> staged rows -> coalesced scatter
+        // ---- 5. out = x1 + (O + b2) -> coalesced scatter through R1 in two 64-row halves;
+        //         R0 (act_a, consumed) immediately receives the next tile's A by TMA, and each
+        //         thread prefetches its next residual row right after staging its output
         mbar_wait(&bars[5], ph);
         if (threadIdx.x == 0 && it < 4) FWA_TR(9 + 12 * it);
         fence_after_sync();
+        const int64_t next = tile + gridDim.x;
+        if (threadIdx.x == 0 && next < ntiles) {
+            mbar_arrive_expect_tx(&bars[1], 32768);
+            bulk_g2s(sR, cat_img + next * 32768, 32768, &bars[1]);
+        }
         {
             uint32_t v[32];
             tmem_ld32(TP + lane_off + c0, v);
@@ -600,33 +613,38 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
 #pragma unroll
             for (int j = 0; j < 32; j += 4) {
                 const float4 b2 = *reinterpret_cast<const float4*>(sVec + 128 + c0 + j);
-                float4 o;
-                o.x = x1[j + 0] + (__uint_as_float(v[j + 0]) + b2.x);
-                o.y = x1[j + 1] + (__uint_as_float(v[j + 1]) + b2.y);
-                o.z = x1[j + 2] + (__uint_as_float(v[j + 2]) + b2.z);
-                o.w = x1[j + 3] + (__uint_as_float(v[j + 3]) + b2.w);
-                *reinterpret_cast<float4*>(sR + stage_off(row, (c0 + j) >> 2)) = o;
+                x1[j + 0] = x1[j + 0] + (__uint_as_float(v[j + 0]) + b2.x);
+                x1[j + 1] = x1[j + 1] + (__uint_as_float(v[j + 1]) + b2.y);
+                x1[j + 2] = x1[j + 2] + (__uint_as_float(v[j + 2]) + b2.z);
+                x1[j + 3] = x1[j + 3] + (__uint_as_float(v[j + 3]) + b2.w);
             }
         }
-        cta_sync_tc();
-        {
-            const int rbase = warp * 8;
-            int myid = 0;
-            const int64_t gl = tile * 128 + rbase + (lane & 7);
-            if (lane < 8 && gl < rows) myid = sidx ? sidx[gl] : static_cast<int>(gl);
+#pragma unroll 1
+        for (int hf = 0; hf < 2; ++hf) {
+            if ((row >> 6) == hf) {  // my row is in this half: stage it, then prefetch
+                const int rr = row & 63;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int64_t id = __shfl_sync(0xffffffffu, myid, i);
-                const float4 o = *reinterpret_cast<const float4*>(sR + stage_off(rbase + i, lane));
-                if (tile * 128 + rbase + i < rows) reinterpret_cast<float4*>(x_out + id * 128)[lane] = o;
+                for (int j = 0; j < 32; j += 4)
+                    *reinterpret_cast<float4*>(sR1 + stage_off(rr, (c0 + j) >> 2)) =
+                        make_float4(x1[j], x1[j + 1], x1[j + 2], x1[j + 3]);
+                if (next < ntiles) load_residual<kF64>(x_in, x_in64, ridx, rows, next * 128 + row, c0, x1);
             }
+            __syncthreads();
+            {
+                const int rbase = warp * 4;  // 16 warps x 4 rows = 64 rows of this half
+                int myid = 0;
+                const int64_t gl = tile * 128 + hf * 64 + rbase + (lane & 3);
+                if (lane < 4 && gl < rows) myid = sidx ? sidx[gl] : static_cast<int>(gl);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int64_t id = __shfl_sync(0xffffffffu, myid, i);
+                    const float4 o = *reinterpret_cast<const float4*>(sR1 + stage_off(rbase + i, lane));
+                    if (tile * 128 + hf * 64 + rbase + i < rows) reinterpret_cast<float4*>(x_out + id * 128)[lane] = o;
+                }
+            }
+            __syncthreads();
         }
-        __syncthreads();  // R free: prefetch the next tile's attention rows
         if (threadIdx.x == 0 && it < 4) FWA_TR(10 + 12 * it);
-        if (threadIdx.x == 0 && tile + gridDim.x < ntiles) {
-            mbar_arrive_expect_tx(&bars[1], 32768);
-            bulk_g2s(sR, cat_img + (tile + gridDim.x) * 32768, 32768, &bars[1]);
-        }
     }
     if (threadIdx.x == 0 && blockIdx.x >= ntiles) mbar_wait(&bars[0], 0);
     cta_sync_tc();
