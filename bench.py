@@ -257,6 +257,12 @@ def run_ours(args, rank, world, local_rank, dist):
     clk = clocks.stop()
     assert nk_e2e == nk
 
+    # ---------------------------------------------------------------- config 4: one F250 scene
+    # split by group ranges across the ranks, NCCL all-gather of each block's rows
+    split = None
+    if not args.no_split:
+        split = run_split_scene(args, F, ctx, cfg, dev, stream, rank, world, dist, flush)
+
     # ---------------------------------------------------------------- reduce over ranks
     t_dev = torch.tensor([dev_ms, e2e_s, float(n), float(nk)], dtype=torch.float64, device=dev)
     if dist:
@@ -331,8 +337,59 @@ def run_ours(args, rank, world, local_rank, dist):
         "frame_tflops": tot_flop / (ms_per_step / 1e3) / 1e12,
         "frame_frac_of_sustained": tot_flop / (ms_per_step / 1e3) / 1e12 / pk_sus,
         "cache": {"computed": cache[0], "hits": cache[1]},
+        "config4_split": split,
     }
     print(json.dumps(line), flush=True)
+
+
+def run_split_scene(args, F, ctx, cfg, dev, stream, rank, world, dist, flush):
+    """BASELINE config 4: the F250 scene (255,066 pillars) split by group ranges across
+    the ranks with an all-gather of each block's sorted-order rows (NCCL over NVLink);
+    device time per scene, max over ranks (strong scaling: total work fixed)."""
+    import torch
+
+    from paper_2301_08739_b200.split import DeviceRunner, split_forward
+    ps = F.make_pillars(F.SCENES["F250"], 42)  # replicated on every rank
+    n = ps.size()
+    d_coords = torch.from_numpy(ps.coords).to(dev)
+    d_feats = torch.from_numpy(ps.features.astype(np.float32)).to(dev)
+
+    def all_gather(dst, src):
+        if dist:
+            dist.all_gather_into_tensor(dst, src)
+        else:
+            dst.copy_(src)
+
+    def alloc(rows):
+        return torch.empty((rows, cfg.d_model), dtype=torch.float32, device=dev)
+
+    def one():
+        runner = DeviceRunner(ctx, d_coords, d_feats, cfg)
+        return split_forward(runner, cfg.n_blocks, cfg.group_size, world, rank, all_gather, alloc)
+
+    steps = max(3, args.steps // 5)
+    for _ in range(2):
+        one()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms = 0.0
+    for _ in range(steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        out = one()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms += a.elapsed_time(b)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0]) / steps
+    return {"workload": "F250 scene (255,066 pillars), 8 blocks, group-range split, all-gather per block",
+            "pillars": n, "kept": int(out.shape[0]), "ms_per_scene": ms, "pillars_per_s": n / (ms / 1e3),
+            "exchange": "NCCL all_gather_into_tensor of each block's K x 128 fp32 rows" if dist
+            else "single rank (no exchange)", "scaling": "strong", "steps": steps}
 
 
 def main():
@@ -342,6 +399,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-split", action="store_true", help="skip the config-4 split-scene measurement")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -154,6 +154,24 @@ int fwa_b200_backbone_forward_device(fwa_b200_ctx* ctx, const double* d_coords,
                                      float* d_out_features, int32_t* d_out_kept,
                                      int64_t* n_kept_out);
 
+/* Group-range split of ONE scene across ranks (BASELINE config 4), device buffers:
+ *  split_begin:   build the full index schedule + PE from replicated coordinates (every
+ *                 rank gets the identical schedule); *k_out = kept rows K.
+ *  split_block:   block b over groups [group_begin, group_end) of its window-sort order:
+ *                 reads d_x (pillar-id rows; block 0: the caller's f32 input), writes the
+ *                 (group_end - group_begin)*G sorted-order output rows to d_y (local rows;
+ *                 the all-gather of the ranks' d_y in rank order is the block's K x D output).
+ *  split_scatter: after the caller's all-gather of d_y (NCCL), write the K rows back to
+ *                 pillar-id order in d_dst (the next block's d_x), or -- for the last
+ *                 block -- to active (ascending-id) order, the backbone output.
+ * Block b's rows depend on every row of block b-1 (each block re-sorts), hence the
+ * exchange between blocks (flatten.hpp:150-161, backbone.hpp:215-317). */
+int fwa_b200_split_begin(fwa_b200_ctx* ctx, const double* d_coords, int64_t n, const fwa_config_t* cfg,
+                         int64_t* k_out);
+int fwa_b200_split_block(fwa_b200_ctx* ctx, int block, int64_t group_begin, int64_t group_end,
+                         const float* d_x, float* d_y);
+int fwa_b200_split_scatter(fwa_b200_ctx* ctx, int block, const float* d_y, float* d_dst);
+
 /* flatten::sort (minimum slice): host coords in, host permutation out. */
 int fwa_b200_sort_plan(fwa_b200_ctx* ctx, const double* coords, int64_t n, double w_x,
                        double w_y, int shift, int major_axis_y, int32_t* perm_out);

@@ -36,6 +36,7 @@ EXPORTS = [
     "fwa_b200_backbone_forward", "fwa_b200_backbone_forward_batch",
     "fwa_b200_backbone_forward_device", "fwa_b200_sort_plan", "fwa_b200_block_forward",
     "fwa_b200_positional_embedding", "fwa_b200_generate_pillars", "fwa_b200_init_params",
+    "fwa_b200_split_begin", "fwa_b200_split_block", "fwa_b200_split_scatter",
 ]
 
 PREC_BF16, PREC_FP32 = 0, 1
@@ -135,6 +136,9 @@ def lib():
         L.fwa_b200_generate_pillars.argtypes = [C.POINTER(_Scene), C.c_uint64, C.c_double, i32,
                                                 C.c_uint64, vp, vp]
         L.fwa_b200_generate_pillars.restype = i64
+        L.fwa_b200_split_begin.argtypes = [vp, vp, i64, C.POINTER(_Cfg), C.POINTER(i64)]
+        L.fwa_b200_split_block.argtypes = [vp, C.c_int, i64, i64, vp, vp]
+        L.fwa_b200_split_scatter.argtypes = [vp, C.c_int, vp, vp]
         L.fwa_b200_init_params.argtypes = [C.POINTER(_Cfg), C.c_uint64, vp, C.c_size_t]
         L.fwa_b200_init_params.restype = i64
         _lib_handle = L
@@ -395,6 +399,19 @@ class Context:
             self._h, C.c_void_p(d_coords), C.c_void_p(d_feats), _ptr(off), len(off) - 1,
             C.byref(c), C.c_void_p(d_out), C.c_void_p(d_kept) if d_kept else None, C.byref(nk)))
         return int(nk.value)
+
+    # ---- group-range split (BASELINE config 4), see paper_2301_08739_b200/split.py
+    def split_begin(self, d_coords: int, n: int, cfg: FwaConfig) -> int:
+        c = cfg.c()
+        k = C.c_int64()
+        self._check(lib().fwa_b200_split_begin(self._h, C.c_void_p(d_coords), n, C.byref(c), C.byref(k)))
+        return int(k.value)
+
+    def split_block(self, b: int, g0: int, g1: int, d_x: int, d_y: int):
+        self._check(lib().fwa_b200_split_block(self._h, b, g0, g1, C.c_void_p(d_x), C.c_void_p(d_y)))
+
+    def split_scatter(self, b: int, d_y: int, d_dst: int):
+        self._check(lib().fwa_b200_split_scatter(self._h, b, C.c_void_p(d_y), C.c_void_p(d_dst)))
 
     def sync_check(self):
         """Wait for the stream; raise deferred device-side errors of forward_device."""

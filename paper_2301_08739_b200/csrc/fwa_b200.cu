@@ -88,6 +88,17 @@ struct fwa_b200_ctx {
     int64_t g_launches = 0;
     int64_t* g_tab = nullptr;  // frame table owned by the captured graph
     bool g_disabled = false;
+    // group-range split of one scene across ranks (BASELINE config 4)
+    struct Split {
+        bool ready = false;
+        fwa_config_t cfg{};
+        int64_t ntot = 0, K = 0;
+        int32_t *idx = nullptr, *out_pos = nullptr;  // into ws buffers of the last schedule
+        float* pe = nullptr;
+        __half* pe16 = nullptr;
+        bool fast = false;
+        uint64_t ws_epoch = 0;
+    } split;
     int64_t* h_tab = nullptr;  // pinned frame-table staging (2 slots)
     size_t h_tab_cap = 0;
     int h_tab_slot = 0;
@@ -693,6 +704,23 @@ void run_block(fwa_b200_ctx* c, const BlockParams& p, const fwa_config_t* cfg, i
     check_launch();
 }
 
+// Size every per-block workspace for `rows` rows up front (the split API keeps raw
+// pointers into the workspace between calls).
+void reserve_block_ws(fwa_b200_ctx* c, const fwa_config_t* cfg, int64_t rows, bool fast) {
+    const size_t d = static_cast<size_t>(cfg->d_model), r = static_cast<size_t>(rows);
+    if (fast) {
+        ws<__nv_bfloat16>(c, "qkv16", r * 3 * d);
+        ws<__nv_bfloat16>(c, "cat16", static_cast<size_t>((rows + 127) / 128) * 128 * d);
+    } else {
+        ws<float>(c, "h32", r * d);
+        ws<float>(c, "qkv32", r * 3 * d);
+        ws<float>(c, "cat32", r * d);
+        ws<float>(c, "mid32", r * d);
+        ws<float>(c, "ln2_32", r * d);
+        ws<float>(c, "act32", r * static_cast<size_t>(cfg->d_ff));
+    }
+}
+
 void require_params(fwa_b200_ctx* c, const fwa_config_t* cfg) {
     if (!c->have_params) throw FwaError{FWA_ERR_CONTRACT, "no parameters loaded (fwa_b200_load_params)"};
     if (static_cast<int>(c->blocks.size()) != cfg->n_blocks)
@@ -1090,6 +1118,79 @@ int fwa_b200_backbone_forward_device(fwa_b200_ctx* c, const double* d_coords, co
         c->g_key = key;
         c->g_key.ws_epoch = c->ws_epoch;
         CUDA_OK(cudaGraphLaunch(c->g_exec, c->stream));
+    });
+}
+
+// ---- group-range split (BASELINE config 4): every rank builds the identical schedule
+// from replicated coordinates, computes a contiguous range of groups of each block, and
+// the ranks exchange the block's sorted-order output rows (NCCL all-gather, done by the
+// caller) before scattering them back to pillar-id order for the next block.
+int fwa_b200_split_begin(fwa_b200_ctx* c, const double* d_coords, int64_t n, const fwa_config_t* cfg,
+                         int64_t* k_out) {
+    return guarded(c, [&] {
+        validate_cfg(cfg);
+        require_params(c, cfg);
+        Schedule S;
+        const int64_t off[2] = {0, n};
+        host_frames(off, 1, cfg->group_size, S);
+        cudaStream_t st = c->stream;
+        const int d = cfg->d_model;
+        CUDA_OK(cudaMemsetAsync(c->d_flag, 0, 2 * sizeof(int), st));
+        const bool fast = fast_path_ok(c, d, cfg->n_heads, cfg->d_ff, cfg->group_size);
+        float* pe = fast ? nullptr : ws<float>(c, "pe", static_cast<size_t>(n) * d);
+        __half* pe16 = fast ? ws<__half>(c, "pe16", static_cast<size_t>(n) * d) : nullptr;
+        launch_positional_embedding(d_coords, n, d, pe_freq(c, d), pe, pe16, st, &c->launches);
+        c->exact_bins = true;  // host-sized bins: one-time cost per scene
+        struct Reset {
+            fwa_b200_ctx* c;
+            ~Reset() { c->exact_bins = false; }
+        } reset{c};
+        build_schedule(c, d_coords, cfg, S);
+        check_launch();
+        reserve_block_ws(c, cfg, S.K, fast);
+        c->split.ready = true;
+        c->split.cfg = *cfg;
+        c->split.ntot = n;
+        c->split.K = S.K;
+        c->split.idx = S.idx;
+        c->split.out_pos = S.out_pos;
+        c->split.pe = pe;
+        c->split.pe16 = pe16;
+        c->split.fast = fast;
+        c->split.ws_epoch = c->ws_epoch;
+        if (k_out) *k_out = S.K;
+    });
+}
+
+int fwa_b200_split_block(fwa_b200_ctx* c, int block, int64_t group_begin, int64_t group_end,
+                         const float* d_x, float* d_y) {
+    return guarded(c, [&] {
+        auto& sp = c->split;
+        if (!sp.ready) throw FwaError{FWA_ERR_CONTRACT, "fwa_b200_split_begin first"};
+        const int G = sp.cfg.group_size;
+        if (block < 0 || block >= sp.cfg.n_blocks || group_begin < 0 || group_end < group_begin ||
+            group_end * G > sp.K)
+            throw FwaError{FWA_ERR_SHAPE, "split: block / group range out of bounds"};
+        const int64_t r0 = group_begin * G, rows = (group_end - group_begin) * G;
+        const int32_t* idx = sp.idx + sp.K * (block % 4) + r0;
+        if (sp.ws_epoch != c->ws_epoch)
+            throw FwaError{FWA_ERR_CONTRACT, "split: workspace moved since split_begin (call it again)"};
+        run_block(c, c->blocks[static_cast<size_t>(block)], &sp.cfg, rows, idx, d_x, nullptr, sp.pe, sp.pe16,
+                  d_y, nullptr, sp.fast);
+    });
+}
+
+int fwa_b200_split_scatter(fwa_b200_ctx* c, int block, const float* d_y, float* d_dst) {
+    return guarded(c, [&] {
+        auto& sp = c->split;
+        if (!sp.ready) throw FwaError{FWA_ERR_CONTRACT, "fwa_b200_split_begin first"};
+        if (block < 0 || block >= sp.cfg.n_blocks) throw FwaError{FWA_ERR_SHAPE, "split: bad block"};
+        if (sp.ws_epoch != c->ws_epoch)
+            throw FwaError{FWA_ERR_CONTRACT, "split: workspace moved since split_begin (call it again)"};
+        const bool last = block == sp.cfg.n_blocks - 1;
+        const int32_t* pos = last ? sp.out_pos : sp.idx + sp.K * (block % 4);
+        launch_scatter_sorted(d_y, pos, sp.K, sp.cfg.d_model, d_dst, c->stream, &c->launches);
+        check_launch();
     });
 }
 

@@ -131,5 +131,8 @@ void launch_outproj_ffn_tc(const __nv_bfloat16* cat, const float* x_in, const do
 // ------------------------------------------------------------------ misc
 void launch_scatter_rows(const float* src, const int32_t* ids, const uint32_t* rank, int64_t n,
                          int d, float* dst, cudaStream_t s, int64_t* launches);
+// dst[pos[r]] = src[r] for r < n (d % 4 == 0)
+void launch_scatter_sorted(const float* src, const int32_t* pos, int64_t n, int d, float* dst, cudaStream_t s,
+                           int64_t* launches);
 
 } // namespace fwa_b200

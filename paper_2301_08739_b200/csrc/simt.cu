@@ -287,4 +287,21 @@ void launch_scatter_rows(const float* src, const int32_t* ids, const uint32_t* r
     ++*launches;
 }
 
+// dst[pos[r]] = src[r] (pos = the block's sorted pillar ids, or their output rows):
+// the inverse of the block's gather, one warp per 512 B row
+__global__ void k_scatter_sorted(const float* __restrict__ src, const int32_t* __restrict__ pos, int64_t n,
+                                 int d, float* __restrict__ dst) {
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (r >= n) return;
+    const int64_t o = pos[r];
+    for (int c = (threadIdx.x & 31) * 4; c < d; c += 128)
+        *reinterpret_cast<float4*>(dst + o * d + c) = *reinterpret_cast<const float4*>(src + r * d + c);
+}
+
+void launch_scatter_sorted(const float* src, const int32_t* pos, int64_t n, int d, float* dst, cudaStream_t s,
+                           int64_t* launches) {
+    k_scatter_sorted<<<static_cast<unsigned>((n + 7) / 8), 256, 0, s>>>(src, pos, n, d, dst);
+    ++*launches;
+}
+
 } // namespace fwa_b200
