@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <climits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -69,6 +70,7 @@ struct fwa_b200_ctx {
     int* h_flag = nullptr;     // pinned, 2 ints
     bool exact_bins = false;   // set for one call after an overflow: host-sized bins
     uint64_t ws_epoch = 0;     // bumped whenever a workspace buffer moves
+    const void* hist_clean = nullptr;  // sync-free histogram buffer known to be zeroed
     uint64_t params_version = 0;
     // CUDA graph of the device-resident forward (replayed while its key is unchanged)
     struct GraphKey {
@@ -432,18 +434,24 @@ int32_t* sort_specs(fwa_b200_ctx* c, const double* d_coords, int64_t ntot, int n
     long long* win = ws<long long>(c, "win", 2 * static_cast<size_t>(total));
     double* loc = ws<double>(c, "loc", 2 * static_cast<size_t>(total));
     long long* mm = ws<long long>(c, "minmax", 16);
-    launch_sort_keys(d_coords, ntot, n_specs, w_x, w_y, win, loc, mm, st, &c->launches);
+    const int64_t n_part = sort_keys_partials(ntot);
+    long long* partials = ws<long long>(c, "key_partials", static_cast<size_t>(n_part) * 4 * n_specs);
+    launch_sort_keys(d_coords, ntot, n_specs, w_x, w_y, win, loc, partials, st, &c->launches);
     check_launch();
     if (!exact) {
         SpecBins* d_sb = ws<SpecBins>(c, "specbins", 4);
         uint32_t* d_nbins = ws<uint32_t>(c, "nbins", 4);
         uint32_t* hist = ws<uint32_t>(c, "hist", static_cast<size_t>(kBinCap));
+        if (hist != c->hist_clean) {  // fresh buffer: zero once; the sort kernels keep it zeroed
+            CUDA_OK(cudaMemsetAsync(hist, 0, c->ws["hist"].cap, st));
+            c->hist_clean = hist;
+        }
         uint32_t* bin_start = ws<uint32_t>(c, "bin_start", static_cast<size_t>(kBinCap));
         uint32_t* cursor = ws<uint32_t>(c, "cursor", static_cast<size_t>(kBinCap));
         uint32_t* tile_sums = ws<uint32_t>(c, "bin_tile_sums", 1024);
         uint32_t* bin_of = ws<uint32_t>(c, "bin_of", static_cast<size_t>(total));
-        launch_bins_setup(mm, n_specs, nf, kBinCap, d_sb, d_nbins, c->d_flag + 1, st, &c->launches);
-        launch_zero_bins(hist, d_nbins, st, &c->launches);
+        launch_bins_setup(partials, n_part, n_specs, nf, kBinCap, mm, d_sb, d_nbins, c->d_flag + 1, st,
+                          &c->launches);
         launch_bins_hist(win, ntot, n_specs, d_off, nf, d_sb, bin_of, hist, d_nbins, st, &c->launches);
         launch_scan_bins_dev(hist, bin_start, cursor, d_nbins, kBinCap, tile_sums, st, &c->launches);
         int32_t* pre = ws<int32_t>(c, "pre", static_cast<size_t>(total));
@@ -457,6 +465,11 @@ int32_t* sort_specs(fwa_b200_ctx* c, const double* d_coords, int64_t ntot, int n
                         &c->launches);
         check_launch();
         return sorted;
+    }
+    {
+        SpecBins* d_sb0 = ws<SpecBins>(c, "specbins", 4);
+        uint32_t* d_nb0 = ws<uint32_t>(c, "nbins", 4);
+        launch_bins_setup(partials, n_part, n_specs, nf, LLONG_MAX, mm, d_sb0, d_nb0, nullptr, st, &c->launches);
     }
     CUDA_OK(cudaMemcpyAsync(c->h_minmax, mm, 16 * 8, cudaMemcpyDeviceToHost, st));
     CUDA_OK(cudaStreamSynchronize(st));
@@ -540,29 +553,30 @@ void build_schedule_body(fwa_b200_ctx* c, const double* d_coords, const fwa_conf
     uint32_t* scan_tmp = ws<uint32_t>(c, "scan_tmp", scan_tmp_words(total) + 8);
 
     // drops (block 0 = spec 0), kept set
-    S.dropped = ws<uint8_t>(c, "dropped", static_cast<size_t>(ntot));
-    CUDA_OK(cudaMemsetAsync(S.dropped, 0, static_cast<size_t>(ntot), st));
     S.dropped_ids = ws<int32_t>(c, "dropped_ids", static_cast<size_t>(S.n_drop) + 1);
-    launch_drop_mark(S.sorted, ntot, d_off, d_rows, d_drop_off, nf, S.dropped, S.dropped_ids, st,
-                     &c->launches);
     S.kept_rank = ws<uint32_t>(c, "kept_rank", static_cast<size_t>(ntot));
     S.kept_ids = ws<int32_t>(c, "kept_ids", static_cast<size_t>(S.K));
     S.idx = ws<int32_t>(c, "idx", static_cast<size_t>(S.K) * n_specs);
     S.out_pos = ws<int32_t>(c, "out_pos", static_cast<size_t>(S.K));
     const int s_last = (cfg->n_blocks - 1) % 4;
     if (S.n_drop <= kMaxDropTable) {
-        // few drops (<= G-1 per frame): binary-search compaction, no grid-wide scans
+        // few drops (<= G-1 per frame): the drop tables read the tails of spec 0's plan,
+        // compaction is a binary search -- no flags, no grid-wide scans
         const int nd = static_cast<int>(S.n_drop);
         int32_t* drop_sorted = ws<int32_t>(c, "drop_sorted", static_cast<size_t>(nd) + 1);
         int32_t* drop_pos = ws<int32_t>(c, "drop_pos", static_cast<size_t>(nd + 1) * n_specs);
         if (nd > 0)
-            launch_drop_tables(S.dropped_ids, nd, S.sorted_inv, ntot, n_specs, drop_sorted, drop_pos, st,
-                               &c->launches);
-        launch_compact_all(S.sorted, ntot, n_specs, S.dropped, drop_sorted, drop_pos, nd, S.K, s_last, S.idx,
+            launch_drop_tables(S.sorted, nd, d_off, d_rows, d_drop_off, nf, S.sorted_inv, ntot, n_specs,
+                               S.dropped_ids, drop_sorted, drop_pos, st, &c->launches);
+        launch_compact_all(S.sorted, ntot, n_specs, drop_sorted, drop_pos, nd, S.K, s_last, S.idx,
                            S.kept_rank, S.kept_ids, S.out_pos, st, &c->launches);
         check_launch();
         return;
     }
+    S.dropped = ws<uint8_t>(c, "dropped", static_cast<size_t>(ntot));
+    CUDA_OK(cudaMemsetAsync(S.dropped, 0, static_cast<size_t>(ntot), st));
+    launch_drop_mark(S.sorted, ntot, d_off, d_rows, d_drop_off, nf, S.dropped, S.dropped_ids, st,
+                     &c->launches);
     // many drops (huge group sizes x many frames): flag scans
     uint32_t* flags = ws<uint32_t>(c, "flags", static_cast<size_t>(std::max(total, ntot)));
     launch_keep_flags(S.dropped, ntot, flags, st, &c->launches);
@@ -651,9 +665,15 @@ void run_block(fwa_b200_ctx* c, const BlockParams& p, const fwa_config_t* cfg, i
             return v && v[0] == '1';
         }();
         unsigned long long* tr = trace_on && !x_in64 ? ws<unsigned long long>(c, "trace", 2 * 148 * 64) : nullptr;
+        // the gathered residual rows, tile-transposed so the out-proj kernel reads them coalesced
+        static const bool no_xq = [] {
+            const char* v = std::getenv("FWA_B200_NO_XQ");
+            return v && v[0] == '1';
+        }();
+        float* xq = no_xq ? nullptr : ws<float>(c, "xq", static_cast<size_t>((rows + 127) / 128) * 128 * 128);
         {
             StageEv t(c, FWA_PROF_LN_QKV);
-            launch_ln1_qkv_tc(x_in, x_in64, pe16, ridx, rows, p.tc, qkv, c->d_flag, st, &c->launches, tr);
+            launch_ln1_qkv_tc(x_in, x_in64, pe16, ridx, rows, p.tc, qkv, c->d_flag, xq, st, &c->launches, tr);
             check_launch("k_ln1_qkv_tc");
         }
         {
@@ -663,7 +683,7 @@ void run_block(fwa_b200_ctx* c, const BlockParams& p, const fwa_config_t* cfg, i
         }
         {
             StageEv t(c, FWA_PROF_OUTPROJ_FFN);
-            launch_outproj_ffn_tc(cat, x_in, x_in64, ridx, rows, p.tc, x_out, sidx, st, &c->launches,
+            launch_outproj_ffn_tc(cat, x_in, x_in64, ridx, rows, p.tc, x_out, sidx, xq, st, &c->launches,
                                   tr ? tr + 148 * 64 : nullptr);
             check_launch("k_outproj_ffn_tc");
         }
@@ -709,6 +729,7 @@ void run_block(fwa_b200_ctx* c, const BlockParams& p, const fwa_config_t* cfg, i
 void reserve_block_ws(fwa_b200_ctx* c, const fwa_config_t* cfg, int64_t rows, bool fast) {
     const size_t d = static_cast<size_t>(cfg->d_model), r = static_cast<size_t>(rows);
     if (fast) {
+        ws<float>(c, "xq", static_cast<size_t>((rows + 127) / 128) * 128 * 128);
         ws<__nv_bfloat16>(c, "qkv16", r * 3 * d);
         ws<__nv_bfloat16>(c, "cat16", static_cast<size_t>((rows + 127) / 128) * 128 * d);
     } else {

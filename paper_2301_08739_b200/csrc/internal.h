@@ -30,15 +30,20 @@ struct SpecBins {
     long long base;             // first global bin id of this spec
 };
 
+// writes per-CTA window min/max partials ([spec][sort_keys_partials(ntot)][4])
+int64_t sort_keys_partials(int64_t ntot);
 void launch_sort_keys(const double* coords, int64_t ntot, int n_specs, double w_x, double w_y,
-                      long long* win, double* loc, long long* minmax, cudaStream_t s,
+                      long long* win, double* loc, long long* partials, cudaStream_t s,
                       int64_t* launches);
 // d_nbins (may be null): device-side bin count of the sync-free path; 0 disables
 void launch_bins_hist(const long long* win, int64_t ntot, int n_specs, const int64_t* d_frame_off,
                       int n_frames, const SpecBins* d_specs, uint32_t* bin_of, uint32_t* hist,
                       const uint32_t* d_nbins, cudaStream_t s, int64_t* launches);
-void launch_bins_setup(const long long* mm, int n_specs, int nf, long long cap, SpecBins* specs,
-                       uint32_t* d_nbins, int* overflow, cudaStream_t s, int64_t* launches);
+// reduces the key partials -> mm[4*n_specs] (min/max per spec), bin specs, *d_nbins
+// (0 + *overflow = 1 when the dense range exceeds cap)
+void launch_bins_setup(const long long* partials, int64_t n_part, int n_specs, int nf, long long cap,
+                       long long* mm, SpecBins* specs, uint32_t* d_nbins, int* overflow, cudaStream_t s,
+                       int64_t* launches);
 void launch_zero_bins(uint32_t* hist, const uint32_t* d_nbins, cudaStream_t s, int64_t* launches);
 void launch_scan_bins_dev(const uint32_t* hist, uint32_t* bin_start, uint32_t* cursor, const uint32_t* d_nbins,
                           long long cap, uint32_t* tile_sums, cudaStream_t s, int64_t* launches);
@@ -46,18 +51,21 @@ void launch_bin_scatter(const uint32_t* bin_of, const double* loc, int64_t ntot,
                         uint32_t* cursor, int32_t* pre, double* pre_loc, const uint32_t* d_nbins,
                         cudaStream_t s, int64_t* launches);
 // also writes the inverse permutation inv[s*ntot + id] = position in sorted
-void launch_bin_sort(const uint32_t* bin_start, const uint32_t* hist, uint32_t n_bins,
+// zeroes hist[] as it consumes it (the sync-free path relies on a clean histogram)
+void launch_bin_sort(const uint32_t* bin_start, uint32_t* hist, uint32_t n_bins,
                      const int32_t* pre, const double* pre_loc, const double* loc, int64_t ntot,
                      int32_t* sorted, int32_t* inv, int32_t* scratch,
                      uint32_t* large /* 1 + n_bins words */, const uint32_t* d_nbins, cudaStream_t s,
                      int64_t* launches);
 constexpr int kMaxDropTable = 8192;
-void launch_drop_tables(const int32_t* dropped_ids, int n, const int32_t* inv, int64_t ntot, int n_specs,
-                        int32_t* drop_sorted, int32_t* drop_pos, cudaStream_t s, int64_t* launches);
-void launch_compact_all(const int32_t* sorted, int64_t ntot, int n_specs, const uint8_t* dropped,
-                        const int32_t* drop_sorted, const int32_t* drop_pos, int n_drop, int64_t K,
-                        int s_last, int32_t* idx, uint32_t* kept_rank, int32_t* kept_ids, int32_t* out_pos,
-                        cudaStream_t s, int64_t* launches);
+void launch_drop_tables(const int32_t* sorted0, int n, const int64_t* frame_off, const int64_t* rows,
+                        const int64_t* drop_off, int n_frames, const int32_t* inv, int64_t ntot, int n_specs,
+                        int32_t* dropped_ids, int32_t* drop_sorted, int32_t* drop_pos, cudaStream_t s,
+                        int64_t* launches);
+void launch_compact_all(const int32_t* sorted, int64_t ntot, int n_specs, const int32_t* drop_sorted,
+                        const int32_t* drop_pos, int n_drop, int64_t K, int s_last, int32_t* idx,
+                        uint32_t* kept_rank, int32_t* kept_ids, int32_t* out_pos, cudaStream_t s,
+                        int64_t* launches);
 
 // ------------------------------------------------------------------ schedule (backbone.hpp:236-316)
 void launch_drop_mark(const int32_t* sorted0, int64_t ntot, const int64_t* d_frame_off,
@@ -118,15 +126,15 @@ void swizzle_weight_bf16(const float* w, int rows, int k, uint16_t* out);
 
 void launch_ln1_qkv_tc(const float* x, const double* x64, const __half* pe16, const int32_t* idx,
                        int64_t rows, const TcBlockWeights& w, __nv_bfloat16* qkv,
-                       int* d_nonfinite, cudaStream_t s, int64_t* launches,
-                       unsigned long long* trace = nullptr);
+                       int* d_nonfinite, float* xq /* optional tile-transposed x copy */, cudaStream_t s,
+                       int64_t* launches, unsigned long long* trace = nullptr);
 void launch_attention_mma(const __nv_bfloat16* qkv, int64_t rows, int G, __nv_bfloat16* cat,
                           cudaStream_t s, int64_t* launches);
 // x_out[sidx[r]] = FFN-block(x_in[ridx[r]] + cat[r] Wout^T + b_out)
 void launch_outproj_ffn_tc(const __nv_bfloat16* cat, const float* x_in, const double* x_in64,
                            const int32_t* ridx, int64_t rows, const TcBlockWeights& w,
-                           float* x_out, const int32_t* sidx, cudaStream_t s, int64_t* launches,
-                           unsigned long long* trace = nullptr);
+                           float* x_out, const int32_t* sidx, const float* xq, cudaStream_t s,
+                           int64_t* launches, unsigned long long* trace = nullptr);
 
 // ------------------------------------------------------------------ misc
 void launch_scatter_rows(const float* src, const int32_t* ids, const uint32_t* rank, int64_t n,

@@ -190,19 +190,19 @@ __global__ void __launch_bounds__(256) k_sort_keys(const double* __restrict__ co
         long long v = red[q][0];
         for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
             v = (q & 1) ? (red[q][w] > v ? red[q][w] : v) : (red[q][w] < v ? red[q][w] : v);
-        long long* dst = minmax + s * 4 + q;
-        if (q & 1) atomicMax(dst, v);
-        else atomicMin(dst, v);
+        // per-CTA partial [spec][cta][4]; reduced by k_bins_setup (no init, no atomics)
+        minmax[(static_cast<int64_t>(s) * gridDim.x + blockIdx.x) * 4 + q] = v;
     }
 }
 
+int64_t sort_keys_partials(int64_t ntot) { return (ntot + 255) / 256; }
+
 void launch_sort_keys(const double* coords, int64_t ntot, int n_specs, double w_x, double w_y,
-                      long long* win, double* loc, long long* minmax, cudaStream_t s,
+                      long long* win, double* loc, long long* partials, cudaStream_t s,
                       int64_t* launches) {
-    k_init_minmax<<<1, 32, 0, s>>>(minmax, 4 * n_specs);
-    dim3 grid(static_cast<unsigned>((ntot + 255) / 256), static_cast<unsigned>(n_specs));
-    k_sort_keys<<<grid, 256, 0, s>>>(coords, ntot, n_specs, w_x, w_y, win, loc, minmax);
-    *launches += 2;
+    dim3 grid(static_cast<unsigned>(sort_keys_partials(ntot)), static_cast<unsigned>(n_specs));
+    k_sort_keys<<<grid, 256, 0, s>>>(coords, ntot, n_specs, w_x, w_y, win, loc, partials);
+    *launches += 1;
 }
 
 // ------------------------------------------------------------------ K2 bins + histogram
@@ -287,7 +287,7 @@ constexpr int kBinWarps = 8;
 // One warp sorts one window bin (<= kWarpBin points) by rank counting in shared memory;
 // bigger bins are queued for k_bin_sort_large.  Writes sorted[] and the inverse inv[].
 FWA_DEVINL void sort_one_small_bin(uint32_t bin, const uint32_t* __restrict__ bin_start,
-                                   const uint32_t* __restrict__ hist, const int32_t* __restrict__ pre,
+                                   uint32_t* __restrict__ hist, const int32_t* __restrict__ pre,
                                    const double* __restrict__ ploc, int64_t ntot, int32_t* __restrict__ sorted,
                                    int32_t* __restrict__ inv, uint32_t* __restrict__ large, double* sa,
                                    double* sb, int* si, int lane) {
@@ -297,6 +297,8 @@ FWA_DEVINL void sort_one_small_bin(uint32_t bin, const uint32_t* __restrict__ bi
         return;
     }
     if (n == 0) return;
+    __syncwarp();
+    if (lane == 0) hist[bin] = 0u;  // leave the histogram zeroed for the next call
     const uint32_t start = bin_start[bin];
     const int64_t spec_base = (static_cast<int64_t>(start) / ntot) * ntot;
     if (n == 1) {
@@ -326,7 +328,7 @@ FWA_DEVINL void sort_one_small_bin(uint32_t bin, const uint32_t* __restrict__ bi
 }
 
 __global__ void __launch_bounds__(kBinWarps * 32) k_bin_sort_small(
-    const uint32_t* __restrict__ bin_start, const uint32_t* __restrict__ hist, uint32_t n_bins,
+    const uint32_t* __restrict__ bin_start, uint32_t* __restrict__ hist, uint32_t n_bins,
     const int32_t* __restrict__ pre, const double* __restrict__ ploc, int64_t ntot,
     int32_t* __restrict__ sorted, int32_t* __restrict__ inv, uint32_t* __restrict__ large,
     const uint32_t* __restrict__ d_nbins) {
@@ -341,7 +343,7 @@ __global__ void __launch_bounds__(kBinWarps * 32) k_bin_sort_small(
 }
 
 __global__ void __launch_bounds__(512) k_bin_sort_large(
-    const uint32_t* __restrict__ bin_start, const uint32_t* __restrict__ hist,
+    const uint32_t* __restrict__ bin_start, uint32_t* __restrict__ hist,
     const uint32_t* __restrict__ large, const int32_t* __restrict__ pre,
     const double* __restrict__ loc, int64_t ntot, int32_t* __restrict__ sorted,
     int32_t* __restrict__ inv, int32_t* __restrict__ scratch) {
@@ -411,10 +413,11 @@ __global__ void __launch_bounds__(512) k_bin_sort_large(
             }
             __syncthreads();
         }
+        if (threadIdx.x == 0) hist[bin] = 0u;  // zeroed for the next call
     }
 }
 
-void launch_bin_sort(const uint32_t* bin_start, const uint32_t* hist, uint32_t n_bins,
+void launch_bin_sort(const uint32_t* bin_start, uint32_t* hist, uint32_t n_bins,
                      const int32_t* pre, const double* pre_loc, const double* loc, int64_t ntot,
                      int32_t* sorted, int32_t* inv, int32_t* scratch, uint32_t* large,
                      const uint32_t* d_nbins, cudaStream_t s, int64_t* launches) {
@@ -543,48 +546,61 @@ FWA_DEVINL int count_less(const int32_t* a, int n, int32_t v) {
 // spec's full-set plan (inv[s][id]).  Bitonic sort in shared memory, n <= kMaxDrop.
 constexpr int kMaxDrop = 8192;
 
-__global__ void __launch_bounds__(1024) k_drop_tables(const int32_t* __restrict__ dropped_ids, int n,
+__global__ void __launch_bounds__(1024) k_drop_tables(const int32_t* __restrict__ sorted0, int n,
+                                                      const int64_t* __restrict__ frame_off,
+                                                      const int64_t* __restrict__ rows,
+                                                      const int64_t* __restrict__ drop_off, int n_frames,
                                                       const int32_t* __restrict__ inv, int64_t ntot,
-                                                      int n_specs, int32_t* __restrict__ drop_sorted,
+                                                      int n_specs, int32_t* __restrict__ dropped_ids,
+                                                      int32_t* __restrict__ drop_sorted,
                                                       int32_t* __restrict__ drop_pos) {
     __shared__ int32_t v[kMaxDrop];
     int P = 1;
     while (P < n) P <<= 1;
-    {  // one CTA per table: blockIdx.x 0 = dropped ids, 1 + s = positions in spec s
-        const int pass = static_cast<int>(blockIdx.x) - 1;
-        for (int k = threadIdx.x; k < P; k += blockDim.x) {
-            int32_t x = INT32_MAX;
-            if (k < n) {
-                const int32_t id = dropped_ids[k];
-                x = pass < 0 ? id : inv[static_cast<int64_t>(pass) * ntot + id];
-            }
-            v[k] = x;
+    // one CTA per table: blockIdx.x 0 = dropped ids, 1 + s = their positions in spec s.
+    // Block 0 (spec 0) drops each frame's tail beyond rows_f (flatten.hpp:134-146).
+    const int pass = static_cast<int>(blockIdx.x) - 1;
+    for (int k = threadIdx.x; k < P; k += blockDim.x) {
+        int32_t x = INT32_MAX;
+        if (k < n) {
+            int f = 0;
+            while (f + 1 < n_frames && drop_off[f + 1] <= k) ++f;
+            const int32_t id = sorted0[frame_off[f] + rows[f] + (k - drop_off[f])];
+            if (pass < 0 && dropped_ids) dropped_ids[k] = id;  // tail order (backbone.hpp:285-291)
+            x = pass < 0 ? id : inv[static_cast<int64_t>(pass) * ntot + id];
         }
-        __syncthreads();
-        for (int size = 2; size <= P; size <<= 1)
-            for (int stride = size >> 1; stride > 0; stride >>= 1) {
-                for (int t = threadIdx.x; t < P / 2; t += blockDim.x) {
-                    const int lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
-                    const bool up = (lo & size) == 0;
-                    const int32_t a = v[lo], b = v[hi];
-                    if ((b < a) == up) {
-                        v[lo] = b;
-                        v[hi] = a;
-                    }
-                }
-                __syncthreads();
-            }
-        int32_t* dst = pass < 0 ? drop_sorted : drop_pos + static_cast<int64_t>(pass) * (n > 0 ? n : 1);
-        for (int k = threadIdx.x; k < n; k += blockDim.x) dst[k] = v[k];
+        v[k] = x;
     }
+    __syncthreads();
+    for (int size = 2; size <= P; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = threadIdx.x; t < P / 2; t += blockDim.x) {
+                const int lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const int32_t a = v[lo], b = v[hi];
+                if ((b < a) == up) {
+                    v[lo] = b;
+                    v[hi] = a;
+                }
+            }
+            __syncthreads();
+        }
+    int32_t* dst = pass < 0 ? drop_sorted : drop_pos + static_cast<int64_t>(pass) * (n > 0 ? n : 1);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) dst[k] = v[k];
 }
 
 // Grid over n_specs * ntot plan entries + ntot pillar ids:
 //   plan entry (s, j): kept id -> idx[s][j - #drop_pos[s] < j]; for the last block's
 //   spec also out_pos[that] = kept_rank(id)
 //   pillar id i: kept_rank[i] = i - #drop_sorted < i; kept_ids[kept_rank] = i
+FWA_DEVINL bool is_dropped(const int32_t* drop_sorted, int n, int32_t id, int* lb_out) {
+    const int lb = count_less(drop_sorted, n, id);
+    if (lb_out) *lb_out = lb;
+    return lb < n && drop_sorted[lb] == id;
+}
+
 __global__ void k_compact_all(const int32_t* __restrict__ sorted, int64_t ntot, int n_specs,
-                              const uint8_t* __restrict__ dropped, const int32_t* __restrict__ drop_sorted,
+                              const int32_t* __restrict__ drop_sorted,
                               const int32_t* __restrict__ drop_pos, int n_drop, int64_t K, int s_last,
                               int32_t* __restrict__ idx, uint32_t* __restrict__ kept_rank,
                               int32_t* __restrict__ kept_ids, int32_t* __restrict__ out_pos) {
@@ -593,35 +609,39 @@ __global__ void k_compact_all(const int32_t* __restrict__ sorted, int64_t ntot, 
     if (t < total) {
         const int s = static_cast<int>(t / ntot);
         const int32_t id = sorted[t];
-        if (dropped[id]) return;
+        int lb;
+        if (is_dropped(drop_sorted, n_drop, id, &lb)) return;
         const int64_t j = t - static_cast<int64_t>(s) * ntot;
         const int64_t c = j - count_less(drop_pos + static_cast<int64_t>(s) * (n_drop > 0 ? n_drop : 1), n_drop,
                                          static_cast<int32_t>(t));
         idx[static_cast<int64_t>(s) * K + c] = id;
-        if (s == s_last) out_pos[c] = id - count_less(drop_sorted, n_drop, id);
+        if (s == s_last) out_pos[c] = id - lb;
     } else if (t < total + ntot) {
         const int32_t i = static_cast<int32_t>(t - total);
-        if (dropped[i]) return;
-        const int32_t r = i - count_less(drop_sorted, n_drop, i);
+        int lb;
+        if (is_dropped(drop_sorted, n_drop, i, &lb)) return;
+        const int32_t r = i - lb;
         kept_rank[i] = static_cast<uint32_t>(r);
         kept_ids[r] = i;
     }
 }
 
-void launch_drop_tables(const int32_t* dropped_ids, int n, const int32_t* inv, int64_t ntot, int n_specs,
-                        int32_t* drop_sorted, int32_t* drop_pos, cudaStream_t s, int64_t* launches) {
-    k_drop_tables<<<1 + n_specs, 1024, 0, s>>>(dropped_ids, n, inv, ntot, n_specs, drop_sorted, drop_pos);
+void launch_drop_tables(const int32_t* sorted0, int n, const int64_t* frame_off, const int64_t* rows,
+                        const int64_t* drop_off, int n_frames, const int32_t* inv, int64_t ntot, int n_specs,
+                        int32_t* dropped_ids, int32_t* drop_sorted, int32_t* drop_pos, cudaStream_t s,
+                        int64_t* launches) {
+    k_drop_tables<<<1 + n_specs, 1024, 0, s>>>(sorted0, n, frame_off, rows, drop_off, n_frames, inv, ntot,
+                                               n_specs, dropped_ids, drop_sorted, drop_pos);
     ++*launches;
 }
 
-void launch_compact_all(const int32_t* sorted, int64_t ntot, int n_specs, const uint8_t* dropped,
-                        const int32_t* drop_sorted, const int32_t* drop_pos, int n_drop, int64_t K,
-                        int s_last, int32_t* idx, uint32_t* kept_rank, int32_t* kept_ids, int32_t* out_pos,
-                        cudaStream_t s, int64_t* launches) {
+void launch_compact_all(const int32_t* sorted, int64_t ntot, int n_specs, const int32_t* drop_sorted,
+                        const int32_t* drop_pos, int n_drop, int64_t K, int s_last, int32_t* idx,
+                        uint32_t* kept_rank, int32_t* kept_ids, int32_t* out_pos, cudaStream_t s,
+                        int64_t* launches) {
     const int64_t total = ntot * (n_specs + 1);
     k_compact_all<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
-        sorted, ntot, n_specs, dropped, drop_sorted, drop_pos, n_drop, K, s_last, idx, kept_rank, kept_ids,
-        out_pos);
+        sorted, ntot, n_specs, drop_sorted, drop_pos, n_drop, K, s_last, idx, kept_rank, kept_ids, out_pos);
     ++*launches;
 }
 
@@ -633,25 +653,57 @@ void launch_compact_all(const int32_t* sorted, int64_t ntot, int n_specs, const 
 // capacity; a frame set whose dense window range exceeds it raises *overflow (nbins = 0
 // disables every bin kernel) and the host re-runs the exact-size path.
 
-__global__ void k_bins_setup(const long long* __restrict__ mm, int n_specs, int nf, long long cap,
-                             SpecBins* __restrict__ specs, uint32_t* __restrict__ d_nbins,
-                             int* __restrict__ overflow) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__global__ void __launch_bounds__(1024) k_bins_setup(const long long* __restrict__ partials, int64_t n_part,
+                                                      int n_specs, int nf, long long cap,
+                                                      long long* __restrict__ mm,
+                                                      SpecBins* __restrict__ specs,
+                                                      uint32_t* __restrict__ d_nbins,
+                                                      int* __restrict__ overflow) {
+    __shared__ long long red[32][4];
+    __shared__ long long fin[4][4];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int s = 0; s < n_specs; ++s) {
+        long long v[4] = {LLONG_MAX, LLONG_MIN, LLONG_MAX, LLONG_MIN};
+        for (int64_t i = threadIdx.x; i < n_part; i += blockDim.x) {
+            const long long* p = partials + (static_cast<int64_t>(s) * n_part + i) * 4;
+            v[0] = p[0] < v[0] ? p[0] : v[0];
+            v[1] = p[1] > v[1] ? p[1] : v[1];
+            v[2] = p[2] < v[2] ? p[2] : v[2];
+            v[3] = p[3] > v[3] ? p[3] : v[3];
+        }
+        v[0] = wmin(v[0]);
+        v[1] = wmax(v[1]);
+        v[2] = wmin(v[2]);
+        v[3] = wmax(v[3]);
+        if (lane == 0)
+            for (int q = 0; q < 4; ++q) red[wid][q] = v[q];
+        __syncthreads();
+        if (threadIdx.x < 4) {
+            const int q = threadIdx.x;
+            long long r = red[0][q];
+            for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
+                r = (q & 1) ? (red[w][q] > r ? red[w][q] : r) : (red[w][q] < r ? red[w][q] : r);
+            fin[s][q] = r;
+            mm[4 * s + q] = r;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x != 0) return;
     long long nbins = 0;
     bool bad = false;
     for (int s = 0; s < n_specs; ++s) {
-        const long long rM = mm[4 * s + 1] - mm[4 * s + 0] + 1, rm = mm[4 * s + 3] - mm[4 * s + 2] + 1;
+        const long long rM = fin[s][1] - fin[s][0] + 1, rm = fin[s][3] - fin[s][2] + 1;
         if (rM <= 0 || rm <= 0 || rM > (1LL << 31) || rm > (1LL << 31) ||
             static_cast<double>(rM) * static_cast<double>(rm) * nf > 1.5e9) {
             bad = true;
             break;
         }
-        specs[s] = SpecBins{mm[4 * s + 0], mm[4 * s + 2], rm, rM * rm, nbins};
+        specs[s] = SpecBins{fin[s][0], fin[s][2], rm, rM * rm, nbins};
         nbins += rM * rm * nf;
     }
     if (bad || nbins > cap) {
         *d_nbins = 0u;
-        *overflow = 1;
+        if (overflow) *overflow = 1;
     } else {
         *d_nbins = static_cast<uint32_t>(nbins);
     }
@@ -751,9 +803,10 @@ __global__ void k_scan_add_dev(uint32_t* __restrict__ out, uint32_t* __restrict_
     }
 }
 
-void launch_bins_setup(const long long* mm, int n_specs, int nf, long long cap, SpecBins* specs,
-                       uint32_t* d_nbins, int* overflow, cudaStream_t s, int64_t* launches) {
-    k_bins_setup<<<1, 32, 0, s>>>(mm, n_specs, nf, cap, specs, d_nbins, overflow);
+void launch_bins_setup(const long long* partials, int64_t n_part, int n_specs, int nf, long long cap,
+                       long long* mm, SpecBins* specs, uint32_t* d_nbins, int* overflow, cudaStream_t s,
+                       int64_t* launches) {
+    k_bins_setup<<<1, 1024, 0, s>>>(partials, n_part, n_specs, nf, cap, mm, specs, d_nbins, overflow);
     ++*launches;
 }
 

@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(kQkvThreads, 1)
     k_ln1_qkv_tc(const float* __restrict__ x, const double* __restrict__ x64,
                  const __half* __restrict__ pe16, const int32_t* __restrict__ idx, int64_t rows,
                  TcBlockWeights w, __nv_bfloat16* __restrict__ qkv, int* __restrict__ nonfinite,
-                 unsigned long long* __restrict__ trace) {
+                 float* __restrict__ xq, unsigned long long* __restrict__ trace) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
     uint8_t* sW = smem;
@@ -237,6 +237,16 @@ __global__ void __launch_bounds__(kQkvThreads, 1)
             for (int p = 0; p < 4; ++p) {  // rows of pass p+1 in flight while pass p is reduced
                 if (p + 1 < 4) load_row_eighth<kF64>(x, x64, pe16, id[p + 1], sub, ok[p + 1], v[(p + 1) & 1], ph[(p + 1) & 1]);
                 ln1_row_to_tile(v[p & 1], ph[p & 1], ok[p], warp * 16 + p * 4 + rl, sub, sG, sB, A, bad);
+                if (xq && ok[p]) {
+                    // the gathered fp32 row, tile-transposed for the out-proj kernel's residual:
+                    // float4 ((tile*4 + cq)*8 + j)*128 + row  (cq = channel/32, j = channel%32/4)
+                    const int r = warp * 16 + p * 4 + rl;
+                    float4* q = reinterpret_cast<float4*>(xq) + ((tile * 4 + (sub >> 1)) * 8 + (sub & 1) * 4) * 128 + r;
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj)
+                        q[jj * 128] = make_float4(v[p & 1][4 * jj], v[p & 1][4 * jj + 1], v[p & 1][4 * jj + 2],
+                                                  v[p & 1][4 * jj + 3]);
+                }
             }
             fence_proxy_async_smem();
             __syncwarp();
@@ -312,7 +322,7 @@ __global__ void __launch_bounds__(kQkvThreads, 1)
 
 void launch_ln1_qkv_tc(const float* x, const double* x64, const __half* pe, const int32_t* idx,
                        int64_t rows, const TcBlockWeights& w, __nv_bfloat16* qkv, int* d_nonfinite,
-                       cudaStream_t s, int64_t* launches, unsigned long long* trace) {
+                       float* xq, cudaStream_t s, int64_t* launches, unsigned long long* trace) {
     static bool init = false;
     if (!init) {
         cudaFuncSetAttribute(k_ln1_qkv_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kQkvSmem);
@@ -323,10 +333,10 @@ void launch_ln1_qkv_tc(const float* x, const double* x64, const __half* pe, cons
     const unsigned grid = static_cast<unsigned>(ntiles < kNumSMs ? ntiles : kNumSMs);
     if (x64)
         launch_pdl(k_ln1_qkv_tc<true>, grid, kQkvThreads, kQkvSmem, s, x, x64, pe, idx, rows, w, qkv,
-                   d_nonfinite, trace);
+                   d_nonfinite, xq, trace);
     else
         launch_pdl(k_ln1_qkv_tc<false>, grid, kQkvThreads, kQkvSmem, s, x, x64, pe, idx, rows, w, qkv,
-                   d_nonfinite, trace);
+                   d_nonfinite, xq, trace);
     ++*launches;
 }
 
@@ -401,7 +411,22 @@ FWA_DEVINL void cta_sync_tc() {
 
 template <bool kF64>
 FWA_DEVINL void load_residual(const float* x_in, const double* x_in64, const int32_t* ridx, int64_t rows,
-                              int64_t grow, int c0, float (&x1)[32]) {
+                              int64_t grow, int c0, float (&x1)[32], const float* xq) {
+    if (xq) {  // tile-transposed copy written by the QKV kernel: lanes = consecutive rows
+        if (grow < rows) {
+            const float4* q = reinterpret_cast<const float4*>(xq) + ((grow >> 7) * 4 + (c0 >> 5)) * 8 * 128 +
+                              (grow & 127);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float4 f4 = __ldg(q + j * 128);
+                x1[4 * j] = f4.x; x1[4 * j + 1] = f4.y; x1[4 * j + 2] = f4.z; x1[4 * j + 3] = f4.w;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) x1[j] = 0.f;
+        }
+        return;
+    }
     if (grow < rows) {
         const int64_t src = ridx ? ridx[grow] : grow;
         if (kF64) {
@@ -431,7 +456,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
     k_outproj_ffn_tc(const uint8_t* __restrict__ cat_img, const float* __restrict__ x_in,
                      const double* __restrict__ x_in64, const int32_t* __restrict__ ridx,
                      int64_t rows, TcBlockWeights w, float* __restrict__ x_out,
-                     const int32_t* __restrict__ sidx, unsigned long long* __restrict__ trace) {
+                     const int32_t* __restrict__ sidx, const float* __restrict__ xq,
+                     unsigned long long* __restrict__ trace) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
     uint8_t* sWo = smem;
@@ -481,7 +507,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
     // x1 holds the residual row of the CURRENT tile on loop entry (prefetched while the
     // previous tile's output was being stored)
     float x1[32];
-    load_residual<kF64>(x_in, x_in64, ridx, rows, static_cast<int64_t>(blockIdx.x) * 128 + row, c0, x1);
+    load_residual<kF64>(x_in, x_in64, ridx, rows, static_cast<int64_t>(blockIdx.x) * 128 + row, c0, x1, xq);
     int it = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const uint32_t ph = it & 1;
@@ -627,7 +653,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
                 for (int j = 0; j < 32; j += 4)
                     *reinterpret_cast<float4*>(sR1 + stage_off(rr, (c0 + j) >> 2)) =
                         make_float4(x1[j], x1[j + 1], x1[j + 2], x1[j + 3]);
-                if (next < ntiles) load_residual<kF64>(x_in, x_in64, ridx, rows, next * 128 + row, c0, x1);
+                if (next < ntiles) load_residual<kF64>(x_in, x_in64, ridx, rows, next * 128 + row, c0, x1, xq);
             }
             __syncthreads();
             {
@@ -653,7 +679,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
 
 void launch_outproj_ffn_tc(const __nv_bfloat16* cat, const float* x_in, const double* x_in64,
                            const int32_t* ridx, int64_t rows, const TcBlockWeights& w, float* x_out,
-                           const int32_t* sidx, cudaStream_t s, int64_t* launches,
+                           const int32_t* sidx, const float* xq, cudaStream_t s, int64_t* launches,
                            unsigned long long* trace) {
     static bool init = false;
     if (!init) {
@@ -666,10 +692,10 @@ void launch_outproj_ffn_tc(const __nv_bfloat16* cat, const float* x_in, const do
     const uint8_t* img = reinterpret_cast<const uint8_t*>(cat);
     if (x_in64)
         launch_pdl(k_outproj_ffn_tc<true>, grid, kFfnThreads, kFfnSmem, s, img, x_in, x_in64, ridx, rows, w,
-                   x_out, sidx, trace);
+                   x_out, sidx, xq, trace);
     else
         launch_pdl(k_outproj_ffn_tc<false>, grid, kFfnThreads, kFfnSmem, s, img, x_in, x_in64, ridx, rows, w,
-                   x_out, sidx, trace);
+                   x_out, sidx, xq, trace);
     ++*launches;
 }
 
