@@ -40,6 +40,11 @@ sys.path.insert(0, ROOT)
 METRIC = "pillars/sec and ms/frame, FlatFormer backbone fwd, 1/2/4/8 B200 vs CPU ref"
 FLOP_PER_ROW = {"ln1_qkv": 2 * 128 * 384, "attention": 2 * 2 * 69 * 128,
                 "outproj_ffn": 2 * (128 * 128 + 2 * 128 * 256)}  # 297,472 per kept pillar per block
+# algorithmic HBM bytes per kept row: the data each kernel must move
+BYTES_PER_ROW = {"ln1_qkv": 512 + 256 + 4 + 768,      # fp32 row + fp16 PE row + id in, bf16 q|k|v out
+                 "attention": 768 + 256,               # q|k|v in, head outputs out
+                 "outproj_ffn": 256 + 512 + 8 + 512}   # head outputs + fp32 residual + ids in, fp32 row out
+NCU_KERNEL = {"ln1_qkv": "k_ln1_qkv_tc", "attention": "k_attention_mma", "outproj_ffn": "k_outproj_ffn_tc"}
 WORKLOAD = "F60 frame (60,897 pillars), full FlatFormer backbone: 8 blocks, G 69, D 128, H 8, D_ff 256"
 
 
@@ -53,7 +58,7 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms while running."""
+    """nvidia-smi clocks + throttle reasons sampled every 50 ms while running."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -67,7 +72,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200",
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "50",
                  "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -281,30 +286,44 @@ def run_ours(args, rank, world, local_rank, dist):
     e2e_value = pillars_all * args.steps / e2e_max
 
     hbm, pk_burst, pk_sus, pk_kind = peaks()
+    ridge = pk_sus * 1e12 / (hbm * 1e9)  # FLOP/B where the sustained tensor and HBM roofs meet
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")) as f:
+            ncu_traffic = json.load(f)
+    except Exception:
+        ncu_traffic = {}
     kernels = {}
     for k, rows_flop in FLOP_PER_ROW.items():
         tot_ms, calls = prof[k]
         if calls:
             avg = tot_ms / calls
-            flop = rows_flop * nk
-            kernels[k] = {"avg_ms": avg, "calls": calls, "tflops": flop / (avg / 1e3) / 1e12,
-                          "frac_of_sustained": flop / (avg / 1e3) / 1e12 / pk_sus}
-    for k in ("schedule", "pe"):
-        tot_ms, calls = prof[k]
-        if calls:
-            kernels[k] = {"avg_ms": tot_ms / calls, "calls": calls}
-    if prof["schedule"][1]:
-        # sort/group/drop/compaction bytes per call: coords 16 B + per spec (4 specs):
-        # keys 32 B write + 32 B read, bin id 4+4, scatter 4+4, per-bin sort 4+16+4 read/write,
-        # compaction 4+1+4+4 (SURVEY §8d counts 16 B in + 4 B perm out per pillar per spec)
-        alg = n * (16 + 4 * 4)
-        kernels["schedule"]["algorithmic_gbs"] = alg / (kernels["schedule"]["avg_ms"] / 1e3) / 1e9
+            flop, byts = rows_flop * nk, BYTES_PER_ROW[k] * nk
+            tf = flop / (avg / 1e3) / 1e12
+            gbs = byts / (avg / 1e3) / 1e9
+            kernels[k] = {"avg_ms": avg, "calls": calls, "tflops": tf, "frac_tensor_sustained": tf / pk_sus,
+                          "gbs": gbs, "frac_hbm": gbs / hbm,
+                          "intensity_flop_per_byte": rows_flop / BYTES_PER_ROW[k],
+                          "bound": "hbm" if rows_flop / BYTES_PER_ROW[k] < ridge else "tensor",
+                          "ncu_dram_bytes_per_launch": ncu_traffic.get(NCU_KERNEL[k], {}).get("dram_bytes_per_launch")}
+    tot_ms, calls = prof["schedule"]
+    if calls:
+        # sort/group/drop: 16 B coords in + per spec 4 B plan out per pillar
+        kernels["schedule"] = {"avg_ms": tot_ms / calls, "calls": calls,
+                               "algorithmic_gbs": n * (16 + 4 * 4) / (tot_ms / calls / 1e3) / 1e9}
     dom = max(FLOP_PER_ROW, key=lambda k: prof[k][0])
     dk = kernels[dom]
-    roofline = {"bound": "tensor", "kernel": dom, "achieved": dk["tflops"], "peak": pk_sus,
-                "unit": "TFLOP/s", "frac": dk["tflops"] / pk_sus, "traffic": None,
-                "peak_kind": f"{pk_kind} bf16 sustained (kernel timed inside the step)",
-                "flop_per_launch": FLOP_PER_ROW[dom] * nk}
+    if dk["bound"] == "hbm":
+        roofline = {"bound": "hbm", "kernel": dom, "achieved": dk["gbs"], "peak": hbm, "unit": "GB/s",
+                    "frac": dk["gbs"] / hbm, "traffic": dk["ncu_dram_bytes_per_launch"],
+                    "algorithmic_bytes_per_launch": BYTES_PER_ROW[dom] * nk,
+                    "peak_kind": f"{pk_kind} HBM copy bandwidth",
+                    "note": "intensity %.0f FLOP/B < ridge %.0f; tensor frac %.3f of sustained bf16" % (
+                        dk["intensity_flop_per_byte"], ridge, dk["frac_tensor_sustained"])}
+    else:
+        roofline = {"bound": "tensor", "kernel": dom, "achieved": dk["tflops"], "peak": pk_sus,
+                    "unit": "TFLOP/s", "frac": dk["tflops"] / pk_sus, "traffic": dk["ncu_dram_bytes_per_launch"],
+                    "flop_per_launch": FLOP_PER_ROW[dom] * nk,
+                    "peak_kind": f"{pk_kind} bf16 sustained (kernel timed inside the step)"}
     tot_flop = 297472 * nk * 8
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -395,7 +414,7 @@ def run_split_scene(args, F, ctx, cfg, dev, stream, rank, world, dist, flush):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
