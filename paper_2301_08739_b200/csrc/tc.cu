@@ -59,58 +59,59 @@ FWA_DEVINL uint8_t* align1024(uint8_t* p) { return p + ((1024u - (smem_u32(p) & 
 
 // ------------------------------------------------------------------ K_a: gather + LN1 + PE + QKV
 //
-// Warp-specialised persistent kernel, 12 warps:
-//   warps 0-7  producers: 16 rows each per 128-row tile, 8 lanes per row (16 channels:
-//              64 B of the fp32 row + 32 B of the fp16 PE row per lane), 4-row passes
-//              software-pipelined (pass p+1 in flight while pass p is reduced), the
-//              pillar ids of the NEXT tile prefetched; LN1 + affine + PE in fp32 -> bf16
-//              SW128 A tile.  A is double-buffered so tile t+1 is gathered while tile t
-//              is multiplied.
-//   warps 8-15 MMA issue (one elected thread) + epilogue (lane quarter x column half):
-//              TMEM -> +bias -> bf16,
-//              written chunk-major (q|k|v as 12 column chunks of [rows x 32]) so each
-//              warp store is 2 KB contiguous and the attention kernel reads each
-//              group's rows as contiguous runs.
-// mbarriers: full[s] (8 producer warps), empty[s] (tcgen05.commit), done (commit).
+// Warp-specialised persistent kernel, 16 warps:
+//   warps 0-11  producers: a 128-row tile is 32 passes of 4 rows (8 lanes per row, each
+//              lane 16 channels 32i + 4*sub + e, so every load instruction reads whole
+//              128 B lines: 64 B of fp32 x, 32 B of fp16 PE per lane), passes w, w+12,
+//              w+24 per warp software-pipelined (pass k+1 in flight while pass k is
+//              reduced), pillar ids of the NEXT tile prefetched; LN1 + affine + PE in
+//              fp32 -> bf16 SW128 A tile; the gathered fp32 row also goes to the
+//              tile-transposed residual copy xq.  A is double-buffered.
+//   warps 12-15 MMA issue (one elected thread) + epilogue (TMEM lane quarter each):
+//              TMEM -> +bias -> bf16 rows staged in shared memory -> one bulk TMA store
+//              per (tile, column chunk): the chunk-major q|k|v layout (12 chunks of
+//              [rows x 32]) makes each such block 8 KB contiguous, and the attention
+//              kernel reads each group's rows as contiguous runs.
+// mbarriers: full[s] (12 producer warps), empty[s] (tcgen05.commit), done (commit).
 
 constexpr int kQkvW = 384 * 128 * 2;   // 98304 B weight image
 constexpr int kTileA = 128 * 128 * 2;  // 32768 B per A stage
 constexpr int kQkvThreads = 512;
-constexpr int kQkvSmem = kQkvW + 2 * kTileA + (384 + 256) * 4 /*bias, ln1 g|b*/ + 128 /*bars*/ + 1024;
+constexpr int kQkvProd = 12;  // producer warps; the remaining 4 drain TMEM (MMA issue: the first of them)
+constexpr int kQkvStage = 2 * 16384;  // 2 x (2 chunks x 128 rows x 64 B) qkv store staging
+constexpr int kQkvSmem = kQkvW + 2 * kTileA + kQkvStage + (384 + 256) * 4 /*bias, ln1 g|b*/ + 128 /*bars*/ + 1024;
 
-// One lane's 16 channels (an eighth of a row): 64 B of the fp32 row, 32 B of the fp16 PE row.
+// One lane's 16 channels of a row: channels 32i + 4*sub + e (i, e < 4), so each load
+// instruction of the 8 lanes sharing a row reads one contiguous 128 B line of the fp32
+// row (64 B of the fp16 PE row).
 template <bool kF64>
-FWA_DEVINL void load_row_eighth(const float* x, const double* x64, const __half* pe16, int64_t id,
-                                int sub, bool valid, float (&v)[16], uint4 (&ph)[2]) {
+FWA_DEVINL void load_row_quads(const float* x, const double* x64, const __half* pe16, int64_t id,
+                               int sub, bool valid, float (&v)[16], uint2 (&ph)[4]) {
     if (!valid) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] = 0.f;
-        ph[0] = ph[1] = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) ph[i] = make_uint2(0u, 0u);
         return;
     }
-    if (kF64) {
-        const double2* p = reinterpret_cast<const double2*>(x64 + id * 128 + sub * 16);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const double2 d2 = __ldg(p + j);
-            v[2 * j] = static_cast<float>(d2.x);
-            v[2 * j + 1] = static_cast<float>(d2.y);
-        }
-    } else {
-        const float4* p = reinterpret_cast<const float4*>(x + id * 128 + sub * 16);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const float4 f4 = __ldg(p + j);
-            v[4 * j] = f4.x; v[4 * j + 1] = f4.y; v[4 * j + 2] = f4.z; v[4 * j + 3] = f4.w;
+    for (int i = 0; i < 4; ++i) {
+        if (kF64) {
+            const double2* p = reinterpret_cast<const double2*>(x64 + id * 128 + 32 * i + 4 * sub);
+            const double2 d0 = __ldg(p), d1 = __ldg(p + 1);
+            v[4 * i] = static_cast<float>(d0.x); v[4 * i + 1] = static_cast<float>(d0.y);
+            v[4 * i + 2] = static_cast<float>(d1.x); v[4 * i + 3] = static_cast<float>(d1.y);
+        } else {
+            const float4 f4 = __ldg(reinterpret_cast<const float4*>(x + id * 128 + 32 * i + 4 * sub));
+            v[4 * i] = f4.x; v[4 * i + 1] = f4.y; v[4 * i + 2] = f4.z; v[4 * i + 3] = f4.w;
         }
     }
-    const uint4* pp = reinterpret_cast<const uint4*>(pe16 + id * 128 + sub * 16);
-    ph[0] = __ldg(pp);
-    ph[1] = __ldg(pp + 1);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) ph[i] = __ldg(reinterpret_cast<const uint2*>(pe16 + id * 128 + 32 * i + 4 * sub));
 }
 
-// LN1 (two-pass, 8 lanes per row) + affine + PE -> 2 bf16 chunks of the A image.
-FWA_DEVINL void ln1_row_to_tile(const float (&v)[16], const uint4 (&ph)[2], bool valid, int r, int sub,
+// LN1 (two-pass, 8 lanes per row) + affine + PE -> 4 x 8 B of the bf16 SW128 A image.
+FWA_DEVINL void ln1_row_to_tile(const float (&v)[16], const uint2 (&ph)[4], bool valid, int r, int sub,
                                 const float* sG, const float* sB, uint8_t* A, bool& bad) {
     float sm = 0.f;
 #pragma unroll
@@ -130,26 +131,26 @@ FWA_DEVINL void ln1_row_to_tile(const float (&v)[16], const uint4 (&ph)[2], bool
     sq += __shfl_xor_sync(0xffffffffu, sq, 4);
     const float inv = 1.0f / sqrtf(sq * (1.0f / 128.0f) + 1e-5f);
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {  // 8 channels = one 16 B chunk of the SW128 image
-        const float4 g0 = *reinterpret_cast<const float4*>(sG + sub * 16 + c * 8);
-        const float4 g1 = *reinterpret_cast<const float4*>(sG + sub * 16 + c * 8 + 4);
-        const float4 b0 = *reinterpret_cast<const float4*>(sB + sub * 16 + c * 8);
-        const float4 b1 = *reinterpret_cast<const float4*>(sB + sub * 16 + c * 8 + 4);
-        const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-        const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-        const uint32_t hw[4] = {ph[c].x, ph[c].y, ph[c].z, ph[c].w};
-        uint32_t o[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const float2 pf = __half22float2(*reinterpret_cast<const __half2*>(&hw[e]));
-            bad |= !(isfinite(pf.x) && isfinite(pf.y));
-            const int j = c * 8 + 2 * e;
-            o[e] = pack_bf16x2(gg[2 * e] * ((v[j] - mean) * inv) + bb[2 * e] + pf.x,
-                               gg[2 * e + 1] * ((v[j + 1] - mean) * inv) + bb[2 * e + 1] + pf.y);
-        }
-        if (!valid) o[0] = o[1] = o[2] = o[3] = 0u;
-        *reinterpret_cast<uint4*>(A + sw128_offset(r, sub * 16 + c * 8, 128)) = make_uint4(o[0], o[1], o[2], o[3]);
+    for (int i = 0; i < 4; ++i) {
+        const int c = 32 * i + 4 * sub;
+        const float4 g = *reinterpret_cast<const float4*>(sG + c);
+        const float4 b = *reinterpret_cast<const float4*>(sB + c);
+        const float2 p0 = __half22float2(*reinterpret_cast<const __half2*>(&ph[i].x));
+        const float2 p1 = __half22float2(*reinterpret_cast<const __half2*>(&ph[i].y));
+        bad |= !(isfinite(p0.x) && isfinite(p0.y) && isfinite(p1.x) && isfinite(p1.y));
+        uint32_t o0 = pack_bf16x2(g.x * ((v[4 * i] - mean) * inv) + b.x + p0.x,
+                                  g.y * ((v[4 * i + 1] - mean) * inv) + b.y + p0.y);
+        uint32_t o1 = pack_bf16x2(g.z * ((v[4 * i + 2] - mean) * inv) + b.z + p1.x,
+                                  g.w * ((v[4 * i + 3] - mean) * inv) + b.w + p1.y);
+        if (!valid) o0 = o1 = 0u;
+        *reinterpret_cast<uint2*>(A + sw128_offset(r, c, 128)) = make_uint2(o0, o1);
     }
+}
+
+FWA_DEVINL uint4 pick4(const uint4 (&P)[4], int j) {
+    const uint4 a = (j & 1) ? P[1] : P[0];
+    const uint4 b = (j & 1) ? P[3] : P[2];
+    return (j & 2) ? b : a;
 }
 
 template <bool kF64>
@@ -162,7 +163,8 @@ __global__ void __launch_bounds__(kQkvThreads, 1)
     uint8_t* smem = align1024(smem_raw);
     uint8_t* sW = smem;
     uint8_t* sA = smem + kQkvW;                                        // 2 stages
-    float* sBias = reinterpret_cast<float*>(sA + 2 * kTileA);          // 384
+    uint8_t* sStage = sA + 2 * kTileA;                                 // 2 staging buffers
+    float* sBias = reinterpret_cast<float*>(sStage + kQkvStage);       // 384
     float* sG = sBias + 384;                                           // 128
     float* sB = sG + 128;                                              // 128
     uint64_t* bars = reinterpret_cast<uint64_t*>(sB + 128);            // wbar, full[2], empty[2], done
@@ -176,8 +178,8 @@ __global__ void __launch_bounds__(kQkvThreads, 1)
     griddep_launch_dependents();
     if (threadIdx.x == 0) {
         mbar_init(wbar, 1);
-        mbar_init(&full[0], 8);
-        mbar_init(&full[1], 8);
+        mbar_init(&full[0], kQkvProd);
+        mbar_init(&full[1], kQkvProd);
         mbar_init(&empty[0], 1);
         mbar_init(&empty[1], 1);
         mbar_init(done, 1);
@@ -188,7 +190,7 @@ __global__ void __launch_bounds__(kQkvThreads, 1)
         sG[i] = w.ln1_g[i];
         sB[i] = w.ln1_b[i];
     }
-    if (warp == 8) {
+    if (warp == kQkvProd) {
         __syncwarp();
         tmem_alloc(tmem_slot, 512);
     }
@@ -198,7 +200,7 @@ __global__ void __launch_bounds__(kQkvThreads, 1)
     const uint32_t tmem = *tmem_slot;
     const int64_t ntiles = (rows + 127) / 128;
 
-    if (warp < 8) {
+    if (warp < kQkvProd) {
         // ------------------------------------------------ producers
         if (threadIdx.x == 0) {
             mbar_arrive_expect_tx(wbar, kQkvW);
@@ -206,46 +208,54 @@ __global__ void __launch_bounds__(kQkvThreads, 1)
             for (int c = 0; c < 3; ++c)
                 bulk_g2s(sW + c * 32768, reinterpret_cast<const uint8_t*>(w.w_qkv) + c * 32768, 32768, wbar);
         }
-        auto tile_ids = [&](int64_t tile) {  // lane l < 16 holds the id of row warp*16 + l
-            const int64_t g = tile * 128 + warp * 16 + (lane & 15);
-            return (tile < ntiles && g < rows) ? (idx ? idx[g] : static_cast<int>(g)) : 0;
-        };
         bool bad = false;
         if (threadIdx.x == 0) FWA_TR(0);
         griddep_wait();  // x / PE / ids come from earlier kernels
         const int sub = lane & 7, rl = lane >> 3;  // 8 lanes per row, 4 rows per pass
-        int ids = tile_ids(blockIdx.x);
+        // 32 passes of 4 rows per tile over kQkvProd warps: warp w owns passes w, w+P, w+2P
+        constexpr int kMaxPass = (32 + kQkvProd - 1) / kQkvProd;
+        const int n_my = (32 - warp + kQkvProd - 1) / kQkvProd;
+        auto pass_id = [&](int64_t tile, int p) {
+            const int64_t g = tile * 128 + p * 4 + rl;
+            return (tile < ntiles && p < 32 && g < rows) ? (idx ? idx[g] : static_cast<int>(g)) : 0;
+        };
+        int ids[kMaxPass];
+#pragma unroll
+        for (int k = 0; k < kMaxPass; ++k) ids[k] = pass_id(blockIdx.x, warp + k * kQkvProd);
         int it = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
             const int s = it & 1;
             float v[2][16];
-            uint4 ph[2][2];
-            int64_t id[4];
-            bool ok[4];
+            uint2 ph[2][4];
+            int64_t id[kMaxPass];
+            bool ok[kMaxPass];
 #pragma unroll
-            for (int p = 0; p < 4; ++p) {
-                id[p] = __shfl_sync(0xffffffffu, ids, p * 4 + rl);
-                ok[p] = tile * 128 + warp * 16 + p * 4 + rl < rows;
+            for (int k = 0; k < kMaxPass; ++k) {
+                id[k] = ids[k];
+                ok[k] = k < n_my && tile * 128 + (warp + k * kQkvProd) * 4 + rl < rows;
             }
-            ids = tile_ids(tile + gridDim.x);  // prefetch the next tile's pillar ids
-            load_row_eighth<kF64>(x, x64, pe16, id[0], sub, ok[0], v[0], ph[0]);
+#pragma unroll
+            for (int k = 0; k < kMaxPass; ++k) ids[k] = pass_id(tile + gridDim.x, warp + k * kQkvProd);  // prefetch
+            load_row_quads<kF64>(x, x64, pe16, id[0], sub, ok[0], v[0], ph[0]);
             if (threadIdx.x == 0 && it < 6) FWA_TR(1 + 4 * it);
             if (it >= 2) mbar_wait(&empty[s], ((it >> 1) - 1) & 1);
             if (threadIdx.x == 0 && it < 6) FWA_TR(2 + 4 * it);
             uint8_t* A = sA + s * kTileA;
 #pragma unroll
-            for (int p = 0; p < 4; ++p) {  // rows of pass p+1 in flight while pass p is reduced
-                if (p + 1 < 4) load_row_eighth<kF64>(x, x64, pe16, id[p + 1], sub, ok[p + 1], v[(p + 1) & 1], ph[(p + 1) & 1]);
-                ln1_row_to_tile(v[p & 1], ph[p & 1], ok[p], warp * 16 + p * 4 + rl, sub, sG, sB, A, bad);
-                if (xq && ok[p]) {
+            for (int k = 0; k < kMaxPass; ++k) {  // pass k+1's rows in flight while pass k is reduced
+                if (k >= n_my) break;
+                if (k + 1 < n_my)
+                    load_row_quads<kF64>(x, x64, pe16, id[k + 1], sub, ok[k + 1], v[(k + 1) & 1], ph[(k + 1) & 1]);
+                const int r = (warp + k * kQkvProd) * 4 + rl;
+                ln1_row_to_tile(v[k & 1], ph[k & 1], ok[k], r, sub, sG, sB, A, bad);
+                if (xq && ok[k]) {
                     // the gathered fp32 row, tile-transposed for the out-proj kernel's residual:
                     // float4 ((tile*4 + cq)*8 + j)*128 + row  (cq = channel/32, j = channel%32/4)
-                    const int r = warp * 16 + p * 4 + rl;
-                    float4* q = reinterpret_cast<float4*>(xq) + ((tile * 4 + (sub >> 1)) * 8 + (sub & 1) * 4) * 128 + r;
+                    float4* q = reinterpret_cast<float4*>(xq) + (tile * 32 + sub) * 128 + r;
 #pragma unroll
-                    for (int jj = 0; jj < 4; ++jj)
-                        q[jj * 128] = make_float4(v[p & 1][4 * jj], v[p & 1][4 * jj + 1], v[p & 1][4 * jj + 2],
-                                                  v[p & 1][4 * jj + 3]);
+                    for (int i = 0; i < 4; ++i)
+                        q[i * 1024] = make_float4(v[k & 1][4 * i], v[k & 1][4 * i + 1], v[k & 1][4 * i + 2],
+                                                  v[k & 1][4 * i + 3]);
                 }
             }
             fence_proxy_async_smem();
@@ -255,14 +265,16 @@ __global__ void __launch_bounds__(kQkvThreads, 1)
         }
         if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(nonfinite, 1);
     } else {
-        // ------------------------------------------------ MMA issue + epilogue (warps 8..15)
-        const int q = (warp - 8) & 3, half = (warp - 8) >> 2;  // lane quarter, column half
+        // ------------------------------------------------ MMA issue + epilogue (warps kQkvProd..15)
+        const int q = warp - kQkvProd;  // TMEM lane quarter = tile rows 32q..32q+31
+        const bool issuer = warp == kQkvProd && lane == 0;
         const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+        const int erow = q * 32 + lane, rot = (lane >> 1) & 3;
         constexpr uint32_t idesc = idesc_bf16_f32(128, 128);
-        int it = 0;
+        int it = 0, sit = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
             const int s = it & 1;
-            if (warp == 8 && lane == 0) {
+            if (issuer) {
                 if (it == 0) mbar_wait(wbar, 0);
                 mbar_wait(&full[s], (it >> 1) & 1);
                 fence_after_sync();
@@ -283,41 +295,60 @@ __global__ void __launch_bounds__(kQkvThreads, 1)
             __syncwarp();
             mbar_wait(done, it & 1);
             fence_after_sync();
-            if (warp == 8 && lane == 0 && it < 6) FWA_TR(31 + 4 * it);
-            const int64_t grow = tile * 128 + q * 32 + lane;
+            if (issuer && it < 6) FWA_TR(31 + 4 * it);
+            const int64_t vrows = rows - tile * 128 < 128 ? rows - tile * 128 : 128;
+            // TMEM -> +bias -> bf16 rows staged in shared memory (the 64 B row pieces written
+            // in a lane-rotated order: conflict-free), then each chunk's [rows x 32] block --
+            // contiguous in the chunk-major qkv layout -- leaves by one bulk TMA store.
 #pragma unroll 1
-            for (int ch = half * 6; ch < half * 6 + 6; ch += 2) {
+            for (int ch = 0; ch < 12; ch += 2, ++sit) {
                 uint32_t v[32], u[32];
                 tmem_ld32(tmem + lane_off + ch * 32, v);
                 tmem_ld32(tmem + lane_off + ch * 32 + 32, u);
                 tmem_ld_wait();
-                if (grow < rows) {
+                uint8_t* stg = sStage + (sit & 1) * 16384;
 #pragma unroll
-                    for (int hh = 0; hh < 2; ++hh) {
-                        const uint32_t* src = hh ? u : v;
-                        const float* bias = sBias + (ch + hh) * 32;
-                        uint32_t o[16];
+                for (int hh = 0; hh < 2; ++hh) {
+                    const uint32_t* src = hh ? u : v;
+                    const float* bias = sBias + (ch + hh) * 32;
+                    uint4 P[4];
 #pragma unroll
-                        for (int j = 0; j < 16; ++j)
-                            o[j] = pack_bf16x2(__uint_as_float(src[2 * j]) + bias[2 * j],
-                                               __uint_as_float(src[2 * j + 1]) + bias[2 * j + 1]);
-                        uint4* dst = reinterpret_cast<uint4*>(qkv + (static_cast<int64_t>(ch + hh) * rows + grow) * 32);
+                    for (int j = 0; j < 4; ++j) {
+                        const float4 b0 = *reinterpret_cast<const float4*>(bias + 8 * j);
+                        const float4 b1 = *reinterpret_cast<const float4*>(bias + 8 * j + 4);
+                        P[j] = make_uint4(pack_bf16x2(__uint_as_float(src[8 * j]) + b0.x, __uint_as_float(src[8 * j + 1]) + b0.y),
+                                          pack_bf16x2(__uint_as_float(src[8 * j + 2]) + b0.z, __uint_as_float(src[8 * j + 3]) + b0.w),
+                                          pack_bf16x2(__uint_as_float(src[8 * j + 4]) + b1.x, __uint_as_float(src[8 * j + 5]) + b1.y),
+                                          pack_bf16x2(__uint_as_float(src[8 * j + 6]) + b1.z, __uint_as_float(src[8 * j + 7]) + b1.w));
+                    }
+                    uint8_t* rowp = stg + hh * 8192 + erow * 64;
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) dst[j] = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+                    for (int jj = 0; jj < 4; ++jj) {
+                        const int j = (jj + rot) & 3;
+                        *reinterpret_cast<uint4*>(rowp + j * 16) = pick4(P, j);
                     }
                 }
+                fence_proxy_async_smem();
+                fence_before_sync();  // on the last pair: TMEM drained before the next tile's MMA
+                if (issuer) bulk_wait_read_all();  // the other buffer's store has left shared memory
+                asm volatile("bar.sync 1, %0;" ::"n"((16 - kQkvProd) * 32) : "memory");
+                if (issuer) {
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh)
+                        bulk_s2g(qkv + (static_cast<int64_t>(ch + hh) * rows + tile * 128) * 32, stg + hh * 8192,
+                                 static_cast<uint32_t>(vrows * 64));
+                    bulk_commit();
+                }
             }
-            fence_before_sync();
-            asm volatile("bar.sync 1, 256;" ::: "memory");  // TMEM drained before the next MMA
-            fence_after_sync();
-            if (warp == 8 && lane == 0 && it < 6) FWA_TR(32 + 4 * it);
+            if (issuer && it < 6) FWA_TR(32 + 4 * it);
         }
-        if (warp == 8 && lane == 0) FWA_TR(60);
+        if (issuer) bulk_wait_all();
+        if (warp == kQkvProd && lane == 0) FWA_TR(60);
     }
     fence_before_sync();
     __syncthreads();
     fence_after_sync();
-    if (warp == 8) tmem_dealloc(tmem, 512);
+    if (warp == kQkvProd) tmem_dealloc(tmem, 512);
 }
 
 void launch_ln1_qkv_tc(const float* x, const double* x64, const __half* pe, const int32_t* idx,

@@ -40,6 +40,18 @@ FWA_DEVINL void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b
         : "memory");
 }
 
+// 1-D bulk async copy shared -> global (TMA engine), tracked by bulk async-groups.
+FWA_DEVINL void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+FWA_DEVINL void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// every committed store has finished READING shared memory (the buffer may be reused)
+FWA_DEVINL void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+// every committed store is complete
+FWA_DEVINL void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 // ---- programmatic dependent launch (PDL): the next kernel in the stream may start
 // its prologue (barrier init, TMEM alloc, weight TMA) while this one drains; data
 // produced by the previous kernel is read only after griddep_wait().
