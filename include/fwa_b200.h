@@ -50,7 +50,9 @@ enum fwa_status {
 enum fwa_precision {
     FWA_PREC_BF16 = 0, /* tcgen05/TMEM GEMMs + mma.sync attention, bf16 operands, fp32
                           accumulate / LN / softmax / residual (default) */
-    FWA_PREC_FP32 = 1  /* fp32 FFMA check mode (tolerance 1e-4) */
+    FWA_PREC_FP32 = 1, /* fp32 FFMA check mode (tolerance 1e-4) */
+    FWA_PREC_BF16_3K = 2 /* bf16 numerics as FWA_PREC_BF16, but the three-kernel block pipeline
+                            instead of the fused CTA-pair block kernel (A/B and regression) */
 };
 
 /* fwa::backbone::FwaConfig (backbone.hpp:22-34).  Window metres are

@@ -39,7 +39,8 @@ EXPORTS = [
     "fwa_b200_split_begin", "fwa_b200_split_block", "fwa_b200_split_scatter",
 ]
 
-PREC_BF16, PREC_FP32 = 0, 1
+PREC_BF16, PREC_FP32, PREC_BF16_3K = 0, 1, 2
+_PREC = {"bf16": PREC_BF16, "fp32": PREC_FP32, "bf16_3k": PREC_BF16_3K}
 
 
 # ----------------------------------------------------------------------------- errors (error.hpp)
@@ -288,7 +289,9 @@ class Context:
             raise _ERRS.get(rc, FwaError)(msg)
 
     def set_precision(self, precision: str):
-        self._check(lib().fwa_b200_set_precision(self._h, PREC_FP32 if precision == "fp32" else PREC_BF16))
+        if precision not in _PREC:
+            raise ValueError(f"precision must be one of {sorted(_PREC)}")
+        self._check(lib().fwa_b200_set_precision(self._h, _PREC[precision]))
         self.precision = precision
 
     @property

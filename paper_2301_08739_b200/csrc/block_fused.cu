@@ -1,0 +1,914 @@
+// One whole FlatFormer block in ONE persistent kernel on CTA pairs (bf16 fast path:
+// d_model 128, 8 heads of 16, d_ff 256, group size <= 128).
+//
+// Reference: fwa_block_forward (kernels.hpp:636-650) composed with the block loop's
+// gather / scatter (backbone.hpp:245-283):
+//   gather rows by the window-sort permutation -> LN1 + affine + PE (kernels.hpp:472-485)
+//   -> packed QKV (488-500) -> per-group, per-head softmax attention (512-548)
+//   -> out-proj + b_out + residual (550-560) -> LN2 -> W1 + b1 -> exact-erf GELU
+//   -> W2 + b2 + residual (575-633) -> scatter to the pillar-id row (278-283).
+//
+// Work unit = floor(256 / G) whole groups (3 groups = 207 rows at G = 69), owned by a
+// CTA pair (a 2-CTA cluster on one TPC): rank 0 holds unit rows [0, 128), rank 1 rows
+// [128, R).  Every GEMM is ONE tcgen05.mma.cta_group::2 with M = 256 (each CTA's 128 rows
+// as A, each CTA holding HALF of the weight's output features as B), so the four
+// weight matrices (256 KB bf16) fit the pair's shared memory: 128 KB per CTA, resident
+// for the whole kernel.  Nothing between the gather and the scatter leaves the SM pair:
+//   R_A  (32 KB, SW128 image): LN1 out -> [QKV MMA] -> Q, overwritten in place by the
+//        attention output O -> [out-proj MMA] -> LN2 out -> [FFN1] -> GELU half b
+//        -> [FFN2] -> fp32 output staging
+//   R_KV (60 KB): K|V of 4 heads per pass (272 B row pitch: conflict-free ldmatrix), plus
+//        the rows of the one group that straddles the two CTAs, PUSHED by the peer over
+//        DSMEM (st.shared::cluster) -> GELU half a (SW128 image) -> [FFN2]
+//   TMEM (512 columns): QKV [0,384) | the gathered fp32 residual rows [384,512), onto
+//        which the out-proj MMA accumulates | FFN1 U [128,384) | FFN2 O [0,128) | LN2
+//        row-statistics exchange [0,8)
+// The unit's rows are split between the pair at `split` (chosen on the host so that both
+// CTAs need the same number of attention task rounds); padding rows (A = 0) fill each
+// CTA's 128 MMA rows.
+// The leader (rank 0) thread 0 issues every MMA after both CTAs arrive on its "ready"
+// mbarrier (remote arrive from rank 1); commits are multicast to both CTAs.
+//
+// Attention: tasks = (head, 16-query tile of one group part); QK^T and PV on
+// mma.sync.m16n8k16 (bf16, fp32 accumulate); max-subtracted softmax with the exponent
+// argument in fp32 and ex2.approx.bf16x2 producing P directly as the PV operand; the row
+// sums come out of the PV MMA (an all-ones B fragment), so they are the sums of exactly
+// the P values that are multiplied with V.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "internal.h"
+#include "tcgen05.cuh"
+
+namespace fwa_b200 {
+
+using namespace tc;
+
+namespace {
+
+constexpr int kThreads = 512;
+constexpr int kWBytes = 131072;  // per-rank weight image
+constexpr int kOffWqkv = 0, kOffWout = 49152, kOffW1 = 65536, kOffW2 = 98304;
+constexpr int kOffRA = kWBytes;                 // 32768
+constexpr int kOffKV = kOffRA + 32768;          // 163840
+constexpr int kKVPitch = 272;
+constexpr int kKVRows = 224;
+constexpr int kOffVec = kOffKV + kKVRows * kKVPitch;  // 224768
+constexpr int kVecFloats = 1152;  // b_qkv 384 | b_out 128 | b2 128 | b1' 256 | ln1_g 128 | ln1_b 128
+constexpr int kOffBars = kOffVec + kVecFloats * 4;    // 229376
+constexpr int kSmem = kOffBars + 128 + 1024;          // + base-alignment slack
+static_assert(kSmem <= 232448, "shared memory budget");
+
+// ---------------------------------------------------------------- cluster / pair PTX
+FWA_DEVINL uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+FWA_DEVINL uint32_t mapa(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+FWA_DEVINL void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+FWA_DEVINL void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+FWA_DEVINL void mbar_wait_acq_cluster(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAITC_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+FWA_DEVINL void st_cluster_v4(uint32_t addr, uint4 v) {
+    asm volatile("st.shared::cluster.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+FWA_DEVINL void tmem_alloc2(uint32_t* dst_smem, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+FWA_DEVINL void tmem_dealloc2(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+// D[tmem] (+)= A[smem, both CTAs] * B[smem, both CTAs]^T, M = 256 across the pair
+FWA_DEVINL void mma2_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+}
+// arrive on `bar` (same offset) in BOTH CTAs when the leader's prior MMAs complete
+FWA_DEVINL void mma_commit_pair(uint64_t* bar) {
+    const uint16_t mask = 3;
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
+FWA_DEVINL void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+}
+FWA_DEVINL void tmem_st1(uint32_t taddr, float v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(__float_as_uint(v))
+                 : "memory");
+}
+FWA_DEVINL void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]),
+        "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]),
+        "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]),
+        "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+        : "memory");
+}
+FWA_DEVINL void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+FWA_DEVINL float4 tmem_ld4(uint32_t taddr) {
+    uint32_t a, b, c, d;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    return make_float4(__uint_as_float(a), __uint_as_float(b), __uint_as_float(c), __uint_as_float(d));
+}
+FWA_DEVINL void cta_sync_tc() {
+    fence_before_sync();
+    __syncthreads();
+    fence_after_sync();
+}
+FWA_DEVINL uint8_t* align1024(uint8_t* p) { return p + ((1024u - (smem_u32(p) & 1023u)) & 1023u); }
+
+// ---------------------------------------------------------------- attention helpers
+FWA_DEVINL void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+FWA_DEVINL void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+FWA_DEVINL void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                         uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// P = 2^x for two fp32 exponent arguments -> bf16x2 (the PV A-operand format);
+// -inf -> +0.  The bf16 rounding of x (|x| 2^-9) is below the bf16 rounding of P.
+FWA_DEVINL uint32_t ex2_bf16x2(float lo, float hi) {
+    uint32_t x = pack_bf16x2(lo, hi), y;
+    asm("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
+// byte offset of element (row, col) in a 128-row K-major SW128 bf16 image
+FWA_DEVINL uint32_t img_off(int row, int col) {
+    return static_cast<uint32_t>((col >> 6) * 16384 + row * 128 + ((((col & 63) >> 3) ^ (row & 7)) << 4) +
+                                 (col & 7) * 2);
+}
+
+// One attention task: head `head` (K/V at pass-local slot hp), query rows [m0, m0+16)
+// of a group whose keys are the extended rows [ke0, ke0 + G); rows >= qend are computed
+// but not stored.  Q is read from and O written to the R_A image (same cells).
+template <int NT, int GC>
+FWA_DEVINL void attn_task(uint32_t sRA, uint32_t sKV, uint8_t* pRA, int head, int hp, int m0, int qend,
+                          int ke0, int G_rt) {
+    const int G = GC > 0 ? GC : G_rt;
+    const int lane = threadIdx.x & 31;
+    const int g = lane >> 2, t4 = lane & 3;
+    constexpr float kScaleLog2 = 0.25f * 1.4426950408889634f;  // (1/sqrt(16)) * log2(e)
+    const int nt_live = (G + 7) >> 3;
+    uint32_t a0, a1, a2, a3;
+    {
+        const int qrow = m0 + (lane & 7) + ((lane >> 3) & 1) * 8;
+        const int col = head * 16 + (lane >> 4) * 8;
+        ldsm_x4(sRA + img_off(qrow, col), a0, a1, a2, a3);
+    }
+    uint32_t kb[NT][2];
+#pragma unroll
+    for (int np = 0; np < NT; np += 2) {
+        const int krow = ke0 + (np + (lane >> 4)) * 8 + (lane & 7);
+        ldsm_x4(sKV + krow * kKVPitch + hp * 32 + ((lane >> 3) & 1) * 16, kb[np][0], kb[np][1], kb[np + 1][0],
+                kb[np + 1][1]);
+    }
+    uint32_t vb[NT / 2][4];
+#pragma unroll
+    for (int kt = 0; kt < NT / 2; ++kt) {
+        const int vrow = ke0 + kt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+        ldsm_x4_t(sKV + vrow * kKVPitch + 128 + hp * 32 + (lane >> 4) * 16, vb[kt][0], vb[kt][1], vb[kt][2],
+                  vb[kt][3]);
+    }
+    float s[NT][4];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+        s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+        if (nt < nt_live) mma16816(s[nt], a0, a1, a2, a3, kb[nt][0], kb[nt][1]);
+    }
+    float m0v = -INFINITY, m1v = -INFINITY;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+        if (nt >= nt_live) continue;
+        if (nt * 8 + 8 > G) {
+            const int col = nt * 8 + 2 * t4;
+            if (col >= G) { s[nt][0] = -INFINITY; s[nt][2] = -INFINITY; }
+            if (col + 1 >= G) { s[nt][1] = -INFINITY; s[nt][3] = -INFINITY; }
+        }
+        m0v = fmaxf(m0v, fmaxf(s[nt][0], s[nt][1]));
+        m1v = fmaxf(m1v, fmaxf(s[nt][2], s[nt][3]));
+    }
+    m0v = fmaxf(m0v, __shfl_xor_sync(0xffffffffu, m0v, 1));
+    m0v = fmaxf(m0v, __shfl_xor_sync(0xffffffffu, m0v, 2));
+    m1v = fmaxf(m1v, __shfl_xor_sync(0xffffffffu, m1v, 1));
+    m1v = fmaxf(m1v, __shfl_xor_sync(0xffffffffu, m1v, 2));
+    const float mb0 = m0v * kScaleLog2, mb1 = m1v * kScaleLog2;
+    uint32_t p[NT][2];  // bf16x2: [0] row g, [1] row g + 8
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+        if (nt < nt_live) {
+            p[nt][0] = ex2_bf16x2(fmaf(s[nt][0], kScaleLog2, -mb0), fmaf(s[nt][1], kScaleLog2, -mb0));
+            p[nt][1] = ex2_bf16x2(fmaf(s[nt][2], kScaleLog2, -mb1), fmaf(s[nt][3], kScaleLog2, -mb1));
+        } else {
+            p[nt][0] = p[nt][1] = 0u;
+        }
+    }
+    constexpr uint32_t kOnes = 0x3F803F80u;  // bf16x2 (1, 1)
+    float o[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    float l[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int kt = 0; kt < NT / 2; ++kt) {
+        if (2 * kt >= nt_live) continue;
+        mma16816(o[0], p[2 * kt][0], p[2 * kt][1], p[2 * kt + 1][0], p[2 * kt + 1][1], vb[kt][0], vb[kt][1]);
+        mma16816(o[1], p[2 * kt][0], p[2 * kt][1], p[2 * kt + 1][0], p[2 * kt + 1][1], vb[kt][2], vb[kt][3]);
+        mma16816(l, p[2 * kt][0], p[2 * kt][1], p[2 * kt + 1][0], p[2 * kt + 1][1], kOnes, kOnes);
+    }
+    const float i0 = 1.0f / l[0], i1 = 1.0f / l[2];
+    const int r0 = m0 + g, r1 = r0 + 8;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+        const int col = head * 16 + nt * 8 + 2 * t4;
+        if (r0 < qend) *reinterpret_cast<uint32_t*>(pRA + img_off(r0, col)) = pack_bf16x2(o[nt][0] * i0, o[nt][1] * i0);
+        if (r1 < qend) *reinterpret_cast<uint32_t*>(pRA + img_off(r1, col)) = pack_bf16x2(o[nt][2] * i1, o[nt][3] * i1);
+    }
+}
+
+// ---------------------------------------------------------------- row I/O
+// One lane's 16 channels of a pillar row, 8 lanes per row: channels 32i + 4*sub + e
+// (i, e < 4), so each load instruction of the 8 lanes reads one whole 128 B line of the
+// fp32 row (64 B of the fp16 PE row).
+template <bool kF64>
+FWA_DEVINL void load_row_quads(const float* x, const double* x64, const __half* pe16, int64_t id, int sub,
+                               bool valid, float (&v)[16], uint2 (&ph)[4]) {
+    if (!valid) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = 0.f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) ph[i] = make_uint2(0u, 0u);
+        return;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        if (kF64) {
+            const double2* p = reinterpret_cast<const double2*>(x64 + id * 128 + 32 * i + 4 * sub);
+            const double2 d0 = __ldg(p), d1 = __ldg(p + 1);
+            v[4 * i] = static_cast<float>(d0.x); v[4 * i + 1] = static_cast<float>(d0.y);
+            v[4 * i + 2] = static_cast<float>(d1.x); v[4 * i + 3] = static_cast<float>(d1.y);
+        } else {
+            const float4 f4 = __ldg(reinterpret_cast<const float4*>(x + id * 128 + 32 * i + 4 * sub));
+            v[4 * i] = f4.x; v[4 * i + 1] = f4.y; v[4 * i + 2] = f4.z; v[4 * i + 3] = f4.w;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) ph[i] = __ldg(reinterpret_cast<const uint2*>(pe16 + id * 128 + 32 * i + 4 * sub));
+}
+
+// LN1 (two-pass mean / variance over the 8 lanes of a row, eps inside the sqrt,
+// kernels.hpp:235-249) + affine + PE (472-485) -> 4 x 8 B of the bf16 SW128 A image.
+FWA_DEVINL void ln1_row_to_image(const float (&v)[16], const uint2 (&ph)[4], bool valid, int r, int sub,
+                                 const float* sG, const float* sB, uint8_t* A, bool& bad) {
+    float sm = 0.f;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) sm += v[j];
+    sm += __shfl_xor_sync(0xffffffffu, sm, 1);
+    sm += __shfl_xor_sync(0xffffffffu, sm, 2);
+    sm += __shfl_xor_sync(0xffffffffu, sm, 4);
+    const float mean = sm * (1.0f / 128.0f);
+    float sq = 0.f;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        bad |= !isfinite(v[j]);
+        sq += (v[j] - mean) * (v[j] - mean);
+    }
+    sq += __shfl_xor_sync(0xffffffffu, sq, 1);
+    sq += __shfl_xor_sync(0xffffffffu, sq, 2);
+    sq += __shfl_xor_sync(0xffffffffu, sq, 4);
+    const float inv = 1.0f / sqrtf(sq * (1.0f / 128.0f) + 1e-5f);
+    __half2 pesum = __floats2half2_rn(0.f, 0.f);  // |PE| <= 1: the f16 sum cannot overflow
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int c = 32 * i + 4 * sub;
+        const float4 g = *reinterpret_cast<const float4*>(sG + c);
+        const float4 b = *reinterpret_cast<const float4*>(sB + c);
+        const __half2 h0 = *reinterpret_cast<const __half2*>(&ph[i].x);
+        const __half2 h1 = *reinterpret_cast<const __half2*>(&ph[i].y);
+        pesum = __hadd2(pesum, __hadd2(h0, h1));
+        const float2 p0 = __half22float2(h0), p1 = __half22float2(h1);
+        uint32_t o0 = pack_bf16x2(g.x * ((v[4 * i] - mean) * inv) + b.x + p0.x,
+                                  g.y * ((v[4 * i + 1] - mean) * inv) + b.y + p0.y);
+        uint32_t o1 = pack_bf16x2(g.z * ((v[4 * i + 2] - mean) * inv) + b.z + p1.x,
+                                  g.w * ((v[4 * i + 3] - mean) * inv) + b.w + p1.y);
+        if (!valid) o0 = o1 = 0u;
+        *reinterpret_cast<uint2*>(A + sw128_offset(r, c, 128)) = make_uint2(o0, o1);
+    }
+    const float2 ps = __half22float2(pesum);
+    bad |= !(isfinite(ps.x) && isfinite(ps.y));
+}
+
+// f32 row staging: row r (512 B) chunk c (16 B) at r*512 + ((c ^ (r & 7)) * 16)
+FWA_DEVINL uint32_t stage_off(int r, int c) { return static_cast<uint32_t>(r * 512 + ((c ^ (r & 7)) << 4)); }
+
+// reference exact-erf GELU (dense.hpp:67-72); see tc.cu gelu_fast for the error budget
+FWA_DEVINL float tanh_approx(float x) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+FWA_DEVINL float gelu_fast(float x) {
+    const float xc = fminf(fmaxf(x, -6.0f), 6.0f);
+    const float x2 = xc * xc;
+    const float p = fmaf(fmaf(fmaf(-4.71338576e-06f, x2, -3.19044083e-04f), x2, 3.69914203e-02f), x2,
+                         7.97462955e-01f);
+    const float t = tanh_approx(xc * p);
+    const float hx = 0.5f * x;
+    return fmaf(hx, t, hx);
+}
+
+struct FusedArgs {
+    const float* x;          // residual rows by pillar id (f32) ...
+    const double* x64;       // ... or the caller's f64 rows (block 0)
+    const __half* pe16;      // PE rows by pillar id
+    const int32_t* ridx;     // block row -> pillar id (gather)
+    const int32_t* sidx;     // block row -> output row (scatter)
+    float* x_out;
+    int64_t rows;            // n_groups * G
+    int G, gpu, n_units;
+    int split;               // rank 0 holds unit rows [0, split), rank 1 [split, R)
+    const uint8_t* wpair;    // [rank 0 image | rank 1 image], kWBytes each
+    const float* vec;        // b_qkv | b_out | b2 | b1'
+    const float *ln1_g, *ln1_b;
+    int* nonfinite;
+    unsigned long long* trace;  // FWA_B200_TRACE: 64 SM-clock slots per CTA (phase boundaries)
+};
+
+#define FTR(k)                                                                                  \
+    do {                                                                                        \
+        if (a.trace && threadIdx.x == 0 && (k) < 64)                                            \
+            a.trace[blockIdx.x * 64 + (k)] = static_cast<unsigned long long>(clock64());        \
+    } while (0)
+
+template <int NT, int GC, bool kF64>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block_fused(FusedArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = align1024(smem_raw);
+    const uint32_t rank = cluster_rank();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int q = warp & 3, cq = warp >> 2;
+    const int row = q * 32 + lane;  // local row == TMEM lane
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    const int c0 = cq * 32;
+    uint8_t* sW = smem;
+    uint8_t* pRA = smem + kOffRA;
+    uint8_t* pKV = smem + kOffKV;
+    float* sVec = reinterpret_cast<float*>(smem + kOffVec);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBars);
+    uint64_t* bW = bars;
+    uint64_t* bReady = bars + 1;  // leader only: 2 arrivals (one per CTA) per handshake
+    uint64_t* bQKV = bars + 2;
+    uint64_t* bP = bars + 3;
+    uint64_t* bUa = bars + 4;
+    uint64_t* bUb = bars + 5;
+    uint64_t* bO = bars + 6;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+    const uint32_t sRA = smem_u32(pRA), sKV = smem_u32(pKV), sWa = smem_u32(sW);
+    const bool leader = rank == 0 && threadIdx.x == 0;
+
+    if (smem - smem_raw > 1024) __trap();
+    griddep_launch_dependents();
+    if (threadIdx.x == 0) {
+        mbar_init(bW, 1);
+        mbar_init(bReady, 2);
+        for (int i = 2; i < 7; ++i) mbar_init(&bars[i], 1);
+        fence_mbar_init();
+    }
+    {
+        uint4* kv = reinterpret_cast<uint4*>(pKV);  // slack rows must hold finite values
+        for (int i = threadIdx.x; i < kKVRows * kKVPitch / 16; i += kThreads) kv[i] = make_uint4(0u, 0u, 0u, 0u);
+    }
+    for (int i = threadIdx.x; i < kVecFloats; i += kThreads)
+        sVec[i] = i < 896 ? a.vec[i] : (i < 1024 ? a.ln1_g[i - 896] : a.ln1_b[i - 1024]);
+    if (warp == 0) {
+        __syncwarp();
+        tmem_alloc2(tmem_slot, 512);
+    }
+    __syncthreads();  // barrier inits before the weight TMA uses bW
+    if (threadIdx.x == 0) {
+        mbar_arrive_expect_tx(bW, kWBytes);
+        const uint8_t* src = a.wpair + static_cast<size_t>(rank) * kWBytes;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) bulk_g2s(sW + c * 32768, src + c * 32768, 32768, bW);
+    }
+    fence_before_sync();
+    cluster_sync_all();  // peer barriers initialised, TMEM allocated in both CTAs
+    fence_after_sync();
+    const uint32_t tmem = *tmem_slot;
+    const int G = GC > 0 ? GC : a.G;
+    const int R = a.gpu * G;
+    const int npairs = static_cast<int>(gridDim.x >> 1), pair = static_cast<int>(blockIdx.x >> 1);
+    const uint32_t ready_remote = mapa(smem_u32(bReady), 0);
+    constexpr uint32_t id256 = idesc_bf16_f32(256, 128);
+    bool bad = false;
+    uint32_t hs = 0;  // handshake count (parity of bReady, leader)
+
+    // all threads: make this CTA's smem operands visible to the MMA and tell the leader
+    auto handshake = [&]() {
+        fence_proxy_async_smem();
+        fence_before_sync();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            if (rank == 0) mbar_arrive(bReady);
+            else mbar_arrive_cluster(ready_remote);
+        }
+    };
+    auto leader_wait = [&]() {
+        mbar_wait_acq_cluster(bReady, hs & 1);
+        fence_after_sync();
+    };
+
+    griddep_wait();  // x / PE / ids come from earlier kernels
+    if (threadIdx.x == 0) mbar_wait(bW, 0);
+    FTR(0);
+    int it = 0;
+    for (int u = pair; u < a.n_units; u += npairs, ++it) {
+        const uint32_t ph = it & 1;
+        const int64_t ubase = static_cast<int64_t>(u) * R;
+        const int urows = static_cast<int>(a.rows - ubase < R ? a.rows - ubase : R);
+        const int split = a.split < urows ? a.split : urows;
+        const int urow0 = rank ? split : 0;
+        const int nloc = rank ? urows - split : split;
+        // the one group that straddles the two CTAs: unit rows [S, S + G), split inside it
+        const int S = (split / G) * G;
+        const bool strad = S < split && split < urows;
+        const int h0 = strad ? split - S : 0;       // its rows in rank 0
+        const int tail = strad ? S + G - split : 0; // its rows in rank 1
+        // extended K/V rows: rank 0 = unit rows [0, split) + halo [split, split + tail);
+        // rank 1 = halo (unit rows [S, split)) at [0, h0) + its rows at h0 + r
+        const int ext0 = rank ? h0 : 0;
+        const int tb = 1 + 16 * it;
+        FTR(tb);
+
+        // ---- 1. gather (8 lanes per row: every load instruction reads whole 128 B lines)
+        //         + LN1 + affine + PE -> bf16 A image (R_A).  The fp32 rows are parked in
+        //         TMEM columns [384, 512) (through a 32 KB staging in R_KV, one 64-row half
+        //         at a time); the out-proj MMA accumulates onto them (= the residual).
+        {
+            const int sub = lane & 7, rl = lane >> 3;
+            float v[2][16];
+            uint2 pe[2][4];
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                const int r = hf * 64 + warp * 4 + rl;
+                const bool ok = r < nloc;
+                const int64_t id = ok ? (a.ridx ? a.ridx[ubase + urow0 + r] : ubase + urow0 + r) : 0;
+                load_row_quads<kF64>(a.x, a.x64, a.pe16, id, sub, ok, v[hf], pe[hf]);
+            }
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                const int r = hf * 64 + warp * 4 + rl;
+                ln1_row_to_image(v[hf], pe[hf], r < nloc, r, sub, sVec + 896, sVec + 1024, pRA, bad);
+                if (hf == 0) FTR(tb + 1);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    *reinterpret_cast<float4*>(pKV + stage_off(r & 63, 8 * i + sub)) =
+                        make_float4(v[hf][4 * i], v[hf][4 * i + 1], v[hf][4 * i + 2], v[hf][4 * i + 3]);
+                __syncthreads();
+                if ((row >> 6) == hf) {
+                    float xr[32];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const float4 f = *reinterpret_cast<const float4*>(pKV + stage_off(row & 63, 8 * cq + j));
+                        xr[4 * j] = f.x; xr[4 * j + 1] = f.y; xr[4 * j + 2] = f.z; xr[4 * j + 3] = f.w;
+                    }
+                    tmem_st32(tmem + lane_off + 384 + c0, xr);
+                    tmem_st_wait();
+                }
+                __syncthreads();
+            }
+        }
+        FTR(tb + 2);
+        handshake();
+        if (leader) {
+            leader_wait();
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                const uint64_t ad = sdesc_sw128(sRA + (ks >> 2) * 16384 + (ks & 3) * 32);
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    mma2_bf16(tmem + c * 128, ad,
+                              sdesc_sw128(sWa + kOffWqkv + c * 16384 + (ks >> 2) * 8192 + (ks & 3) * 32), id256,
+                              ks > 0);
+            }
+            mma_commit_pair(bQKV);
+        }
+        ++hs;
+
+        // ---- 2. QKV epilogue + attention, 4 heads per pass
+        mbar_wait(bQKV, ph);
+        fence_after_sync();
+        FTR(tb + 3);
+#pragma unroll 1
+        for (int pass = 0; pass < 2; ++pass) {
+            {
+                const int h = 4 * pass + cq;  // this thread's head in the epilogue
+                uint32_t qv[16], kv[16], vv[16];
+                tmem_ld16(tmem + lane_off + 16 * h, qv);
+                tmem_ld16(tmem + lane_off + 128 + 16 * h, kv);
+                tmem_ld16(tmem + lane_off + 256 + 16 * h, vv);
+                tmem_ld_wait();
+                uint4 Q[2], K[2], V[2];
+#pragma unroll
+                for (int hf = 0; hf < 2; ++hf) {
+                    uint32_t oq[4], ok[4], ov[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int j = 8 * hf + 2 * e;
+                        const float* bq = sVec + 16 * h + j;
+                        oq[e] = pack_bf16x2(__uint_as_float(qv[j]) + bq[0], __uint_as_float(qv[j + 1]) + bq[1]);
+                        ok[e] = pack_bf16x2(__uint_as_float(kv[j]) + bq[128], __uint_as_float(kv[j + 1]) + bq[129]);
+                        ov[e] = pack_bf16x2(__uint_as_float(vv[j]) + bq[256], __uint_as_float(vv[j + 1]) + bq[257]);
+                    }
+                    Q[hf] = make_uint4(oq[0], oq[1], oq[2], oq[3]);
+                    K[hf] = make_uint4(ok[0], ok[1], ok[2], ok[3]);
+                    V[hf] = make_uint4(ov[0], ov[1], ov[2], ov[3]);
+                }
+#pragma unroll
+                for (int hf = 0; hf < 2; ++hf)
+                    *reinterpret_cast<uint4*>(pRA + sw128_offset(row, 16 * h + 8 * hf, 128)) = Q[hf];
+                // every extended row a key tile can touch gets finite data each unit (padding
+                // rows: bias-only K/V) -- except rank 0's padding rows under the halo
+                if (rank == 1 || row < nloc || row >= split + tail) {
+                    uint8_t* kvrow = pKV + (ext0 + row) * kKVPitch + cq * 32;
+                    reinterpret_cast<uint4*>(kvrow)[0] = K[0];
+                    reinterpret_cast<uint4*>(kvrow)[1] = K[1];
+                    reinterpret_cast<uint4*>(kvrow + 128)[0] = V[0];
+                    reinterpret_cast<uint4*>(kvrow + 128)[1] = V[1];
+                }
+                // the straddling group's rows also go to the peer's extended rows
+                int rext = -1;
+                if (strad) {
+                    if (rank == 0 && row >= S && row < split) rext = row - S;  // peer halo rows [0, h0)
+                    if (rank == 1 && row < tail) rext = split + row;           // peer halo rows [split, split + tail)
+                }
+                if (rext >= 0) {
+                    const uint32_t dst = mapa(sKV + rext * kKVPitch + cq * 32, rank ^ 1);
+                    st_cluster_v4(dst, K[0]);
+                    st_cluster_v4(dst + 16, K[1]);
+                    st_cluster_v4(dst + 128, V[0]);
+                    st_cluster_v4(dst + 144, V[1]);
+                }
+            }
+            fence_before_sync();
+            cluster_sync_all();  // local + pushed K/V and Q visible
+            FTR(tb + 4 + 2 * pass);
+            if (nloc > 0) {
+                const int gA = urow0 / G, gB = (urow0 + nloc - 1) / G;
+                int ntasks = 0;
+                for (int gg = gA; gg <= gB; ++gg) {
+                    const int qa = gg * G - urow0 < 0 ? 0 : gg * G - urow0;
+                    const int qb = gg * G + G - urow0 > nloc ? nloc : gg * G + G - urow0;
+                    ntasks += (qb - qa + 15) >> 4;
+                }
+                ntasks *= 4;
+#pragma unroll 1
+                for (int t = warp; t < ntasks; t += 16) {
+                    const int hp = t & 3;
+                    int mt = t >> 2, gg = gA, qa = 0, qb = 0;
+                    for (;; ++gg) {
+                        qa = gg * G - urow0 < 0 ? 0 : gg * G - urow0;
+                        qb = gg * G + G - urow0 > nloc ? nloc : gg * G + G - urow0;
+                        const int nm = (qb - qa + 15) >> 4;
+                        if (mt < nm) break;
+                        mt -= nm;
+                    }
+                    attn_task<NT, GC>(sRA, sKV, pRA, 4 * pass + hp, hp, qa + 16 * mt, qb, gg * G - urow0 + ext0, G);
+                }
+            }
+            if (pass == 0) cluster_sync_all();  // pass-0 K/V fully consumed before pass-1 writes / pushes
+            FTR(tb + 5 + 2 * pass);
+        }
+
+        // ---- 3. out-proj: P = O Wout^T (TMEM [0,128)); residual reload overlaps the MMA
+        handshake();
+        if (leader) {
+            leader_wait();
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks)
+                mma2_bf16(tmem + 384, sdesc_sw128(sRA + (ks >> 2) * 16384 + (ks & 3) * 32),
+                          sdesc_sw128(sWa + kOffWout + (ks >> 2) * 8192 + (ks & 3) * 32), id256, 1u);
+            mma_commit_pair(bP);
+        }
+        ++hs;
+        float x1[32];
+        mbar_wait(bP, ph);
+        fence_after_sync();
+        FTR(tb + 8);
+        {
+            uint32_t v[32];
+            tmem_ld32(tmem + lane_off + 384 + c0, v);  // x + P (the MMA accumulated onto x)
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) x1[j] = __uint_as_float(v[j]) + sVec[384 + c0 + j];
+        }
+        // ---- 4. LN2 (affine folded into W1 / b1) -> R_A
+        {
+            float sm = 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) sm += x1[j];
+            tmem_st1(tmem + lane_off + cq, sm);
+            tmem_st_wait();
+            cta_sync_tc();
+            float4 ps = tmem_ld4(tmem + lane_off);
+            const float mean = ((ps.x + ps.y) + (ps.z + ps.w)) * (1.0f / 128.0f);
+            float v2 = 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v2 += (x1[j] - mean) * (x1[j] - mean);
+            tmem_st1(tmem + lane_off + 4 + cq, v2);
+            tmem_st_wait();
+            cta_sync_tc();
+            ps = tmem_ld4(tmem + lane_off + 4);
+            const float inv = 1.0f / sqrtf(((ps.x + ps.y) + (ps.z + ps.w)) * (1.0f / 128.0f) + 1e-5f);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                uint32_t o[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int k = 8 * j + 2 * e;
+                    o[e] = pack_bf16x2((x1[k] - mean) * inv, (x1[k + 1] - mean) * inv);
+                }
+                *reinterpret_cast<uint4*>(pRA + sw128_offset(row, c0 + 8 * j, 128)) = make_uint4(o[0], o[1], o[2], o[3]);
+            }
+        }
+        FTR(tb + 9);
+        handshake();
+        if (leader) {
+            leader_wait();
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks)
+                    mma2_bf16(tmem + 128 + 128 * hh, sdesc_sw128(sRA + (ks >> 2) * 16384 + (ks & 3) * 32),
+                              sdesc_sw128(sWa + kOffW1 + hh * 16384 + (ks >> 2) * 8192 + (ks & 3) * 32), id256,
+                              ks > 0);
+                mma_commit_pair(hh ? bUb : bUa);
+            }
+        }
+        ++hs;
+        // ---- 5. GELU halves -> act_a (R_KV image), act_b (R_A image); FFN2 accumulates
+#pragma unroll 1
+        for (int hh = 0; hh < 2; ++hh) {
+            mbar_wait(hh ? bUb : bUa, ph);
+            fence_after_sync();
+            FTR(tb + 10 + 2 * hh);
+            uint8_t* act = hh ? pRA : pKV;
+            uint32_t v[32];
+            tmem_ld32(tmem + lane_off + 128 + 128 * hh + c0, v);
+            tmem_ld_wait();
+            const float* b1 = sVec + 640 + 128 * hh + c0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                uint32_t o[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int k = 8 * j + 2 * e;
+                    o[e] = pack_bf16x2(gelu_fast(__uint_as_float(v[k]) + b1[k]),
+                                       gelu_fast(__uint_as_float(v[k + 1]) + b1[k + 1]));
+                }
+                *reinterpret_cast<uint4*>(act + sw128_offset(row, c0 + 8 * j, 128)) = make_uint4(o[0], o[1], o[2], o[3]);
+            }
+            handshake();
+            if (leader) {
+                leader_wait();
+                const uint32_t a0 = smem_u32(act);
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks)
+                    mma2_bf16(tmem, sdesc_sw128(a0 + (ks >> 2) * 16384 + (ks & 3) * 32),
+                              sdesc_sw128(sWa + kOffW2 + (2 * hh + (ks >> 2)) * 8192 + (ks & 3) * 32), id256,
+                              (hh | ks) > 0);
+                if (hh) mma_commit_pair(bO);
+            }
+            ++hs;
+            FTR(tb + 11 + 2 * hh);
+        }
+        // ---- 6. out = x1 + (O + b2) -> staged in R_A (two 64-row halves) -> row scatter
+        mbar_wait(bO, ph);
+        fence_after_sync();
+        FTR(tb + 14);
+        {
+            uint32_t v[32];
+            tmem_ld32(tmem + lane_off + c0, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) x1[j] = x1[j] + (__uint_as_float(v[j]) + sVec[512 + c0 + j]);
+        }
+#pragma unroll 1
+        for (int hf = 0; hf < 2; ++hf) {
+            if ((row >> 6) == hf) {
+                const int rr = row & 63;
+#pragma unroll
+                for (int j = 0; j < 32; j += 4)
+                    *reinterpret_cast<float4*>(pRA + stage_off(rr, (c0 + j) >> 2)) =
+                        make_float4(x1[j], x1[j + 1], x1[j + 2], x1[j + 3]);
+            }
+            __syncthreads();
+            {
+                const int rbase = warp * 4;  // 16 warps x 4 rows = the 64 rows of this half
+                const int lr0 = hf * 64 + rbase;
+                int myid = 0;
+                if (lane < 4 && lr0 + lane < nloc) {
+                    const int64_t gl = ubase + urow0 + lr0 + lane;
+                    myid = a.sidx ? a.sidx[gl] : static_cast<int>(gl);
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int64_t id = __shfl_sync(0xffffffffu, myid, i);
+                    const float4 o = *reinterpret_cast<const float4*>(pRA + stage_off(rbase + i, lane));
+                    if (lr0 + i < nloc) reinterpret_cast<float4*>(a.x_out + id * 128)[lane] = o;
+                }
+            }
+            __syncthreads();
+        }
+        FTR(tb + 15);
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(a.nonfinite, 1);
+    fence_before_sync();
+    cluster_sync_all();
+    fence_after_sync();
+    if (warp == 0) tmem_dealloc2(tmem, 512);
+}
+
+template <int NT, int GC, bool kF64>
+int max_pairs() {
+    static int n = -1;
+    if (n < 0) {
+        cudaFuncSetAttribute(k_block_fused<NT, GC, kF64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(2 * kNumSMs);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = kSmem;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int c = 0;
+        if (cudaOccupancyMaxActiveClusters(&c, k_block_fused<NT, GC, kF64>, &cfg) != cudaSuccess || c <= 0) {
+            cudaGetLastError();
+            c = kNumSMs / 2;
+        }
+        n = c;
+    }
+    return n;
+}
+
+template <int NT, int GC, bool kF64>
+void launch_t(const FusedArgs& a, cudaStream_t s) {
+    const int np = max_pairs<NT, GC, kF64>();
+    const int pairs = a.n_units < np ? a.n_units : np;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_block_fused<NT, GC, kF64>, a);
+}
+
+template <int NT, int GC>
+void launch_nt(const FusedArgs& a, bool f64, cudaStream_t s) {
+    if (f64) launch_t<NT, GC, true>(a, s);
+    else launch_t<NT, GC, false>(a, s);
+}
+
+// the rows of the extended K/V region one unit touches (both ranks), for the unit
+// geometry of group size G (the full unit; a partial last unit touches a subset)
+int kernel_nt(int G) {
+    const int nt = ((G + 15) / 16) * 2;
+    return G == 69 ? 10 : nt <= 4 ? 4 : nt <= 8 ? 8 : nt <= 12 ? 12 : 16;
+}
+
+// rows of the extended K/V region a full unit touches (both ranks) for group size G
+// and row split `split`; a partial last unit touches a subset
+int ext_rows_needed(int G, int split) {
+    const int gpu = 256 / G, R = gpu * G;
+    const int NT = kernel_nt(G);
+    const int S = (split / G) * G;
+    const bool strad = S < split && split < R;
+    const int h0 = strad ? split - S : 0, tail = strad ? S + G - split : 0;
+    int need = split + tail;
+    if (h0 + (R - split) > need) need = h0 + (R - split);
+    for (int g = 0; g < gpu; ++g) {
+        const int gs = g * G;
+        if (gs < split && gs + NT * 8 > need) need = gs + NT * 8;
+        if (gs + G > split) {
+            const int ke = (gs > split ? gs - split : 0) + (gs >= split ? h0 : 0);
+            if (ke + NT * 8 > need) need = ke + NT * 8;
+        }
+    }
+    return need;
+}
+
+// attention m-tiles of the rows [r0, r1) of a unit (16-query tiles per group part)
+int mtiles(int G, int r0, int r1) {
+    int n = 0;
+    for (int g = r0 / G; g * G < r1; ++g) {
+        const int a = g * G > r0 ? g * G : r0, b = g * G + G < r1 ? g * G + G : r1;
+        n += (b - a + 15) / 16;
+    }
+    return n;
+}
+
+// the row split of a full unit: fewest attention task rounds (4 heads x m-tiles per
+// pass over 16 warps) on the slower CTA, then the most even split of the rows
+int choose_split(int G) {
+    const int R = (256 / G) * G;
+    int best = -1, best_rounds = 1 << 30, best_skew = 1 << 30;
+    for (int s = R - 128 > 1 ? R - 128 : 1; s <= 128 && s <= R; ++s) {
+        if (ext_rows_needed(G, s) > kKVRows) continue;
+        const int t0 = 4 * mtiles(G, 0, s), t1 = 4 * mtiles(G, s, R);
+        const int rounds = ((t0 + 15) / 16 > (t1 + 15) / 16) ? (t0 + 15) / 16 : (t1 + 15) / 16;
+        const int skew = s > R - s ? s - (R - s) : (R - s) - s;
+        if (rounds < best_rounds || (rounds == best_rounds && skew < best_skew)) {
+            best = s;
+            best_rounds = rounds;
+            best_skew = skew;
+        }
+    }
+    return best;
+}
+
+}  // namespace
+
+bool block_fused_supported(int G) { return G >= 1 && G <= 128 && choose_split(G) > 0; }
+
+void launch_block_fused(const float* x, const double* x64, const __half* pe16, const int32_t* ridx,
+                        const int32_t* sidx, float* x_out, int64_t rows, int G, const TcBlockWeights& w,
+                        int* d_nonfinite, cudaStream_t s, int64_t* launches, unsigned long long* trace) {
+    if (rows <= 0) return;
+    FusedArgs a{};
+    a.x = x; a.x64 = x64; a.pe16 = pe16; a.ridx = ridx; a.sidx = sidx; a.x_out = x_out;
+    a.rows = rows; a.G = G; a.gpu = 256 / G;
+    a.split = choose_split(G);
+    const int64_t n_groups = rows / G;
+    a.n_units = static_cast<int>((n_groups + a.gpu - 1) / a.gpu);
+    a.wpair = w.w_pair; a.vec = w.vec; a.ln1_g = w.ln1_g; a.ln1_b = w.ln1_b; a.nonfinite = d_nonfinite;
+    a.trace = trace;
+    const bool f64 = x64 != nullptr;
+    switch (kernel_nt(G)) {
+        case 10: launch_nt<10, 69>(a, f64, s); break;  // FwaConfig default group size (backbone.hpp:26)
+        case 4: launch_nt<4, 0>(a, f64, s); break;
+        case 8: launch_nt<8, 0>(a, f64, s); break;
+        case 12: launch_nt<12, 0>(a, f64, s); break;
+        default: launch_nt<16, 0>(a, f64, s); break;
+    }
+    ++*launches;
+}
+
+}  // namespace fwa_b200

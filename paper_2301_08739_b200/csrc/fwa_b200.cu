@@ -219,7 +219,7 @@ void validate_cfg(const fwa_config_t* c) {
 }
 
 bool fast_path_ok(const fwa_b200_ctx* c, int d, int h, int dff, int G) {
-    return c->precision == FWA_PREC_BF16 && d == 128 && dff == 256 && h > 0 && d / h == 16 &&
+    return c->precision != FWA_PREC_FP32 && d == 128 && dff == 256 && h > 0 && d / h == 16 &&
            G >= 1 && G <= 128;
 }
 
@@ -282,7 +282,7 @@ std::vector<BlockParams> upload_block_params(const std::vector<Record>& recs, De
     const float* base = static_cast<const float*>(pf32.p);
     std::vector<BlockParams> blocks(nb);
     const bool tc = d == 128 && dff == 256;
-    const size_t tc_elems = 384 * 128 + 128 * 128 + 256 * 128 + 128 * 256;
+    const size_t tc_elems = 2 * (384 * 128 + 128 * 128 + 256 * 128 + 128 * 256);  // + pair images
     // per block, after the bf16 images: f32 [b_qkv 384 | b_out 128 | b2 128 | b1' 256]
     constexpr size_t kTcVec = 896;
     std::vector<uint16_t> sw;
@@ -341,12 +341,14 @@ std::vector<BlockParams> upload_block_params(const std::vector<Record>& recs, De
             for (int i = 0; i < 128; ++i) tcv[b * kTcVec + 384 + i] = hw_out[d * d + i];          // b_out
             for (int i = 0; i < 128; ++i) tcv[b * kTcVec + 512 + i] = hw2[static_cast<size_t>(d) * dff + i];  // b2
             swizzle_weight_bf16(hw2, 128, 256, o + 384 * 128 + 128 * 128 + 256 * 128);
+            build_pair_images(hw_qkv, hw_out, w1f.data(), hw2, o + tc_elems / 2);
             const __nv_bfloat16* dbase =
                 static_cast<const __nv_bfloat16*>(pbf16.p) + b * tc_elems;
             bp.tc.w_qkv = dbase;
             bp.tc.w_out = dbase + 384 * 128;
             bp.tc.w1 = dbase + 384 * 128 + 128 * 128;
             bp.tc.w2 = dbase + 384 * 128 + 128 * 128 + 256 * 128;
+            bp.tc.w_pair = reinterpret_cast<const uint8_t*>(dbase + tc_elems / 2);
             const float* vbase = reinterpret_cast<const float*>(
                                      static_cast<const __nv_bfloat16*>(pbf16.p) + tc_elems * nb) +
                                  b * kTcVec;
@@ -655,6 +657,17 @@ void run_block(fwa_b200_ctx* c, const BlockParams& p, const fwa_config_t* cfg, i
     cudaStream_t st = c->stream;
     const int d = cfg->d_model, dff = cfg->d_ff, G = cfg->group_size;
     if (rows == 0) return;
+    if (fast && c->precision == FWA_PREC_BF16 && block_fused_supported(G)) {
+        static const bool trace_fused = [] {
+            const char* v = std::getenv("FWA_B200_TRACE");
+            return v && v[0] == '1';
+        }();
+        unsigned long long* tr = trace_fused && !x_in64 ? ws<unsigned long long>(c, "trace", 2 * 148 * 64) : nullptr;
+        StageEv t(c, FWA_PROF_OUTPROJ_FFN);
+        launch_block_fused(x_in, x_in64, pe16, ridx, sidx, x_out, rows, G, p.tc, c->d_flag, st, &c->launches, tr);
+        check_launch("k_block_fused");
+        return;
+    }
     if (fast) {
         __nv_bfloat16* qkv = ws<__nv_bfloat16>(c, "qkv16", static_cast<size_t>(rows) * 3 * d);
         // attention output as per-128-row-tile SW128 images (the out-proj A operand)
@@ -967,7 +980,7 @@ const char* fwa_b200_last_error(const fwa_b200_ctx* c) { return c ? c->err.c_str
 
 int fwa_b200_set_precision(fwa_b200_ctx* c, int precision) {
     if (!c) return FWA_ERR_CONFIG;
-    if (precision != FWA_PREC_BF16 && precision != FWA_PREC_FP32) {
+    if (precision != FWA_PREC_BF16 && precision != FWA_PREC_FP32 && precision != FWA_PREC_BF16_3K) {
         c->err = "unknown precision";
         return FWA_ERR_CONFIG;
     }

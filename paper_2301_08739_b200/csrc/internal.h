@@ -119,6 +119,10 @@ struct TcBlockWeights {
     const __nv_bfloat16* w2;    // 128 x 256, swizzled
     const float* vec;           // [b_qkv 384 | b_out 128 | b2 128 | b1 + W1 b2ln 256]
     const float *ln1_g, *ln1_b;
+    // CTA-pair images for the fused block kernel: [rank 0 | rank 1], 128 KB each; rank v
+    // holds output-feature rows [64v, 64v+64) of every 128-row weight chunk:
+    // W_qkv chunks q,k,v (3 x 16 KB) | W_out (16 KB) | W1' halves (2 x 16 KB) | W2 (32 KB)
+    const uint8_t* w_pair;
 };
 // Host-side: write the UMMA SW128 K-major smem image of a row-major f32
 // [rows x k] weight as bf16 (rows multiple of 8, k multiple of 64).
@@ -135,6 +139,17 @@ void launch_outproj_ffn_tc(const __nv_bfloat16* cat, const float* x_in, const do
                            const int32_t* ridx, int64_t rows, const TcBlockWeights& w,
                            float* x_out, const int32_t* sidx, const float* xq, cudaStream_t s,
                            int64_t* launches, unsigned long long* trace = nullptr);
+
+// One whole block (gather .. scatter) in one persistent kernel on CTA pairs
+// (block_fused.cu); supported group sizes: see block_fused_supported.
+bool block_fused_supported(int G);
+void launch_block_fused(const float* x, const double* x64, const __half* pe16, const int32_t* ridx,
+                        const int32_t* sidx, float* x_out, int64_t rows, int G, const TcBlockWeights& w,
+                        int* d_nonfinite, cudaStream_t s, int64_t* launches,
+                        unsigned long long* trace = nullptr);
+// host: the per-rank pair images (2 x 128 KB) of one block's weights (W1 LN2-folded)
+void build_pair_images(const float* w_qkv, const float* w_out, const float* w1f, const float* w2,
+                       uint16_t* out /* 2 * 65536 bf16 */);
 
 // ------------------------------------------------------------------ misc
 void launch_scatter_rows(const float* src, const int32_t* ids, const uint32_t* rank, int64_t n,

@@ -47,6 +47,17 @@ void swizzle_weight_bf16(const float* w, int rows, int k, uint16_t* out) {
             out[sw128_offset(r, c, rows) / 2] = f32_to_bf16_rn(w[static_cast<size_t>(r) * k + c]);
 }
 
+void build_pair_images(const float* w_qkv, const float* w_out, const float* w1f, const float* w2,
+                       uint16_t* out) {
+    for (int v = 0; v < 2; ++v) {
+        uint16_t* o = out + v * 65536;  // 128 KB per rank
+        for (int c = 0; c < 3; ++c) swizzle_weight_bf16(w_qkv + (128 * c + 64 * v) * 128, 64, 128, o + c * 8192);
+        swizzle_weight_bf16(w_out + 64 * v * 128, 64, 128, o + 24576);
+        for (int h = 0; h < 2; ++h) swizzle_weight_bf16(w1f + (128 * h + 64 * v) * 128, 64, 128, o + 32768 + h * 8192);
+        swizzle_weight_bf16(w2 + 64 * v * 256, 64, 256, o + 49152);
+    }
+}
+
 // Phase tracing (FWA_B200_TRACE=1): SM clock at phase boundaries, 64 slots per CTA.
 #define FWA_TR(k)                                                                         \
     do {                                                                                  \
