@@ -12,14 +12,17 @@
 // CTA pair (a 2-CTA cluster on one TPC): rank 0 holds unit rows [0, 128), rank 1 rows
 // [128, R).  Every GEMM is ONE tcgen05.mma.cta_group::2 with M = 256 (each CTA's 128 rows
 // as A, each CTA holding HALF of the weight's output features as B), so the four
-// weight matrices (256 KB bf16) fit the pair's shared memory: 128 KB per CTA, resident
-// for the whole kernel.  Nothing between the gather and the scatter leaves the SM pair:
+// weight matrices (256 KB bf16) fit the pair's shared memory: 128 KB per CTA.  Nothing
+// between the gather and the scatter leaves the SM pair:
 //   R_A  (32 KB, SW128 image): LN1 out -> [QKV MMA] -> Q, overwritten in place by the
 //        attention output O -> [out-proj MMA] -> LN2 out -> [FFN1] -> GELU half b
 //        -> [FFN2] -> fp32 output staging
-//   R_KV (60 KB): K|V of 4 heads per pass (272 B row pitch: conflict-free ldmatrix), plus
-//        the rows of the one group that straddles the two CTAs, PUSHED by the peer over
-//        DSMEM (st.shared::cluster) -> GELU half a (SW128 image) -> [FFN2]
+//   K/V  (92 KB = the W2 slot + R_X): K|V rows of all 8 heads (528 B pitch:
+//        conflict-free ldmatrix), plus the rows of the one group that straddles the two
+//        CTAs, PUSHED by the peer over DSMEM (st.async, completing transaction bytes on
+//        the receiver's mbarrier); W2 is re-fetched from L2 into its slot (TMA bulk) once
+//        the unit's attention is done
+//   R_X  (60 KB): LN1 fp32 staging -> ... -> GELU half a (SW128 image) -> [FFN2]
 //   TMEM (512 columns): QKV [0,384) | the gathered fp32 residual rows [384,512), onto
 //        which the out-proj MMA accumulates | FFN1 U [128,384) | FFN2 O [0,128) | LN2
 //        row-statistics exchange [0,8)
@@ -30,10 +33,9 @@
 // mbarrier (remote arrive from rank 1); commits are multicast to both CTAs.
 //
 // Attention: tasks = (head, 16-query tile of one group part); QK^T and PV on
-// mma.sync.m16n8k16 (bf16, fp32 accumulate); max-subtracted softmax with the exponent
-// argument in fp32 and ex2.approx.bf16x2 producing P directly as the PV operand; the row
-// sums come out of the PV MMA (an all-ones B fragment), so they are the sums of exactly
-// the P values that are multiplied with V.
+// mma.sync.m16n8k16 (bf16, fp32 accumulate); max-subtracted softmax in fp32 (ex2 on the
+// SFU, P rounded to bf16 as the PV operand); the row sums come out of the PV MMA (an
+// all-ones B fragment), so they are the sums of exactly the P values multiplied with V.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -50,16 +52,20 @@ using namespace tc;
 namespace {
 
 constexpr int kThreads = 512;
-constexpr int kWBytes = 131072;  // per-rank weight image
-constexpr int kOffWqkv = 0, kOffWout = 49152, kOffW1 = 65536, kOffW2 = 98304;
-constexpr int kOffRA = kWBytes;                 // 32768
-constexpr int kOffKV = kOffRA + 32768;          // 163840
-constexpr int kKVPitch = 272;
-constexpr int kKVRows = 224;
-constexpr int kOffVec = kOffKV + kKVRows * kKVPitch;  // 224768
+constexpr int kWBytes = 131072;  // per-rank weight image in HBM: W_qkv 48K | W_out 16K | W1' 32K | W2 32K
+constexpr int kOffWqkv = 0, kOffWout = 49152, kOffW1 = 65536;
+constexpr int kOffRA = 98304;                   // 32 KB SW128 image
+constexpr int kOffW2 = 131072;                  // 32 KB; lent to the K/V rows during attention
+constexpr int kOffKV = kOffW2;                  // K|V rows of all 8 heads over W2 + R_X
+constexpr int kOffRX = kOffW2 + 32768;          // 163840: LN1 staging / GELU-a image
+constexpr int kRXBytes = 60928;
+constexpr int kKVPitch = 528;                   // 8 x 32 B K | 8 x 32 B V | 16 B pad
+constexpr int kKVRows = (32768 + kRXBytes) / kKVPitch;  // 177
+constexpr int kOffVec = kOffRX + kRXBytes;      // 224768
 constexpr int kVecFloats = 1152;  // b_qkv 384 | b_out 128 | b2 128 | b1' 256 | ln1_g 128 | ln1_b 128
 constexpr int kOffBars = kOffVec + kVecFloats * 4;    // 229376
-constexpr int kSmem = kOffBars + 128 + 1024;          // + base-alignment slack
+constexpr int kOffTab = kOffBars + 128;               // m-tile table: 16 x int4 + count
+constexpr int kSmem = kOffTab + 512 + 1024;           // + base-alignment slack
 static_assert(kSmem <= 232448, "shared memory budget");
 
 // ---------------------------------------------------------------- cluster / pair PTX
@@ -88,9 +94,12 @@ FWA_DEVINL void mbar_wait_acq_cluster(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-FWA_DEVINL void st_cluster_v4(uint32_t addr, uint4 v) {
-    asm volatile("st.shared::cluster.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z),
-                 "r"(v.w)
+// 16 B into the peer CTA's shared memory; completes 16 transaction bytes on the peer's
+// mbarrier (both addresses in the peer's shared::cluster window)
+FWA_DEVINL void st_async_v4(uint32_t addr, uint4 v, uint32_t bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1,%2,%3,%4}, [%5];" ::"r"(
+                     addr),
+                 "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(bar)
                  : "memory");
 }
 FWA_DEVINL void tmem_alloc2(uint32_t* dst_smem, uint32_t ncols) {
@@ -178,25 +187,26 @@ FWA_DEVINL void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, u
         : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
-// P = 2^x for two fp32 exponent arguments -> bf16x2 (the PV A-operand format);
-// -inf -> +0.  The bf16 rounding of x (|x| 2^-9) is below the bf16 rounding of P.
-FWA_DEVINL uint32_t ex2_bf16x2(float lo, float hi) {
-    uint32_t x = pack_bf16x2(lo, hi), y;
-    asm("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(y) : "r"(x));
+// P = 2^x (SFU, rel err 2^-22, -inf -> +0) for two exponent arguments -> bf16x2 (the
+// PV A-operand format)
+FWA_DEVINL float ex2f(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+FWA_DEVINL uint32_t ex2_bf16x2(float lo, float hi) { return pack_bf16x2(ex2f(lo), ex2f(hi)); }
 // byte offset of element (row, col) in a 128-row K-major SW128 bf16 image
 FWA_DEVINL uint32_t img_off(int row, int col) {
     return static_cast<uint32_t>((col >> 6) * 16384 + row * 128 + ((((col & 63) >> 3) ^ (row & 7)) << 4) +
                                  (col & 7) * 2);
 }
 
-// One attention task: head `head` (K/V at pass-local slot hp), query rows [m0, m0+16)
+// One attention task: head `head`, query rows [m0, m0+16)
 // of a group whose keys are the extended rows [ke0, ke0 + G); rows >= qend are computed
 // but not stored.  Q is read from and O written to the R_A image (same cells).
 template <int NT, int GC>
-FWA_DEVINL void attn_task(uint32_t sRA, uint32_t sKV, uint8_t* pRA, int head, int hp, int m0, int qend,
-                          int ke0, int G_rt) {
+FWA_DEVINL void attn_task(uint32_t sRA, uint32_t sKV, uint8_t* pRA, int head, int m0, int qend, int ke0,
+                          int G_rt) {
     const int G = GC > 0 ? GC : G_rt;
     const int lane = threadIdx.x & 31;
     const int g = lane >> 2, t4 = lane & 3;
@@ -212,14 +222,14 @@ FWA_DEVINL void attn_task(uint32_t sRA, uint32_t sKV, uint8_t* pRA, int head, in
 #pragma unroll
     for (int np = 0; np < NT; np += 2) {
         const int krow = ke0 + (np + (lane >> 4)) * 8 + (lane & 7);
-        ldsm_x4(sKV + krow * kKVPitch + hp * 32 + ((lane >> 3) & 1) * 16, kb[np][0], kb[np][1], kb[np + 1][0],
+        ldsm_x4(sKV + krow * kKVPitch + head * 32 + ((lane >> 3) & 1) * 16, kb[np][0], kb[np][1], kb[np + 1][0],
                 kb[np + 1][1]);
     }
     uint32_t vb[NT / 2][4];
 #pragma unroll
     for (int kt = 0; kt < NT / 2; ++kt) {
         const int vrow = ke0 + kt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
-        ldsm_x4_t(sKV + vrow * kKVPitch + 128 + hp * 32 + (lane >> 4) * 16, vb[kt][0], vb[kt][1], vb[kt][2],
+        ldsm_x4_t(sKV + vrow * kKVPitch + 256 + head * 32 + (lane >> 4) * 16, vb[kt][0], vb[kt][1], vb[kt][2],
                   vb[kt][3]);
     }
     float s[NT][4];
@@ -402,6 +412,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
     uint8_t* sW = smem;
     uint8_t* pRA = smem + kOffRA;
     uint8_t* pKV = smem + kOffKV;
+    uint8_t* pRX = smem + kOffRX;
+    int4* sTab = reinterpret_cast<int4*>(smem + kOffTab);
     float* sVec = reinterpret_cast<float*>(smem + kOffVec);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBars);
     uint64_t* bW = bars;
@@ -411,7 +423,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
     uint64_t* bUa = bars + 4;
     uint64_t* bUb = bars + 5;
     uint64_t* bO = bars + 6;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+    uint64_t* bW2 = bars + 7;    // W2 re-fetch after each unit's attention
+    uint64_t* bHalo = bars + 8;  // the peer's K|V rows of the straddling group (st.async bytes)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
     const uint32_t sRA = smem_u32(pRA), sKV = smem_u32(pKV), sWa = smem_u32(sW);
     const bool leader = rank == 0 && threadIdx.x == 0;
 
@@ -420,12 +434,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
     if (threadIdx.x == 0) {
         mbar_init(bW, 1);
         mbar_init(bReady, 2);
-        for (int i = 2; i < 7; ++i) mbar_init(&bars[i], 1);
+        for (int i = 2; i < 9; ++i) mbar_init(&bars[i], 1);
         fence_mbar_init();
     }
     {
-        uint4* kv = reinterpret_cast<uint4*>(pKV);  // slack rows must hold finite values
-        for (int i = threadIdx.x; i < kKVRows * kKVPitch / 16; i += kThreads) kv[i] = make_uint4(0u, 0u, 0u, 0u);
+        uint4* rx = reinterpret_cast<uint4*>(pRX);  // K/V slack rows must hold finite values
+        for (int i = threadIdx.x; i < kRXBytes / 16; i += kThreads) rx[i] = make_uint4(0u, 0u, 0u, 0u);
     }
     for (int i = threadIdx.x; i < kVecFloats; i += kThreads)
         sVec[i] = i < 896 ? a.vec[i] : (i < 1024 ? a.ln1_g[i - 896] : a.ln1_b[i - 1024]);
@@ -438,7 +452,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         mbar_arrive_expect_tx(bW, kWBytes);
         const uint8_t* src = a.wpair + static_cast<size_t>(rank) * kWBytes;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) bulk_g2s(sW + c * 32768, src + c * 32768, 32768, bW);
+        for (int c = 0; c < 3; ++c) bulk_g2s(sW + c * 32768, src + c * 32768, 32768, bW);
+        bulk_g2s(smem + kOffW2, src + 98304, 32768, bW);
     }
     fence_before_sync();
     cluster_sync_all();  // peer barriers initialised, TMEM allocated in both CTAs
@@ -448,6 +463,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
     const int R = a.gpu * G;
     const int npairs = static_cast<int>(gridDim.x >> 1), pair = static_cast<int>(blockIdx.x >> 1);
     const uint32_t ready_remote = mapa(smem_u32(bReady), 0);
+    const uint32_t halo_remote = mapa(smem_u32(bHalo), rank ^ 1);
     constexpr uint32_t id256 = idesc_bf16_f32(256, 128);
     bool bad = false;
     uint32_t hs = 0;  // handshake count (parity of bReady, leader)
@@ -488,6 +504,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         const int ext0 = rank ? h0 : 0;
         const int tb = 1 + 16 * it;
         FTR(tb);
+        // this unit's halo: K|V (8 heads x 64 B) of the straddling group's rows held by the peer
+        if (threadIdx.x == 0) mbar_arrive_expect_tx(bHalo, static_cast<uint32_t>((rank ? h0 : tail) * 512));
 
         // ---- 1. gather (8 lanes per row: every load instruction reads whole 128 B lines)
         //         + LN1 + affine + PE -> bf16 A image (R_A).  The fp32 rows are parked in
@@ -511,14 +529,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
                 if (hf == 0) FTR(tb + 1);
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
-                    *reinterpret_cast<float4*>(pKV + stage_off(r & 63, 8 * i + sub)) =
+                    *reinterpret_cast<float4*>(pRX + stage_off(r & 63, 8 * i + sub)) =
                         make_float4(v[hf][4 * i], v[hf][4 * i + 1], v[hf][4 * i + 2], v[hf][4 * i + 3]);
                 __syncthreads();
                 if ((row >> 6) == hf) {
                     float xr[32];
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
-                        const float4 f = *reinterpret_cast<const float4*>(pKV + stage_off(row & 63, 8 * cq + j));
+                        const float4 f = *reinterpret_cast<const float4*>(pRX + stage_off(row & 63, 8 * cq + j));
                         xr[4 * j] = f.x; xr[4 * j + 1] = f.y; xr[4 * j + 2] = f.z; xr[4 * j + 3] = f.w;
                     }
                     tmem_st32(tmem + lane_off + 384 + c0, xr);
@@ -544,90 +562,91 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         }
         ++hs;
 
-        // ---- 2. QKV epilogue + attention, 4 heads per pass
+        // ---- 2. QKV epilogue (all 8 heads) + attention
         mbar_wait(bQKV, ph);
         fence_after_sync();
         FTR(tb + 3);
-#pragma unroll 1
-        for (int pass = 0; pass < 2; ++pass) {
-            {
-                const int h = 4 * pass + cq;  // this thread's head in the epilogue
-                uint32_t qv[16], kv[16], vv[16];
-                tmem_ld16(tmem + lane_off + 16 * h, qv);
-                tmem_ld16(tmem + lane_off + 128 + 16 * h, kv);
-                tmem_ld16(tmem + lane_off + 256 + 16 * h, vv);
-                tmem_ld_wait();
-                uint4 Q[2], K[2], V[2];
-#pragma unroll
-                for (int hf = 0; hf < 2; ++hf) {
-                    uint32_t oq[4], ok[4], ov[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int j = 8 * hf + 2 * e;
-                        const float* bq = sVec + 16 * h + j;
-                        oq[e] = pack_bf16x2(__uint_as_float(qv[j]) + bq[0], __uint_as_float(qv[j + 1]) + bq[1]);
-                        ok[e] = pack_bf16x2(__uint_as_float(kv[j]) + bq[128], __uint_as_float(kv[j + 1]) + bq[129]);
-                        ov[e] = pack_bf16x2(__uint_as_float(vv[j]) + bq[256], __uint_as_float(vv[j + 1]) + bq[257]);
-                    }
-                    Q[hf] = make_uint4(oq[0], oq[1], oq[2], oq[3]);
-                    K[hf] = make_uint4(ok[0], ok[1], ok[2], ok[3]);
-                    V[hf] = make_uint4(ov[0], ov[1], ov[2], ov[3]);
-                }
-#pragma unroll
-                for (int hf = 0; hf < 2; ++hf)
-                    *reinterpret_cast<uint4*>(pRA + sw128_offset(row, 16 * h + 8 * hf, 128)) = Q[hf];
-                // every extended row a key tile can touch gets finite data each unit (padding
-                // rows: bias-only K/V) -- except rank 0's padding rows under the halo
-                if (rank == 1 || row < nloc || row >= split + tail) {
-                    uint8_t* kvrow = pKV + (ext0 + row) * kKVPitch + cq * 32;
-                    reinterpret_cast<uint4*>(kvrow)[0] = K[0];
-                    reinterpret_cast<uint4*>(kvrow)[1] = K[1];
-                    reinterpret_cast<uint4*>(kvrow + 128)[0] = V[0];
-                    reinterpret_cast<uint4*>(kvrow + 128)[1] = V[1];
-                }
-                // the straddling group's rows also go to the peer's extended rows
-                int rext = -1;
-                if (strad) {
-                    if (rank == 0 && row >= S && row < split) rext = row - S;  // peer halo rows [0, h0)
-                    if (rank == 1 && row < tail) rext = split + row;           // peer halo rows [split, split + tail)
-                }
-                if (rext >= 0) {
-                    const uint32_t dst = mapa(sKV + rext * kKVPitch + cq * 32, rank ^ 1);
-                    st_cluster_v4(dst, K[0]);
-                    st_cluster_v4(dst + 16, K[1]);
-                    st_cluster_v4(dst + 128, V[0]);
-                    st_cluster_v4(dst + 144, V[1]);
-                }
-            }
-            fence_before_sync();
-            cluster_sync_all();  // local + pushed K/V and Q visible
-            FTR(tb + 4 + 2 * pass);
-            if (nloc > 0) {
-                const int gA = urow0 / G, gB = (urow0 + nloc - 1) / G;
-                int ntasks = 0;
-                for (int gg = gA; gg <= gB; ++gg) {
+        if (threadIdx.x == 0) {  // this CTA's attention m-tiles: (first query row, part end, key ext row)
+            int n = 0;
+            if (nloc > 0)
+                for (int gg = urow0 / G; gg * G < urow0 + nloc; ++gg) {
                     const int qa = gg * G - urow0 < 0 ? 0 : gg * G - urow0;
                     const int qb = gg * G + G - urow0 > nloc ? nloc : gg * G + G - urow0;
-                    ntasks += (qb - qa + 15) >> 4;
+                    for (int m0 = qa; m0 < qb; m0 += 16) sTab[n++] = make_int4(m0, qb, gg * G - urow0 + ext0, 0);
                 }
-                ntasks *= 4;
-#pragma unroll 1
-                for (int t = warp; t < ntasks; t += 16) {
-                    const int hp = t & 3;
-                    int mt = t >> 2, gg = gA, qa = 0, qb = 0;
-                    for (;; ++gg) {
-                        qa = gg * G - urow0 < 0 ? 0 : gg * G - urow0;
-                        qb = gg * G + G - urow0 > nloc ? nloc : gg * G + G - urow0;
-                        const int nm = (qb - qa + 15) >> 4;
-                        if (mt < nm) break;
-                        mt -= nm;
-                    }
-                    attn_task<NT, GC>(sRA, sKV, pRA, 4 * pass + hp, hp, qa + 16 * mt, qb, gg * G - urow0 + ext0, G);
-                }
-            }
-            if (pass == 0) cluster_sync_all();  // pass-0 K/V fully consumed before pass-1 writes / pushes
-            FTR(tb + 5 + 2 * pass);
+            sTab[16].x = n;
         }
+        // every thread: heads 2cq, 2cq+1 of its row -> Q (R_A, in place of O), K|V rows
+#pragma unroll 1
+        for (int hh = 0; hh < 2; ++hh) {
+            const int h = 2 * cq + hh;
+            uint32_t qv[16], kv[16], vv[16];
+            tmem_ld16(tmem + lane_off + 16 * h, qv);
+            tmem_ld16(tmem + lane_off + 128 + 16 * h, kv);
+            tmem_ld16(tmem + lane_off + 256 + 16 * h, vv);
+            tmem_ld_wait();
+            uint4 Q[2], K[2], V[2];
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                uint32_t oq[4], ok[4], ov[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int j = 8 * hf + 2 * e;
+                    const float* bq = sVec + 16 * h + j;
+                    oq[e] = pack_bf16x2(__uint_as_float(qv[j]) + bq[0], __uint_as_float(qv[j + 1]) + bq[1]);
+                    ok[e] = pack_bf16x2(__uint_as_float(kv[j]) + bq[128], __uint_as_float(kv[j + 1]) + bq[129]);
+                    ov[e] = pack_bf16x2(__uint_as_float(vv[j]) + bq[256], __uint_as_float(vv[j + 1]) + bq[257]);
+                }
+                Q[hf] = make_uint4(oq[0], oq[1], oq[2], oq[3]);
+                K[hf] = make_uint4(ok[0], ok[1], ok[2], ok[3]);
+                V[hf] = make_uint4(ov[0], ov[1], ov[2], ov[3]);
+            }
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf)
+                *reinterpret_cast<uint4*>(pRA + sw128_offset(row, 16 * h + 8 * hf, 128)) = Q[hf];
+            // every extended row a key tile can touch gets finite data each unit (padding
+            // rows: bias-only K/V) -- except rank 0's padding rows under the halo
+            if (rank == 1 || row < nloc || row >= split + tail) {
+                uint8_t* kvrow = pKV + (ext0 + row) * kKVPitch + h * 32;
+                reinterpret_cast<uint4*>(kvrow)[0] = K[0];
+                reinterpret_cast<uint4*>(kvrow)[1] = K[1];
+                reinterpret_cast<uint4*>(kvrow + 256)[0] = V[0];
+                reinterpret_cast<uint4*>(kvrow + 256)[1] = V[1];
+            }
+            // the straddling group's rows also go to the peer's extended rows
+            int rext = -1;
+            if (strad) {
+                if (rank == 0 && row >= S && row < split) rext = row - S;  // peer halo rows [0, h0)
+                if (rank == 1 && row < tail) rext = split + row;           // peer halo rows [split, split + tail)
+            }
+            if (rext >= 0) {
+                const uint32_t dst = mapa(sKV + rext * kKVPitch + h * 32, rank ^ 1);
+                st_async_v4(dst, K[0], halo_remote);
+                st_async_v4(dst + 16, K[1], halo_remote);
+                st_async_v4(dst + 256, V[0], halo_remote);
+                st_async_v4(dst + 272, V[1], halo_remote);
+            }
+        }
+        __syncthreads();        // local K/V, Q and the m-tile table visible
+        mbar_wait(bHalo, ph);   // the peer's halo rows have landed
+        FTR(tb + 4);
+        {
+            const int ntasks = sTab[16].x * 8;
+#pragma unroll 1
+            for (int t = warp; t < ntasks; t += 16) {
+                const int4 e = sTab[t >> 3];
+                attn_task<NT, GC>(sRA, sKV, pRA, t & 7, e.x, e.y, e.z, G);
+            }
+        }
+        FTR(tb + 5);
+        __syncthreads();  // K/V consumed: W2 comes back into its slot (needed by FFN2)
+        if (threadIdx.x == 0) {
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(bW2, 32768);
+            bulk_g2s(smem + kOffW2, a.wpair + static_cast<size_t>(rank) * kWBytes + 98304, 32768, bW2);
+        }
+        FTR(tb + 6);
+        FTR(tb + 7);
 
         // ---- 3. out-proj: P = O Wout^T (TMEM [0,128)); residual reload overlaps the MMA
         handshake();
@@ -701,7 +720,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
             mbar_wait(hh ? bUb : bUa, ph);
             fence_after_sync();
             FTR(tb + 10 + 2 * hh);
-            uint8_t* act = hh ? pRA : pKV;
+            uint8_t* act = hh ? pRA : pRX;
             uint32_t v[32];
             tmem_ld32(tmem + lane_off + 128 + 128 * hh + c0, v);
             tmem_ld_wait();
@@ -717,6 +736,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
                 }
                 *reinterpret_cast<uint4*>(act + sw128_offset(row, c0 + 8 * j, 128)) = make_uint4(o[0], o[1], o[2], o[3]);
             }
+            if (hh == 0 && threadIdx.x == 0) mbar_wait(bW2, ph);  // FFN2 reads W2 in both CTAs
             handshake();
             if (leader) {
                 leader_wait();
