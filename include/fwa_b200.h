@@ -187,6 +187,9 @@ int fwa_b200_block_forward(fwa_b200_ctx* ctx, const float* f, const float* pe, i
 /* positional_embedding: host coords N x 2 f64 -> host N x d f32. */
 int fwa_b200_positional_embedding(fwa_b200_ctx* ctx, const double* coords, int64_t n,
                                   int32_t d_model, float* out);
+/* the bf16 fast path's fp16 PE rows (IEEE binary16 bits, N x d), for parity tests */
+int fwa_b200_positional_embedding_f16(fwa_b200_ctx* ctx, const double* coords, int64_t n,
+                                      int32_t d_model, uint16_t* out);
 
 /* ---- host-side input generators (bit-identical to the reference's) ---- */
 

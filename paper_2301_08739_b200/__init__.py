@@ -35,7 +35,7 @@ EXPORTS = [
     "fwa_b200_set_profiling", "fwa_b200_get_profile", "fwa_b200_sync_check",
     "fwa_b200_backbone_forward", "fwa_b200_backbone_forward_batch",
     "fwa_b200_backbone_forward_device", "fwa_b200_sort_plan", "fwa_b200_block_forward",
-    "fwa_b200_positional_embedding", "fwa_b200_generate_pillars", "fwa_b200_init_params",
+    "fwa_b200_positional_embedding", "fwa_b200_positional_embedding_f16", "fwa_b200_generate_pillars", "fwa_b200_init_params",
     "fwa_b200_split_begin", "fwa_b200_split_block", "fwa_b200_split_scatter",
 ]
 
@@ -134,6 +134,7 @@ def lib():
         L.fwa_b200_sort_plan.argtypes = [vp, vp, i64, C.c_double, C.c_double, C.c_int, C.c_int, vp]
         L.fwa_b200_block_forward.argtypes = [vp, vp, vp, i64, i32, vp, C.c_size_t, vp]
         L.fwa_b200_positional_embedding.argtypes = [vp, vp, i64, i32, vp]
+        L.fwa_b200_positional_embedding_f16.argtypes = [vp, vp, i64, i32, vp]
         L.fwa_b200_generate_pillars.argtypes = [C.POINTER(_Scene), C.c_uint64, C.c_double, i32,
                                                 C.c_uint64, vp, vp]
         L.fwa_b200_generate_pillars.restype = i64
@@ -433,6 +434,14 @@ class Context:
         out = np.empty((coords.shape[0], d_model), np.float32)
         self._check(lib().fwa_b200_positional_embedding(self._h, _ptr(coords), coords.shape[0],
                                                         d_model, _ptr(out)))
+        return out
+
+    def positional_embedding_f16(self, coords: np.ndarray, d_model: int) -> np.ndarray:
+        """The bf16 fast path's fp16 PE rows (fp32 range-reduced sincospi on the device)."""
+        coords = np.ascontiguousarray(coords, np.float64)
+        out = np.empty((coords.shape[0], d_model), np.float16)
+        self._check(lib().fwa_b200_positional_embedding_f16(self._h, _ptr(coords), coords.shape[0],
+                                                            d_model, _ptr(out)))
         return out
 
     def fwa_block_forward(self, f: np.ndarray, pe: np.ndarray, record: bytes, n_groups: int) -> np.ndarray:

@@ -71,6 +71,7 @@ struct fwa_b200_ctx {
     bool exact_bins = false;   // set for one call after an overflow: host-sized bins
     uint64_t ws_epoch = 0;     // bumped whenever a workspace buffer moves
     const void* hist_clean = nullptr;  // sync-free histogram buffer known to be zeroed
+    const void* ticket_clean = nullptr;  // key-kernel CTA ticket known to be zeroed
     uint64_t params_version = 0;
     // CUDA graph of the device-resident forward (replayed while its key is unchanged)
     struct GraphKey {
@@ -373,10 +374,19 @@ const double* pe_freq(fwa_b200_ctx* c, int d) {
         for (int k = 0; k < nf; ++k)  // kernels.hpp:373-377
             f[static_cast<size_t>(k)] =
                 nf == 1 ? f_min : f_min * std::pow(f_max / f_min, static_cast<double>(k) / (nf - 1));
+        // + the fp16 PE kernel's (hi, lo) float split of 2 f_k
+        std::vector<float> f2(2 * static_cast<size_t>(nf));
+        for (int k = 0; k < nf; ++k) {
+            const double t = 2.0 * f[static_cast<size_t>(k)];
+            f2[2 * k] = static_cast<float>(t);
+            f2[2 * k + 1] = static_cast<float>(t - static_cast<double>(f2[2 * k]));
+        }
         if (c->freq.p) cudaFree(c->freq.p);
         c->freq.p = nullptr;
-        CUDA_OK(cudaMalloc(&c->freq.p, f.size() * 8));
+        CUDA_OK(cudaMalloc(&c->freq.p, f.size() * 16));
         CUDA_OK(cudaMemcpyAsync(c->freq.p, f.data(), f.size() * 8, cudaMemcpyHostToDevice, c->stream));
+        CUDA_OK(cudaMemcpyAsync(static_cast<double*>(c->freq.p) + nf, f2.data(), f2.size() * 4,
+                                cudaMemcpyHostToDevice, c->stream));
         CUDA_OK(cudaStreamSynchronize(c->stream));
         c->freq_d = d;
     }
@@ -438,11 +448,21 @@ int32_t* sort_specs(fwa_b200_ctx* c, const double* d_coords, int64_t ntot, int n
     long long* mm = ws<long long>(c, "minmax", 16);
     const int64_t n_part = sort_keys_partials(ntot);
     long long* partials = ws<long long>(c, "key_partials", static_cast<size_t>(n_part) * 4 * n_specs);
-    launch_sort_keys(d_coords, ntot, n_specs, w_x, w_y, win, loc, partials, st, &c->launches);
-    check_launch();
     if (!exact) {
         SpecBins* d_sb = ws<SpecBins>(c, "specbins", 4);
         uint32_t* d_nbins = ws<uint32_t>(c, "nbins", 4);
+        unsigned* ticket = ws<unsigned>(c, "sort_ticket", 4);  // [0] key kernel, [1] bin scan
+        uint32_t* large = ws<uint32_t>(c, "large_bins", static_cast<size_t>(kBinCap) + 1);
+        if (ticket != c->ticket_clean) {  // fresh buffer: zero once; the key kernel resets it
+            CUDA_OK(cudaMemsetAsync(ticket, 0, 4 * sizeof(unsigned), st));
+            c->ticket_clean = ticket;
+        }
+        BinsFuse fz;
+        fz.ticket = ticket; fz.nf = nf; fz.cap = kBinCap; fz.mm = mm; fz.specs = d_sb; fz.d_nbins = d_nbins;
+        fz.overflow = c->d_flag + 1;
+        fz.large = large;
+        launch_sort_keys(d_coords, ntot, n_specs, w_x, w_y, win, loc, partials, st, &c->launches, fz);
+        check_launch();
         uint32_t* hist = ws<uint32_t>(c, "hist", static_cast<size_t>(kBinCap));
         if (hist != c->hist_clean) {  // fresh buffer: zero once; the sort kernels keep it zeroed
             CUDA_OK(cudaMemsetAsync(hist, 0, c->ws["hist"].cap, st));
@@ -452,22 +472,21 @@ int32_t* sort_specs(fwa_b200_ctx* c, const double* d_coords, int64_t ntot, int n
         uint32_t* cursor = ws<uint32_t>(c, "cursor", static_cast<size_t>(kBinCap));
         uint32_t* tile_sums = ws<uint32_t>(c, "bin_tile_sums", 1024);
         uint32_t* bin_of = ws<uint32_t>(c, "bin_of", static_cast<size_t>(total));
-        launch_bins_setup(partials, n_part, n_specs, nf, kBinCap, mm, d_sb, d_nbins, c->d_flag + 1, st,
-                          &c->launches);
         launch_bins_hist(win, ntot, n_specs, d_off, nf, d_sb, bin_of, hist, d_nbins, st, &c->launches);
-        launch_scan_bins_dev(hist, bin_start, cursor, d_nbins, kBinCap, tile_sums, st, &c->launches);
+        launch_scan_bins_dev(hist, bin_start, cursor, d_nbins, kBinCap, tile_sums, ticket + 1, st, &c->launches);
         int32_t* pre = ws<int32_t>(c, "pre", static_cast<size_t>(total));
         double* pre_loc = ws<double>(c, "pre_loc", 2 * static_cast<size_t>(total));
-        launch_bin_scatter(bin_of, loc, ntot, n_specs, cursor, pre, pre_loc, d_nbins, st, &c->launches);
+        launch_bin_scatter(bin_of, loc, ntot, n_specs, cursor, pre, pre_loc, d_nbins, tile_sums, st, &c->launches);
         int32_t* sorted = ws<int32_t>(c, "sorted", static_cast<size_t>(total));
         int32_t* inv = ws<int32_t>(c, "sorted_inv", static_cast<size_t>(total));
         int32_t* scratch = ws<int32_t>(c, "sort_scratch", 2 * static_cast<size_t>(total));
-        uint32_t* large = ws<uint32_t>(c, "large_bins", static_cast<size_t>(kBinCap) + 1);
-        launch_bin_sort(bin_start, hist, 0u, pre, pre_loc, loc, ntot, sorted, inv, scratch, large, d_nbins, st,
-                        &c->launches);
+        launch_bin_sort(bin_start, hist, 0u, pre, pre_loc, loc, ntot, sorted, inv, scratch, large, d_nbins,
+                        tile_sums, st, &c->launches);
         check_launch();
         return sorted;
     }
+    launch_sort_keys(d_coords, ntot, n_specs, w_x, w_y, win, loc, partials, st, &c->launches);
+    check_launch();
     {
         SpecBins* d_sb0 = ws<SpecBins>(c, "specbins", 4);
         uint32_t* d_nb0 = ws<uint32_t>(c, "nbins", 4);
@@ -502,13 +521,13 @@ int32_t* sort_specs(fwa_b200_ctx* c, const double* d_coords, int64_t ntot, int n
     CUDA_OK(cudaMemcpyAsync(cursor, bin_start, static_cast<size_t>(nbins) * 4, cudaMemcpyDeviceToDevice, st));
     int32_t* pre = ws<int32_t>(c, "pre", static_cast<size_t>(total));
     double* pre_loc = ws<double>(c, "pre_loc", 2 * static_cast<size_t>(total));
-    launch_bin_scatter(bin_of, loc, ntot, n_specs, cursor, pre, pre_loc, nullptr, st, &c->launches);
+    launch_bin_scatter(bin_of, loc, ntot, n_specs, cursor, pre, pre_loc, nullptr, nullptr, st, &c->launches);
     int32_t* sorted = ws<int32_t>(c, "sorted", static_cast<size_t>(total));
     int32_t* inv = ws<int32_t>(c, "sorted_inv", static_cast<size_t>(total));
     int32_t* scratch = ws<int32_t>(c, "sort_scratch", 2 * static_cast<size_t>(total));
     uint32_t* large = ws<uint32_t>(c, "large_bins", static_cast<size_t>(nbins) + 1);
     launch_bin_sort(bin_start, hist, static_cast<uint32_t>(nbins), pre, pre_loc, loc, ntot, sorted, inv,
-                    scratch, large, nullptr, st, &c->launches);
+                    scratch, large, nullptr, nullptr, st, &c->launches);
     check_launch();
     return sorted;
 }
@@ -1306,6 +1325,23 @@ int fwa_b200_positional_embedding(fwa_b200_ctx* c, const double* coords, int64_t
         launch_positional_embedding(dc, n, d, pe_freq(c, d), dp, nullptr, st, &c->launches);
         check_launch();
         CUDA_OK(cudaMemcpyAsync(out, dp, static_cast<size_t>(n) * d * 4, cudaMemcpyDeviceToHost, st));
+        CUDA_OK(cudaStreamSynchronize(st));
+    });
+}
+
+int fwa_b200_positional_embedding_f16(fwa_b200_ctx* c, const double* coords, int64_t n, int32_t d,
+                                      uint16_t* out) {
+    return guarded(c, [&] {
+        if (d < 4 || d % 4 != 0)
+            throw FwaError{FWA_ERR_CONFIG, "positional_embedding: d_model must be divisible by 4"};
+        if (n == 0) return;
+        cudaStream_t st = c->stream;
+        double* dc = ws<double>(c, "pe_coords", 2 * static_cast<size_t>(n));
+        __half* dp = ws<__half>(c, "pe_out16", static_cast<size_t>(n) * d);
+        CUDA_OK(cudaMemcpyAsync(dc, coords, static_cast<size_t>(n) * 16, cudaMemcpyHostToDevice, st));
+        launch_positional_embedding(dc, n, d, pe_freq(c, d), nullptr, dp, st, &c->launches);
+        check_launch();
+        CUDA_OK(cudaMemcpyAsync(out, dp, static_cast<size_t>(n) * d * 2, cudaMemcpyDeviceToHost, st));
         CUDA_OK(cudaStreamSynchronize(st));
     });
 }

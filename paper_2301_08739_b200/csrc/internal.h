@@ -30,11 +30,22 @@ struct SpecBins {
     long long base;             // first global bin id of this spec
 };
 
-// writes per-CTA window min/max partials ([spec][sort_keys_partials(ntot)][4])
+// writes per-CTA window min/max partials ([spec][sort_keys_partials(ntot)][4]); with
+// BinsFuse::ticket set, the last CTA also does launch_bins_setup's work
 int64_t sort_keys_partials(int64_t ntot);
+struct BinsFuse {
+    unsigned* ticket = nullptr;  // zero-initialised once; reset by the kernel
+    int nf = 1;
+    long long cap = 0;
+    long long* mm = nullptr;
+    SpecBins* specs = nullptr;
+    uint32_t* d_nbins = nullptr;
+    int* overflow = nullptr;
+    uint32_t* large = nullptr;   // reset to 0 (launch_bin_sort's queue counter)
+};
 void launch_sort_keys(const double* coords, int64_t ntot, int n_specs, double w_x, double w_y,
                       long long* win, double* loc, long long* partials, cudaStream_t s,
-                      int64_t* launches);
+                      int64_t* launches, const BinsFuse& fz = BinsFuse{});
 // d_nbins (may be null): device-side bin count of the sync-free path; 0 disables
 void launch_bins_hist(const long long* win, int64_t ntot, int n_specs, const int64_t* d_frame_off,
                       int n_frames, const SpecBins* d_specs, uint32_t* bin_of, uint32_t* hist,
@@ -45,18 +56,21 @@ void launch_bins_setup(const long long* partials, int64_t n_part, int n_specs, i
                        long long* mm, SpecBins* specs, uint32_t* d_nbins, int* overflow, cudaStream_t s,
                        int64_t* launches);
 void launch_zero_bins(uint32_t* hist, const uint32_t* d_nbins, cudaStream_t s, int64_t* launches);
+// tile-local exclusive scan; tile_sums becomes the per-4096-bin tile offsets the
+// consumers add (tile_off below); ticket: zero-initialised, self-resetting
 void launch_scan_bins_dev(const uint32_t* hist, uint32_t* bin_start, uint32_t* cursor, const uint32_t* d_nbins,
-                          long long cap, uint32_t* tile_sums, cudaStream_t s, int64_t* launches);
+                          long long cap, uint32_t* tile_sums, unsigned* ticket, cudaStream_t s,
+                          int64_t* launches);
 void launch_bin_scatter(const uint32_t* bin_of, const double* loc, int64_t ntot, int n_specs,
                         uint32_t* cursor, int32_t* pre, double* pre_loc, const uint32_t* d_nbins,
-                        cudaStream_t s, int64_t* launches);
+                        const uint32_t* tile_off, cudaStream_t s, int64_t* launches);
 // also writes the inverse permutation inv[s*ntot + id] = position in sorted
 // zeroes hist[] as it consumes it (the sync-free path relies on a clean histogram)
 void launch_bin_sort(const uint32_t* bin_start, uint32_t* hist, uint32_t n_bins,
                      const int32_t* pre, const double* pre_loc, const double* loc, int64_t ntot,
                      int32_t* sorted, int32_t* inv, int32_t* scratch,
-                     uint32_t* large /* 1 + n_bins words */, const uint32_t* d_nbins, cudaStream_t s,
-                     int64_t* launches);
+                     uint32_t* large /* 1 + n_bins words */, const uint32_t* d_nbins,
+                     const uint32_t* tile_off, cudaStream_t s, int64_t* launches);
 constexpr int kMaxDropTable = 8192;
 void launch_drop_tables(const int32_t* sorted0, int n, const int64_t* frame_off, const int64_t* rows,
                         const int64_t* drop_off, int n_frames, const int32_t* inv, int64_t ntot, int n_specs,

@@ -143,12 +143,18 @@ FWA_DEVINL long long wmax(long long v) {
     return v;
 }
 
+__device__ void bins_setup_cta(const long long* __restrict__ partials, int64_t n_part, int n_specs, int nf,
+                               long long cap, long long* __restrict__ mm, SpecBins* __restrict__ specs,
+                               uint32_t* __restrict__ d_nbins, int* __restrict__ overflow);
+
 // One thread per (spec, point).  flatten.hpp:49-69, op by op, round-to-nearest.
+// With `fz`, the last CTA to finish (atomic ticket) also reduces the min/max partials
+// into the bin layout (bins_setup_cta) -- no separate launch.
 __global__ void __launch_bounds__(256) k_sort_keys(const double* __restrict__ coords, int64_t ntot,
                                                    int n_specs, double w_x, double w_y,
                                                    long long* __restrict__ win,
                                                    double* __restrict__ loc,
-                                                   long long* __restrict__ minmax) {
+                                                   long long* __restrict__ minmax, BinsFuse fz) {
     const int s = blockIdx.y;
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const bool axis_y = s >= 2, shift = (s & 1) != 0;
@@ -190,8 +196,23 @@ __global__ void __launch_bounds__(256) k_sort_keys(const double* __restrict__ co
         long long v = red[q][0];
         for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
             v = (q & 1) ? (red[q][w] > v ? red[q][w] : v) : (red[q][w] < v ? red[q][w] : v);
-        // per-CTA partial [spec][cta][4]; reduced by k_bins_setup (no init, no atomics)
+        // per-CTA partial [spec][cta][4]; reduced by the last CTA or k_bins_setup
         minmax[(static_cast<int64_t>(s) * gridDim.x + blockIdx.x) * 4 + q] = v;
+    }
+    if (fz.ticket) {
+        __shared__ bool last;
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) last = atomicAdd(fz.ticket, 1u) == gridDim.x * gridDim.y - 1;
+        __syncthreads();
+        if (last) {
+            __threadfence();
+            bins_setup_cta(minmax, gridDim.x, n_specs, fz.nf, fz.cap, fz.mm, fz.specs, fz.d_nbins, fz.overflow);
+            if (threadIdx.x == 0) {
+                *fz.ticket = 0u;  // self-resetting for the next call
+                if (fz.large) *fz.large = 0u;  // the bin sort's oversize-bin queue
+            }
+        }
     }
 }
 
@@ -199,9 +220,9 @@ int64_t sort_keys_partials(int64_t ntot) { return (ntot + 255) / 256; }
 
 void launch_sort_keys(const double* coords, int64_t ntot, int n_specs, double w_x, double w_y,
                       long long* win, double* loc, long long* partials, cudaStream_t s,
-                      int64_t* launches) {
+                      int64_t* launches, const BinsFuse& fz) {
     dim3 grid(static_cast<unsigned>(sort_keys_partials(ntot)), static_cast<unsigned>(n_specs));
-    k_sort_keys<<<grid, 256, 0, s>>>(coords, ntot, n_specs, w_x, w_y, win, loc, partials);
+    k_sort_keys<<<grid, 256, 0, s>>>(coords, ntot, n_specs, w_x, w_y, win, loc, partials, fz);
     *launches += 1;
 }
 
@@ -252,11 +273,13 @@ __global__ void __launch_bounds__(256) k_bin_scatter(const uint32_t* __restrict_
                                                      int64_t ntot, uint32_t* __restrict__ cursor,
                                                      int32_t* __restrict__ pre,
                                                      double* __restrict__ pre_loc,
-                                                     const uint32_t* __restrict__ d_nbins) {
+                                                     const uint32_t* __restrict__ d_nbins,
+                                                     const uint32_t* __restrict__ tile_off) {
     const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (e >= total) return;
     if (d_nbins && *d_nbins == 0u) return;
-    const uint32_t pos = atomicAdd(cursor + bin_of[e], 1u);
+    const uint32_t b = bin_of[e];
+    const uint32_t pos = atomicAdd(cursor + b, 1u) + (tile_off ? tile_off[b / kScanTile] : 0u);
     pre[pos] = static_cast<int32_t>(e % ntot);
     // the window-local keys travel with the id: the per-bin sort reads them contiguously
     reinterpret_cast<double2*>(pre_loc)[pos] = reinterpret_cast<const double2*>(loc)[e];
@@ -264,10 +287,11 @@ __global__ void __launch_bounds__(256) k_bin_scatter(const uint32_t* __restrict_
 
 void launch_bin_scatter(const uint32_t* bin_of, const double* loc, int64_t ntot, int n_specs,
                         uint32_t* cursor, int32_t* pre, double* pre_loc, const uint32_t* d_nbins,
-                        cudaStream_t s, int64_t* launches) {
+                        const uint32_t* tile_off, cudaStream_t s, int64_t* launches) {
     const int64_t total = ntot * n_specs;
     k_bin_scatter<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(bin_of, loc, total, ntot,
-                                                                           cursor, pre, pre_loc, d_nbins);
+                                                                           cursor, pre, pre_loc, d_nbins,
+                                                                           tile_off);
     ++*launches;
 }
 
@@ -284,13 +308,59 @@ constexpr int kWarpBin = 128;   // bins up to this size: one warp, shared memory
 constexpr int kCtaBin = 4096;   // up to this: one CTA, shared-memory rank sort
 constexpr int kBinWarps = 8;
 
-// One warp sorts one window bin (<= kWarpBin points) by rank counting in shared memory;
-// bigger bins are queued for k_bin_sort_large.  Writes sorted[] and the inverse inv[].
+// Order-preserving integer image of a window-local coordinate: unsigned compare of the
+// images == the reference's double compare (key_less, flatten.hpp:41-47), with -0.0 and
+// +0.0 equal (both map to the +0.0 image).  Coordinates are finite.
+FWA_DEVINL unsigned long long ord_key(double d) {
+    const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(d == 0.0 ? 0.0 : d));
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ULL);
+}
+
+// rank of each of this lane's NQ elements (lane + 32q) among the bin's n elements, and
+// its placement; every element j is read once (shared-memory broadcast) per warp
+template <int NQ>
+FWA_DEVINL void rank_place(int n, int lane, const unsigned long long* sa, const unsigned long long* sb,
+                           const int* si, uint32_t start, int64_t spec_base, int32_t* __restrict__ sorted,
+                           int32_t* __restrict__ inv) {
+    unsigned long long ea[NQ], eb[NQ];
+    int ei[NQ], er[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const int k = lane + 32 * q;
+        const bool ok = k < n;
+        ea[q] = ok ? sa[k] : ~0ULL;
+        eb[q] = ok ? sb[k] : ~0ULL;
+        ei[q] = ok ? si[k] : 0x7fffffff;
+        er[q] = 0;
+    }
+#pragma unroll 4
+    for (int j = 0; j < n; ++j) {
+        const unsigned long long a = sa[j], b = sb[j];
+        const int id = si[j];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+            er[q] += (a < ea[q]) | ((a == ea[q]) & ((b < eb[q]) | ((b == eb[q]) & (id < ei[q]))));
+    }
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const int k = lane + 32 * q;
+        if (k < n) {
+            sorted[start + er[q]] = ei[q];
+            inv[spec_base + ei[q]] = static_cast<int32_t>(start + er[q]);
+        }
+    }
+}
+
+// One warp sorts one window bin (<= kWarpBin points) by rank counting in shared memory:
+// lane l owns elements l, l+32, l+64, l+96; every element j is broadcast once and
+// compared with all of them (integer keys, no fp64 compares).  Bigger bins are queued
+// for k_bin_sort_large.  Writes sorted[] and the inverse inv[].
 FWA_DEVINL void sort_one_small_bin(uint32_t bin, const uint32_t* __restrict__ bin_start,
                                    uint32_t* __restrict__ hist, const int32_t* __restrict__ pre,
                                    const double* __restrict__ ploc, int64_t ntot, int32_t* __restrict__ sorted,
-                                   int32_t* __restrict__ inv, uint32_t* __restrict__ large, double* sa,
-                                   double* sb, int* si, int lane) {
+                                   int32_t* __restrict__ inv, uint32_t* __restrict__ large,
+                                   const uint32_t* __restrict__ tile_off,
+                                   unsigned long long* sa, unsigned long long* sb, int* si, int lane) {
     const int n = static_cast<int>(hist[bin]);
     if (n > kWarpBin) {  // queue for the CTA-level kernel; large[0] = count
         if (lane == 0) large[1 + atomicAdd(large, 1u)] = bin;
@@ -299,7 +369,7 @@ FWA_DEVINL void sort_one_small_bin(uint32_t bin, const uint32_t* __restrict__ bi
     if (n == 0) return;
     __syncwarp();
     if (lane == 0) hist[bin] = 0u;  // leave the histogram zeroed for the next call
-    const uint32_t start = bin_start[bin];
+    const uint32_t start = bin_start[bin] + (tile_off ? tile_off[bin / kScanTile] : 0u);
     const int64_t spec_base = (static_cast<int64_t>(start) / ntot) * ntot;
     if (n == 1) {
         if (lane == 0) {
@@ -311,19 +381,16 @@ FWA_DEVINL void sort_one_small_bin(uint32_t bin, const uint32_t* __restrict__ bi
     }
     for (int k = lane; k < n; k += 32) {
         const double2 l = reinterpret_cast<const double2*>(ploc)[start + k];
-        sa[k] = l.x;
-        sb[k] = l.y;
+        sa[k] = ord_key(l.x);
+        sb[k] = ord_key(l.y);
         si[k] = pre[start + k];
     }
     __syncwarp();
-    for (int k = lane; k < n; k += 32) {
-        const double a = sa[k], b = sb[k];
-        const int id = si[k];
-        int rank = 0;
-        for (int j = 0; j < n; ++j) rank += loc_less(sa[j], sb[j], si[j], a, b, id);
-        sorted[start + rank] = id;
-        inv[spec_base + id] = static_cast<int32_t>(start + rank);
-    }
+    const int nq = (n + 31) >> 5;
+    if (nq == 1) rank_place<1>(n, lane, sa, sb, si, start, spec_base, sorted, inv);
+    else if (nq == 2) rank_place<2>(n, lane, sa, sb, si, start, spec_base, sorted, inv);
+    else if (nq == 3) rank_place<3>(n, lane, sa, sb, si, start, spec_base, sorted, inv);
+    else rank_place<4>(n, lane, sa, sb, si, start, spec_base, sorted, inv);
     __syncwarp();
 }
 
@@ -331,22 +398,22 @@ __global__ void __launch_bounds__(kBinWarps * 32) k_bin_sort_small(
     const uint32_t* __restrict__ bin_start, uint32_t* __restrict__ hist, uint32_t n_bins,
     const int32_t* __restrict__ pre, const double* __restrict__ ploc, int64_t ntot,
     int32_t* __restrict__ sorted, int32_t* __restrict__ inv, uint32_t* __restrict__ large,
-    const uint32_t* __restrict__ d_nbins) {
-    __shared__ double s_a[kBinWarps][kWarpBin];
-    __shared__ double s_b[kBinWarps][kWarpBin];
+    const uint32_t* __restrict__ d_nbins, const uint32_t* __restrict__ tile_off) {
+    __shared__ unsigned long long s_a[kBinWarps][kWarpBin];
+    __shared__ unsigned long long s_b[kBinWarps][kWarpBin];
     __shared__ int s_i[kBinWarps][kWarpBin];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (d_nbins) n_bins = *d_nbins;  // sync-free path: grid-stride over the device-side count
     for (uint32_t bin = blockIdx.x * kBinWarps + wid; bin < n_bins; bin += gridDim.x * kBinWarps)
-        sort_one_small_bin(bin, bin_start, hist, pre, ploc, ntot, sorted, inv, large, s_a[wid], s_b[wid],
-                           s_i[wid], lane);
+        sort_one_small_bin(bin, bin_start, hist, pre, ploc, ntot, sorted, inv, large, tile_off, s_a[wid],
+                           s_b[wid], s_i[wid], lane);
 }
 
 __global__ void __launch_bounds__(512) k_bin_sort_large(
     const uint32_t* __restrict__ bin_start, uint32_t* __restrict__ hist,
     const uint32_t* __restrict__ large, const int32_t* __restrict__ pre,
     const double* __restrict__ loc, int64_t ntot, int32_t* __restrict__ sorted,
-    int32_t* __restrict__ inv, int32_t* __restrict__ scratch) {
+    int32_t* __restrict__ inv, int32_t* __restrict__ scratch, const uint32_t* __restrict__ tile_off) {
     extern __shared__ unsigned char smem_raw[];
     double* s_a = reinterpret_cast<double*>(smem_raw);
     double* s_b = s_a + kCtaBin;
@@ -355,7 +422,7 @@ __global__ void __launch_bounds__(512) k_bin_sort_large(
     for (uint32_t li = blockIdx.x; li < n_large; li += gridDim.x) {
         const uint32_t bin = large[1 + li];
         const int n = static_cast<int>(hist[bin]);
-        const uint32_t start = bin_start[bin];
+        const uint32_t start = bin_start[bin] + (tile_off ? tile_off[bin / kScanTile] : 0u);
         const int64_t spec_base = (static_cast<int64_t>(start) / ntot) * ntot;
         const double2* L = reinterpret_cast<const double2*>(loc) + spec_base;
         if (n <= kCtaBin) {
@@ -420,12 +487,12 @@ __global__ void __launch_bounds__(512) k_bin_sort_large(
 void launch_bin_sort(const uint32_t* bin_start, uint32_t* hist, uint32_t n_bins,
                      const int32_t* pre, const double* pre_loc, const double* loc, int64_t ntot,
                      int32_t* sorted, int32_t* inv, int32_t* scratch, uint32_t* large,
-                     const uint32_t* d_nbins, cudaStream_t s, int64_t* launches) {
+                     const uint32_t* d_nbins, const uint32_t* tile_off, cudaStream_t s, int64_t* launches) {
     // host-known n_bins: one warp per bin; device-side count: grid-stride
     const unsigned grid = d_nbins ? kNumSMs * 16 : (n_bins + kBinWarps - 1) / kBinWarps;
-    cudaMemsetAsync(large, 0, sizeof(uint32_t), s);
+    if (!d_nbins) cudaMemsetAsync(large, 0, sizeof(uint32_t), s);  // sync-free path: reset by the key kernel
     k_bin_sort_small<<<grid, kBinWarps * 32, 0, s>>>(bin_start, hist, n_bins, pre, pre_loc, ntot,
-                                                     sorted, inv, large, d_nbins);
+                                                     sorted, inv, large, d_nbins, tile_off);
     static bool attr_set = false;
     const int smem = kCtaBin * (8 + 8 + 4);
     if (!attr_set) {
@@ -433,7 +500,7 @@ void launch_bin_sort(const uint32_t* bin_start, uint32_t* hist, uint32_t n_bins,
         attr_set = true;
     }
     k_bin_sort_large<<<kNumSMs, 512, smem, s>>>(bin_start, hist, large, pre, loc, ntot, sorted, inv,
-                                                scratch);
+                                                scratch, tile_off);
     *launches += 2;
 }
 
@@ -653,12 +720,11 @@ void launch_compact_all(const int32_t* sorted, int64_t ntot, int n_specs, const 
 // capacity; a frame set whose dense window range exceeds it raises *overflow (nbins = 0
 // disables every bin kernel) and the host re-runs the exact-size path.
 
-__global__ void __launch_bounds__(1024) k_bins_setup(const long long* __restrict__ partials, int64_t n_part,
-                                                      int n_specs, int nf, long long cap,
-                                                      long long* __restrict__ mm,
-                                                      SpecBins* __restrict__ specs,
-                                                      uint32_t* __restrict__ d_nbins,
-                                                      int* __restrict__ overflow) {
+// One CTA (blockDim a multiple of 32, <= 1024) reduces the key kernel's per-CTA window
+// min/max partials into the dense bin layout of every spec and the device-side bin count.
+__device__ void bins_setup_cta(const long long* __restrict__ partials, int64_t n_part, int n_specs, int nf,
+                               long long cap, long long* __restrict__ mm, SpecBins* __restrict__ specs,
+                               uint32_t* __restrict__ d_nbins, int* __restrict__ overflow) {
     __shared__ long long red[32][4];
     __shared__ long long fin[4][4];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -666,10 +732,11 @@ __global__ void __launch_bounds__(1024) k_bins_setup(const long long* __restrict
         long long v[4] = {LLONG_MAX, LLONG_MIN, LLONG_MAX, LLONG_MIN};
         for (int64_t i = threadIdx.x; i < n_part; i += blockDim.x) {
             const long long* p = partials + (static_cast<int64_t>(s) * n_part + i) * 4;
-            v[0] = p[0] < v[0] ? p[0] : v[0];
-            v[1] = p[1] > v[1] ? p[1] : v[1];
-            v[2] = p[2] < v[2] ? p[2] : v[2];
-            v[3] = p[3] > v[3] ? p[3] : v[3];
+            const long long p0 = __ldcg(p), p1 = __ldcg(p + 1), p2 = __ldcg(p + 2), p3 = __ldcg(p + 3);
+            v[0] = p0 < v[0] ? p0 : v[0];
+            v[1] = p1 > v[1] ? p1 : v[1];
+            v[2] = p2 < v[2] ? p2 : v[2];
+            v[3] = p3 > v[3] ? p3 : v[3];
         }
         v[0] = wmin(v[0]);
         v[1] = wmax(v[1]);
@@ -709,16 +776,30 @@ __global__ void __launch_bounds__(1024) k_bins_setup(const long long* __restrict
     }
 }
 
+__global__ void __launch_bounds__(1024) k_bins_setup(const long long* __restrict__ partials, int64_t n_part,
+                                                      int n_specs, int nf, long long cap,
+                                                      long long* __restrict__ mm,
+                                                      SpecBins* __restrict__ specs,
+                                                      uint32_t* __restrict__ d_nbins,
+                                                      int* __restrict__ overflow) {
+    bins_setup_cta(partials, n_part, n_specs, nf, cap, mm, specs, d_nbins, overflow);
+}
+
 __global__ void k_zero_bins(uint32_t* __restrict__ a, const uint32_t* __restrict__ d_n) {
     const uint32_t n = *d_n;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = 0u;
 }
 
 // exclusive scan of hist[0, *d_n) into bin_start and cursor (<= 1024 tiles of 4096)
+// Tile-local exclusive scan into out[] and cursor[]; the last active tile (atomic ticket)
+// turns tile_sums[] into the exclusive tile offsets.  Consumers add
+// tile_off[bin / kScanTile] (one launch instead of three).
 __global__ void __launch_bounds__(kScanThreads) k_scan_tiles_dev(const uint32_t* __restrict__ in,
                                                                    uint32_t* __restrict__ out,
+                                                                   uint32_t* __restrict__ cursor,
                                                                    const uint32_t* __restrict__ d_n,
-                                                                   uint32_t* __restrict__ tile_sums) {
+                                                                   uint32_t* __restrict__ tile_sums,
+                                                                   unsigned* __restrict__ ticket) {
     const int64_t n = *d_n;
     if (static_cast<int64_t>(blockIdx.x) * kScanTile >= n) return;
     __shared__ uint32_t warp_tot[32];
@@ -755,52 +836,42 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tiles_dev(const uint32_t*
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
         const int64_t i = base + k;
-        if (i < n) out[i] = v[k] + excl;
+        if (i < n) {
+            out[i] = v[k] + excl;
+            cursor[i] = v[k] + excl;
+        }
     }
     if (threadIdx.x == kScanThreads - 1) tile_sums[blockIdx.x] = excl + run;
-}
-
-__global__ void __launch_bounds__(1024) k_scan_sums_dev(uint32_t* __restrict__ sums, const uint32_t* __restrict__ d_n) {
-    const int tiles = static_cast<int>((static_cast<int64_t>(*d_n) + kScanTile - 1) / kScanTile);
-    __shared__ uint32_t warp_tot[32];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const uint32_t v = threadIdx.x < tiles ? sums[threadIdx.x] : 0u;
-    uint32_t x = v;
+    const unsigned tiles = static_cast<unsigned>((n + kScanTile - 1) / kScanTile);
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == tiles - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const uint32_t t = threadIdx.x < tiles ? __ldcg(tile_sums + threadIdx.x) : 0u;
+    uint32_t y = t;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
+        const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
+        if (lane >= o) y += z;
     }
-    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (lane == 31) warp_tot[wid] = y;
     __syncthreads();
     if (wid == 0) {
         uint32_t w = warp_tot[lane];
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-            if (lane >= o) w += y;
+            const uint32_t z = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += z;
         }
         warp_tot[lane] = w;
     }
     __syncthreads();
-    if (threadIdx.x < tiles) sums[threadIdx.x] = x - v + (wid ? warp_tot[wid - 1] : 0u);
-}
-
-__global__ void k_scan_add_dev(uint32_t* __restrict__ out, uint32_t* __restrict__ cursor,
-                               const uint32_t* __restrict__ d_n, const uint32_t* __restrict__ tile_off) {
-    const int64_t n = *d_n;
-    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kScanTile;
-    if (i0 >= n) return;
-    const uint32_t add = tile_off[blockIdx.x];
-#pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-        const int64_t j = i0 + threadIdx.x + static_cast<int64_t>(k) * kScanThreads;
-        if (j < n) {
-            const uint32_t v = out[j] + add;
-            out[j] = v;
-            cursor[j] = v;
-        }
-    }
+    if (threadIdx.x < tiles) tile_sums[threadIdx.x] = y - t + (wid ? warp_tot[wid - 1] : 0u);
+    if (threadIdx.x == 0) *ticket = 0u;
 }
 
 void launch_bins_setup(const long long* partials, int64_t n_part, int n_specs, int nf, long long cap,
@@ -816,12 +887,11 @@ void launch_zero_bins(uint32_t* hist, const uint32_t* d_nbins, cudaStream_t s, i
 }
 
 void launch_scan_bins_dev(const uint32_t* hist, uint32_t* bin_start, uint32_t* cursor, const uint32_t* d_nbins,
-                          long long cap, uint32_t* tile_sums, cudaStream_t s, int64_t* launches) {
+                          long long cap, uint32_t* tile_sums, unsigned* ticket, cudaStream_t s,
+                          int64_t* launches) {
     const unsigned tiles = static_cast<unsigned>((cap + kScanTile - 1) / kScanTile);
-    k_scan_tiles_dev<<<tiles, kScanThreads, 0, s>>>(hist, bin_start, d_nbins, tile_sums);
-    k_scan_sums_dev<<<1, 1024, 0, s>>>(tile_sums, d_nbins);
-    k_scan_add_dev<<<tiles, kScanThreads, 0, s>>>(bin_start, cursor, d_nbins, tile_sums);
-    *launches += 3;
+    k_scan_tiles_dev<<<tiles, kScanThreads, 0, s>>>(hist, bin_start, cursor, d_nbins, tile_sums, ticket);
+    *launches += 1;
 }
 
 } // namespace fwa_b200

@@ -96,6 +96,17 @@ def test_positional_embedding(ctx32):
     assert np.max(np.abs(got - want)) <= 1e-6  # fp64 sin/cos, f32 rounding
 
 
+def test_positional_embedding_fp16_fast_path(ctx16):
+    """fp16 PE rows of the bf16 path: within fp16 rounding of the reference's fp64 values,
+    on F60 and on coordinates far from the origin (large phases, exact range reduction)."""
+    for coords in (F.make_pillars(F.SCENES["F60"], 42).coords,
+                   np.random.default_rng(7).uniform(-3000.0, 3000.0, size=(5000, 2))):
+        got = ctx16.positional_embedding_f16(coords, 128).astype(np.float64)
+        want = O.port_positional_embedding(coords, 128).astype(np.float64)
+        # half an fp16 ulp of |v| <= 1 is 2^-12; + 1e-6 for the fp32 sincospi
+        assert np.max(np.abs(got - want)) <= 2.0 ** -12 + 1e-6
+
+
 # ----------------------------------------------------------------------------- block
 
 def test_block_forward_fp32_vs_f64_oracle(ctx32):
