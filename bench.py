@@ -39,12 +39,17 @@ sys.path.insert(0, ROOT)
 
 METRIC = "pillars/sec and ms/frame, FlatFormer backbone fwd, 1/2/4/8 B200 vs CPU ref"
 FLOP_PER_ROW = {"ln1_qkv": 2 * 128 * 384, "attention": 2 * 2 * 69 * 128,
-                "outproj_ffn": 2 * (128 * 128 + 2 * 128 * 256)}  # 297,472 per kept pillar per block
+                "outproj_ffn": 2 * (128 * 128 + 2 * 128 * 256),
+                "block_fused": 297472}  # 297,472 per kept pillar per block
 # algorithmic HBM bytes per kept row: the data each kernel must move
 BYTES_PER_ROW = {"ln1_qkv": 512 + 256 + 4 + 768,      # fp32 row + fp16 PE row + id in, bf16 q|k|v out
                  "attention": 768 + 256,               # q|k|v in, head outputs out
-                 "outproj_ffn": 256 + 512 + 8 + 512}   # head outputs + fp32 residual + ids in, fp32 row out
-NCU_KERNEL = {"ln1_qkv": "k_ln1_qkv_tc", "attention": "k_attention_mma", "outproj_ffn": "k_outproj_ffn_tc"}
+                 "outproj_ffn": 256 + 512 + 8 + 512,   # head outputs + fp32 residual + ids in, fp32 row out
+                 # fused block: residual row in (fp32; the f64 PillarSet row in block 0) + fp16 PE
+                 # row + gather/scatter ids, fp32 row out -- averaged over the 8 blocks
+                 "block_fused": (7 * (512 + 256 + 8 + 512) + (1024 + 256 + 8 + 512)) / 8}
+NCU_KERNEL = {"ln1_qkv": "k_ln1_qkv_tc", "attention": "k_attention_mma", "outproj_ffn": "k_outproj_ffn_tc",
+              "block_fused": "k_block_fused"}
 WORKLOAD = "F60 frame (60,897 pillars), full FlatFormer backbone: 8 blocks, G 69, D 128, H 8, D_ff 256"
 
 

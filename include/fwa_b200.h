@@ -113,7 +113,8 @@ enum fwa_prof_slot {
     FWA_PROF_OUTPROJ_FFN = 4,  /* out-proj + residual + LN2 + FFN + residual + scatter */
     FWA_PROF_H2D = 5,
     FWA_PROF_D2H = 6,
-    FWA_PROF_SLOTS = 7
+    FWA_PROF_BLOCK = 7,        /* the fused one-launch block kernel (gather .. scatter) */
+    FWA_PROF_SLOTS = 8
 };
 int fwa_b200_set_profiling(fwa_b200_ctx* ctx, int enable);
 int fwa_b200_get_profile(fwa_b200_ctx* ctx, double* ms, int64_t* counts);

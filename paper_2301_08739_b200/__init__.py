@@ -299,7 +299,7 @@ class Context:
     def kernel_launches(self) -> int:
         return int(lib().fwa_b200_kernel_launches(self._h))
 
-    PROF_SLOTS = ("schedule", "pe", "ln1_qkv", "attention", "outproj_ffn", "h2d", "d2h")
+    PROF_SLOTS = ("schedule", "pe", "ln1_qkv", "attention", "outproj_ffn", "h2d", "d2h", "block_fused")
 
     def set_profiling(self, enable: bool = True):
         self._check(lib().fwa_b200_set_profiling(self._h, int(enable)))

@@ -82,8 +82,12 @@ FWA_DEVINL uint32_t mapa(uint32_t saddr, uint32_t rank) {
 FWA_DEVINL void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// remote arrive on the leader's barrier (default .release.cta semantics, as CUTLASS's
+// ClusterBarrier::arrive(cta_id)); a .release.cluster arrive costs a MEMBAR.ALL.GPU.  The
+// operand this orders is the arriving CTA's own shared-memory A tile, read by its own
+// SM's half of the pair MMA after fence.proxy.async + __syncthreads.
 FWA_DEVINL void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 FWA_DEVINL void mbar_wait_acq_cluster(uint64_t* bar, uint32_t parity) {
     asm volatile(
@@ -631,7 +635,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         mbar_wait(bHalo, ph);   // the peer's halo rows have landed
         FTR(tb + 4);
         {
-            const int ntasks = sTab[16].x * 8;
+            const int ntasks = sTab[16].x * 8;  // (m-tile, head)
 #pragma unroll 1
             for (int t = warp; t < ntasks; t += 16) {
                 const int4 e = sTab[t >> 3];

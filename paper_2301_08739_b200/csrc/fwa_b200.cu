@@ -682,7 +682,7 @@ void run_block(fwa_b200_ctx* c, const BlockParams& p, const fwa_config_t* cfg, i
             return v && v[0] == '1';
         }();
         unsigned long long* tr = trace_fused && !x_in64 ? ws<unsigned long long>(c, "trace", 2 * 148 * 64) : nullptr;
-        StageEv t(c, FWA_PROF_OUTPROJ_FFN);
+        StageEv t(c, FWA_PROF_BLOCK);
         launch_block_fused(x_in, x_in64, pe16, ridx, sidx, x_out, rows, G, p.tc, c->d_flag, st, &c->launches, tr);
         check_launch("k_block_fused");
         return;
