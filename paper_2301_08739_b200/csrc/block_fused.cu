@@ -487,7 +487,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         fence_after_sync();
     };
 
+    // this lane's two gather ids of unit u (8 lanes per row; rows hf*64 + warp*4 + lane/8)
+    // -- prefetched one unit ahead, so the row loads do not wait on the id loads
+    auto unit_ids = [&](const int32_t* idx, int u, int (&ids)[2]) {
+        ids[0] = ids[1] = 0;
+        if (u >= a.n_units) return;
+        const int64_t ub = static_cast<int64_t>(u) * R;
+        const int ur = static_cast<int>(a.rows - ub < R ? a.rows - ub : R);
+        const int sp = a.split < ur ? a.split : ur;
+        const int r0 = rank ? sp : 0, nl = rank ? ur - sp : sp;
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+            const int r = hf * 64 + warp * 4 + (lane >> 3);
+            if (r < nl) ids[hf] = idx ? idx[ub + r0 + r] : static_cast<int>(ub + r0 + r);
+        }
+    };
     griddep_wait();  // x / PE / ids come from earlier kernels
+    int gid[2], sid[2];
+    unit_ids(a.ridx, pair, gid);
     if (threadIdx.x == 0) mbar_wait(bW, 0);
     FTR(0);
     int it = 0;
@@ -522,10 +539,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
                 const int r = hf * 64 + warp * 4 + rl;
-                const bool ok = r < nloc;
-                const int64_t id = ok ? (a.ridx ? a.ridx[ubase + urow0 + r] : ubase + urow0 + r) : 0;
-                load_row_quads<kF64>(a.x, a.x64, a.pe16, id, sub, ok, v[hf], pe[hf]);
+                load_row_quads<kF64>(a.x, a.x64, a.pe16, gid[hf], sub, r < nloc, v[hf], pe[hf]);
             }
+            // this unit's scatter ids (== the gather ids except in the last block), then the
+            // next unit's gather ids, in flight behind this unit's rows
+            if (a.sidx == a.ridx) {
+                sid[0] = gid[0];
+                sid[1] = gid[1];
+            } else {
+                unit_ids(a.sidx, u, sid);
+            }
+            unit_ids(a.ridx, u + npairs, gid);
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
                 const int r = hf * 64 + warp * 4 + rl;
@@ -779,14 +803,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
             {
                 const int rbase = warp * 4;  // 16 warps x 4 rows = the 64 rows of this half
                 const int lr0 = hf * 64 + rbase;
-                int myid = 0;
-                if (lane < 4 && lr0 + lane < nloc) {
-                    const int64_t gl = ubase + urow0 + lr0 + lane;
-                    myid = a.sidx ? a.sidx[gl] : static_cast<int>(gl);
-                }
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    const int64_t id = __shfl_sync(0xffffffffu, myid, i);
+                    // row lr0 + i's scatter id was prefetched by lanes 8i..8i+7 (gather layout)
+                    const int64_t id = __shfl_sync(0xffffffffu, hf ? sid[1] : sid[0], 8 * i);
                     const float4 o = *reinterpret_cast<const float4*>(pRA + stage_off(rbase + i, lane));
                     if (lr0 + i < nloc) reinterpret_cast<float4*>(a.x_out + id * 128)[lane] = o;
                 }
