@@ -399,8 +399,18 @@ struct FusedArgs {
 
 #define FTR(k)                                                                                  \
     do {                                                                                        \
-        if (a.trace && threadIdx.x == 0 && (k) < 64)                                            \
+        if (a.trace && threadIdx.x == 0 && (k) < 56)                                            \
             a.trace[blockIdx.x * 64 + (k)] = static_cast<unsigned long long>(clock64());        \
+    } while (0)
+// global-timer (ns) marks in slots 56..63: 63 entry, 60 after griddepcontrol.wait,
+// 59 weights landed, 61 unit loop done, 62 exit
+#define FTRG(k)                                                                                 \
+    do {                                                                                        \
+        if (a.trace && threadIdx.x == 0) {                                                      \
+            unsigned long long g_;                                                              \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_));                              \
+            a.trace[blockIdx.x * 64 + (k)] = g_;                                                \
+        }                                                                                       \
     } while (0)
 
 template <int NT, int GC, bool kF64>
@@ -434,6 +444,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
     const bool leader = rank == 0 && threadIdx.x == 0;
 
     if (smem - smem_raw > 1024) __trap();
+    FTRG(63);
     griddep_launch_dependents();
     if (threadIdx.x == 0) {
         mbar_init(bW, 1);
@@ -503,9 +514,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         }
     };
     griddep_wait();  // x / PE / ids come from earlier kernels
+    FTRG(60);
     int gid[2], sid[2];
     unit_ids(a.ridx, pair, gid);
     if (threadIdx.x == 0) mbar_wait(bW, 0);
+    FTRG(59);
     FTR(0);
     int it = 0;
     for (int u = pair; u < a.n_units; u += npairs, ++it) {
@@ -815,11 +828,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         }
         FTR(tb + 15);
     }
+    FTRG(61);
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(a.nonfinite, 1);
     fence_before_sync();
     cluster_sync_all();
     fence_after_sync();
     if (warp == 0) tmem_dealloc2(tmem, 512);
+    FTRG(62);
 }
 
 template <int NT, int GC, bool kF64>

@@ -476,12 +476,14 @@ int32_t* sort_specs(fwa_b200_ctx* c, const double* d_coords, int64_t ntot, int n
         launch_scan_bins_dev(hist, bin_start, cursor, d_nbins, kBinCap, tile_sums, ticket + 1, st, &c->launches);
         int32_t* pre = ws<int32_t>(c, "pre", static_cast<size_t>(total));
         double* pre_loc = ws<double>(c, "pre_loc", 2 * static_cast<size_t>(total));
-        launch_bin_scatter(bin_of, loc, ntot, n_specs, cursor, pre, pre_loc, d_nbins, tile_sums, st, &c->launches);
+        uint32_t* pre_bin = ws<uint32_t>(c, "pre_bin", static_cast<size_t>(total));
+        launch_bin_scatter(bin_of, loc, ntot, n_specs, cursor, pre, pre_loc, d_nbins, tile_sums, pre_bin, st,
+                           &c->launches);
         int32_t* sorted = ws<int32_t>(c, "sorted", static_cast<size_t>(total));
         int32_t* inv = ws<int32_t>(c, "sorted_inv", static_cast<size_t>(total));
         int32_t* scratch = ws<int32_t>(c, "sort_scratch", 2 * static_cast<size_t>(total));
-        launch_bin_sort(bin_start, hist, 0u, pre, pre_loc, loc, ntot, sorted, inv, scratch, large, d_nbins,
-                        tile_sums, st, &c->launches);
+        launch_bin_sort(bin_start, hist, 0u, pre, pre_loc, pre_bin, loc, ntot, n_specs, sorted, inv, scratch,
+                        large, d_nbins, tile_sums, st, &c->launches);
         check_launch();
         return sorted;
     }
@@ -521,13 +523,15 @@ int32_t* sort_specs(fwa_b200_ctx* c, const double* d_coords, int64_t ntot, int n
     CUDA_OK(cudaMemcpyAsync(cursor, bin_start, static_cast<size_t>(nbins) * 4, cudaMemcpyDeviceToDevice, st));
     int32_t* pre = ws<int32_t>(c, "pre", static_cast<size_t>(total));
     double* pre_loc = ws<double>(c, "pre_loc", 2 * static_cast<size_t>(total));
-    launch_bin_scatter(bin_of, loc, ntot, n_specs, cursor, pre, pre_loc, nullptr, nullptr, st, &c->launches);
+    uint32_t* pre_bin = ws<uint32_t>(c, "pre_bin", static_cast<size_t>(total));
+    launch_bin_scatter(bin_of, loc, ntot, n_specs, cursor, pre, pre_loc, nullptr, nullptr, pre_bin, st,
+                       &c->launches);
     int32_t* sorted = ws<int32_t>(c, "sorted", static_cast<size_t>(total));
     int32_t* inv = ws<int32_t>(c, "sorted_inv", static_cast<size_t>(total));
     int32_t* scratch = ws<int32_t>(c, "sort_scratch", 2 * static_cast<size_t>(total));
     uint32_t* large = ws<uint32_t>(c, "large_bins", static_cast<size_t>(nbins) + 1);
-    launch_bin_sort(bin_start, hist, static_cast<uint32_t>(nbins), pre, pre_loc, loc, ntot, sorted, inv,
-                    scratch, large, nullptr, nullptr, st, &c->launches);
+    launch_bin_sort(bin_start, hist, static_cast<uint32_t>(nbins), pre, pre_loc, pre_bin, loc, ntot, n_specs,
+                    sorted, inv, scratch, large, nullptr, nullptr, st, &c->launches);
     check_launch();
     return sorted;
 }

@@ -61,14 +61,16 @@ void launch_zero_bins(uint32_t* hist, const uint32_t* d_nbins, cudaStream_t s, i
 void launch_scan_bins_dev(const uint32_t* hist, uint32_t* bin_start, uint32_t* cursor, const uint32_t* d_nbins,
                           long long cap, uint32_t* tile_sums, unsigned* ticket, cudaStream_t s,
                           int64_t* launches);
+// pre[pos] = id, pre_loc[pos] = (integer key images of loc_major, loc_minor) as 2 x u64,
+// pre_bin[pos] = window bin, pos = the element's slot in its bin
 void launch_bin_scatter(const uint32_t* bin_of, const double* loc, int64_t ntot, int n_specs,
                         uint32_t* cursor, int32_t* pre, double* pre_loc, const uint32_t* d_nbins,
-                        const uint32_t* tile_off, cudaStream_t s, int64_t* launches);
+                        const uint32_t* tile_off, uint32_t* pre_bin, cudaStream_t s, int64_t* launches);
 // also writes the inverse permutation inv[s*ntot + id] = position in sorted
 // zeroes hist[] as it consumes it (the sync-free path relies on a clean histogram)
 void launch_bin_sort(const uint32_t* bin_start, uint32_t* hist, uint32_t n_bins,
-                     const int32_t* pre, const double* pre_loc, const double* loc, int64_t ntot,
-                     int32_t* sorted, int32_t* inv, int32_t* scratch,
+                     const int32_t* pre, const double* pre_loc, const uint32_t* pre_bin, const double* loc,
+                     int64_t ntot, int n_specs, int32_t* sorted, int32_t* inv, int32_t* scratch,
                      uint32_t* large /* 1 + n_bins words */, const uint32_t* d_nbins,
                      const uint32_t* tile_off, cudaStream_t s, int64_t* launches);
 constexpr int kMaxDropTable = 8192;

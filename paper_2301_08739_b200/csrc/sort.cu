@@ -266,6 +266,14 @@ void launch_bins_hist(const long long* win, int64_t ntot, int n_specs, const int
     ++*launches;
 }
 
+// Order-preserving integer image of a window-local coordinate: unsigned compare of the
+// images == the reference's double compare (key_less, flatten.hpp:41-47), with -0.0 and
+// +0.0 equal (both map to the +0.0 image).  Coordinates are finite.
+FWA_DEVINL unsigned long long ord_key(double d) {
+    const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(d == 0.0 ? 0.0 : d));
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ULL);
+}
+
 // ------------------------------------------------------------------ K3 scatter into bins
 
 __global__ void __launch_bounds__(256) k_bin_scatter(const uint32_t* __restrict__ bin_of,
@@ -274,24 +282,28 @@ __global__ void __launch_bounds__(256) k_bin_scatter(const uint32_t* __restrict_
                                                      int32_t* __restrict__ pre,
                                                      double* __restrict__ pre_loc,
                                                      const uint32_t* __restrict__ d_nbins,
-                                                     const uint32_t* __restrict__ tile_off) {
+                                                     const uint32_t* __restrict__ tile_off,
+                                                     uint32_t* __restrict__ pre_bin) {
     const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (e >= total) return;
     if (d_nbins && *d_nbins == 0u) return;
     const uint32_t b = bin_of[e];
     const uint32_t pos = atomicAdd(cursor + b, 1u) + (tile_off ? tile_off[b / kScanTile] : 0u);
     pre[pos] = static_cast<int32_t>(e % ntot);
-    // the window-local keys travel with the id: the per-bin sort reads them contiguously
-    reinterpret_cast<double2*>(pre_loc)[pos] = reinterpret_cast<const double2*>(loc)[e];
+    pre_bin[pos] = b;
+    // the window-local keys travel with the id as order-preserving integer images: the
+    // per-bin rank kernel reads them contiguously and compares integers
+    const double2 l = reinterpret_cast<const double2*>(loc)[e];
+    reinterpret_cast<ulonglong2*>(pre_loc)[pos] = make_ulonglong2(ord_key(l.x), ord_key(l.y));
 }
 
 void launch_bin_scatter(const uint32_t* bin_of, const double* loc, int64_t ntot, int n_specs,
                         uint32_t* cursor, int32_t* pre, double* pre_loc, const uint32_t* d_nbins,
-                        const uint32_t* tile_off, cudaStream_t s, int64_t* launches) {
+                        const uint32_t* tile_off, uint32_t* pre_bin, cudaStream_t s, int64_t* launches) {
     const int64_t total = ntot * n_specs;
     k_bin_scatter<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(bin_of, loc, total, ntot,
                                                                            cursor, pre, pre_loc, d_nbins,
-                                                                           tile_off);
+                                                                           tile_off, pre_bin);
     ++*launches;
 }
 
@@ -308,105 +320,48 @@ constexpr int kWarpBin = 128;   // bins up to this size: one warp, shared memory
 constexpr int kCtaBin = 4096;   // up to this: one CTA, shared-memory rank sort
 constexpr int kBinWarps = 8;
 
-// Order-preserving integer image of a window-local coordinate: unsigned compare of the
-// images == the reference's double compare (key_less, flatten.hpp:41-47), with -0.0 and
-// +0.0 equal (both map to the +0.0 image).  Coordinates are finite.
-FWA_DEVINL unsigned long long ord_key(double d) {
-    const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(d == 0.0 ? 0.0 : d));
-    return (u >> 63) ? ~u : (u | 0x8000000000000000ULL);
-}
-
-// rank of each of this lane's NQ elements (lane + 32q) among the bin's n elements, and
-// its placement; every element j is read once (shared-memory broadcast) per warp
-template <int NQ>
-FWA_DEVINL void rank_place(int n, int lane, const unsigned long long* sa, const unsigned long long* sb,
-                           const int* si, uint32_t start, int64_t spec_base, int32_t* __restrict__ sorted,
-                           int32_t* __restrict__ inv) {
-    unsigned long long ea[NQ], eb[NQ];
-    int ei[NQ], er[NQ];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-        const int k = lane + 32 * q;
-        const bool ok = k < n;
-        ea[q] = ok ? sa[k] : ~0ULL;
-        eb[q] = ok ? sb[k] : ~0ULL;
-        ei[q] = ok ? si[k] : 0x7fffffff;
-        er[q] = 0;
+// One thread per binned element: its rank among the elements of its window bin (integer
+// key images, then the original index -- key_less, flatten.hpp:41-47) by one pass over
+// the bin (n <= kWarpBin; the bin's elements are contiguous, so the loads of a warp are
+// shared-memory-like broadcasts out of L1).  Bigger bins are queued for
+// k_bin_sort_large by their first element.  Writes sorted[] and the inverse inv[].
+__global__ void __launch_bounds__(256) k_bin_rank(const uint32_t* __restrict__ bin_start,
+                                                  uint32_t* __restrict__ hist, uint32_t n_bins,
+                                                  const int32_t* __restrict__ pre,
+                                                  const ulonglong2* __restrict__ pkey,
+                                                  const uint32_t* __restrict__ pre_bin, int64_t total,
+                                                  int64_t ntot, int32_t* __restrict__ sorted,
+                                                  int32_t* __restrict__ inv, uint32_t* __restrict__ large,
+                                                  const uint32_t* __restrict__ d_nbins,
+                                                  const uint32_t* __restrict__ tile_off) {
+    const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (d_nbins) {
+        n_bins = *d_nbins;
+        if (n_bins == 0u) return;
     }
-#pragma unroll 4
-    for (int j = 0; j < n; ++j) {
-        const unsigned long long a = sa[j], b = sb[j];
-        const int id = si[j];
-#pragma unroll
-        for (int q = 0; q < NQ; ++q)
-            er[q] += (a < ea[q]) | ((a == ea[q]) & ((b < eb[q]) | ((b == eb[q]) & (id < ei[q]))));
-    }
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-        const int k = lane + 32 * q;
-        if (k < n) {
-            sorted[start + er[q]] = ei[q];
-            inv[spec_base + ei[q]] = static_cast<int32_t>(start + er[q]);
-        }
-    }
-}
-
-// One warp sorts one window bin (<= kWarpBin points) by rank counting in shared memory:
-// lane l owns elements l, l+32, l+64, l+96; every element j is broadcast once and
-// compared with all of them (integer keys, no fp64 compares).  Bigger bins are queued
-// for k_bin_sort_large.  Writes sorted[] and the inverse inv[].
-FWA_DEVINL void sort_one_small_bin(uint32_t bin, const uint32_t* __restrict__ bin_start,
-                                   uint32_t* __restrict__ hist, const int32_t* __restrict__ pre,
-                                   const double* __restrict__ ploc, int64_t ntot, int32_t* __restrict__ sorted,
-                                   int32_t* __restrict__ inv, uint32_t* __restrict__ large,
-                                   const uint32_t* __restrict__ tile_off,
-                                   unsigned long long* sa, unsigned long long* sb, int* si, int lane) {
-    const int n = static_cast<int>(hist[bin]);
-    if (n > kWarpBin) {  // queue for the CTA-level kernel; large[0] = count
-        if (lane == 0) large[1 + atomicAdd(large, 1u)] = bin;
+    if (p >= total) return;
+    const uint32_t b = pre_bin[p];
+    const int64_t start = bin_start[b] + (tile_off ? tile_off[b / kScanTile] : 0u);
+    const int64_t end = b + 1 < n_bins ? bin_start[b + 1] + (tile_off ? tile_off[(b + 1) / kScanTile] : 0u) : total;
+    const int n = static_cast<int>(end - start);
+    if (n > kWarpBin) {
+        if (p == start) large[1 + atomicAdd(large, 1u)] = b;  // k_bin_sort_large zeroes hist[b]
         return;
     }
-    if (n == 0) return;
-    __syncwarp();
-    if (lane == 0) hist[bin] = 0u;  // leave the histogram zeroed for the next call
-    const uint32_t start = bin_start[bin] + (tile_off ? tile_off[bin / kScanTile] : 0u);
-    const int64_t spec_base = (static_cast<int64_t>(start) / ntot) * ntot;
-    if (n == 1) {
-        if (lane == 0) {
-            const int id = pre[start];
-            sorted[start] = id;
-            inv[spec_base + id] = static_cast<int32_t>(start);
-        }
-        return;
+    if (p == start) hist[b] = 0u;  // leave the histogram zeroed for the next call
+    const ulonglong2 me = pkey[p];
+    const int my = pre[p];
+    int rank = 0;
+    const int nn = n;
+#pragma unroll 8
+    for (int j = 0; j < nn; ++j) {
+        const ulonglong2 o = __ldg(pkey + start + j);
+        const int oid = __ldg(pre + start + j);
+        rank += (o.x < me.x) | ((o.x == me.x) & ((o.y < me.y) | ((o.y == me.y) & (oid < my))));
     }
-    for (int k = lane; k < n; k += 32) {
-        const double2 l = reinterpret_cast<const double2*>(ploc)[start + k];
-        sa[k] = ord_key(l.x);
-        sb[k] = ord_key(l.y);
-        si[k] = pre[start + k];
-    }
-    __syncwarp();
-    const int nq = (n + 31) >> 5;
-    if (nq == 1) rank_place<1>(n, lane, sa, sb, si, start, spec_base, sorted, inv);
-    else if (nq == 2) rank_place<2>(n, lane, sa, sb, si, start, spec_base, sorted, inv);
-    else if (nq == 3) rank_place<3>(n, lane, sa, sb, si, start, spec_base, sorted, inv);
-    else rank_place<4>(n, lane, sa, sb, si, start, spec_base, sorted, inv);
-    __syncwarp();
-}
-
-__global__ void __launch_bounds__(kBinWarps * 32) k_bin_sort_small(
-    const uint32_t* __restrict__ bin_start, uint32_t* __restrict__ hist, uint32_t n_bins,
-    const int32_t* __restrict__ pre, const double* __restrict__ ploc, int64_t ntot,
-    int32_t* __restrict__ sorted, int32_t* __restrict__ inv, uint32_t* __restrict__ large,
-    const uint32_t* __restrict__ d_nbins, const uint32_t* __restrict__ tile_off) {
-    __shared__ unsigned long long s_a[kBinWarps][kWarpBin];
-    __shared__ unsigned long long s_b[kBinWarps][kWarpBin];
-    __shared__ int s_i[kBinWarps][kWarpBin];
-    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (d_nbins) n_bins = *d_nbins;  // sync-free path: grid-stride over the device-side count
-    for (uint32_t bin = blockIdx.x * kBinWarps + wid; bin < n_bins; bin += gridDim.x * kBinWarps)
-        sort_one_small_bin(bin, bin_start, hist, pre, ploc, ntot, sorted, inv, large, tile_off, s_a[wid],
-                           s_b[wid], s_i[wid], lane);
+    const int64_t spec_base = (start / ntot) * ntot;
+    sorted[start + rank] = my;
+    inv[spec_base + my] = static_cast<int32_t>(start + rank);
 }
 
 __global__ void __launch_bounds__(512) k_bin_sort_large(
@@ -485,14 +440,15 @@ __global__ void __launch_bounds__(512) k_bin_sort_large(
 }
 
 void launch_bin_sort(const uint32_t* bin_start, uint32_t* hist, uint32_t n_bins,
-                     const int32_t* pre, const double* pre_loc, const double* loc, int64_t ntot,
-                     int32_t* sorted, int32_t* inv, int32_t* scratch, uint32_t* large,
-                     const uint32_t* d_nbins, const uint32_t* tile_off, cudaStream_t s, int64_t* launches) {
-    // host-known n_bins: one warp per bin; device-side count: grid-stride
-    const unsigned grid = d_nbins ? kNumSMs * 16 : (n_bins + kBinWarps - 1) / kBinWarps;
+                     const int32_t* pre, const double* pre_loc, const uint32_t* pre_bin, const double* loc,
+                     int64_t ntot, int n_specs, int32_t* sorted, int32_t* inv, int32_t* scratch,
+                     uint32_t* large, const uint32_t* d_nbins, const uint32_t* tile_off, cudaStream_t s,
+                     int64_t* launches) {
+    const int64_t total = ntot * n_specs;
     if (!d_nbins) cudaMemsetAsync(large, 0, sizeof(uint32_t), s);  // sync-free path: reset by the key kernel
-    k_bin_sort_small<<<grid, kBinWarps * 32, 0, s>>>(bin_start, hist, n_bins, pre, pre_loc, ntot,
-                                                     sorted, inv, large, d_nbins, tile_off);
+    k_bin_rank<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
+        bin_start, hist, n_bins, pre, reinterpret_cast<const ulonglong2*>(pre_loc), pre_bin, total, ntot, sorted,
+        inv, large, d_nbins, tile_off);
     static bool attr_set = false;
     const int smem = kCtaBin * (8 + 8 + 4);
     if (!attr_set) {
@@ -725,36 +681,49 @@ void launch_compact_all(const int32_t* sorted, int64_t ntot, int n_specs, const 
 __device__ void bins_setup_cta(const long long* __restrict__ partials, int64_t n_part, int n_specs, int nf,
                                long long cap, long long* __restrict__ mm, SpecBins* __restrict__ specs,
                                uint32_t* __restrict__ d_nbins, int* __restrict__ overflow) {
-    __shared__ long long red[32][4];
+    // one pass over all specs' partials (loads of every spec in flight together), then a
+    // shared-memory reduction of the 4 x n_specs values
+    __shared__ long long red[32][16];
     __shared__ long long fin[4][4];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int s = 0; s < n_specs; ++s) {
-        long long v[4] = {LLONG_MAX, LLONG_MIN, LLONG_MAX, LLONG_MIN};
-        for (int64_t i = threadIdx.x; i < n_part; i += blockDim.x) {
-            const long long* p = partials + (static_cast<int64_t>(s) * n_part + i) * 4;
-            const long long p0 = __ldcg(p), p1 = __ldcg(p + 1), p2 = __ldcg(p + 2), p3 = __ldcg(p + 3);
-            v[0] = p0 < v[0] ? p0 : v[0];
-            v[1] = p1 > v[1] ? p1 : v[1];
-            v[2] = p2 < v[2] ? p2 : v[2];
-            v[3] = p3 > v[3] ? p3 : v[3];
-        }
-        v[0] = wmin(v[0]);
-        v[1] = wmax(v[1]);
-        v[2] = wmin(v[2]);
-        v[3] = wmax(v[3]);
-        if (lane == 0)
-            for (int q = 0; q < 4; ++q) red[wid][q] = v[q];
-        __syncthreads();
-        if (threadIdx.x < 4) {
-            const int q = threadIdx.x;
-            long long r = red[0][q];
-            for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
-                r = (q & 1) ? (red[w][q] > r ? red[w][q] : r) : (red[w][q] < r ? red[w][q] : r);
-            fin[s][q] = r;
-            mm[4 * s + q] = r;
-        }
-        __syncthreads();
+    long long v[4][4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        v[s][0] = LLONG_MAX; v[s][1] = LLONG_MIN; v[s][2] = LLONG_MAX; v[s][3] = LLONG_MIN;
     }
+    for (int64_t i = threadIdx.x; i < n_part; i += blockDim.x) {
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            if (s >= n_specs) break;
+            const longlong2* p = reinterpret_cast<const longlong2*>(partials + (static_cast<int64_t>(s) * n_part + i) * 4);
+            const longlong2 a = __ldcg(p), b = __ldcg(p + 1);
+            v[s][0] = a.x < v[s][0] ? a.x : v[s][0];
+            v[s][1] = a.y > v[s][1] ? a.y : v[s][1];
+            v[s][2] = b.x < v[s][2] ? b.x : v[s][2];
+            v[s][3] = b.y > v[s][3] ? b.y : v[s][3];
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        v[s][0] = wmin(v[s][0]);
+        v[s][1] = wmax(v[s][1]);
+        v[s][2] = wmin(v[s][2]);
+        v[s][3] = wmax(v[s][3]);
+        if (lane == 0)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) red[wid][4 * s + q] = v[s][q];
+    }
+    __syncthreads();
+    if (threadIdx.x < 4 * n_specs) {
+        const int s = threadIdx.x >> 2, q = threadIdx.x & 3;
+        long long r = red[0][threadIdx.x];
+        for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
+            r = (q & 1) ? (red[w][threadIdx.x] > r ? red[w][threadIdx.x] : r)
+                        : (red[w][threadIdx.x] < r ? red[w][threadIdx.x] : r);
+        fin[s][q] = r;
+        mm[4 * s + q] = r;
+    }
+    __syncthreads();
     if (threadIdx.x != 0) return;
     long long nbins = 0;
     bool bad = false;

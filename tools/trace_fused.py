@@ -16,11 +16,18 @@ buf = np.zeros(2 * 148 * 64, np.uint64)
 F.lib().fwa_b200_debug_trace.argtypes = [C.c_void_p, C.c_void_p]
 assert F.lib().fwa_b200_debug_trace(ctx._h, buf.ctypes.data) == 0
 t = buf.reshape(2, 148, 64).astype(np.int64)[0]
+g = buf.reshape(2, 148, 64).astype(np.int64)[0]
+e0 = g[:, 63].min()
+def st(col): v = (g[:, col] - e0) / 1e3; return f"min {v.min():7.2f} med {np.median(v):7.2f} max {v.max():7.2f} us"
+print("fused kernel, global timer relative to the first CTA entry (us):")
+for col, nm in ((63, "entry"), (60, "griddep_wait done"), (59, "weights landed"), (61, "unit loop done"), (62, "exit")):
+    print(f"  {nm:18s} {st(col)}")
 names = ["start", "ln1_ld", "ln1", "qkv", "ep0", "att0", "ep1", "att1", "P", "ln2", "Ua", "ffn2a", "Ub", "ffn2b", "O", "out"]
 for cta in (0, 1, 40, 41, 146, 147):
     row = t[cta]
     print(f"cta {cta}: setup {row[1] - row[0] if row[1] else 0}")
     for u in range(3):
+        if 1 + 16 * u + 15 >= 56: break
         b = 1 + 16 * u
         if not row[b]:
             break
