@@ -377,3 +377,65 @@ def test_device_api_graph_replay_matches_host_api(ctx16):
         assert nk == len(want.kept_indices)
         assert np.array_equal(kept[:nk].cpu().numpy(), want.kept_indices), i
         assert np.array_equal(out[:nk].cpu().numpy(), want.features), i
+
+
+# ----------------------------------------------------------------------------- fused block kernel
+
+def test_fused_block_kernel_matches_three_kernel_pipeline():
+    """The one-launch CTA-pair block kernel (default bf16 path) and the three-kernel bf16
+    pipeline (FWA_PREC_BF16_3K) compute the same block with the same bf16 numerics."""
+    ps = F.make_pillars(F.SCENES["F10"], 43)
+    cfg = F.FwaConfig(n_blocks=4)
+    blob = F.init_backbone_params(cfg, 11)
+    outs = {}
+    for prec in ("bf16", "bf16_3k"):
+        ctx = F.Context(0, precision=prec)
+        ctx.load_params(cfg, blob)
+        outs[prec] = ctx.run_backbone(ps, cfg)
+    a, b = outs["bf16"], outs["bf16_3k"]
+    assert np.array_equal(a.kept_indices, b.kept_indices)
+    assert O.max_rel_err(a.features, b.features) <= 2e-3
+    w = O.port_run_backbone(ps.coords, ps.features.astype(np.float32), O.make_cfg(n_blocks=4), blob)
+    assert O.max_rel_err(a.features, w["features"]) <= TOL_BF16
+
+
+@pytest.mark.parametrize("n", [69, 70, 137, 138, 207, 208, 276, 415, 1000])
+def test_fused_block_kernel_partial_units(ctx16, n):
+    """Frames whose kept rows end inside a CTA pair's unit (1..3 groups of 69, rank 1 empty
+    or partly filled, the straddling group present or not): ints exact, features in tol."""
+    rng = np.random.default_rng(n)
+    c = rng.uniform(-8.0, 8.0, size=(n, 2)).round(2)
+    f = rng.normal(size=(n, 128))
+    cfg = F.FwaConfig(n_blocks=2)
+    blob = F.init_backbone_params(cfg, 5)
+    ctx16.load_params(cfg, blob)
+    r = ctx16.run_backbone(F.PillarSet(c, f), cfg)
+    w = O.port_run_backbone(c, f.astype(np.float32), O.make_cfg(n_blocks=2), blob)
+    _check_ints(r, w["kept"], w["dropped"], w["dropped_per_block"], w["cache"])
+    assert O.max_rel_err(r.features, w["features"]) <= TOL_BF16
+
+
+@pytest.mark.parametrize("G", [16, 33, 100, 128])
+def test_fused_block_kernel_group_sizes_backbone(ctx16, G):
+    """Full backbone through the fused kernel at non-default group sizes (other unit
+    geometries and row splits)."""
+    ps = F.make_pillars(F.SCENES["F10"], 44)
+    cfg = F.FwaConfig(group_size=G, n_blocks=2)
+    blob = F.init_backbone_params(cfg, 6)
+    ctx16.load_params(cfg, blob)
+    r = ctx16.run_backbone(ps, cfg)
+    w = O.port_run_backbone(ps.coords, ps.features.astype(np.float32), O.make_cfg(group_size=G, n_blocks=2), blob)
+    _check_ints(r, w["kept"], w["dropped"], w["dropped_per_block"], w["cache"])
+    assert O.max_rel_err(r.features, w["features"]) <= TOL_BF16
+
+
+def test_fused_block_kernel_nonfinite_input_raises(ctx16):
+    """kernels.hpp:460-461 through the fused kernel's gather (numeric_error)."""
+    cfg = F.FwaConfig(n_blocks=1)
+    ctx16.load_params(cfg, F.init_backbone_params(cfg, 1))
+    rng = np.random.default_rng(3)
+    c = rng.uniform(0, 10, size=(300, 2))
+    f = rng.normal(size=(300, 128))
+    f[17, 5] = np.inf
+    with pytest.raises(F.NumericError):
+        ctx16.run_backbone(F.PillarSet(c, f), cfg)
