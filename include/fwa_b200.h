@@ -15,6 +15,9 @@
  *   fwa_b200_positional_embedding    fwa::kernels::positional_embedding  include/fwa/kernels.hpp:364-393
  *   fwa_b200_load_params             fwa::kernels::load_params (FWAP records)  include/fwa/kernels.hpp:177-206
  *                                    + fwa::kernels::validate  kernels.hpp:75-90
+ *   fwa_b200_pillarize[_device]      fwa::geometry::pillarize on the GPU  include/fwa/geometry.hpp:246-300
+ *   fwa_b200_generate_points         fwa::geometry::generate_synthetic  include/fwa/geometry.hpp:355-386
+ *   fwa_b200_pillar_params           fwa::geometry::random_pillar_params  include/fwa/geometry.hpp:71-79
  *   fwa_b200_generate_pillars        fwa::geometry::generate_synthetic + pillarize +
  *                                    random_pillar_params  include/fwa/geometry.hpp:355-386, 246-300, 71-79
  *   fwa_b200_init_params             fwa::backbone::init_backbone_params  include/fwa/backbone.hpp:83-102
@@ -192,6 +195,22 @@ int fwa_b200_positional_embedding(fwa_b200_ctx* ctx, const double* coords, int64
 int fwa_b200_positional_embedding_f16(fwa_b200_ctx* ctx, const double* coords, int64_t n,
                                       int32_t d_model, uint16_t* out);
 
+/* geometry::pillarize (geometry.hpp:246-300) on the GPU: points x,y (n x 2 f64) +
+ * features (n x f_in f64) -> pillars in ascending lexicographic (x-cell, y-cell) order,
+ * members mean-pooled with the reference's pairwise summation in ingestion order, then
+ * gelu(bias + W pooled) (W: d_out x f_in, bias may be NULL = zeros).  Cell order and
+ * coordinates are bit-exact; features use the reference's fp64 operation order (CUDA erf
+ * for libm erf).  coords_out == NULL only counts.  Host buffers; *n_pillars = P. */
+int fwa_b200_pillarize(fwa_b200_ctx* ctx, const double* xy, const double* feats, int64_t n, int32_t f_in,
+                       double resolution, const double* weight, const double* bias, int32_t d_out,
+                       double* coords_out, double* feats_out, int64_t* n_pillars);
+/* The same with device buffers (capacity = rows available in the outputs; n is always
+ * enough), so the pillars can feed fwa_b200_backbone_forward_device directly. */
+int fwa_b200_pillarize_device(fwa_b200_ctx* ctx, const double* d_xy, const double* d_feats, int64_t n,
+                              int32_t f_in, double resolution, const double* d_weight, const double* d_bias,
+                              int32_t d_out, double* d_coords_out, double* d_feats_out, int64_t capacity,
+                              int64_t* n_pillars);
+
 /* ---- host-side input generators (bit-identical to the reference's) ---- */
 
 /* geometry::SceneSpec (geometry.hpp:310-319). */
@@ -208,6 +227,13 @@ typedef struct fwa_scene_spec {
 int64_t fwa_b200_generate_pillars(const fwa_scene_spec_t* spec, uint64_t seed, double resolution,
                                   int32_t d_out, uint64_t param_seed, double* coords,
                                   double* feats);
+
+/* generate_synthetic(spec, seed) raw point cloud: returns n; xy (n x 2) and feats
+ * (n x f_in) filled when xy != NULL. */
+int64_t fwa_b200_generate_points(const fwa_scene_spec_t* spec, uint64_t seed, double* xy, double* feats);
+/* random_pillar_params(f_in, d_out, seed) weight (d_out x f_in, N(0, 0.5^2)); bias is 0.
+ * Returns d_out * f_in or -status. */
+int64_t fwa_b200_pillar_params(int32_t f_in, int32_t d_out, uint64_t seed, double* weight);
 
 /* init_backbone_params(cfg, f_in == d_model, seed) as FWAP records.  Returns
  * the blob length (out may be NULL to size) or -status. */

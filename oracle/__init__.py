@@ -336,3 +336,43 @@ def max_rel_err(got, want):
     if want.size == 0:
         return 0.0
     return float(np.max(np.abs(got - want)) / max(float(np.max(np.abs(want))), 1e-30))
+
+
+def _pairwise_sum(v):
+    """dense.hpp:84-94: <= 8 values summed left to right from 0.0, else the two halves."""
+    if len(v) <= 8:
+        s = 0.0
+        for x in v:
+            s += x
+        return s
+    h = len(v) // 2
+    return _pairwise_sum(v[:h]) + _pairwise_sum(v[h:])
+
+
+def np_pillarize(xy, feats, resolution, weight, bias=None):
+    """Pure-Python restatement of geometry::pillarize (geometry.hpp:246-300) for small
+    clouds: cells (floor(x / res), floor(y / res)) in lexicographic order (std::map),
+    members in ingestion order, pairwise mean pooling, gelu(bias + W pooled) in fp64
+    with libm erf (math.erf), coords (cell + 0.5) * res.  Returns (coords, features)."""
+    import math
+    xy = np.asarray(xy, np.float64)
+    feats = np.asarray(feats, np.float64).reshape(xy.shape[0], -1)
+    weight = np.asarray(weight, np.float64)
+    d_out, f_in = weight.shape
+    cells = {}
+    for i in range(xy.shape[0]):
+        key = (int(math.floor(xy[i, 0] / resolution)), int(math.floor(xy[i, 1] / resolution)))
+        cells.setdefault(key, []).append(i)
+    coords, out = [], []
+    for key in sorted(cells):
+        mem = cells[key]
+        pooled = [_pairwise_sum([float(feats[m, c]) for m in mem]) / float(len(mem)) for c in range(f_in)]
+        row = []
+        for o in range(d_out):
+            acc = 0.0 if bias is None else float(bias[o])
+            for c in range(f_in):
+                acc += float(weight[o, c]) * pooled[c]
+            row.append(0.5 * acc * (1.0 + math.erf(acc / 1.4142135623730951)))
+        out.append(row)
+        coords.append(((key[0] + 0.5) * resolution, (key[1] + 0.5) * resolution))
+    return (np.array(coords, np.float64).reshape(-1, 2), np.array(out, np.float64).reshape(-1, d_out))

@@ -37,6 +37,7 @@ EXPORTS = [
     "fwa_b200_backbone_forward_device", "fwa_b200_sort_plan", "fwa_b200_block_forward",
     "fwa_b200_positional_embedding", "fwa_b200_positional_embedding_f16", "fwa_b200_generate_pillars", "fwa_b200_init_params",
     "fwa_b200_split_begin", "fwa_b200_split_block", "fwa_b200_split_scatter",
+    "fwa_b200_pillarize", "fwa_b200_pillarize_device", "fwa_b200_generate_points", "fwa_b200_pillar_params",
 ]
 
 PREC_BF16, PREC_FP32, PREC_BF16_3K = 0, 1, 2
@@ -143,6 +144,13 @@ def lib():
         L.fwa_b200_split_scatter.argtypes = [vp, C.c_int, vp, vp]
         L.fwa_b200_init_params.argtypes = [C.POINTER(_Cfg), C.c_uint64, vp, C.c_size_t]
         L.fwa_b200_init_params.restype = i64
+        L.fwa_b200_pillarize.argtypes = [vp, vp, vp, i64, i32, C.c_double, vp, vp, i32, vp, vp, C.POINTER(i64)]
+        L.fwa_b200_pillarize_device.argtypes = [vp, vp, vp, i64, i32, C.c_double, vp, vp, i32, vp, vp, i64,
+                                                C.POINTER(i64)]
+        L.fwa_b200_generate_points.argtypes = [C.POINTER(_Scene), C.c_uint64, vp, vp]
+        L.fwa_b200_generate_points.restype = i64
+        L.fwa_b200_pillar_params.argtypes = [i32, i32, C.c_uint64, vp]
+        L.fwa_b200_pillar_params.restype = i64
         _lib_handle = L
     return _lib_handle
 
@@ -444,6 +452,23 @@ class Context:
                                                             d_model, _ptr(out)))
         return out
 
+    def pillarize(self, xy: np.ndarray, feats: np.ndarray, resolution: float, weight: np.ndarray,
+                  bias: Optional[np.ndarray] = None) -> "PillarSet":
+        """geometry::pillarize (geometry.hpp:246-300) on the GPU."""
+        xy = np.ascontiguousarray(xy, np.float64)
+        feats = np.ascontiguousarray(feats, np.float64)
+        weight = np.ascontiguousarray(weight, np.float64)
+        n, f_in = xy.shape[0], (feats.shape[1] if feats.ndim == 2 else 0)
+        d_out = weight.shape[0]
+        b = None if bias is None else np.ascontiguousarray(bias, np.float64)
+        np_ = C.c_int64(0)
+        coords = np.empty((max(n, 1), 2), np.float64)
+        out = np.empty((max(n, 1), d_out), np.float64)
+        self._check(lib().fwa_b200_pillarize(self._h, _ptr(xy), _ptr(feats), n, f_in, resolution, _ptr(weight),
+                                              _ptr(b), d_out, _ptr(coords), _ptr(out), C.byref(np_)))
+        p = np_.value
+        return PillarSet(coords[:p].copy(), out[:p].copy(), resolution)
+
     def fwa_block_forward(self, f: np.ndarray, pe: np.ndarray, record: bytes, n_groups: int) -> np.ndarray:
         f = np.ascontiguousarray(f, np.float32)
         pe = np.ascontiguousarray(pe, np.float32)
@@ -544,8 +569,7 @@ def make_pillars(scene: SceneSpec, seed: int, d_out: int = 128, param_seed: Opti
                  resolution: float = 0.32) -> PillarSet:
     """generate_synthetic(scene, seed) -> pillarize(., resolution,
     random_pillar_params(f_in, d_out, param_seed)) — bit-identical to the reference."""
-    s = _Scene(scene.n_clusters, scene.points_per_cluster_min, scene.points_per_cluster_max,
-               scene.cluster_sigma, scene.extent_x, scene.extent_y, scene.n_background, scene.f_in)
+    s = _scene_c(scene)
     ps = seed if param_seed is None else param_seed
     n = lib().fwa_b200_generate_pillars(C.byref(s), seed, resolution, d_out, ps, None, None)
     if n < 0:
@@ -554,6 +578,33 @@ def make_pillars(scene: SceneSpec, seed: int, d_out: int = 128, param_seed: Opti
     feats = np.empty((n, d_out), np.float64)
     lib().fwa_b200_generate_pillars(C.byref(s), seed, resolution, d_out, ps, _ptr(coords), _ptr(feats))
     return PillarSet(coords, feats, resolution)
+
+
+def _scene_c(scene: SceneSpec):
+    return _Scene(scene.n_clusters, scene.points_per_cluster_min, scene.points_per_cluster_max,
+                  scene.cluster_sigma, scene.extent_x, scene.extent_y, scene.n_background, scene.f_in)
+
+
+def generate_points(scene: SceneSpec, seed: int):
+    """generate_synthetic(scene, seed) (geometry.hpp:355-386): (xy n x 2, features n x f_in),
+    bit-identical to the reference's point cloud."""
+    s = _scene_c(scene)
+    n = lib().fwa_b200_generate_points(C.byref(s), seed, None, None)
+    if n < 0:
+        raise _ERRS.get(-n, FwaError)("generate_synthetic failed")
+    xy = np.empty((n, 2), np.float64)
+    f = np.empty((n, scene.f_in), np.float64)
+    lib().fwa_b200_generate_points(C.byref(s), seed, _ptr(xy), _ptr(f))
+    return xy, f
+
+
+def pillar_params(f_in: int, d_out: int, seed: int) -> np.ndarray:
+    """random_pillar_params (geometry.hpp:71-79): weight d_out x f_in ~ N(0, 0.5^2), bias 0."""
+    w = np.empty((d_out, f_in), np.float64)
+    n = lib().fwa_b200_pillar_params(f_in, d_out, seed, _ptr(w))
+    if n < 0:
+        raise _ERRS.get(-n, FwaError)("random_pillar_params failed")
+    return w
 
 
 def fnv1a64_hex(b: bytes) -> str:

@@ -1333,6 +1333,60 @@ int fwa_b200_positional_embedding(fwa_b200_ctx* c, const double* coords, int64_t
     });
 }
 
+// geometry::pillarize (geometry.hpp:246-300) on the device; returns the pillar count P
+// (one host round trip for the cell range, one for P).  coords_out == nullptr: count only.
+static int64_t pillarize_device(fwa_b200_ctx* c, const double* d_xy, const double* d_feats, int64_t n, int32_t f_in,
+                                double res, const double* d_w, const double* d_b, int32_t d_out, double* d_coords,
+                                double* d_out_feats, int64_t cap) {
+    if (!(res > 0.0)) throw FwaError{FWA_ERR_CONFIG, "pillarize: resolution must be > 0"};
+    if (d_out < 1) throw FwaError{FWA_ERR_CONFIG, "pillarize: d_out must be >= 1"};
+    if (f_in < 0 || n < 0) throw FwaError{FWA_ERR_SHAPE, "pillarize: negative size"};
+    if (n == 0) return 0;
+    cudaStream_t st = c->stream;
+    long long* cell = ws<long long>(c, "pz_cell", 2 * static_cast<size_t>(n));
+    long long* mm = ws<long long>(c, "pz_mm", 4);
+    launch_cell_keys(d_xy, n, res, cell, mm, st, &c->launches);
+    check_launch("k_cell_keys");
+    CUDA_OK(cudaMemcpyAsync(c->h_minmax, mm, 4 * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+    const long long min_x = c->h_minmax[0], min_y = c->h_minmax[2];
+    const long long rx = c->h_minmax[1] - min_x + 1, ry = c->h_minmax[3] - min_y + 1;
+    if (rx <= 0 || ry <= 0 || static_cast<double>(rx) * static_cast<double>(ry) > 2.0e9)
+        throw FwaError{FWA_ERR_CONFIG, "pillarize: cell index range too large for the dense cell grid"};
+    const int64_t ncell = rx * ry;
+    uint32_t* hist = ws<uint32_t>(c, "pz_hist", static_cast<size_t>(ncell));
+    uint32_t* cell_id = ws<uint32_t>(c, "pz_cellid", static_cast<size_t>(n));
+    CUDA_OK(cudaMemsetAsync(hist, 0, static_cast<size_t>(ncell) * 4, st));
+    launch_cell_hist(cell, n, min_x, min_y, ry, cell_id, hist, st, &c->launches);
+    uint32_t* start = ws<uint32_t>(c, "pz_start", static_cast<size_t>(ncell));
+    uint32_t* flag = ws<uint32_t>(c, "pz_flag", static_cast<size_t>(ncell));
+    uint32_t* prow = ws<uint32_t>(c, "pz_prow", static_cast<size_t>(ncell));
+    uint32_t* tmp = ws<uint32_t>(c, "pz_scan_tmp", scan_tmp_words(ncell) + 8);
+    uint32_t* d_total = ws<uint32_t>(c, "pz_total", 4);
+    exclusive_scan_u32(hist, start, ncell, tmp, nullptr, st, &c->launches);
+    launch_nonempty(hist, ncell, flag, st, &c->launches);
+    exclusive_scan_u32(flag, prow, ncell, tmp, d_total, st, &c->launches);
+    CUDA_OK(cudaMemcpyAsync(c->h_flag, d_total, 4, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+    check_launch("pillarize cells");
+    const int64_t np = static_cast<uint32_t>(*c->h_flag);
+    if (!d_coords) return np;
+    if (np > cap) throw FwaError{FWA_ERR_SHAPE, "pillarize: output capacity smaller than the pillar count"};
+    uint32_t* pcell = ws<uint32_t>(c, "pz_pcell", static_cast<size_t>(np));
+    launch_pillar_cells(hist, prow, ncell, min_x, min_y, ry, res, pcell, d_coords, st, &c->launches);
+    uint32_t* cursor = ws<uint32_t>(c, "pz_cursor", static_cast<size_t>(ncell));
+    CUDA_OK(cudaMemcpyAsync(cursor, start, static_cast<size_t>(ncell) * 4, cudaMemcpyDeviceToDevice, st));
+    int32_t* slot = ws<int32_t>(c, "pz_slot", static_cast<size_t>(n));
+    const size_t fi = static_cast<size_t>(f_in > 0 ? f_in : 1);
+    double* fs = ws<double>(c, "pz_fs", static_cast<size_t>(n) * fi);
+    launch_cell_members(cell_id, n, cursor, slot, start, hist, d_feats, f_in, fs, st, &c->launches);
+    double* pooled = ws<double>(c, "pz_pooled", static_cast<size_t>(np) * fi);
+    launch_pillar_features(pcell, start, hist, np, f_in, fs, pooled, d_w, d_b, d_out, d_out_feats, st,
+                           &c->launches);
+    check_launch("pillarize features");
+    return np;
+}
+
 int fwa_b200_positional_embedding_f16(fwa_b200_ctx* c, const double* coords, int64_t n, int32_t d,
                                       uint16_t* out) {
     return guarded(c, [&] {
@@ -1346,6 +1400,49 @@ int fwa_b200_positional_embedding_f16(fwa_b200_ctx* c, const double* coords, int
         launch_positional_embedding(dc, n, d, pe_freq(c, d), nullptr, dp, st, &c->launches);
         check_launch();
         CUDA_OK(cudaMemcpyAsync(out, dp, static_cast<size_t>(n) * d * 2, cudaMemcpyDeviceToHost, st));
+        CUDA_OK(cudaStreamSynchronize(st));
+    });
+}
+
+
+int fwa_b200_pillarize_device(fwa_b200_ctx* c, const double* d_xy, const double* d_feats, int64_t n, int32_t f_in,
+                              double resolution, const double* d_weight, const double* d_bias, int32_t d_out,
+                              double* d_coords_out, double* d_feats_out, int64_t capacity, int64_t* n_pillars) {
+    return guarded(c, [&] {
+        if (!n_pillars) throw FwaError{FWA_ERR_SHAPE, "null n_pillars"};
+        *n_pillars = pillarize_device(c, d_xy, d_feats, n, f_in, resolution, d_weight, d_bias, d_out, d_coords_out,
+                                      d_feats_out, capacity);
+    });
+}
+
+int fwa_b200_pillarize(fwa_b200_ctx* c, const double* xy, const double* feats, int64_t n, int32_t f_in,
+                       double resolution, const double* weight, const double* bias, int32_t d_out,
+                       double* coords_out, double* feats_out, int64_t* n_pillars) {
+    return guarded(c, [&] {
+        if (!n_pillars || (n > 0 && !xy) || (n > 0 && f_in > 0 && (!feats || !weight)))
+            throw FwaError{FWA_ERR_SHAPE, "null buffer"};
+        cudaStream_t st = c->stream;
+        const size_t un = static_cast<size_t>(n > 0 ? n : 1), fi = static_cast<size_t>(f_in > 0 ? f_in : 1);
+        double* dxy = ws<double>(c, "pzh_xy", 2 * un);
+        double* df = ws<double>(c, "pzh_f", un * fi);
+        double* dw = ws<double>(c, "pzh_w", static_cast<size_t>(d_out > 0 ? d_out : 1) * fi);
+        double* db = bias ? ws<double>(c, "pzh_b", static_cast<size_t>(d_out > 0 ? d_out : 1)) : nullptr;
+        if (n > 0) {
+            CUDA_OK(cudaMemcpyAsync(dxy, xy, static_cast<size_t>(n) * 16, cudaMemcpyHostToDevice, st));
+            if (f_in > 0) {
+                CUDA_OK(cudaMemcpyAsync(df, feats, static_cast<size_t>(n) * fi * 8, cudaMemcpyHostToDevice, st));
+                CUDA_OK(cudaMemcpyAsync(dw, weight, static_cast<size_t>(d_out) * fi * 8, cudaMemcpyHostToDevice, st));
+            }
+            if (bias) CUDA_OK(cudaMemcpyAsync(db, bias, static_cast<size_t>(d_out) * 8, cudaMemcpyHostToDevice, st));
+        }
+        double* dco = coords_out ? ws<double>(c, "pzh_co", 2 * un) : nullptr;
+        double* dfo = coords_out ? ws<double>(c, "pzh_fo", un * static_cast<size_t>(d_out > 0 ? d_out : 1)) : nullptr;
+        const int64_t np = pillarize_device(c, dxy, df, n, f_in, resolution, dw, db, d_out, dco, dfo, n);
+        *n_pillars = np;
+        if (coords_out && np > 0) {
+            CUDA_OK(cudaMemcpyAsync(coords_out, dco, static_cast<size_t>(np) * 16, cudaMemcpyDeviceToHost, st));
+            CUDA_OK(cudaMemcpyAsync(feats_out, dfo, static_cast<size_t>(np) * d_out * 8, cudaMemcpyDeviceToHost, st));
+        }
         CUDA_OK(cudaStreamSynchronize(st));
     });
 }

@@ -113,6 +113,35 @@ static Cloud generate_synthetic(const fwa_scene_spec_t& s, uint64_t seed) {
 
 using namespace fwa_b200;
 
+extern "C" int64_t fwa_b200_generate_points(const fwa_scene_spec_t* spec, uint64_t seed, double* xy,
+                                            double* feats) {
+    if (!spec) return -FWA_ERR_CONFIG;
+    const auto& s = *spec;
+    if (s.extent_x <= 0.0 || s.extent_y <= 0.0 || s.n_clusters < 0 || s.n_background < 0 ||
+        s.points_per_cluster_min < 1 || s.points_per_cluster_max < s.points_per_cluster_min ||
+        s.cluster_sigma < 0.0 || s.f_in < 0)
+        return -FWA_ERR_CONFIG;
+    const Cloud pc = generate_synthetic(s, seed);
+    const size_t n = pc.x.size();
+    if (xy) {
+        for (size_t i = 0; i < n; ++i) {
+            xy[2 * i] = pc.x[i];
+            xy[2 * i + 1] = pc.y[i];
+        }
+        if (feats) std::copy(pc.f.begin(), pc.f.end(), feats);
+    }
+    return static_cast<int64_t>(n);
+}
+
+extern "C" int64_t fwa_b200_pillar_params(int32_t f_in, int32_t d_out, uint64_t seed, double* weight) {
+    if (f_in < 0 || d_out < 1) return -FWA_ERR_CONFIG;
+    // random_pillar_params (geometry.hpp:71-79): weight d_out x f_in ~ N(0, 0.5^2), bias 0
+    DetRng prng(seed);
+    const size_t k = static_cast<size_t>(d_out) * static_cast<size_t>(f_in);
+    for (size_t i = 0; i < k; ++i) weight[i] = prng.normal(0.0, 0.5);
+    return static_cast<int64_t>(k);
+}
+
 extern "C" int64_t fwa_b200_generate_pillars(const fwa_scene_spec_t* spec, uint64_t seed,
                                              double resolution, int32_t d_out,
                                              uint64_t param_seed, double* coords, double* feats) {

@@ -167,6 +167,22 @@ void launch_block_fused(const float* x, const double* x64, const __half* pe16, c
 void build_pair_images(const float* w_qkv, const float* w_out, const float* w1f, const float* w2,
                        uint16_t* out /* 2 * 65536 bf16 */);
 
+// ------------------------------------------------------------------ pillarization (pillarize.cu)
+void launch_cell_keys(const double* xy, int64_t n, double res, long long* cell, long long* mm, cudaStream_t s,
+                      int64_t* launches);
+void launch_cell_hist(const long long* cell, int64_t n, long long min_x, long long min_y, long long range_y,
+                      uint32_t* cell_id, uint32_t* hist, cudaStream_t s, int64_t* launches);
+void launch_nonempty(const uint32_t* hist, int64_t ncell, uint32_t* flag, cudaStream_t s, int64_t* launches);
+void launch_pillar_cells(const uint32_t* hist, const uint32_t* prow, int64_t ncell, long long min_x, long long min_y,
+                         long long range_y, double res, uint32_t* pcell, double* coords, cudaStream_t s,
+                         int64_t* launches);
+void launch_cell_members(const uint32_t* cell_id, int64_t n, uint32_t* cursor, int32_t* slot_pt,
+                         const uint32_t* start, const uint32_t* hist, const double* feats, int f_in, double* fs,
+                         cudaStream_t s, int64_t* launches);
+void launch_pillar_features(const uint32_t* pcell, const uint32_t* start, const uint32_t* hist, int64_t np,
+                            int f_in, const double* fs, double* pooled, const double* w, const double* bias,
+                            int d_out, double* out, cudaStream_t s, int64_t* launches);
+
 // ------------------------------------------------------------------ misc
 void launch_scatter_rows(const float* src, const int32_t* ids, const uint32_t* rank, int64_t n,
                          int d, float* dst, cudaStream_t s, int64_t* launches);

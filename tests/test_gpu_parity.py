@@ -439,3 +439,52 @@ def test_fused_block_kernel_nonfinite_input_raises(ctx16):
     f[17, 5] = np.inf
     with pytest.raises(F.NumericError):
         ctx16.run_backbone(F.PillarSet(c, f), cfg)
+
+
+# ----------------------------------------------------------------------------- pillarization (§8f next-1)
+
+@pytest.mark.parametrize("name", ["F10", "PINNED", "F60"])
+def test_gpu_pillarize_matches_reference_pillars(ctx16, name):
+    """geometry::pillarize on the GPU vs the reference's generate_synthetic + pillarize
+    (host port pinned bit-exact to it): cell order and coordinates bit-exact; features
+    equal up to CUDA's erf vs libm's (<= a few ulp)."""
+    scene = F.SCENES[name]
+    xy, f = F.generate_points(scene, 42)
+    w = F.pillar_params(scene.f_in, 128, 42)
+    got = ctx16.pillarize(xy, f, 0.32, w)
+    want = F.make_pillars(scene, 42)
+    assert np.array_equal(got.coords, want.coords)
+    np.testing.assert_allclose(got.features, want.features, rtol=1e-14, atol=1e-15)  # CUDA vs libm erf
+
+
+def test_gpu_pillarize_edge_cases_vs_oracle(ctx16):
+    """Cell-boundary coordinates, negative cells, crowded cells (pairwise recursion past
+    8 and 32 members), non-zero bias, f_in = 3, and an empty cloud."""
+    rng = np.random.default_rng(5)
+    res = 0.32
+    grid = np.stack(np.meshgrid(np.arange(-6, 7) * res, np.arange(-5, 6) * res), -1).reshape(-1, 2)
+    crowd = np.full((70, 2), [1.01, -2.17]) + rng.uniform(0, 0.05, size=(70, 2))
+    rand = rng.uniform(-4, 4, size=(400, 2))
+    xy = np.concatenate([grid, crowd, rand, grid[::7]])
+    f = rng.normal(size=(xy.shape[0], 3))
+    w = rng.normal(size=(24, 3))
+    b = rng.normal(size=24)
+    got = ctx16.pillarize(xy, f, res, w, b)
+    wc, wf = O.np_pillarize(xy, f, res, w, b)
+    assert np.array_equal(got.coords, wc)
+    np.testing.assert_allclose(got.features, wf, rtol=1e-14, atol=1e-15)
+    empty = ctx16.pillarize(np.zeros((0, 2)), np.zeros((0, 3)), res, w, b)
+    assert empty.size() == 0
+
+
+def test_gpu_pillarize_feeds_backbone(ctx16):
+    """points -> GPU pillarize -> backbone == host pillars -> backbone (ints exact)."""
+    scene = F.SCENES["F10"]
+    xy, f = F.generate_points(scene, 42)
+    ps = ctx16.pillarize(xy, f, 0.32, F.pillar_params(scene.f_in, 128, 42))
+    cfg = F.FwaConfig(n_blocks=2)
+    ctx16.load_params(cfg, F.init_backbone_params(cfg, 42))
+    a = ctx16.run_backbone(ps, cfg)
+    b = ctx16.run_backbone(F.make_pillars(scene, 42), cfg)
+    assert np.array_equal(a.kept_indices, b.kept_indices)
+    assert O.max_rel_err(a.features, b.features) <= 1e-3

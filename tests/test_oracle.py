@@ -173,3 +173,20 @@ def test_port_equals_reference_live():
             assert np.array_equal(O.ref_sort(c, 2.88, 2.88, sh, ay), O.port_sort(c, 2.88, 2.88, sh, ay))
             assert np.array_equal(O.ref_sort(c, 2.88, 2.88, sh, ay, brute=True),
                                   O.np_sort(c, 2.88, 2.88, sh, ay))
+
+
+def test_np_pillarize_matches_reference_pillars():
+    """The pillarize restatement (oracle.np_pillarize) reproduces the compiled reference's
+    generate_synthetic + pillarize bit for bit on a small scene (coords, order, features)."""
+    import paper_2301_08739_b200 as F
+    scene = F.SceneSpec(6, 20, 40, 1.0, 20.0, 20.0, 150, 2)
+    xy, f = F.generate_points(scene, 9)
+    w = F.pillar_params(2, 16, 9)
+    coords, feats = O.np_pillarize(xy, f, 0.32, w)
+    want = F.make_pillars(scene, 9, d_out=16)          # host port, pinned to the reference
+    assert np.array_equal(coords, want.coords)
+    assert np.array_equal(feats, want.features)
+    if O.have_ref():
+        r = O.ref_make_pillars({"n_clusters": 6, "ppc_min": 20, "ppc_max": 40, "sigma": 1.0, "ext_x": 20.0,
+                                "ext_y": 20.0, "n_bg": 150, "f_in": 2}, 9, d_out=16)
+        assert np.array_equal(coords, r[0]) and np.array_equal(feats, r[1])
