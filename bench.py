@@ -272,6 +272,9 @@ def run_ours(args, rank, world, local_rank, dist):
     batch = None
     if not args.no_batch:
         batch = run_batch_frames(args, F, ctx, cfg, dev, stream, rank, world, dist, flush)
+    points = None
+    if world == 1 and not args.no_points:
+        points = run_points_pipeline(args, F, ctx, cfg, dev, stream, flush)
     split = None
     if not args.no_split:
         split = run_split_scene(args, F, ctx, cfg, dev, stream, rank, world, dist, flush)
@@ -364,6 +367,7 @@ def run_ours(args, rank, world, local_rank, dist):
         "frame_tflops": tot_flop / (ms_per_step / 1e3) / 1e12,
         "frame_frac_of_sustained": tot_flop / (ms_per_step / 1e3) / 1e12 / pk_sus,
         "cache": {"computed": cache[0], "hits": cache[1]},
+        "pillarize": points,
         "config3_batch": batch,
         "config4_split": split,
     }
@@ -428,6 +432,79 @@ def run_batch_frames(args, F, ctx, cfg, dev, stream, rank, world, dist, flush):
             "l2": "flushed by a 256 MiB write before every timed step"}
 
 
+def run_points_pipeline(args, F, ctx, cfg, dev, stream, flush):
+    """the stage before the boundary on the GPU.  (a) pillarize alone:
+    the F60 point cloud (86,934 points, device-resident) -> 60,897 pillars; (b) raw points
+    in, features out: points H2D (pinned) + GPU pillarize + the 8-block backbone + features
+    D2H, i.e. the reference's generate -> pillarize -> run_backbone chain minus the
+    generator, with 2.8 MB instead of 63 MB crossing PCIe."""
+    import torch
+    scene = F.SCENES["F60"]
+    xy, f = F.generate_points(scene, 42)
+    w = F.pillar_params(scene.f_in, cfg.d_model, 42)
+    n = xy.shape[0]
+    d_xy = torch.from_numpy(xy).to(dev)
+    d_f = torch.from_numpy(f).to(dev)
+    d_w = torch.from_numpy(w).to(dev)
+    d_pc = torch.empty((n, 2), dtype=torch.float64, device=dev)
+    d_pf = torch.empty((n, cfg.d_model), dtype=torch.float64, device=dev)
+
+    def pz():
+        return ctx.pillarize_device(d_xy.data_ptr(), d_f.data_ptr(), n, scene.f_in, 0.32, d_w.data_ptr(), 0,
+                                    cfg.d_model, d_pc.data_ptr(), d_pf.data_ptr(), n)
+
+    for _ in range(3):
+        pz()
+    steps = max(5, args.steps // 5)
+    ms = 0.0
+    for _ in range(steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        npil = pz()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms += a.elapsed_time(b)
+    ms /= steps
+    # (b) points -> features through the host boundary
+    h_xy = torch.from_numpy(xy).pin_memory()
+    h_f = torch.from_numpy(f).pin_memory()
+    h_out = torch.empty((n, cfg.d_model), dtype=torch.float32).pin_memory()
+    d_feats32 = torch.empty((n, cfg.d_model), dtype=torch.float32, device=dev)
+    d_out = torch.empty((n, cfg.d_model), dtype=torch.float32, device=dev)
+    d_kept = torch.empty(n, dtype=torch.int32, device=dev)
+
+    def e2e():
+        d_xy.copy_(h_xy, non_blocking=True)
+        d_f.copy_(h_f, non_blocking=True)
+        p = pz()
+        d_feats32[:p].copy_(d_pf[:p])  # PillarSet f64 -> f32 (backbone.hpp:195-196)
+        k = ctx.forward_device(d_pc.data_ptr(), d_feats32.data_ptr(), [0, p], cfg, d_out.data_ptr(),
+                               d_kept.data_ptr())
+        h_out[:k].copy_(d_out[:k], non_blocking=True)
+        torch.cuda.synchronize()
+        return p, k
+
+    for _ in range(2):
+        e2e()
+    t_e2e = 0.0
+    for _ in range(steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        p, k = e2e()
+        t_e2e += time.perf_counter() - t0
+    t_e2e /= steps
+    return {"workload": "F60 point cloud (86,934 points, f_in 2) -> 60,897 pillars at 0.32 m (geometry.hpp:246-300)",
+            "points": n, "pillars": int(npil), "pillarize_ms": ms, "points_per_s": n / (ms / 1e3),
+            "points_to_features_e2e_ms": 1e3 * t_e2e,
+            "points_to_features_e2e_pillars_per_s": p / t_e2e,
+            "h2d_bytes_per_step": int(n * (2 + scene.f_in) * 8), "d2h_bytes_per_step": int(k * cfg.d_model * 4),
+            "note": "pillarize has two host round trips (cell range, pillar count); timed with events "
+                    "around the call, L2 flushed"}
+
+
 def run_split_scene(args, F, ctx, cfg, dev, stream, rank, world, dist, flush):
     """BASELINE config 4: the F250 scene (255,066 pillars) split by group ranges across
     the ranks with an all-gather of each block's sorted-order rows (NCCL over NVLink);
@@ -487,6 +564,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-split", action="store_true", help="skip the config-4 split-scene measurement")
     ap.add_argument("--no-batch", action="store_true", help="skip the config-3 64-frame batch measurement")
+    ap.add_argument("--no-points", action="store_true", help="skip the GPU pillarization measurement")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

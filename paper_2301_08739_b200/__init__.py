@@ -469,6 +469,15 @@ class Context:
         p = np_.value
         return PillarSet(coords[:p].copy(), out[:p].copy(), resolution)
 
+    def pillarize_device(self, d_xy: int, d_feats: int, n: int, f_in: int, resolution: float, d_weight: int,
+                         d_bias: int, d_out: int, d_coords: int, d_out_feats: int, capacity: int) -> int:
+        """Device-pointer pillarize (the pillars stay in HBM for forward_device); returns P."""
+        np_ = C.c_int64(0)
+        self._check(lib().fwa_b200_pillarize_device(self._h, d_xy, d_feats, n, f_in, resolution, d_weight,
+                                                     d_bias or None, d_out, d_coords, d_out_feats, capacity,
+                                                     C.byref(np_)))
+        return np_.value
+
     def fwa_block_forward(self, f: np.ndarray, pe: np.ndarray, record: bytes, n_groups: int) -> np.ndarray:
         f = np.ascontiguousarray(f, np.float32)
         pe = np.ascontiguousarray(pe, np.float32)
