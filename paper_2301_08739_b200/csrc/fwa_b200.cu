@@ -66,6 +66,8 @@ struct fwa_b200_ctx {
     DevBuf freq;
     cudaStream_t side = nullptr;             // PE overlaps the schedule's host round trip
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaStream_t copy = nullptr;             // host API: feature H2D overlaps the schedule
+    cudaEvent_t ev_copy = nullptr, ev_feats = nullptr;
     int* d_flag = nullptr;     // [0] non-finite input, [1] window-bin capacity overflow
     int* h_flag = nullptr;     // pinned, 2 ints
     bool exact_bins = false;   // set for one call after an overflow: host-sized bins
@@ -790,7 +792,8 @@ void require_params(fwa_b200_ctx* c, const fwa_config_t* cfg) {
 // (K x d, active order) and, optionally, d_kept.
 void forward_device(fwa_b200_ctx* c, const double* d_coords, const float* d_feats,
                     const double* d_feats64, const fwa_config_t* cfg, Schedule& S, float* d_out,
-                    int32_t* d_kept, const int64_t* d_tab_fixed = nullptr) {
+                    int32_t* d_kept, const int64_t* d_tab_fixed = nullptr,
+                    cudaEvent_t feats_ready = nullptr) {
     cudaStream_t st = c->stream;
     const int d = cfg->d_model;
     CUDA_OK(cudaMemsetAsync(c->d_flag, 0, 2 * sizeof(int), st));
@@ -810,6 +813,7 @@ void forward_device(fwa_b200_ctx* c, const double* d_coords, const float* d_feat
         build_schedule(c, d_coords, cfg, S, d_tab_fixed);
     }
     CUDA_OK(cudaStreamWaitEvent(st, c->ev_join, 0));
+    if (feats_ready) CUDA_OK(cudaStreamWaitEvent(st, feats_ready, 0));  // block 0 reads them
     float* X = ws<float>(c, "X", static_cast<size_t>(S.ntot) * d);
     for (int b = 0; b < cfg->n_blocks; ++b) {
         const int s = b % 4;
@@ -862,18 +866,23 @@ void forward_host(fwa_b200_ctx* c, const double* coords, const void* feats, int 
     const double* d_f64 = nullptr;
     StageEv* h2d = new StageEv(c, FWA_PROF_H2D);
     CUDA_OK(cudaMemcpyAsync(d_coords, coords, static_cast<size_t>(S.ntot) * 16, cudaMemcpyHostToDevice, st));
+    delete h2d;
+    // the features (the bulk of the input) cross PCIe on a copy stream while the schedule
+    // and the PE run (they need only the coordinates); block 0 waits for them
+    CUDA_OK(cudaEventRecord(c->ev_copy, st));  // previous users of the buffer are done
+    CUDA_OK(cudaStreamWaitEvent(c->copy, c->ev_copy, 0));
     if (f64) {
         double* p = ws<double>(c, "in_feats64", static_cast<size_t>(S.ntot) * d);
-        CUDA_OK(cudaMemcpyAsync(p, feats, static_cast<size_t>(S.ntot) * d * 8, cudaMemcpyHostToDevice, st));
+        CUDA_OK(cudaMemcpyAsync(p, feats, static_cast<size_t>(S.ntot) * d * 8, cudaMemcpyHostToDevice, c->copy));
         d_f64 = p;
     } else {
         float* p = ws<float>(c, "in_feats32", static_cast<size_t>(S.ntot) * d);
-        CUDA_OK(cudaMemcpyAsync(p, feats, static_cast<size_t>(S.ntot) * d * 4, cudaMemcpyHostToDevice, st));
+        CUDA_OK(cudaMemcpyAsync(p, feats, static_cast<size_t>(S.ntot) * d * 4, cudaMemcpyHostToDevice, c->copy));
         d_f32 = p;
     }
-    delete h2d;
+    CUDA_OK(cudaEventRecord(c->ev_feats, c->copy));
     float* d_out = ws<float>(c, "out_feats", static_cast<size_t>(S.ntot) * d);
-    forward_device(c, d_coords, d_f32, d_f64, cfg, S, d_out, nullptr);
+    forward_device(c, d_coords, d_f32, d_f64, cfg, S, d_out, nullptr, nullptr, c->ev_feats);
     StageEv* d2h = new StageEv(c, FWA_PROF_D2H);
     CUDA_OK(cudaMemcpyAsync(out->features, d_out, static_cast<size_t>(S.K) * d * 4, cudaMemcpyDeviceToHost, st));
     if (out->kept_indices)
@@ -955,6 +964,9 @@ int fwa_b200_ctx_create(int device, void* stream, fwa_b200_ctx** out) {
         CUDA_OK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
         CUDA_OK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
         CUDA_OK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+        CUDA_OK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+        CUDA_OK(cudaEventCreateWithFlags(&c->ev_copy, cudaEventDisableTiming));
+        CUDA_OK(cudaEventCreateWithFlags(&c->ev_feats, cudaEventDisableTiming));
         CUDA_OK(cudaEventCreateWithFlags(&c->ev_tab[0], cudaEventDisableTiming));
         CUDA_OK(cudaEventCreateWithFlags(&c->ev_tab[1], cudaEventDisableTiming));
         CUDA_OK(cudaMalloc(&c->d_flag, 2 * sizeof(int)));
@@ -995,6 +1007,12 @@ void fwa_b200_ctx_destroy(fwa_b200_ctx* c) {
         if (e) cudaEventDestroy(e);
     if (c->h_tab) cudaFreeHost(c->h_tab);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
+    if (c->copy) {
+        cudaStreamSynchronize(c->copy);
+        cudaStreamDestroy(c->copy);
+    }
+    if (c->ev_copy) cudaEventDestroy(c->ev_copy);
+    if (c->ev_feats) cudaEventDestroy(c->ev_feats);
     if (c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
 }
