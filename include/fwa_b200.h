@@ -16,6 +16,7 @@
  *   fwa_b200_load_params             fwa::kernels::load_params (FWAP records)  include/fwa/kernels.hpp:177-206
  *                                    + fwa::kernels::validate  kernels.hpp:75-90
  *   fwa_b200_pillarize[_device]      fwa::geometry::pillarize on the GPU  include/fwa/geometry.hpp:246-300
+ *   fwa_b200_row_checksums           `fwa attend` row_checksums  tools/fwa_cli.cpp:214-218
  *   fwa_b200_generate_points         fwa::geometry::generate_synthetic  include/fwa/geometry.hpp:355-386
  *   fwa_b200_pillar_params           fwa::geometry::random_pillar_params  include/fwa/geometry.hpp:71-79
  *   fwa_b200_generate_pillars        fwa::geometry::generate_synthetic + pillarize +
@@ -210,6 +211,13 @@ int fwa_b200_pillarize_device(fwa_b200_ctx* ctx, const double* d_xy, const doubl
                               int32_t f_in, double resolution, const double* d_weight, const double* d_bias,
                               int32_t d_out, double* d_coords_out, double* d_feats_out, int64_t capacity,
                               int64_t* n_pillars);
+
+/* FNV-1a-64 of a byte string (bench.hpp:62-72): the `fwa attend` feature_hash over the
+ * f32 feature bytes and the config_digest over the config JSON (host). */
+uint64_t fwa_b200_fnv1a64(const void* bytes, size_t n);
+/* `fwa attend` row checksums (tools/fwa_cli.cpp:214-218) of device features (n x d f32)
+ * into device doubles: sum = 0.0; sum += (double)f[c] in column order -- bit-exact. */
+int fwa_b200_row_checksums(fwa_b200_ctx* ctx, const float* d_features, int64_t n, int32_t d, double* d_out);
 
 /* ---- host-side input generators (bit-identical to the reference's) ---- */
 

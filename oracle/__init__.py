@@ -85,6 +85,11 @@ def ref():
         lib.ref_generate_points.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                             C.c_double, C.c_int, C.c_int, C.c_uint64, C.c_void_p,
                                             C.c_int64]
+        lib.ref_config_json.restype = C.c_int64
+        lib.ref_config_json.argtypes = [C.POINTER(CfgC), C.c_char_p, C.c_int64]
+        lib.ref_fnv1a64_hex.argtypes = [C.c_void_p, C.c_int64, C.c_char_p]
+        lib.ref_write_points.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
+                                         C.c_int, C.c_int, C.c_uint64, C.c_char_p, C.c_int]
         lib.ref_init_params_fwap.restype = C.c_int64
         lib.ref_init_params_fwap.argtypes = [C.POINTER(CfgC), C.c_int64, C.c_uint64, C.c_void_p,
                                              C.c_int64]
@@ -376,3 +381,25 @@ def np_pillarize(xy, feats, resolution, weight, bias=None):
         out.append(row)
         coords.append(((key[0] + 0.5) * resolution, (key[1] + 0.5) * resolution))
     return (np.array(coords, np.float64).reshape(-1, 2), np.array(out, np.float64).reshape(-1, d_out))
+
+
+def ref_config_json(cfg):
+    """nlohmann::json(FwaConfig).dump() of the reference (backbone.hpp:49-57)."""
+    buf = C.create_string_buffer(4096)
+    n = ref().ref_config_json(C.byref(cfg), buf, 4096)
+    _check_ref(0 if n >= 0 else -n)
+    return buf.value.decode()
+
+
+def ref_fnv1a64_hex(b: bytes) -> str:
+    """bench.hpp:62-72."""
+    out = C.create_string_buffer(32)
+    ref().ref_fnv1a64_hex(b, len(b), out)
+    return out.value.decode()
+
+
+def ref_write_points(scene, seed, path, binary):
+    """generate_synthetic + write_binary / write_csv (geometry.hpp:202-237)."""
+    _check_ref(ref().ref_write_points(scene["n_clusters"], scene["ppc_min"], scene["ppc_max"], scene["sigma"],
+                                      scene["ext_x"], scene["ext_y"], scene["n_bg"], scene["f_in"], seed,
+                                      path.encode(), int(binary)))

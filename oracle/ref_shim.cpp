@@ -20,11 +20,13 @@
 
 #include <cstdint>
 #include <cstring>
+#include <fstream>
 #include <sstream>
 #include <string>
 #include <vector>
 
 #include "fwa/backbone.hpp"
+#include "fwa/bench.hpp"
 #include "fwa/flatten.hpp"
 #include "fwa/geometry.hpp"
 #include "fwa/kernels.hpp"
@@ -161,6 +163,35 @@ int64_t ref_generate_points(int n_clusters, int ppc_min, int ppc_max, double sig
         }
     });
     return rc ? -rc : n;
+}
+
+// `fwa attend` output-contract pieces (tools/fwa_cli.cpp:71-73, 204-241; bench.hpp:62-72):
+// the config JSON (nlohmann dump) and its FNV-1a digest, FNV-1a of arbitrary bytes, and
+// the point-file writers (geometry.hpp:202-237) for the ingest parity tests.
+int64_t ref_config_json(const CfgC* c, char* out, int64_t cap) {
+    int64_t n = -1;
+    int rc = guarded([&] {
+        const std::string s = nlohmann::json(to_cfg(c)).dump();
+        n = static_cast<int64_t>(s.size());
+        if (out && n < cap) std::memcpy(out, s.c_str(), s.size() + 1);
+    });
+    return rc ? -rc : n;
+}
+
+void ref_fnv1a64_hex(const void* bytes, int64_t n, char* out19) {
+    const std::string h = bench::fnv1a64_hex(std::string(static_cast<const char*>(bytes), static_cast<size_t>(n)));
+    std::memcpy(out19, h.c_str(), h.size() + 1);
+}
+
+int ref_write_points(int n_clusters, int ppc_min, int ppc_max, double sigma, double ext_x, double ext_y,
+                     int n_background, int f_in, uint64_t seed, const char* path, int binary) {
+    return guarded([&] {
+        geometry::SceneSpec s{n_clusters, ppc_min, ppc_max, sigma, ext_x, ext_y, n_background, f_in};
+        const auto cloud = geometry::generate_synthetic(s, seed);
+        std::ofstream f(path, binary ? std::ios::binary : std::ios::out);
+        if (binary) geometry::write_binary(f, cloud);
+        else geometry::write_csv(f, cloud);
+    });
 }
 
 // init_backbone_params(cfg, f_in, seed) serialised as back-to-back FWAP records.

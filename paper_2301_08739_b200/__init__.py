@@ -38,6 +38,7 @@ EXPORTS = [
     "fwa_b200_positional_embedding", "fwa_b200_positional_embedding_f16", "fwa_b200_generate_pillars", "fwa_b200_init_params",
     "fwa_b200_split_begin", "fwa_b200_split_block", "fwa_b200_split_scatter",
     "fwa_b200_pillarize", "fwa_b200_pillarize_device", "fwa_b200_generate_points", "fwa_b200_pillar_params",
+    "fwa_b200_row_checksums", "fwa_b200_fnv1a64",
 ]
 
 PREC_BF16, PREC_FP32, PREC_BF16_3K = 0, 1, 2
@@ -151,6 +152,9 @@ def lib():
         L.fwa_b200_generate_points.restype = i64
         L.fwa_b200_pillar_params.argtypes = [i32, i32, C.c_uint64, vp]
         L.fwa_b200_pillar_params.restype = i64
+        L.fwa_b200_row_checksums.argtypes = [vp, vp, i64, i32, vp]
+        L.fwa_b200_fnv1a64.argtypes = [C.c_char_p, C.c_size_t]
+        L.fwa_b200_fnv1a64.restype = C.c_uint64
         _lib_handle = L
     return _lib_handle
 
@@ -617,9 +621,5 @@ def pillar_params(f_in: int, d_out: int, seed: int) -> np.ndarray:
 
 
 def fnv1a64_hex(b: bytes) -> str:
-    """bench.hpp:62-72 (feature_hash of the CLI `attend` output)."""
-    h = 0xcbf29ce484222325
-    for c in b:
-        h ^= c
-        h = (h * 0x100000001b3) & 0xFFFFFFFFFFFFFFFF
-    return f"0x{h:016x}"
+    """bench.hpp:62-72 (feature_hash / config_digest of the CLI `attend` output)."""
+    return f"0x{lib().fwa_b200_fnv1a64(b, len(b)):016x}"

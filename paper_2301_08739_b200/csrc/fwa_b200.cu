@@ -1465,4 +1465,12 @@ int fwa_b200_pillarize(fwa_b200_ctx* c, const double* xy, const double* feats, i
     });
 }
 
+int fwa_b200_row_checksums(fwa_b200_ctx* c, const float* d_features, int64_t n, int32_t d, double* d_out) {
+    return guarded(c, [&] {
+        if (n < 0 || d < 1) throw FwaError{FWA_ERR_SHAPE, "row_checksums: bad shape"};
+        launch_row_checksums(d_features, n, d, d_out, c->stream, &c->launches);
+        check_launch("k_row_checksums");
+    });
+}
+
 } // extern "C"

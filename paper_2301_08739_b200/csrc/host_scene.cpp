@@ -113,6 +113,17 @@ static Cloud generate_synthetic(const fwa_scene_spec_t& s, uint64_t seed) {
 
 using namespace fwa_b200;
 
+// FNV-1a-64 (bench.hpp:62-72): the `fwa attend` feature_hash over the f32 feature bytes
+extern "C" uint64_t fwa_b200_fnv1a64(const void* bytes, size_t n) {
+    const unsigned char* p = static_cast<const unsigned char*>(bytes);
+    uint64_t h = 0xcbf29ce484222325ull;
+    for (size_t i = 0; i < n; ++i) {
+        h ^= p[i];
+        h *= 0x100000001b3ull;
+    }
+    return h;
+}
+
 extern "C" int64_t fwa_b200_generate_points(const fwa_scene_spec_t* spec, uint64_t seed, double* xy,
                                             double* feats) {
     if (!spec) return -FWA_ERR_CONFIG;

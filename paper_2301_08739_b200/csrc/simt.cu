@@ -70,6 +70,23 @@ __global__ void k_pe_fp16(const double* __restrict__ coords, int64_t n, int nf, 
     }
 }
 
+// `fwa attend` row checksums (tools/fwa_cli.cpp:214-218): sum = 0.0; sum += (double)f[c]
+// for c = 0..d-1, in that order -- one thread per row, bit-exact
+__global__ void k_row_checksums(const float* __restrict__ f, int64_t n, int d, double* __restrict__ out) {
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const float* row = f + r * d;
+    double s = 0.0;
+    for (int c = 0; c < d; ++c) s = __dadd_rn(s, static_cast<double>(row[c]));
+    out[r] = s;
+}
+
+void launch_row_checksums(const float* f, int64_t n, int d, double* out, cudaStream_t s, int64_t* launches) {
+    if (n <= 0) return;
+    k_row_checksums<<<static_cast<unsigned>((n + 127) / 128), 128, 0, s>>>(f, n, d, out);
+    ++*launches;
+}
+
 void launch_positional_embedding(const double* coords, int64_t n, int d, const double* d_freq,
                                  float* pe, __half* pe16, cudaStream_t s, int64_t* launches) {
     if (!pe && pe16 && (d / 4) % 4 == 0) {  // d_freq holds [nf doubles | nf float2 (2f hi, lo)]

@@ -488,3 +488,41 @@ def test_gpu_pillarize_feeds_backbone(ctx16):
     b = ctx16.run_backbone(F.make_pillars(scene, 42), cfg)
     assert np.array_equal(a.kept_indices, b.kept_indices)
     assert O.max_rel_err(a.features, b.features) <= 1e-3
+
+
+# ----------------------------------------------------------------------------- `fwa attend` (§8f next-2)
+
+def test_attend_json_matches_reference(tmp_path, ctx16):
+    """`fwa attend` on the B200 path (points -> GPU pillarize -> GPU backbone -> GPU row
+    checksums) vs the reference library on the same FWPC file: every integer / structural
+    field exact, row checksums within the bf16 feature tolerance, and the checksums bit-exact
+    sums of the FWFB-dumped features (fwa_cli.cpp:214-218)."""
+    from paper_2301_08739_b200.attend import attend, config_digest
+    if not O.have_ref():
+        pytest.skip("reference oracle not built")
+    scene = {"n_clusters": 12, "ppc_min": 150, "ppc_max": 300, "sigma": 1.5, "ext_x": 60.0, "ext_y": 60.0,
+             "n_bg": 2000, "f_in": 2}
+    path = str(tmp_path / "pts.fwpc")
+    O.ref_write_points(scene, 11, path, True)
+    cfg = F.FwaConfig(n_blocks=4)
+    fwfb = str(tmp_path / "feat.fwfb")
+    j = attend(ctx16, path, cfg, None, 11, fwfb)
+    # the reference: generate -> pillarize -> init_backbone_params(seed) -> run_backbone
+    rc = O.make_cfg(n_blocks=4)
+    coords, feats64 = O.ref_make_pillars(scene, 11, d_out=128, param_seed=11)
+    blob = O.ref_init_params(rc, 128, 11)
+    w = O.ref_run_backbone(coords, feats64, rc, blob)
+    assert j["n_input"] == coords.shape[0] and j["n_kept"] == len(w["kept"])
+    assert (j["cache"]["computed"], j["cache"]["hits"]) == tuple(w["cache"])
+    assert j["dropped_per_block"] == list(w["dropped_per_block"])
+    assert j["config_digest"] == config_digest(cfg)
+    assert np.array_equal(np.array(j["coords"]), coords[w["kept"]])
+    want_sums = np.cumsum(w["features"].astype(np.float64), axis=1)[:, -1]
+    got_sums = np.array(j["row_checksums"])
+    assert np.max(np.abs(got_sums - want_sums)) <= TOL_BF16 * np.max(np.abs(want_sums))
+    raw = open(fwfb, "rb").read()
+    assert raw[:4] == b"FWFB"
+    n, d = np.frombuffer(raw[4:12], np.uint32)
+    f = np.frombuffer(raw[12:], np.float32).reshape(n, d)
+    assert np.array_equal(np.cumsum(f.astype(np.float64), axis=1)[:, -1], got_sums)
+    assert j["feature_hash"] == F.fnv1a64_hex(f.tobytes())

@@ -7,6 +7,7 @@ import re
 import numpy as np
 import pytest
 
+import oracle as O
 import paper_2301_08739_b200 as F
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -84,3 +85,51 @@ def test_generator_equals_reference_live():
     cfg = O.make_cfg(n_blocks=3, d_model=64, n_heads=4, d_ff=96)
     assert F.init_backbone_params(F.FwaConfig(n_blocks=3, d_model=64, n_heads=4, d_ff=96), 9) == \
         O.ref_init_params(cfg, 64, 9)
+
+
+# ----------------------------------------------------------------------------- `fwa attend` output contract
+
+def test_attend_config_digest_and_fnv_match_reference():
+    """config_digest = FNV-1a-64 of nlohmann::json(FwaConfig).dump() (fwa_cli.cpp:71-73,
+    backbone.hpp:49-57); fnv1a64_hex = bench.hpp:62-72."""
+    from paper_2301_08739_b200.attend import config_digest, config_json
+    if not O.have_ref():
+        pytest.skip("reference oracle not built")
+    for kw in ({}, {"resolution": 0.25, "group_size": 32, "n_blocks": 2}, {"d_model": 64, "n_heads": 4, "d_ff": 96},
+               {"resolution": 0.1, "window": (7, 11)}):
+        win = kw.pop("window", (9, 9))
+        cfg = F.FwaConfig(window_px=win[0], window_py=win[1], **kw)
+        rc = O.make_cfg(window=win, **kw)
+        assert config_json(cfg) == O.ref_config_json(rc)
+        assert config_digest(cfg) == O.ref_fnv1a64_hex(O.ref_config_json(rc).encode())
+    b = np.random.default_rng(1).integers(0, 256, size=100_000, dtype=np.uint8).tobytes()
+    assert F.fnv1a64_hex(b) == O.ref_fnv1a64_hex(b)
+
+
+@pytest.mark.parametrize("binary", [True, False])
+def test_attend_ingest_reads_reference_point_files(tmp_path, binary):
+    """ingest (geometry.hpp:125-200) of FWPC / CSV files written by the reference's own
+    writers (geometry.hpp:202-237) == the generated cloud."""
+    from paper_2301_08739_b200.attend import ingest_points
+    if not O.have_ref():
+        pytest.skip("reference oracle not built")
+    scene = {"n_clusters": 5, "ppc_min": 10, "ppc_max": 30, "sigma": 1.0, "ext_x": 30.0, "ext_y": 20.0,
+             "n_bg": 200, "f_in": 3}
+    path = str(tmp_path / ("p.fwpc" if binary else "p.csv"))
+    O.ref_write_points(scene, 7, path, binary)
+    xy, f = ingest_points(path)
+    gxy, gf = F.generate_points(F.SceneSpec(5, 10, 30, 1.0, 30.0, 20.0, 200, 3), 7)
+    assert np.array_equal(xy, gxy) and np.array_equal(f, gf)
+
+
+def test_attend_cache_and_drops_match_port():
+    """The cache / drop bookkeeping of the attend JSON == the reference rule (port)."""
+    from paper_2301_08739_b200.attend import cache_and_drops
+    rng = np.random.default_rng(2)
+    for n, nb in ((700, 8), (690, 8), (75, 2), (69, 1), (300, 5)):
+        c = rng.uniform(0, 20, size=(n, 2))
+        blob = F.init_backbone_params(F.FwaConfig(d_model=16, n_heads=4, d_ff=32, n_blocks=nb), 1)
+        w = O.port_run_backbone(c, np.zeros((n, 16), np.float32), O.make_cfg(d_model=16, n_heads=4, d_ff=32,
+                                                                             n_blocks=nb), blob)
+        (comp, hit), drops = cache_and_drops(n, F.FwaConfig(n_blocks=nb))
+        assert (comp, hit) == tuple(w["cache"]) and drops == list(w["dropped_per_block"])
