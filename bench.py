@@ -275,6 +275,9 @@ def run_ours(args, rank, world, local_rank, dist):
     points = None
     if world == 1 and not args.no_points:
         points = run_points_pipeline(args, F, ctx, cfg, dev, stream, flush)
+    ew = None
+    if world == 1 and not args.no_equal_window:
+        ew = run_equal_window(args, F, ctx, cfg, dev, stream, flush)
     split = None
     if not args.no_split:
         split = run_split_scene(args, F, ctx, cfg, dev, stream, rank, world, dist, flush)
@@ -368,6 +371,7 @@ def run_ours(args, rank, world, local_rank, dist):
         "frame_frac_of_sustained": tot_flop / (ms_per_step / 1e3) / 1e12 / pk_sus,
         "cache": {"computed": cache[0], "hits": cache[1]},
         "pillarize": points,
+        "equal_window": ew,
         "config3_batch": batch,
         "config4_split": split,
     }
@@ -505,6 +509,51 @@ def run_points_pipeline(args, F, ctx, cfg, dev, stream, flush):
                     "around the call, L2 flushed"}
 
 
+def run_equal_window(args, F, ctx, cfg, dev, stream, flush):
+    """SURVEY §8f next-3 / the reference's C11 comparison (bench.hpp:215-242 vs 266-326):
+    one block (X axis, no shift) over the F60 frame, equal-size groups of 69 (the FlatFormer
+    path: sort + group + gather + block + scatter) vs equal-window partition padded per
+    occupancy bucket (16/32/64/128/256) through the same block kernels; device time per
+    call (the equal-window path includes its two host round trips), L2 flushed."""
+    import torch
+    ps = F.make_pillars(F.SCENES["F60"], 42)
+    n = ps.size()
+    c1 = F.FwaConfig(n_blocks=1)
+    ctx.load_params(c1, F.init_backbone_params(c1, 42))
+    d_c = torch.from_numpy(ps.coords).to(dev)
+    d_f = torch.from_numpy(ps.features.astype(np.float32)).to(dev)
+    d_o = torch.empty_like(d_f)
+    d_k = torch.empty(n, dtype=torch.int32, device=dev)
+
+    def timed(fn, steps):
+        for _ in range(3):
+            fn()
+        ms = 0.0
+        for _ in range(steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            r = fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ms += a.elapsed_time(b)
+        return ms / steps, r
+
+    steps = max(5, args.steps // 5)
+    es_ms, _ = timed(lambda: ctx.forward_device(d_c.data_ptr(), d_f.data_ptr(), [0, n], c1, d_o.data_ptr(),
+                                                d_k.data_ptr()), steps)
+    ew_ms, rep = timed(lambda: ctx.equal_window_forward(d_c.data_ptr(), d_f.data_ptr(), n, c1, d_o.data_ptr()),
+                       steps)
+    ctx.load_params(cfg, F.init_backbone_params(cfg, 42))  # restore the 8-block model
+    return {"workload": "one block (X, no shift) over the F60 frame: equal-size groups of 69 vs "
+                        "equal-window padding (bucket edges 16/32/64/128/256)",
+            "equal_size_ms": es_ms, "equal_window_ms": ew_ms, "equal_window_over_equal_size": ew_ms / es_ms,
+            "n_windows": rep["n_windows"], "max_occ": rep["max_occ"], "padding_factor_macs": rep["padding_factor"],
+            "rows_padded": rep["rows_padded"], "buckets": rep["buckets"],
+            "reference_cpu_ratio": "3.01x (test_output.txt:30, pinned scene, D=64, 1 thread)"}
+
+
 def run_split_scene(args, F, ctx, cfg, dev, stream, rank, world, dist, flush):
     """BASELINE config 4: the F250 scene (255,066 pillars) split by group ranges across
     the ranks with an all-gather of each block's sorted-order rows (NCCL over NVLink);
@@ -565,6 +614,7 @@ def main():
     ap.add_argument("--no-split", action="store_true", help="skip the config-4 split-scene measurement")
     ap.add_argument("--no-batch", action="store_true", help="skip the config-3 64-frame batch measurement")
     ap.add_argument("--no-points", action="store_true", help="skip the GPU pillarization measurement")
+    ap.add_argument("--no-equal-window", action="store_true", help="skip the equal-window baseline comparison")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

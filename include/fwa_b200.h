@@ -17,6 +17,8 @@
  *                                    + fwa::kernels::validate  kernels.hpp:75-90
  *   fwa_b200_pillarize[_device]      fwa::geometry::pillarize on the GPU  include/fwa/geometry.hpp:246-300
  *   fwa_b200_row_checksums           `fwa attend` row_checksums  tools/fwa_cli.cpp:214-218
+ *   fwa_b200_equal_window_forward    fwa::bench::bench_equal_window (padded SST-style baseline)
+ *                                    include/fwa/bench.hpp:266-326
  *   fwa_b200_generate_points         fwa::geometry::generate_synthetic  include/fwa/geometry.hpp:355-386
  *   fwa_b200_pillar_params           fwa::geometry::random_pillar_params  include/fwa/geometry.hpp:71-79
  *   fwa_b200_generate_pillars        fwa::geometry::generate_synthetic + pillarize +
@@ -211,6 +213,25 @@ int fwa_b200_pillarize_device(fwa_b200_ctx* ctx, const double* d_xy, const doubl
                               int32_t f_in, double resolution, const double* d_weight, const double* d_bias,
                               int32_t d_out, double* d_coords_out, double* d_feats_out, int64_t capacity,
                               int64_t* n_pillars);
+
+/* Equal-window (SST-style) padded baseline (bench.hpp:266-326, workload.hpp:44-142):
+ * partition by window (X axis, no shift), bucket windows by occupancy (bucket_edges,
+ * strictly increasing, <= 8), pad each window to its bucket's largest occupancy with zero
+ * rows, run block 0 of the loaded params per bucket with G = pad (the same kernels as
+ * the equal-size path).  Device buffers; d_out = N x d_model features of the real rows
+ * (input order).  The report mirrors WorkloadReport. */
+typedef struct fwa_ew_report {
+    int64_t n_windows;
+    int32_t max_occ, min_nonzero_occ;
+    double padding_factor; /* padded / actual attention MACs (workload.hpp:24-30, 92-142) */
+    int64_t rows_padded;   /* rows pushed through the block kernel (sum of windows x pad) */
+    int32_t n_buckets;
+    int32_t bucket_edge[8], bucket_pad[8];
+    int64_t bucket_windows[8];
+} fwa_ew_report_t;
+int fwa_b200_equal_window_forward(fwa_b200_ctx* ctx, const double* d_coords, const float* d_feats, int64_t n,
+                                  const fwa_config_t* cfg, const int32_t* bucket_edges, int32_t n_edges,
+                                  float* d_out, fwa_ew_report_t* report);
 
 /* FNV-1a-64 of a byte string (bench.hpp:62-72): the `fwa attend` feature_hash over the
  * f32 feature bytes and the config_digest over the config JSON (host). */

@@ -403,3 +403,40 @@ def ref_write_points(scene, seed, path, binary):
     _check_ref(ref().ref_write_points(scene["n_clusters"], scene["ppc_min"], scene["ppc_max"], scene["sigma"],
                                       scene["ext_x"], scene["ext_y"], scene["n_bg"], scene["f_in"], seed,
                                       path.encode(), int(binary)))
+
+
+def np_equal_window_forward(coords, feats32, record, w_x, w_y, edges=(16, 32, 64, 128, 256)):
+    """bench_equal_window (bench.hpp:266-326) computed: windows of
+    partition_equal_window (workload.hpp:44-68: floor(x / w_x), floor(y / w_y),
+    lexicographic, members in ingestion order), bucketed by occupancy, padded with zero
+    feature / zero PE rows to the bucket's largest occupancy, then the reference block
+    (port) per bucket.  Returns the real rows' outputs in input order."""
+    c = np.asarray(coords, np.float64)
+    f = np.asarray(feats32, np.float32)
+    n, d = f.shape
+    wm, wn, _, _ = np_sort_keys(c, w_x, w_y, 0, 0)
+    order = np.lexsort((np.arange(n), wn, wm))
+    key = np.stack([wm[order], wn[order]], 1)
+    starts = np.flatnonzero(np.r_[True, np.any(key[1:] != key[:-1], axis=1)])
+    ends = np.r_[starts[1:], n]
+    occ = ends - starts
+    bucket = np.searchsorted(np.asarray(edges), occ, side="left")
+    pe = port_positional_embedding(c, d)
+    out = np.zeros_like(f)
+    for b in range(len(edges)):
+        wins = np.flatnonzero(bucket == b)
+        if wins.size == 0:
+            continue
+        pad = int(occ[wins].max())
+        bf = np.zeros((wins.size * pad, d), np.float32)
+        bp = np.zeros_like(bf)
+        ids = []
+        for j, w in enumerate(wins):
+            mem = order[starts[w]:ends[w]]
+            bf[j * pad:j * pad + mem.size] = f[mem]
+            bp[j * pad:j * pad + mem.size] = pe[mem]
+            ids.append((j * pad, mem))
+        o = port_block_forward(bf, bp, wins.size, record)
+        for r0, mem in ids:
+            out[mem] = o[r0:r0 + mem.size]
+    return out

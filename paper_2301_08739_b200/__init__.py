@@ -38,7 +38,7 @@ EXPORTS = [
     "fwa_b200_positional_embedding", "fwa_b200_positional_embedding_f16", "fwa_b200_generate_pillars", "fwa_b200_init_params",
     "fwa_b200_split_begin", "fwa_b200_split_block", "fwa_b200_split_scatter",
     "fwa_b200_pillarize", "fwa_b200_pillarize_device", "fwa_b200_generate_points", "fwa_b200_pillar_params",
-    "fwa_b200_row_checksums", "fwa_b200_fnv1a64",
+    "fwa_b200_row_checksums", "fwa_b200_fnv1a64", "fwa_b200_equal_window_forward",
 ]
 
 PREC_BF16, PREC_FP32, PREC_BF16_3K = 0, 1, 2
@@ -95,6 +95,12 @@ class _Out(C.Structure):
     _fields_ = [("features", C.c_void_p), ("kept_indices", C.c_void_p), ("dropped_ids", C.c_void_p),
                 ("dropped_per_block", C.c_void_p), ("block_perms", C.c_void_p),
                 ("n_kept", C.c_int64), ("cache_computed", C.c_int32), ("cache_hits", C.c_int32)]
+
+
+class _EwReport(C.Structure):
+    _fields_ = [("n_windows", C.c_int64), ("max_occ", C.c_int32), ("min_nonzero_occ", C.c_int32),
+                ("padding_factor", C.c_double), ("rows_padded", C.c_int64), ("n_buckets", C.c_int32),
+                ("bucket_edge", C.c_int32 * 8), ("bucket_pad", C.c_int32 * 8), ("bucket_windows", C.c_int64 * 8)]
 
 
 class _Scene(C.Structure):
@@ -155,6 +161,8 @@ def lib():
         L.fwa_b200_row_checksums.argtypes = [vp, vp, i64, i32, vp]
         L.fwa_b200_fnv1a64.argtypes = [C.c_char_p, C.c_size_t]
         L.fwa_b200_fnv1a64.restype = C.c_uint64
+        L.fwa_b200_equal_window_forward.argtypes = [vp, vp, vp, i64, C.POINTER(_Cfg), vp, i32, vp,
+                                                     C.POINTER(_EwReport)]
         _lib_handle = L
     return _lib_handle
 
@@ -481,6 +489,22 @@ class Context:
                                                      d_bias or None, d_out, d_coords, d_out_feats, capacity,
                                                      C.byref(np_)))
         return np_.value
+
+    def equal_window_forward(self, d_coords: int, d_feats: int, n: int, cfg: FwaConfig, d_out: int,
+                             bucket_edges=(16, 32, 64, 128, 256)) -> dict:
+        """The equal-window padded baseline (bench.hpp:266-326) on device buffers: block 0 of
+        the loaded params over windows padded to their occupancy bucket's maximum."""
+        e = np.ascontiguousarray(bucket_edges, np.int32)
+        r = _EwReport()
+        c = cfg.c()
+        self._check(lib().fwa_b200_equal_window_forward(self._h, C.c_void_p(d_coords), C.c_void_p(d_feats), n,
+                                                         C.byref(c), _ptr(e), len(e), C.c_void_p(d_out),
+                                                         C.byref(r)))
+        nb = r.n_buckets
+        return {"n_windows": r.n_windows, "max_occ": r.max_occ, "min_nonzero_occ": r.min_nonzero_occ,
+                "padding_factor": r.padding_factor, "rows_padded": r.rows_padded,
+                "buckets": [{"edge": r.bucket_edge[b], "pad": r.bucket_pad[b], "windows": r.bucket_windows[b]}
+                            for b in range(nb)]}
 
     def fwa_block_forward(self, f: np.ndarray, pe: np.ndarray, record: bytes, n_groups: int) -> np.ndarray:
         f = np.ascontiguousarray(f, np.float32)

@@ -931,6 +931,7 @@ int choose_split(int G) {
     int best = -1, best_rounds = 1 << 30, best_skew = 1 << 30;
     for (int s = R - 128 > 1 ? R - 128 : 1; s <= 128 && s <= R; ++s) {
         if (ext_rows_needed(G, s) > kKVRows) continue;
+        if (mtiles(G, 0, s) > 16 || mtiles(G, s, R) > 16) continue;  // the per-CTA m-tile table
         const int t0 = 4 * mtiles(G, 0, s), t1 = 4 * mtiles(G, s, R);
         const int rounds = ((t0 + 15) / 16 > (t1 + 15) / 16) ? (t0 + 15) / 16 : (t1 + 15) / 16;
         const int skew = s > R - s ? s - (R - s) : (R - s) - s;

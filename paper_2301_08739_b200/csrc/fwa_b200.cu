@@ -1473,4 +1473,128 @@ int fwa_b200_row_checksums(fwa_b200_ctx* c, const float* d_features, int64_t n, 
     });
 }
 
+
+int fwa_b200_equal_window_forward(fwa_b200_ctx* c, const double* d_coords, const float* d_feats, int64_t n,
+                                  const fwa_config_t* cfg, const int32_t* edges, int32_t n_edges, float* d_out,
+                                  fwa_ew_report_t* rep) {
+    return guarded(c, [&] {
+        validate_cfg(cfg);
+        require_params(c, cfg);
+        if (n <= 0) throw FwaError{FWA_ERR_CONFIG, "bench: empty input"};
+        if (!edges || n_edges < 1 || n_edges > 8) throw FwaError{FWA_ERR_CONFIG, "padding_cost: no bucket edges"};
+        for (int i = 1; i < n_edges; ++i)
+            if (edges[i] <= edges[i - 1])
+                throw FwaError{FWA_ERR_CONFIG, "padding_cost: bucket edges must be strictly increasing"};
+        cudaStream_t st = c->stream;
+        const int d = cfg->d_model;
+        // ---- partition: the window sort of spec 0 (X axis, no shift), windows in lexicographic order
+        int64_t off_h[2] = {0, n};
+        int64_t* d_off = ws<int64_t>(c, "ew_off", 2);
+        CUDA_OK(cudaMemcpyAsync(d_off, off_h, sizeof(off_h), cudaMemcpyHostToDevice, st));
+        const double w_x = cfg->window_px * cfg->resolution, w_y = cfg->window_py * cfg->resolution;
+        int32_t* sorted = sort_specs(c, d_coords, n, 1, w_x, w_y, d_off, 1, true);
+        const uint32_t* bin_of = ws<uint32_t>(c, "bin_of", static_cast<size_t>(n));
+        uint32_t* flag = ws<uint32_t>(c, "ew_flag", static_cast<size_t>(n));
+        uint32_t* ex = ws<uint32_t>(c, "ew_ex", static_cast<size_t>(n));
+        uint32_t* tmp = ws<uint32_t>(c, "ew_scan_tmp", scan_tmp_words(n) + 8);
+        uint32_t* d_cnt = ws<uint32_t>(c, "ew_cnt", 4);
+        launch_ew_runs(sorted, bin_of, n, flag, st, &c->launches);
+        exclusive_scan_u32(flag, ex, n, tmp, d_cnt, st, &c->launches);
+        uint32_t W32 = 0;
+        CUDA_OK(cudaMemcpyAsync(&W32, d_cnt, 4, cudaMemcpyDeviceToHost, st));
+        CUDA_OK(cudaStreamSynchronize(st));
+        const int64_t W = W32;
+        uint32_t* wstart = ws<uint32_t>(c, "ew_wstart", static_cast<size_t>(W));
+        launch_ew_starts(flag, ex, n, wstart, st, &c->launches);
+        int32_t* d_edges = ws<int32_t>(c, "ew_edges", 8);
+        CUDA_OK(cudaMemcpyAsync(d_edges, edges, static_cast<size_t>(n_edges) * 4, cudaMemcpyHostToDevice, st));
+        uint32_t* wocc = ws<uint32_t>(c, "ew_wocc", static_cast<size_t>(W));
+        int32_t* wbucket = ws<int32_t>(c, "ew_wbucket", static_cast<size_t>(W));
+        uint32_t* bstat = ws<uint32_t>(c, "ew_bstat", 18);  // bmax[8] | bcnt[8] | overflow
+        CUDA_OK(cudaMemsetAsync(bstat, 0, 18 * 4, st));
+        launch_ew_bucket(wstart, W, n, d_edges, n_edges, wocc, wbucket, bstat, bstat + 8,
+                         reinterpret_cast<int*>(bstat + 16), st, &c->launches);
+        uint32_t hb[18];
+        std::vector<uint32_t> hocc(static_cast<size_t>(W));
+        CUDA_OK(cudaMemcpyAsync(hb, bstat, sizeof(hb), cudaMemcpyDeviceToHost, st));
+        CUDA_OK(cudaMemcpyAsync(hocc.data(), wocc, static_cast<size_t>(W) * 4, cudaMemcpyDeviceToHost, st));
+        CUDA_OK(cudaStreamSynchronize(st));
+        check_launch("equal-window partition");
+        if (hb[16]) throw FwaError{FWA_ERR_CONFIG, "bench: occupancy exceeds final bucket edge"};
+        // ---- extended inputs: row n = zeros (padding gathers it), row n + 1 = sink for padding outputs
+        float* xe = ws<float>(c, "ew_x", static_cast<size_t>(n + 2) * d);
+        CUDA_OK(cudaMemcpyAsync(xe, d_feats, static_cast<size_t>(n) * d * 4, cudaMemcpyDeviceToDevice, st));
+        CUDA_OK(cudaMemsetAsync(xe + static_cast<size_t>(n) * d, 0, 2 * static_cast<size_t>(d) * 4, st));
+        bool any_fast = false, any_slow = false;
+        for (int b = 0; b < n_edges; ++b)
+            if (hb[8 + b]) {
+                const bool f = fast_path_ok(c, d, cfg->n_heads, cfg->d_ff, static_cast<int>(hb[b]));
+                any_fast |= f;
+                any_slow |= !f;
+            }
+        __half* pe16 = any_fast ? ws<__half>(c, "ew_pe16", static_cast<size_t>(n + 2) * d) : nullptr;
+        float* pe32 = any_slow ? ws<float>(c, "ew_pe32", static_cast<size_t>(n + 2) * d) : nullptr;
+        if (pe16) {
+            launch_positional_embedding(d_coords, n, d, pe_freq(c, d), nullptr, pe16, st, &c->launches);
+            CUDA_OK(cudaMemsetAsync(pe16 + static_cast<size_t>(n) * d, 0, 2 * static_cast<size_t>(d) * 2, st));
+        }
+        if (pe32) {
+            launch_positional_embedding(d_coords, n, d, pe_freq(c, d), pe32, nullptr, st, &c->launches);
+            CUDA_OK(cudaMemsetAsync(pe32 + static_cast<size_t>(n) * d, 0, 2 * static_cast<size_t>(d) * 4, st));
+        }
+        float* oe = ws<float>(c, "ew_out", static_cast<size_t>(n + 2) * d);
+        uint32_t* wrank = ws<uint32_t>(c, "ew_wrank", static_cast<size_t>(W));
+        CUDA_OK(cudaMemsetAsync(c->d_flag, 0, 2 * sizeof(int), st));
+        int64_t rows_padded = 0;
+        for (int b = 0; b < n_edges; ++b) {
+            const int64_t cnt = hb[8 + b];
+            if (!cnt) continue;
+            const int pad = static_cast<int>(hb[b]);
+            const int64_t rows = cnt * pad;
+            rows_padded += rows;
+            launch_ew_bflag(wbucket, W, b, flag, st, &c->launches);
+            exclusive_scan_u32(flag, wrank, W, tmp, nullptr, st, &c->launches);
+            int32_t* ridx = ws<int32_t>(c, "ew_ridx", static_cast<size_t>(rows));
+            int32_t* sidx = ws<int32_t>(c, "ew_sidx", static_cast<size_t>(rows));
+            launch_ew_fill(wstart, wocc, wbucket, wrank, W, b, pad, sorted, n, ridx, sidx, st, &c->launches);
+            fwa_config_t cb = *cfg;
+            cb.group_size = pad;
+            run_block(c, c->blocks[0], &cb, rows, ridx, xe, nullptr, pe32, pe16, oe, sidx,
+                      fast_path_ok(c, d, cfg->n_heads, cfg->d_ff, pad));
+        }
+        CUDA_OK(cudaMemcpyAsync(d_out, oe, static_cast<size_t>(n) * d * 4, cudaMemcpyDeviceToDevice, st));
+        CUDA_OK(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CUDA_OK(cudaStreamSynchronize(st));
+        check_launch("equal-window blocks");
+        if (*c->h_flag) throw FwaError{FWA_ERR_NUMERIC, "group_attention: non-finite input"};
+        if (rep) {
+            // WorkloadReport (workload.hpp:92-142): MACs 2 L^2 D + 4 L D^2 per window
+            auto macs = [&](double l) { return 2.0 * l * l * d + 4.0 * l * d * static_cast<double>(d); };
+            double act = 0, padded = 0;
+            int mx = 0, mn = 1 << 30;
+            for (int64_t w = 0; w < W; ++w) {
+                const int o = static_cast<int>(hocc[static_cast<size_t>(w)]);
+                int b = 0;
+                while (b < n_edges && o > edges[b]) ++b;
+                act += macs(o);
+                padded += macs(hb[b]);
+                mx = std::max(mx, o);
+                mn = std::min(mn, o);
+            }
+            *rep = fwa_ew_report_t{};
+            rep->n_windows = W;
+            rep->max_occ = mx;
+            rep->min_nonzero_occ = mn;
+            rep->padding_factor = padded / act;
+            rep->rows_padded = rows_padded;
+            rep->n_buckets = n_edges;
+            for (int b = 0; b < n_edges; ++b) {
+                rep->bucket_edge[b] = edges[b];
+                rep->bucket_pad[b] = static_cast<int32_t>(hb[b]);
+                rep->bucket_windows[b] = hb[8 + b];
+            }
+        }
+    });
+}
+
 } // extern "C"

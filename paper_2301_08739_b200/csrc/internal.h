@@ -184,6 +184,19 @@ void launch_pillar_features(const uint32_t* pcell, const uint32_t* start, const 
                             int f_in, const double* fs, double* pooled, const double* w, const double* bias,
                             int d_out, double* out, cudaStream_t s, int64_t* launches);
 
+// ------------------------------------------------------------------ equal-window baseline (equal_window.cu)
+void launch_ew_runs(const int32_t* sorted, const uint32_t* bin_of, int64_t n, uint32_t* flag, cudaStream_t s,
+                    int64_t* launches);
+void launch_ew_starts(const uint32_t* flag, const uint32_t* ex, int64_t n, uint32_t* wstart, cudaStream_t s,
+                      int64_t* launches);
+void launch_ew_bucket(const uint32_t* wstart, int64_t W, int64_t n, const int32_t* edges, int n_edges, uint32_t* wocc,
+                      int32_t* wbucket, uint32_t* bmax, uint32_t* bcnt, int* overflow, cudaStream_t s,
+                      int64_t* launches);
+void launch_ew_bflag(const int32_t* wbucket, int64_t W, int b, uint32_t* flag, cudaStream_t s, int64_t* launches);
+void launch_ew_fill(const uint32_t* wstart, const uint32_t* wocc, const int32_t* wbucket, const uint32_t* wrank,
+                    int64_t W, int b, int pad, const int32_t* sorted, int64_t n, int32_t* ridx, int32_t* sidx,
+                    cudaStream_t s, int64_t* launches);
+
 // ------------------------------------------------------------------ misc
 void launch_scatter_rows(const float* src, const int32_t* ids, const uint32_t* rank, int64_t n,
                          int d, float* dst, cudaStream_t s, int64_t* launches);

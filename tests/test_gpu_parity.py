@@ -526,3 +526,31 @@ def test_attend_json_matches_reference(tmp_path, ctx16):
     f = np.frombuffer(raw[12:], np.float32).reshape(n, d)
     assert np.array_equal(np.cumsum(f.astype(np.float64), axis=1)[:, -1], got_sums)
     assert j["feature_hash"] == F.fnv1a64_hex(f.tobytes())
+
+
+# ----------------------------------------------------------------------------- equal-window baseline (§8f next-3)
+
+def test_equal_window_baseline_vs_oracle(ctx16):
+    """The SST-style padded baseline (bench.hpp:266-326) on the GPU == the reference block
+    run on the same padded windows (oracle), and its WorkloadReport statistics."""
+    import torch
+    ps = F.make_pillars(F.SCENES["F10"], 42)
+    cfg = F.FwaConfig(n_blocks=1)
+    blob = F.init_backbone_params(cfg, 3)
+    ctx16.load_params(cfg, blob)
+    n = ps.size()
+    f32 = ps.features.astype(np.float32)
+    d_c = torch.from_numpy(ps.coords).cuda()
+    d_f = torch.from_numpy(f32).cuda()
+    d_o = torch.empty_like(d_f)
+    torch.cuda.synchronize()
+    rep = ctx16.equal_window_forward(d_c.data_ptr(), d_f.data_ptr(), n, cfg, d_o.data_ptr())
+    got = d_o.cpu().numpy()
+    w = 9 * 0.32
+    want = O.np_equal_window_forward(ps.coords, f32, blob[:16 + 4 * 132480], w, w)
+    assert O.max_rel_err(got, want) <= TOL_BF16
+    wm, wn, _, _ = O.np_sort_keys(ps.coords, w, w, 0, 0)
+    _, counts = np.unique(np.stack([wm, wn], 1), axis=0, return_counts=True)
+    assert rep["n_windows"] == counts.size
+    assert rep["max_occ"] == counts.max() and rep["min_nonzero_occ"] == counts.min()
+    assert rep["rows_padded"] >= n and rep["padding_factor"] >= 1.0
