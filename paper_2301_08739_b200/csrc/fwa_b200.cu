@@ -807,6 +807,11 @@ void forward_device(fwa_b200_ctx* c, const double* d_coords, const float* d_feat
     CUDA_OK(cudaEventRecord(c->ev_fork, st));
     CUDA_OK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
     launch_positional_embedding(d_coords, S.ntot, d, freq, pe, pe16, c->side, &c->launches);
+    // block 0's input rows into L2 while the schedule runs (the host API's copy stream
+    // lands them later; then they are already in L2)
+    if (!feats_ready)
+        launch_prefetch_l2(d_feats ? static_cast<const void*>(d_feats) : static_cast<const void*>(d_feats64),
+                           S.ntot * d * (d_feats ? 4 : 8), c->side, &c->launches);
     CUDA_OK(cudaEventRecord(c->ev_join, c->side));
     {
         StageEv t(c, FWA_PROF_SCHEDULE);

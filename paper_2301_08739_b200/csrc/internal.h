@@ -100,6 +100,7 @@ void launch_spec_compact(const int32_t* sorted, int64_t total, const uint8_t* dr
 // f32 PE (pe != nullptr) and/or fp16 PE rows (pe16 != nullptr, the bf16 fast path's copy)
 void launch_positional_embedding(const double* coords, int64_t n, int d, const double* d_freq,
                                  float* pe, __half* pe16, cudaStream_t s, int64_t* launches);
+void launch_prefetch_l2(const void* p, int64_t bytes, cudaStream_t s, int64_t* launches);
 void launch_row_checksums(const float* f, int64_t n, int d, double* out, cudaStream_t s, int64_t* launches);
 void launch_f32_to_f16(const float* in, int64_t n, __half* out, cudaStream_t s, int64_t* launches);
 // h[r] = LN1(x[idx[r]]) * g + b + pe[idx[r]]  (x f32, or f64 when x64 != nullptr)
