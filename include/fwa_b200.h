@@ -17,6 +17,7 @@
  *                                    + fwa::kernels::validate  kernels.hpp:75-90
  *   fwa_b200_pillarize[_device]      fwa::geometry::pillarize on the GPU  include/fwa/geometry.hpp:246-300
  *   fwa_b200_row_checksums           `fwa attend` row_checksums  tools/fwa_cli.cpp:214-218
+ *   fwa_b200_block_backward          fwa::kernels::fwa_block_backward  include/fwa/kernels.hpp:660-765
  *   fwa_b200_equal_window_forward    fwa::bench::bench_equal_window (padded SST-style baseline)
  *                                    include/fwa/bench.hpp:266-326
  *   fwa_b200_generate_points         fwa::geometry::generate_synthetic  include/fwa/geometry.hpp:355-386
@@ -213,6 +214,14 @@ int fwa_b200_pillarize_device(fwa_b200_ctx* ctx, const double* d_xy, const doubl
                               int32_t f_in, double resolution, const double* d_weight, const double* d_bias,
                               int32_t d_out, double* d_coords_out, double* d_feats_out, int64_t capacity,
                               int64_t* n_pillars);
+
+/* fwa_block_forward (cached) + fwa_block_backward (kernels.hpp:636-765) on the GPU, fp32,
+ * deterministic: f, pe, grad_out are rows x d (n_groups blocks of G consecutive rows);
+ * grad_f (rows x d) and grad_record (one FWAP record of the parameter gradients, the
+ * record's size, may be NULL) are host buffers. */
+int fwa_b200_block_backward(fwa_b200_ctx* ctx, const float* f, const float* pe, int64_t rows, int32_t n_groups,
+                            const void* record, size_t record_len, const float* grad_out, float* grad_f,
+                            void* grad_record);
 
 /* Equal-window (SST-style) padded baseline (bench.hpp:266-326, workload.hpp:44-142):
  * partition by window (X axis, no shift), bucket windows by occupancy (bucket_edges,

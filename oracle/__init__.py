@@ -90,6 +90,9 @@ def ref():
         lib.ref_fnv1a64_hex.argtypes = [C.c_void_p, C.c_int64, C.c_char_p]
         lib.ref_write_points.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                          C.c_int, C.c_int, C.c_uint64, C.c_char_p, C.c_int]
+        lib.ref_block_backward.restype = C.c_int64
+        lib.ref_block_backward.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_void_p,
+                                           C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]
         lib.ref_init_params_fwap.restype = C.c_int64
         lib.ref_init_params_fwap.argtypes = [C.POINTER(CfgC), C.c_int64, C.c_uint64, C.c_void_p,
                                              C.c_int64]
@@ -440,3 +443,18 @@ def np_equal_window_forward(coords, feats32, record, w_x, w_y, edges=(16, 32, 64
         for r0, mem in ids:
             out[mem] = o[r0:r0 + mem.size]
     return out
+
+
+def ref_block_backward(f, pe, n_groups, record, grad_out):
+    """fwa_block_forward (cached) + fwa_block_backward (kernels.hpp:636-765) of the
+    reference: (grad_f rows x d, parameter gradients as one FWAP record)."""
+    f = np.ascontiguousarray(f, np.float32)
+    pe = np.ascontiguousarray(pe, np.float32)
+    g = np.ascontiguousarray(grad_out, np.float32)
+    gf = np.empty_like(f)
+    out = np.empty(len(record), np.uint8)
+    bb = np.frombuffer(record, np.uint8)
+    n = ref().ref_block_backward(_p(f), _p(pe), f.shape[0], f.shape[1], n_groups, _p(bb), len(record), _p(g),
+                                 _p(gf), _p(out), len(record))
+    _check_ref(0 if n >= 0 else -n)
+    return gf, out[:n].tobytes()

@@ -370,6 +370,34 @@ int ref_block_forward(const float* f, const float* pe, int64_t rows, int64_t d, 
     });
 }
 
+// fwa_block_forward with a cache, then fwa_block_backward (kernels.hpp:636-765): the input
+// gradient (rows x d) and the parameter gradients serialised as one FWAP record.
+int64_t ref_block_backward(const float* f, const float* pe, int64_t rows, int64_t d, int n_groups,
+                           const void* blob, int64_t blob_len, const float* grad_out, float* grad_f,
+                           void* grad_blob, int64_t cap) {
+    int64_t len = -1;
+    int rc = guarded([&] {
+        const auto params = parse_blob(blob, static_cast<std::size_t>(blob_len));
+        if (params.size() != 1) throw config_error("expected exactly one FWAP record");
+        Dense2<float> F(static_cast<std::size_t>(rows), static_cast<std::size_t>(d));
+        Dense2<float> P(static_cast<std::size_t>(rows), static_cast<std::size_t>(d));
+        Dense2<float> G(static_cast<std::size_t>(rows), static_cast<std::size_t>(d));
+        std::memcpy(F.data.data(), f, F.data.size() * sizeof(float));
+        std::memcpy(P.data.data(), pe, P.data.size() * sizeof(float));
+        std::memcpy(G.data.data(), grad_out, G.data.size() * sizeof(float));
+        kernels::FwaBlockCache<float> cache;
+        kernels::fwa_block_forward(F, P, params[0], n_groups, &cache, 1);
+        const auto gr = kernels::fwa_block_backward(G, cache, params[0]);
+        std::memcpy(grad_f, gr.grad_f.data.data(), gr.grad_f.data.size() * sizeof(float));
+        std::ostringstream os;
+        kernels::save_params(os, gr.params);
+        const std::string sp = os.str();
+        len = static_cast<int64_t>(sp.size());
+        if (grad_blob && len <= cap) std::memcpy(grad_blob, sp.data(), sp.size());
+    });
+    return rc ? -rc : len;
+}
+
 // f64 dense-oracle attention + unfused FFN (oracle.hpp:90-173, 205-228).
 int ref_oracle_block(const double* f, const double* pe, int64_t rows, int64_t d, int n_groups,
                      const void* blob, int64_t blob_len, double* out) {

@@ -38,7 +38,7 @@ EXPORTS = [
     "fwa_b200_positional_embedding", "fwa_b200_positional_embedding_f16", "fwa_b200_generate_pillars", "fwa_b200_init_params",
     "fwa_b200_split_begin", "fwa_b200_split_block", "fwa_b200_split_scatter",
     "fwa_b200_pillarize", "fwa_b200_pillarize_device", "fwa_b200_generate_points", "fwa_b200_pillar_params",
-    "fwa_b200_row_checksums", "fwa_b200_fnv1a64", "fwa_b200_equal_window_forward",
+    "fwa_b200_row_checksums", "fwa_b200_fnv1a64", "fwa_b200_equal_window_forward", "fwa_b200_block_backward",
 ]
 
 PREC_BF16, PREC_FP32, PREC_BF16_3K = 0, 1, 2
@@ -161,6 +161,7 @@ def lib():
         L.fwa_b200_row_checksums.argtypes = [vp, vp, i64, i32, vp]
         L.fwa_b200_fnv1a64.argtypes = [C.c_char_p, C.c_size_t]
         L.fwa_b200_fnv1a64.restype = C.c_uint64
+        L.fwa_b200_block_backward.argtypes = [vp, vp, vp, i64, i32, vp, C.c_size_t, vp, vp, vp]
         L.fwa_b200_equal_window_forward.argtypes = [vp, vp, vp, i64, C.POINTER(_Cfg), vp, i32, vp,
                                                      C.POINTER(_EwReport)]
         _lib_handle = L
@@ -489,6 +490,19 @@ class Context:
                                                      d_bias or None, d_out, d_coords, d_out_feats, capacity,
                                                      C.byref(np_)))
         return np_.value
+
+    def fwa_block_backward(self, f: np.ndarray, pe: np.ndarray, record: bytes, n_groups: int,
+                           grad_out: np.ndarray):
+        """kernels.hpp:660-765 on the GPU: (grad_f, parameter gradients as one FWAP record)."""
+        f = np.ascontiguousarray(f, np.float32)
+        pe = np.ascontiguousarray(pe, np.float32)
+        go = np.ascontiguousarray(grad_out, np.float32)
+        gf = np.empty_like(f)
+        gr = np.empty(len(record), np.uint8)
+        rb = np.frombuffer(record, np.uint8)
+        self._check(lib().fwa_b200_block_backward(self._h, _ptr(f), _ptr(pe), f.shape[0], n_groups, _ptr(rb),
+                                                   len(record), _ptr(go), _ptr(gf), _ptr(gr)))
+        return gf, gr.tobytes()
 
     def equal_window_forward(self, d_coords: int, d_feats: int, n: int, cfg: FwaConfig, d_out: int,
                              bucket_edges=(16, 32, 64, 128, 256)) -> dict:

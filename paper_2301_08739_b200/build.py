@@ -19,7 +19,7 @@ CUFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-rela
            f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
 CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", f"-I{os.path.join(ROOT, 'include')}"]
 
-CU_SOURCES = ["sort.cu", "simt.cu", "tc.cu", "attn_mma.cu", "block_fused.cu", "pillarize.cu", "equal_window.cu", "fwa_b200.cu"]
+CU_SOURCES = ["sort.cu", "simt.cu", "tc.cu", "attn_mma.cu", "block_fused.cu", "pillarize.cu", "equal_window.cu", "backward.cu", "fwa_b200.cu"]
 CXX_SOURCES = ["host_scene.cpp"]
 
 

@@ -1602,4 +1602,144 @@ int fwa_b200_equal_window_forward(fwa_b200_ctx* c, const double* d_coords, const
     });
 }
 
+
+int fwa_b200_block_backward(fwa_b200_ctx* c, const float* f, const float* pe, int64_t rows, int32_t n_groups,
+                            const void* record, size_t record_len, const float* grad_out, float* grad_f,
+                            void* grad_record) {
+    return guarded(c, [&] {
+        std::vector<std::vector<float>> keep;
+        const auto recs = parse_fwap(record, record_len, keep);
+        if (recs.size() != 1) throw FwaError{FWA_ERR_CONFIG, "expected exactly one FWAP record"};
+        const Record& r = recs[0];
+        const int d = r.d, h = r.h, dff = r.dff;
+        if (n_groups < 1 || rows < 1 || rows % n_groups != 0)
+            throw FwaError{FWA_ERR_SHAPE, "group_attention: rows not divisible by n_groups"};
+        const int G = static_cast<int>(rows / n_groups);
+        const std::vector<BlockParams> bp =
+            upload_block_params(recs, c->ws["bw_params_f32"], c->ws["bw_params_bf16"], c->stream);
+        const BlockParams& P = bp[0];
+        cudaStream_t st = c->stream;
+        const size_t R = static_cast<size_t>(rows), D = static_cast<size_t>(d), F = static_cast<size_t>(dff);
+        auto buf = [&](const char* name, size_t n) { return ws<float>(c, name, n); };
+        // inputs
+        float* df = buf("bw_f", R * D);
+        float* dpe = buf("bw_pe", R * D);
+        float* dgo = buf("bw_go", R * D);
+        CUDA_OK(cudaMemcpyAsync(df, f, R * D * 4, cudaMemcpyHostToDevice, st));
+        CUDA_OK(cudaMemcpyAsync(dpe, pe, R * D * 4, cudaMemcpyHostToDevice, st));
+        CUDA_OK(cudaMemcpyAsync(dgo, grad_out, R * D * 4, cudaMemcpyHostToDevice, st));
+        // transposed weights for the input gradients (dX = dY W = dY (W^T)^T)
+        std::vector<float> tr;
+        auto transpose_up = [&](const char* name, const float* hw, int J, int K) {
+            tr.assign(static_cast<size_t>(J) * K, 0.f);
+            for (int j = 0; j < J; ++j)
+                for (int k = 0; k < K; ++k) tr[static_cast<size_t>(k) * J + j] = hw[static_cast<size_t>(j) * K + k];
+            float* dw = buf(name, tr.size());
+            CUDA_OK(cudaMemcpyAsync(dw, tr.data(), tr.size() * 4, cudaMemcpyHostToDevice, st));
+            CUDA_OK(cudaStreamSynchronize(st));  // tr is reused
+            return dw;
+        };
+        const float* hw = r.t;
+        const float* h_wqkv = hw;
+        const float* h_wout = hw + 3 * D * D + 3 * D;
+        const float* h_w1 = h_wout + D * D + D + 4 * D;
+        const float* h_w2 = h_w1 + F * D + F;
+        float* wqkvT = transpose_up("bw_wqkvT", h_wqkv, 3 * d, d);
+        float* woutT = transpose_up("bw_woutT", h_wout, d, d);
+        float* w1T = transpose_up("bw_w1T", h_w1, dff, d);
+        float* w2T = transpose_up("bw_w2T", h_w2, d, dff);
+        // ---- forward with caches (kernels.hpp:447-633)
+        float* hb = buf("bw_h", R * D);
+        float* xhat1 = buf("bw_xhat1", R * D);
+        float* inv1 = buf("bw_inv1", R);
+        float* qkv = buf("bw_qkv", R * 3 * D);
+        float* probs = buf("bw_probs", static_cast<size_t>(n_groups) * h * G * G);
+        float* cat = buf("bw_cat", R * D);
+        float* mid = buf("bw_mid", R * D);
+        float* ln2 = buf("bw_ln2", R * D);
+        float* xhat2 = buf("bw_xhat2", R * D);
+        float* inv2 = buf("bw_inv2", R);
+        float* u = buf("bw_u", R * F);
+        float* a = buf("bw_a", R * F);
+        launch_ln_fwd_cache(df, dpe, rows, d, P.ln1_g, P.ln1_b, hb, xhat1, inv1, st, &c->launches);
+        GemmArgs g{};
+        g.A = hb; g.M = rows; g.K = d; g.W = P.w_qkv; g.N = 3 * d; g.bias = P.b_qkv; g.C = qkv;
+        launch_gemm_f32(g, EPI_BIAS, st, &c->launches);
+        launch_attn_probs(qkv, n_groups, G, d, h, probs, cat, st, &c->launches);
+        g = GemmArgs{};
+        g.A = cat; g.M = rows; g.K = d; g.W = P.w_out; g.N = d; g.bias = P.b_out; g.C = mid; g.R = df;
+        launch_gemm_f32(g, EPI_RESID_GATHER, st, &c->launches);
+        launch_ln_fwd_cache(mid, nullptr, rows, d, P.ln2_g, P.ln2_b, ln2, xhat2, inv2, st, &c->launches);
+        g = GemmArgs{};
+        g.A = ln2; g.M = rows; g.K = d; g.W = P.w1; g.N = dff; g.bias = P.b1; g.C = u;
+        launch_gemm_f32(g, EPI_BIAS, st, &c->launches);
+        launch_gelu_fwd(u, static_cast<int64_t>(R * F), a, st, &c->launches);
+        // ---- backward (kernels.hpp:681-764)
+        const int nc = reduce_chunks(rows);
+        float* part = buf("bw_part", static_cast<size_t>(nc) * static_cast<size_t>(std::max(3 * d * d, dff * d)));
+        const size_t rec_f = record_floats(d, dff);
+        float* gp = buf("bw_gparams", rec_f);  // FWAP field order
+        float* g_wqkv = gp;
+        float* g_bqkv = g_wqkv + 3 * D * D;
+        float* g_wout = g_bqkv + 3 * D;
+        float* g_bout = g_wout + D * D;
+        float* g_ln1g = g_bout + D;
+        float* g_ln1b = g_ln1g + D;
+        float* g_ln2g = g_ln1b + D;
+        float* g_ln2b = g_ln2g + D;
+        float* g_w1 = g_ln2b + D;
+        float* g_b1 = g_w1 + F * D;
+        float* g_w2 = g_b1 + F;
+        float* g_b2 = g_w2 + D * F;
+        float* ga = buf("bw_ga", R * F);
+        float* gu = buf("bw_gu", R * F);
+        float* gln2 = buf("bw_gln2", R * D);
+        float* gfp = buf("bw_gfp", R * D);
+        float* tmp = buf("bw_tmp", R * D);
+        float* gcat = buf("bw_gcat", R * D);
+        float* gqkv = buf("bw_gqkv", R * 3 * D);
+        float* gh = buf("bw_gh", R * D);
+        float* gfo = buf("bw_gfo", R * D);
+        // FFN sublayer
+        launch_colsum(dgo, rows, d, part, g_b2, st, &c->launches);
+        launch_wgrad(dgo, a, rows, d, dff, part, g_w2, st, &c->launches);
+        g = GemmArgs{};
+        g.A = dgo; g.M = rows; g.K = d; g.W = w2T; g.N = dff; g.C = ga;  // g_a = dY W2
+        launch_gemm_f32(g, EPI_BIAS, st, &c->launches);
+        launch_gelu_back(ga, u, static_cast<int64_t>(R * F), gu, st, &c->launches);
+        launch_colsum(gu, rows, dff, part, g_b1, st, &c->launches);
+        launch_wgrad(gu, ln2, rows, dff, d, part, g_w1, st, &c->launches);
+        g = GemmArgs{};
+        g.A = gu; g.M = rows; g.K = dff; g.W = w1T; g.N = d; g.C = gln2;  // g_ln2 = g_u W1
+        launch_gemm_f32(g, EPI_BIAS, st, &c->launches);
+        launch_ln_back(gln2, xhat2, inv2, P.ln2_g, rows, d, dgo, gfp, tmp, st, &c->launches);  // + residual
+        launch_colsum(tmp, rows, d, part, g_ln2g, st, &c->launches);
+        launch_colsum(gln2, rows, d, part, g_ln2b, st, &c->launches);
+        // attention sublayer
+        launch_colsum(gfp, rows, d, part, g_bout, st, &c->launches);
+        launch_wgrad(gfp, cat, rows, d, d, part, g_wout, st, &c->launches);
+        g = GemmArgs{};
+        g.A = gfp; g.M = rows; g.K = d; g.W = woutT; g.N = d; g.C = gcat;
+        launch_gemm_f32(g, EPI_BIAS, st, &c->launches);
+        if (!launch_attn_back(qkv, probs, gcat, n_groups, G, d, h, gqkv, st, &c->launches))
+            throw FwaError{FWA_ERR_CONFIG, "block_backward: group size too large"};
+        launch_colsum(gqkv, rows, 3 * d, part, g_bqkv, st, &c->launches);
+        launch_wgrad(gqkv, hb, rows, 3 * d, d, part, g_wqkv, st, &c->launches);
+        g = GemmArgs{};
+        g.A = gqkv; g.M = rows; g.K = 3 * d; g.W = wqkvT; g.N = d; g.C = gh;
+        launch_gemm_f32(g, EPI_BIAS, st, &c->launches);
+        launch_ln_back(gh, xhat1, inv1, P.ln1_g, rows, d, gfp, gfo, tmp, st, &c->launches);  // grad_f
+        launch_colsum(tmp, rows, d, part, g_ln1g, st, &c->launches);
+        launch_colsum(gh, rows, d, part, g_ln1b, st, &c->launches);
+        check_launch("block_backward");
+        CUDA_OK(cudaMemcpyAsync(grad_f, gfo, R * D * 4, cudaMemcpyDeviceToHost, st));
+        if (grad_record) {
+            std::memcpy(grad_record, record, 16);  // FWAP magic + dims
+            CUDA_OK(cudaMemcpyAsync(static_cast<uint8_t*>(grad_record) + 16, gp, rec_f * 4, cudaMemcpyDeviceToHost,
+                                    st));
+        }
+        CUDA_OK(cudaStreamSynchronize(st));
+    });
+}
+
 } // extern "C"

@@ -198,6 +198,23 @@ void launch_ew_fill(const uint32_t* wstart, const uint32_t* wocc, const int32_t*
                     int64_t W, int b, int pad, const int32_t* sorted, int64_t n, int32_t* ridx, int32_t* sidx,
                     cudaStream_t s, int64_t* launches);
 
+// ------------------------------------------------------------------ block backward (backward.cu)
+void launch_ln_fwd_cache(const float* x, const float* pe, int64_t rows, int d, const float* g, const float* b,
+                         float* y, float* xhat, float* inv_std, cudaStream_t s, int64_t* launches);
+void launch_attn_probs(const float* qkv, int64_t n_groups, int G, int d, int heads, float* probs, float* cat,
+                       cudaStream_t s, int64_t* launches);
+void launch_gelu_fwd(const float* u, int64_t n, float* a, cudaStream_t s, int64_t* launches);
+void launch_gelu_back(const float* ga, const float* u, int64_t n, float* gu, cudaStream_t s, int64_t* launches);
+void launch_ln_back(const float* gy, const float* xhat, const float* inv_std, const float* gamma, int64_t rows,
+                    int d, const float* add, float* gx, float* gy_xhat, cudaStream_t s, int64_t* launches);
+bool launch_attn_back(const float* qkv, const float* probs, const float* gcat, int64_t n_groups, int G, int d,
+                      int heads, float* gqkv, cudaStream_t s, int64_t* launches);
+int reduce_chunks(int64_t rows);
+void launch_wgrad(const float* dy, const float* x, int64_t rows, int J, int K, float* part, float* dw, cudaStream_t s,
+                  int64_t* launches);
+void launch_colsum(const float* y, int64_t rows, int J, float* part, float* out, cudaStream_t s, int64_t* launches);
+void launch_mul(const float* a, const float* b, int64_t n, float* out, cudaStream_t s, int64_t* launches);
+
 // ------------------------------------------------------------------ misc
 void launch_scatter_rows(const float* src, const int32_t* ids, const uint32_t* rank, int64_t n,
                          int d, float* dst, cudaStream_t s, int64_t* launches);

@@ -554,3 +554,40 @@ def test_equal_window_baseline_vs_oracle(ctx16):
     assert rep["n_windows"] == counts.size
     assert rep["max_occ"] == counts.max() and rep["min_nonzero_occ"] == counts.min()
     assert rep["rows_padded"] >= n and rep["padding_factor"] >= 1.0
+
+
+# ----------------------------------------------------------------------------- block backward (§8f next-4)
+
+def _fwap_tensors(blob, d, dff):
+    v = np.frombuffer(blob[16:], np.float32)
+    sizes = [3 * d * d, 3 * d, d * d, d, d, d, d, d, dff * d, dff, d * dff, d]
+    out, o = [], 0
+    for n in sizes:
+        out.append(v[o:o + n])
+        o += n
+    return out
+
+
+@pytest.mark.parametrize("d,h,dff,G,ng", [(32, 4, 64, 8, 4), (128, 8, 256, 69, 3), (16, 2, 32, 1, 5), (64, 4, 96, 33, 2)])
+def test_block_backward_vs_reference(ctx32, d, h, dff, G, ng):
+    """fwa_block_backward (kernels.hpp:660-765) on the GPU vs the compiled reference: the
+    input gradient and all twelve parameter gradients (normwise rel err <= 1e-4, fp32)."""
+    if not O.have_ref():
+        pytest.skip("reference oracle not built")
+    cfg = F.FwaConfig(d_model=d, n_heads=h, d_ff=dff, group_size=G, n_blocks=1)
+    rec = F.init_backbone_params(cfg, d + G)
+    # non-trivial norms / biases so every gradient path is exercised
+    v = np.frombuffer(rec[16:], np.float32).copy()
+    v += 0.05 * np.random.default_rng(G).normal(size=v.shape).astype(np.float32)
+    rec = rec[:16] + v.tobytes()
+    rng = np.random.default_rng(d * 7 + G)
+    rows = ng * G
+    f = rng.normal(size=(rows, d)).astype(np.float32)
+    pe = (0.3 * rng.normal(size=(rows, d))).astype(np.float32)
+    go = rng.normal(size=(rows, d)).astype(np.float32)
+    gf, gr = ctx32.fwa_block_backward(f, pe, rec, ng, go)
+    wf, wr = O.ref_block_backward(f, pe, ng, rec, go)
+    assert O.max_rel_err(gf, wf) <= 1e-4
+    assert gr[:16] == wr[:16]
+    for i, (a, b) in enumerate(zip(_fwap_tensors(gr, d, dff), _fwap_tensors(wr, d, dff))):
+        assert O.max_rel_err(a, b) <= 1e-4, i
