@@ -560,7 +560,7 @@ def run_split_scene(args, F, ctx, cfg, dev, stream, rank, world, dist, flush):
     device time per scene, max over ranks (strong scaling: total work fixed)."""
     import torch
 
-    from paper_2301_08739_b200.split import DeviceRunner, split_forward
+    from paper_2301_08739_b200.split import DeviceRunner, split_forward, split_forward_a2a
     ps = F.make_pillars(F.SCENES["F250"], 42)  # replicated on every rank
     n = ps.size()
     d_coords = torch.from_numpy(ps.coords).to(dev)
@@ -572,11 +572,23 @@ def run_split_scene(args, F, ctx, cfg, dev, stream, rank, world, dist, flush):
         else:
             dst.copy_(src)
 
+    def all_to_all(dst, src, dst_counts, src_counts):
+        if dist:
+            dist.all_to_all_single(dst, src, dst_counts, src_counts)
+        else:
+            dst.copy_(src)
+
     def alloc(rows):
         return torch.empty((rows, cfg.d_model), dtype=torch.float32, device=dev)
 
+    # all-to-all of only the needed rows when there are peers; one rank has nothing to exchange
+    exchange = args.split_exchange or ("a2a" if world > 1 else "allgather")
+
     def one():
         runner = DeviceRunner(ctx, d_coords, d_feats, cfg)
+        if exchange == "a2a":
+            return split_forward_a2a(runner, cfg.n_blocks, cfg.group_size, world, rank, all_gather, all_to_all,
+                                     alloc)
         return split_forward(runner, cfg.n_blocks, cfg.group_size, world, rank, all_gather, alloc)
 
     steps = max(3, args.steps // 5)
@@ -598,10 +610,15 @@ def run_split_scene(args, F, ctx, cfg, dev, stream, rank, world, dist, flush):
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t[0]) / steps
-    return {"workload": "F250 scene (255,066 pillars), 8 blocks, group-range split, all-gather per block",
+    if exchange == "a2a":
+        how = ("NCCL all_to_all_single of only the rows each rank needs for its next group range "
+               "(~K/P x 128 fp32 rows per rank per block; all-gather after the last block)")
+    else:
+        how = "NCCL all_gather_into_tensor of each block's K x 128 fp32 rows"
+    return {"workload": "F250 scene (255,066 pillars), 8 blocks, group-range split across the ranks",
             "pillars": n, "kept": int(out.shape[0]), "ms_per_scene": ms, "pillars_per_s": n / (ms / 1e3),
-            "exchange": "NCCL all_gather_into_tensor of each block's K x 128 fp32 rows" if dist
-            else "single rank (no exchange)", "scaling": "strong", "steps": steps}
+            "exchange": how if dist else f"single rank ({exchange} exchange path, no peers)",
+            "scaling": "strong", "steps": steps}
 
 
 def main():
@@ -612,6 +629,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-split", action="store_true", help="skip the config-4 split-scene measurement")
+    ap.add_argument("--split-exchange", default=None, choices=["a2a", "allgather"],
+                    help="config-4 exchange between blocks (default: a2a with peers, allgather alone)")
     ap.add_argument("--no-batch", action="store_true", help="skip the config-3 64-frame batch measurement")
     ap.add_argument("--no-points", action="store_true", help="skip the GPU pillarization measurement")
     ap.add_argument("--no-equal-window", action="store_true", help="skip the equal-window baseline comparison")

@@ -181,6 +181,12 @@ int fwa_b200_split_begin(fwa_b200_ctx* ctx, const double* d_coords, int64_t n, c
 int fwa_b200_split_block(fwa_b200_ctx* ctx, int block, int64_t group_begin, int64_t group_end,
                          const float* d_x, float* d_y);
 int fwa_b200_split_scatter(fwa_b200_ctx* ctx, int block, const float* d_y, float* d_dst);
+/* block's window-sort order (K pillar ids, host buffer): lets the ranks derive, from the
+ * replicated schedule, exactly which rows each peer needs for the next block (the
+ * all-to-all exchange of split.py) */
+int fwa_b200_split_plan(fwa_b200_ctx* ctx, int block, int32_t* ids_out);
+/* the same into a device buffer (K int32), enqueued on the context stream */
+int fwa_b200_split_plan_device(fwa_b200_ctx* ctx, int block, int32_t* d_ids_out);
 
 /* flatten::sort (minimum slice): host coords in, host permutation out. */
 int fwa_b200_sort_plan(fwa_b200_ctx* ctx, const double* coords, int64_t n, double w_x,

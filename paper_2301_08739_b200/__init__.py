@@ -36,7 +36,8 @@ EXPORTS = [
     "fwa_b200_backbone_forward", "fwa_b200_backbone_forward_batch",
     "fwa_b200_backbone_forward_device", "fwa_b200_sort_plan", "fwa_b200_block_forward",
     "fwa_b200_positional_embedding", "fwa_b200_positional_embedding_f16", "fwa_b200_generate_pillars", "fwa_b200_init_params",
-    "fwa_b200_split_begin", "fwa_b200_split_block", "fwa_b200_split_scatter",
+    "fwa_b200_split_begin", "fwa_b200_split_block", "fwa_b200_split_scatter", "fwa_b200_split_plan",
+    "fwa_b200_split_plan_device",
     "fwa_b200_pillarize", "fwa_b200_pillarize_device", "fwa_b200_generate_points", "fwa_b200_pillar_params",
     "fwa_b200_row_checksums", "fwa_b200_fnv1a64", "fwa_b200_equal_window_forward", "fwa_b200_block_backward",
 ]
@@ -149,6 +150,8 @@ def lib():
         L.fwa_b200_split_begin.argtypes = [vp, vp, i64, C.POINTER(_Cfg), C.POINTER(i64)]
         L.fwa_b200_split_block.argtypes = [vp, C.c_int, i64, i64, vp, vp]
         L.fwa_b200_split_scatter.argtypes = [vp, C.c_int, vp, vp]
+        L.fwa_b200_split_plan.argtypes = [vp, C.c_int, vp]
+        L.fwa_b200_split_plan_device.argtypes = [vp, C.c_int, vp]
         L.fwa_b200_init_params.argtypes = [C.POINTER(_Cfg), C.c_uint64, vp, C.c_size_t]
         L.fwa_b200_init_params.restype = i64
         L.fwa_b200_pillarize.argtypes = [vp, vp, vp, i64, i32, C.c_double, vp, vp, i32, vp, vp, C.POINTER(i64)]
@@ -437,6 +440,14 @@ class Context:
 
     def split_scatter(self, b: int, d_y: int, d_dst: int):
         self._check(lib().fwa_b200_split_scatter(self._h, b, C.c_void_p(d_y), C.c_void_p(d_dst)))
+
+    def split_plan_device(self, b: int, d_ids: int):
+        self._check(lib().fwa_b200_split_plan_device(self._h, b, C.c_void_p(d_ids)))
+
+    def split_plan(self, b: int, K: int) -> np.ndarray:
+        ids = np.empty(K, np.int32)
+        self._check(lib().fwa_b200_split_plan(self._h, b, _ptr(ids)))
+        return ids
 
     def sync_check(self):
         """Wait for the stream; raise deferred device-side errors of forward_device."""

@@ -604,10 +604,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         ++hs;
 
         // ---- 2. QKV epilogue (all 8 heads) + attention
-        mbar_wait(bQKV, ph);
-        fence_after_sync();
-        FTR(tb + 3);
-        if (threadIdx.x == 0) {  // this CTA's attention m-tiles: (first query row, part end, key ext row)
+        // this CTA's attention m-tiles (first query row, part end, key ext row), built while
+        // the QKV MMA runs; read after the epilogue's __syncthreads
+        if (threadIdx.x == 0) {
             int n = 0;
             if (nloc > 0)
                 for (int gg = urow0 / G; gg * G < urow0 + nloc; ++gg) {
@@ -617,6 +616,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
                 }
             sTab[16].x = n;
         }
+        mbar_wait(bQKV, ph);
+        fence_after_sync();
+        FTR(tb + 3);
         // every thread: heads 2cq, 2cq+1 of its row -> Q (R_A, in place of O), K|V rows
 #pragma unroll 1
         for (int hh = 0; hh < 2; ++hh) {

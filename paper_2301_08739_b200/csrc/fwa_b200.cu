@@ -1260,6 +1260,27 @@ int fwa_b200_split_block(fwa_b200_ctx* c, int block, int64_t group_begin, int64_
     });
 }
 
+int fwa_b200_split_plan(fwa_b200_ctx* c, int block, int32_t* ids_out) {
+    return guarded(c, [&] {
+        auto& sp = c->split;
+        if (!sp.ready) throw FwaError{FWA_ERR_CONTRACT, "fwa_b200_split_begin first"};
+        if (block < 0 || block >= sp.cfg.n_blocks || !ids_out) throw FwaError{FWA_ERR_SHAPE, "split: bad block"};
+        CUDA_OK(cudaMemcpyAsync(ids_out, sp.idx + sp.K * (block % 4), static_cast<size_t>(sp.K) * 4,
+                                cudaMemcpyDeviceToHost, c->stream));
+        CUDA_OK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int fwa_b200_split_plan_device(fwa_b200_ctx* c, int block, int32_t* d_ids_out) {
+    return guarded(c, [&] {
+        auto& sp = c->split;
+        if (!sp.ready) throw FwaError{FWA_ERR_CONTRACT, "fwa_b200_split_begin first"};
+        if (block < 0 || block >= sp.cfg.n_blocks || !d_ids_out) throw FwaError{FWA_ERR_SHAPE, "split: bad block"};
+        CUDA_OK(cudaMemcpyAsync(d_ids_out, sp.idx + sp.K * (block % 4), static_cast<size_t>(sp.K) * 4,
+                                cudaMemcpyDeviceToDevice, c->stream));
+    });
+}
+
 int fwa_b200_split_scatter(fwa_b200_ctx* c, int block, const float* d_y, float* d_dst) {
     return guarded(c, [&] {
         auto& sp = c->split;

@@ -7,6 +7,10 @@ the sorted-order output rows (NCCL over NVLink on GPUs), and every rank scatters
 to pillar-id order (`fwa_b200_split_scatter`) because block b+1 re-sorts with another
 (axis, shift) and needs rows from everywhere (flatten.hpp:150-161, backbone.hpp:215-317).
 
+`split_forward_a2a` replaces the all-gather between blocks by an all-to-all of only the
+rows each rank needs for its next group range (the per-peer lists follow from the
+replicated schedule), cutting the exchange from K rows to about K/P rows per rank.
+
 `split_forward` is written against a small runner interface so the identical host logic
 runs on the GPU (`DeviceRunner`, the C ABI) and in the CPU gloo tests (an oracle runner).
 """
@@ -14,6 +18,8 @@ from __future__ import annotations
 
 import math
 from typing import Callable, List, Tuple
+
+import numpy as np
 
 
 def partition_groups(n_groups: int, world: int) -> Tuple[List[Tuple[int, int]], int]:
@@ -43,6 +49,70 @@ def split_forward(runner, n_blocks: int, group_size: int, world: int, rank: int,
         dst = runner.out_buffer() if b == n_blocks - 1 else runner.x_buffer()
         runner.scatter(b, y_all, dst)
         x = dst
+    return runner.out_buffer()
+
+
+def exchange_tables(idx_b, idx_next, ranges, per, group_size, rank, world):
+    """Block b -> b+1 exchange of `split_forward_a2a`: which of this rank's block-b output
+    rows each peer needs for its block-(b+1) group range, and which pillar ids this rank
+    receives from each peer.  Both sides list rows in the RECEIVER's block-(b+1) order, so
+    the tables agree without communication (every rank holds the same schedule).
+    Returns (send_local (concatenated local row indices), send_counts, recv_ids
+    (concatenated pillar ids), recv_counts)."""
+    import numpy as np
+    idx_b = np.asarray(idx_b, np.int64)
+    idx_next = np.asarray(idx_next, np.int64)
+    chunk = per * group_size
+    pos_b = np.empty(int(max(idx_b.max(), idx_next.max())) + 1, np.int64)
+    pos_b[idx_b] = np.arange(idx_b.size)
+    send_local, send_counts, recv_ids, recv_counts = [], [], [], []
+    for s in range(world):
+        a, b = ranges[s][0] * group_size, ranges[s][1] * group_size
+        need = idx_next[a:b]                       # peer s's block-(b+1) rows, in its order
+        src = pos_b[need] // chunk                 # their owners in block b
+        sel = src == rank
+        send_local.append(pos_b[need[sel]] - rank * chunk)
+        send_counts.append(int(sel.sum()))
+        if s == rank:
+            for r in range(world):
+                m = src == r
+                recv_ids.append(need[m])
+                recv_counts.append(int(m.sum()))
+    return (np.concatenate(send_local), send_counts, np.concatenate(recv_ids), recv_counts)
+
+
+def split_forward_a2a(runner, n_blocks: int, group_size: int, world: int, rank: int,
+                      all_gather: Callable, all_to_all: Callable, alloc: Callable):
+    """`split_forward` with an all-to-all of only the rows each rank needs next (about
+    K/P rows in and out per rank and block instead of the all-gather's K): the ranks
+    derive the per-peer row lists from the replicated schedule (runner.plan(b): block b's
+    window-sort order).  The final block still all-gathers (the output is replicated).
+    all_to_all(dst, src, dst_counts, src_counts): rows, rank-ordered chunks (NCCL / gloo
+    all_to_all_single).  runner additionally: pack(y_local, local_idx) -> rows,
+    unpack(rows, pillar_ids, dst) (dst[pillar_ids] = rows), alloc_rows(n)."""
+    K = runner.begin()
+    n_groups = K // group_size
+    ranges, per = partition_groups(n_groups, world)
+    g0, g1 = ranges[rank]
+    y_local = alloc(per * group_size)
+    y_all = alloc(world * per * group_size)
+    if hasattr(runner, "exchange_tables_all"):
+        tables = runner.exchange_tables_all(n_blocks, ranges, per, group_size, rank, world)
+    else:
+        tables = [runner.exchange_tables(b, ranges, per, group_size, rank, world) for b in range(n_blocks - 1)]
+    x = runner.input()
+    for b in range(n_blocks):
+        runner.block(b, g0, g1, x, y_local)
+        if b == n_blocks - 1:
+            all_gather(y_all, y_local)
+            runner.scatter(b, y_all, runner.out_buffer())
+            break
+        send_local, send_counts, recv_ids, recv_counts = tables[b]
+        send = runner.pack(y_local, send_local)
+        recv = runner.alloc_rows(int(sum(recv_counts)))
+        all_to_all(recv, send, recv_counts, send_counts)
+        x = runner.x_buffer()
+        runner.unpack(recv, recv_ids, x)
     return runner.out_buffer()
 
 
@@ -76,6 +146,53 @@ class DeviceRunner:
 
     def block(self, b, g0, g1, x, y_local):
         self.ctx.split_block(b, g0, g1, x.data_ptr(), y_local.data_ptr())
+        self.ctx.sync_check()  # the library's stream -> torch's (collectives, index ops)
 
     def scatter(self, b, y_all, dst):
         self.ctx.split_scatter(b, y_all.data_ptr(), dst.data_ptr())
+
+    # ---- all-to-all exchange (split_forward_a2a)
+    def exchange_tables_all(self, n_blocks, ranges, per, group_size, rank, world):
+        """exchange_tables() of every block transition on the device (torch ops over the
+        schedule's window-sort orders, once per scene); the per-peer counts (the
+        collective's splits) come back to the host in ONE copy."""
+        import torch
+        K = self.out.shape[0]
+        plans = []
+        for i in range(n_blocks):
+            p32 = torch.empty(K, dtype=torch.int32, device=self.dev)
+            self.ctx.split_plan_device(i, p32.data_ptr())
+            plans.append(p32)
+        self.ctx.sync_check()
+        plans = [p.long() for p in plans]
+        chunk = per * group_size
+        a, e = ranges[rank][0] * group_size, ranges[rank][1] * group_size
+        pos_b = torch.empty(int(self.n), dtype=torch.long, device=self.dev)
+        ar = torch.arange(K, device=self.dev)
+        out, counts = [], []
+        for b in range(n_blocks - 1):
+            idx_b, idx_n = plans[b], plans[b + 1]
+            pos_b[idx_b] = ar
+            pos_n = pos_b[idx_n]                      # block-b position of block-(b+1) row k
+            src = torch.div(pos_n, chunk, rounding_mode="floor")
+            send_k = torch.nonzero(src == rank).squeeze(1)  # ascending k = grouped by destination
+            send_local = pos_n[send_k] - rank * chunk
+            my_src = src[a:e]
+            recv_ids = idx_n[a:e][torch.argsort(my_src, stable=True)]
+            counts.append(torch.bincount(torch.div(send_k, chunk, rounding_mode="floor"), minlength=world))
+            counts.append(torch.bincount(my_src, minlength=world))
+            out.append((send_local, recv_ids))
+        c = torch.stack(counts).cpu().tolist() if counts else []
+        return [(sl, c[2 * i], ri, c[2 * i + 1]) for i, (sl, ri) in enumerate(out)]
+
+    def pack(self, y_local, local_idx):
+        return y_local.index_select(0, local_idx)
+
+    def unpack(self, rows, pillar_ids, dst):
+        import torch
+        dst.index_copy_(0, pillar_ids, rows)
+        torch.cuda.synchronize(self.dev)  # before the next block kernel (library stream) reads dst
+
+    def alloc_rows(self, n):
+        import torch
+        return torch.empty((n, self.cfg.d_model), dtype=torch.float32, device=self.dev)

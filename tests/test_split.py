@@ -12,7 +12,7 @@ import pytest
 
 import oracle as O
 import paper_2301_08739_b200 as F
-from paper_2301_08739_b200.split import partition_groups, split_forward
+from paper_2301_08739_b200.split import exchange_tables, partition_groups, split_forward, split_forward_a2a
 
 D, H, DFF, G, NB = 16, 4, 32, 16, 4
 
@@ -70,12 +70,49 @@ class OracleRunner:
         pos = self.out_pos if b == NB - 1 else self.idx[b]
         dst[pos] = y_all[:len(pos)]
 
+    # all-to-all exchange (split_forward_a2a)
+    def exchange_tables(self, b, ranges, per, group_size, rank, world):
+        return exchange_tables(self.idx[b], self.idx[b + 1], ranges, per, group_size, rank, world)
+
+    def pack(self, y_local, local_idx):
+        return y_local[local_idx]
+
+    def unpack(self, rows, pillar_ids, dst):
+        dst[pillar_ids] = rows
+
+    def alloc_rows(self, n):
+        return np.zeros((n, D), np.float32)
+
 
 def test_partition_groups():
     r, per = partition_groups(10, 3)
     assert r == [(0, 4), (4, 8), (8, 10)] and per == 4
     r, per = partition_groups(2, 4)
     assert r == [(0, 1), (1, 2), (2, 2), (2, 2)] and per == 1
+
+
+def _gloo_worker_a2a(rank, world, port, coords, feats, blob, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        def all_gather(dst, src):
+            parts = [torch.empty_like(torch.from_numpy(src)) for _ in range(world)]
+            dist.all_gather(parts, torch.from_numpy(src))
+            dst[:] = torch.cat(parts).numpy()
+
+        def all_to_all(dst, src, dst_counts, src_counts):
+            out = torch.from_numpy(dst)
+            dist.all_to_all_single(out, torch.from_numpy(np.ascontiguousarray(src)), dst_counts, src_counts)
+
+        runner = OracleRunner(coords, feats, blob)
+        out = split_forward_a2a(runner, NB, G, world, rank, all_gather, all_to_all,
+                                lambda rows: np.zeros((rows, D), np.float32))
+        q.put((rank, out.copy()))
+    finally:
+        dist.destroy_process_group()
 
 
 def _gloo_worker(rank, world, port, coords, feats, blob, q):
@@ -118,6 +155,50 @@ def test_split_gloo_world2_equals_single_process():
         assert np.array_equal(outs[r], want["features"]), r
 
 
+def test_exchange_tables_cover_every_next_block_row():
+    """Every rank receives exactly its next-block rows, each from its block-b owner."""
+    rng = np.random.default_rng(3)
+    K, world = 37 * G, 3
+    kept = rng.permutation(K + 5)[:K]  # both blocks order the same kept pillars
+    idx_b, idx_n = rng.permutation(kept), rng.permutation(kept)
+    ranges, per = partition_groups(K // G, world)
+    tabs = [exchange_tables(idx_b, idx_n, ranges, per, G, r, world) for r in range(world)]
+    for s_ in range(world):
+        a, b = ranges[s_][0] * G, ranges[s_][1] * G
+        got = np.concatenate([tabs[s_][2]])
+        assert sorted(got.tolist()) == sorted(idx_n[a:b].tolist())
+        # what s_ receives from r is what r sends to s_, in the same order
+        off = np.cumsum([0] + tabs[s_][3])
+        for r in range(world):
+            s_off = np.cumsum([0] + tabs[r][1])
+            sent_local = tabs[r][0][s_off[s_]:s_off[s_ + 1]]
+            sent_ids = idx_b[sent_local + r * per * G]
+            assert np.array_equal(sent_ids, got[off[r]:off[r + 1]])
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_split_a2a_gloo_equals_single_process(world):
+    """The all-to-all exchange (only the rows each rank needs next) == the single-process
+    oracle backbone, bit for bit, at world sizes 2 and 3 over gloo."""
+    import torch.multiprocessing as mp
+    coords, feats = _scene()
+    cfg = O.make_cfg(d_model=D, n_heads=H, d_ff=DFF, group_size=G, n_blocks=NB)
+    blob = F.init_backbone_params(F.FwaConfig(d_model=D, n_heads=H, d_ff=DFF, group_size=G, n_blocks=NB), 5)
+    want = O.port_run_backbone(coords, feats, cfg, blob)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 30500 + (os.getpid() % 1000) + world
+    procs = [ctx.Process(target=_gloo_worker_a2a, args=(r, world, port, coords, feats, blob, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert all(p.exitcode == 0 for p in procs)
+    for r in range(world):
+        assert np.array_equal(outs[r], want["features"]), r
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("world", [1, 3])
 def test_split_device_runner_equals_run_backbone(world):
@@ -148,5 +229,27 @@ def test_split_device_runner_equals_run_backbone(world):
         runner.scatter(b, y_all, dst)
         x = dst
     out = runner.out_buffer()
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), want.features)
+
+
+@pytest.mark.gpu
+def test_split_a2a_device_runner_equals_run_backbone():
+    """The all-to-all exchange with the C-ABI runner (plan / pack / unpack on the device),
+    one rank: bitwise equal to run_backbone."""
+    import torch
+    from paper_2301_08739_b200.split import DeviceRunner
+    ps = F.make_pillars(F.SCENES["F10"], 42)
+    cfg = F.FwaConfig()
+    ctx = F.Context(0, precision="bf16")
+    ctx.load_params(cfg, F.init_backbone_params(cfg, 42))
+    want = ctx.run_backbone(F.PillarSet(ps.coords, ps.features.astype(np.float32)), cfg)
+    dev = torch.device("cuda", 0)
+    runner = DeviceRunner(ctx, torch.from_numpy(ps.coords).to(dev),
+                          torch.from_numpy(ps.features.astype(np.float32)).to(dev), cfg)
+    out = split_forward_a2a(runner, cfg.n_blocks, cfg.group_size, 1, 0,
+                            lambda dst, src: dst.copy_(src),
+                            lambda dst, src, dc, sc: dst.copy_(src),
+                            lambda rows: torch.zeros((rows, 128), dtype=torch.float32, device=dev))
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy(), want.features)
