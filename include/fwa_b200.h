@@ -9,6 +9,9 @@
  *   fwa_b200_backbone_forward_device the same, inputs/outputs already in HBM
  *   fwa_b200_backbone_forward_batch  the same over F independent frames (one model), frame-
  *                                    parallel inside one GPU (BASELINE config 3)
+ *   fwa_b200_backbone_forward_frames a stream of frames (one run_backbone each), PCIe copies
+ *                                    pipelined with compute; = run_backbone per frame
+ *                                    include/fwa/backbone.hpp:159-325
  *   fwa_b200_sort_plan               fwa::flatten::sort(coords, WindowSpec)  include/fwa/flatten.hpp:97-120
  *   fwa_b200_block_forward           fwa::kernels::fwa_block_forward(f, pe, params, n_groups)
  *                                    include/fwa/kernels.hpp:636-650
@@ -152,6 +155,15 @@ int fwa_b200_backbone_forward_batch(fwa_b200_ctx* ctx, const double* coords, con
                                     int feats_is_f64, const int64_t* frame_offsets, int n_frames,
                                     const fwa_config_t* cfg, fwa_output_t* out,
                                     int64_t* kept_per_frame);
+
+/* A stream of F independent frames in separate host buffers, each exactly one
+ * fwa_b200_backbone_forward (same outputs, same errors), pipelined: frame f+1's inputs
+ * cross PCIe and frame f-1's outputs come back while frame f computes.  outs[f] as for
+ * fwa_b200_backbone_forward (block_perms must be NULL): a caller's loop of
+ * fwa::backbone::run_backbone over a frame sequence (include/fwa/backbone.hpp:159-325). */
+int fwa_b200_backbone_forward_frames(fwa_b200_ctx* ctx, int n_frames, const double* const* coords,
+                                     const void* const* feats, int feats_is_f64, const int64_t* n,
+                                     const fwa_config_t* cfg, fwa_output_t* outs);
 
 /* Device-resident variant (inputs already in HBM, outputs written to HBM,
  * enqueued on the context stream without a trailing host sync).  d_feats is

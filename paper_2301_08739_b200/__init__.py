@@ -33,7 +33,7 @@ EXPORTS = [
     "fwa_b200_ctx_create", "fwa_b200_ctx_destroy", "fwa_b200_last_error", "fwa_b200_set_precision",
     "fwa_b200_kernel_launches", "fwa_b200_fast_path", "fwa_b200_load_params",
     "fwa_b200_set_profiling", "fwa_b200_get_profile", "fwa_b200_sync_check",
-    "fwa_b200_backbone_forward", "fwa_b200_backbone_forward_batch",
+    "fwa_b200_backbone_forward", "fwa_b200_backbone_forward_batch", "fwa_b200_backbone_forward_frames",
     "fwa_b200_backbone_forward_device", "fwa_b200_sort_plan", "fwa_b200_block_forward",
     "fwa_b200_positional_embedding", "fwa_b200_positional_embedding_f16", "fwa_b200_generate_pillars", "fwa_b200_init_params",
     "fwa_b200_split_begin", "fwa_b200_split_block", "fwa_b200_split_scatter", "fwa_b200_split_plan",
@@ -136,6 +136,8 @@ def lib():
         L.fwa_b200_load_params.argtypes = [vp, C.POINTER(_Cfg), vp, C.c_size_t]
         L.fwa_b200_backbone_forward.argtypes = [vp, vp, vp, C.c_int, i64, C.POINTER(_Cfg),
                                                 C.POINTER(_Out)]
+        L.fwa_b200_backbone_forward_frames.argtypes = [vp, C.c_int, vp, vp, C.c_int, vp, C.POINTER(_Cfg),
+                                                       C.POINTER(_Out)]
         L.fwa_b200_backbone_forward_batch.argtypes = [vp, vp, vp, C.c_int, vp, C.c_int,
                                                       C.POINTER(_Cfg), C.POINTER(_Out), vp]
         L.fwa_b200_backbone_forward_device.argtypes = [vp, vp, vp, vp, C.c_int, C.POINTER(_Cfg),
@@ -393,6 +395,56 @@ class Context:
                                                     C.c_void_p(feats_ptr), int(feats_is_f64), n,
                                                     C.byref(c), C.byref(o)))
         return int(o.n_kept), (int(o.cache_computed), int(o.cache_hits))
+
+    def run_frames(self, frames: Sequence[PillarSet], cfg: FwaConfig) -> List[BackboneOutput]:
+        """run_backbone over a sequence of frames with the PCIe copies pipelined against
+        the compute (fwa_b200_backbone_forward_frames); output i == run_backbone(frames[i])."""
+        keep, bufs = [], []
+        f64 = None
+        for ps in frames:
+            coords = np.ascontiguousarray(ps.coords, np.float64)
+            is64 = ps.features.dtype == np.float64
+            if f64 is None:
+                f64 = is64
+            elif f64 != is64:
+                raise ShapeError("frames: mixed feature dtypes")
+            feats = np.ascontiguousarray(ps.features, np.float64 if is64 else np.float32)
+            n = coords.shape[0]
+            if feats.shape != (n, cfg.d_model):
+                raise ShapeError("backbone: pillar width != d_model and no input projection")
+            out_f = np.empty((n, cfg.d_model), np.float32)
+            kept = np.empty(max(n, 1), np.int32)
+            dropped = np.empty(max(n, 1), np.int32)
+            dpb = np.zeros(cfg.n_blocks, np.int32)
+            keep.append((coords, feats, out_f, kept, dropped, dpb))
+        ptrs = [(k[0].ctypes.data, k[1].ctypes.data, k[0].shape[0], k[2].ctypes.data, k[3].ctypes.data,
+                 k[4].ctypes.data, k[5].ctypes.data) for k in keep]
+        stats = self.run_frames_ptrs(ptrs, bool(f64), cfg)
+        outs = []
+        for (coords, _, out_f, kept, dropped, dpb), (k, cache) in zip(keep, stats):
+            dropped_lists, w = [], 0
+            for b in range(cfg.n_blocks):
+                dropped_lists.append(dropped[w:w + dpb[b]].copy())
+                w += int(dpb[b])
+            outs.append(BackboneOutput(features=out_f[:k], coords=coords[kept[:k]], kept_indices=kept[:k],
+                                       dropped_indices=dropped_lists,
+                                       stats=RunStats(CacheStats(*cache), [int(x) for x in dpb]),
+                                       n_input=coords.shape[0], block_perms=None))
+        return outs
+
+    def run_frames_ptrs(self, frames, feats_is_f64: bool, cfg: FwaConfig):
+        """fwa_b200_backbone_forward_frames on caller-owned HOST buffers: `frames` is a list
+        of (coords_ptr, feats_ptr, n, out_features_ptr, kept_ptr, dropped_ptr,
+        dropped_per_block_ptr) (0 = not wanted).  Returns [(n_kept, (computed, hits))]."""
+        F = len(frames)
+        cp = (C.c_void_p * F)(*[f[0] for f in frames])
+        fp = (C.c_void_p * F)(*[f[1] for f in frames])
+        ns = (C.c_int64 * F)(*[int(f[2]) for f in frames])
+        outs = (_Out * F)(*[_Out(f[3], f[4] or None, f[5] or None, f[6] or None, None, 0, 0, 0) for f in frames])
+        c = cfg.c()
+        self._check(lib().fwa_b200_backbone_forward_frames(self._h, F, cp, fp, int(feats_is_f64), ns, C.byref(c),
+                                                           outs))
+        return [(int(o.n_kept), (int(o.cache_computed), int(o.cache_hits))) for o in outs]
 
     def run_batch(self, coords: np.ndarray, feats: np.ndarray, frame_offsets: Sequence[int],
                   cfg: FwaConfig):

@@ -68,12 +68,17 @@ struct fwa_b200_ctx {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaStream_t copy = nullptr;             // host API: feature H2D overlaps the schedule
     cudaEvent_t ev_copy = nullptr, ev_feats = nullptr;
+    cudaStream_t d2h = nullptr;              // pipelined frames: outputs back while the next computes
+    cudaEvent_t fr_ev[8] = {};
+    int* h_fr_flags = nullptr;               // pinned, 2 ints per frame
+    size_t h_fr_cap = 0;
     int* d_flag = nullptr;     // [0] non-finite input, [1] window-bin capacity overflow
     int* h_flag = nullptr;     // pinned, 2 ints
     bool exact_bins = false;   // set for one call after an overflow: host-sized bins
     uint64_t ws_epoch = 0;     // bumped whenever a workspace buffer moves
     const void* hist_clean = nullptr;  // sync-free histogram buffer known to be zeroed
     const void* ticket_clean = nullptr;  // key-kernel CTA ticket known to be zeroed
+    const void* amm_clean = nullptr;     // key-kernel running min/max known to be armed
     uint64_t params_version = 0;
     // CUDA graph of the device-resident forward (replayed while its key is unchanged)
     struct GraphKey {
@@ -455,14 +460,21 @@ int32_t* sort_specs(fwa_b200_ctx* c, const double* d_coords, int64_t ntot, int n
         uint32_t* d_nbins = ws<uint32_t>(c, "nbins", 4);
         unsigned* ticket = ws<unsigned>(c, "sort_ticket", 4);  // [0] key kernel, [1] bin scan
         uint32_t* large = ws<uint32_t>(c, "large_bins", static_cast<size_t>(kBinCap) + 1);
-        if (ticket != c->ticket_clean) {  // fresh buffer: zero once; the key kernel resets it
+        long long* amm = ws<long long>(c, "sort_amm", 16);
+        if (ticket != c->ticket_clean || amm != c->amm_clean) {  // fresh buffers: arm once; the kernels re-arm
             CUDA_OK(cudaMemsetAsync(ticket, 0, 4 * sizeof(unsigned), st));
+            long long init[16];
+            for (int i = 0; i < 16; ++i) init[i] = (i & 1) ? LLONG_MIN : LLONG_MAX;
+            CUDA_OK(cudaMemcpyAsync(amm, init, sizeof(init), cudaMemcpyHostToDevice, st));
+            CUDA_OK(cudaStreamSynchronize(st));  // `init` is a stack buffer
             c->ticket_clean = ticket;
+            c->amm_clean = amm;
         }
         BinsFuse fz;
         fz.ticket = ticket; fz.nf = nf; fz.cap = kBinCap; fz.mm = mm; fz.specs = d_sb; fz.d_nbins = d_nbins;
         fz.overflow = c->d_flag + 1;
         fz.large = large;
+        fz.amm = amm;
         launch_sort_keys(d_coords, ntot, n_specs, w_x, w_y, win, loc, partials, st, &c->launches, fz);
         check_launch();
         uint32_t* hist = ws<uint32_t>(c, "hist", static_cast<size_t>(kBinCap));
@@ -946,6 +958,118 @@ void forward_host(fwa_b200_ctx* c, const double* coords, const void* feats, int 
     }
 }
 
+// Pipelined host-buffer forward over independent frames, each exactly one run_backbone
+// (backbone.hpp:159-325, called once per frame of a sequence): while frame f
+// computes on the context stream, frame f+1's inputs cross PCIe on the copy stream and
+// frame f-1's outputs come back on the d2h stream (two slots of device buffers).  Device-
+// side conditions are collected per frame and raised after the pipeline drains; a frame
+// whose window range overflowed the sync-free bin histogram is re-run alone.
+void forward_frames(fwa_b200_ctx* c, int F, const double* const* coords, const void* const* feats, int f64,
+                    const int64_t* n, const fwa_config_t* cfg, fwa_output_t* outs) {
+    validate_cfg(cfg);
+    require_params(c, cfg);
+    if (F < 1 || !coords || !feats || !n || !outs) throw FwaError{FWA_ERR_SHAPE, "need >= 1 frame"};
+    const int d = cfg->d_model, G = cfg->group_size;
+    int64_t nmax = 0;
+    for (int f = 0; f < F; ++f) {
+        if (!coords[f] || !feats[f] || !outs[f].features) throw FwaError{FWA_ERR_SHAPE, "null buffer"};
+        if (outs[f].block_perms) throw FwaError{FWA_ERR_CONTRACT, "block_perms: use fwa_b200_backbone_forward"};
+        if (n[f] < G)  // backbone.hpp:218-222, before anything is enqueued
+            throw FwaError{FWA_ERR_NUMERIC, "backbone: block 0 has " + std::to_string(n[f]) +
+                                                " pillars, fewer than group size " + std::to_string(G) +
+                                                "; refusing to emit empty output"};
+        nmax = std::max(nmax, n[f]);
+    }
+    const size_t esz = f64 ? 8 : 4, nm = static_cast<size_t>(nmax);
+    // every slot buffer sized up front: a workspace move frees memory copies are using
+    double* in_c[2];
+    void* in_f[2];
+    float* o_f[2];
+    int32_t* o_ids[2];  // [kept (K) | dropped (< G)]
+    static const char* kNames[2][4] = {{"fr_c0", "fr_f0", "fr_o0", "fr_i0"}, {"fr_c1", "fr_f1", "fr_o1", "fr_i1"}};
+    for (int s = 0; s < 2; ++s) {
+        in_c[s] = ws<double>(c, kNames[s][0], 2 * nm);
+        in_f[s] = ws<uint8_t>(c, kNames[s][1], nm * d * esz);
+        o_f[s] = ws<float>(c, kNames[s][2], nm * d);
+        o_ids[s] = ws<int32_t>(c, kNames[s][3], nm + G);
+    }
+    ws<float>(c, "X", nm * d);
+    if (!c->d2h) CUDA_OK(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+    for (auto* e : {&c->fr_ev[0], &c->fr_ev[1], &c->fr_ev[2], &c->fr_ev[3], &c->fr_ev[4], &c->fr_ev[5],
+                    &c->fr_ev[6], &c->fr_ev[7]})
+        if (!*e) CUDA_OK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    cudaEvent_t* ev_inc = c->fr_ev;      // [2] coordinates landed
+    cudaEvent_t* ev_inf = c->fr_ev + 2;  // [2] features landed
+    cudaEvent_t* ev_done = c->fr_ev + 4; // [2] frame computed (inputs free, outputs ready)
+    cudaEvent_t* ev_out = c->fr_ev + 6;  // [2] outputs copied back (slot free)
+    if (c->h_fr_cap < static_cast<size_t>(F)) {
+        if (c->h_fr_flags) CUDA_OK(cudaFreeHost(c->h_fr_flags));
+        c->h_fr_flags = nullptr;
+        CUDA_OK(cudaMallocHost(&c->h_fr_flags, 2 * sizeof(int) * static_cast<size_t>(F)));
+        c->h_fr_cap = static_cast<size_t>(F);
+    }
+    cudaStream_t st = c->stream;
+    CUDA_OK(cudaEventRecord(c->ev_copy, st));  // earlier users of the slot buffers are done
+    CUDA_OK(cudaStreamWaitEvent(c->copy, c->ev_copy, 0));
+    CUDA_OK(cudaStreamWaitEvent(c->d2h, c->ev_copy, 0));
+    std::vector<int64_t> K(static_cast<size_t>(F)), nd(static_cast<size_t>(F));
+    for (int f = 0; f < F; ++f) {
+        const int s = f & 1;
+        const size_t nf = static_cast<size_t>(n[f]);
+        if (f >= 2) CUDA_OK(cudaStreamWaitEvent(c->copy, ev_done[s], 0));
+        CUDA_OK(cudaMemcpyAsync(in_c[s], coords[f], nf * 16, cudaMemcpyHostToDevice, c->copy));
+        CUDA_OK(cudaEventRecord(ev_inc[s], c->copy));
+        CUDA_OK(cudaMemcpyAsync(in_f[s], feats[f], nf * d * esz, cudaMemcpyHostToDevice, c->copy));
+        CUDA_OK(cudaEventRecord(ev_inf[s], c->copy));
+        CUDA_OK(cudaStreamWaitEvent(st, ev_inc[s], 0));
+        if (f >= 2) CUDA_OK(cudaStreamWaitEvent(st, ev_out[s], 0));
+        Schedule S;
+        const int64_t off[2] = {0, n[f]};
+        host_frames(off, 1, G, S);
+        forward_device(c, in_c[s], f64 ? nullptr : static_cast<const float*>(in_f[s]),
+                       f64 ? static_cast<const double*>(in_f[s]) : nullptr, cfg, S, o_f[s], nullptr, nullptr,
+                       ev_inf[s]);
+        K[f] = S.K;
+        nd[f] = S.n_drop;
+        CUDA_OK(cudaMemcpyAsync(o_ids[s], S.kept_ids, static_cast<size_t>(S.K) * 4, cudaMemcpyDeviceToDevice, st));
+        if (S.n_drop)
+            CUDA_OK(cudaMemcpyAsync(o_ids[s] + S.K, S.dropped_ids, static_cast<size_t>(S.n_drop) * 4,
+                                    cudaMemcpyDeviceToDevice, st));
+        CUDA_OK(cudaMemcpyAsync(c->h_fr_flags + 2 * f, c->d_flag, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+        CUDA_OK(cudaEventRecord(ev_done[s], st));
+        CUDA_OK(cudaStreamWaitEvent(c->d2h, ev_done[s], 0));
+        fwa_output_t& o = outs[f];
+        CUDA_OK(cudaMemcpyAsync(o.features, o_f[s], static_cast<size_t>(S.K) * d * 4, cudaMemcpyDeviceToHost,
+                                c->d2h));
+        if (o.kept_indices)
+            CUDA_OK(cudaMemcpyAsync(o.kept_indices, o_ids[s], static_cast<size_t>(S.K) * 4, cudaMemcpyDeviceToHost,
+                                    c->d2h));
+        if (o.dropped_ids && S.n_drop)
+            CUDA_OK(cudaMemcpyAsync(o.dropped_ids, o_ids[s] + S.K, static_cast<size_t>(S.n_drop) * 4,
+                                    cudaMemcpyDeviceToHost, c->d2h));
+        CUDA_OK(cudaEventRecord(ev_out[s], c->d2h));
+    }
+    CUDA_OK(cudaEventRecord(c->ev_copy, c->d2h));
+    CUDA_OK(cudaStreamWaitEvent(st, c->ev_copy, 0));  // later work on the context stream follows
+    CUDA_OK(cudaStreamSynchronize(c->d2h));
+    CUDA_OK(cudaStreamSynchronize(st));
+    for (int f = 0; f < F; ++f) {
+        if (c->h_fr_flags[2 * f + 1]) {  // window-bin capacity overflow: this frame alone, exact bins
+            const int64_t off[2] = {0, n[f]};
+            forward_host(c, coords[f], feats[f], f64, off, 1, cfg, &outs[f], nullptr);
+            continue;
+        }
+        if (c->h_fr_flags[2 * f]) throw FwaError{FWA_ERR_NUMERIC, "group_attention: non-finite input"};
+        fwa_output_t& o = outs[f];
+        o.n_kept = K[static_cast<size_t>(f)];
+        std::vector<int64_t> drops;
+        cache_stats(cfg->n_blocks, n[f], G, &o.cache_computed, &o.cache_hits, &drops);
+        if (o.dropped_per_block)
+            for (int b = 0; b < cfg->n_blocks; ++b)
+                o.dropped_per_block[b] = static_cast<int32_t>(b == 0 ? nd[static_cast<size_t>(f)] : 0);
+    }
+}
+
 } // namespace
 
 extern "C" {
@@ -1017,6 +1141,13 @@ void fwa_b200_ctx_destroy(fwa_b200_ctx* c) {
         cudaStreamDestroy(c->copy);
     }
     if (c->ev_copy) cudaEventDestroy(c->ev_copy);
+    if (c->d2h) {
+        cudaStreamSynchronize(c->d2h);
+        cudaStreamDestroy(c->d2h);
+    }
+    for (auto e : c->fr_ev)
+        if (e) cudaEventDestroy(e);
+    if (c->h_fr_flags) cudaFreeHost(c->h_fr_flags);
     if (c->ev_feats) cudaEventDestroy(c->ev_feats);
     if (c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
@@ -1118,6 +1249,12 @@ int fwa_b200_backbone_forward_batch(fwa_b200_ctx* c, const double* coords, const
         if (frame_offsets[0] != 0) throw FwaError{FWA_ERR_SHAPE, "frame_offsets[0] must be 0"};
         forward_host(c, coords, feats, f64, frame_offsets, n_frames, cfg, out, kept_per_frame);
     });
+}
+
+int fwa_b200_backbone_forward_frames(fwa_b200_ctx* c, int n_frames, const double* const* coords,
+                                     const void* const* feats, int f64, const int64_t* n,
+                                     const fwa_config_t* cfg, fwa_output_t* outs) {
+    return guarded(c, [&] { forward_frames(c, n_frames, coords, feats, f64, n, cfg, outs); });
 }
 
 int fwa_b200_backbone_forward_device(fwa_b200_ctx* c, const double* d_coords, const float* d_feats,

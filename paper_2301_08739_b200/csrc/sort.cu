@@ -146,10 +146,14 @@ FWA_DEVINL long long wmax(long long v) {
 __device__ void bins_setup_cta(const long long* __restrict__ partials, int64_t n_part, int n_specs, int nf,
                                long long cap, long long* __restrict__ mm, SpecBins* __restrict__ specs,
                                uint32_t* __restrict__ d_nbins, int* __restrict__ overflow);
+__device__ void bins_from_minmax(const long long (*fin)[4], int n_specs, int nf, long long cap,
+                                 SpecBins* __restrict__ specs, uint32_t* __restrict__ d_nbins,
+                                 int* __restrict__ overflow);
 
 // One thread per (spec, point).  flatten.hpp:49-69, op by op, round-to-nearest.
-// With `fz`, the last CTA to finish (atomic ticket) also reduces the min/max partials
-// into the bin layout (bins_setup_cta) -- no separate launch.
+// With `fz`, every CTA folds its window range into a running min/max with 64-bit atomics
+// and the last CTA to finish (atomic ticket) turns it into the bin layout -- no separate
+// launch and no partials pass.
 __global__ void __launch_bounds__(256) k_sort_keys(const double* __restrict__ coords, int64_t ntot,
                                                    int n_specs, double w_x, double w_y,
                                                    long long* __restrict__ win,
@@ -196,8 +200,15 @@ __global__ void __launch_bounds__(256) k_sort_keys(const double* __restrict__ co
         long long v = red[q][0];
         for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
             v = (q & 1) ? (red[q][w] > v ? red[q][w] : v) : (red[q][w] < v ? red[q][w] : v);
-        // per-CTA partial [spec][cta][4]; reduced by the last CTA or k_bins_setup
-        minmax[(static_cast<int64_t>(s) * gridDim.x + blockIdx.x) * 4 + q] = v;
+        if (fz.ticket) {
+            // fused: folded into the spec's running min / max (64-bit atomics); the last
+            // CTA turns the 4 x n_specs values into the bin layout and re-arms them
+            if (q & 1) atomicMax(fz.amm + 4 * s + q, v);
+            else atomicMin(fz.amm + 4 * s + q, v);
+        } else {
+            // per-CTA partial [spec][cta][4], reduced by k_bins_setup
+            minmax[(static_cast<int64_t>(s) * gridDim.x + blockIdx.x) * 4 + q] = v;
+        }
     }
     if (fz.ticket) {
         __shared__ bool last;
@@ -205,13 +216,17 @@ __global__ void __launch_bounds__(256) k_sort_keys(const double* __restrict__ co
         __syncthreads();
         if (threadIdx.x == 0) last = atomicAdd(fz.ticket, 1u) == gridDim.x * gridDim.y - 1;
         __syncthreads();
-        if (last) {
+        if (last && threadIdx.x == 0) {
             __threadfence();
-            bins_setup_cta(minmax, gridDim.x, n_specs, fz.nf, fz.cap, fz.mm, fz.specs, fz.d_nbins, fz.overflow);
-            if (threadIdx.x == 0) {
-                *fz.ticket = 0u;  // self-resetting for the next call
-                if (fz.large) *fz.large = 0u;  // the bin sort's oversize-bin queue
+            long long fin[4][4];
+            for (int t = 0; t < 4 * n_specs; ++t) {
+                fin[t >> 2][t & 3] = __ldcg(fz.amm + t);
+                fz.mm[t] = fin[t >> 2][t & 3];
+                fz.amm[t] = (t & 1) ? LLONG_MIN : LLONG_MAX;  // re-armed for the next call
             }
+            bins_from_minmax(fin, n_specs, fz.nf, fz.cap, fz.specs, fz.d_nbins, fz.overflow);
+            *fz.ticket = 0u;               // self-resetting for the next call
+            if (fz.large) *fz.large = 0u;  // the bin sort's oversize-bin queue
         }
     }
 }
@@ -725,6 +740,13 @@ __device__ void bins_setup_cta(const long long* __restrict__ partials, int64_t n
     }
     __syncthreads();
     if (threadIdx.x != 0) return;
+    bins_from_minmax(fin, n_specs, nf, cap, specs, d_nbins, overflow);
+}
+
+// one thread: window ranges -> dense bin layout of every spec + the device-side bin count
+__device__ void bins_from_minmax(const long long (*fin)[4], int n_specs, int nf, long long cap,
+                                 SpecBins* __restrict__ specs, uint32_t* __restrict__ d_nbins,
+                                 int* __restrict__ overflow) {
     long long nbins = 0;
     bool bad = false;
     for (int s = 0; s < n_specs; ++s) {
@@ -770,52 +792,56 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tiles_dev(const uint32_t*
                                                                    uint32_t* __restrict__ tile_sums,
                                                                    unsigned* __restrict__ ticket) {
     const int64_t n = *d_n;
-    if (static_cast<int64_t>(blockIdx.x) * kScanTile >= n) return;
     __shared__ uint32_t warp_tot[32];
-    const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
-    uint32_t v[kScanItems];
-    uint32_t run = 0;
-#pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-        const int64_t i = base + k;
-        const uint32_t t = i < n ? in[i] : 0u;
-        v[k] = run;
-        run += t;
-    }
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint32_t x = run;
+    // persistent: CTA b scans tiles b, b + gridDim.x, ...
+    for (int64_t tile = blockIdx.x; tile * kScanTile < n; tile += gridDim.x) {
+        const int64_t base = tile * kScanTile + threadIdx.x * kScanItems;
+        uint32_t v[kScanItems];
+        uint32_t run = 0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) warp_tot[wid] = x;
-    __syncthreads();
-    if (wid == 0) {
-        uint32_t w = warp_tot[lane];
+        for (int k = 0; k < kScanItems; ++k) {
+            const int64_t i = base + k;
+            const uint32_t t = i < n ? in[i] : 0u;
+            v[k] = run;
+            run += t;
+        }
+        uint32_t x = run;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-            if (lane >= o) w += y;
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
         }
-        warp_tot[lane] = w;
-    }
-    __syncthreads();
-    const uint32_t excl = x - run + (wid ? warp_tot[wid - 1] : 0u);
+        if (lane == 31) warp_tot[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            uint32_t w = warp_tot[lane];
 #pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-        const int64_t i = base + k;
-        if (i < n) {
-            out[i] = v[k] + excl;
-            cursor[i] = v[k] + excl;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += y;
+            }
+            warp_tot[lane] = w;
         }
+        __syncthreads();
+        const uint32_t excl = x - run + (wid ? warp_tot[wid - 1] : 0u);
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) {
+            const int64_t i = base + k;
+            if (i < n) {
+                out[i] = v[k] + excl;
+                cursor[i] = v[k] + excl;
+            }
+        }
+        if (threadIdx.x == kScanThreads - 1) tile_sums[tile] = excl + run;
+        __syncthreads();  // warp_tot reused by the next tile
     }
-    if (threadIdx.x == kScanThreads - 1) tile_sums[blockIdx.x] = excl + run;
     const unsigned tiles = static_cast<unsigned>((n + kScanTile - 1) / kScanTile);
+    if (tiles == 0) return;  // capacity overflow: nothing binned
     __shared__ bool last;
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == tiles - 1;
+    if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
     __syncthreads();
     if (!last) return;
     __threadfence();
@@ -859,7 +885,8 @@ void launch_scan_bins_dev(const uint32_t* hist, uint32_t* bin_start, uint32_t* c
                           long long cap, uint32_t* tile_sums, unsigned* ticket, cudaStream_t s,
                           int64_t* launches) {
     const unsigned tiles = static_cast<unsigned>((cap + kScanTile - 1) / kScanTile);
-    k_scan_tiles_dev<<<tiles, kScanThreads, 0, s>>>(hist, bin_start, cursor, d_nbins, tile_sums, ticket);
+    const unsigned grid = tiles < static_cast<unsigned>(kNumSMs) ? tiles : static_cast<unsigned>(kNumSMs);
+    k_scan_tiles_dev<<<grid, kScanThreads, 0, s>>>(hist, bin_start, cursor, d_nbins, tile_sums, ticket);
     *launches += 1;
 }
 

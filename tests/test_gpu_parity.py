@@ -280,6 +280,36 @@ def test_batch_equals_per_frame(prec, ctx32, ctx16):
         assert np.array_equal(res["features"][ko[i]:ko[i + 1]], r.features)
 
 
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_frame_stream_equals_per_frame(prec, ctx32, ctx16):
+    """Pipelined frame stream (fwa_b200_backbone_forward_frames): every frame bitwise
+    equal to its own run_backbone -- growing and shrinking frame sizes (workspace moves),
+    f64 features, a wide frame that overflows the sync-free bin histogram (re-run alone)."""
+    ctx = ctx32 if prec == "fp32" else ctx16
+    cfg = F.FwaConfig(n_blocks=4)
+    ctx.load_params(cfg, F.init_backbone_params(cfg, 42))
+    frames = [F.make_pillars(F.SCENES[s], seed) for s, seed in
+              (("F10", 1), ("F30", 2), ("F10", 3), ("PINNED", 4), ("F30", 5))]
+    rng = np.random.default_rng(9)
+    frames.insert(2, F.PillarSet(rng.uniform(-5000, 5000, size=(3000, 2)), rng.normal(size=(3000, 128))))
+    outs = ctx.run_frames(frames, cfg)
+    assert len(outs) == len(frames)
+    for ps, o in zip(frames, outs):
+        r = ctx.run_backbone(ps, cfg)
+        assert np.array_equal(o.kept_indices, r.kept_indices)
+        assert np.array_equal(o.features, r.features)
+        assert [d.tolist() for d in o.dropped_indices] == [d.tolist() for d in r.dropped_indices]
+        assert (o.stats.cache.computed, o.stats.cache.hits) == (r.stats.cache.computed, r.stats.cache.hits)
+        assert o.stats.dropped_per_block == r.stats.dropped_per_block
+    small = F.PillarSet(np.zeros((5, 2)), np.zeros((5, 128)))
+    with pytest.raises(F.NumericError):  # backbone.hpp:218-222, raised before any frame runs
+        ctx.run_frames([frames[0], small], cfg)
+    bad = F.PillarSet(frames[0].coords, frames[0].features.copy())
+    bad.features[7, 3] = np.inf
+    with pytest.raises(F.NumericError):  # kernels.hpp:460-461
+        ctx.run_frames([frames[1], bad], cfg)
+
+
 def test_errors_mirror_reference(ctx32):
     cfg = F.FwaConfig(d_model=16, n_heads=4, d_ff=32, group_size=8, n_blocks=2)
     blob = F.init_backbone_params(cfg, 1)
