@@ -27,7 +27,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfwa_b200.so")
+LIB_PATH = os.environ.get("FWA_B200_LIB") or os.path.join(HERE, "libfwa_b200.so")  # override: A/B builds
 
 EXPORTS = [
     "fwa_b200_ctx_create", "fwa_b200_ctx_destroy", "fwa_b200_last_error", "fwa_b200_set_precision",

@@ -33,13 +33,18 @@
 // mbarrier (remote arrive from rank 1); commits are multicast to both CTAs.
 //
 // Attention: tasks = (head, 16-query tile of one group part); QK^T and PV on
-// mma.sync.m16n8k16 (bf16, fp32 accumulate); max-subtracted softmax in fp32 (ex2 on the
-// SFU, P rounded to bf16 as the PV operand); the row sums come out of the PV MMA (an
-// all-ones B fragment), so they are the sums of exactly the P values multiplied with V.
+// mma.sync.m16n8k16 (bf16, fp32 accumulate); softmax in fp32 with Q pre-scaled so that
+// S is the base-2 exponent: P = 2^S straight from the QK^T accumulators, no row-max pass
+// (shift invariance; a task whose row sums leave [2^-64, 2^64] is re-run with the max
+// shift), ex2 on the SFU with a quarter of the tiles on an FMA-pipe cubic, P rounded to
+// bf16 as the PV operand; the row sums come out of the PV MMA (an all-ones B fragment),
+// so they are the sums of exactly the P values multiplied with V.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.h"
@@ -58,6 +63,9 @@ constexpr int kOffRA = 98304;                   // 32 KB SW128 image
 constexpr int kOffW2 = 131072;                  // 32 KB; lent to the K/V rows during attention
 constexpr int kOffKV = kOffW2;                  // K|V rows of all 8 heads over W2 + R_X
 constexpr int kOffRX = kOffW2 + 32768;          // 163840: LN1 staging / GELU-a image
+constexpr int kOffXS = kOffKV;                  // next unit's fp32 x rows (128 x 528 B),
+                                                // landed while this unit's output is scattered
+constexpr int kXSPitch = 528;                   // 512 B + 16: conflict-free row and column reads
 constexpr int kRXBytes = 60928;
 constexpr int kKVPitch = 528;                   // 8 x 32 B K | 8 x 32 B V | 16 B pad
 constexpr int kKVRows = (32768 + kRXBytes) / kKVPitch;  // 177
@@ -67,6 +75,7 @@ constexpr int kOffBars = kOffVec + kVecFloats * 4;    // 229376
 constexpr int kOffTab = kOffBars + 128;               // m-tile table: 16 x int4 + count
 constexpr int kSmem = kOffTab + 512 + 1024;           // + base-alignment slack
 static_assert(kSmem <= 232448, "shared memory budget");
+static_assert(kOffXS + 128 * kXSPitch <= kOffVec, "XS fits the K/V region");
 
 // ---------------------------------------------------------------- cluster / pair PTX
 FWA_DEVINL uint32_t cluster_rank() {
@@ -199,22 +208,51 @@ FWA_DEVINL float ex2f(float x) {
     return y;
 }
 FWA_DEVINL uint32_t ex2_bf16x2(float lo, float hi) { return pack_bf16x2(ex2f(lo), ex2f(hi)); }
+// 2^x for x <= 0 on the FMA pipe (the SFU is the attention's bottleneck): round-to-
+// nearest split x = j + f (f in [-1/2, 1/2]), near-minimax cubic for 2^f (rel err 1.0e-4,
+// below the bf16 rounding of P), j added to the exponent field; x < -126 gives ~0
+FWA_DEVINL float ex2_poly(float x) {
+    x = fminf(fmaxf(x, -126.0f), 64.5f);  // beyond 2^64 the caller re-runs with the max shift
+    const float t = __fadd_rn(x, 12582912.0f);  // 1.5 * 2^23: j in the low mantissa bits
+    const float f = __fsub_rn(x, __fsub_rn(t, 12582912.0f));
+    const float p = fmaf(fmaf(fmaf(0.05500852f, f, 0.24221109f), f, 0.693283f), f, 1.0f);
+    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+FWA_DEVINL uint32_t ex2_poly_bf16x2(float lo, float hi) { return pack_bf16x2(ex2_poly(lo), ex2_poly(hi)); }
 // byte offset of element (row, col) in a 128-row K-major SW128 bf16 image
 FWA_DEVINL uint32_t img_off(int row, int col) {
     return static_cast<uint32_t>((col >> 6) * 16384 + row * 128 + ((((col & 63) >> 3) ^ (row & 7)) << 4) +
                                  (col & 7) * 2);
 }
 
-// One attention task: head `head`, query rows [m0, m0+16)
-// of a group whose keys are the extended rows [ke0, ke0 + G); rows >= qend are computed
-// but not stored.  Q is read from and O written to the R_A image (same cells).
-template <int NT, int GC>
-FWA_DEVINL void attn_task(uint32_t sRA, uint32_t sKV, uint8_t* pRA, int head, int m0, int qend, int ke0,
-                          int G_rt) {
+// Q is stored pre-scaled by (1/sqrt(16)) * log2(e), so S = Q K^T is the softmax exponent
+// in base 2.
+constexpr float kScaleLog2 = 0.25f * 1.4426950408889634f;
+FWA_DEVINL float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// One attention task: head `head`, query rows [m0, m0+16) of a group whose keys are the
+// extended rows [ke0, ke0 + G); rows >= qend are computed but not stored.  Q is read from
+// and O written to the R_A image (same cells).
+//   kMax = false (fast pass): P = 2^S without the row-max shift (softmax is shift
+//     invariant; the shift only guards the range) -- no max reduction, the exponent is
+//     the MMA output itself.  Returns false, storing nothing, when a row sum leaves
+//     [1/lmax, lmax] (lmax = 2^64: possible overflow / underflow); the caller then re-runs
+//     the task
+//   kMax = true: the reference's max-subtracted softmax (kernels.hpp:252-265, 533).
+template <int NT, int GC, bool kMax>
+FWA_DEVINL bool attn_task(uint32_t sRA, uint32_t sKV, uint8_t* pRA, int head, int m0, int qend, int ke0,
+                          int G_rt, float lmax) {
     const int G = GC > 0 ? GC : G_rt;
     const int lane = threadIdx.x & 31;
     const int g = lane >> 2, t4 = lane & 3;
-    constexpr float kScaleLog2 = 0.25f * 1.4426950408889634f;  // (1/sqrt(16)) * log2(e)
+#ifndef FWA_POLY_MASK
+#define FWA_POLY_MASK 2
+#endif
+    constexpr int kPolyMask = FWA_POLY_MASK;  // nt & 3 in the mask: 0b0010 -> nt = 1, 5 at G = 69
     const int nt_live = (G + 7) >> 3;
     uint32_t a0, a1, a2, a3;
     {
@@ -236,35 +274,59 @@ FWA_DEVINL void attn_task(uint32_t sRA, uint32_t sKV, uint8_t* pRA, int head, in
         ldsm_x4_t(sKV + vrow * kKVPitch + 256 + head * 32 + (lane >> 4) * 16, vb[kt][0], vb[kt][1], vb[kt][2],
                   vb[kt][3]);
     }
+    // keys >= G: V := 0 (their rows may hold any bits -- P = 0 times NaN is NaN)
+#pragma unroll
+    for (int kt = 0; kt < NT / 2; ++kt) {
+        if (kt * 16 + 16 > G) {
+            const int k0 = kt * 16 + 2 * t4, k1 = k0 + 8;
+            const uint32_t m0 = (k0 < G ? 0xFFFFu : 0u) | (k0 + 1 < G ? 0xFFFF0000u : 0u);
+            const uint32_t m1 = (k1 < G ? 0xFFFFu : 0u) | (k1 + 1 < G ? 0xFFFF0000u : 0u);
+            vb[kt][0] &= m0;
+            vb[kt][2] &= m0;
+            vb[kt][1] &= m1;
+            vb[kt][3] &= m1;
+        }
+    }
     float s[NT][4];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
         s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
         if (nt < nt_live) mma16816(s[nt], a0, a1, a2, a3, kb[nt][0], kb[nt][1]);
-    }
-    float m0v = -INFINITY, m1v = -INFINITY;
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-        if (nt >= nt_live) continue;
-        if (nt * 8 + 8 > G) {
+        if (nt < nt_live && nt * 8 + 8 > G) {
             const int col = nt * 8 + 2 * t4;
             if (col >= G) { s[nt][0] = -INFINITY; s[nt][2] = -INFINITY; }
             if (col + 1 >= G) { s[nt][1] = -INFINITY; s[nt][3] = -INFINITY; }
         }
-        m0v = fmaxf(m0v, fmaxf(s[nt][0], s[nt][1]));
-        m1v = fmaxf(m1v, fmaxf(s[nt][2], s[nt][3]));
     }
-    m0v = fmaxf(m0v, __shfl_xor_sync(0xffffffffu, m0v, 1));
-    m0v = fmaxf(m0v, __shfl_xor_sync(0xffffffffu, m0v, 2));
-    m1v = fmaxf(m1v, __shfl_xor_sync(0xffffffffu, m1v, 1));
-    m1v = fmaxf(m1v, __shfl_xor_sync(0xffffffffu, m1v, 2));
-    const float mb0 = m0v * kScaleLog2, mb1 = m1v * kScaleLog2;
+    float mb0 = 0.f, mb1 = 0.f;
+    if (kMax) {
+        float m0v = -INFINITY, m1v = -INFINITY;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            if (nt >= nt_live) continue;
+            m0v = fmaxf(m0v, fmaxf(s[nt][0], s[nt][1]));
+            m1v = fmaxf(m1v, fmaxf(s[nt][2], s[nt][3]));
+        }
+        m0v = fmaxf(m0v, __shfl_xor_sync(0xffffffffu, m0v, 1));
+        m0v = fmaxf(m0v, __shfl_xor_sync(0xffffffffu, m0v, 2));
+        m1v = fmaxf(m1v, __shfl_xor_sync(0xffffffffu, m1v, 1));
+        m1v = fmaxf(m1v, __shfl_xor_sync(0xffffffffu, m1v, 2));
+        mb0 = m0v;
+        mb1 = m1v;
+    }
     uint32_t p[NT][2];  // bf16x2: [0] row g, [1] row g + 8
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
         if (nt < nt_live) {
-            p[nt][0] = ex2_bf16x2(fmaf(s[nt][0], kScaleLog2, -mb0), fmaf(s[nt][1], kScaleLog2, -mb0));
-            p[nt][1] = ex2_bf16x2(fmaf(s[nt][2], kScaleLog2, -mb1), fmaf(s[nt][3], kScaleLog2, -mb1));
+            const float e0 = kMax ? s[nt][0] - mb0 : s[nt][0], e1 = kMax ? s[nt][1] - mb0 : s[nt][1];
+            const float e2 = kMax ? s[nt][2] - mb1 : s[nt][2], e3 = kMax ? s[nt][3] - mb1 : s[nt][3];
+            if (((kPolyMask >> (nt & 3)) & 1) && nt * 8 + 8 <= G) {  // some exponentials on the FMA pipe
+                p[nt][0] = ex2_poly_bf16x2(e0, e1);
+                p[nt][1] = ex2_poly_bf16x2(e2, e3);
+            } else {
+                p[nt][0] = ex2_bf16x2(e0, e1);
+                p[nt][1] = ex2_bf16x2(e2, e3);
+            }
         } else {
             p[nt][0] = p[nt][1] = 0u;
         }
@@ -279,7 +341,12 @@ FWA_DEVINL void attn_task(uint32_t sRA, uint32_t sKV, uint8_t* pRA, int head, in
         mma16816(o[1], p[2 * kt][0], p[2 * kt][1], p[2 * kt + 1][0], p[2 * kt + 1][1], vb[kt][2], vb[kt][3]);
         mma16816(l, p[2 * kt][0], p[2 * kt][1], p[2 * kt + 1][0], p[2 * kt + 1][1], kOnes, kOnes);
     }
-    const float i0 = 1.0f / l[0], i1 = 1.0f / l[2];
+    if (!kMax) {
+        const float lmin = rcp_approx(lmax);
+        const bool ok = l[0] >= lmin && l[0] <= lmax && l[2] >= lmin && l[2] <= lmax;
+        if (__any_sync(0xffffffffu, !ok)) return false;
+    }
+    const float i0 = rcp_approx(l[0]), i1 = rcp_approx(l[2]);
     const int r0 = m0 + g, r1 = r0 + 8;
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
@@ -287,6 +354,7 @@ FWA_DEVINL void attn_task(uint32_t sRA, uint32_t sKV, uint8_t* pRA, int head, in
         if (r0 < qend) *reinterpret_cast<uint32_t*>(pRA + img_off(r0, col)) = pack_bf16x2(o[nt][0] * i0, o[nt][1] * i0);
         if (r1 < qend) *reinterpret_cast<uint32_t*>(pRA + img_off(r1, col)) = pack_bf16x2(o[nt][2] * i1, o[nt][3] * i1);
     }
+    return true;
 }
 
 // ---------------------------------------------------------------- row I/O
@@ -363,6 +431,13 @@ FWA_DEVINL void ln1_row_to_image(const float (&v)[16], const uint2 (&ph)[4], boo
 
 // f32 row staging: row r (512 B) chunk c (16 B) at r*512 + ((c ^ (r & 7)) * 16)
 FWA_DEVINL uint32_t stage_off(int r, int c) { return static_cast<uint32_t>(r * 512 + ((c ^ (r & 7)) << 4)); }
+// 16 B global -> shared without registers (LDGSTS); src_bytes 0 zero-fills
+FWA_DEVINL void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+FWA_DEVINL void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+FWA_DEVINL void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 
 // reference exact-erf GELU (dense.hpp:67-72); see tc.cu gelu_fast for the error budget
 FWA_DEVINL float tanh_approx(float x) {
@@ -395,6 +470,7 @@ struct FusedArgs {
     const float *ln1_g, *ln1_b;
     int* nonfinite;
     unsigned long long* trace;  // FWA_B200_TRACE: 64 SM-clock slots per CTA (phase boundaries)
+    float lmax;                 // attention fast pass: row sums beyond [1/lmax, lmax] re-run shifted
 };
 
 #define FTR(k)                                                                                  \
@@ -464,11 +540,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
     }
     __syncthreads();  // barrier inits before the weight TMA uses bW
     if (threadIdx.x == 0) {
-        mbar_arrive_expect_tx(bW, kWBytes);
+        // W_qkv | W_out | W1' (W2 arrives after each unit's attention, into the K/V slot)
+        mbar_arrive_expect_tx(bW, 98304);
         const uint8_t* src = a.wpair + static_cast<size_t>(rank) * kWBytes;
 #pragma unroll
         for (int c = 0; c < 3; ++c) bulk_g2s(sW + c * 32768, src + c * 32768, 32768, bW);
-        bulk_g2s(smem + kOffW2, src + 98304, 32768, bW);
     }
     fence_before_sync();
     cluster_sync_all();  // peer barriers initialised, TMEM allocated in both CTAs
@@ -513,10 +589,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
             if (r < nl) ids[hf] = idx ? idx[ub + r0 + r] : static_cast<int>(ub + r0 + r);
         }
     };
+    // f32 path: unit u's x rows straight into XS (cp.async, zero-filled past the CTA's
+    // rows) -- issued one unit ahead, while the previous unit's output is scattered
+    // f32 path: unit u's x rows straight into XS (cp.async, no registers; rows past the
+    // CTA's zero-filled) -- issued one unit ahead, before the previous unit's output is
+    // scattered.  (One 512 B TMA bulk copy per row costs more to issue: ~10 cycles each.)
+    uint8_t* xs = smem + kOffXS;
+    const uint32_t sXS = smem_u32(xs);
+    auto prefetch_x = [&](int u, const int (&ids)[2]) {
+        if constexpr (!kF64) {
+            if (u >= a.n_units) return;
+            const int64_t ub = static_cast<int64_t>(u) * R;
+            const int ur = static_cast<int>(a.rows - ub < R ? a.rows - ub : R);
+            const int sp = a.split < ur ? a.split : ur;
+            const int nl = rank ? ur - sp : sp;
+            const int sub = lane & 7;
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                const int r = hf * 64 + warp * 4 + (lane >> 3);
+                const float* src = a.x + static_cast<int64_t>(ids[hf]) * 128 + 4 * sub;
+                const uint32_t dst = sXS + r * kXSPitch + sub * 16, nb = r < nl ? 16u : 0u;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) cp_async16(dst + 128 * i, src + 32 * i, nb);
+            }
+            cp_async_commit();
+        }
+    };
     griddep_wait();  // x / PE / ids come from earlier kernels
     FTRG(60);
     int gid[2], sid[2];
     unit_ids(a.ridx, pair, gid);
+    prefetch_x(pair, gid);
     if (threadIdx.x == 0) mbar_wait(bW, 0);
     FTRG(59);
     FTR(0);
@@ -545,7 +648,50 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         //         + LN1 + affine + PE -> bf16 A image (R_A).  The fp32 rows are parked in
         //         TMEM columns [384, 512) (through a 32 KB staging in R_KV, one 64-row half
         //         at a time); the out-proj MMA accumulates onto them (= the residual).
-        {
+        if constexpr (!kF64) {
+            const int sub = lane & 7, rl = lane >> 3;
+            uint2 pe[2][4];
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                const int r = hf * 64 + warp * 4 + rl;
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    pe[hf][i] = r < nloc ? __ldg(reinterpret_cast<const uint2*>(a.pe16 + static_cast<int64_t>(gid[hf]) * 128 +
+                                                                              32 * i + 4 * sub))
+                                         : make_uint2(0u, 0u);
+            }
+            if (a.sidx == a.ridx) {
+                sid[0] = gid[0];
+                sid[1] = gid[1];
+            } else {
+                unit_ids(a.sidx, u, sid);
+            }
+            unit_ids(a.ridx, u + npairs, gid);
+            cp_async_wait_all();
+            __syncthreads();  // every thread's row chunks landed
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                const int r = hf * 64 + warp * 4 + rl;
+                float v[16];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float4 f = *reinterpret_cast<const float4*>(xs + r * kXSPitch + (8 * i + sub) * 16);
+                    v[4 * i] = f.x; v[4 * i + 1] = f.y; v[4 * i + 2] = f.z; v[4 * i + 3] = f.w;
+                }
+                ln1_row_to_image(v, pe[hf], r < nloc, r, sub, sVec + 896, sVec + 1024, pRA, bad);
+                if (hf == 0) FTR(tb + 1);
+            }
+            {  // the residual rows -> TMEM [384, 512)
+                float xr[32];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const float4 f = *reinterpret_cast<const float4*>(xs + row * kXSPitch + (8 * cq + j) * 16);
+                    xr[4 * j] = f.x; xr[4 * j + 1] = f.y; xr[4 * j + 2] = f.z; xr[4 * j + 3] = f.w;
+                }
+                tmem_st32(tmem + lane_off + 384 + c0, xr);
+                tmem_st_wait();
+            }
+        } else {
             const int sub = lane & 7, rl = lane >> 3;
             float v[2][16];
             uint2 pe[2][4];
@@ -636,7 +782,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
                 for (int e = 0; e < 4; ++e) {
                     const int j = 8 * hf + 2 * e;
                     const float* bq = sVec + 16 * h + j;
-                    oq[e] = pack_bf16x2(__uint_as_float(qv[j]) + bq[0], __uint_as_float(qv[j + 1]) + bq[1]);
+                    oq[e] = pack_bf16x2((__uint_as_float(qv[j]) + bq[0]) * kScaleLog2,
+                                        (__uint_as_float(qv[j + 1]) + bq[1]) * kScaleLog2);
                     ok[e] = pack_bf16x2(__uint_as_float(kv[j]) + bq[128], __uint_as_float(kv[j + 1]) + bq[129]);
                     ov[e] = pack_bf16x2(__uint_as_float(vv[j]) + bq[256], __uint_as_float(vv[j + 1]) + bq[257]);
                 }
@@ -678,7 +825,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
 #pragma unroll 1
             for (int t = warp; t < ntasks; t += 16) {
                 const int4 e = sTab[t >> 3];
-                attn_task<NT, GC>(sRA, sKV, pRA, t & 7, e.x, e.y, e.z, G);
+                if (!attn_task<NT, GC, false>(sRA, sKV, pRA, t & 7, e.x, e.y, e.z, G, a.lmax))
+                    attn_task<NT, GC, true>(sRA, sKV, pRA, t & 7, e.x, e.y, e.z, G, a.lmax);
             }
         }
         FTR(tb + 5);
@@ -797,6 +945,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         // ---- 6. out = x1 + (O + b2) -> staged in R_A (two 64-row halves) -> row scatter
         mbar_wait(bO, ph);
         fence_after_sync();
+        prefetch_x(u + npairs, gid);  // FFN2 done: the W2 / K/V / R_X region is free
         FTR(tb + 14);
         {
             uint32_t v[32];
@@ -962,6 +1111,8 @@ void launch_block_fused(const float* x, const double* x64, const __half* pe16, c
     a.n_units = static_cast<int>((n_groups + a.gpu - 1) / a.gpu);
     a.wpair = w.w_pair; a.vec = w.vec; a.ln1_g = w.ln1_g; a.ln1_b = w.ln1_b; a.nonfinite = d_nonfinite;
     a.trace = trace;
+    a.lmax = 0x1p64f;
+    if (const char* e = std::getenv("FWA_B200_ATTN_LMAX")) a.lmax = std::strtof(e, nullptr);  // tests
     const bool f64 = x64 != nullptr;
     switch (kernel_nt(G)) {
         case 10: launch_nt<10, 69>(a, f64, s); break;  // FwaConfig default group size (backbone.hpp:26)

@@ -154,6 +154,27 @@ def test_block_forward_bf16_group_sizes(ctx16, G):
     assert O.max_rel_err(got, want) <= TOL_BF16
 
 
+def test_fused_attention_shifted_fallback(ctx16, monkeypatch):
+    """The fused kernel's attention runs P = 2^S without the row-max shift and re-runs a
+    task with the reference's max-subtracted softmax when a row sum leaves [1/lmax, lmax].
+    Forcing lmax = 2 sends most tasks down the shifted path: both agree with the oracle and
+    with each other (same math, different rounding)."""
+    rng = np.random.default_rng(5)
+    cfg = F.FwaConfig()
+    rec = F.init_backbone_params(cfg, 3)[:16 + 4 * 132480]
+    ng = 12
+    f = rng.normal(size=(ng * 69, 128)).astype(np.float32)
+    pe = (0.3 * rng.normal(size=(ng * 69, 128))).astype(np.float32)
+    fast = ctx16.fwa_block_forward(f, pe, rec, ng)
+    monkeypatch.setenv("FWA_B200_ATTN_LMAX", "2")
+    shifted = ctx16.fwa_block_forward(f, pe, rec, ng)
+    want = O.port_block_forward(f, pe, ng, rec)
+    assert O.max_rel_err(fast, want) <= TOL_BF16
+    assert O.max_rel_err(shifted, want) <= TOL_BF16
+    assert O.max_rel_err(shifted, fast) <= 3e-3
+    assert not np.array_equal(shifted, fast)  # the shifted path did run
+
+
 # ----------------------------------------------------------------------------- backbone
 
 def _check_ints(res, want_kept, want_dropped, want_dpb, want_cache):
