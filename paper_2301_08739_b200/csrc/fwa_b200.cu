@@ -78,7 +78,6 @@ struct fwa_b200_ctx {
     uint64_t ws_epoch = 0;     // bumped whenever a workspace buffer moves
     const void* hist_clean = nullptr;  // sync-free histogram buffer known to be zeroed
     const void* ticket_clean = nullptr;  // key-kernel CTA ticket known to be zeroed
-    const void* amm_clean = nullptr;     // key-kernel running min/max known to be armed
     uint64_t params_version = 0;
     // CUDA graph of the device-resident forward (replayed while its key is unchanged)
     struct GraphKey {
@@ -460,21 +459,14 @@ int32_t* sort_specs(fwa_b200_ctx* c, const double* d_coords, int64_t ntot, int n
         uint32_t* d_nbins = ws<uint32_t>(c, "nbins", 4);
         unsigned* ticket = ws<unsigned>(c, "sort_ticket", 4);  // [0] key kernel, [1] bin scan
         uint32_t* large = ws<uint32_t>(c, "large_bins", static_cast<size_t>(kBinCap) + 1);
-        long long* amm = ws<long long>(c, "sort_amm", 16);
-        if (ticket != c->ticket_clean || amm != c->amm_clean) {  // fresh buffers: arm once; the kernels re-arm
+        if (ticket != c->ticket_clean) {  // fresh buffer: zero once; the key kernel resets it
             CUDA_OK(cudaMemsetAsync(ticket, 0, 4 * sizeof(unsigned), st));
-            long long init[16];
-            for (int i = 0; i < 16; ++i) init[i] = (i & 1) ? LLONG_MIN : LLONG_MAX;
-            CUDA_OK(cudaMemcpyAsync(amm, init, sizeof(init), cudaMemcpyHostToDevice, st));
-            CUDA_OK(cudaStreamSynchronize(st));  // `init` is a stack buffer
             c->ticket_clean = ticket;
-            c->amm_clean = amm;
         }
         BinsFuse fz;
         fz.ticket = ticket; fz.nf = nf; fz.cap = kBinCap; fz.mm = mm; fz.specs = d_sb; fz.d_nbins = d_nbins;
         fz.overflow = c->d_flag + 1;
         fz.large = large;
-        fz.amm = amm;
         launch_sort_keys(d_coords, ntot, n_specs, w_x, w_y, win, loc, partials, st, &c->launches, fz);
         check_launch();
         uint32_t* hist = ws<uint32_t>(c, "hist", static_cast<size_t>(kBinCap));

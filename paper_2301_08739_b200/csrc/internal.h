@@ -42,7 +42,6 @@ struct BinsFuse {
     uint32_t* d_nbins = nullptr;
     int* overflow = nullptr;
     uint32_t* large = nullptr;   // reset to 0 (launch_bin_sort's queue counter)
-    long long* amm = nullptr;    // 16 running min/max (armed to +-inf once; re-armed by the kernel)
 };
 void launch_sort_keys(const double* coords, int64_t ntot, int n_specs, double w_x, double w_y,
                       long long* win, double* loc, long long* partials, cudaStream_t s,

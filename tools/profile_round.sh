@@ -2,12 +2,13 @@
 # The ncu evidence summarised under profiles/ (run on ONE GPU under gpurun; numbers
 # printed under ncu are never bench values):
 #   gpurun --timeout 1500 -- 'bash tools/profile_round.sh'
+# (launch list: python tools/launches.py gpurun_out/launches.csv --frame -1)
 # then here:  python tools/launches.py gpurun_out/launches.csv > profiles/rN_launches_f60.txt
 #             python tools/ncu_summary.py gpurun_out/<rep>.ncu-rep profiles/rN_ncu_<name>.txt ...
 OUT=gpurun_out
 mkdir -p $OUT
 # 1. every launch of the third F60 frame (host API, 8 blocks), warm caches
-ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none -s 40 -c 22 --csv \
+ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none -c 400 --csv \
     --log-file $OUT/launches.csv python tools/prof_f60.py bf16 3 > $OUT/launches.log 2>&1
 # 2. the fused block kernel (block 1 of the second frame), full set + source
 ncu --set full --import-source on --clock-control none -k regex:k_block_fused -s 9 -c 1 \
