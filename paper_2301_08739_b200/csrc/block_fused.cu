@@ -73,7 +73,8 @@ constexpr int kOffVec = kOffRX + kRXBytes;      // 224768
 constexpr int kVecFloats = 1152;  // b_qkv 384 | b_out 128 | b2 128 | b1' 256 | ln1_g 128 | ln1_b 128
 constexpr int kOffBars = kOffVec + kVecFloats * 4;    // 229376
 constexpr int kOffTab = kOffBars + 128;               // m-tile table: 16 x int4 + count
-constexpr int kSmem = kOffTab + 512 + 1024;           // + base-alignment slack
+constexpr int kOffRowId = kOffTab + 512;              // the pending output rows' pillar ids (128)
+constexpr int kSmem = kOffRowId + 512 + 1024;         // + base-alignment slack
 static_assert(kSmem <= 232448, "shared memory budget");
 static_assert(kOffXS + 128 * kXSPitch <= kOffVec, "XS fits the K/V region");
 
@@ -179,6 +180,9 @@ FWA_DEVINL void cta_sync_tc() {
     __syncthreads();
     fence_after_sync();
 }
+// named barrier 1 (barrier 0 is __syncthreads): arrive without waiting / wait for `n` threads
+FWA_DEVINL void bar1_arrive(int n) { asm volatile("bar.arrive 1, %0;" ::"r"(n) : "memory"); }
+FWA_DEVINL void bar1_sync(int n) { asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory"); }
 FWA_DEVINL uint8_t* align1024(uint8_t* p) { return p + ((1024u - (smem_u32(p) & 1023u)) & 1023u); }
 
 // ---------------------------------------------------------------- attention helpers
@@ -504,6 +508,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
     uint8_t* pKV = smem + kOffKV;
     uint8_t* pRX = smem + kOffRX;
     int4* sTab = reinterpret_cast<int4*>(smem + kOffTab);
+    int* sRowId = reinterpret_cast<int*>(smem + kOffRowId);
     float* sVec = reinterpret_cast<float*>(smem + kOffVec);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBars);
     uint64_t* bW = bars;
@@ -623,6 +628,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
     if (threadIdx.x == 0) mbar_wait(bW, 0);
     FTRG(59);
     FTR(0);
+    // The previous unit's output rows (x1 = out) are written while THIS unit's QKV MMA runs:
+    // every warp stages its rows into the K/V region (free until this unit's epilogue, clear
+    // of the rows the peer's halo push may be landing in), warp 0 -- which holds the MMA
+    // issuer in rank 0 -- only arrives on named barrier 1, warps 1..15 store the 512 B rows.
+    float x1[32];
+    int pnloc = 0;
+    bool pend = false;
+    auto stage_out = [&](uint8_t* stg) {
+        if (row < pnloc)
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+                *reinterpret_cast<float4*>(stg + stage_off(row, (c0 + j) >> 2)) =
+                    make_float4(x1[j], x1[j + 1], x1[j + 2], x1[j + 3]);
+    };
+    auto store_out = [&](const uint8_t* stg, int w0, int nw) {  // warps [w0, w0 + nw): rows w - w0 + nw*k
+        for (int r = warp - w0; r < pnloc; r += nw) {
+            const float4 o = *reinterpret_cast<const float4*>(stg + stage_off(r, lane));
+            reinterpret_cast<float4*>(a.x_out + static_cast<int64_t>(sRowId[r]) * 128)[lane] = o;
+        }
+    };
+    // m-tile table (first query row, part end, key ext row) of this CTA's 16-query tiles,
+    // lanes 0..16 of one warp in parallel
+    auto build_table = [&](int nloc_, int urow0_, int ext0_) {
+        if (lane <= 16) {
+            int n = 0;
+            int4 mine = make_int4(0, 0, 0, 0);
+            if (nloc_ > 0)
+                for (int gg = urow0_ / G; gg * G < urow0_ + nloc_; ++gg) {
+                    const int qa = gg * G - urow0_ < 0 ? 0 : gg * G - urow0_;
+                    const int qb = gg * G + G - urow0_ > nloc_ ? nloc_ : gg * G + G - urow0_;
+                    const int nt = (qb - qa + 15) >> 4;
+                    if (lane >= n && lane < n + nt) mine = make_int4(qa + 16 * (lane - n), qb, gg * G - urow0_ + ext0_, 0);
+                    n += nt;
+                }
+            if (lane < 16 && lane < n) sTab[lane] = mine;
+            if (lane == 16) sTab[16].x = n;
+        }
+    };
     int it = 0;
     for (int u = pair; u < a.n_units; u += npairs, ++it) {
         const uint32_t ph = it & 1;
@@ -734,6 +777,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         }
         FTR(tb + 2);
         handshake();
+        uint8_t* stg = pKV;  // the previous unit's output staging: clear of this unit's halo rows
+        if (rank == 1 && strad) stg += (h0 * kKVPitch + 15) & ~15;
+        if (pend) {
+            stage_out(stg);
+            if (warp == 0) bar1_arrive(kThreads);
+        }
         if (leader) {
             leader_wait();
 #pragma unroll
@@ -748,20 +797,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
             mma_commit_pair(bQKV);
         }
         ++hs;
-
-        // ---- 2. QKV epilogue (all 8 heads) + attention
-        // this CTA's attention m-tiles (first query row, part end, key ext row), built while
-        // the QKV MMA runs; read after the epilogue's __syncthreads
-        if (threadIdx.x == 0) {
-            int n = 0;
-            if (nloc > 0)
-                for (int gg = urow0 / G; gg * G < urow0 + nloc; ++gg) {
-                    const int qa = gg * G - urow0 < 0 ? 0 : gg * G - urow0;
-                    const int qb = gg * G + G - urow0 > nloc ? nloc : gg * G + G - urow0;
-                    for (int m0 = qa; m0 < qb; m0 += 16) sTab[n++] = make_int4(m0, qb, gg * G - urow0 + ext0, 0);
-                }
-            sTab[16].x = n;
+        if (pend && warp != 0) {
+            bar1_sync(kThreads);
+            store_out(stg, 1, 15);
         }
+        // ---- 2. QKV epilogue (all 8 heads) + attention
+        // the attention m-tile table, built while the QKV MMA runs; read after the
+        // epilogue's __syncthreads
+        if (warp == 0) build_table(nloc, urow0, ext0);
+        if (pend) __syncthreads();  // staging read before the epilogue's K/V rows overwrite it
         mbar_wait(bQKV, ph);
         fence_after_sync();
         FTR(tb + 3);
@@ -850,7 +894,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
             mma_commit_pair(bP);
         }
         ++hs;
-        float x1[32];
         mbar_wait(bP, ph);
         fence_after_sync();
         FTR(tb + 8);
@@ -954,30 +997,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
 #pragma unroll
             for (int j = 0; j < 32; ++j) x1[j] = x1[j] + (__uint_as_float(v[j]) + sVec[512 + c0 + j]);
         }
-#pragma unroll 1
-        for (int hf = 0; hf < 2; ++hf) {
-            if ((row >> 6) == hf) {
-                const int rr = row & 63;
-#pragma unroll
-                for (int j = 0; j < 32; j += 4)
-                    *reinterpret_cast<float4*>(pRA + stage_off(rr, (c0 + j) >> 2)) =
-                        make_float4(x1[j], x1[j + 1], x1[j + 2], x1[j + 3]);
-            }
-            __syncthreads();
-            {
-                const int rbase = warp * 4;  // 16 warps x 4 rows = the 64 rows of this half
-                const int lr0 = hf * 64 + rbase;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    // row lr0 + i's scatter id was prefetched by lanes 8i..8i+7 (gather layout)
-                    const int64_t id = __shfl_sync(0xffffffffu, hf ? sid[1] : sid[0], 8 * i);
-                    const float4 o = *reinterpret_cast<const float4*>(pRA + stage_off(rbase + i, lane));
-                    if (lr0 + i < nloc) reinterpret_cast<float4*>(a.x_out + id * 128)[lane] = o;
-                }
-            }
-            __syncthreads();
+// this unit's output is written during the next unit's QKV MMA (or after the loop)
+        if ((lane & 7) == 0) {
+            sRowId[warp * 4 + (lane >> 3)] = sid[0];
+            sRowId[64 + warp * 4 + (lane >> 3)] = sid[1];
         }
+        pnloc = nloc;
+        pend = true;
         FTR(tb + 15);
+    }
+    if (pend) {  // the last unit's output
+        __syncthreads();  // the row ids
+        stage_out(pKV);
+        __syncthreads();
+        store_out(pKV, 0, 16);
     }
     FTRG(61);
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(a.nonfinite, 1);
@@ -1065,6 +1098,17 @@ int ext_rows_needed(int G, int split) {
     return need;
 }
 
+// the previous unit's output staging (its rows x 512 B) fits the K/V region beside the rows
+// the peer's halo push for the running unit may be landing in: rank 0 stages below its
+// halo (rows < split), rank 1 above it (the kernel uses the same offsets)
+bool staging_fits(int G, int split) {
+    const int R = (256 / G) * G;
+    const int S = (split / G) * G;
+    const bool strad = S < split && split < R;
+    const int h0 = strad ? split - S : 0;
+    return ((h0 * kKVPitch + 15) & ~15) + (R - split) * 512 <= kKVRows * kKVPitch && split * 512 <= kKVRows * kKVPitch;
+}
+
 // attention m-tiles of the rows [r0, r1) of a unit (16-query tiles per group part)
 int mtiles(int G, int r0, int r1) {
     int n = 0;
@@ -1082,6 +1126,7 @@ int choose_split(int G) {
     int best = -1, best_rounds = 1 << 30, best_skew = 1 << 30;
     for (int s = R - 128 > 1 ? R - 128 : 1; s <= 128 && s <= R; ++s) {
         if (ext_rows_needed(G, s) > kKVRows) continue;
+        if (!staging_fits(G, s)) continue;
         if (mtiles(G, 0, s) > 16 || mtiles(G, s, R) > 16) continue;  // the per-CTA m-tile table
         const int t0 = 4 * mtiles(G, 0, s), t1 = 4 * mtiles(G, s, R);
         const int rounds = ((t0 + 15) / 16 > (t1 + 15) / 16) ? (t0 + 15) / 16 : (t1 + 15) / 16;
