@@ -20,6 +20,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include <cstring>
 
 #include "common.cuh"
@@ -49,6 +51,11 @@ void swizzle_weight_bf16(const float* w, int rows, int k, uint16_t* out) {
 
 void build_pair_images(const float* w_qkv, const float* w_out, const float* w1f, const float* w2,
                        uint16_t* out) {
+    // the fused kernel's GELU omits its factor 1/2 (x (1 + tanh g) instead of x/2 (1 + tanh g)):
+    // W2 carries it (exact: a power of two)
+    std::vector<float> w2h(w2, w2 + 128 * 256);
+    for (float& v : w2h) v *= 0.5f;
+    w2 = w2h.data();
     for (int v = 0; v < 2; ++v) {
         uint16_t* o = out + v * 65536;  // 128 KB per rank
         for (int c = 0; c < 3; ++c) swizzle_weight_bf16(w_qkv + (128 * c + 64 * v) * 128, 64, 128, o + c * 8192);
