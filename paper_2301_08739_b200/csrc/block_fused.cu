@@ -394,19 +394,25 @@ FWA_DEVINL void load_row_quads(const float* x, const double* x64, const __half* 
 // LN1 (two-pass mean / variance over the 8 lanes of a row, eps inside the sqrt,
 // kernels.hpp:235-249) + affine + PE (472-485) -> 4 x 8 B of the bf16 SW128 A image.
 FWA_DEVINL void ln1_row_to_image(const float (&v)[16], const uint2 (&ph)[4], bool valid, int r, int sub,
-                                 const float* sG, const float* sB, uint8_t* A, bool& bad) {
+                                 const float* sG, uint8_t* A, bool& bad) {
     float sm = 0.f;
 #pragma unroll
     for (int j = 0; j < 16; ++j) sm += v[j];
     sm += __shfl_xor_sync(0xffffffffu, sm, 1);
     sm += __shfl_xor_sync(0xffffffffu, sm, 2);
     sm += __shfl_xor_sync(0xffffffffu, sm, 4);
+    // a non-finite input makes the row sum non-finite; only then look at the values (a
+    // finite row whose sum overflows is not an error, as in the reference)
+    if (!isfinite(sm)) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) bad |= !isfinite(v[j]);
+    }
     const float mean = sm * (1.0f / 128.0f);
-    float sq = 0.f;
+    float d[16], sq = 0.f;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-        bad |= !isfinite(v[j]);
-        sq += (v[j] - mean) * (v[j] - mean);
+        d[j] = v[j] - mean;
+        sq = fmaf(d[j], d[j], sq);
     }
     sq += __shfl_xor_sync(0xffffffffu, sq, 1);
     sq += __shfl_xor_sync(0xffffffffu, sq, 2);
@@ -417,15 +423,13 @@ FWA_DEVINL void ln1_row_to_image(const float (&v)[16], const uint2 (&ph)[4], boo
     for (int i = 0; i < 4; ++i) {
         const int c = 32 * i + 4 * sub;
         const float4 g = *reinterpret_cast<const float4*>(sG + c);
-        const float4 b = *reinterpret_cast<const float4*>(sB + c);
         const __half2 h0 = *reinterpret_cast<const __half2*>(&ph[i].x);
         const __half2 h1 = *reinterpret_cast<const __half2*>(&ph[i].y);
         pesum = __hadd2(pesum, __hadd2(h0, h1));
         const float2 p0 = __half22float2(h0), p1 = __half22float2(h1);
-        uint32_t o0 = pack_bf16x2(g.x * ((v[4 * i] - mean) * inv) + b.x + p0.x,
-                                  g.y * ((v[4 * i + 1] - mean) * inv) + b.y + p0.y);
-        uint32_t o1 = pack_bf16x2(g.z * ((v[4 * i + 2] - mean) * inv) + b.z + p1.x,
-                                  g.w * ((v[4 * i + 3] - mean) * inv) + b.w + p1.y);
+        // gamma * xhat + PE (LN1's beta is folded into b_qkv on the host)
+        uint32_t o0 = pack_bf16x2(fmaf(g.x, d[4 * i] * inv, p0.x), fmaf(g.y, d[4 * i + 1] * inv, p0.y));
+        uint32_t o1 = pack_bf16x2(fmaf(g.z, d[4 * i + 2] * inv, p1.x), fmaf(g.w, d[4 * i + 3] * inv, p1.y));
         if (!valid) o0 = o1 = 0u;
         *reinterpret_cast<uint2*>(A + sw128_offset(r, c, 128)) = make_uint2(o0, o1);
     }
@@ -471,8 +475,7 @@ struct FusedArgs {
     int G, gpu, n_units;
     int split;               // rank 0 holds unit rows [0, split), rank 1 [split, R)
     const uint8_t* wpair;    // [rank 0 image | rank 1 image], kWBytes each
-    const float* vec;        // b_qkv | b_out | b2 | b1'
-    const float *ln1_g, *ln1_b;
+    const float* vec;        // TcBlockWeights::vec_pair (1152 floats)
     int* nonfinite;
     unsigned long long* trace;  // FWA_B200_TRACE: 64 SM-clock slots per CTA (phase boundaries)
     float lmax;                 // attention fast pass: row sums beyond [1/lmax, lmax] re-run shifted
@@ -539,7 +542,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         for (int i = threadIdx.x; i < kRXBytes / 16; i += kThreads) rx[i] = make_uint4(0u, 0u, 0u, 0u);
     }
     for (int i = threadIdx.x; i < kVecFloats; i += kThreads)
-        sVec[i] = i < 896 ? a.vec[i] : (i < 1024 ? a.ln1_g[i - 896] : a.ln1_b[i - 1024]);
+        sVec[i] = a.vec[i];
     if (warp == 0) {
         __syncwarp();
         tmem_alloc2(tmem_slot, 512);
@@ -722,7 +725,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
                     const float4 f = *reinterpret_cast<const float4*>(xs + r * kXSPitch + (8 * i + sub) * 16);
                     v[4 * i] = f.x; v[4 * i + 1] = f.y; v[4 * i + 2] = f.z; v[4 * i + 3] = f.w;
                 }
-                ln1_row_to_image(v, pe[hf], r < nloc, r, sub, sVec + 896, sVec + 1024, pRA, bad);
+                ln1_row_to_image(v, pe[hf], r < nloc, r, sub, sVec + 896, pRA, bad);
                 if (hf == 0) FTR(tb + 1);
             }
             {  // the residual rows -> TMEM [384, 512)
@@ -756,7 +759,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
                 const int r = hf * 64 + warp * 4 + rl;
-                ln1_row_to_image(v[hf], pe[hf], r < nloc, r, sub, sVec + 896, sVec + 1024, pRA, bad);
+                ln1_row_to_image(v[hf], pe[hf], r < nloc, r, sub, sVec + 896, pRA, bad);
                 if (hf == 0) FTR(tb + 1);
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
@@ -827,8 +830,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
                 for (int e = 0; e < 4; ++e) {
                     const int j = 8 * hf + 2 * e;
                     const float* bq = sVec + 16 * h + j;
-                    oq[e] = pack_bf16x2((__uint_as_float(qv[j]) + bq[0]) * kScaleLog2,
-                                        (__uint_as_float(qv[j + 1]) + bq[1]) * kScaleLog2);
+                    oq[e] = pack_bf16x2(__uint_as_float(qv[j]) + bq[0], __uint_as_float(qv[j + 1]) + bq[1]);
                     ok[e] = pack_bf16x2(__uint_as_float(kv[j]) + bq[128], __uint_as_float(kv[j + 1]) + bq[129]);
                     ov[e] = pack_bf16x2(__uint_as_float(vv[j]) + bq[256], __uint_as_float(vv[j + 1]) + bq[257]);
                 }
@@ -1155,7 +1157,7 @@ void launch_block_fused(const float* x, const double* x64, const __half* pe16, c
     a.split = choose_split(G);
     const int64_t n_groups = rows / G;
     a.n_units = static_cast<int>((n_groups + a.gpu - 1) / a.gpu);
-    a.wpair = w.w_pair; a.vec = w.vec; a.ln1_g = w.ln1_g; a.ln1_b = w.ln1_b; a.nonfinite = d_nonfinite;
+    a.wpair = w.w_pair; a.vec = w.vec_pair; a.nonfinite = d_nonfinite;
     a.trace = trace;
     a.lmax = 0x1p64f;
     if (const char* e = std::getenv("FWA_B200_ATTN_LMAX")) a.lmax = std::strtof(e, nullptr);  // tests

@@ -291,12 +291,13 @@ std::vector<BlockParams> upload_block_params(const std::vector<Record>& recs, De
     const bool tc = d == 128 && dff == 256;
     const size_t tc_elems = 2 * (384 * 128 + 128 * 128 + 256 * 128 + 128 * 256);  // + pair images
     // per block, after the bf16 images: f32 [b_qkv 384 | b_out 128 | b2 128 | b1' 256]
-    constexpr size_t kTcVec = 896;
+    constexpr size_t kTcVec = 896, kPairVec = 1152;
     std::vector<uint16_t> sw;
-    std::vector<float> tcv;
+    std::vector<float> tcv, pv;
     if (tc) {
-        sw.assign(tc_elems * nb + kTcVec * 2 * nb, 0);
+        sw.assign(tc_elems * nb + (kTcVec + kPairVec) * 2 * nb, 0);
         tcv.assign(kTcVec * nb, 0.f);
+        pv.assign(kPairVec * nb, 0.f);
         const size_t tb = sw.size() * 2;
         if (pbf16.cap < tb) {
             if (pbf16.p) cudaFree(pbf16.p);
@@ -348,7 +349,21 @@ std::vector<BlockParams> upload_block_params(const std::vector<Record>& recs, De
             for (int i = 0; i < 128; ++i) tcv[b * kTcVec + 384 + i] = hw_out[d * d + i];          // b_out
             for (int i = 0; i < 128; ++i) tcv[b * kTcVec + 512 + i] = hw2[static_cast<size_t>(d) * dff + i];  // b2
             swizzle_weight_bf16(hw2, 128, 256, o + 384 * 128 + 128 * 128 + 256 * 128);
-            build_pair_images(hw_qkv, hw_out, w1f.data(), hw2, o + tc_elems / 2);
+            // fused kernel: LN1's beta into b_qkv (fp64), Q rows scaled to the base-2 exponent
+            constexpr double kQScale = 0.25 * 1.4426950408889634;  // block_fused.cu kScaleLog2
+            const float* hln1g = hw_out + d * d + d;
+            const float* hln1b = hln1g + d;
+            std::vector<float> wq(hw_qkv, hw_qkv + 3 * d * d);
+            float* pvb = pv.data() + b * kPairVec;
+            for (int j = 0; j < 3 * d; ++j) {
+                double acc = hw_qkv[3 * d * d + j];
+                for (int i = 0; i < d; ++i) acc += static_cast<double>(hw_qkv[static_cast<size_t>(j) * d + i]) * hln1b[i];
+                pvb[j] = static_cast<float>(j < d ? acc * kQScale : acc);
+            }
+            for (size_t i = 0; i < static_cast<size_t>(d) * d; ++i) wq[i] = static_cast<float>(wq[i] * kQScale);
+            for (int i = 0; i < 512; ++i) pvb[384 + i] = tcv[b * kTcVec + 384 + i];  // b_out | b2 | b1'
+            for (int i = 0; i < d; ++i) pvb[896 + i] = hln1g[i];                      // ln1_g | (beta: 0)
+            build_pair_images(wq.data(), hw_out, w1f.data(), hw2, o + tc_elems / 2);
             const __nv_bfloat16* dbase =
                 static_cast<const __nv_bfloat16*>(pbf16.p) + b * tc_elems;
             bp.tc.w_qkv = dbase;
@@ -360,12 +375,15 @@ std::vector<BlockParams> upload_block_params(const std::vector<Record>& recs, De
                                      static_cast<const __nv_bfloat16*>(pbf16.p) + tc_elems * nb) +
                                  b * kTcVec;
             bp.tc.vec = vbase;  // b_qkv | b_out | b2 | b1 (LN2-folded)
+            bp.tc.vec_pair = reinterpret_cast<const float*>(static_cast<const __nv_bfloat16*>(pbf16.p) + tc_elems * nb +
+                                                            kTcVec * 2 * nb) + b * kPairVec;
             bp.tc.ln1_g = bp.ln1_g;
             bp.tc.ln1_b = bp.ln1_b;
         }
     }
     if (tc) {
         std::memcpy(sw.data() + tc_elems * nb, tcv.data(), tcv.size() * 4);
+        std::memcpy(sw.data() + tc_elems * nb + kTcVec * 2 * nb, pv.data(), pv.size() * 4);
         CUDA_OK(cudaMemcpyAsync(pbf16.p, sw.data(), sw.size() * 2, cudaMemcpyHostToDevice, st));
     }
     CUDA_OK(cudaStreamSynchronize(st));  // host staging vectors die on return

@@ -141,6 +141,10 @@ struct TcBlockWeights {
     // holds output-feature rows [64v, 64v+64) of every 128-row weight chunk:
     // W_qkv chunks q,k,v (3 x 16 KB) | W_out (16 KB) | W1' halves (2 x 16 KB) | W2 (32 KB)
     const uint8_t* w_pair;
+    // the fused kernel's vectors: [b_qkv' 384 | b_out 128 | b2 128 | b1' 256 | ln1_g 128 | 0 128]
+    // with LN1's beta folded into b_qkv' (+ W_qkv beta1) and the Q rows (W_q in w_pair, b_q')
+    // pre-scaled by log2(e) / sqrt(16) -- the attention's base-2 exponent
+    const float* vec_pair;
 };
 // Host-side: write the UMMA SW128 K-major smem image of a row-major f32
 // [rows x k] weight as bf16 (rows multiple of 8, k multiple of 64).
