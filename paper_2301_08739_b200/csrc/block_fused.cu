@@ -654,18 +654,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
     };
     // m-tile table (first query row, part end, key ext row) of this CTA's 16-query tiles,
     // lanes 0..16 of one warp in parallel
-    auto build_table = [&](int nloc_, int urow0_, int ext0_) {
+    // The straddling group's tiles (.w = 1: they read the peer's halo rows) come LAST, so
+    // the other groups' tasks run while the halo is still in flight.
+    auto build_table = [&](int nloc_, int urow0_, int ext0_, int straddle_g) {
         if (lane <= 16) {
             int n = 0;
             int4 mine = make_int4(0, 0, 0, 0);
-            if (nloc_ > 0)
-                for (int gg = urow0_ / G; gg * G < urow0_ + nloc_; ++gg) {
+            if (nloc_ > 0) {
+                const int g0 = urow0_ / G, g1 = (urow0_ + nloc_ - 1) / G;
+                for (int k = 0; k <= g1 - g0; ++k) {
+                    const int gg = rank ? g1 - k : g0 + k;  // rank 1 holds the straddle group first
                     const int qa = gg * G - urow0_ < 0 ? 0 : gg * G - urow0_;
                     const int qb = gg * G + G - urow0_ > nloc_ ? nloc_ : gg * G + G - urow0_;
                     const int nt = (qb - qa + 15) >> 4;
-                    if (lane >= n && lane < n + nt) mine = make_int4(qa + 16 * (lane - n), qb, gg * G - urow0_ + ext0_, 0);
+                    if (lane >= n && lane < n + nt)
+                        mine = make_int4(qa + 16 * (lane - n), qb, gg * G - urow0_ + ext0_, gg == straddle_g ? 1 : 0);
                     n += nt;
                 }
+            }
             if (lane < 16 && lane < n) sTab[lane] = mine;
             if (lane == 16) sTab[16].x = n;
         }
@@ -808,7 +814,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         // ---- 2. QKV epilogue (all 8 heads) + attention
         // the attention m-tile table, built while the QKV MMA runs; read after the
         // epilogue's __syncthreads
-        if (warp == 0) build_table(nloc, urow0, ext0);
+        if (warp == 0) build_table(nloc, urow0, ext0, strad ? S / G : -1);
         if (pend) __syncthreads();  // staging read before the epilogue's K/V rows overwrite it
         mbar_wait(bQKV, ph);
         fence_after_sync();
@@ -865,13 +871,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
             }
         }
         __syncthreads();        // local K/V, Q and the m-tile table visible
-        mbar_wait(bHalo, ph);   // the peer's halo rows have landed
         FTR(tb + 4);
         {
             const int ntasks = sTab[16].x * 8;  // (m-tile, head)
+            bool halo = false;
 #pragma unroll 1
             for (int t = warp; t < ntasks; t += 16) {
                 const int4 e = sTab[t >> 3];
+                if (e.w && !halo) {  // the peer's halo rows have landed (st.async bytes)
+                    mbar_wait(bHalo, ph);
+                    halo = true;
+                }
                 if (!attn_task<NT, GC, false>(sRA, sKV, pRA, t & 7, e.x, e.y, e.z, G, a.lmax))
                     attn_task<NT, GC, true>(sRA, sKV, pRA, t & 7, e.x, e.y, e.z, G, a.lmax);
             }
