@@ -887,16 +887,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
             }
         }
         FTR(tb + 5);
-        __syncthreads();  // K/V consumed: W2 comes back into its slot (needed by FFN2)
-        if (threadIdx.x == 0) {
-            fence_proxy_async_smem();
-            mbar_arrive_expect_tx(bW2, 32768);
-            bulk_g2s(smem + kOffW2, a.wpair + static_cast<size_t>(rank) * kWBytes + 98304, 32768, bW2);
-        }
         FTR(tb + 6);
         FTR(tb + 7);
 
-        // ---- 3. out-proj: P = O Wout^T (TMEM [0,128)); residual reload overlaps the MMA
+        // ---- 3. out-proj: P = O Wout^T (TMEM [0,128)); residual reload overlaps the MMA.
+        // The handshake's barrier also retires the K/V reads: W2 comes back into its slot
+        // (needed by FFN2) right after (the leader: after issuing the out-proj MMAs).
         handshake();
         if (leader) {
             leader_wait();
@@ -905,6 +901,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
                 mma2_bf16(tmem + 384, sdesc_sw128(sRA + (ks >> 2) * 16384 + (ks & 3) * 32),
                           sdesc_sw128(sWa + kOffWout + (ks >> 2) * 8192 + (ks & 3) * 32), id256, 1u);
             mma_commit_pair(bP);
+        }
+        if (threadIdx.x == 0) {
+            mbar_arrive_expect_tx(bW2, 32768);
+            bulk_g2s(smem + kOffW2, a.wpair + static_cast<size_t>(rank) * kWBytes + 98304, 32768, bW2);
         }
         ++hs;
         mbar_wait(bP, ph);
