@@ -171,6 +171,31 @@ def _cpu_model():
     return None
 
 
+def pcie_floor(h_in, h_out, dev, reps=10):
+    """ms per frame for the frame's H2D (f64 features) and D2H (f32 features) bytes copied
+    concurrently on two streams -- the lower bound of the streamed e2e."""
+    import torch
+    d_in = torch.empty(h_in.numel() * h_in.element_size(), dtype=torch.uint8, device=dev)
+    d_out = torch.empty(h_out.numel() * h_out.element_size(), dtype=torch.uint8, device=dev)
+    hi = h_in.view(-1).view(torch.uint8)
+    ho = h_out.view(-1).view(torch.uint8)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def once():
+        with torch.cuda.stream(s1):
+            d_in.copy_(hi, non_blocking=True)
+        with torch.cuda.stream(s2):
+            ho.copy_(d_out, non_blocking=True)
+
+    once()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        once()
+    torch.cuda.synchronize()
+    return 1e3 * (time.perf_counter() - t0) / reps
+
+
 def run_ours(args, rank, world, local_rank, dist):
     import torch
 
@@ -285,6 +310,9 @@ def run_ours(args, rank, world, local_rank, dist):
     assert torch.equal(h_out2[0][:nk], h_out2[1][:nk]) if args.steps > 1 else True
     clk = clocks.stop()
     assert nk_e2e == nk
+    # the PCIe floor of e2e: the same bytes per frame as one pinned H2D and one D2H copy
+    # running together (no compute), on this box
+    pcie_floor_ms = pcie_floor(h_feats, h_out, dev)
 
     # ---------------------------------------------------------------- config 4: one F250 scene
     # split by group ranges across the ranks, NCCL all-gather of each block's rows
@@ -384,6 +412,8 @@ def run_ours(args, rank, world, local_rank, dist):
                 "api": "fwa_b200_backbone_forward_frames over the step's frames from pinned host buffers "
                        "(f64 PillarSet in, f32 features + kept/dropped ids out), copies pipelined "
                        "against the compute; wall clock around the call",
+                "pcie_floor_ms_per_frame": pcie_floor_ms,
+                "frac_of_pcie_floor": pcie_floor_ms / (1e3 * e2e_max / args.steps),
                 "single_frame": {"value": pillars_all * args.steps / e2e1_max, "unit": "pillars/s",
                                  "ms_per_frame": 1e3 * e2e1_max / args.steps,
                                  "api": "fwa_b200_backbone_forward, one call per step, L2 flushed before each"}},
