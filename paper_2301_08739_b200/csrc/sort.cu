@@ -168,10 +168,11 @@ __global__ void __launch_bounds__(256) k_sort_keys(const double* __restrict__ co
                                                    long long* __restrict__ minmax, BinsFuse fz) {
     pdl_entry();
     const int s = blockIdx.y;
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const bool axis_y = s >= 2, shift = (s & 1) != 0;
     long long wM = LLONG_MAX, wm = LLONG_MAX, xM = LLONG_MIN, xm = LLONG_MIN;
-    if (i < ntot) {
+    // grid-stride: few CTAs per spec -> few partials and few last-CTA tickets
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < ntot;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const double2 c = reinterpret_cast<const double2*>(coords)[i];
         double cx = c.x, cy = c.y;
         if (shift) {
@@ -187,8 +188,10 @@ __global__ void __launch_bounds__(256) k_sort_keys(const double* __restrict__ co
         const int64_t e = static_cast<int64_t>(s) * ntot + i;
         reinterpret_cast<longlong2*>(win)[e] = make_longlong2(a, b);
         reinterpret_cast<double2*>(loc)[e] = make_double2(la, lb);
-        wM = xM = a;
-        wm = xm = b;
+        wM = a < wM ? a : wM;
+        xM = a > xM ? a : xM;
+        wm = b < wm ? b : wm;
+        xm = b > xm ? b : xm;
     }
     wM = wmin(wM);
     xM = wmax(xM);
@@ -229,7 +232,10 @@ __global__ void __launch_bounds__(256) k_sort_keys(const double* __restrict__ co
     }
 }
 
-int64_t sort_keys_partials(int64_t ntot) { return (ntot + 255) / 256; }
+int64_t sort_keys_partials(int64_t ntot) {  // CTAs (= min/max partials) per spec
+    const int64_t n = (ntot + 255) / 256;
+    return n < 74 ? n : 74;
+}
 
 void launch_sort_keys(const double* coords, int64_t ntot, int n_specs, double w_x, double w_y,
                       long long* win, double* loc, long long* partials, cudaStream_t s,

@@ -16,6 +16,7 @@ d_out = torch.empty((n, 128), dtype=torch.float32, device=dev)
 d_kept = torch.empty(n, dtype=torch.int32, device=dev)
 flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 res = {}
+noflush = "--noflush" in sys.argv
 for nb in (1, 2, 4, 8):
     cfg = F.FwaConfig(n_blocks=nb)
     ctx.load_params(cfg, F.init_backbone_params(cfg, 42))
@@ -23,7 +24,8 @@ for nb in (1, 2, 4, 8):
         ctx.forward_device(d_coords.data_ptr(), d_feats.data_ptr(), [0, n], cfg, d_out.data_ptr(), d_kept.data_ptr())
     tot = 0.0
     for _ in range(30):
-        flush.zero_()
+        if not noflush:
+            flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         ctx.forward_device(d_coords.data_ptr(), d_feats.data_ptr(), [0, n], cfg, d_out.data_ptr(), d_kept.data_ptr())
