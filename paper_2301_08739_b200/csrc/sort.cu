@@ -375,11 +375,27 @@ __global__ void __launch_bounds__(256) k_bin_rank(const uint32_t* __restrict__ b
     const int my = pre[p];
     int rank = 0;
     const int nn = n;
+    const uint32_t mxh = static_cast<uint32_t>(me.x >> 32), mxl = static_cast<uint32_t>(me.x);
+    const uint32_t myh = static_cast<uint32_t>(me.y >> 32), myl = static_cast<uint32_t>(me.y);
 #pragma unroll 8
     for (int j = 0; j < nn; ++j) {
         const ulonglong2 o = __ldg(pkey + start + j);
         const int oid = __ldg(pre + start + j);
-        rank += (o.x < me.x) | ((o.x == me.x) & ((o.y < me.y) | ((o.y == me.y) & (oid < my))));
+        // (o.x, o.y, oid) < (me.x, me.y, my) lexicographically == the borrow of the 160-bit
+        // subtraction o - me (every field unsigned, fixed width): one carry chain
+        uint32_t b;
+        asm("{\n\t.reg .u32 t;\n\t"
+            "sub.cc.u32 t, %1, %2;\n\t"
+            "subc.cc.u32 t, %3, %4;\n\t"
+            "subc.cc.u32 t, %5, %6;\n\t"
+            "subc.cc.u32 t, %7, %8;\n\t"
+            "subc.cc.u32 t, %9, %10;\n\t"
+            "subc.u32 %0, 0, 0;\n\t}"
+            : "=r"(b)
+            : "r"(static_cast<uint32_t>(oid)), "r"(static_cast<uint32_t>(my)),
+              "r"(static_cast<uint32_t>(o.y)), "r"(myl), "r"(static_cast<uint32_t>(o.y >> 32)), "r"(myh),
+              "r"(static_cast<uint32_t>(o.x)), "r"(mxl), "r"(static_cast<uint32_t>(o.x >> 32)), "r"(mxh));
+        rank -= static_cast<int>(b);  // b = 0xFFFFFFFF when o < me
     }
     const int64_t spec_base = (start / ntot) * ntot;
     sorted[start + rank] = my;
