@@ -232,6 +232,9 @@ FWA_DEVINL uint32_t img_off(int row, int col) {
 // Q is stored pre-scaled by (1/sqrt(16)) * log2(e), so S = Q K^T is the softmax exponent
 // in base 2.
 constexpr float kScaleLog2 = 0.25f * 1.4426950408889634f;
+#ifndef FWA_POLY_MASK
+#define FWA_POLY_MASK 2  // key tiles nt with bit (nt & 3) set take the FMA-pipe exp2
+#endif
 FWA_DEVINL float rcp_approx(float x) {
     float y;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -253,9 +256,6 @@ FWA_DEVINL bool attn_task(uint32_t sRA, uint32_t sKV, uint8_t* pRA, int head, in
     const int G = GC > 0 ? GC : G_rt;
     const int lane = threadIdx.x & 31;
     const int g = lane >> 2, t4 = lane & 3;
-#ifndef FWA_POLY_MASK
-#define FWA_POLY_MASK 2
-#endif
     constexpr int kPolyMask = FWA_POLY_MASK;  // nt & 3 in the mask: 0b0010 -> nt = 1, 5 at G = 69
     const int nt_live = (G + 7) >> 3;
     uint32_t a0, a1, a2, a3;
@@ -359,6 +359,102 @@ FWA_DEVINL bool attn_task(uint32_t sRA, uint32_t sKV, uint8_t* pRA, int head, in
         if (r1 < qend) *reinterpret_cast<uint32_t*>(pRA + img_off(r1, col)) = pack_bf16x2(o[nt][2] * i1, o[nt][3] * i1);
     }
     return true;
+}
+
+// Two attention tasks interleaved in one warp, streamed per 16-key slab: K tile -> S ->
+// P = 2^S -> V tile -> PV accumulate, so only one slab's S/P/K/V is live per task (~40
+// registers) and the two independent chains hide each other's MMA / SFU latency.  The
+// fast pass of attn_task (no row-max shift); bit b of the result set = task b must be
+// re-run with the shift (its row sums left [1/lmax, lmax]); nothing stored for it.
+template <int NT, int GC>
+FWA_DEVINL uint32_t attn_task2(uint32_t sRA, uint32_t sKV, uint8_t* pRA, const int (&head)[2], const int4 (&e)[2],
+                               int G_rt, float lmax) {
+    const int G = GC > 0 ? GC : G_rt;
+    const int lane = threadIdx.x & 31;
+    const int g = lane >> 2, t4 = lane & 3;
+    constexpr int kPolyMask = FWA_POLY_MASK;
+    const int nt_live = (G + 7) >> 3;
+    constexpr uint32_t kOnes = 0x3F803F80u;  // bf16x2 (1, 1)
+    uint32_t a[2][4];
+    float o[2][2][4] = {}, l[2][4] = {};
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int qrow = e[k].x + (lane & 7) + ((lane >> 3) & 1) * 8;
+        const int col = head[k] * 16 + (lane >> 4) * 8;
+        ldsm_x4(sRA + img_off(qrow, col), a[k][0], a[k][1], a[k][2], a[k][3]);
+    }
+#pragma unroll
+    for (int kt = 0; kt < NT / 2; ++kt) {
+        if (2 * kt >= nt_live) continue;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int ke0 = e[k].z;
+            uint32_t kb[2][2], vb[4];
+            {
+                const int krow = ke0 + (2 * kt + (lane >> 4)) * 8 + (lane & 7);
+                ldsm_x4(sKV + krow * kKVPitch + head[k] * 32 + ((lane >> 3) & 1) * 16, kb[0][0], kb[0][1], kb[1][0],
+                        kb[1][1]);
+                const int vrow = ke0 + kt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+                ldsm_x4_t(sKV + vrow * kKVPitch + 256 + head[k] * 32 + (lane >> 4) * 16, vb[0], vb[1], vb[2], vb[3]);
+            }
+            if (kt * 16 + 16 > G) {  // keys >= G: V := 0 (their rows may hold any bits)
+                const int k0 = kt * 16 + 2 * t4, k1 = k0 + 8;
+                const uint32_t m0 = (k0 < G ? 0xFFFFu : 0u) | (k0 + 1 < G ? 0xFFFF0000u : 0u);
+                const uint32_t m1 = (k1 < G ? 0xFFFFu : 0u) | (k1 + 1 < G ? 0xFFFF0000u : 0u);
+                vb[0] &= m0;
+                vb[2] &= m0;
+                vb[1] &= m1;
+                vb[3] &= m1;
+            }
+            uint32_t p[2][2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int nt = 2 * kt + h;
+                if (nt >= nt_live) {
+                    p[h][0] = p[h][1] = 0u;
+                    continue;
+                }
+                float sv[4] = {0.f, 0.f, 0.f, 0.f};
+                mma16816(sv, a[k][0], a[k][1], a[k][2], a[k][3], kb[h][0], kb[h][1]);
+                if (nt * 8 + 8 > G) {
+                    const int col = nt * 8 + 2 * t4;
+                    if (col >= G) { sv[0] = -INFINITY; sv[2] = -INFINITY; }
+                    if (col + 1 >= G) { sv[1] = -INFINITY; sv[3] = -INFINITY; }
+                }
+                if (((kPolyMask >> (nt & 3)) & 1) && nt * 8 + 8 <= G) {
+                    p[h][0] = ex2_poly_bf16x2(sv[0], sv[1]);
+                    p[h][1] = ex2_poly_bf16x2(sv[2], sv[3]);
+                } else {
+                    p[h][0] = ex2_bf16x2(sv[0], sv[1]);
+                    p[h][1] = ex2_bf16x2(sv[2], sv[3]);
+                }
+            }
+            mma16816(o[k][0], p[0][0], p[0][1], p[1][0], p[1][1], vb[0], vb[1]);
+            mma16816(o[k][1], p[0][0], p[0][1], p[1][0], p[1][1], vb[2], vb[3]);
+            mma16816(l[k], p[0][0], p[0][1], p[1][0], p[1][1], kOnes, kOnes);
+        }
+    }
+    const float lmin = rcp_approx(lmax);
+    uint32_t redo = 0;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const bool ok = l[k][0] >= lmin && l[k][0] <= lmax && l[k][2] >= lmin && l[k][2] <= lmax;
+        if (__any_sync(0xffffffffu, !ok)) {
+            redo |= 1u << k;
+            continue;
+        }
+        const float i0 = rcp_approx(l[k][0]), i1 = rcp_approx(l[k][2]);
+        const int r0 = e[k].x + g, r1 = r0 + 8;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+            const int col = head[k] * 16 + nt * 8 + 2 * t4;
+            if (r0 < e[k].y)
+                *reinterpret_cast<uint32_t*>(pRA + img_off(r0, col)) = pack_bf16x2(o[k][nt][0] * i0, o[k][nt][1] * i0);
+            if (r1 < e[k].y)
+                *reinterpret_cast<uint32_t*>(pRA + img_off(r1, col)) = pack_bf16x2(o[k][nt][2] * i1, o[k][nt][3] * i1);
+        }
+    }
+    return redo;
 }
 
 // ---------------------------------------------------------------- row I/O
@@ -875,6 +971,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         {
             const int ntasks = sTab[16].x * 8;  // (m-tile, head)
             bool halo = false;
+#ifndef FWA_ATTN_PAIRS
+#define FWA_ATTN_PAIRS 1
+#endif
+#if FWA_ATTN_PAIRS
+            // tasks t and t + 16 of this warp together (the same head, two m-tiles)
+#pragma unroll 1
+            for (int t = warp; t < ntasks; t += 32) {
+                const bool two = t + 16 < ntasks;
+                const int4 ee[2] = {sTab[t >> 3], two ? sTab[(t + 16) >> 3] : sTab[t >> 3]};
+                if ((ee[0].w || (two && ee[1].w)) && !halo) {  // the peer's halo rows have landed
+                    mbar_wait(bHalo, ph);
+                    halo = true;
+                }
+                if (two) {
+                    const int hd[2] = {t & 7, (t + 16) & 7};
+                    const uint32_t redo = attn_task2<NT, GC>(sRA, sKV, pRA, hd, ee, G, a.lmax);
+                    for (int k = 0; k < 2; ++k)
+                        if (redo & (1u << k)) attn_task<NT, GC, true>(sRA, sKV, pRA, hd[k], ee[k].x, ee[k].y, ee[k].z, G, a.lmax);
+                } else if (!attn_task<NT, GC, false>(sRA, sKV, pRA, t & 7, ee[0].x, ee[0].y, ee[0].z, G, a.lmax)) {
+                    attn_task<NT, GC, true>(sRA, sKV, pRA, t & 7, ee[0].x, ee[0].y, ee[0].z, G, a.lmax);
+                }
+            }
+#else
 #pragma unroll 1
             for (int t = warp; t < ntasks; t += 16) {
                 const int4 e = sTab[t >> 3];
@@ -885,6 +1004,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
                 if (!attn_task<NT, GC, false>(sRA, sKV, pRA, t & 7, e.x, e.y, e.z, G, a.lmax))
                     attn_task<NT, GC, true>(sRA, sKV, pRA, t & 7, e.x, e.y, e.z, G, a.lmax);
             }
+#endif
         }
         FTR(tb + 5);
         FTR(tb + 6);

@@ -32,13 +32,6 @@
 
 namespace fwa_b200 {
 
-// The schedule kernels are chained with programmatic dependent launch: each one lets the
-// next be scheduled at once and waits for its predecessor's results before touching
-// memory (the launch latency of the 8-kernel chain overlaps the running kernel).
-__device__ __forceinline__ void pdl_entry() {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-}
 
 // ------------------------------------------------------------------ scan
 
@@ -166,7 +159,6 @@ __global__ void __launch_bounds__(256) k_sort_keys(const double* __restrict__ co
                                                    long long* __restrict__ win,
                                                    double* __restrict__ loc,
                                                    long long* __restrict__ minmax, BinsFuse fz) {
-    pdl_entry();
     const int s = blockIdx.y;
     const bool axis_y = s >= 2, shift = (s & 1) != 0;
     long long wM = LLONG_MAX, wm = LLONG_MAX, xM = LLONG_MIN, xm = LLONG_MIN;
@@ -241,7 +233,7 @@ void launch_sort_keys(const double* coords, int64_t ntot, int n_specs, double w_
                       long long* win, double* loc, long long* partials, cudaStream_t s,
                       int64_t* launches, const BinsFuse& fz) {
     dim3 grid(static_cast<unsigned>(sort_keys_partials(ntot)), static_cast<unsigned>(n_specs));
-    launch_pdl(k_sort_keys, grid, 256, 0, s, coords, ntot, n_specs, w_x, w_y, win, loc, partials, fz);
+    k_sort_keys<<<grid, 256, 0, s>>>(coords, ntot, n_specs, w_x, w_y, win, loc, partials, fz);
     *launches += 1;
 }
 
@@ -263,7 +255,6 @@ __global__ void __launch_bounds__(256) k_bins_hist(const long long* __restrict__
                                                    uint32_t* __restrict__ bin_of,
                                                    uint32_t* __restrict__ hist,
                                                    const uint32_t* __restrict__ d_nbins) {
-    pdl_entry();
     const int s = blockIdx.y;
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= ntot) return;
@@ -282,7 +273,7 @@ void launch_bins_hist(const long long* win, int64_t ntot, int n_specs, const int
                       int n_frames, const SpecBins* d_specs, uint32_t* bin_of, uint32_t* hist,
                       const uint32_t* d_nbins, cudaStream_t s, int64_t* launches) {
     dim3 grid(static_cast<unsigned>((ntot + 255) / 256), static_cast<unsigned>(n_specs));
-    launch_pdl(k_bins_hist, grid, 256, 0, s, win, ntot, d_frame_off, n_frames, d_specs, bin_of, hist, d_nbins);
+    k_bins_hist<<<grid, 256, 0, s>>>(win, ntot, d_frame_off, n_frames, d_specs, bin_of, hist, d_nbins);
     ++*launches;
 }
 
@@ -304,7 +295,6 @@ __global__ void __launch_bounds__(256) k_bin_scatter(const uint32_t* __restrict_
                                                      const uint32_t* __restrict__ d_nbins,
                                                      const uint32_t* __restrict__ tile_off,
                                                      uint32_t* __restrict__ pre_bin) {
-    pdl_entry();
     const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (e >= total) return;
     if (d_nbins && *d_nbins == 0u) return;
@@ -322,7 +312,7 @@ void launch_bin_scatter(const uint32_t* bin_of, const double* loc, int64_t ntot,
                         uint32_t* cursor, int32_t* pre, double* pre_loc, const uint32_t* d_nbins,
                         const uint32_t* tile_off, uint32_t* pre_bin, cudaStream_t s, int64_t* launches) {
     const int64_t total = ntot * n_specs;
-    launch_pdl(k_bin_scatter, static_cast<unsigned>((total + 255) / 256), 256, 0, s, bin_of, loc, total, ntot,
+    k_bin_scatter<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(bin_of, loc, total, ntot,
                                                                            cursor, pre, pre_loc, d_nbins,
                                                                            tile_off, pre_bin);
     ++*launches;
@@ -355,11 +345,20 @@ __global__ void __launch_bounds__(256) k_bin_rank(const uint32_t* __restrict__ b
                                                   int32_t* __restrict__ inv, uint32_t* __restrict__ large,
                                                   const uint32_t* __restrict__ d_nbins,
                                                   const uint32_t* __restrict__ tile_off) {
-    pdl_entry();
     const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (d_nbins) {
         n_bins = *d_nbins;
-        if (n_bins == 0u) return;
+        if (n_bins == 0u) {
+            // bin-capacity overflow (the host re-runs the frame set with exact bins): leave an
+            // identity permutation so every consumer of the plans (drop tables, compaction,
+            // the block kernels' gathers) stays in bounds on this discarded pass
+            if (p < total) {
+                const int64_t id = p % ntot;
+                sorted[p] = static_cast<int32_t>(id);
+                inv[p] = static_cast<int32_t>(p);
+            }
+            return;
+        }
     }
     if (p >= total) return;
     const uint32_t b = pre_bin[p];
@@ -407,7 +406,6 @@ __global__ void __launch_bounds__(512) k_bin_sort_large(
     const uint32_t* __restrict__ large, const int32_t* __restrict__ pre,
     const double* __restrict__ loc, int64_t ntot, int32_t* __restrict__ sorted,
     int32_t* __restrict__ inv, int32_t* __restrict__ scratch, const uint32_t* __restrict__ tile_off) {
-    pdl_entry();
     extern __shared__ unsigned char smem_raw[];
     double* s_a = reinterpret_cast<double*>(smem_raw);
     double* s_b = s_a + kCtaBin;
@@ -485,7 +483,7 @@ void launch_bin_sort(const uint32_t* bin_start, uint32_t* hist, uint32_t n_bins,
                      int64_t* launches) {
     const int64_t total = ntot * n_specs;
     if (!d_nbins) cudaMemsetAsync(large, 0, sizeof(uint32_t), s);  // sync-free path: reset by the key kernel
-    launch_pdl(k_bin_rank, static_cast<unsigned>((total + 255) / 256), 256, 0, s, 
+    k_bin_rank<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
         bin_start, hist, n_bins, pre, reinterpret_cast<const ulonglong2*>(pre_loc), pre_bin, total, ntot, sorted,
         inv, large, d_nbins, tile_off);
     static bool attr_set = false;
@@ -494,7 +492,7 @@ void launch_bin_sort(const uint32_t* bin_start, uint32_t* hist, uint32_t n_bins,
         cudaFuncSetAttribute(k_bin_sort_large, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr_set = true;
     }
-    launch_pdl(k_bin_sort_large, kNumSMs, 512, smem, s, bin_start, hist, large, pre, loc, ntot, sorted, inv,
+    k_bin_sort_large<<<kNumSMs, 512, smem, s>>>(bin_start, hist, large, pre, loc, ntot, sorted, inv,
                                                 scratch, tile_off);
     *launches += 2;
 }
@@ -616,7 +614,6 @@ __global__ void __launch_bounds__(1024) k_drop_tables(const int32_t* __restrict_
                                                       int n_specs, int32_t* __restrict__ dropped_ids,
                                                       int32_t* __restrict__ drop_sorted,
                                                       int32_t* __restrict__ drop_pos) {
-    pdl_entry();
     __shared__ int32_t v[kMaxDrop];
     int P = 1;
     while (P < n) P <<= 1;
@@ -667,7 +664,6 @@ __global__ void k_compact_all(const int32_t* __restrict__ sorted, int64_t ntot, 
                               const int32_t* __restrict__ drop_pos, int n_drop, int64_t K, int s_last,
                               int32_t* __restrict__ idx, uint32_t* __restrict__ kept_rank,
                               int32_t* __restrict__ kept_ids, int32_t* __restrict__ out_pos) {
-    pdl_entry();
     const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t total = ntot * n_specs;
     if (t < total) {
@@ -694,7 +690,7 @@ void launch_drop_tables(const int32_t* sorted0, int n, const int64_t* frame_off,
                         const int64_t* drop_off, int n_frames, const int32_t* inv, int64_t ntot, int n_specs,
                         int32_t* dropped_ids, int32_t* drop_sorted, int32_t* drop_pos, cudaStream_t s,
                         int64_t* launches) {
-    launch_pdl(k_drop_tables, 1 + n_specs, 1024, 0, s, sorted0, n, frame_off, rows, drop_off, n_frames, inv, ntot,
+    k_drop_tables<<<1 + n_specs, 1024, 0, s>>>(sorted0, n, frame_off, rows, drop_off, n_frames, inv, ntot,
                                                n_specs, dropped_ids, drop_sorted, drop_pos);
     ++*launches;
 }
@@ -704,7 +700,7 @@ void launch_compact_all(const int32_t* sorted, int64_t ntot, int n_specs, const 
                         uint32_t* kept_rank, int32_t* kept_ids, int32_t* out_pos, cudaStream_t s,
                         int64_t* launches) {
     const int64_t total = ntot * (n_specs + 1);
-    launch_pdl(k_compact_all, static_cast<unsigned>((total + 255) / 256), 256, 0, s, 
+    k_compact_all<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
         sorted, ntot, n_specs, drop_sorted, drop_pos, n_drop, K, s_last, idx, kept_rank, kept_ids, out_pos);
     ++*launches;
 }
@@ -817,7 +813,6 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tiles_dev(const uint32_t*
                                                                    const uint32_t* __restrict__ d_n,
                                                                    uint32_t* __restrict__ tile_sums,
                                                                    unsigned* __restrict__ ticket) {
-    pdl_entry();
     const int64_t n = *d_n;
     __shared__ uint32_t warp_tot[32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -913,7 +908,7 @@ void launch_scan_bins_dev(const uint32_t* hist, uint32_t* bin_start, uint32_t* c
                           int64_t* launches) {
     const unsigned tiles = static_cast<unsigned>((cap + kScanTile - 1) / kScanTile);
     const unsigned grid = tiles < static_cast<unsigned>(kNumSMs) ? tiles : static_cast<unsigned>(kNumSMs);
-    launch_pdl(k_scan_tiles_dev, grid, kScanThreads, 0, s, hist, bin_start, cursor, d_nbins, tile_sums, ticket);
+    k_scan_tiles_dev<<<grid, kScanThreads, 0, s>>>(hist, bin_start, cursor, d_nbins, tile_sums, ticket);
     *launches += 1;
 }
 

@@ -331,6 +331,27 @@ def test_frame_stream_equals_per_frame(prec, ctx32, ctx16):
         ctx.run_frames([frames[1], bad], cfg)
 
 
+@pytest.mark.parametrize("prec", ["bf16", "bf16_3k"])
+def test_repeated_calls_bitwise_stable(prec):
+    """Repeated host-API and frame-stream calls on one context (workspaces reused, a
+    bin-overflow frame in the mix) reproduce the first results bit for bit -- a guard
+    against cross-stream / cross-launch races (it caught one: programmatic dependent
+    launch on the schedule kernels)."""
+    ctx = F.Context(0, precision=prec)
+    cfg = F.FwaConfig(n_blocks=4)
+    ctx.load_params(cfg, F.init_backbone_params(cfg, 42))
+    frames = [F.make_pillars(F.SCENES[s], seed) for s, seed in (("F10", 1), ("F30", 2), ("PINNED", 4), ("F30", 5))]
+    rng = np.random.default_rng(9)
+    frames.insert(2, F.PillarSet(rng.uniform(-5000, 5000, size=(3000, 2)), rng.normal(size=(3000, 128))))
+    ref = [ctx.run_backbone(ps, cfg) for ps in frames]
+    for _ in range(3):
+        for ps, r0 in zip(frames, ref):
+            r = ctx.run_backbone(ps, cfg)
+            assert np.array_equal(r.kept_indices, r0.kept_indices) and np.array_equal(r.features, r0.features)
+        for o, r0 in zip(ctx.run_frames(frames, cfg), ref):
+            assert np.array_equal(o.kept_indices, r0.kept_indices) and np.array_equal(o.features, r0.features)
+
+
 def test_errors_mirror_reference(ctx32):
     cfg = F.FwaConfig(d_model=16, n_heads=4, d_ff=32, group_size=8, n_blocks=2)
     blob = F.init_backbone_params(cfg, 1)
