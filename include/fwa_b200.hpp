@@ -60,16 +60,7 @@ public:
     // resident ones, then runs the backbone.
     backbone::BackboneOutput run(const geometry::PillarSet& pillars, const backbone::FwaConfig& cfg,
                                  const backbone::BackboneParams& params) {
-        backbone::validate(cfg);
-        const fwa_config_t cc = to_c(cfg);
-        std::ostringstream os;
-        for (const auto& b : params.blocks) kernels::save_params(os, b);
-        const std::string blob = os.str();
-        if (blob != blob_) {
-            throw_status(fwa_b200_load_params(ctx_.get(), &cc, blob.data(), blob.size()),
-                         fwa_b200_last_error(ctx_.get()));
-            blob_ = blob;
-        }
+        const fwa_config_t cc = upload(cfg, params);
         const std::size_t n = pillars.size();
         const std::size_t d = static_cast<std::size_t>(cfg.d_model);
         // Optional input projection (backbone.hpp:179-190): a host GEMV per pillar in
@@ -100,34 +91,106 @@ public:
             coords[2 * i] = pillars.coords[i][0];
             coords[2 * i + 1] = pillars.coords[i][1];
         }
-        backbone::BackboneOutput out;
-        out.n_input = n;
-        out.features = Dense2<float>(n, d);
-        std::vector<int32_t> kept(n), dropped(n ? n : 1), dpb(static_cast<std::size_t>(cfg.n_blocks));
-        fwa_output_t o{out.features.data.data(), kept.data(), dropped.data(), dpb.data(), nullptr, 0, 0, 0};
+        Frame fr(pillars, cfg);
         throw_status(fwa_b200_backbone_forward(ctx_.get(), coords.data(), feats, f64,
-                                               static_cast<int64_t>(n), &cc, &o),
+                                               static_cast<int64_t>(n), &cc, &fr.o),
                      fwa_b200_last_error(ctx_.get()));
-        const std::size_t k = static_cast<std::size_t>(o.n_kept);
-        out.features.rows = k;
-        out.features.data.resize(k * d);
-        out.kept_indices.assign(kept.begin(), kept.begin() + static_cast<std::ptrdiff_t>(k));
-        out.coords.reserve(k);
-        for (std::size_t i = 0; i < k; ++i) out.coords.push_back(pillars.coords[static_cast<std::size_t>(kept[i])]);
-        std::size_t w = 0;
-        for (int b = 0; b < cfg.n_blocks; ++b) {
-            const std::size_t m = static_cast<std::size_t>(dpb[static_cast<std::size_t>(b)]);
-            out.dropped_indices.emplace_back(dropped.begin() + static_cast<std::ptrdiff_t>(w),
-                                             dropped.begin() + static_cast<std::ptrdiff_t>(w + m));
-            out.stats.dropped_per_block.push_back(static_cast<int>(m));
-            w += m;
+        return fr.finish(pillars, cfg);
+    }
+
+    // A sequence of frames, each exactly run(frames[i], cfg, params), with the PCIe copies of
+    // neighbouring frames pipelined against the compute (fwa_b200_backbone_forward_frames).
+    std::vector<backbone::BackboneOutput> run_frames(const std::vector<geometry::PillarSet>& frames,
+                                                     const backbone::FwaConfig& cfg,
+                                                     const backbone::BackboneParams& params) {
+        std::vector<backbone::BackboneOutput> outs;
+        if (params.input_proj) {  // host projection per frame: no streaming to gain
+            for (const auto& f : frames) outs.push_back(run(f, cfg, params));
+            return outs;
         }
-        out.stats.cache.computed = o.cache_computed;
-        out.stats.cache.hits = o.cache_hits;
-        return out;
+        const fwa_config_t cc = upload(cfg, params);
+        const std::size_t d = static_cast<std::size_t>(cfg.d_model);
+        std::vector<std::vector<double>> coords(frames.size());
+        std::vector<Frame> fr;
+        fr.reserve(frames.size());
+        std::vector<const double*> cp(frames.size());
+        std::vector<const void*> fp(frames.size());
+        std::vector<int64_t> ns(frames.size());
+        std::vector<fwa_output_t> os(frames.size());
+        for (std::size_t i = 0; i < frames.size(); ++i) {
+            const auto& p = frames[i];
+            if (p.features.cols != d) throw fwa::shape_error("backbone: pillar width != d_model and no input projection");
+            coords[i].resize(2 * p.size());
+            for (std::size_t j = 0; j < p.size(); ++j) {
+                coords[i][2 * j] = p.coords[j][0];
+                coords[i][2 * j + 1] = p.coords[j][1];
+            }
+            fr.emplace_back(p, cfg);
+            cp[i] = coords[i].data();
+            fp[i] = p.features.data.data();
+            ns[i] = static_cast<int64_t>(p.size());
+            os[i] = fr.back().o;
+        }
+        throw_status(fwa_b200_backbone_forward_frames(ctx_.get(), static_cast<int>(frames.size()), cp.data(), fp.data(),
+                                                      1, ns.data(), &cc, os.data()),
+                     fwa_b200_last_error(ctx_.get()));
+        for (std::size_t i = 0; i < frames.size(); ++i) {
+            fr[i].o = os[i];
+            outs.push_back(fr[i].finish(frames[i], cfg));
+        }
+        return outs;
     }
 
 private:
+    // params -> FWAP records (kernels.hpp:151-175), uploaded when they differ from the resident ones
+    fwa_config_t upload(const backbone::FwaConfig& cfg, const backbone::BackboneParams& params) {
+        backbone::validate(cfg);
+        const fwa_config_t cc = to_c(cfg);
+        std::ostringstream os;
+        for (const auto& b : params.blocks) kernels::save_params(os, b);
+        const std::string blob = os.str();
+        if (blob != blob_) {
+            throw_status(fwa_b200_load_params(ctx_.get(), &cc, blob.data(), blob.size()),
+                         fwa_b200_last_error(ctx_.get()));
+            blob_ = blob;
+        }
+        return cc;
+    }
+
+    // one frame's output buffers and the BackboneOutput rebuilt from them
+    struct Frame {
+        backbone::BackboneOutput out;
+        std::vector<int32_t> kept, dropped, dpb;
+        fwa_output_t o{};
+        Frame(const geometry::PillarSet& p, const backbone::FwaConfig& cfg)
+            : kept(p.size()), dropped(p.size() ? p.size() : 1), dpb(static_cast<std::size_t>(cfg.n_blocks)) {
+            out.n_input = p.size();
+            out.features = Dense2<float>(p.size(), static_cast<std::size_t>(cfg.d_model));
+            o = fwa_output_t{out.features.data.data(), kept.data(), dropped.data(), dpb.data(), nullptr, 0, 0, 0};
+        }
+        Frame(Frame&&) = default;
+        backbone::BackboneOutput finish(const geometry::PillarSet& pillars, const backbone::FwaConfig& cfg) {
+            const std::size_t d = static_cast<std::size_t>(cfg.d_model);
+            const std::size_t k = static_cast<std::size_t>(o.n_kept);
+            out.features.rows = k;
+            out.features.data.resize(k * d);
+            out.kept_indices.assign(kept.begin(), kept.begin() + static_cast<std::ptrdiff_t>(k));
+            out.coords.reserve(k);
+            for (std::size_t i = 0; i < k; ++i) out.coords.push_back(pillars.coords[static_cast<std::size_t>(kept[i])]);
+            std::size_t w = 0;
+            for (int b = 0; b < cfg.n_blocks; ++b) {
+                const std::size_t m = static_cast<std::size_t>(dpb[static_cast<std::size_t>(b)]);
+                out.dropped_indices.emplace_back(dropped.begin() + static_cast<std::ptrdiff_t>(w),
+                                                 dropped.begin() + static_cast<std::ptrdiff_t>(w + m));
+                out.stats.dropped_per_block.push_back(static_cast<int>(m));
+                w += m;
+            }
+            out.stats.cache.computed = o.cache_computed;
+            out.stats.cache.hits = o.cache_hits;
+            return std::move(out);
+        }
+    };
+
     struct Del {
         void operator()(fwa_b200_ctx* c) const { fwa_b200_ctx_destroy(c); }
     };

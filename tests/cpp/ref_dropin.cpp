@@ -4,6 +4,7 @@
 // tests/test_gpu_integration.py on the GPU box.  Prints one JSON line.
 #include <cmath>
 #include <cstdio>
+#include <vector>
 
 #include "fwa/backbone.hpp"
 #include "fwa/geometry.hpp"
@@ -37,9 +38,24 @@ int main() {
     } catch (const fwa::numeric_error&) {
         threw = true;
     }
+    // a frame sequence through the streamed entry point: each output == its own single call
+    std::vector<geometry::PillarSet> frames;
+    for (std::uint64_t sd : {43ull, 44ull, 45ull})
+        frames.push_back(geometry::pillarize(geometry::generate_synthetic(spec, sd), 0.32,
+                                             geometry::random_pillar_params(2, 128, sd)));
+    b200::Backbone dev(0);
+    const auto outs = dev.run_frames(frames, cfg, params);
+    bool stream_equal = outs.size() == frames.size();
+    for (std::size_t i = 0; stream_equal && i < frames.size(); ++i) {
+        const auto one = dev.run(frames[i], cfg, params);
+        stream_equal = outs[i].features.data == one.features.data && outs[i].kept_indices == one.kept_indices &&
+                       outs[i].dropped_indices == one.dropped_indices && outs[i].coords == one.coords &&
+                       outs[i].stats.dropped_per_block == one.stats.dropped_per_block;
+    }
     std::printf("{\"n\": %zu, \"n_kept\": %zu, \"ints_equal\": %s, \"rel_err\": %.3e, \"numeric_error\": %s, "
-                "\"cache\": [%d, %d]}\n",
+                "\"cache\": [%d, %d], \"stream_equal\": %s}\n",
                 pillars.size(), got.kept_indices.size(), ints ? "true" : "false", max_abs / max_ref,
-                threw ? "true" : "false", got.stats.cache.computed, got.stats.cache.hits);
-    return ints && threw && max_abs / max_ref <= 1e-2 ? 0 : 1;
+                threw ? "true" : "false", got.stats.cache.computed, got.stats.cache.hits,
+                stream_equal ? "true" : "false");
+    return ints && threw && stream_equal && max_abs / max_ref <= 1e-2 ? 0 : 1;
 }

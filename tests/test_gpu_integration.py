@@ -20,3 +20,4 @@ def test_reference_caller_drop_in():
     assert r.returncode == 0, (r.stdout, r.stderr)
     assert out["ints_equal"] and out["numeric_error"]
     assert out["rel_err"] <= 1e-2
+    assert out["stream_equal"]  # Backbone::run_frames == run per frame, bit for bit
