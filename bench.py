@@ -406,7 +406,10 @@ def run_ours(args, rank, world, local_rank, dist):
         "config": {"workload": WORKLOAD, "pillars_per_frame": n, "kept_per_frame": nk,
                    "frames_per_step_per_gpu": 1, "parallelism": f"frame-parallel x{world}",
                    "l2": "flushed by a 256 MiB write before every timed step",
-                   "precision": "bf16 tensor cores, fp32 accumulate/LN/softmax/residual"},
+                   "precision": "bf16 tensor cores, fp32 accumulate/LN/softmax/residual",
+                   "input": "value: HBM-resident f32 features (fwa_b200_backbone_forward_device's format, the "
+                            "reference's backbone.hpp:195 cast done before the step); e2e: the f64 PillarSet "
+                            "from host memory, cast on the GPU inside block 0's gather"},
         "e2e": {"value": e2e_value, "unit": "pillars/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_frame": 1e3 * e2e_max / args.steps,
                 "api": "fwa_b200_backbone_forward_frames over the step's frames from pinned host buffers "
