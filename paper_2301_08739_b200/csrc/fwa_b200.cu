@@ -842,7 +842,8 @@ void forward_device(fwa_b200_ctx* c, const double* d_coords, const float* d_feat
     CUDA_OK(cudaStreamWaitEvent(st, c->ev_join, 0));
     if (feats_ready) CUDA_OK(cudaStreamWaitEvent(st, feats_ready, 0));  // block 0 reads them
     float* X = ws<float>(c, "X", static_cast<size_t>(S.ntot) * d);
-    for (int b = 0; b < cfg->n_blocks; ++b) {
+    static const bool skip_blocks = std::getenv("FWA_B200_DEBUG_SCHEDULE_ONLY") != nullptr;  // timing probe
+    for (int b = 0; b < (skip_blocks ? 0 : cfg->n_blocks); ++b) {
         const int s = b % 4;
         const int32_t* idx = S.idx + S.K * s;
         const bool last = b == cfg->n_blocks - 1;
