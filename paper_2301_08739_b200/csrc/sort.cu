@@ -266,7 +266,9 @@ __global__ void __launch_bounds__(256) k_bins_hist(const long long* __restrict__
     const long long bin = sb.base + static_cast<long long>(f) * sb.bins_per_frame +
                           (w.x - sb.min_major) * sb.range_minor + (w.y - sb.min_minor);
     bin_of[e] = static_cast<uint32_t>(bin);
-    atomicAdd(hist + bin, 1u);
+    // warp-aggregated: consecutive pillar ids mostly share a window
+    const unsigned grp = __match_any_sync(__activemask(), static_cast<uint32_t>(bin));
+    if ((threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(hist + bin, static_cast<uint32_t>(__popc(grp)));
 }
 
 void launch_bins_hist(const long long* win, int64_t ntot, int n_specs, const int64_t* d_frame_off,
@@ -299,7 +301,15 @@ __global__ void __launch_bounds__(256) k_bin_scatter(const uint32_t* __restrict_
     if (e >= total) return;
     if (d_nbins && *d_nbins == 0u) return;
     const uint32_t b = bin_of[e];
-    const uint32_t pos = atomicAdd(cursor + b, 1u) + (tile_off ? tile_off[b / kScanTile] : 0u);
+    // warp-aggregated slot claims (the order inside a bin is irrelevant: the rank sort
+    // orders by (key, key, id))
+    const unsigned grp = __match_any_sync(__activemask(), b);
+    const int lane = threadIdx.x & 31, leader = __ffs(grp) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(cursor + b, static_cast<uint32_t>(__popc(grp)));
+    base = __shfl_sync(grp, base, leader);
+    const uint32_t pos = base + static_cast<uint32_t>(__popc(grp & ((1u << lane) - 1u))) +
+                         (tile_off ? tile_off[b / kScanTile] : 0u);
     pre[pos] = static_cast<int32_t>(e % ntot);
     pre_bin[pos] = b;
     // the window-local keys travel with the id as order-preserving integer images: the
