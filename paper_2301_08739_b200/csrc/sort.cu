@@ -162,10 +162,20 @@ __global__ void __launch_bounds__(256) k_sort_keys(const double* __restrict__ co
     const int s = blockIdx.y;
     const bool axis_y = s >= 2, shift = (s & 1) != 0;
     long long wM = LLONG_MAX, wm = LLONG_MAX, xM = LLONG_MIN, xm = LLONG_MIN;
-    // grid-stride: few CTAs per spec -> few partials and few last-CTA tickets
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < ntot;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const double2 c = reinterpret_cast<const double2*>(coords)[i];
+    // grid-stride: few CTAs per spec -> few partials and few last-CTA tickets; the
+    // coordinates of 4 strides are loaded up front (independent loads in flight)
+    const int64_t gs = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i0 < ntot; i0 += 4 * gs) {
+      double2 cc[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+          cc[u] = i0 + u * gs < ntot ? __ldg(reinterpret_cast<const double2*>(coords) + i0 + u * gs)
+                                     : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = i0 + u * gs;
+        if (i >= ntot) break;
+        const double2 c = cc[u];
         double cx = c.x, cy = c.y;
         if (shift) {
             cx = __dadd_rn(cx, __ddiv_rn(w_x, 2.0));
@@ -184,6 +194,7 @@ __global__ void __launch_bounds__(256) k_sort_keys(const double* __restrict__ co
         xM = a > xM ? a : xM;
         wm = b < wm ? b : wm;
         xm = b > xm ? b : xm;
+      }
     }
     wM = wmin(wM);
     xM = wmax(xM);
