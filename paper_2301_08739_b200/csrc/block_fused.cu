@@ -579,7 +579,7 @@ struct FusedArgs {
 
 #define FTR(k)                                                                                  \
     do {                                                                                        \
-        if (a.trace && threadIdx.x == 0 && (k) < 56)                                            \
+        if (a.trace && threadIdx.x == 0 && (k) < 49)                                            \
             a.trace[blockIdx.x * 64 + (k)] = static_cast<unsigned long long>(clock64());        \
     } while (0)
 // global-timer (ns) marks in slots 56..63: 63 entry, 60 after griddepcontrol.wait,
@@ -1145,6 +1145,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         __syncthreads();
         store_out(pKV, 0, 16);
     }
+    if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 64 + 49] = static_cast<unsigned long long>(clock64());
     FTRG(61);
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(a.nonfinite, 1);
     fence_before_sync();

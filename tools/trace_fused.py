@@ -27,9 +27,15 @@ for cta in (0, 1, 40, 41, 146, 147):
     row = t[cta]
     print(f"cta {cta}: setup {row[1] - row[0] if row[1] else 0}")
     for u in range(3):
-        if 1 + 16 * u + 15 >= 56: break
+        if 1 + 16 * u + 15 >= 49: break
         b = 1 + 16 * u
         if not row[b]:
             break
         seg = [(names[k], int(row[b + k] - row[b + k - 1])) for k in range(1, 16) if row[b + k]]
         print("   u%d total %d: " % (u, int(row[b + 15] - row[b])) + " ".join(f"{n}={v}" for n, v in seg))
+
+clk = (t[:, 49] - t[:, 0]).astype(np.float64)
+ns = (g[:, 61] - g[:, 59]).astype(np.float64)
+ok = (clk > 0) & (ns > 0)
+print(f"SM clock inside the unit loop: median {np.median(clk[ok] / ns[ok]) * 1e3:.0f} MHz "
+      f"(min {np.min(clk[ok] / ns[ok]) * 1e3:.0f}, max {np.max(clk[ok] / ns[ok]) * 1e3:.0f})")
