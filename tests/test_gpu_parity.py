@@ -487,7 +487,7 @@ def test_fused_block_kernel_partial_units(ctx16, n):
     assert O.max_rel_err(r.features, w["features"]) <= TOL_BF16
 
 
-@pytest.mark.parametrize("G", [16, 33, 100, 128])
+@pytest.mark.parametrize("G", [16, 32, 33, 48, 96, 100, 128])  # + BASELINE config 5's G sweep (32..128)
 def test_fused_block_kernel_group_sizes_backbone(ctx16, G):
     """Full backbone through the fused kernel at non-default group sizes (other unit
     geometries and row splits)."""
