@@ -533,6 +533,63 @@ FWA_DEVINL void ln1_row_to_image(const float (&v)[16], const uint2 (&ph)[4], boo
     bad |= !(isfinite(ps.x) && isfinite(ps.y));
 }
 
+// ln1_row_to_image for a thread's two rows at once: the two rows' shuffle reductions are
+// independent chains, interleaved
+FWA_DEVINL void ln1_rows2_to_image(const float (&v)[2][16], const uint2 (&ph)[2][4], const bool (&valid)[2],
+                                   const int (&r)[2], int sub, const float* sG, uint8_t* A, bool& bad) {
+    float sm[2] = {0.f, 0.f};
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) sm[h] += v[h][j];
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+        const float t0 = __shfl_xor_sync(0xffffffffu, sm[0], o), t1 = __shfl_xor_sync(0xffffffffu, sm[1], o);
+        sm[0] += t0;
+        sm[1] += t1;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+        if (!isfinite(sm[h])) {  // a non-finite input makes the row sum non-finite
+#pragma unroll
+            for (int j = 0; j < 16; ++j) bad |= !isfinite(v[h][j]);
+        }
+    const float mean[2] = {sm[0] * (1.0f / 128.0f), sm[1] * (1.0f / 128.0f)};
+    float sq[2] = {0.f, 0.f};
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) sq[h] = fmaf(v[h][j] - mean[h], v[h][j] - mean[h], sq[h]);
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+        const float t0 = __shfl_xor_sync(0xffffffffu, sq[0], o), t1 = __shfl_xor_sync(0xffffffffu, sq[1], o);
+        sq[0] += t0;
+        sq[1] += t1;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const float inv = 1.0f / sqrtf(sq[h] * (1.0f / 128.0f) + 1e-5f);
+        __half2 pesum = __floats2half2_rn(0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int c = 32 * i + 4 * sub;
+            const float4 g = *reinterpret_cast<const float4*>(sG + c);
+            const __half2 h0 = *reinterpret_cast<const __half2*>(&ph[h][i].x);
+            const __half2 h1 = *reinterpret_cast<const __half2*>(&ph[h][i].y);
+            pesum = __hadd2(pesum, __hadd2(h0, h1));
+            const float2 p0 = __half22float2(h0), p1 = __half22float2(h1);
+            uint32_t o0 = pack_bf16x2(fmaf(g.x, (v[h][4 * i] - mean[h]) * inv, p0.x),
+                                      fmaf(g.y, (v[h][4 * i + 1] - mean[h]) * inv, p0.y));
+            uint32_t o1 = pack_bf16x2(fmaf(g.z, (v[h][4 * i + 2] - mean[h]) * inv, p1.x),
+                                      fmaf(g.w, (v[h][4 * i + 3] - mean[h]) * inv, p1.y));
+            if (!valid[h]) o0 = o1 = 0u;
+            *reinterpret_cast<uint2*>(A + sw128_offset(r[h], c, 128)) = make_uint2(o0, o1);
+        }
+        const float2 ps = __half22float2(pesum);
+        bad |= !(isfinite(ps.x) && isfinite(ps.y));
+    }
+}
+
 // f32 row staging: row r (512 B) chunk c (16 B) at r*512 + ((c ^ (r & 7)) * 16)
 FWA_DEVINL uint32_t stage_off(int r, int c) { return static_cast<uint32_t>(r * 512 + ((c ^ (r & 7)) << 4)); }
 // 16 B global -> shared without registers (LDGSTS); src_bytes 0 zero-fills
@@ -818,17 +875,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
             unit_ids(a.ridx, u + npairs, gid);
             cp_async_wait_all();
             __syncthreads();  // every thread's row chunks landed
+            {
+                float v[2][16];
+                const int rr[2] = {warp * 4 + rl, 64 + warp * 4 + rl};
+                const bool vv[2] = {rr[0] < nloc, rr[1] < nloc};
 #pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-                const int r = hf * 64 + warp * 4 + rl;
-                float v[16];
+                for (int hf = 0; hf < 2; ++hf)
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const float4 f = *reinterpret_cast<const float4*>(xs + r * kXSPitch + (8 * i + sub) * 16);
-                    v[4 * i] = f.x; v[4 * i + 1] = f.y; v[4 * i + 2] = f.z; v[4 * i + 3] = f.w;
-                }
-                ln1_row_to_image(v, pe[hf], r < nloc, r, sub, sVec + 896, pRA, bad);
-                if (hf == 0) FTR(tb + 1);
+                    for (int i = 0; i < 4; ++i) {
+                        const float4 f = *reinterpret_cast<const float4*>(xs + rr[hf] * kXSPitch + (8 * i + sub) * 16);
+                        v[hf][4 * i] = f.x; v[hf][4 * i + 1] = f.y; v[hf][4 * i + 2] = f.z; v[hf][4 * i + 3] = f.w;
+                    }
+                ln1_rows2_to_image(v, pe, vv, rr, sub, sVec + 896, pRA, bad);
+                FTR(tb + 1);
             }
             {  // the residual rows -> TMEM [384, 512)
                 float xr[32];
