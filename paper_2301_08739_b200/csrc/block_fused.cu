@@ -975,7 +975,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         fence_after_sync();
         FTR(tb + 3);
         // every thread: heads 2cq, 2cq+1 of its row -> Q (R_A, in place of O), K|V rows
-#pragma unroll 1
+#pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
             const int h = 2 * cq + hh;
             uint32_t qv[16], kv[16], vv[16];
