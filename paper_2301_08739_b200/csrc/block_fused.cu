@@ -15,14 +15,16 @@
 // weight matrices (256 KB bf16) fit the pair's shared memory: 128 KB per CTA.  Nothing
 // between the gather and the scatter leaves the SM pair:
 //   R_A  (32 KB, SW128 image): LN1 out -> [QKV MMA] -> Q, overwritten in place by the
-//        attention output O -> [out-proj MMA] -> LN2 out -> [FFN1] -> GELU half b
-//        -> [FFN2] -> fp32 output staging
+//        attention output O -> [out-proj MMA] -> LN2 out -> [FFN1] -> GELU half b -> [FFN2]
 //   K/V  (92 KB = the W2 slot + R_X): K|V rows of all 8 heads (528 B pitch:
 //        conflict-free ldmatrix), plus the rows of the one group that straddles the two
 //        CTAs, PUSHED by the peer over DSMEM (st.async, completing transaction bytes on
 //        the receiver's mbarrier); W2 is re-fetched from L2 into its slot (TMA bulk) once
-//        the unit's attention is done
-//   R_X  (60 KB): LN1 fp32 staging -> ... -> GELU half a (SW128 image) -> [FFN2]
+//        the unit's attention is done.  Between FFN2 and the next unit's epilogue the
+//        region holds XS, the NEXT unit's fp32 x rows (cp.async, issued as soon as FFN2
+//        completes), and then the staging of THIS unit's output rows, which warps 1-15
+//        store while the next unit's QKV MMA runs (warp 0 holds the MMA issuer)
+//   R_X  (60 KB, inside K/V): GELU half a (SW128 image) -> [FFN2]
 //   TMEM (512 columns): QKV [0,384) | the gathered fp32 residual rows [384,512), onto
 //        which the out-proj MMA accumulates | FFN1 U [128,384) | FFN2 O [0,128) | LN2
 //        row-statistics exchange [0,8)
@@ -30,15 +32,18 @@
 // CTAs need the same number of attention task rounds); padding rows (A = 0) fill each
 // CTA's 128 MMA rows.
 // The leader (rank 0) thread 0 issues every MMA after both CTAs arrive on its "ready"
-// mbarrier (remote arrive from rank 1); commits are multicast to both CTAs.
+// mbarrier (remote arrive from rank 1); commits are multicast to both CTAs.  Issuing
+// blocks the thread for the MMAs' tensor time (measured 64 clk per M256.N128.K16).
 //
-// Attention: tasks = (head, 16-query tile of one group part); QK^T and PV on
-// mma.sync.m16n8k16 (bf16, fp32 accumulate); softmax in fp32 with Q pre-scaled so that
-// S is the base-2 exponent: P = 2^S straight from the QK^T accumulators, no row-max pass
-// (shift invariance; a task whose row sums leave [2^-64, 2^64] is re-run with the max
-// shift), ex2 on the SFU with a quarter of the tiles on an FMA-pipe cubic, P rounded to
-// bf16 as the PV operand; the row sums come out of the PV MMA (an all-ones B fragment),
-// so they are the sums of exactly the P values multiplied with V.
+// Attention: tasks = (head, 16-query tile of one group part), two per warp interleaved
+// and streamed per 16-key slab; QK^T and PV on mma.sync.m16n8k16 (bf16, fp32
+// accumulate); softmax in fp32 with Q pre-scaled so that S is the base-2 exponent:
+// P = 2^S straight from the QK^T accumulators, no row-max pass (shift invariance; a task
+// whose row sums leave [2^-64, 2^64] is re-run with the max shift), ex2 on the SFU with 2
+// of 9 key tiles on an FMA-pipe cubic, P rounded to bf16 as the PV operand; the row sums
+// come out of the PV MMA (an all-ones B fragment), so they are the sums of exactly the P
+// values multiplied with V.  The straddling group's tasks run last, each warp waiting for
+// the peer's halo only before its first such task.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
