@@ -316,18 +316,27 @@ def run_ours(args, rank, world, local_rank, dist):
 
     # ---------------------------------------------------------------- config 4: one F250 scene
     # split by group ranges across the ranks, NCCL all-gather of each block's rows
+    # the secondary measurements never take the headline line down with them (a failure is
+    # reported in its object instead)
+    def secondary(fn, *a):
+        try:
+            return fn(*a)
+        except Exception as e:  # noqa: BLE001
+            torch.cuda.synchronize()
+            return {"error": f"{type(e).__name__}: {e}"[:400]}
+
     batch = None
     if not args.no_batch:
-        batch = run_batch_frames(args, F, ctx, cfg, dev, stream, rank, world, dist, flush)
+        batch = secondary(run_batch_frames, args, F, ctx, cfg, dev, stream, rank, world, dist, flush)
     points = None
     if world == 1 and not args.no_points:
-        points = run_points_pipeline(args, F, ctx, cfg, dev, stream, flush)
+        points = secondary(run_points_pipeline, args, F, ctx, cfg, dev, stream, flush)
     ew = None
     if world == 1 and not args.no_equal_window:
-        ew = run_equal_window(args, F, ctx, cfg, dev, stream, flush)
+        ew = secondary(run_equal_window, args, F, ctx, cfg, dev, stream, flush)
     split = None
     if not args.no_split:
-        split = run_split_scene(args, F, ctx, cfg, dev, stream, rank, world, dist, flush)
+        split = secondary(run_split_scene, args, F, ctx, cfg, dev, stream, rank, world, dist, flush)
 
     # ---------------------------------------------------------------- reduce over ranks
     t_dev = torch.tensor([dev_ms, e2e_stream_s, float(n), float(nk), e2e_s], dtype=torch.float64, device=dev)
