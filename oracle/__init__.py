@@ -88,6 +88,7 @@ def ref():
         lib.ref_config_json.restype = C.c_int64
         lib.ref_config_json.argtypes = [C.POINTER(CfgC), C.c_char_p, C.c_int64]
         lib.ref_fnv1a64_hex.argtypes = [C.c_void_p, C.c_int64, C.c_char_p]
+        lib.ref_bench_summarize.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_void_p]
         lib.ref_write_points.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                          C.c_int, C.c_int, C.c_uint64, C.c_char_p, C.c_int]
         lib.ref_block_backward.restype = C.c_int64
@@ -392,6 +393,14 @@ def ref_config_json(cfg):
     n = ref().ref_config_json(C.byref(cfg), buf, 4096)
     _check_ref(0 if n >= 0 else -n)
     return buf.value.decode()
+
+
+def ref_bench_summarize(samples, runs, warmup):
+    """bench::summarize (bench.hpp:124-143): (mean, p50, p95, outliers_excluded)."""
+    v = np.ascontiguousarray(samples, np.float64)
+    out = np.zeros(4, np.float64)
+    _check_ref(ref().ref_bench_summarize(_p(v), v.size, runs, warmup, _p(out)))
+    return float(out[0]), float(out[1]), float(out[2]), int(out[3])
 
 
 def ref_fnv1a64_hex(b: bytes) -> str:

@@ -178,6 +178,19 @@ int64_t ref_config_json(const CfgC* c, char* out, int64_t cap) {
     return rc ? -rc : n;
 }
 
+// bench.hpp:75-143 (percentile, 3x IQR exclusion, summarize) for the `fwa bench` protocol
+// parity: out = {mean, p50, p95, outliers_excluded}
+int ref_bench_summarize(const double* samples, int64_t n, int runs, int warmup, double* out4) {
+    return guarded([&] {
+        const std::vector<double> v(samples, samples + n);
+        const auto r = bench::summarize("x", 0, "", v, runs, warmup);
+        out4[0] = r.mean_ms;
+        out4[1] = r.p50_ms;
+        out4[2] = r.p95_ms;
+        out4[3] = r.outliers_excluded;
+    });
+}
+
 void ref_fnv1a64_hex(const void* bytes, int64_t n, char* out19) {
     const std::string h = bench::fnv1a64_hex(std::string(static_cast<const char*>(bytes), static_cast<size_t>(n)));
     std::memcpy(out19, h.c_str(), h.size() + 1);

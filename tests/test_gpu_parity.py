@@ -6,6 +6,7 @@ must be bit-exact.  Features: normwise max rel err (tests/test_kernels.cpp:25-33
 north-star tolerances).  Full-size frames are checked through size-independent
 properties (sortedness of the reference keys, permutation/partition invariants,
 zero-weight identity, determinism, batch == per-frame)."""
+import json
 import os
 
 import numpy as np
@@ -563,6 +564,35 @@ def test_gpu_pillarize_feeds_backbone(ctx16):
 
 
 # ----------------------------------------------------------------------------- `fwa attend` (§8f next-2)
+
+def test_fwa_bench_cli_modes(tmp_path):
+    """`fwa bench` (tools/fwa_bench.py, fwa_cli.cpp:249-281) in all three modes on a small
+    FWPC file: the reference's BenchResult document, its config digest, exit code 2 for an
+    unknown mode."""
+    import subprocess
+    import sys
+    from paper_2301_08739_b200.attend import config_digest
+    if not O.have_ref():
+        pytest.skip("reference oracle not built (point-file writer)")
+    scene = {"n_clusters": 6, "ppc_min": 150, "ppc_max": 300, "sigma": 1.5, "ext_x": 40.0, "ext_y": 40.0,
+             "n_bg": 500, "f_in": 2}
+    path = str(tmp_path / "pts.fwpc")
+    O.ref_write_points(scene, 5, path, True)
+    tool = os.path.join(os.path.dirname(os.path.dirname(__file__)), "tools", "fwa_bench.py")
+    for mode in ("group", "global", "equal-window"):
+        r = subprocess.run([sys.executable, tool, path, "--mode", mode, "--runs", "4", "--warmup", "1"],
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr
+        j = json.loads(r.stdout)
+        assert j["name"] == mode and j["runs"] == 4 and j["warmup"] == 1 and j["n_points"] > 0
+        assert j["config_digest"] == config_digest(F.FwaConfig())
+        w = j["wall_time_ms"]
+        assert 0 < w["p50"] <= w["p95"] and w["mean"] > 0
+        if mode == "group":
+            assert j["stage_ms"].get("block_fused", 0) > 0 and j["stage_ms"].get("schedule", 0) > 0
+    r = subprocess.run([sys.executable, tool, path, "--mode", "nope"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 2
+
 
 def test_attend_json_matches_reference(tmp_path, ctx16):
     """`fwa attend` on the B200 path (points -> GPU pillarize -> GPU backbone -> GPU row

@@ -133,3 +133,24 @@ def test_attend_cache_and_drops_match_port():
                                                                              n_blocks=nb), blob)
         (comp, hit), drops = cache_and_drops(n, F.FwaConfig(n_blocks=nb))
         assert (comp, hit) == tuple(w["cache"]) and drops == list(w["dropped_per_block"])
+
+
+@pytest.mark.skipif(not O.have_ref(), reason="oracle/_ref not built")
+def test_bench_protocol_matches_reference():
+    """`fwa bench` protocol (bench.hpp:75-143): linear-interpolation percentiles, the 3x IQR
+    outlier exclusion and the mean over the kept samples -- bit-identical to the compiled
+    reference on random samples with injected outliers."""
+    from paper_2301_08739_b200 import benchcli as B
+    rng = np.random.default_rng(11)
+    for n in (1, 2, 3, 4, 5, 9, 50, 101):
+        for trial in range(5):
+            s = list(rng.gamma(2.0, 1.0, size=n))
+            if n >= 5 and trial % 2:
+                s[n // 2] = 1e3
+                s[-1] = -5.0
+            want = O.ref_bench_summarize(s, n, 3)
+            got = B.summarize("group", 10, "0x0", s, n, 3)
+            assert (got["wall_time_ms"]["mean"], got["wall_time_ms"]["p50"], got["wall_time_ms"]["p95"],
+                    got["outliers_excluded"]) == want
+    assert set(B.summarize("g", 1, "d", [1.0], 1, 0)) == {
+        "name", "n_points", "config_digest", "wall_time_ms", "outliers_excluded", "runs", "warmup", "stage_ms"}
