@@ -518,7 +518,7 @@ FWA_DEVINL void ln1_row_to_image(const float (&v)[16], const uint2 (&ph)[4], boo
     sq += __shfl_xor_sync(0xffffffffu, sq, 1);
     sq += __shfl_xor_sync(0xffffffffu, sq, 2);
     sq += __shfl_xor_sync(0xffffffffu, sq, 4);
-    const float inv = 1.0f / sqrtf(sq * (1.0f / 128.0f) + 1e-5f);
+    const float inv = rsqrtf(sq * (1.0f / 128.0f) + 1e-5f);
     __half2 pesum = __floats2half2_rn(0.f, 0.f);  // |PE| <= 1: the f16 sum cannot overflow
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -573,7 +573,7 @@ FWA_DEVINL void ln1_rows2_to_image(const float (&v)[2][16], const uint2 (&ph)[2]
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-        const float inv = 1.0f / sqrtf(sq[h] * (1.0f / 128.0f) + 1e-5f);
+        const float inv = rsqrtf(sq[h] * (1.0f / 128.0f) + 1e-5f);
         __half2 pesum = __floats2half2_rn(0.f, 0.f);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -1118,7 +1118,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
             tmem_st_wait();
             cta_sync_tc();
             ps = tmem_ld4(tmem + lane_off + 4);
-            const float inv = 1.0f / sqrtf(((ps.x + ps.y) + (ps.z + ps.w)) * (1.0f / 128.0f) + 1e-5f);
+            const float inv = rsqrtf(((ps.x + ps.y) + (ps.z + ps.w)) * (1.0f / 128.0f) + 1e-5f);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 uint32_t o[4];
