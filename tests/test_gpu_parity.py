@@ -323,6 +323,11 @@ def test_frame_stream_equals_per_frame(prec, ctx32, ctx16):
         assert [d.tolist() for d in o.dropped_indices] == [d.tolist() for d in r.dropped_indices]
         assert (o.stats.cache.computed, o.stats.cache.hits) == (r.stats.cache.computed, r.stats.cache.hits)
         assert o.stats.dropped_per_block == r.stats.dropped_per_block
+    # f32 features (feats_is_f64 = 0) through the same stream
+    f32 = [F.PillarSet(p.coords, p.features.astype(np.float32)) for p in frames[:3]]
+    for ps, o in zip(f32, ctx.run_frames(f32, cfg)):
+        r = ctx.run_backbone(ps, cfg)
+        assert np.array_equal(o.kept_indices, r.kept_indices) and np.array_equal(o.features, r.features)
     small = F.PillarSet(np.zeros((5, 2)), np.zeros((5, 128)))
     with pytest.raises(F.NumericError):  # backbone.hpp:218-222, raised before any frame runs
         ctx.run_frames([frames[0], small], cfg)
