@@ -189,11 +189,14 @@ def pcie_floor(h_in, h_out, dev, reps=10):
 
     once()
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(reps):
-        once()
-    torch.cuda.synchronize()
-    return 1e3 * (time.perf_counter() - t0) / reps
+    best = float("inf")
+    for _ in range(3):  # a floor: the best of three trials (PCIe throughput varies run to run)
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            once()
+        torch.cuda.synchronize()
+        best = min(best, 1e3 * (time.perf_counter() - t0) / reps)
+    return best
 
 
 def run_ours(args, rank, world, local_rank, dist):
