@@ -237,6 +237,9 @@ FWA_DEVINL uint32_t img_off(int row, int col) {
 // Q is stored pre-scaled by (1/sqrt(16)) * log2(e), so S = Q K^T is the softmax exponent
 // in base 2.
 constexpr float kScaleLog2 = 0.25f * 1.4426950408889634f;
+#ifndef FWA_GELU_POLY
+#define FWA_GELU_POLY 8  // every FWA_GELU_POLY-th activation on the FMA pipe (gelu2_poly)
+#endif
 #ifndef FWA_POLY_MASK
 #define FWA_POLY_MASK 2  // key tiles nt with bit (nt & 3) set take the FMA-pipe exp2
 #endif
@@ -621,6 +624,21 @@ FWA_DEVINL float tanh_approx(float x) {
 FWA_DEVINL float gelu2_fast(float x) {
     const float t = tanh_approx(x * fmaf(3.470089e-02f, x * x, 8.0015708e-01f));
     return fmaf(x, t, x);
+}
+
+// the same on the FMA pipe only (no SFU): 2 GELU(x) = x + E(x), E(x) = x erf(x/sqrt 2)
+// = x^2 Q(x^2) on |x| <= 4 (Q degree 6, minimax), |x| beyond: |GELU error| <= 1.9e-4.
+// 12 instructions per element with the bias add; a share of the elements takes this form
+// so the SFU and the FMA pipe finish together.
+FWA_DEVINL float gelu2_poly(float x) {
+    const float x2 = x * x;
+    float p = fmaf(4.556269317e-08f, x2, -3.197195383e-06f);
+    p = fmaf(p, x2, 9.591085836e-05f);
+    p = fmaf(p, x2, -1.628029277e-03f);
+    p = fmaf(p, x2, 1.754476875e-02f);
+    p = fmaf(p, x2, -1.291462034e-01f);
+    p = fmaf(p, x2, 7.957667112e-01f);
+    return x + (x2 > 16.0f ? fabsf(x) : p * x2);
 }
 
 struct FusedArgs {
@@ -1163,8 +1181,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int k = 8 * j + 2 * e;
+                    const float g1 = __uint_as_float(v[k + 1]) + b1[k + 1];
                     o[e] = pack_bf16x2(gelu2_fast(__uint_as_float(v[k]) + b1[k]),
-                                       gelu2_fast(__uint_as_float(v[k + 1]) + b1[k + 1]));
+                                       (FWA_GELU_POLY && (k + 1) % FWA_GELU_POLY == FWA_GELU_POLY - 1)
+                                           ? gelu2_poly(g1) : gelu2_fast(g1));
                 }
                 *reinterpret_cast<uint4*>(act + sw128_offset(row, c0 + 8 * j, 128)) = make_uint4(o[0], o[1], o[2], o[3]);
             }
