@@ -354,8 +354,8 @@ constexpr int kBinWarps = 8;
 
 // One thread per binned element: its rank among the elements of its window bin (integer
 // key images, then the original index -- key_less, flatten.hpp:41-47) by one pass over
-// the bin (n <= kWarpBin; the bin's elements are contiguous, so the loads of a warp are
-// shared-memory-like broadcasts out of L1).  Bigger bins are queued for
+// the bin (n <= kWarpBin; the bin's elements are contiguous and staged in shared memory
+// per CTA, so the loads of a warp are broadcasts).  Bigger bins are queued for
 // k_bin_sort_large by their first element.  Writes sorted[] and the inverse inv[].
 __global__ void __launch_bounds__(256) k_bin_rank(const uint32_t* __restrict__ bin_start,
                                                   uint32_t* __restrict__ hist, uint32_t n_bins,
@@ -381,6 +381,19 @@ __global__ void __launch_bounds__(256) k_bin_rank(const uint32_t* __restrict__ b
             return;
         }
     }
+    // every bin that holds one of this CTA's elements lies inside [c0, c0 + 512) (bins of
+    // up to kWarpBin elements): its keys and ids are staged in shared memory once
+    __shared__ ulonglong2 s_key[256 + 2 * kWarpBin];
+    __shared__ int s_id[256 + 2 * kWarpBin];
+    const int64_t c0 = static_cast<int64_t>(blockIdx.x) * blockDim.x - kWarpBin;
+    for (int i = threadIdx.x; i < 256 + 2 * kWarpBin; i += blockDim.x) {
+        const int64_t q = c0 + i;
+        if (q >= 0 && q < total) {
+            s_key[i] = pkey[q];
+            s_id[i] = pre[q];
+        }
+    }
+    __syncthreads();
     if (p >= total) return;
     const uint32_t b = pre_bin[p];
     const int64_t start = bin_start[b] + (tile_off ? tile_off[b / kScanTile] : 0u);
@@ -399,8 +412,8 @@ __global__ void __launch_bounds__(256) k_bin_rank(const uint32_t* __restrict__ b
     const uint32_t myh = static_cast<uint32_t>(me.y >> 32), myl = static_cast<uint32_t>(me.y);
 #pragma unroll 8
     for (int j = 0; j < nn; ++j) {
-        const ulonglong2 o = __ldg(pkey + start + j);
-        const int oid = __ldg(pre + start + j);
+        const ulonglong2 o = s_key[start + j - c0];
+        const int oid = s_id[start + j - c0];
         // (o.x, o.y, oid) < (me.x, me.y, my) lexicographically == the borrow of the 160-bit
         // subtraction o - me (every field unsigned, fixed width): one carry chain
         uint32_t b;
