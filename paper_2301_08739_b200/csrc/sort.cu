@@ -637,7 +637,8 @@ FWA_DEVINL int count_less(const int32_t* a, int n, int32_t v) {
 }
 
 // One CTA: sort the dropped ids, then (per spec) the positions of those ids in the
-// spec's full-set plan (inv[s][id]).  Bitonic sort in shared memory, n <= kMaxDrop.
+// spec's full-set plan (inv[s][id]).  Rank sort for n <= blockDim.x, else a bitonic sort
+// in shared memory, n <= kMaxDrop.
 constexpr int kMaxDrop = 8192;
 
 __global__ void __launch_bounds__(1024) k_drop_tables(const int32_t* __restrict__ sorted0, int n,
@@ -666,6 +667,18 @@ __global__ void __launch_bounds__(1024) k_drop_tables(const int32_t* __restrict_
         v[k] = x;
     }
     __syncthreads();
+    int32_t* dst = pass < 0 ? drop_sorted : drop_pos + static_cast<int64_t>(pass) * (n > 0 ? n : 1);
+    if (n <= static_cast<int>(blockDim.x)) {
+        // the usual case (one frame drops at most G - 1): the values are distinct (pillar ids,
+        // or their positions in one plan), so each one's rank is its count of smaller values
+        if (static_cast<int>(threadIdx.x) < n) {
+            const int32_t x = v[threadIdx.x];
+            int r = 0;
+            for (int j = 0; j < n; ++j) r += v[j] < x;
+            dst[r] = x;
+        }
+        return;
+    }
     for (int size = 2; size <= P; size <<= 1)
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
             for (int t = threadIdx.x; t < P / 2; t += blockDim.x) {
@@ -679,7 +692,6 @@ __global__ void __launch_bounds__(1024) k_drop_tables(const int32_t* __restrict_
             }
             __syncthreads();
         }
-    int32_t* dst = pass < 0 ? drop_sorted : drop_pos + static_cast<int64_t>(pass) * (n > 0 ? n : 1);
     for (int k = threadIdx.x; k < n; k += blockDim.x) dst[k] = v[k];
 }
 

@@ -302,6 +302,23 @@ def test_batch_equals_per_frame(prec, ctx32, ctx16):
         assert np.array_equal(res["features"][ko[i]:ko[i + 1]], r.features)
 
 
+def test_batch_many_drops_sorting_network(ctx16):
+    """A batch whose block-0 drops exceed one CTA's rank sort (> 1024: the drop tables take
+    the bitonic network): still bitwise equal to per-frame runs, dropped ids included."""
+    cfg = F.FwaConfig(n_blocks=2)
+    ctx16.load_params(cfg, F.init_backbone_params(cfg, 42))
+    frames = [F.make_pillars(F.SCENES["F10"], s) for s in range(100, 148)]
+    assert sum(p.size() % cfg.group_size for p in frames) > 1024
+    off = np.cumsum([0] + [p.size() for p in frames])
+    res = ctx16.run_batch(np.concatenate([p.coords for p in frames]),
+                          np.concatenate([p.features for p in frames]), off, cfg)
+    ko = np.concatenate([[0], np.cumsum(res["kept_per_frame"])])
+    for i, p in enumerate(frames):
+        r = ctx16.run_backbone(p, cfg)
+        assert np.array_equal(res["kept"][ko[i]:ko[i + 1]] - off[i], r.kept_indices)
+        assert np.array_equal(res["features"][ko[i]:ko[i + 1]], r.features)
+
+
 @pytest.mark.parametrize("prec", ["fp32", "bf16"])
 def test_frame_stream_equals_per_frame(prec, ctx32, ctx16):
     """Pipelined frame stream (fwa_b200_backbone_forward_frames): every frame bitwise
