@@ -18,6 +18,7 @@
  *   fwa_b200_positional_embedding    fwa::kernels::positional_embedding  include/fwa/kernels.hpp:364-393
  *   fwa_b200_load_params             fwa::kernels::load_params (FWAP records)  include/fwa/kernels.hpp:177-206
  *                                    + fwa::kernels::validate  kernels.hpp:75-90
+ *   fwa_b200_load_input_proj         BackboneParams::input_proj  include/fwa/backbone.hpp:74-81, 179-190
  *   fwa_b200_pillarize[_device]      fwa::geometry::pillarize on the GPU  include/fwa/geometry.hpp:246-300
  *   fwa_b200_row_checksums           `fwa attend` row_checksums  tools/fwa_cli.cpp:214-218
  *   fwa_b200_block_backward          fwa::kernels::fwa_block_backward  include/fwa/kernels.hpp:660-765
@@ -81,7 +82,22 @@ typedef struct fwa_config {
  * tail order, blocks concatenated); dropped_per_block: n_blocks;
  * block_perms (optional, may be NULL; single-frame calls only): n_blocks x N,
  * row b holds block b's permutation as local indices into that block's
- * active list (the parity hook for flatten::sort/group). */
+ * active list (the parity hook for flatten::sort/group).
+ * stage_ms: StageTimes (backbone.hpp:109-126) of this call, device time measured with
+ * CUDA events on the context stream, in FWA_STAGE_* order.  sort = the window sorts
+ * (keys, bins, per-bin exact sort), group = groups / drops / kept set (compaction);
+ * the fused block kernel does gather .. scatter in ONE launch, so its event time is
+ * apportioned to gather / attention / ffn / scatter by the kernel's own per-phase
+ * SM-clock counters.  Written by the host-buffer entry points. */
+enum fwa_stage {
+    FWA_STAGE_SORT = 0,
+    FWA_STAGE_GROUP = 1,
+    FWA_STAGE_GATHER = 2,
+    FWA_STAGE_ATTENTION = 3,
+    FWA_STAGE_FFN = 4,
+    FWA_STAGE_SCATTER = 5,
+    FWA_STAGES = 6
+};
 typedef struct fwa_output {
     float* features;
     int32_t* kept_indices;
@@ -91,7 +107,18 @@ typedef struct fwa_output {
     int64_t n_kept;
     int32_t cache_computed; /* SortStats::sorts_computed (flatten.hpp:82-86) */
     int32_t cache_hits;     /* SortStats::cache_hits */
+    double stage_ms[FWA_STAGES];
 } fwa_output_t;
+
+/* Per-frame results of a batch call: each frame is its own run_backbone, so each has
+ * its own kept count, block-0 drop count (N mod G; later blocks drop nothing: K is a
+ * multiple of G) and sort-cache statistics (the reference rule, backbone.hpp:224-234,
+ * 285-316, evaluated on that frame's N). */
+typedef struct fwa_frame_stats {
+    int64_t n_kept;
+    int32_t n_dropped;
+    int32_t cache_computed, cache_hits;
+} fwa_frame_stats_t;
 
 typedef struct fwa_b200_ctx fwa_b200_ctx;
 
@@ -99,6 +126,8 @@ typedef struct fwa_b200_ctx fwa_b200_ctx;
  * cudaStream_t; NULL = the context creates its own).  Calls on one context are
  * serialised on that stream; contexts on different devices run concurrently. */
 int fwa_b200_ctx_create(int device, void* cuda_stream, fwa_b200_ctx** out);
+/* The calling thread's current CUDA device (cudaGetDevice; 0 if none is set). */
+int fwa_b200_current_device(void);
 void fwa_b200_ctx_destroy(fwa_b200_ctx* ctx);
 const char* fwa_b200_last_error(const fwa_b200_ctx* ctx);
 int fwa_b200_set_precision(fwa_b200_ctx* ctx, int precision);
@@ -138,6 +167,16 @@ int fwa_b200_fast_path(const fwa_b200_ctx* ctx, const fwa_config_t* cfg);
 int fwa_b200_load_params(fwa_b200_ctx* ctx, const fwa_config_t* cfg, const void* fwap_blob,
                          size_t blob_len);
 
+/* BackboneParams::input_proj (backbone.hpp:74-81, 179-190): weight d_model x f_in
+ * (row-major fp32), bias d_model (NULL = zeros).  Resident like the block params;
+ * f_in == 0 removes it.  The group-range split API (fwa_b200_split_*) takes d_model rows
+ * and refuses to run while a projection is loaded (FWA_ERR_CONTRACT).  While one is loaded, the feats of every backbone_forward*
+ * call are N x f_in (f64 or f32; the device-resident entry point: f32) and are projected
+ * to d_model on the device, bit-exact with the reference's fp32 loop (acc = bias[j];
+ * acc += w[j][c] * (float)x[c] in c order, no FMA contraction). */
+int fwa_b200_load_input_proj(fwa_b200_ctx* ctx, int32_t d_model, int32_t f_in, const float* weight,
+                             const float* bias);
+
 /* run_backbone with HOST buffers: coords N x 2 f64 (pillar centres),
  * feats N x d_model, f64 if feats_is_f64 (cast to f32 on device exactly as
  * backbone.hpp:195-196) else f32.  Blocks until `out` is filled. */
@@ -148,13 +187,14 @@ int fwa_b200_backbone_forward(fwa_b200_ctx* ctx, const double* coords, const voi
 /* Same over F frames concatenated along rows: frame f owns rows
  * [frame_offsets[f], frame_offsets[f+1]).  Each frame is an independent
  * run_backbone (own sort, groups, drops); outputs are concatenated per frame
- * (kept ids are global row ids); out->n_kept is the total, kept_per_frame
- * (optional, capacity F) receives per-frame counts. cache stats are per frame
- * (identical for every frame). */
+ * (kept ids and dropped ids are global row ids, dropped ids frame by frame);
+ * out->n_kept is the total, out->dropped_per_block the sums over frames,
+ * out->cache_* are frame 0's; per_frame (optional, capacity F) receives every
+ * frame's own counts and cache statistics. */
 int fwa_b200_backbone_forward_batch(fwa_b200_ctx* ctx, const double* coords, const void* feats,
                                     int feats_is_f64, const int64_t* frame_offsets, int n_frames,
                                     const fwa_config_t* cfg, fwa_output_t* out,
-                                    int64_t* kept_per_frame);
+                                    fwa_frame_stats_t* per_frame);
 
 /* A stream of F independent frames in separate host buffers, each exactly one
  * fwa_b200_backbone_forward (same outputs, same errors), pipelined: frame f+1's inputs
@@ -294,6 +334,11 @@ int64_t fwa_b200_pillar_params(int32_t f_in, int32_t d_out, uint64_t seed, doubl
 /* init_backbone_params(cfg, f_in == d_model, seed) as FWAP records.  Returns
  * the blob length (out may be NULL to size) or -status. */
 int64_t fwa_b200_init_params(const fwa_config_t* cfg, uint64_t seed, void* out, size_t cap);
+/* init_backbone_params(cfg, f_in, seed) for any input width: when f_in != d_model the
+ * input projection weight (d_model x f_in, N(0, 0.1^2); its bias is 0) is drawn first into
+ * proj_weight, as the reference does, then the FWAP records. */
+int64_t fwa_b200_init_params_fin(const fwa_config_t* cfg, int32_t f_in, uint64_t seed, void* out, size_t cap,
+                                 float* proj_weight);
 
 #ifdef __cplusplus
 }

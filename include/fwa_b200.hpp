@@ -14,7 +14,9 @@
 #pragma once
 
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -56,43 +58,21 @@ public:
         if (fp32_check_mode) throw_status(fwa_b200_set_precision(c, FWA_PREC_FP32), nullptr);
     }
 
-    // Uploads params (FWAP records, kernels.hpp:151-175) when they differ from the
-    // resident ones, then runs the backbone.
+    // Uploads params (FWAP records, kernels.hpp:151-175, and the optional input projection,
+    // backbone.hpp:74-81) when they differ from the resident ones, then runs the backbone.
+    // The input projection (backbone.hpp:179-190) runs on the device, bit-exact.
     backbone::BackboneOutput run(const geometry::PillarSet& pillars, const backbone::FwaConfig& cfg,
                                  const backbone::BackboneParams& params) {
         const fwa_config_t cc = upload(cfg, params);
+        check_width(pillars, cfg, params);
         const std::size_t n = pillars.size();
-        const std::size_t d = static_cast<std::size_t>(cfg.d_model);
-        // Optional input projection (backbone.hpp:179-190): a host GEMV per pillar in
-        // the reference's order; never used on the north-star path (f_in == d_model).
-        std::vector<float> proj;
-        const void* feats = pillars.features.data.data();
-        int f64 = 1;
-        if (params.input_proj) {
-            const auto& pr = *params.input_proj;
-            if (pr.weight.cols != pillars.features.cols)
-                throw fwa::shape_error("backbone: input projection width mismatch");
-            proj.resize(n * d);
-            for (std::size_t r = 0; r < n; ++r)
-                for (std::size_t j = 0; j < d; ++j) {
-                    float acc = pr.bias[j];
-                    const float* w = pr.weight.row(j);
-                    for (std::size_t c = 0; c < pr.weight.cols; ++c)
-                        acc += w[c] * static_cast<float>(pillars.features(r, c));
-                    proj[r * d + j] = acc;
-                }
-            feats = proj.data();
-            f64 = 0;
-        } else if (pillars.features.cols != d) {
-            throw fwa::shape_error("backbone: pillar width != d_model and no input projection");
-        }
         std::vector<double> coords(2 * n);
         for (std::size_t i = 0; i < n; ++i) {
             coords[2 * i] = pillars.coords[i][0];
             coords[2 * i + 1] = pillars.coords[i][1];
         }
         Frame fr(pillars, cfg);
-        throw_status(fwa_b200_backbone_forward(ctx_.get(), coords.data(), feats, f64,
+        throw_status(fwa_b200_backbone_forward(ctx_.get(), coords.data(), pillars.features.data.data(), 1,
                                                static_cast<int64_t>(n), &cc, &fr.o),
                      fwa_b200_last_error(ctx_.get()));
         return fr.finish(pillars, cfg);
@@ -104,10 +84,6 @@ public:
                                                      const backbone::FwaConfig& cfg,
                                                      const backbone::BackboneParams& params) {
         std::vector<backbone::BackboneOutput> outs;
-        if (params.input_proj) {  // host projection per frame: no streaming to gain
-            for (const auto& f : frames) outs.push_back(run(f, cfg, params));
-            return outs;
-        }
         const fwa_config_t cc = upload(cfg, params);
         const std::size_t d = static_cast<std::size_t>(cfg.d_model);
         std::vector<std::vector<double>> coords(frames.size());
@@ -119,7 +95,7 @@ public:
         std::vector<fwa_output_t> os(frames.size());
         for (std::size_t i = 0; i < frames.size(); ++i) {
             const auto& p = frames[i];
-            if (p.features.cols != d) throw fwa::shape_error("backbone: pillar width != d_model and no input projection");
+            check_width(p, cfg, params);
             coords[i].resize(2 * p.size());
             for (std::size_t j = 0; j < p.size(); ++j) {
                 coords[i][2 * j] = p.coords[j][0];
@@ -154,7 +130,43 @@ private:
                          fwa_b200_last_error(ctx_.get()));
             blob_ = blob;
         }
+        // BackboneParams::input_proj (backbone.hpp:74-81): resident on the device as well
+        std::vector<float> pr;
+        if (params.input_proj) {
+            const auto& p = *params.input_proj;
+            pr.push_back(static_cast<float>(p.weight.rows));
+            pr.push_back(static_cast<float>(p.weight.cols));
+            pr.insert(pr.end(), p.weight.data.begin(), p.weight.data.end());
+            pr.insert(pr.end(), p.bias.begin(), p.bias.end());
+        }
+        if (pr != proj_) {
+            if (params.input_proj) {
+                const auto& p = *params.input_proj;
+                if (p.weight.rows != static_cast<std::size_t>(cfg.d_model) ||
+                    (!p.bias.empty() && p.bias.size() != p.weight.rows))
+                    throw fwa::shape_error("backbone: input projection shape mismatch");
+                throw_status(fwa_b200_load_input_proj(ctx_.get(), static_cast<int32_t>(p.weight.rows),
+                                                      static_cast<int32_t>(p.weight.cols), p.weight.data.data(),
+                                                      p.bias.empty() ? nullptr : p.bias.data()),
+                             fwa_b200_last_error(ctx_.get()));
+            } else {
+                throw_status(fwa_b200_load_input_proj(ctx_.get(), 0, 0, nullptr, nullptr),
+                             fwa_b200_last_error(ctx_.get()));
+            }
+            proj_ = pr;
+        }
         return cc;
+    }
+
+    // backbone.hpp:179-194: the projection's width, or d_model without one
+    static void check_width(const geometry::PillarSet& p, const backbone::FwaConfig& cfg,
+                            const backbone::BackboneParams& params) {
+        if (params.input_proj) {
+            if (params.input_proj->weight.cols != p.features.cols)
+                throw fwa::shape_error("backbone: input projection width mismatch");
+        } else if (p.features.cols != static_cast<std::size_t>(cfg.d_model)) {
+            throw fwa::shape_error("backbone: pillar width != d_model and no input projection");
+        }
     }
 
     // one frame's output buffers and the BackboneOutput rebuilt from them
@@ -166,7 +178,11 @@ private:
             : kept(p.size()), dropped(p.size() ? p.size() : 1), dpb(static_cast<std::size_t>(cfg.n_blocks)) {
             out.n_input = p.size();
             out.features = Dense2<float>(p.size(), static_cast<std::size_t>(cfg.d_model));
-            o = fwa_output_t{out.features.data.data(), kept.data(), dropped.data(), dpb.data(), nullptr, 0, 0, 0};
+            o = fwa_output_t{};
+            o.features = out.features.data.data();
+            o.kept_indices = kept.data();
+            o.dropped_ids = dropped.data();
+            o.dropped_per_block = dpb.data();
         }
         Frame(Frame&&) = default;
         backbone::BackboneOutput finish(const geometry::PillarSet& pillars, const backbone::FwaConfig& cfg) {
@@ -187,6 +203,13 @@ private:
             }
             out.stats.cache.computed = o.cache_computed;
             out.stats.cache.hits = o.cache_hits;
+            // StageTimes (backbone.hpp:109-126): device time per stage of this call
+            out.stats.stages.sort_ms = o.stage_ms[FWA_STAGE_SORT];
+            out.stats.stages.group_ms = o.stage_ms[FWA_STAGE_GROUP];
+            out.stats.stages.gather_ms = o.stage_ms[FWA_STAGE_GATHER];
+            out.stats.stages.attention_ms = o.stage_ms[FWA_STAGE_ATTENTION];
+            out.stats.stages.ffn_ms = o.stage_ms[FWA_STAGE_FFN];
+            out.stats.stages.scatter_ms = o.stage_ms[FWA_STAGE_SCATTER];
             return std::move(out);
         }
     };
@@ -196,17 +219,36 @@ private:
     };
     std::unique_ptr<fwa_b200_ctx, Del> ctx_;
     std::string blob_;
+    std::vector<float> proj_;
 };
 
 // Same signature as fwa::backbone::run_backbone; n_threads is accepted for API
-// parity (the GPU result does not depend on it).  One context per device, reused.
+// parity (the GPU result does not depend on it).  One context per device (the caller's
+// current CUDA device), created on first use and reused; concurrent callers on one device
+// are serialised on its mutex (the reference function is reentrant), callers on
+// different devices run concurrently.
 inline backbone::BackboneOutput run_backbone(const geometry::PillarSet& pillars,
                                              const backbone::FwaConfig& cfg,
                                              const backbone::BackboneParams& params,
                                              int n_threads = 1) {
     (void)n_threads;
-    static Backbone device0(0);
-    return device0.run(pillars, cfg, params);
+    struct Slot {
+        std::mutex m;
+        std::unique_ptr<Backbone> bb;
+    };
+    static std::mutex registry_m;
+    static std::map<int, std::unique_ptr<Slot>> registry;
+    const int dev = fwa_b200_current_device();
+    Slot* slot;
+    {
+        std::lock_guard<std::mutex> g(registry_m);
+        auto& p = registry[dev];
+        if (!p) p = std::make_unique<Slot>();
+        slot = p.get();
+    }
+    std::lock_guard<std::mutex> g(slot->m);
+    if (!slot->bb) slot->bb = std::make_unique<Backbone>(dev);
+    return slot->bb->run(pillars, cfg, params);
 }
 
 // Seed overload (backbone.hpp:328-334).

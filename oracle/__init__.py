@@ -103,6 +103,10 @@ def ref():
                                          C.POINTER(CfgC), C.c_void_p, C.c_int64, C.c_int,
                                          C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.c_void_p,
                                          C.c_void_p, C.c_void_p, C.c_void_p]
+        lib.ref_run_backbone_seeded.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
+                                                C.POINTER(CfgC), C.c_uint64, C.c_int, C.c_void_p, C.c_void_p,
+                                                C.POINTER(C.c_int64), C.c_void_p, C.c_void_p, C.c_void_p,
+                                                C.c_void_p]
         lib.ref_block_plans.argtypes = [C.c_void_p, C.c_int64, C.POINTER(CfgC), C.c_void_p,
                                         C.c_void_p]
         for fn in (lib.ref_sort, lib.ref_oracle_sort):
@@ -200,6 +204,27 @@ def ref_run_backbone(coords, feats64, cfg, blob, n_threads=1):
     return dict(features=out[:k].copy(), kept=kept[:k].copy(),
                 dropped=dropped[:int(dpb.sum())].copy(), dropped_per_block=dpb,
                 cache=(int(cache[0]), int(cache[1])), stage_ms=stages)
+
+
+def ref_run_backbone_seeded(coords, feats64, cfg, seed, n_threads=1):
+    """The seed overload run_backbone(ps, cfg, seed) (backbone.hpp:328-334): draws the input
+    projection when the pillar width != d_model.  Returns the outputs + that weight."""
+    lib = ref()
+    coords = np.ascontiguousarray(coords, np.float64)
+    feats64 = np.ascontiguousarray(feats64, np.float64)
+    n, d_in = feats64.shape
+    out = np.empty((n, cfg.d_model), np.float32)
+    kept = np.empty(n, np.int32)
+    dropped = np.empty(n, np.int32)
+    dpb = np.empty(cfg.n_blocks, np.int32)
+    cache = np.empty(2, np.int32)
+    w = np.zeros((cfg.d_model, d_in), np.float32)
+    nk = C.c_int64()
+    _check_ref(lib.ref_run_backbone_seeded(_p(coords), _p(feats64), n, d_in, C.byref(cfg), seed, n_threads,
+                                           _p(out), _p(kept), C.byref(nk), _p(dropped), _p(dpb), _p(cache), _p(w)))
+    k = nk.value
+    return dict(features=out[:k].copy(), kept=kept[:k].copy(), dropped=dropped[:int(dpb.sum())].copy(),
+                dropped_per_block=dpb, cache=(int(cache[0]), int(cache[1])), proj_weight=w)
 
 
 def ref_block_plans(coords, cfg):

@@ -238,46 +238,71 @@ int64_t ref_zero_params_fwap(const CfgC* c, void* out, int64_t cap) {
 
 // run_backbone on (coords, f64 feats). Outputs are caller-allocated with
 // capacity N (features N*d_model, kept N, dropped N, dropped_per_block n_blocks).
+namespace {
+void run_marshal(const double* coords, const double* feats, int64_t n, int64_t d_in, const CfgC* c,
+                 const backbone::BackboneParams& params, int n_threads, float* out_feats, int32_t* out_kept,
+                 int64_t* out_n_kept, int32_t* out_dropped, int32_t* out_dropped_per_block, int32_t* out_cache,
+                 double* out_stage_ms) {
+    geometry::PillarSet ps;
+    ps.resolution = c->resolution;
+    ps.coords.resize(static_cast<std::size_t>(n));
+    for (int64_t i = 0; i < n; ++i) ps.coords[i] = {coords[2 * i], coords[2 * i + 1]};
+    ps.features = Dense2<double>(static_cast<std::size_t>(n), static_cast<std::size_t>(d_in));
+    std::memcpy(ps.features.data.data(), feats, static_cast<std::size_t>(n * d_in) * sizeof(double));
+    const auto out = backbone::run_backbone(ps, to_cfg(c), params, n_threads);
+    *out_n_kept = static_cast<int64_t>(out.kept_indices.size());
+    if (out_feats) std::memcpy(out_feats, out.features.data.data(), out.features.data.size() * sizeof(float));
+    if (out_kept)
+        for (std::size_t i = 0; i < out.kept_indices.size(); ++i) out_kept[i] = out.kept_indices[i];
+    std::size_t w = 0;
+    for (std::size_t b = 0; b < out.dropped_indices.size(); ++b) {
+        if (out_dropped_per_block) out_dropped_per_block[b] = static_cast<int32_t>(out.dropped_indices[b].size());
+        for (const int id : out.dropped_indices[b])
+            if (out_dropped) out_dropped[w++] = id;
+    }
+    if (out_cache) {
+        out_cache[0] = out.stats.cache.computed;
+        out_cache[1] = out.stats.cache.hits;
+    }
+    if (out_stage_ms) {
+        const auto& s = out.stats.stages;
+        out_stage_ms[0] = s.sort_ms;
+        out_stage_ms[1] = s.group_ms;
+        out_stage_ms[2] = s.gather_ms;
+        out_stage_ms[3] = s.attention_ms;
+        out_stage_ms[4] = s.ffn_ms;
+        out_stage_ms[5] = s.scatter_ms;
+    }
+}
+}  // namespace
+
 int ref_run_backbone(const double* coords, const double* feats, int64_t n, int64_t d_in,
                      const CfgC* c, const void* blob, int64_t blob_len, int n_threads,
                      float* out_feats, int32_t* out_kept, int64_t* out_n_kept,
                      int32_t* out_dropped, int32_t* out_dropped_per_block, int32_t* out_cache,
                      double* out_stage_ms) {
     return guarded([&] {
-        geometry::PillarSet ps;
-        ps.resolution = c->resolution;
-        ps.coords.resize(static_cast<std::size_t>(n));
-        for (int64_t i = 0; i < n; ++i) ps.coords[i] = {coords[2 * i], coords[2 * i + 1]};
-        ps.features = Dense2<double>(static_cast<std::size_t>(n), static_cast<std::size_t>(d_in));
-        std::memcpy(ps.features.data.data(), feats, static_cast<std::size_t>(n * d_in) * sizeof(double));
         backbone::BackboneParams params;
         params.blocks = parse_blob(blob, static_cast<std::size_t>(blob_len));
-        const auto out = backbone::run_backbone(ps, to_cfg(c), params, n_threads);
-        *out_n_kept = static_cast<int64_t>(out.kept_indices.size());
-        if (out_feats)
-            std::memcpy(out_feats, out.features.data.data(), out.features.data.size() * sizeof(float));
-        if (out_kept)
-            for (std::size_t i = 0; i < out.kept_indices.size(); ++i) out_kept[i] = out.kept_indices[i];
-        std::size_t w = 0;
-        for (std::size_t b = 0; b < out.dropped_indices.size(); ++b) {
-            if (out_dropped_per_block)
-                out_dropped_per_block[b] = static_cast<int32_t>(out.dropped_indices[b].size());
-            for (const int id : out.dropped_indices[b])
-                if (out_dropped) out_dropped[w++] = id;
-        }
-        if (out_cache) {
-            out_cache[0] = out.stats.cache.computed;
-            out_cache[1] = out.stats.cache.hits;
-        }
-        if (out_stage_ms) {
-            const auto& s = out.stats.stages;
-            out_stage_ms[0] = s.sort_ms;
-            out_stage_ms[1] = s.group_ms;
-            out_stage_ms[2] = s.gather_ms;
-            out_stage_ms[3] = s.attention_ms;
-            out_stage_ms[4] = s.ffn_ms;
-            out_stage_ms[5] = s.scatter_ms;
-        }
+        run_marshal(coords, feats, n, d_in, c, params, n_threads, out_feats, out_kept, out_n_kept, out_dropped,
+                    out_dropped_per_block, out_cache, out_stage_ms);
+    });
+}
+
+// The seed overload (backbone.hpp:328-334): init_backbone_params(cfg, d_in, seed), which
+// draws the input projection when d_in != d_model, then run_backbone.  proj_weight_out
+// (d_model x d_in, may be null) receives the drawn projection weight.
+int ref_run_backbone_seeded(const double* coords, const double* feats, int64_t n, int64_t d_in, const CfgC* c,
+                            uint64_t seed, int n_threads, float* out_feats, int32_t* out_kept, int64_t* out_n_kept,
+                            int32_t* out_dropped, int32_t* out_dropped_per_block, int32_t* out_cache,
+                            float* proj_weight_out) {
+    return guarded([&] {
+        const auto params = backbone::init_backbone_params(to_cfg(c), static_cast<std::size_t>(d_in), seed);
+        if (proj_weight_out && params.input_proj)
+            std::memcpy(proj_weight_out, params.input_proj->weight.data.data(),
+                        params.input_proj->weight.data.size() * sizeof(float));
+        run_marshal(coords, feats, n, d_in, c, params, n_threads, out_feats, out_kept, out_n_kept, out_dropped,
+                    out_dropped_per_block, out_cache, nullptr);
     });
 }
 

@@ -40,6 +40,7 @@ EXPORTS = [
     "fwa_b200_split_plan_device",
     "fwa_b200_pillarize", "fwa_b200_pillarize_device", "fwa_b200_generate_points", "fwa_b200_pillar_params",
     "fwa_b200_row_checksums", "fwa_b200_fnv1a64", "fwa_b200_equal_window_forward", "fwa_b200_block_backward",
+    "fwa_b200_load_input_proj", "fwa_b200_init_params_fin", "fwa_b200_current_device",
 ]
 
 PREC_BF16, PREC_FP32, PREC_BF16_3K = 0, 1, 2
@@ -95,7 +96,16 @@ class _Cfg(C.Structure):
 class _Out(C.Structure):
     _fields_ = [("features", C.c_void_p), ("kept_indices", C.c_void_p), ("dropped_ids", C.c_void_p),
                 ("dropped_per_block", C.c_void_p), ("block_perms", C.c_void_p),
-                ("n_kept", C.c_int64), ("cache_computed", C.c_int32), ("cache_hits", C.c_int32)]
+                ("n_kept", C.c_int64), ("cache_computed", C.c_int32), ("cache_hits", C.c_int32),
+                ("stage_ms", C.c_double * 6)]
+
+
+class _FrameStats(C.Structure):
+    _fields_ = [("n_kept", C.c_int64), ("n_dropped", C.c_int32), ("cache_computed", C.c_int32),
+                ("cache_hits", C.c_int32)]
+
+
+STAGES = ("sort", "group", "gather", "attention", "ffn", "scatter")  # StageTimes order (backbone.hpp:109-126)
 
 
 class _EwReport(C.Structure):
@@ -134,6 +144,7 @@ def lib():
         L.fwa_b200_sync_check.argtypes = [vp]
         L.fwa_b200_get_profile.argtypes = [vp, vp, vp]
         L.fwa_b200_load_params.argtypes = [vp, C.POINTER(_Cfg), vp, C.c_size_t]
+        L.fwa_b200_load_input_proj.argtypes = [vp, i32, i32, vp, vp]
         L.fwa_b200_backbone_forward.argtypes = [vp, vp, vp, C.c_int, i64, C.POINTER(_Cfg),
                                                 C.POINTER(_Out)]
         L.fwa_b200_backbone_forward_frames.argtypes = [vp, C.c_int, vp, vp, C.c_int, vp, C.POINTER(_Cfg),
@@ -156,6 +167,8 @@ def lib():
         L.fwa_b200_split_plan_device.argtypes = [vp, C.c_int, vp]
         L.fwa_b200_init_params.argtypes = [C.POINTER(_Cfg), C.c_uint64, vp, C.c_size_t]
         L.fwa_b200_init_params.restype = i64
+        L.fwa_b200_init_params_fin.argtypes = [C.POINTER(_Cfg), i32, C.c_uint64, vp, C.c_size_t, vp]
+        L.fwa_b200_init_params_fin.restype = i64
         L.fwa_b200_pillarize.argtypes = [vp, vp, vp, i64, i32, C.c_double, vp, vp, i32, vp, vp, C.POINTER(i64)]
         L.fwa_b200_pillarize_device.argtypes = [vp, vp, vp, i64, i32, C.c_double, vp, vp, i32, vp, vp, i64,
                                                 C.POINTER(i64)]
@@ -251,9 +264,29 @@ class CacheStats:
 
 
 @dataclass
+class StageTimes:
+    """backbone.hpp:109-126: milliseconds per stage of one call (device time, CUDA events;
+    the fused block kernel's time apportioned by its per-phase SM-clock counters)."""
+    sort_ms: float = 0.0
+    group_ms: float = 0.0
+    gather_ms: float = 0.0
+    attention_ms: float = 0.0
+    ffn_ms: float = 0.0
+    scatter_ms: float = 0.0
+
+    def total(self) -> float:
+        return self.sort_ms + self.group_ms + self.gather_ms + self.attention_ms + self.ffn_ms + self.scatter_ms
+
+    @classmethod
+    def from_c(cls, a) -> "StageTimes":
+        return cls(*[float(a[i]) for i in range(6)])
+
+
+@dataclass
 class RunStats:
     cache: CacheStats = field(default_factory=CacheStats)
     dropped_per_block: List[int] = field(default_factory=list)
+    stages: StageTimes = field(default_factory=StageTimes)
 
 
 @dataclass
@@ -353,8 +386,7 @@ class Context:
         f64 = 1 if feats.dtype == np.float64 else 0
         feats = np.ascontiguousarray(feats, np.float64 if f64 else np.float32)
         n = coords.shape[0]
-        if feats.shape != (n, cfg.d_model):
-            raise ShapeError("backbone: pillar width != d_model and no input projection")
+        self._check_width(feats, n, cfg)
         out_f = np.empty((n, cfg.d_model), np.float32)
         kept = np.empty(n, np.int32)
         dropped = np.empty(max(n, 1), np.int32)
@@ -379,8 +411,31 @@ class Context:
         return BackboneOutput(features=out_f[:k], coords=coords[kept[:k]], kept_indices=kept[:k],
                               dropped_indices=dropped_lists,
                               stats=RunStats(CacheStats(int(o.cache_computed), int(o.cache_hits)),
-                                             [int(x) for x in dpb]),
+                                             [int(x) for x in dpb], StageTimes.from_c(o.stage_ms)),
                               n_input=n, block_perms=bp)
+
+    def _check_width(self, feats, n, cfg):
+        w = self._proj_in or cfg.d_model
+        if feats.ndim != 2 or feats.shape[0] != n:
+            raise ShapeError("backbone: features must be N x width")
+        if feats.shape[1] != w:
+            raise ShapeError("backbone: input projection width mismatch" if self._proj_in else
+                             "backbone: pillar width != d_model and no input projection")
+
+    _proj_in = 0
+
+    def load_input_proj(self, weight: Optional[np.ndarray], bias: Optional[np.ndarray] = None):
+        """BackboneParams::input_proj (backbone.hpp:74-81): weight d_model x f_in, bias d_model
+        (None = zeros); None removes it.  Projected on the device, bit-exact."""
+        if weight is None:
+            self._check(lib().fwa_b200_load_input_proj(self._h, 0, 0, None, None))
+            self._proj_in = 0
+            return
+        w = np.ascontiguousarray(weight, np.float32)
+        b = None if bias is None else np.ascontiguousarray(bias, np.float32)
+        self._check(lib().fwa_b200_load_input_proj(self._h, w.shape[0], w.shape[1], _ptr(w),
+                                                     _ptr(b) if b is not None else None))
+        self._proj_in = int(w.shape[1])
 
     def run_backbone_ptrs(self, coords_ptr: int, feats_ptr: int, feats_is_f64: bool, n: int,
                           cfg: FwaConfig, out_features_ptr: int, kept_ptr: int = 0,
@@ -410,8 +465,7 @@ class Context:
                 raise ShapeError("frames: mixed feature dtypes")
             feats = np.ascontiguousarray(ps.features, np.float64 if is64 else np.float32)
             n = coords.shape[0]
-            if feats.shape != (n, cfg.d_model):
-                raise ShapeError("backbone: pillar width != d_model and no input projection")
+            self._check_width(feats, n, cfg)
             out_f = np.empty((n, cfg.d_model), np.float32)
             kept = np.empty(max(n, 1), np.int32)
             dropped = np.empty(max(n, 1), np.int32)
@@ -419,20 +473,20 @@ class Context:
             keep.append((coords, feats, out_f, kept, dropped, dpb))
         ptrs = [(k[0].ctypes.data, k[1].ctypes.data, k[0].shape[0], k[2].ctypes.data, k[3].ctypes.data,
                  k[4].ctypes.data, k[5].ctypes.data) for k in keep]
-        stats = self.run_frames_ptrs(ptrs, bool(f64), cfg)
+        stats = self.run_frames_ptrs(ptrs, bool(f64), cfg, stages=True)
         outs = []
-        for (coords, _, out_f, kept, dropped, dpb), (k, cache) in zip(keep, stats):
+        for (coords, _, out_f, kept, dropped, dpb), (k, cache, stg) in zip(keep, stats):
             dropped_lists, w = [], 0
             for b in range(cfg.n_blocks):
                 dropped_lists.append(dropped[w:w + dpb[b]].copy())
                 w += int(dpb[b])
             outs.append(BackboneOutput(features=out_f[:k], coords=coords[kept[:k]], kept_indices=kept[:k],
                                        dropped_indices=dropped_lists,
-                                       stats=RunStats(CacheStats(*cache), [int(x) for x in dpb]),
+                                       stats=RunStats(CacheStats(*cache), [int(x) for x in dpb], stg),
                                        n_input=coords.shape[0], block_perms=None))
         return outs
 
-    def run_frames_ptrs(self, frames, feats_is_f64: bool, cfg: FwaConfig):
+    def run_frames_ptrs(self, frames, feats_is_f64: bool, cfg: FwaConfig, stages: bool = False):
         """fwa_b200_backbone_forward_frames on caller-owned HOST buffers: `frames` is a list
         of (coords_ptr, feats_ptr, n, out_features_ptr, kept_ptr, dropped_ptr,
         dropped_per_block_ptr) (0 = not wanted).  Returns [(n_kept, (computed, hits))]."""
@@ -444,6 +498,9 @@ class Context:
         c = cfg.c()
         self._check(lib().fwa_b200_backbone_forward_frames(self._h, F, cp, fp, int(feats_is_f64), ns, C.byref(c),
                                                            outs))
+        if stages:
+            return [(int(o.n_kept), (int(o.cache_computed), int(o.cache_hits)), StageTimes.from_c(o.stage_ms))
+                    for o in outs]
         return [(int(o.n_kept), (int(o.cache_computed), int(o.cache_hits))) for o in outs]
 
     def run_batch(self, coords: np.ndarray, feats: np.ndarray, frame_offsets: Sequence[int],
@@ -459,15 +516,19 @@ class Context:
         kept = np.empty(n, np.int32)
         dropped = np.empty(max(n, 1), np.int32)
         dpb = np.zeros(cfg.n_blocks, np.int32)
-        kpf = np.empty(nf, np.int64)
+        fs = (_FrameStats * nf)()
         o = _Out(_ptr(out_f).value, _ptr(kept).value, _ptr(dropped).value, _ptr(dpb).value, None, 0, 0, 0)
         c = cfg.c()
         self._check(lib().fwa_b200_backbone_forward_batch(self._h, _ptr(coords), _ptr(feats), f64,
-                                                          _ptr(off), nf, C.byref(c), C.byref(o),
-                                                          _ptr(kpf)))
+                                                          _ptr(off), nf, C.byref(c), C.byref(o), fs))
         k = int(o.n_kept)
+        frame_stats = [dict(n_kept=int(x.n_kept), n_dropped=int(x.n_dropped),
+                            cache=(int(x.cache_computed), int(x.cache_hits)),
+                            dropped_per_block=[int(x.n_dropped)] + [0] * (cfg.n_blocks - 1)) for x in fs]
         return dict(features=out_f[:k], kept=kept[:k], dropped=dropped[:int(dpb.sum())],
-                    kept_per_frame=kpf, cache=(int(o.cache_computed), int(o.cache_hits)))
+                    kept_per_frame=np.array([x["n_kept"] for x in frame_stats], np.int64),
+                    frame_stats=frame_stats, cache=(int(o.cache_computed), int(o.cache_hits)),
+                    stages=StageTimes.from_c(o.stage_ms))
 
     def forward_device(self, d_coords: int, d_feats: int, frame_offsets: Sequence[int],
                        cfg: FwaConfig, d_out: int, d_kept: Optional[int] = None) -> int:
@@ -608,15 +669,21 @@ def default_context(device: int = 0, precision: str = "bf16") -> Context:
 # ----------------------------------------------------------------------------- reference-shaped API
 
 def run_backbone(pillars: PillarSet, cfg: FwaConfig, params, n_threads: int = 1, *,
-                 device: int = 0, precision: str = "bf16", want_block_perms=False) -> BackboneOutput:
+                 device: int = 0, precision: str = "bf16", want_block_perms=False,
+                 input_proj=None) -> BackboneOutput:
     """backbone.hpp:159-325.  `params` = FWAP bytes (n_blocks records) or an int seed
-    (the seed overload, backbone.hpp:328-334).  `n_threads` is accepted for API
-    parity; the GPU path's results do not depend on it."""
+    (the seed overload, backbone.hpp:328-334: with pillar width != d_model it also draws
+    the input projection).  `input_proj` = (weight d_model x f_in, bias or None), the
+    optional BackboneParams::input_proj.  `n_threads` is accepted for API parity; the
+    GPU path's results do not depend on it."""
     validate(cfg)
     if isinstance(params, (int, np.integer)):
-        params = init_backbone_params(cfg, int(params))
+        params, w = init_backbone_params_fin(cfg, int(pillars.features.shape[1]), int(params))
+        if w is not None:
+            input_proj = (w, None)
     ctx = default_context(device, precision)
     ctx.load_params(cfg, params)
+    ctx.load_input_proj(*(input_proj or (None,)))
     return ctx.run_backbone(pillars, cfg, want_block_perms=want_block_perms)
 
 
@@ -652,6 +719,21 @@ def init_backbone_params(cfg: FwaConfig, seed: int) -> bytes:
     buf = np.empty(n, np.uint8)
     lib().fwa_b200_init_params(C.byref(c), seed, _ptr(buf), n)
     return buf.tobytes()
+
+
+def init_backbone_params_fin(cfg: FwaConfig, f_in: int, seed: int):
+    """init_backbone_params(cfg, f_in, seed) (backbone.hpp:83-102): (FWAP bytes, input
+    projection weight d_model x f_in or None when f_in == d_model)."""
+    c = cfg.c()
+    n = lib().fwa_b200_init_params_fin(C.byref(c), f_in, seed, None, 0, None)
+    if n < 0:
+        raise _ERRS.get(-n, FwaError)("init_backbone_params failed")
+    buf = np.empty(n, np.uint8)
+    w = np.empty((cfg.d_model, f_in), np.float32) if f_in != cfg.d_model else None
+    r = lib().fwa_b200_init_params_fin(C.byref(c), f_in, seed, _ptr(buf), n, _ptr(w) if w is not None else None)
+    if r < 0:
+        raise _ERRS.get(-r, FwaError)("init_backbone_params failed")
+    return buf.tobytes(), w
 
 
 @dataclass

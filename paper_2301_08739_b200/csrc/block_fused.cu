@@ -268,7 +268,11 @@ FWA_DEVINL bool attn_task(uint32_t sRA, uint32_t sKV, uint8_t* pRA, int head, in
     const int nt_live = (G + 7) >> 3;
     uint32_t a0, a1, a2, a3;
     {
-        const int qrow = m0 + (lane & 7) + ((lane >> 3) & 1) * 8;
+        // rows >= qend belong to another task's m-tile (same head columns, which that task
+        // overwrites with its O): read this task's first row instead -- discarded rows, no
+        // cross-warp hazard
+        int qrow = m0 + (lane & 7) + ((lane >> 3) & 1) * 8;
+        if (qrow >= qend) qrow = m0;
         const int col = head * 16 + (lane >> 4) * 8;
         ldsm_x4(sRA + img_off(qrow, col), a0, a1, a2, a3);
     }
@@ -353,13 +357,14 @@ FWA_DEVINL bool attn_task(uint32_t sRA, uint32_t sKV, uint8_t* pRA, int head, in
         mma16816(o[1], p[2 * kt][0], p[2 * kt][1], p[2 * kt + 1][0], p[2 * kt + 1][1], vb[kt][2], vb[kt][3]);
         mma16816(l, p[2 * kt][0], p[2 * kt][1], p[2 * kt + 1][0], p[2 * kt + 1][1], kOnes, kOnes);
     }
-    if (!kMax) {
+    const int r0 = m0 + g, r1 = r0 + 8;
+    if (!kMax) {  // only the kept rows (< qend) decide whether the task is re-run shifted
         const float lmin = rcp_approx(lmax);
-        const bool ok = l[0] >= lmin && l[0] <= lmax && l[2] >= lmin && l[2] <= lmax;
+        const bool ok = (r0 >= qend || (l[0] >= lmin && l[0] <= lmax)) && (r1 >= qend || (l[2] >= lmin && l[2] <= lmax));
         if (__any_sync(0xffffffffu, !ok)) return false;
     }
     const float i0 = rcp_approx(l[0]), i1 = rcp_approx(l[2]);
-    const int r0 = m0 + g, r1 = r0 + 8;
+    __syncwarp();  // every lane's Q fragment reads (ldmatrix) precede any lane's O writes
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
         const int col = head * 16 + nt * 8 + 2 * t4;
@@ -387,7 +392,8 @@ FWA_DEVINL uint32_t attn_task2(uint32_t sRA, uint32_t sKV, uint8_t* pRA, const i
     float o[2][2][4] = {}, l[2][4] = {};
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-        const int qrow = e[k].x + (lane & 7) + ((lane >> 3) & 1) * 8;
+        int qrow = e[k].x + (lane & 7) + ((lane >> 3) & 1) * 8;
+        if (qrow >= e[k].y) qrow = e[k].x;  // rows past the part end: this task's own row (see attn_task)
         const int col = head[k] * 16 + (lane >> 4) * 8;
         ldsm_x4(sRA + img_off(qrow, col), a[k][0], a[k][1], a[k][2], a[k][3]);
     }
@@ -444,15 +450,18 @@ FWA_DEVINL uint32_t attn_task2(uint32_t sRA, uint32_t sKV, uint8_t* pRA, const i
     }
     const float lmin = rcp_approx(lmax);
     uint32_t redo = 0;
+    __syncwarp();  // every lane's Q fragment reads (ldmatrix) precede any lane's O writes
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-        const bool ok = l[k][0] >= lmin && l[k][0] <= lmax && l[k][2] >= lmin && l[k][2] <= lmax;
+        const int r0 = e[k].x + g, r1 = r0 + 8;
+        // only the kept rows (< part end) decide whether the task is re-run shifted
+        const bool ok = (r0 >= e[k].y || (l[k][0] >= lmin && l[k][0] <= lmax)) &&
+                        (r1 >= e[k].y || (l[k][2] >= lmin && l[k][2] <= lmax));
         if (__any_sync(0xffffffffu, !ok)) {
             redo |= 1u << k;
             continue;
         }
         const float i0 = rcp_approx(l[k][0]), i1 = rcp_approx(l[k][2]);
-        const int r0 = e[k].x + g, r1 = r0 + 8;
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) {
             const int col = head[k] * 16 + nt * 8 + 2 * t4;
@@ -655,6 +664,7 @@ struct FusedArgs {
     const float* vec;        // TcBlockWeights::vec_pair (1152 floats)
     int* nonfinite;
     unsigned long long* trace;  // FWA_B200_TRACE: 64 SM-clock slots per CTA (phase boundaries)
+    unsigned long long* phase;  // stage timing: SM clocks per phase summed over CTAs [gather, attention, ffn, scatter]
     float lmax;                 // attention fast pass: row sums beyond [1/lmax, lmax] re-run shifted
 };
 
@@ -671,6 +681,19 @@ struct FusedArgs {
             unsigned long long g_;                                                              \
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_));                              \
             a.trace[blockIdx.x * 64 + (k)] = g_;                                                \
+        }                                                                                       \
+    } while (0)
+
+// stage timing (fwa_output_t::stage_ms): thread 0 of every CTA sums the SM clocks of the
+// unit loop's phases -- gather (rows landed, LN1, residual parked), attention (QKV MMA
+// .. out-proj), ffn (LN2 .. FFN2), scatter (output staging; the row stores themselves
+// overlap the next unit's QKV MMA) -- into a.phase[0..3] once, at exit
+#define FPH(k)                                                                                  \
+    do {                                                                                        \
+        if (a.phase && threadIdx.x == 0) {                                                      \
+            const unsigned long long t_ = static_cast<unsigned long long>(clock64());           \
+            if ((k) >= 0) ph_acc[(k)] += t_ - ph_t;                                             \
+            ph_t = t_;                                                                          \
         }                                                                                       \
     } while (0)
 
@@ -853,6 +876,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
             if (lane == 16) sTab[16].x = n;
         }
     };
+    unsigned long long ph_acc[4] = {0ull, 0ull, 0ull, 0ull}, ph_t = 0ull;
+    FPH(-1);
     int it = 0;
     for (int u = pair; u < a.n_units; u += npairs, ++it) {
         const uint32_t ph = it & 1;
@@ -965,6 +990,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
             }
         }
         FTR(tb + 2);
+        FPH(0);
         handshake();
         uint8_t* stg = pKV;  // the previous unit's output staging: clear of this unit's halo rows
         if (rank == 1 && strad) stg += (h0 * kKVPitch + 15) & ~15;
@@ -1113,6 +1139,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         mbar_wait(bP, ph);
         fence_after_sync();
         FTR(tb + 8);
+        FPH(1);
         {
             uint32_t v[32];
             tmem_ld32(tmem + lane_off + 384 + c0, v);  // x + P (the MMA accumulated onto x)
@@ -1208,6 +1235,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         fence_after_sync();
         prefetch_x(u + npairs, gid);  // FFN2 done: the W2 / K/V / R_X region is free
         FTR(tb + 14);
+        FPH(2);
         {
             uint32_t v[32];
             tmem_ld32(tmem + lane_off + c0, v);
@@ -1223,13 +1251,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         pnloc = nloc;
         pend = true;
         FTR(tb + 15);
+        FPH(3);
     }
     if (pend) {  // the last unit's output
         __syncthreads();  // the row ids
         stage_out(pKV);
         __syncthreads();
         store_out(pKV, 0, 16);
+        __syncthreads();
+        FPH(3);
     }
+    if (a.phase && threadIdx.x == 0)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) atomicAdd(a.phase + k, ph_acc[k]);
     if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 64 + 49] = static_cast<unsigned long long>(clock64());
     FTRG(61);
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(a.nonfinite, 1);
@@ -1365,9 +1399,11 @@ bool block_fused_supported(int G) { return G >= 1 && G <= 128 && choose_split(G)
 
 void launch_block_fused(const float* x, const double* x64, const __half* pe16, const int32_t* ridx,
                         const int32_t* sidx, float* x_out, int64_t rows, int G, const TcBlockWeights& w,
-                        int* d_nonfinite, cudaStream_t s, int64_t* launches, unsigned long long* trace) {
+                        int* d_nonfinite, cudaStream_t s, int64_t* launches, unsigned long long* trace,
+                        unsigned long long* phase) {
     if (rows <= 0) return;
     FusedArgs a{};
+    a.phase = phase;
     a.x = x; a.x64 = x64; a.pe16 = pe16; a.ridx = ridx; a.sidx = sidx; a.x_out = x_out;
     a.rows = rows; a.G = G; a.gpu = 256 / G;
     a.split = choose_split(G);

@@ -42,6 +42,8 @@ struct DevBuf {
     size_t cap = 0;
 };
 
+struct StageRec;
+
 struct BlockParams {
     // fp32 tensors (device), FWAP field order
     const float *w_qkv, *b_qkv, *w_out, *b_out, *ln1_g, *ln1_b, *ln2_g, *ln2_b, *w1, *b1, *w2, *b2;
@@ -121,6 +123,15 @@ struct fwa_b200_ctx {
     std::vector<Pending> pending;
     double prof_ms[FWA_PROF_SLOTS] = {};
     int64_t prof_n[FWA_PROF_SLOTS] = {};
+    // BackboneParams::input_proj (backbone.hpp:74-81), resident; proj_in == 0: none
+    int proj_in = 0;
+    DevBuf proj_w, proj_b;
+    bool proj_bias = false;
+    // StageTimes of the host-API calls (fwa_output_t::stage_ms): event spans of the call
+    // being enqueued (null: not recorded) and the event pool they come from
+    StageRec* rec = nullptr;
+    std::vector<cudaEvent_t> st_pool;
+    size_t st_used = 0;
 };
 
 namespace {
@@ -194,6 +205,90 @@ void prof_collect(fwa_b200_ctx* c) {
     c->pending.clear();
     c->ev_used = 0;
 }
+
+// ---- StageTimes (backbone.hpp:109-126) for the host-buffer entry points.  Spans of
+// device work between two events on the context stream, per reference stage; a span of
+// the fused block kernel (stage -1) is apportioned to gather / attention / ffn / scatter
+// by the kernel's per-phase SM-clock sums (block_fused.cu FPH).
+struct StageSpan {
+    int stage;
+    cudaEvent_t a, b;
+    int phase_slot;
+};
+struct StageRec {
+    std::vector<StageSpan> spans;
+    unsigned long long* d_phase = nullptr;  // n_slots x 4, zeroed when the call starts
+    int n_slots = 0, next_slot = 0;
+    std::vector<unsigned long long> h_phase;
+};
+
+cudaEvent_t st_event(fwa_b200_ctx* c) {
+    if (c->st_used == c->st_pool.size()) {
+        cudaEvent_t e;
+        CUDA_OK(cudaEventCreate(&e));
+        c->st_pool.push_back(e);
+    }
+    return c->st_pool[c->st_used++];
+}
+
+struct RecSpan {
+    fwa_b200_ctx* c;
+    StageRec* r;
+    int stage, slot;
+    cudaEvent_t a = nullptr;
+    RecSpan(fwa_b200_ctx* c_, int stage_, int slot_ = -1) : c(c_), r(c_->rec), stage(stage_), slot(slot_) {
+        if (r) {
+            a = st_event(c);
+            cudaEventRecord(a, c->stream);
+        }
+    }
+    ~RecSpan() {
+        if (!a) return;
+        cudaEvent_t b = st_event(c);
+        cudaEventRecord(b, c->stream);
+        r->spans.push_back({stage, a, b, slot});
+    }
+};
+
+// call after the stream work of `r` completed (and r.h_phase was copied back)
+void stage_finish(const StageRec& r, double* out) {
+    for (int i = 0; i < FWA_STAGES; ++i) out[i] = 0.0;
+    for (const auto& sp : r.spans) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, sp.a, sp.b) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        if (sp.stage >= 0) {
+            out[sp.stage] += ms;
+            continue;
+        }
+        const unsigned long long* p = r.h_phase.data() + 4 * sp.phase_slot;
+        const double tot = static_cast<double>(p[0]) + p[1] + p[2] + p[3];
+        if (!(tot > 0)) {
+            out[FWA_STAGE_ATTENTION] += ms;
+            continue;
+        }
+        out[FWA_STAGE_GATHER] += ms * (p[0] / tot);
+        out[FWA_STAGE_ATTENTION] += ms * (p[1] / tot);
+        out[FWA_STAGE_FFN] += ms * (p[2] / tot);
+        out[FWA_STAGE_SCATTER] += ms * (p[3] / tot);
+    }
+}
+
+// record a host-API call's StageTimes: spans on the context stream + the fused kernel's
+// phase counters (n_slots blocks); the guard detaches the record on every exit path
+struct StageScope {
+    fwa_b200_ctx* c;
+    StageScope(fwa_b200_ctx* c_, StageRec& r, unsigned long long* d_phase, int n_slots) : c(c_) {
+        r.d_phase = d_phase;
+        r.n_slots = n_slots;
+        r.next_slot = 0;
+        CUDA_OK(cudaMemsetAsync(d_phase, 0, static_cast<size_t>(n_slots) * 4 * sizeof(unsigned long long), c->stream));
+        c->rec = &r;
+    }
+    ~StageScope() { c->rec = nullptr; }
+};
 
 // FWA_B200_SYNC_DEBUG=1: synchronise after every launch group and name the failing stage.
 bool sync_debug() {
@@ -511,37 +606,66 @@ int32_t* sort_specs(fwa_b200_ctx* c, const double* d_coords, int64_t ntot, int n
         check_launch();
         return sorted;
     }
+    // exact path (one host round trip): every frame's own window range per spec, so frames
+    // far apart (world coordinates) cost no empty bins; window sets too wide for a dense bin
+    // per window (a far outlier) are rank-compressed by a radix sort instead -- any finite
+    // coordinates sort exactly
     launch_sort_keys(d_coords, ntot, n_specs, w_x, w_y, win, loc, partials, st, &c->launches);
     check_launch();
-    {
-        SpecBins* d_sb0 = ws<SpecBins>(c, "specbins", 4);
-        uint32_t* d_nb0 = ws<uint32_t>(c, "nbins", 4);
-        launch_bins_setup(partials, n_part, n_specs, nf, LLONG_MAX, mm, d_sb0, d_nb0, nullptr, st, &c->launches);
-    }
-    CUDA_OK(cudaMemcpyAsync(c->h_minmax, mm, 16 * 8, cudaMemcpyDeviceToHost, st));
+    long long* mmf = ws<long long>(c, "minmax_frame", 4 * static_cast<size_t>(n_specs) * nf);
+    launch_frame_minmax(win, ntot, n_specs, d_off, nf, mmf, st, &c->launches);
+    std::vector<long long> hm(4 * static_cast<size_t>(n_specs) * nf);
+    CUDA_OK(cudaMemcpyAsync(hm.data(), mmf, hm.size() * 8, cudaMemcpyDeviceToHost, st));
     CUDA_OK(cudaStreamSynchronize(st));
-    SpecBins sb[4];
+    check_launch("window ranges");
+    std::vector<SpecBins> sb(static_cast<size_t>(n_specs) * nf);
+    double dense = 0.0;
     long long nbins = 0;
-    for (int s = 0; s < n_specs; ++s) {
-        const long long* m = c->h_minmax + 4 * s;
-        const long long rM = m[1] - m[0] + 1, rm = m[3] - m[2] + 1;
-        if (rM <= 0 || rm <= 0 || rM > (1LL << 31) || rm > (1LL << 31) ||
-            static_cast<double>(rM) * static_cast<double>(rm) * nf > 1.5e9)
-            throw FwaError{FWA_ERR_INTERNAL,
-                           "window index range too large for the dense window-bin sort"};
-        sb[s] = SpecBins{m[0], m[2], rm, rM * rm, nbins};
-        nbins += rM * rm * nf;
+    for (int s = 0; s < n_specs; ++s)
+        for (int f = 0; f < nf; ++f) {
+            const long long* m = &hm[(static_cast<size_t>(s) * nf + f) * 4];
+            SpecBins& b = sb[static_cast<size_t>(s) * nf + f];
+            if (m[0] > m[1]) {  // empty frame (cannot happen: N >= G >= 1), no bins
+                b = SpecBins{0, 0, 1, 0, nbins};
+                continue;
+            }
+            const double rM = static_cast<double>(m[1]) - static_cast<double>(m[0]) + 1.0;
+            const double rm = static_cast<double>(m[3]) - static_cast<double>(m[2]) + 1.0;
+            dense += rM * rm;
+            if (dense < 4.0e18) {
+                b = SpecBins{m[0], m[2], static_cast<long long>(rm), static_cast<long long>(rM * rm), nbins};
+                nbins += static_cast<long long>(rM * rm);
+            }
+        }
+    const double dense_cap = std::max(static_cast<double>(1 << 22), 2.0 * static_cast<double>(total));
+    uint32_t* bin_of = ws<uint32_t>(c, "bin_of", static_cast<size_t>(total));
+    uint32_t* hist;
+    if (dense <= dense_cap) {
+        SpecBins* d_sb = ws<SpecBins>(c, "specbins_frame", sb.size());
+        CUDA_OK(cudaMemcpyAsync(d_sb, sb.data(), sb.size() * sizeof(SpecBins), cudaMemcpyHostToDevice, st));
+        hist = ws<uint32_t>(c, "hist", static_cast<size_t>(nbins));
+        CUDA_OK(cudaMemsetAsync(hist, 0, static_cast<size_t>(nbins) * 4, st));
+        launch_bins_hist(win, ntot, n_specs, d_off, nf, d_sb, bin_of, hist, nullptr, st, &c->launches, true);
+        CUDA_OK(cudaStreamSynchronize(st));  // sb (host) is read by the copy above
+    } else {
+        const size_t tot = static_cast<size_t>(total);
+        hist = ws<uint32_t>(c, "hist", tot);
+        CUDA_OK(cudaMemsetAsync(hist, 0, tot * 4, st));
+        const size_t tb = window_ranks_temp_bytes(total);
+        uint32_t* d_count = ws<uint32_t>(c, "wr_count", 4);
+        launch_window_ranks(win, ntot, n_specs, d_off, nf, ws<unsigned long long>(c, "wr_k64a", tot),
+                            ws<unsigned long long>(c, "wr_k64b", tot), ws<uint32_t>(c, "wr_va", tot),
+                            ws<uint32_t>(c, "wr_vb", tot), ws<uint32_t>(c, "wr_flag", tot),
+                            ws<uint32_t>(c, "wr_ex", tot), ws<uint32_t>(c, "scan_tmp", scan_tmp_words(total) + 8),
+                            d_count, ws<uint8_t>(c, "wr_temp", tb), tb, bin_of, hist, st, &c->launches);
+        uint32_t cnt = 0;
+        CUDA_OK(cudaMemcpyAsync(&cnt, d_count, 4, cudaMemcpyDeviceToHost, st));
+        CUDA_OK(cudaStreamSynchronize(st));
+        check_launch("window ranks");
+        nbins = cnt;
     }
-    if (nbins > 1500000000LL)
-        throw FwaError{FWA_ERR_INTERNAL, "window index range too large for the dense window-bin sort"};
-    SpecBins* d_sb = ws<SpecBins>(c, "specbins", 4);
-    CUDA_OK(cudaMemcpyAsync(d_sb, sb, sizeof(sb), cudaMemcpyHostToDevice, st));
-    uint32_t* hist = ws<uint32_t>(c, "hist", static_cast<size_t>(nbins));
     uint32_t* bin_start = ws<uint32_t>(c, "bin_start", static_cast<size_t>(nbins));
     uint32_t* scan_tmp = ws<uint32_t>(c, "scan_tmp", scan_tmp_words(std::max<int64_t>(nbins, total)) + 8);
-    uint32_t* bin_of = ws<uint32_t>(c, "bin_of", static_cast<size_t>(total));
-    CUDA_OK(cudaMemsetAsync(hist, 0, static_cast<size_t>(nbins) * 4, st));
-    launch_bins_hist(win, ntot, n_specs, d_off, nf, d_sb, bin_of, hist, nullptr, st, &c->launches);
     exclusive_scan_u32(hist, bin_start, nbins, scan_tmp, nullptr, st, &c->launches);
     uint32_t* cursor = ws<uint32_t>(c, "cursor", static_cast<size_t>(nbins));
     CUDA_OK(cudaMemcpyAsync(cursor, bin_start, static_cast<size_t>(nbins) * 4, cudaMemcpyDeviceToDevice, st));
@@ -597,7 +721,11 @@ void build_schedule_body(fwa_b200_ctx* c, const double* d_coords, const fwa_conf
     cudaStream_t st = c->stream;
 
     const int64_t total = ntot * n_specs;
-    S.sorted = sort_specs(c, d_coords, ntot, n_specs, w_x, w_y, d_off, nf, c->exact_bins);
+    {
+        RecSpan t(c, FWA_STAGE_SORT);
+        S.sorted = sort_specs(c, d_coords, ntot, n_specs, w_x, w_y, d_off, nf, c->exact_bins);
+    }
+    RecSpan t_group(c, FWA_STAGE_GROUP);
     S.sorted_inv = ws<int32_t>(c, "sorted_inv", static_cast<size_t>(total));
     uint32_t* scan_tmp = ws<uint32_t>(c, "scan_tmp", scan_tmp_words(total) + 8);
 
@@ -711,7 +839,11 @@ void run_block(fwa_b200_ctx* c, const BlockParams& p, const fwa_config_t* cfg, i
         }();
         unsigned long long* tr = trace_fused && !x_in64 ? ws<unsigned long long>(c, "trace", 2 * 148 * 64) : nullptr;
         StageEv t(c, FWA_PROF_BLOCK);
-        launch_block_fused(x_in, x_in64, pe16, ridx, sidx, x_out, rows, G, p.tc, c->d_flag, st, &c->launches, tr);
+        StageRec* r = c->rec;
+        const int slot = r && r->next_slot < r->n_slots ? r->next_slot++ : -1;
+        RecSpan span(c, slot >= 0 ? -1 : FWA_STAGE_ATTENTION, slot);
+        launch_block_fused(x_in, x_in64, pe16, ridx, sidx, x_out, rows, G, p.tc, c->d_flag, st, &c->launches, tr,
+                           slot >= 0 ? r->d_phase + 4 * slot : nullptr);
         check_launch("k_block_fused");
         return;
     }
@@ -733,16 +865,19 @@ void run_block(fwa_b200_ctx* c, const BlockParams& p, const fwa_config_t* cfg, i
         float* xq = no_xq ? nullptr : ws<float>(c, "xq", static_cast<size_t>((rows + 127) / 128) * 128 * 128);
         {
             StageEv t(c, FWA_PROF_LN_QKV);
+            RecSpan span(c, FWA_STAGE_ATTENTION);  // gather + LN1 + QKV: one kernel
             launch_ln1_qkv_tc(x_in, x_in64, pe16, ridx, rows, p.tc, qkv, c->d_flag, xq, st, &c->launches, tr);
             check_launch("k_ln1_qkv_tc");
         }
         {
             StageEv t(c, FWA_PROF_ATTENTION);
+            RecSpan span(c, FWA_STAGE_ATTENTION);
             launch_attention_mma(qkv, rows, G, cat, st, &c->launches);
             check_launch("k_attention_mma");
         }
         {
             StageEv t(c, FWA_PROF_OUTPROJ_FFN);
+            RecSpan span(c, FWA_STAGE_FFN);  // out-proj + LN2 + FFN + scatter: one kernel
             launch_outproj_ffn_tc(cat, x_in, x_in64, ridx, rows, p.tc, x_out, sidx, xq, st, &c->launches,
                                   tr ? tr + 148 * 64 : nullptr);
             check_launch("k_outproj_ffn_tc");
@@ -759,20 +894,26 @@ void run_block(fwa_b200_ctx* c, const BlockParams& p, const fwa_config_t* cfg, i
     GemmArgs g{};
     {
         StageEv t(c, FWA_PROF_LN_QKV);
+        RecSpan span(c, FWA_STAGE_GATHER);  // gather + LN1 + PE
         launch_ln_gather_f32(x_in, x_in64, pe, ridx, rows, d, p.ln1_g, p.ln1_b, h, c->d_flag, st,
                              &c->launches);
-        g.A = h; g.M = rows; g.K = d; g.W = p.w_qkv; g.N = 3 * d; g.bias = p.b_qkv; g.C = qkv;
-        launch_gemm_f32(g, EPI_BIAS, st, &c->launches);
     }
     {
         StageEv t(c, FWA_PROF_ATTENTION);
+        RecSpan span(c, FWA_STAGE_ATTENTION);
+        g.A = h; g.M = rows; g.K = d; g.W = p.w_qkv; g.N = 3 * d; g.bias = p.b_qkv; g.C = qkv;
+        launch_gemm_f32(g, EPI_BIAS, st, &c->launches);
         launch_attention_f32(qkv, rows, G, d, cfg->n_heads, cat, st, &c->launches);
     }
     StageEv t_ffn(c, FWA_PROF_OUTPROJ_FFN);
-    g = GemmArgs{};
-    g.A = cat; g.M = rows; g.K = d; g.W = p.w_out; g.N = d; g.bias = p.b_out; g.C = mid;
-    g.R = x_in; g.R64 = x_in64; g.ridx = ridx;
-    launch_gemm_f32(g, EPI_RESID_GATHER, st, &c->launches);
+    {
+        RecSpan span(c, FWA_STAGE_ATTENTION);  // out-proj + residual (kernels.hpp:550-560)
+        g = GemmArgs{};
+        g.A = cat; g.M = rows; g.K = d; g.W = p.w_out; g.N = d; g.bias = p.b_out; g.C = mid;
+        g.R = x_in; g.R64 = x_in64; g.ridx = ridx;
+        launch_gemm_f32(g, EPI_RESID_GATHER, st, &c->launches);
+    }
+    RecSpan span_ffn(c, FWA_STAGE_FFN);  // LN2 + FFN + residual + scatter
     launch_ln_rows_f32(mid, rows, d, p.ln2_g, p.ln2_b, ln2, st, &c->launches);
     g = GemmArgs{};
     g.A = ln2; g.M = rows; g.K = d; g.W = p.w1; g.N = dff; g.bias = p.b1; g.C = act;
@@ -810,14 +951,30 @@ void require_params(fwa_b200_ctx* c, const fwa_config_t* cfg) {
         throw FwaError{FWA_ERR_CONFIG, "backbone: block params disagree with config"};
 }
 
+// BackboneParams::input_proj on the device (backbone.hpp:179-190): N x f_in (f64 or f32)
+// -> N x d_model f32 in `dst`, enqueued on stream `st`
+void project_input(fwa_b200_ctx* c, const void* x, bool f64, int64_t n, int d, float* dst, cudaStream_t st) {
+    if (c->proj_in <= 0) throw FwaError{FWA_ERR_INTERNAL, "no input projection loaded"};
+    if (d != static_cast<int>(c->proj_w.cap / (sizeof(float) * c->proj_in)))
+        throw FwaError{FWA_ERR_SHAPE, "backbone: input projection width mismatch"};
+    launch_input_proj(x, f64, n, c->proj_in, static_cast<const float*>(c->proj_w.p),
+                      c->proj_bias ? static_cast<const float*>(c->proj_b.p) : nullptr, d, dst, st, &c->launches);
+    check_launch("k_input_proj");
+}
+
 // Device-resident forward over S (already host-framed).  Writes d_out
 // (K x d, active order) and, optionally, d_kept.
 void forward_device(fwa_b200_ctx* c, const double* d_coords, const float* d_feats,
                     const double* d_feats64, const fwa_config_t* cfg, Schedule& S, float* d_out,
                     int32_t* d_kept, const int64_t* d_tab_fixed = nullptr,
-                    cudaEvent_t feats_ready = nullptr) {
+                    cudaEvent_t feats_ready = nullptr, bool project_feats = false) {
     cudaStream_t st = c->stream;
     const int d = cfg->d_model;
+    if (project_feats && c->proj_in > 0) {  // device API: d_feats holds N x f_in f32 rows
+        float* pr = ws<float>(c, "proj_dev", static_cast<size_t>(S.ntot) * d);
+        project_input(c, d_feats, false, S.ntot, d, pr, st);
+        d_feats = pr;
+    }
     CUDA_OK(cudaMemsetAsync(c->d_flag, 0, 2 * sizeof(int), st));
     const bool fast = fast_path_ok(c, d, cfg->n_heads, cfg->d_ff, cfg->group_size);
     // fast path: fp16 PE rows (|PE| <= 1, abs err <= 2^-12, below the bf16 rounding of
@@ -881,14 +1038,19 @@ int guarded(fwa_b200_ctx* c, Fn&& fn) {
 // Host-buffer forward shared by the single-frame and batch entry points.
 void forward_host(fwa_b200_ctx* c, const double* coords, const void* feats, int f64,
                   const int64_t* off, int n_frames, const fwa_config_t* cfg, fwa_output_t* out,
-                  int64_t* kept_per_frame) {
+                  fwa_frame_stats_t* per_frame) {
     validate_cfg(cfg);
     require_params(c, cfg);
-    if (!coords || !feats || !out || !out->features) throw FwaError{FWA_ERR_SHAPE, "null buffer"};
     Schedule S;
-    host_frames(off, n_frames, cfg->group_size, S);
+    host_frames(off, n_frames, cfg->group_size, S);  // N < G: numeric_error before any buffer check
+    if (!coords || !feats || !out || !out->features) throw FwaError{FWA_ERR_SHAPE, "null buffer"};
     cudaStream_t st = c->stream;
     const int d = cfg->d_model;
+    const int fin = c->proj_in > 0 ? c->proj_in : d;  // input width (BackboneParams::input_proj)
+    c->st_used = 0;
+    StageRec rec;
+    StageScope scope(c, rec, ws<unsigned long long>(c, "phase_acc", 4 * static_cast<size_t>(cfg->n_blocks)),
+                     cfg->n_blocks);
     double* d_coords = ws<double>(c, "in_coords", 2 * static_cast<size_t>(S.ntot));
     const float* d_f32 = nullptr;
     const double* d_f64 = nullptr;
@@ -896,17 +1058,21 @@ void forward_host(fwa_b200_ctx* c, const double* coords, const void* feats, int 
     CUDA_OK(cudaMemcpyAsync(d_coords, coords, static_cast<size_t>(S.ntot) * 16, cudaMemcpyHostToDevice, st));
     delete h2d;
     // the features (the bulk of the input) cross PCIe on a copy stream while the schedule
-    // and the PE run (they need only the coordinates); block 0 waits for them
+    // and the PE run (they need only the coordinates); block 0 waits for them (and for the
+    // input projection, which runs on the copy stream right behind its input)
     CUDA_OK(cudaEventRecord(c->ev_copy, st));  // previous users of the buffer are done
     CUDA_OK(cudaStreamWaitEvent(c->copy, c->ev_copy, 0));
-    if (f64) {
-        double* p = ws<double>(c, "in_feats64", static_cast<size_t>(S.ntot) * d);
-        CUDA_OK(cudaMemcpyAsync(p, feats, static_cast<size_t>(S.ntot) * d * 8, cudaMemcpyHostToDevice, c->copy));
-        d_f64 = p;
+    const size_t esz = f64 ? 8 : 4;
+    void* p = ws<uint8_t>(c, f64 ? "in_feats64" : "in_feats32", static_cast<size_t>(S.ntot) * fin * esz);
+    CUDA_OK(cudaMemcpyAsync(p, feats, static_cast<size_t>(S.ntot) * fin * esz, cudaMemcpyHostToDevice, c->copy));
+    if (c->proj_in > 0) {
+        float* pr = ws<float>(c, "proj_out", static_cast<size_t>(S.ntot) * d);
+        project_input(c, p, f64 != 0, S.ntot, d, pr, c->copy);
+        d_f32 = pr;
+    } else if (f64) {
+        d_f64 = static_cast<const double*>(p);
     } else {
-        float* p = ws<float>(c, "in_feats32", static_cast<size_t>(S.ntot) * d);
-        CUDA_OK(cudaMemcpyAsync(p, feats, static_cast<size_t>(S.ntot) * d * 4, cudaMemcpyHostToDevice, c->copy));
-        d_f32 = p;
+        d_f32 = static_cast<const float*>(p);
     }
     CUDA_OK(cudaEventRecord(c->ev_feats, c->copy));
     float* d_out = ws<float>(c, "out_feats", static_cast<size_t>(S.ntot) * d);
@@ -929,6 +1095,8 @@ void forward_host(fwa_b200_ctx* c, const double* coords, const void* feats, int 
         CUDA_OK(cudaMemcpyAsync(h_idx.data(), S.idx, h_idx.size() * 4, cudaMemcpyDeviceToHost, st));
         CUDA_OK(cudaMemcpyAsync(h_rank.data(), S.kept_rank, h_rank.size() * 4, cudaMemcpyDeviceToHost, st));
     }
+    rec.h_phase.assign(4 * static_cast<size_t>(rec.n_slots), 0ull);
+    CUDA_OK(cudaMemcpyAsync(rec.h_phase.data(), rec.d_phase, rec.h_phase.size() * 8, cudaMemcpyDeviceToHost, st));
     CUDA_OK(cudaMemcpyAsync(c->h_flag, c->d_flag, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
     delete d2h;
     CUDA_OK(cudaStreamSynchronize(st));
@@ -938,22 +1106,29 @@ void forward_host(fwa_b200_ctx* c, const double* coords, const void* feats, int 
             fwa_b200_ctx* c;
             ~Reset() { c->exact_bins = false; }
         } reset{c};
-        forward_host(c, coords, feats, f64, off, n_frames, cfg, out, kept_per_frame);
+        c->rec = nullptr;
+        forward_host(c, coords, feats, f64, off, n_frames, cfg, out, per_frame);
         return;
     }
     if (c->h_flag[0]) throw FwaError{FWA_ERR_NUMERIC, "group_attention: non-finite input"};
+    stage_finish(rec, out->stage_ms);
     out->n_kept = S.K;
-    std::vector<int64_t> drops;
-    cache_stats(cfg->n_blocks, S.off[1] - S.off[0], cfg->group_size, &out->cache_computed,
-                &out->cache_hits, &drops);
+    // sort-cache statistics: the reference rule per frame (each frame is its own run)
+    for (int f = 0; f < n_frames; ++f) {
+        int32_t comp = 0, hits = 0;
+        cache_stats(cfg->n_blocks, S.off[f + 1] - S.off[f], cfg->group_size, &comp, &hits, nullptr);
+        if (f == 0) {
+            out->cache_computed = comp;
+            out->cache_hits = hits;
+        }
+        if (per_frame) per_frame[f] = fwa_frame_stats_t{S.rows[f], static_cast<int32_t>(S.drop[f]), comp, hits};
+    }
     if (out->dropped_per_block)
         for (int b = 0; b < cfg->n_blocks; ++b) {
             int64_t tot = 0;  // summed over frames (each frame drops only in block 0)
             for (int f = 0; f < n_frames; ++f) tot += b == 0 ? S.drop[f] : 0;
             out->dropped_per_block[b] = static_cast<int32_t>(tot);
         }
-    if (kept_per_frame)
-        for (int f = 0; f < n_frames; ++f) kept_per_frame[f] = S.rows[f];
     if (perms) {
         const int64_t n = S.ntot;
         for (int b = 0; b < cfg->n_blocks; ++b) {
@@ -981,30 +1156,35 @@ void forward_frames(fwa_b200_ctx* c, int F, const double* const* coords, const v
     require_params(c, cfg);
     if (F < 1 || !coords || !feats || !n || !outs) throw FwaError{FWA_ERR_SHAPE, "need >= 1 frame"};
     const int d = cfg->d_model, G = cfg->group_size;
+    const int fin = c->proj_in > 0 ? c->proj_in : d;  // input width (BackboneParams::input_proj)
     int64_t nmax = 0;
     for (int f = 0; f < F; ++f) {
-        if (!coords[f] || !feats[f] || !outs[f].features) throw FwaError{FWA_ERR_SHAPE, "null buffer"};
-        if (outs[f].block_perms) throw FwaError{FWA_ERR_CONTRACT, "block_perms: use fwa_b200_backbone_forward"};
         if (n[f] < G)  // backbone.hpp:218-222, before anything is enqueued
             throw FwaError{FWA_ERR_NUMERIC, "backbone: block 0 has " + std::to_string(n[f]) +
                                                 " pillars, fewer than group size " + std::to_string(G) +
                                                 "; refusing to emit empty output"};
+        if (!coords[f] || !feats[f] || !outs[f].features) throw FwaError{FWA_ERR_SHAPE, "null buffer"};
+        if (outs[f].block_perms) throw FwaError{FWA_ERR_CONTRACT, "block_perms: use fwa_b200_backbone_forward"};
         nmax = std::max(nmax, n[f]);
     }
     const size_t esz = f64 ? 8 : 4, nm = static_cast<size_t>(nmax);
     // every slot buffer sized up front: a workspace move frees memory copies are using
     double* in_c[2];
     void* in_f[2];
+    float* in_p[2] = {nullptr, nullptr};
     float* o_f[2];
     int32_t* o_ids[2];  // [kept (K) | dropped (< G)]
-    static const char* kNames[2][4] = {{"fr_c0", "fr_f0", "fr_o0", "fr_i0"}, {"fr_c1", "fr_f1", "fr_o1", "fr_i1"}};
+    static const char* kNames[2][5] = {{"fr_c0", "fr_f0", "fr_o0", "fr_i0", "fr_p0"},
+                                       {"fr_c1", "fr_f1", "fr_o1", "fr_i1", "fr_p1"}};
     for (int s = 0; s < 2; ++s) {
         in_c[s] = ws<double>(c, kNames[s][0], 2 * nm);
-        in_f[s] = ws<uint8_t>(c, kNames[s][1], nm * d * esz);
+        in_f[s] = ws<uint8_t>(c, kNames[s][1], nm * fin * esz);
+        if (c->proj_in > 0) in_p[s] = ws<float>(c, kNames[s][4], nm * d);
         o_f[s] = ws<float>(c, kNames[s][2], nm * d);
         o_ids[s] = ws<int32_t>(c, kNames[s][3], nm + G);
     }
     ws<float>(c, "X", nm * d);
+    unsigned long long* d_phase = ws<unsigned long long>(c, "phase_acc", 4 * static_cast<size_t>(F) * cfg->n_blocks);
     if (!c->d2h) CUDA_OK(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
     for (auto* e : {&c->fr_ev[0], &c->fr_ev[1], &c->fr_ev[2], &c->fr_ev[3], &c->fr_ev[4], &c->fr_ev[5],
                     &c->fr_ev[6], &c->fr_ev[7]})
@@ -1023,23 +1203,36 @@ void forward_frames(fwa_b200_ctx* c, int F, const double* const* coords, const v
     CUDA_OK(cudaEventRecord(c->ev_copy, st));  // earlier users of the slot buffers are done
     CUDA_OK(cudaStreamWaitEvent(c->copy, c->ev_copy, 0));
     CUDA_OK(cudaStreamWaitEvent(c->d2h, c->ev_copy, 0));
+    CUDA_OK(cudaMemsetAsync(d_phase, 0, 4 * static_cast<size_t>(F) * cfg->n_blocks * 8, st));
     std::vector<int64_t> K(static_cast<size_t>(F)), nd(static_cast<size_t>(F));
+    std::vector<StageRec> recs(static_cast<size_t>(F));
+    c->st_used = 0;
+    struct Detach {
+        fwa_b200_ctx* c;
+        ~Detach() { c->rec = nullptr; }
+    } detach{c};
     for (int f = 0; f < F; ++f) {
         const int s = f & 1;
         const size_t nf = static_cast<size_t>(n[f]);
         if (f >= 2) CUDA_OK(cudaStreamWaitEvent(c->copy, ev_done[s], 0));
         CUDA_OK(cudaMemcpyAsync(in_c[s], coords[f], nf * 16, cudaMemcpyHostToDevice, c->copy));
         CUDA_OK(cudaEventRecord(ev_inc[s], c->copy));
-        CUDA_OK(cudaMemcpyAsync(in_f[s], feats[f], nf * d * esz, cudaMemcpyHostToDevice, c->copy));
+        CUDA_OK(cudaMemcpyAsync(in_f[s], feats[f], nf * fin * esz, cudaMemcpyHostToDevice, c->copy));
+        if (c->proj_in > 0) project_input(c, in_f[s], f64 != 0, n[f], d, in_p[s], c->copy);
         CUDA_OK(cudaEventRecord(ev_inf[s], c->copy));
         CUDA_OK(cudaStreamWaitEvent(st, ev_inc[s], 0));
         if (f >= 2) CUDA_OK(cudaStreamWaitEvent(st, ev_out[s], 0));
         Schedule S;
         const int64_t off[2] = {0, n[f]};
         host_frames(off, 1, G, S);
-        forward_device(c, in_c[s], f64 ? nullptr : static_cast<const float*>(in_f[s]),
-                       f64 ? static_cast<const double*>(in_f[s]) : nullptr, cfg, S, o_f[s], nullptr, nullptr,
-                       ev_inf[s]);
+        StageRec& rec = recs[static_cast<size_t>(f)];
+        rec.d_phase = d_phase + 4 * static_cast<size_t>(f) * cfg->n_blocks;
+        rec.n_slots = cfg->n_blocks;
+        c->rec = &rec;
+        const float* x32 = c->proj_in > 0 ? in_p[s] : (f64 ? nullptr : static_cast<const float*>(in_f[s]));
+        const double* x64 = c->proj_in > 0 || !f64 ? nullptr : static_cast<const double*>(in_f[s]);
+        forward_device(c, in_c[s], x32, x64, cfg, S, o_f[s], nullptr, nullptr, ev_inf[s]);
+        c->rec = nullptr;
         K[f] = S.K;
         nd[f] = S.n_drop;
         CUDA_OK(cudaMemcpyAsync(o_ids[s], S.kept_ids, static_cast<size_t>(S.K) * 4, cudaMemcpyDeviceToDevice, st));
@@ -1062,8 +1255,18 @@ void forward_frames(fwa_b200_ctx* c, int F, const double* const* coords, const v
     }
     CUDA_OK(cudaEventRecord(c->ev_copy, c->d2h));
     CUDA_OK(cudaStreamWaitEvent(st, c->ev_copy, 0));  // later work on the context stream follows
+    std::vector<unsigned long long> h_phase(4 * static_cast<size_t>(F) * cfg->n_blocks);
+    CUDA_OK(cudaMemcpyAsync(h_phase.data(), d_phase, h_phase.size() * 8, cudaMemcpyDeviceToHost, st));
     CUDA_OK(cudaStreamSynchronize(c->d2h));
     CUDA_OK(cudaStreamSynchronize(st));
+    // stage times first (the per-frame event spans live in the context's pool, which a
+    // re-run below reuses), then the deferred device conditions in frame order
+    for (int f = 0; f < F; ++f) {
+        StageRec& rec = recs[static_cast<size_t>(f)];
+        rec.h_phase.assign(h_phase.begin() + 4 * static_cast<size_t>(f) * cfg->n_blocks,
+                           h_phase.begin() + 4 * static_cast<size_t>(f + 1) * cfg->n_blocks);
+        stage_finish(rec, outs[f].stage_ms);
+    }
     for (int f = 0; f < F; ++f) {
         if (c->h_fr_flags[2 * f + 1]) {  // window-bin capacity overflow: this frame alone, exact bins
             const int64_t off[2] = {0, n[f]};
@@ -1073,8 +1276,7 @@ void forward_frames(fwa_b200_ctx* c, int F, const double* const* coords, const v
         if (c->h_fr_flags[2 * f]) throw FwaError{FWA_ERR_NUMERIC, "group_attention: non-finite input"};
         fwa_output_t& o = outs[f];
         o.n_kept = K[static_cast<size_t>(f)];
-        std::vector<int64_t> drops;
-        cache_stats(cfg->n_blocks, n[f], G, &o.cache_computed, &o.cache_hits, &drops);
+        cache_stats(cfg->n_blocks, n[f], G, &o.cache_computed, &o.cache_hits, nullptr);
         if (o.dropped_per_block)
             for (int b = 0; b < cfg->n_blocks; ++b)
                 o.dropped_per_block[b] = static_cast<int32_t>(b == 0 ? nd[static_cast<size_t>(f)] : 0);
@@ -1123,6 +1325,15 @@ int fwa_b200_ctx_create(int device, void* stream, fwa_b200_ctx** out) {
     return FWA_OK;
 }
 
+int fwa_b200_current_device(void) {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess) {
+        cudaGetLastError();
+        d = 0;
+    }
+    return d;
+}
+
 void fwa_b200_ctx_destroy(fwa_b200_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
@@ -1132,6 +1343,9 @@ void fwa_b200_ctx_destroy(fwa_b200_ctx* c) {
     if (c->params_f32.p) cudaFree(c->params_f32.p);
     if (c->params_bf16.p) cudaFree(c->params_bf16.p);
     if (c->freq.p) cudaFree(c->freq.p);
+    if (c->proj_w.p) cudaFree(c->proj_w.p);
+    if (c->proj_b.p) cudaFree(c->proj_b.p);
+    for (auto e : c->st_pool) cudaEventDestroy(e);
     if (c->d_flag) cudaFree(c->d_flag);
     if (c->h_flag) cudaFreeHost(c->h_flag);
     if (c->h_minmax) cudaFreeHost(c->h_minmax);
@@ -1243,6 +1457,35 @@ int fwa_b200_load_params(fwa_b200_ctx* c, const fwa_config_t* cfg, const void* b
     });
 }
 
+int fwa_b200_load_input_proj(fwa_b200_ctx* c, int32_t d_model, int32_t f_in, const float* weight,
+                             const float* bias) {
+    return guarded(c, [&] {
+        if (f_in == 0) {  // remove
+            c->proj_in = 0;
+            ++c->params_version;
+            return;
+        }
+        if (f_in < 0 || d_model < 1) throw FwaError{FWA_ERR_SHAPE, "input projection: bad shape"};
+        if (!weight) throw FwaError{FWA_ERR_SHAPE, "input projection: null weight"};
+        const size_t wb = static_cast<size_t>(d_model) * f_in * sizeof(float);
+        if (c->proj_w.p) cudaFree(c->proj_w.p);
+        c->proj_w.p = nullptr;
+        CUDA_OK(cudaMalloc(&c->proj_w.p, wb));
+        c->proj_w.cap = wb;  // d_model x f_in floats exactly (project_input reads d_model from it)
+        CUDA_OK(cudaMemcpy(c->proj_w.p, weight, wb, cudaMemcpyHostToDevice));
+        c->proj_bias = bias != nullptr;
+        if (bias) {
+            if (c->proj_b.p) cudaFree(c->proj_b.p);
+            c->proj_b.p = nullptr;
+            CUDA_OK(cudaMalloc(&c->proj_b.p, static_cast<size_t>(d_model) * sizeof(float)));
+            c->proj_b.cap = static_cast<size_t>(d_model) * sizeof(float);
+            CUDA_OK(cudaMemcpy(c->proj_b.p, bias, c->proj_b.cap, cudaMemcpyHostToDevice));
+        }
+        c->proj_in = f_in;
+        ++c->params_version;
+    });
+}
+
 int fwa_b200_backbone_forward(fwa_b200_ctx* c, const double* coords, const void* feats, int f64,
                               int64_t n, const fwa_config_t* cfg, fwa_output_t* out) {
     return guarded(c, [&] {
@@ -1254,11 +1497,11 @@ int fwa_b200_backbone_forward(fwa_b200_ctx* c, const double* coords, const void*
 int fwa_b200_backbone_forward_batch(fwa_b200_ctx* c, const double* coords, const void* feats,
                                     int f64, const int64_t* frame_offsets, int n_frames,
                                     const fwa_config_t* cfg, fwa_output_t* out,
-                                    int64_t* kept_per_frame) {
+                                    fwa_frame_stats_t* per_frame) {
     return guarded(c, [&] {
         if (!frame_offsets || n_frames < 1) throw FwaError{FWA_ERR_SHAPE, "need >= 1 frame"};
         if (frame_offsets[0] != 0) throw FwaError{FWA_ERR_SHAPE, "frame_offsets[0] must be 0"};
-        forward_host(c, coords, feats, f64, frame_offsets, n_frames, cfg, out, kept_per_frame);
+        forward_host(c, coords, feats, f64, frame_offsets, n_frames, cfg, out, per_frame);
     });
 }
 
@@ -1297,7 +1540,7 @@ int fwa_b200_backbone_forward_device(fwa_b200_ctx* c, const double* d_coords, co
         key.params_version = c->params_version;
         key.ws_epoch = c->ws_epoch;
         if (no_graph || c->g_disabled || c->profiling || c->exact_bins) {
-            forward_device(c, d_coords, d_feats, nullptr, cfg, S, d_out, d_kept);
+            forward_device(c, d_coords, d_feats, nullptr, cfg, S, d_out, d_kept, nullptr, nullptr, true);
             return;
         }
         if (c->g_exec && c->g_key == key) {
@@ -1306,7 +1549,7 @@ int fwa_b200_backbone_forward_device(fwa_b200_ctx* c, const double* d_coords, co
             return;
         }
         if (!(c->g_warm == key)) {  // first sighting: run eagerly (sizes the workspace)
-            forward_device(c, d_coords, d_feats, nullptr, cfg, S, d_out, d_kept);
+            forward_device(c, d_coords, d_feats, nullptr, cfg, S, d_out, d_kept, nullptr, nullptr, true);
             c->g_warm = key;
             c->g_warm.ws_epoch = c->ws_epoch;
             return;
@@ -1322,7 +1565,7 @@ int fwa_b200_backbone_forward_device(fwa_b200_ctx* c, const double* d_coords, co
         cudaGraph_t graph = nullptr;
         CUDA_OK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         try {
-            forward_device(c, d_coords, d_feats, nullptr, cfg, S, d_out, d_kept, c->g_tab);
+            forward_device(c, d_coords, d_feats, nullptr, cfg, S, d_out, d_kept, c->g_tab, nullptr, true);
         } catch (...) {
             cudaStreamEndCapture(c->stream, &graph);
             if (graph) cudaGraphDestroy(graph);
@@ -1336,7 +1579,7 @@ int fwa_b200_backbone_forward_device(fwa_b200_ctx* c, const double* d_coords, co
             if (graph) cudaGraphDestroy(graph);
             cudaGetLastError();
             c->g_disabled = true;  // not capturable here: stay eager
-            forward_device(c, d_coords, d_feats, nullptr, cfg, S, d_out, d_kept);
+            forward_device(c, d_coords, d_feats, nullptr, cfg, S, d_out, d_kept, nullptr, nullptr, true);
             return;
         }
         cudaGraphDestroy(graph);
@@ -1358,6 +1601,8 @@ int fwa_b200_split_begin(fwa_b200_ctx* c, const double* d_coords, int64_t n, con
     return guarded(c, [&] {
         validate_cfg(cfg);
         require_params(c, cfg);
+        if (c->proj_in > 0)
+            throw FwaError{FWA_ERR_CONTRACT, "split: project the input rows first (no input projection here)"};
         Schedule S;
         const int64_t off[2] = {0, n};
         host_frames(off, 1, cfg->group_size, S);

@@ -213,8 +213,10 @@ extern "C" int64_t fwa_b200_generate_pillars(const fwa_scene_spec_t* spec, uint6
     return n_cells;
 }
 
-extern "C" int64_t fwa_b200_init_params(const fwa_config_t* cfg, uint64_t seed, void* out,
-                                        size_t cap) {
+// init_backbone_params(cfg, f_in, seed) (backbone.hpp:83-102): when f_in != d_model the
+// input projection (d_model x f_in ~ N(0, 0.1^2), bias 0) is drawn first, then the blocks
+extern "C" int64_t fwa_b200_init_params_fin(const fwa_config_t* cfg, int32_t f_in, uint64_t seed, void* out,
+                                            size_t cap, float* proj_weight) {
     if (!cfg) return -FWA_ERR_CONFIG;
     const int d = cfg->d_model, h = cfg->n_heads, f = cfg->d_ff;
     if (cfg->resolution <= 0.0 || cfg->window_px < 1 || cfg->window_py < 1 ||
@@ -227,8 +229,12 @@ extern "C" int64_t fwa_b200_init_params(const fwa_config_t* cfg, uint64_t seed, 
     const size_t total = rec * static_cast<size_t>(cfg->n_blocks);
     if (!out) return static_cast<int64_t>(total);
     if (cap < total) return -FWA_ERR_CONFIG;
-    // f_in == d_model: no input projection is drawn (backbone.hpp:89-96)
+    if (f_in < 0) return -FWA_ERR_SHAPE;
     DetRng rng(seed);
+    if (f_in != d) {  // backbone.hpp:89-96
+        if (!proj_weight) return -FWA_ERR_SHAPE;
+        for (int i = 0; i < d * f_in; ++i) proj_weight[i] = static_cast<float>(rng.normal(0.0, 0.1));
+    }
     uint8_t* p = static_cast<uint8_t*>(out);
     for (int b = 0; b < cfg->n_blocks; ++b) {
         std::memcpy(p, "FWAP", 4);
@@ -253,4 +259,8 @@ extern "C" int64_t fwa_b200_init_params(const fwa_config_t* cfg, uint64_t seed, 
         p += rec;
     }
     return static_cast<int64_t>(total);
+}
+
+extern "C" int64_t fwa_b200_init_params(const fwa_config_t* cfg, uint64_t seed, void* out, size_t cap) {
+    return fwa_b200_init_params_fin(cfg, cfg ? cfg->d_model : 0, seed, out, cap, nullptr);
 }

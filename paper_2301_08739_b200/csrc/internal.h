@@ -49,7 +49,18 @@ void launch_sort_keys(const double* coords, int64_t ntot, int n_specs, double w_
 // d_nbins (may be null): device-side bin count of the sync-free path; 0 disables
 void launch_bins_hist(const long long* win, int64_t ntot, int n_specs, const int64_t* d_frame_off,
                       int n_frames, const SpecBins* d_specs, uint32_t* bin_of, uint32_t* hist,
-                      const uint32_t* d_nbins, cudaStream_t s, int64_t* launches);
+                      const uint32_t* d_nbins, cudaStream_t s, int64_t* launches, bool per_frame = false);
+// exact path: window min/max per (spec, frame) -> mm[(s * nf + f) * 4 + {min_M, max_M, min_m, max_m}]
+void launch_frame_minmax(const long long* win, int64_t ntot, int n_specs, const int64_t* d_frame_off, int n_frames,
+                         long long* mm, cudaStream_t s, int64_t* launches);
+// exact path, window ranges too wide for dense bins: bin_of[e] = dense rank of e's window
+// (spec, frame, win_major, win_minor) by a stable 3-pass radix sort; *d_count = windows;
+// hist (zeroed, capacity total) receives the per-window counts
+size_t window_ranks_temp_bytes(int64_t total);
+void launch_window_ranks(const long long* win, int64_t ntot, int n_specs, const int64_t* d_frame_off, int n_frames,
+                         unsigned long long* k64a, unsigned long long* k64b, uint32_t* va, uint32_t* vb,
+                         uint32_t* flag, uint32_t* ex, uint32_t* scan_tmp, uint32_t* d_count, void* temp,
+                         size_t temp_bytes, uint32_t* bin_of, uint32_t* hist, cudaStream_t s, int64_t* launches);
 // reduces the key partials -> mm[4*n_specs] (min/max per spec), bin specs, *d_nbins
 // (0 + *overflow = 1 when the dense range exceeds cap)
 void launch_bins_setup(const long long* partials, int64_t n_part, int n_specs, int nf, long long cap,
@@ -168,7 +179,11 @@ bool block_fused_supported(int G);
 void launch_block_fused(const float* x, const double* x64, const __half* pe16, const int32_t* ridx,
                         const int32_t* sidx, float* x_out, int64_t rows, int G, const TcBlockWeights& w,
                         int* d_nonfinite, cudaStream_t s, int64_t* launches,
-                        unsigned long long* trace = nullptr);
+                        unsigned long long* trace = nullptr, unsigned long long* phase = nullptr);
+// BackboneParams::input_proj (backbone.hpp:179-190), bit-exact: out[r][j] = bias[j] +
+// sum_c w[j][c] * (float)x[r][c], fp32, c in order, no FMA contraction
+void launch_input_proj(const void* x, bool x_f64, int64_t n, int f_in, const float* w, const float* b,
+                       int d, float* out, cudaStream_t s, int64_t* launches);
 // host: the per-rank pair images (2 x 128 KB) of one block's weights (W1 LN2-folded)
 void build_pair_images(const float* w_qkv, const float* w_out, const float* w1f, const float* w2,
                        uint16_t* out /* 2 * 65536 bf16 */);

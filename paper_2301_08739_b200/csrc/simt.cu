@@ -378,4 +378,30 @@ void launch_scatter_sorted(const float* src, const int32_t* pos, int64_t n, int 
     ++*launches;
 }
 
+// BackboneParams::input_proj (backbone.hpp:179-190): one thread per output element,
+// the reference's fp32 loop op by op (acc = bias[j]; acc += w[j][c] * (float)x[c], c in
+// order; -ffp-contract=off there, explicit round-to-nearest mul/add here) -- bit-exact.
+template <typename T>
+__global__ void k_input_proj(const T* __restrict__ x, int64_t n, int f_in, const float* __restrict__ w,
+                             const float* __restrict__ b, int d, float* __restrict__ out) {
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= n * d) return;
+    const int64_t r = e / d;
+    const int j = static_cast<int>(e - r * d);
+    const T* xr = x + r * f_in;
+    const float* wj = w + static_cast<int64_t>(j) * f_in;
+    float acc = b ? b[j] : 0.0f;
+    for (int c = 0; c < f_in; ++c) acc = __fadd_rn(acc, __fmul_rn(__ldg(wj + c), static_cast<float>(__ldg(xr + c))));
+    out[e] = acc;
+}
+
+void launch_input_proj(const void* x, bool x_f64, int64_t n, int f_in, const float* w, const float* b, int d,
+                       float* out, cudaStream_t s, int64_t* launches) {
+    if (n <= 0) return;
+    const unsigned grid = static_cast<unsigned>((n * d + 255) / 256);
+    if (x_f64) k_input_proj<double><<<grid, 256, 0, s>>>(static_cast<const double*>(x), n, f_in, w, b, d, out);
+    else k_input_proj<float><<<grid, 256, 0, s>>>(static_cast<const float*>(x), n, f_in, w, b, d, out);
+    ++*launches;
+}
+
 } // namespace fwa_b200

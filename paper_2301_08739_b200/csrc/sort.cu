@@ -27,6 +27,8 @@
 
 #include <climits>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -123,7 +125,7 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* 
 // ------------------------------------------------------------------ K1 keys
 
 __global__ void k_init_minmax(long long* mm, int n) {
-    const int i = threadIdx.x;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) mm[i] = (i & 1) ? LLONG_MIN : LLONG_MAX;  // [min_M, max_M, min_m, max_m] per spec
 }
 
@@ -260,21 +262,23 @@ FWA_DEVINL int frame_of(const int64_t* off, int n_frames, int64_t i) {
     return lo;
 }
 
+// specs: one SpecBins per spec (union window range of all frames, bins_per_frame apart),
+// or with per_frame one per (spec, frame) (each frame's own range; base = its first bin)
 __global__ void __launch_bounds__(256) k_bins_hist(const long long* __restrict__ win, int64_t ntot,
                                                    const int64_t* __restrict__ frame_off,
                                                    int n_frames, const SpecBins* __restrict__ specs,
                                                    uint32_t* __restrict__ bin_of,
                                                    uint32_t* __restrict__ hist,
-                                                   const uint32_t* __restrict__ d_nbins) {
+                                                   const uint32_t* __restrict__ d_nbins, int per_frame) {
     const int s = blockIdx.y;
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= ntot) return;
     if (d_nbins && *d_nbins == 0u) return;  // bin capacity overflow: host falls back
-    const SpecBins sb = specs[s];
     const int64_t e = static_cast<int64_t>(s) * ntot + i;
     const longlong2 w = reinterpret_cast<const longlong2*>(win)[e];
     const int f = n_frames > 1 ? frame_of(frame_off, n_frames, i) : 0;
-    const long long bin = sb.base + static_cast<long long>(f) * sb.bins_per_frame +
+    const SpecBins sb = specs[per_frame ? s * n_frames + f : s];
+    const long long bin = sb.base + (per_frame ? 0LL : static_cast<long long>(f) * sb.bins_per_frame) +
                           (w.x - sb.min_major) * sb.range_minor + (w.y - sb.min_minor);
     bin_of[e] = static_cast<uint32_t>(bin);
     // warp-aggregated: consecutive pillar ids mostly share a window
@@ -284,10 +288,154 @@ __global__ void __launch_bounds__(256) k_bins_hist(const long long* __restrict__
 
 void launch_bins_hist(const long long* win, int64_t ntot, int n_specs, const int64_t* d_frame_off,
                       int n_frames, const SpecBins* d_specs, uint32_t* bin_of, uint32_t* hist,
-                      const uint32_t* d_nbins, cudaStream_t s, int64_t* launches) {
+                      const uint32_t* d_nbins, cudaStream_t s, int64_t* launches, bool per_frame) {
     dim3 grid(static_cast<unsigned>((ntot + 255) / 256), static_cast<unsigned>(n_specs));
-    k_bins_hist<<<grid, 256, 0, s>>>(win, ntot, d_frame_off, n_frames, d_specs, bin_of, hist, d_nbins);
+    k_bins_hist<<<grid, 256, 0, s>>>(win, ntot, d_frame_off, n_frames, d_specs, bin_of, hist, d_nbins,
+                                     per_frame ? 1 : 0);
     ++*launches;
+}
+
+// ---- exact (host-sized) path helpers
+
+// window min/max per (spec, frame): mm[((s * nf) + f) * 4 + {min_M, max_M, min_m, max_m}]
+// (initialised to LLONG_MAX / LLONG_MIN).  A CTA's 256 consecutive pillars span few frames:
+// shared-memory atomics for the first 8 frames from the CTA's first one, then one global
+// atomic per touched slot (the rare farther frame goes straight to global)
+__global__ void __launch_bounds__(256) k_frame_minmax(const long long* __restrict__ win, int64_t ntot,
+                                                      const int64_t* __restrict__ frame_off, int n_frames,
+                                                      long long* __restrict__ mm) {
+    const int s = blockIdx.y;
+    __shared__ long long sm[8][4];
+    __shared__ int f0;
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x;
+    if (threadIdx.x < 32) sm[threadIdx.x >> 2][threadIdx.x & 3] = (threadIdx.x & 1) ? LLONG_MIN : LLONG_MAX;
+    if (threadIdx.x == 0) f0 = n_frames > 1 ? frame_of(frame_off, n_frames, base) : 0;
+    __syncthreads();
+    const int64_t i = base + threadIdx.x;
+    if (i < ntot) {
+        const longlong2 w = reinterpret_cast<const longlong2*>(win)[static_cast<int64_t>(s) * ntot + i];
+        const int f = n_frames > 1 ? frame_of(frame_off, n_frames, i) : 0;
+        const int k = f - f0;
+        long long* m = k < 8 ? sm[k] : mm + (static_cast<int64_t>(s) * n_frames + f) * 4;
+        atomicMin(m, w.x);
+        atomicMax(m + 1, w.x);
+        atomicMin(m + 2, w.y);
+        atomicMax(m + 3, w.y);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int k = threadIdx.x >> 2, q = threadIdx.x & 3;
+        const long long v = sm[k][q];
+        if (v != ((q & 1) ? LLONG_MIN : LLONG_MAX) && f0 + k < n_frames) {
+            long long* m = mm + (static_cast<int64_t>(s) * n_frames + f0 + k) * 4 + q;
+            if (q & 1) atomicMax(m, v);
+            else atomicMin(m, v);
+        }
+    }
+}
+
+void launch_frame_minmax(const long long* win, int64_t ntot, int n_specs, const int64_t* d_frame_off, int n_frames,
+                         long long* mm, cudaStream_t s, int64_t* launches) {
+    k_init_minmax<<<(4 * n_specs * n_frames + 255) / 256, 256, 0, s>>>(mm, 4 * n_specs * n_frames);
+    dim3 grid(static_cast<unsigned>((ntot + 255) / 256), static_cast<unsigned>(n_specs));
+    k_frame_minmax<<<grid, 256, 0, s>>>(win, ntot, d_frame_off, n_frames, mm);
+    *launches += 2;
+}
+
+// ---- window-rank compression: the exact path's fallback for window ranges too wide for a
+// dense bin per window (a far outlier, frames kilometres apart).  A stable LSD radix sort of
+// the elements by (spec * nf + frame, win_major, win_minor) -- three CUB passes, least
+// significant key first -- then a new-window flag + scan: bin_of[e] = the dense rank of e's
+// window in lexicographic window order, exactly the bin order of the dense layout.
+FWA_DEVINL unsigned long long flip64(long long v) {
+    return static_cast<unsigned long long>(v) ^ 0x8000000000000000ULL;
+}
+
+__global__ void k_wr_minor(const long long* __restrict__ win, int64_t total, unsigned long long* __restrict__ key,
+                           uint32_t* __restrict__ val) {
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= total) return;
+    key[e] = flip64(reinterpret_cast<const longlong2*>(win)[e].y);
+    val[e] = static_cast<uint32_t>(e);
+}
+
+__global__ void k_wr_major(const long long* __restrict__ win, int64_t total, const uint32_t* __restrict__ val,
+                           unsigned long long* __restrict__ key) {
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= total) return;
+    key[k] = flip64(reinterpret_cast<const longlong2*>(win)[val[k]].x);
+}
+
+__global__ void k_wr_frame(int64_t total, int64_t ntot, const int64_t* __restrict__ frame_off, int n_frames,
+                           const uint32_t* __restrict__ val, uint32_t* __restrict__ key) {
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= total) return;
+    const int64_t e = val[k];
+    const int64_t i = e % ntot;
+    key[k] = static_cast<uint32_t>((e / ntot) * n_frames + (n_frames > 1 ? frame_of(frame_off, n_frames, i) : 0));
+}
+
+__global__ void k_wr_flags(const long long* __restrict__ win, int64_t total, int64_t ntot,
+                           const int64_t* __restrict__ frame_off, int n_frames, const uint32_t* __restrict__ val,
+                           uint32_t* __restrict__ flag) {
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= total) return;
+    uint32_t f = 1u;
+    if (k > 0) {
+        const int64_t a = val[k], b = val[k - 1];
+        const longlong2 wa = reinterpret_cast<const longlong2*>(win)[a];
+        const longlong2 wb = reinterpret_cast<const longlong2*>(win)[b];
+        const int64_t sa = a / ntot, sb = b / ntot;
+        const int fa = n_frames > 1 ? frame_of(frame_off, n_frames, a % ntot) : 0;
+        const int fb = n_frames > 1 ? frame_of(frame_off, n_frames, b % ntot) : 0;
+        f = (sa != sb || fa != fb || wa.x != wb.x || wa.y != wb.y) ? 1u : 0u;
+    }
+    flag[k] = f;
+}
+
+__global__ void k_wr_assign(int64_t total, const uint32_t* __restrict__ val, const uint32_t* __restrict__ flag,
+                            const uint32_t* __restrict__ ex, uint32_t* __restrict__ bin_of,
+                            uint32_t* __restrict__ hist) {
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= total) return;
+    const uint32_t b = ex[k] + flag[k] - 1u;
+    bin_of[val[k]] = b;
+    atomicAdd(hist + b, 1u);
+}
+
+size_t window_ranks_temp_bytes(int64_t total) {
+    size_t a = 0, b = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, a, static_cast<const unsigned long long*>(nullptr),
+                                    static_cast<unsigned long long*>(nullptr), static_cast<const uint32_t*>(nullptr),
+                                    static_cast<uint32_t*>(nullptr), static_cast<int>(total));
+    cub::DeviceRadixSort::SortPairs(nullptr, b, static_cast<const uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
+                                    static_cast<const uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
+                                    static_cast<int>(total));
+    return a > b ? a : b;
+}
+
+void launch_window_ranks(const long long* win, int64_t ntot, int n_specs, const int64_t* d_frame_off, int n_frames,
+                         unsigned long long* k64a, unsigned long long* k64b, uint32_t* va, uint32_t* vb,
+                         uint32_t* flag, uint32_t* ex, uint32_t* scan_tmp, uint32_t* d_count, void* temp,
+                         size_t temp_bytes, uint32_t* bin_of, uint32_t* hist, cudaStream_t s, int64_t* launches) {
+    const int64_t total = ntot * n_specs;
+    const unsigned g = static_cast<unsigned>((total + 255) / 256);
+    const int nt = static_cast<int>(total);
+    k_wr_minor<<<g, 256, 0, s>>>(win, total, k64a, va);
+    size_t tb = temp_bytes;
+    cub::DeviceRadixSort::SortPairs(temp, tb, k64a, k64b, va, vb, nt, 0, 64, s);
+    k_wr_major<<<g, 256, 0, s>>>(win, total, vb, k64a);
+    tb = temp_bytes;
+    cub::DeviceRadixSort::SortPairs(temp, tb, k64a, k64b, vb, va, nt, 0, 64, s);
+    uint32_t* k32a = reinterpret_cast<uint32_t*>(k64a);
+    uint32_t* k32b = reinterpret_cast<uint32_t*>(k64b);
+    k_wr_frame<<<g, 256, 0, s>>>(total, ntot, d_frame_off, n_frames, va, k32a);
+    tb = temp_bytes;
+    cub::DeviceRadixSort::SortPairs(temp, tb, k32a, k32b, va, vb, nt, 0, 32, s);
+    k_wr_flags<<<g, 256, 0, s>>>(win, total, ntot, d_frame_off, n_frames, vb, flag);
+    exclusive_scan_u32(flag, ex, total, scan_tmp, d_count, s, launches);
+    k_wr_assign<<<g, 256, 0, s>>>(total, vb, flag, ex, bin_of, hist);
+    *launches += 8;
 }
 
 // Order-preserving integer image of a window-local coordinate: unsigned compare of the

@@ -21,3 +21,8 @@ def test_reference_caller_drop_in():
     assert out["ints_equal"] and out["numeric_error"]
     assert out["rel_err"] <= 1e-2
     assert out["stream_equal"]  # Backbone::run_frames == run per frame, bit for bit
+    assert out["empty_numeric_error"]  # empty PillarSet -> numeric_error, as backbone.hpp:218-222
+    assert out["stages_ok"], out["stages_ms"]  # RunStats.stages filled (bench_group reads them)
+    assert out["proj_ok"] and out["proj_rel_err"] <= 1e-2  # BackboneParams::input_proj on the device
+    assert out["proj_width_shape_error"]
+    assert out["concurrent_ok"]  # two threads through fwa::b200::run_backbone

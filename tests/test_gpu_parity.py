@@ -715,3 +715,49 @@ def test_block_backward_vs_reference(ctx32, d, h, dff, G, ng):
     assert gr[:16] == wr[:16]
     for i, (a, b) in enumerate(zip(_fwap_tensors(gr, d, dff), _fwap_tensors(wr, d, dff))):
         assert O.max_rel_err(a, b) <= 1e-4, i
+
+
+def test_batch_frames_far_apart_per_frame_bins(ctx32):
+    """Frames in world coordinates kilometres apart (a batch whose union window range
+    would need ~10^9 dense bins): each frame gets its own window range (exact path), the
+    outputs equal the per-frame runs bit for bit (per-frame bins)."""
+    cfg = F.FwaConfig(d_model=16, n_heads=4, d_ff=32, group_size=16, n_blocks=4)
+    ctx32.load_params(cfg, F.init_backbone_params(cfg, 2))
+    rng = np.random.default_rng(9)
+    frames = []
+    for k in range(3):
+        c = np.unique(np.round(rng.uniform(-15, 15, size=(400, 2)) / 0.32) * 0.32 + 0.16, axis=0)
+        c = c + np.array([[k * 40000.0, -k * 25000.0]])
+        frames.append(F.PillarSet(c, rng.normal(size=(c.shape[0], 16))))
+    off = np.cumsum([0] + [p.size() for p in frames])
+    res = ctx32.run_batch(np.concatenate([p.coords for p in frames]),
+                          np.concatenate([p.features for p in frames]), off, cfg)
+    ko = np.concatenate([[0], np.cumsum(res["kept_per_frame"])])
+    for i, p in enumerate(frames):
+        r = ctx32.run_backbone(p, cfg)
+        assert np.array_equal(res["kept"][ko[i]:ko[i + 1]] - off[i], r.kept_indices)
+        assert np.array_equal(res["features"][ko[i]:ko[i + 1]], r.features)
+
+
+def test_far_outlier_window_rank_fallback(ctx32):
+    """One pillar 10^8 m away: no dense window layout fits (the round-1 code raised
+    FWA_ERR_INTERNAL); the exact path rank-compresses the windows with a radix sort and the
+    result equals the oracle bit for bit in every integer output."""
+    rng = np.random.default_rng(10)
+    c = np.unique(np.round(rng.uniform(-20, 20, size=(600, 2)) / 0.32) * 0.32 + 0.16, axis=0)
+    c = np.concatenate([c, [[1.0e8 + 0.16, -3.0e7 + 0.48]]])
+    f = rng.normal(size=(c.shape[0], 16))
+    cfg = F.FwaConfig(d_model=16, n_heads=4, d_ff=32, group_size=16, n_blocks=4)
+    blob = F.init_backbone_params(cfg, 3)
+    ctx32.load_params(cfg, blob)
+    r = ctx32.run_backbone(F.PillarSet(c, f), cfg, want_block_perms=True)
+    w = O.port_run_backbone(c, f.astype(np.float32), O.make_cfg(d_model=16, n_heads=4, d_ff=32,
+                                                                group_size=16, n_blocks=4), blob,
+                            want_perms=True)
+    assert np.array_equal(r.kept_indices, w["kept"])
+    assert np.array_equal(np.concatenate(r.dropped_indices), w["dropped"])
+    for b in range(4):
+        assert np.array_equal(r.block_perms[b], w["block_perms"][b, :len(r.block_perms[b])])
+    assert O.max_rel_err(r.features, w["features"]) <= TOL_FP32
+    for spec in [F.WindowSpec(2.88, 2.88, sh, ax) for sh in (False, True) for ax in ("X", "Y")]:
+        assert np.array_equal(ctx32.sort(c, spec), O.np_sort(c, 2.88, 2.88, int(spec.shift), int(spec.major_axis == "Y")))

@@ -21,6 +21,9 @@ __global__ void k(float* out, long long* clk, int iters) {
             if (OP == 4) asm volatile("tanh.approx.f16x2 %0, %0;" : "+r"(h[i]));
             if (OP == 5) asm volatile("rcp.approx.ftz.f32 %0, %0;" : "+f"(v[i]));
             if (OP == 6) asm volatile("fma.rn.f32 %0, %0, %0, %0;" : "+f"(v[i]));
+            if (OP == 7) asm volatile("tanh.approx.bf16x2 %0, %0;" : "+r"(h[i]));
+            if (OP == 8) asm volatile("cvt.rn.f16x2.f32 %0, %1, %1;" : "+r"(h[i]) : "f"(__uint_as_float(h[i])));
+            if (OP == 9) asm volatile("fma.rn.f16x2 %0, %0, %0, %0;" : "+r"(h[i]));
         }
     }
     __syncthreads();
@@ -41,5 +44,5 @@ template <int OP> void run(const char* name) {
 }
 int main() {
     run<0>("ex2.f32"); run<1>("ex2.f16x2"); run<2>("ex2.bf16x2"); run<3>("tanh.f32"); run<4>("tanh.f16x2");
-    run<5>("rcp.f32"); run<6>("ffma");
+    run<5>("rcp.f32"); run<6>("ffma"); run<7>("tanh.bf16x2"); run<8>("cvt.f16x2.f32"); run<9>("hfma2");
 }
