@@ -358,6 +358,12 @@ def run_ours(args, rank, world, local_rank, dist):
     split = None
     if not args.no_split:
         split = secondary(run_split_scene, args, F, ctx, cfg, dev, stream, rank, world, dist, flush)
+    sweep = None
+    if world == 1 and not args.no_sweep:
+        sweep = secondary(run_sweep, args, F, ctx, dev, stream, flush)
+    f250 = None
+    if world == 1 and not args.no_sweep:
+        f250 = secondary(run_f250_frame, args, F, ctx, cfg, dev, stream, flush)
 
     # ---------------------------------------------------------------- reduce over ranks
     t_dev = torch.tensor([dev_ms, e2e_stream_s, float(n), float(nk), e2e_s], dtype=torch.float64, device=dev)
@@ -469,6 +475,8 @@ def run_ours(args, rank, world, local_rank, dist):
         "equal_window": ew,
         "config3_batch": batch,
         "config4_split": split,
+        "config5_sweep": sweep,
+        "f250_frame": f250,
     }
     print(json.dumps(line), flush=True)
 
@@ -499,6 +507,107 @@ def cpu_baseline_leg(ps, nk):
             "one_thread": {"value": c10.shape[0] / t_one, "unit": "pillars/s", "cores": 1,
                            "sample": f"one full 8-block run_backbone over the F10 frame ({c10.shape[0]} pillars), "
                                      f"1 thread, {t_one:.2f} s"}}
+
+
+def schedule_object(ms, pillars, n_specs=4):
+    """The window-sort schedule (4 sorts + groups + drops + kept-restricted plans) against the
+    HBM roofline: algorithmic bytes per pillar = 16 B coordinates in + per spec a 4 B full plan
+    and a 4 B kept-restricted plan out (SURVEY §8d's sort bytes, both plan forms the blocks
+    consume) = 48 B; frac vs the measured HBM copy bandwidth."""
+    hbm = peaks()[0]
+    byts = pillars * (16 + n_specs * 8)
+    gbs = byts / (ms / 1e3) / 1e9
+    return {"ms": ms, "pillars": pillars, "algorithmic_bytes": byts, "algorithmic_gbs": gbs, "frac_hbm": gbs / hbm,
+            "bytes_per_pillar": 16 + n_specs * 8}
+
+
+def profiled_pass(ctx, fn, flush):
+    """One eager pass with the context's stage events on: {slot: ms}."""
+    import torch
+    flush.zero_()
+    torch.cuda.synchronize()
+    ctx.set_profiling(True)
+    fn()
+    prof = ctx.profile()
+    ctx.set_profiling(False)
+    return {k: v[0] for k, v in prof.items()}
+
+
+def run_sweep(args, F, ctx, dev, stream, flush):
+    """BASELINE config 5: sparsity / group-size sweep (frames F10..F200 x G 32..128) for the
+    kernel roofline characterisation: per point the device time per frame (CUDA graph replay,
+    L2 flushed), the fused block kernel's TFLOP/s (algorithmic 2 (3D^2 + D^2 + 2 D D_ff + 2 G D)
+    FLOP per kept pillar per block) and frac, and the schedule's GB/s and frac."""
+    import torch
+    hbm, pk_burst, pk_sus, _ = peaks()
+    out = []
+    frames = {name: F.make_pillars(F.SCENES[name], 42) for name in ("F10", "F30", "F60", "F100", "F200")}
+    for name, ps in frames.items():
+        n = ps.size()
+        d_coords = torch.from_numpy(ps.coords).to(dev)
+        d_feats = torch.from_numpy(ps.features.astype(np.float32)).to(dev)
+        d_out = torch.empty((n, 128), dtype=torch.float32, device=dev)
+        for G in (32, 48, 69, 96, 128):
+            cfg = F.FwaConfig(group_size=G)
+            ctx.load_params(cfg, F.init_backbone_params(cfg, 42))
+            nk = (n // G) * G
+            fn = lambda: ctx.forward_device(d_coords.data_ptr(), d_feats.data_ptr(), [0, n], cfg, d_out.data_ptr())
+            for _ in range(3):
+                flush.zero_()
+                fn()
+            ms = 0.0
+            steps = 5
+            for _ in range(steps):
+                flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                fn()
+                b.record(stream)
+                torch.cuda.synchronize()
+                ms += a.elapsed_time(b)
+            ms /= steps
+            prof = profiled_pass(ctx, fn, flush)
+            blk_ms = prof["block_fused"] / cfg.n_blocks if prof["block_fused"] else None
+            flop = 2 * (131072 + 256 * G) * nk
+            tf = flop / (blk_ms / 1e3) / 1e12 if blk_ms else None
+            out.append({"frame": name, "pillars": n, "G": G, "ms_per_frame": ms, "pillars_per_s": n / (ms / 1e3),
+                        "block_kernel_ms": blk_ms, "block_tflops": tf,
+                        "block_frac_burst": tf / pk_burst if tf else None,
+                        "schedule": schedule_object(prof["schedule"], n)})
+    ctx.load_params(F.FwaConfig(), F.init_backbone_params(F.FwaConfig(), 42))
+    return {"workload": "BASELINE config 5: frames F10/F30/F60/F100/F200 (9,975..201,224 pillars) x group size "
+                        "32/48/69/96/128, 8 blocks, D 128, H 8, D_ff 256",
+            "timing": "ms_per_frame: CUDA-graph replay, L2 flushed, mean of 5; kernel / schedule times: one "
+                      "stage-timed eager pass", "points": out}
+
+
+def run_f250_frame(args, F, ctx, cfg, dev, stream, flush):
+    """The F250 scene (255,066 pillars) as ONE frame on one GPU (device-resident forward, CUDA
+    graph): ms/frame and the schedule at that size (BASELINE config 4's scene)."""
+    import torch
+    ps = F.make_pillars(F.SCENES["F250"], 42)
+    n = ps.size()
+    d_coords = torch.from_numpy(ps.coords).to(dev)
+    d_feats = torch.from_numpy(ps.features.astype(np.float32)).to(dev)
+    d_out = torch.empty((n, 128), dtype=torch.float32, device=dev)
+    fn = lambda: ctx.forward_device(d_coords.data_ptr(), d_feats.data_ptr(), [0, n], cfg, d_out.data_ptr())
+    for _ in range(3):
+        flush.zero_()
+        fn()
+    ms, steps = 0.0, 5
+    for _ in range(steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms += a.elapsed_time(b)
+    ms /= steps
+    prof = profiled_pass(ctx, fn, flush)
+    return {"workload": "F250 scene (255,066 pillars) as one frame, 8 blocks", "pillars": n, "ms_per_frame": ms,
+            "pillars_per_s": n / (ms / 1e3), "schedule": schedule_object(prof["schedule"], n),
+            "block_kernel_ms": prof["block_fused"] / cfg.n_blocks}
 
 
 def run_batch_frames(args, F, ctx, cfg, dev, stream, rank, world, dist, flush):
@@ -542,6 +651,7 @@ def run_batch_frames(args, F, ctx, cfg, dev, stream, rank, world, dist, flush):
         b.record(stream)
         torch.cuda.synchronize()
         ms += a.elapsed_time(b)
+    sched = schedule_object(profiled_pass(ctx, one, flush)["schedule"], n)
     t = torch.tensor([ms, float(n)], dtype=torch.float64, device=dev)
     if dist:
         mx = t.clone()
@@ -556,7 +666,8 @@ def run_batch_frames(args, F, ctx, cfg, dev, stream, rank, world, dist, flush):
             "frames": total_frames, "frames_per_gpu": per[rank], "pillars": int(n_all),
             "ms_per_batch": ms, "pillars_per_s": n_all / (ms / 1e3), "ms_per_frame": ms / total_frames,
             "collective": "none", "scaling": "strong (64 frames total)", "steps": steps,
-            "l2": "flushed by a 256 MiB write before every timed step"}
+            "l2": "flushed by a 256 MiB write before every timed step",
+            "schedule": dict(sched, note="this rank's batch of frames: one window sort per spec over all of them")}
 
 
 def run_points_pipeline(args, F, ctx, cfg, dev, stream, flush):
@@ -757,6 +868,7 @@ def main():
     ap.add_argument("--no-batch", action="store_true", help="skip the config-3 64-frame batch measurement")
     ap.add_argument("--no-points", action="store_true", help="skip the GPU pillarization measurement")
     ap.add_argument("--no-equal-window", action="store_true", help="skip the equal-window baseline comparison")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the config-5 sweep and the F250 single-frame run")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -731,9 +731,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBars);
     uint64_t* bW = bars;
     uint64_t* bReady = bars + 1;  // leader only: 2 arrivals (one per CTA) per handshake
-    uint64_t* bQKV = bars + 2;   // the Q chunk (the last): all QKV MMAs done
-    uint64_t* bK = bars + 9;     // the K chunk's MMAs done
-    uint64_t* bV = bars + 10;    // the V chunk's MMAs done
+    uint64_t* bQKV = bars + 2;
     uint64_t* bP = bars + 3;
     uint64_t* bUa = bars + 4;
     uint64_t* bUb = bars + 5;
@@ -750,7 +748,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
     if (threadIdx.x == 0) {
         mbar_init(bW, 1);
         mbar_init(bReady, 2);
-        for (int i = 2; i < 11; ++i) mbar_init(&bars[i], 1);
+        for (int i = 2; i < 9; ++i) mbar_init(&bars[i], 1);
         fence_mbar_init();
     }
     {
@@ -895,7 +893,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
     tmem_bias_row<96>(tmem + lane_off + 96 * cq, sVec + 96 * cq);  // the first unit's QKV bias
     tmem_st_wait();
     // phase clock sums live in the barrier block's spare slots (thread 0 only: no registers)
-    unsigned long long* ph_acc = reinterpret_cast<unsigned long long*>(smem + kOffTab + 384);  // [4] sums, [4] last stamp
+    unsigned long long* ph_acc = reinterpret_cast<unsigned long long*>(bars + 9);  // [4] sums, [4] last stamp
     if (kPhase && threadIdx.x == 0)
         for (int k = 0; k < 5; ++k) ph_acc[k] = 0ull;
     FPH(-1);
@@ -1023,19 +1021,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         }
         if (leader) {
             leader_wait();
-            // chunk by chunk, K, V, then Q, each with its own commit: the K / V epilogues run
-            // while the later chunks compute; Q (written in place into R_A, the A operand of
-            // every chunk) waits for all of them
 #pragma unroll
-            for (int ci = 0; ci < 3; ++ci) {
-                const int c = ci == 2 ? 0 : ci + 1;
+            for (int ks = 0; ks < 8; ++ks) {
+                const uint64_t ad = sdesc_sw128(sRA + (ks >> 2) * 16384 + (ks & 3) * 32);
 #pragma unroll
-                for (int ks = 0; ks < 8; ++ks)
-                    mma2_bf16(tmem + c * 128, sdesc_sw128(sRA + (ks >> 2) * 16384 + (ks & 3) * 32),
+                for (int c = 0; c < 3; ++c)
+                    mma2_bf16(tmem + c * 128, ad,
                               sdesc_sw128(sWa + kOffWqkv + c * 16384 + (ks >> 2) * 8192 + (ks & 3) * 32), id256,
                               1u);  // onto the bias
-                mma_commit_pair(ci == 0 ? bK : ci == 1 ? bV : bQKV);
             }
+            mma_commit_pair(bQKV);
         }
         ++hs;
         if (pend && warp != 0) {
@@ -1047,68 +1042,57 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         // epilogue's __syncthreads
         if (warp == 0) build_table(nloc, urow0, ext0, strad ? S / G : -1);
         if (pend) __syncthreads();  // staging read before the epilogue's K/V rows overwrite it
-        // every thread: heads 2cq, 2cq+1 of its row -> K | V rows (K/V region; the straddling
-        // group's rows also to the peer's extended rows), then Q (R_A, in place of O)
-        const bool kv_mine = rank == 1 || row < nloc || row >= split + tail;
-        int rext = -1;  // the straddling group's rows also go to the peer's extended rows
-        if (strad) {
-            if (rank == 0 && row >= S && row < split) rext = row - S;  // peer halo rows [0, h0)
-            if (rank == 1 && row < tail) rext = split + row;           // peer halo rows [split, split + tail)
-        }
-        // every extended row a key tile can touch gets finite data each unit (padding rows:
-        // bias-only K/V) -- except rank 0's padding rows under the halo
-#pragma unroll
-        for (int part = 0; part < 2; ++part) {  // 0: K (columns [128, 256)), 1: V ([256, 384))
-            mbar_wait(part ? bV : bK, ph);
-            fence_after_sync();
-            if (part == 0) FTR(tb + 3);
-            uint32_t kv[2][16];
-            tmem_ld16(tmem + lane_off + 128 + 128 * part + 32 * cq, kv[0]);
-            tmem_ld16(tmem + lane_off + 128 + 128 * part + 32 * cq + 16, kv[1]);
-            tmem_ld_wait();
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                const int h = 2 * cq + hh;
-                uint4 X[2];
-#pragma unroll
-                for (int hf = 0; hf < 2; ++hf) {
-                    uint32_t o[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e)  // the accumulators started at the bias
-                        o[e] = pack_bf16x2(__uint_as_float(kv[hh][8 * hf + 2 * e]), __uint_as_float(kv[hh][8 * hf + 2 * e + 1]));
-                    X[hf] = make_uint4(o[0], o[1], o[2], o[3]);
-                }
-                const int off = 256 * part + h * 32;
-                if (kv_mine) {
-                    uint8_t* kvrow = pKV + (ext0 + row) * kKVPitch + off;
-                    reinterpret_cast<uint4*>(kvrow)[0] = X[0];
-                    reinterpret_cast<uint4*>(kvrow)[1] = X[1];
-                }
-                if (rext >= 0) {
-                    const uint32_t dst = mapa(sKV + rext * kKVPitch + off, rank ^ 1);
-                    st_async_v4(dst, X[0], halo_remote);
-                    st_async_v4(dst + 16, X[1], halo_remote);
-                }
-            }
-        }
         mbar_wait(bQKV, ph);
         fence_after_sync();
-        {
-            uint32_t qv[2][16];
-            tmem_ld16(tmem + lane_off + 32 * cq, qv[0]);
-            tmem_ld16(tmem + lane_off + 32 * cq + 16, qv[1]);
+        FTR(tb + 3);
+        // every thread: heads 2cq, 2cq+1 of its row -> Q (R_A, in place of O), K|V rows
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+            const int h = 2 * cq + hh;
+            uint32_t qv[16], kv[16], vv[16];
+            tmem_ld16(tmem + lane_off + 16 * h, qv);
+            tmem_ld16(tmem + lane_off + 128 + 16 * h, kv);
+            tmem_ld16(tmem + lane_off + 256 + 16 * h, vv);
             tmem_ld_wait();
+            uint4 Q[2], K[2], V[2];
 #pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                const int h = 2 * cq + hh;
+            for (int hf = 0; hf < 2; ++hf) {
+                uint32_t oq[4], ok[4], ov[4];
 #pragma unroll
-                for (int hf = 0; hf < 2; ++hf) {
-                    uint32_t o[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        o[e] = pack_bf16x2(__uint_as_float(qv[hh][8 * hf + 2 * e]), __uint_as_float(qv[hh][8 * hf + 2 * e + 1]));
-                    *reinterpret_cast<uint4*>(pRA + sw128_offset(row, 16 * h + 8 * hf, 128)) = make_uint4(o[0], o[1], o[2], o[3]);
+                for (int e = 0; e < 4; ++e) {  // the accumulators started at the bias
+                    const int j = 8 * hf + 2 * e;
+                    oq[e] = pack_bf16x2(__uint_as_float(qv[j]), __uint_as_float(qv[j + 1]));
+                    ok[e] = pack_bf16x2(__uint_as_float(kv[j]), __uint_as_float(kv[j + 1]));
+                    ov[e] = pack_bf16x2(__uint_as_float(vv[j]), __uint_as_float(vv[j + 1]));
                 }
+                Q[hf] = make_uint4(oq[0], oq[1], oq[2], oq[3]);
+                K[hf] = make_uint4(ok[0], ok[1], ok[2], ok[3]);
+                V[hf] = make_uint4(ov[0], ov[1], ov[2], ov[3]);
+            }
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf)
+                *reinterpret_cast<uint4*>(pRA + sw128_offset(row, 16 * h + 8 * hf, 128)) = Q[hf];
+            // every extended row a key tile can touch gets finite data each unit (padding
+            // rows: bias-only K/V) -- except rank 0's padding rows under the halo
+            if (rank == 1 || row < nloc || row >= split + tail) {
+                uint8_t* kvrow = pKV + (ext0 + row) * kKVPitch + h * 32;
+                reinterpret_cast<uint4*>(kvrow)[0] = K[0];
+                reinterpret_cast<uint4*>(kvrow)[1] = K[1];
+                reinterpret_cast<uint4*>(kvrow + 256)[0] = V[0];
+                reinterpret_cast<uint4*>(kvrow + 256)[1] = V[1];
+            }
+            // the straddling group's rows also go to the peer's extended rows
+            int rext = -1;
+            if (strad) {
+                if (rank == 0 && row >= S && row < split) rext = row - S;  // peer halo rows [0, h0)
+                if (rank == 1 && row < tail) rext = split + row;           // peer halo rows [split, split + tail)
+            }
+            if (rext >= 0) {
+                const uint32_t dst = mapa(sKV + rext * kKVPitch + h * 32, rank ^ 1);
+                st_async_v4(dst, K[0], halo_remote);
+                st_async_v4(dst + 16, K[1], halo_remote);
+                st_async_v4(dst + 256, V[0], halo_remote);
+                st_async_v4(dst + 272, V[1], halo_remote);
             }
         }
         __syncthreads();        // local K/V, Q and the m-tile table visible

@@ -704,14 +704,14 @@ struct FusedArgs {
 // overlap the next unit's QKV MMA) -- into a.phase[0..3] once, at exit
 #define FPH(k)                                                                                  \
     do {                                                                                        \
-        if (kPhase && threadIdx.x == 0) {                                                       \
+        if (false) {                                                                            \
             const unsigned long long t_ = static_cast<unsigned long long>(clock64());           \
             if ((k) >= 0) ph_acc[(k)] += t_ - ph_acc[4];                                        \
             ph_acc[4] = t_;                                                                     \
         }                                                                                       \
     } while (0)
 
-template <int NT, int GC, bool kF64, bool kPhase>
+template <int NT, int GC, bool kF64>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block_fused(FusedArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
@@ -731,9 +731,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBars);
     uint64_t* bW = bars;
     uint64_t* bReady = bars + 1;  // leader only: 2 arrivals (one per CTA) per handshake
-    uint64_t* bQKV = bars + 2;   // the Q chunk (the last): all QKV MMAs done
-    uint64_t* bK = bars + 9;     // the K chunk's MMAs done
-    uint64_t* bV = bars + 10;    // the V chunk's MMAs done
+    uint64_t* bQKV = bars + 2;
     uint64_t* bP = bars + 3;
     uint64_t* bUa = bars + 4;
     uint64_t* bUb = bars + 5;
@@ -750,7 +748,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
     if (threadIdx.x == 0) {
         mbar_init(bW, 1);
         mbar_init(bReady, 2);
-        for (int i = 2; i < 11; ++i) mbar_init(&bars[i], 1);
+        for (int i = 2; i < 9; ++i) mbar_init(&bars[i], 1);
         fence_mbar_init();
     }
     {
@@ -895,8 +893,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
     tmem_bias_row<96>(tmem + lane_off + 96 * cq, sVec + 96 * cq);  // the first unit's QKV bias
     tmem_st_wait();
     // phase clock sums live in the barrier block's spare slots (thread 0 only: no registers)
-    unsigned long long* ph_acc = reinterpret_cast<unsigned long long*>(smem + kOffTab + 384);  // [4] sums, [4] last stamp
-    if (kPhase && threadIdx.x == 0)
+    unsigned long long* ph_acc = reinterpret_cast<unsigned long long*>(bars + 9);  // [4] sums, [4] last stamp
+    if (threadIdx.x == 0)
         for (int k = 0; k < 5; ++k) ph_acc[k] = 0ull;
     FPH(-1);
     int it = 0;
@@ -1023,19 +1021,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         }
         if (leader) {
             leader_wait();
-            // chunk by chunk, K, V, then Q, each with its own commit: the K / V epilogues run
-            // while the later chunks compute; Q (written in place into R_A, the A operand of
-            // every chunk) waits for all of them
 #pragma unroll
-            for (int ci = 0; ci < 3; ++ci) {
-                const int c = ci == 2 ? 0 : ci + 1;
+            for (int ks = 0; ks < 8; ++ks) {
+                const uint64_t ad = sdesc_sw128(sRA + (ks >> 2) * 16384 + (ks & 3) * 32);
 #pragma unroll
-                for (int ks = 0; ks < 8; ++ks)
-                    mma2_bf16(tmem + c * 128, sdesc_sw128(sRA + (ks >> 2) * 16384 + (ks & 3) * 32),
+                for (int c = 0; c < 3; ++c)
+                    mma2_bf16(tmem + c * 128, ad,
                               sdesc_sw128(sWa + kOffWqkv + c * 16384 + (ks >> 2) * 8192 + (ks & 3) * 32), id256,
                               1u);  // onto the bias
-                mma_commit_pair(ci == 0 ? bK : ci == 1 ? bV : bQKV);
             }
+            mma_commit_pair(bQKV);
         }
         ++hs;
         if (pend && warp != 0) {
@@ -1047,68 +1042,57 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         // epilogue's __syncthreads
         if (warp == 0) build_table(nloc, urow0, ext0, strad ? S / G : -1);
         if (pend) __syncthreads();  // staging read before the epilogue's K/V rows overwrite it
-        // every thread: heads 2cq, 2cq+1 of its row -> K | V rows (K/V region; the straddling
-        // group's rows also to the peer's extended rows), then Q (R_A, in place of O)
-        const bool kv_mine = rank == 1 || row < nloc || row >= split + tail;
-        int rext = -1;  // the straddling group's rows also go to the peer's extended rows
-        if (strad) {
-            if (rank == 0 && row >= S && row < split) rext = row - S;  // peer halo rows [0, h0)
-            if (rank == 1 && row < tail) rext = split + row;           // peer halo rows [split, split + tail)
-        }
-        // every extended row a key tile can touch gets finite data each unit (padding rows:
-        // bias-only K/V) -- except rank 0's padding rows under the halo
-#pragma unroll
-        for (int part = 0; part < 2; ++part) {  // 0: K (columns [128, 256)), 1: V ([256, 384))
-            mbar_wait(part ? bV : bK, ph);
-            fence_after_sync();
-            if (part == 0) FTR(tb + 3);
-            uint32_t kv[2][16];
-            tmem_ld16(tmem + lane_off + 128 + 128 * part + 32 * cq, kv[0]);
-            tmem_ld16(tmem + lane_off + 128 + 128 * part + 32 * cq + 16, kv[1]);
-            tmem_ld_wait();
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                const int h = 2 * cq + hh;
-                uint4 X[2];
-#pragma unroll
-                for (int hf = 0; hf < 2; ++hf) {
-                    uint32_t o[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e)  // the accumulators started at the bias
-                        o[e] = pack_bf16x2(__uint_as_float(kv[hh][8 * hf + 2 * e]), __uint_as_float(kv[hh][8 * hf + 2 * e + 1]));
-                    X[hf] = make_uint4(o[0], o[1], o[2], o[3]);
-                }
-                const int off = 256 * part + h * 32;
-                if (kv_mine) {
-                    uint8_t* kvrow = pKV + (ext0 + row) * kKVPitch + off;
-                    reinterpret_cast<uint4*>(kvrow)[0] = X[0];
-                    reinterpret_cast<uint4*>(kvrow)[1] = X[1];
-                }
-                if (rext >= 0) {
-                    const uint32_t dst = mapa(sKV + rext * kKVPitch + off, rank ^ 1);
-                    st_async_v4(dst, X[0], halo_remote);
-                    st_async_v4(dst + 16, X[1], halo_remote);
-                }
-            }
-        }
         mbar_wait(bQKV, ph);
         fence_after_sync();
-        {
-            uint32_t qv[2][16];
-            tmem_ld16(tmem + lane_off + 32 * cq, qv[0]);
-            tmem_ld16(tmem + lane_off + 32 * cq + 16, qv[1]);
+        FTR(tb + 3);
+        // every thread: heads 2cq, 2cq+1 of its row -> Q (R_A, in place of O), K|V rows
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+            const int h = 2 * cq + hh;
+            uint32_t qv[16], kv[16], vv[16];
+            tmem_ld16(tmem + lane_off + 16 * h, qv);
+            tmem_ld16(tmem + lane_off + 128 + 16 * h, kv);
+            tmem_ld16(tmem + lane_off + 256 + 16 * h, vv);
             tmem_ld_wait();
+            uint4 Q[2], K[2], V[2];
 #pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                const int h = 2 * cq + hh;
+            for (int hf = 0; hf < 2; ++hf) {
+                uint32_t oq[4], ok[4], ov[4];
 #pragma unroll
-                for (int hf = 0; hf < 2; ++hf) {
-                    uint32_t o[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        o[e] = pack_bf16x2(__uint_as_float(qv[hh][8 * hf + 2 * e]), __uint_as_float(qv[hh][8 * hf + 2 * e + 1]));
-                    *reinterpret_cast<uint4*>(pRA + sw128_offset(row, 16 * h + 8 * hf, 128)) = make_uint4(o[0], o[1], o[2], o[3]);
+                for (int e = 0; e < 4; ++e) {  // the accumulators started at the bias
+                    const int j = 8 * hf + 2 * e;
+                    oq[e] = pack_bf16x2(__uint_as_float(qv[j]), __uint_as_float(qv[j + 1]));
+                    ok[e] = pack_bf16x2(__uint_as_float(kv[j]), __uint_as_float(kv[j + 1]));
+                    ov[e] = pack_bf16x2(__uint_as_float(vv[j]), __uint_as_float(vv[j + 1]));
                 }
+                Q[hf] = make_uint4(oq[0], oq[1], oq[2], oq[3]);
+                K[hf] = make_uint4(ok[0], ok[1], ok[2], ok[3]);
+                V[hf] = make_uint4(ov[0], ov[1], ov[2], ov[3]);
+            }
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf)
+                *reinterpret_cast<uint4*>(pRA + sw128_offset(row, 16 * h + 8 * hf, 128)) = Q[hf];
+            // every extended row a key tile can touch gets finite data each unit (padding
+            // rows: bias-only K/V) -- except rank 0's padding rows under the halo
+            if (rank == 1 || row < nloc || row >= split + tail) {
+                uint8_t* kvrow = pKV + (ext0 + row) * kKVPitch + h * 32;
+                reinterpret_cast<uint4*>(kvrow)[0] = K[0];
+                reinterpret_cast<uint4*>(kvrow)[1] = K[1];
+                reinterpret_cast<uint4*>(kvrow + 256)[0] = V[0];
+                reinterpret_cast<uint4*>(kvrow + 256)[1] = V[1];
+            }
+            // the straddling group's rows also go to the peer's extended rows
+            int rext = -1;
+            if (strad) {
+                if (rank == 0 && row >= S && row < split) rext = row - S;  // peer halo rows [0, h0)
+                if (rank == 1 && row < tail) rext = split + row;           // peer halo rows [split, split + tail)
+            }
+            if (rext >= 0) {
+                const uint32_t dst = mapa(sKV + rext * kKVPitch + h * 32, rank ^ 1);
+                st_async_v4(dst, K[0], halo_remote);
+                st_async_v4(dst + 16, K[1], halo_remote);
+                st_async_v4(dst + 256, V[0], halo_remote);
+                st_async_v4(dst + 272, V[1], halo_remote);
             }
         }
         __syncthreads();        // local K/V, Q and the m-tile table visible
@@ -1172,10 +1156,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
             bulk_g2s(smem + kOffW2, a.wpair + static_cast<size_t>(rank) * kWBytes + 98304, 32768, bW2);
         }
         ++hs;
-        // while the out-proj MMAs run: the FFN1 accumulators start at b1' (LN2's beta folded
-        // in) -- this row, columns [128 + 64 cq, +64), which the QKV epilogue drained
-        tmem_bias_row<64>(tmem + lane_off + 128 + 64 * cq, sVec + 640 + 64 * cq);
-        tmem_st_wait();
         mbar_wait(bP, ph);
         fence_after_sync();
         FTR(tb + 8);
@@ -1215,6 +1195,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
                 }
                 *reinterpret_cast<uint4*>(pRA + sw128_offset(row, c0 + 8 * j, 128)) = make_uint4(o[0], o[1], o[2], o[3]);
             }
+            // the FFN1 accumulators start at b1' (LN2's beta folded in): this row, columns
+            // [128 + 64 cq, +64) -- the QKV epilogue drained them
+            tmem_bias_row<64>(tmem + lane_off + 128 + 64 * cq, sVec + 640 + 64 * cq);
+            tmem_st_wait();
         }
         FTR(tb + 9);
         handshake();
@@ -1305,7 +1289,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         __syncthreads();
         FPH(3);
     }
-    if (kPhase && threadIdx.x == 0)
+    if (a.phase && threadIdx.x == 0)
 #pragma unroll
         for (int k = 0; k < 4; ++k) atomicAdd(a.phase + k, ph_acc[k]);
     if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 64 + 49] = static_cast<unsigned long long>(clock64());
@@ -1318,11 +1302,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
     FTRG(62);
 }
 
-template <int NT, int GC, bool kF64, bool kPhase>
+template <int NT, int GC, bool kF64>
 int max_pairs() {
     static int n = -1;
     if (n < 0) {
-        cudaFuncSetAttribute(k_block_fused<NT, GC, kF64, kPhase>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+        cudaFuncSetAttribute(k_block_fused<NT, GC, kF64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(2 * kNumSMs);
         cfg.blockDim = dim3(kThreads);
@@ -1335,7 +1319,7 @@ int max_pairs() {
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         int c = 0;
-        if (cudaOccupancyMaxActiveClusters(&c, k_block_fused<NT, GC, kF64, kPhase>, &cfg) != cudaSuccess || c <= 0) {
+        if (cudaOccupancyMaxActiveClusters(&c, k_block_fused<NT, GC, kF64>, &cfg) != cudaSuccess || c <= 0) {
             cudaGetLastError();
             c = kNumSMs / 2;
         }
@@ -1344,9 +1328,9 @@ int max_pairs() {
     return n;
 }
 
-template <int NT, int GC, bool kF64, bool kPhase>
+template <int NT, int GC, bool kF64>
 void launch_t(const FusedArgs& a, cudaStream_t s) {
-    const int np = max_pairs<NT, GC, kF64, kPhase>();
+    const int np = max_pairs<NT, GC, kF64>();
     const int pairs = a.n_units < np ? a.n_units : np;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs));
@@ -1358,20 +1342,13 @@ void launch_t(const FusedArgs& a, cudaStream_t s) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_block_fused<NT, GC, kF64, kPhase>, a);
+    cudaLaunchKernelEx(&cfg, k_block_fused<NT, GC, kF64>, a);
 }
 
 template <int NT, int GC>
 void launch_nt(const FusedArgs& a, bool f64, cudaStream_t s) {
-    // the phase-counting kernels (stage timing of the host API) only for the default G = 69
-    // (the counters cost ~2% when compiled in, so the plain kernels never carry them)
-    if (GC == 69 && a.phase) {
-        if (f64) launch_t<NT, GC, true, GC == 69>(a, s);
-        else launch_t<NT, GC, false, GC == 69>(a, s);
-    } else {
-        if (f64) launch_t<NT, GC, true, false>(a, s);
-        else launch_t<NT, GC, false, false>(a, s);
-    }
+    if (f64) launch_t<NT, GC, true>(a, s);
+    else launch_t<NT, GC, false>(a, s);
 }
 
 // the rows of the extended K/V region one unit touches (both ranks), for the unit

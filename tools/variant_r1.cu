@@ -25,9 +25,8 @@
 //        completes), and then the staging of THIS unit's output rows, which warps 1-15
 //        store while the next unit's QKV MMA runs (warp 0 holds the MMA issuer)
 //   R_X  (60 KB, inside K/V): GELU half a (SW128 image) -> [FFN2]
-//   TMEM (512 columns): QKV [0,384), started at b_qkv (tcgen05.st of the bias rows) |
-//        the gathered fp32 residual rows + b_out [384,512), onto which the out-proj AND the
-//        FFN2 MMAs accumulate (out = TMEM + b2) | FFN1 U [128,384), started at b1' | LN2
+//   TMEM (512 columns): QKV [0,384) | the gathered fp32 residual rows [384,512), onto
+//        which the out-proj MMA accumulates | FFN1 U [128,384) | FFN2 O [0,128) | LN2
 //        row-statistics exchange [0,8)
 // The unit's rows are split between the pair at `split` (chosen on the host so that both
 // CTAs need the same number of attention task rounds); padding rows (A = 0) fill each
@@ -172,19 +171,6 @@ FWA_DEVINL void tmem_st32(uint32_t taddr, const float (&v)[32]) {
         "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
         : "memory");
 }
-FWA_DEVINL void tmem_st8(uint32_t taddr, float4 a, float4 b) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "f"(a.x),
-                 "f"(a.y), "f"(a.z), "f"(a.w), "f"(b.x), "f"(b.y), "f"(b.z), "f"(b.w)
-                 : "memory");
-}
-// this thread's TMEM row, columns [col, col + n): the broadcast bias values v[0, n) (8 at a
-// time: few live registers)
-template <int N>
-FWA_DEVINL void tmem_bias_row(uint32_t taddr, const float* v) {
-#pragma unroll
-    for (int j = 0; j < N; j += 8)
-        tmem_st8(taddr + j, *reinterpret_cast<const float4*>(v + j), *reinterpret_cast<const float4*>(v + j + 4));
-}
 FWA_DEVINL void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 FWA_DEVINL float4 tmem_ld4(uint32_t taddr) {
     uint32_t a, b, c, d;
@@ -282,11 +268,7 @@ FWA_DEVINL bool attn_task(uint32_t sRA, uint32_t sKV, uint8_t* pRA, int head, in
     const int nt_live = (G + 7) >> 3;
     uint32_t a0, a1, a2, a3;
     {
-        // rows >= qend belong to another task's m-tile (same head columns, which that task
-        // overwrites with its O): read this task's first row instead -- discarded rows, no
-        // cross-warp hazard
-        int qrow = m0 + (lane & 7) + ((lane >> 3) & 1) * 8;
-        if (qrow >= qend) qrow = m0;
+        const int qrow = m0 + (lane & 7) + ((lane >> 3) & 1) * 8;
         const int col = head * 16 + (lane >> 4) * 8;
         ldsm_x4(sRA + img_off(qrow, col), a0, a1, a2, a3);
     }
@@ -371,14 +353,13 @@ FWA_DEVINL bool attn_task(uint32_t sRA, uint32_t sKV, uint8_t* pRA, int head, in
         mma16816(o[1], p[2 * kt][0], p[2 * kt][1], p[2 * kt + 1][0], p[2 * kt + 1][1], vb[kt][2], vb[kt][3]);
         mma16816(l, p[2 * kt][0], p[2 * kt][1], p[2 * kt + 1][0], p[2 * kt + 1][1], kOnes, kOnes);
     }
-    const int r0 = m0 + g, r1 = r0 + 8;
-    if (!kMax) {  // only the kept rows (< qend) decide whether the task is re-run shifted
+    if (!kMax) {
         const float lmin = rcp_approx(lmax);
-        const bool ok = (r0 >= qend || (l[0] >= lmin && l[0] <= lmax)) && (r1 >= qend || (l[2] >= lmin && l[2] <= lmax));
+        const bool ok = l[0] >= lmin && l[0] <= lmax && l[2] >= lmin && l[2] <= lmax;
         if (__any_sync(0xffffffffu, !ok)) return false;
     }
     const float i0 = rcp_approx(l[0]), i1 = rcp_approx(l[2]);
-    __syncwarp();  // every lane's Q fragment reads (ldmatrix) precede any lane's O writes
+    const int r0 = m0 + g, r1 = r0 + 8;
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
         const int col = head * 16 + nt * 8 + 2 * t4;
@@ -406,8 +387,7 @@ FWA_DEVINL uint32_t attn_task2(uint32_t sRA, uint32_t sKV, uint8_t* pRA, const i
     float o[2][2][4] = {}, l[2][4] = {};
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-        int qrow = e[k].x + (lane & 7) + ((lane >> 3) & 1) * 8;
-        if (qrow >= e[k].y) qrow = e[k].x;  // rows past the part end: this task's own row (see attn_task)
+        const int qrow = e[k].x + (lane & 7) + ((lane >> 3) & 1) * 8;
         const int col = head[k] * 16 + (lane >> 4) * 8;
         ldsm_x4(sRA + img_off(qrow, col), a[k][0], a[k][1], a[k][2], a[k][3]);
     }
@@ -464,18 +444,15 @@ FWA_DEVINL uint32_t attn_task2(uint32_t sRA, uint32_t sKV, uint8_t* pRA, const i
     }
     const float lmin = rcp_approx(lmax);
     uint32_t redo = 0;
-    __syncwarp();  // every lane's Q fragment reads (ldmatrix) precede any lane's O writes
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-        const int r0 = e[k].x + g, r1 = r0 + 8;
-        // only the kept rows (< part end) decide whether the task is re-run shifted
-        const bool ok = (r0 >= e[k].y || (l[k][0] >= lmin && l[k][0] <= lmax)) &&
-                        (r1 >= e[k].y || (l[k][2] >= lmin && l[k][2] <= lmax));
+        const bool ok = l[k][0] >= lmin && l[k][0] <= lmax && l[k][2] >= lmin && l[k][2] <= lmax;
         if (__any_sync(0xffffffffu, !ok)) {
             redo |= 1u << k;
             continue;
         }
         const float i0 = rcp_approx(l[k][0]), i1 = rcp_approx(l[k][2]);
+        const int r0 = e[k].x + g, r1 = r0 + 8;
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) {
             const int col = head[k] * 16 + nt * 8 + 2 * t4;
@@ -678,7 +655,6 @@ struct FusedArgs {
     const float* vec;        // TcBlockWeights::vec_pair (1152 floats)
     int* nonfinite;
     unsigned long long* trace;  // FWA_B200_TRACE: 64 SM-clock slots per CTA (phase boundaries)
-    unsigned long long* phase;  // stage timing: SM clocks per phase summed over CTAs [gather, attention, ffn, scatter]
     float lmax;                 // attention fast pass: row sums beyond [1/lmax, lmax] re-run shifted
 };
 
@@ -698,20 +674,7 @@ struct FusedArgs {
         }                                                                                       \
     } while (0)
 
-// stage timing (fwa_output_t::stage_ms): thread 0 of every CTA sums the SM clocks of the
-// unit loop's phases -- gather (rows landed, LN1, residual parked), attention (QKV MMA
-// .. out-proj), ffn (LN2 .. FFN2), scatter (output staging; the row stores themselves
-// overlap the next unit's QKV MMA) -- into a.phase[0..3] once, at exit
-#define FPH(k)                                                                                  \
-    do {                                                                                        \
-        if (kPhase && threadIdx.x == 0) {                                                       \
-            const unsigned long long t_ = static_cast<unsigned long long>(clock64());           \
-            if ((k) >= 0) ph_acc[(k)] += t_ - ph_acc[4];                                        \
-            ph_acc[4] = t_;                                                                     \
-        }                                                                                       \
-    } while (0)
-
-template <int NT, int GC, bool kF64, bool kPhase>
+template <int NT, int GC, bool kF64>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block_fused(FusedArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
@@ -731,9 +694,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBars);
     uint64_t* bW = bars;
     uint64_t* bReady = bars + 1;  // leader only: 2 arrivals (one per CTA) per handshake
-    uint64_t* bQKV = bars + 2;   // the Q chunk (the last): all QKV MMAs done
-    uint64_t* bK = bars + 9;     // the K chunk's MMAs done
-    uint64_t* bV = bars + 10;    // the V chunk's MMAs done
+    uint64_t* bQKV = bars + 2;
     uint64_t* bP = bars + 3;
     uint64_t* bUa = bars + 4;
     uint64_t* bUb = bars + 5;
@@ -750,7 +711,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
     if (threadIdx.x == 0) {
         mbar_init(bW, 1);
         mbar_init(bReady, 2);
-        for (int i = 2; i < 11; ++i) mbar_init(&bars[i], 1);
+        for (int i = 2; i < 9; ++i) mbar_init(&bars[i], 1);
         fence_mbar_init();
     }
     {
@@ -892,13 +853,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
             if (lane == 16) sTab[16].x = n;
         }
     };
-    tmem_bias_row<96>(tmem + lane_off + 96 * cq, sVec + 96 * cq);  // the first unit's QKV bias
-    tmem_st_wait();
-    // phase clock sums live in the barrier block's spare slots (thread 0 only: no registers)
-    unsigned long long* ph_acc = reinterpret_cast<unsigned long long*>(smem + kOffTab + 384);  // [4] sums, [4] last stamp
-    if (kPhase && threadIdx.x == 0)
-        for (int k = 0; k < 5; ++k) ph_acc[k] = 0ull;
-    FPH(-1);
     int it = 0;
     for (int u = pair; u < a.n_units; u += npairs, ++it) {
         const uint32_t ph = it & 1;
@@ -964,10 +918,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const float4 f = *reinterpret_cast<const float4*>(xs + row * kXSPitch + (8 * cq + j) * 16);
-                    const float4 bo = *reinterpret_cast<const float4*>(sVec + 384 + c0 + 4 * j);
-                    xr[4 * j] = f.x + bo.x; xr[4 * j + 1] = f.y + bo.y; xr[4 * j + 2] = f.z + bo.z; xr[4 * j + 3] = f.w + bo.w;
+                    xr[4 * j] = f.x; xr[4 * j + 1] = f.y; xr[4 * j + 2] = f.z; xr[4 * j + 3] = f.w;
                 }
-                tmem_st32(tmem + lane_off + 384 + c0, xr);  // x + b_out: the out-proj accumulates onto it
+                tmem_st32(tmem + lane_off + 384 + c0, xr);
+                tmem_st_wait();
             }
         } else {
             const int sub = lane & 7, rl = lane >> 3;
@@ -1002,18 +956,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         const float4 f = *reinterpret_cast<const float4*>(pRX + stage_off(row & 63, 8 * cq + j));
-                        const float4 bo = *reinterpret_cast<const float4*>(sVec + 384 + c0 + 4 * j);
-                        xr[4 * j] = f.x + bo.x; xr[4 * j + 1] = f.y + bo.y; xr[4 * j + 2] = f.z + bo.z;
-                        xr[4 * j + 3] = f.w + bo.w;
+                        xr[4 * j] = f.x; xr[4 * j + 1] = f.y; xr[4 * j + 2] = f.z; xr[4 * j + 3] = f.w;
                     }
-                    tmem_st32(tmem + lane_off + 384 + c0, xr);  // x + b_out
+                    tmem_st32(tmem + lane_off + 384 + c0, xr);
                     tmem_st_wait();
                 }
                 __syncthreads();
             }
         }
         FTR(tb + 2);
-        FPH(0);
         handshake();
         uint8_t* stg = pKV;  // the previous unit's output staging: clear of this unit's halo rows
         if (rank == 1 && strad) stg += (h0 * kKVPitch + 15) & ~15;
@@ -1023,19 +974,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         }
         if (leader) {
             leader_wait();
-            // chunk by chunk, K, V, then Q, each with its own commit: the K / V epilogues run
-            // while the later chunks compute; Q (written in place into R_A, the A operand of
-            // every chunk) waits for all of them
 #pragma unroll
-            for (int ci = 0; ci < 3; ++ci) {
-                const int c = ci == 2 ? 0 : ci + 1;
+            for (int ks = 0; ks < 8; ++ks) {
+                const uint64_t ad = sdesc_sw128(sRA + (ks >> 2) * 16384 + (ks & 3) * 32);
 #pragma unroll
-                for (int ks = 0; ks < 8; ++ks)
-                    mma2_bf16(tmem + c * 128, sdesc_sw128(sRA + (ks >> 2) * 16384 + (ks & 3) * 32),
+                for (int c = 0; c < 3; ++c)
+                    mma2_bf16(tmem + c * 128, ad,
                               sdesc_sw128(sWa + kOffWqkv + c * 16384 + (ks >> 2) * 8192 + (ks & 3) * 32), id256,
-                              1u);  // onto the bias
-                mma_commit_pair(ci == 0 ? bK : ci == 1 ? bV : bQKV);
+                              ks > 0);
             }
+            mma_commit_pair(bQKV);
         }
         ++hs;
         if (pend && warp != 0) {
@@ -1047,68 +995,58 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         // epilogue's __syncthreads
         if (warp == 0) build_table(nloc, urow0, ext0, strad ? S / G : -1);
         if (pend) __syncthreads();  // staging read before the epilogue's K/V rows overwrite it
-        // every thread: heads 2cq, 2cq+1 of its row -> K | V rows (K/V region; the straddling
-        // group's rows also to the peer's extended rows), then Q (R_A, in place of O)
-        const bool kv_mine = rank == 1 || row < nloc || row >= split + tail;
-        int rext = -1;  // the straddling group's rows also go to the peer's extended rows
-        if (strad) {
-            if (rank == 0 && row >= S && row < split) rext = row - S;  // peer halo rows [0, h0)
-            if (rank == 1 && row < tail) rext = split + row;           // peer halo rows [split, split + tail)
-        }
-        // every extended row a key tile can touch gets finite data each unit (padding rows:
-        // bias-only K/V) -- except rank 0's padding rows under the halo
-#pragma unroll
-        for (int part = 0; part < 2; ++part) {  // 0: K (columns [128, 256)), 1: V ([256, 384))
-            mbar_wait(part ? bV : bK, ph);
-            fence_after_sync();
-            if (part == 0) FTR(tb + 3);
-            uint32_t kv[2][16];
-            tmem_ld16(tmem + lane_off + 128 + 128 * part + 32 * cq, kv[0]);
-            tmem_ld16(tmem + lane_off + 128 + 128 * part + 32 * cq + 16, kv[1]);
-            tmem_ld_wait();
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                const int h = 2 * cq + hh;
-                uint4 X[2];
-#pragma unroll
-                for (int hf = 0; hf < 2; ++hf) {
-                    uint32_t o[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e)  // the accumulators started at the bias
-                        o[e] = pack_bf16x2(__uint_as_float(kv[hh][8 * hf + 2 * e]), __uint_as_float(kv[hh][8 * hf + 2 * e + 1]));
-                    X[hf] = make_uint4(o[0], o[1], o[2], o[3]);
-                }
-                const int off = 256 * part + h * 32;
-                if (kv_mine) {
-                    uint8_t* kvrow = pKV + (ext0 + row) * kKVPitch + off;
-                    reinterpret_cast<uint4*>(kvrow)[0] = X[0];
-                    reinterpret_cast<uint4*>(kvrow)[1] = X[1];
-                }
-                if (rext >= 0) {
-                    const uint32_t dst = mapa(sKV + rext * kKVPitch + off, rank ^ 1);
-                    st_async_v4(dst, X[0], halo_remote);
-                    st_async_v4(dst + 16, X[1], halo_remote);
-                }
-            }
-        }
         mbar_wait(bQKV, ph);
         fence_after_sync();
-        {
-            uint32_t qv[2][16];
-            tmem_ld16(tmem + lane_off + 32 * cq, qv[0]);
-            tmem_ld16(tmem + lane_off + 32 * cq + 16, qv[1]);
+        FTR(tb + 3);
+        // every thread: heads 2cq, 2cq+1 of its row -> Q (R_A, in place of O), K|V rows
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+            const int h = 2 * cq + hh;
+            uint32_t qv[16], kv[16], vv[16];
+            tmem_ld16(tmem + lane_off + 16 * h, qv);
+            tmem_ld16(tmem + lane_off + 128 + 16 * h, kv);
+            tmem_ld16(tmem + lane_off + 256 + 16 * h, vv);
             tmem_ld_wait();
+            uint4 Q[2], K[2], V[2];
 #pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                const int h = 2 * cq + hh;
+            for (int hf = 0; hf < 2; ++hf) {
+                uint32_t oq[4], ok[4], ov[4];
 #pragma unroll
-                for (int hf = 0; hf < 2; ++hf) {
-                    uint32_t o[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        o[e] = pack_bf16x2(__uint_as_float(qv[hh][8 * hf + 2 * e]), __uint_as_float(qv[hh][8 * hf + 2 * e + 1]));
-                    *reinterpret_cast<uint4*>(pRA + sw128_offset(row, 16 * h + 8 * hf, 128)) = make_uint4(o[0], o[1], o[2], o[3]);
+                for (int e = 0; e < 4; ++e) {
+                    const int j = 8 * hf + 2 * e;
+                    const float* bq = sVec + 16 * h + j;
+                    oq[e] = pack_bf16x2(__uint_as_float(qv[j]) + bq[0], __uint_as_float(qv[j + 1]) + bq[1]);
+                    ok[e] = pack_bf16x2(__uint_as_float(kv[j]) + bq[128], __uint_as_float(kv[j + 1]) + bq[129]);
+                    ov[e] = pack_bf16x2(__uint_as_float(vv[j]) + bq[256], __uint_as_float(vv[j + 1]) + bq[257]);
                 }
+                Q[hf] = make_uint4(oq[0], oq[1], oq[2], oq[3]);
+                K[hf] = make_uint4(ok[0], ok[1], ok[2], ok[3]);
+                V[hf] = make_uint4(ov[0], ov[1], ov[2], ov[3]);
+            }
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf)
+                *reinterpret_cast<uint4*>(pRA + sw128_offset(row, 16 * h + 8 * hf, 128)) = Q[hf];
+            // every extended row a key tile can touch gets finite data each unit (padding
+            // rows: bias-only K/V) -- except rank 0's padding rows under the halo
+            if (rank == 1 || row < nloc || row >= split + tail) {
+                uint8_t* kvrow = pKV + (ext0 + row) * kKVPitch + h * 32;
+                reinterpret_cast<uint4*>(kvrow)[0] = K[0];
+                reinterpret_cast<uint4*>(kvrow)[1] = K[1];
+                reinterpret_cast<uint4*>(kvrow + 256)[0] = V[0];
+                reinterpret_cast<uint4*>(kvrow + 256)[1] = V[1];
+            }
+            // the straddling group's rows also go to the peer's extended rows
+            int rext = -1;
+            if (strad) {
+                if (rank == 0 && row >= S && row < split) rext = row - S;  // peer halo rows [0, h0)
+                if (rank == 1 && row < tail) rext = split + row;           // peer halo rows [split, split + tail)
+            }
+            if (rext >= 0) {
+                const uint32_t dst = mapa(sKV + rext * kKVPitch + h * 32, rank ^ 1);
+                st_async_v4(dst, K[0], halo_remote);
+                st_async_v4(dst + 16, K[1], halo_remote);
+                st_async_v4(dst + 256, V[0], halo_remote);
+                st_async_v4(dst + 272, V[1], halo_remote);
             }
         }
         __syncthreads();        // local K/V, Q and the m-tile table visible
@@ -1172,20 +1110,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
             bulk_g2s(smem + kOffW2, a.wpair + static_cast<size_t>(rank) * kWBytes + 98304, 32768, bW2);
         }
         ++hs;
-        // while the out-proj MMAs run: the FFN1 accumulators start at b1' (LN2's beta folded
-        // in) -- this row, columns [128 + 64 cq, +64), which the QKV epilogue drained
-        tmem_bias_row<64>(tmem + lane_off + 128 + 64 * cq, sVec + 640 + 64 * cq);
-        tmem_st_wait();
         mbar_wait(bP, ph);
         fence_after_sync();
         FTR(tb + 8);
-        FPH(1);
         {
             uint32_t v[32];
             tmem_ld32(tmem + lane_off + 384 + c0, v);  // x + P (the MMA accumulated onto x)
             tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 32; ++j) x1[j] = __uint_as_float(v[j]);  // (x + b_out) + P
+            for (int j = 0; j < 32; ++j) x1[j] = __uint_as_float(v[j]) + sVec[384 + c0 + j];
         }
         // ---- 4. LN2 (affine folded into W1 / b1) -> R_A
         {
@@ -1226,7 +1159,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
                 for (int ks = 0; ks < 8; ++ks)
                     mma2_bf16(tmem + 128 + 128 * hh, sdesc_sw128(sRA + (ks >> 2) * 16384 + (ks & 3) * 32),
                               sdesc_sw128(sWa + kOffW1 + hh * 16384 + (ks >> 2) * 8192 + (ks & 3) * 32), id256,
-                              1u);  // onto b1'
+                              ks > 0);
                 mma_commit_pair(hh ? bUb : bUa);
             }
         }
@@ -1241,14 +1174,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
             uint32_t v[32];
             tmem_ld32(tmem + lane_off + 128 + 128 * hh + c0, v);
             tmem_ld_wait();
+            const float* b1 = sVec + 640 + 128 * hh + c0;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 uint32_t o[4];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {  // the accumulators started at b1'
+                for (int e = 0; e < 4; ++e) {
                     const int k = 8 * j + 2 * e;
-                    const float g1 = __uint_as_float(v[k + 1]);
-                    o[e] = pack_bf16x2(gelu2_fast(__uint_as_float(v[k])),
+                    const float g1 = __uint_as_float(v[k + 1]) + b1[k + 1];
+                    o[e] = pack_bf16x2(gelu2_fast(__uint_as_float(v[k]) + b1[k]),
                                        (FWA_GELU_POLY && (k + 1) % FWA_GELU_POLY == FWA_GELU_POLY - 1)
                                            ? gelu2_poly(g1) : gelu2_fast(g1));
                 }
@@ -1260,32 +1194,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
                 leader_wait();
                 const uint32_t a0 = smem_u32(act);
 #pragma unroll
-                for (int ks = 0; ks < 8; ++ks)  // onto x1 = (x + b_out) + P in [384, 512)
-                    mma2_bf16(tmem + 384, sdesc_sw128(a0 + (ks >> 2) * 16384 + (ks & 3) * 32),
+                for (int ks = 0; ks < 8; ++ks)
+                    mma2_bf16(tmem, sdesc_sw128(a0 + (ks >> 2) * 16384 + (ks & 3) * 32),
                               sdesc_sw128(sWa + kOffW2 + (2 * hh + (ks >> 2)) * 8192 + (ks & 3) * 32), id256,
-                              1u);
+                              (hh | ks) > 0);
                 if (hh) mma_commit_pair(bO);
             }
             ++hs;
             FTR(tb + 11 + 2 * hh);
         }
-        // the NEXT unit's QKV accumulators start at the bias (b_qkv, LN1's beta folded in): this
-        // thread's row, columns [96 cq, 96 cq + 96).  [0, 384) is free: the handshake above
-        // retired every GELU read of U, and FFN2 accumulates onto [384, 512)
-        tmem_bias_row<96>(tmem + lane_off + 96 * cq, sVec + 96 * cq);
-        tmem_st_wait();
         // ---- 6. out = x1 + (O + b2) -> staged in R_A (two 64-row halves) -> row scatter
         mbar_wait(bO, ph);
         fence_after_sync();
         prefetch_x(u + npairs, gid);  // FFN2 done: the W2 / K/V / R_X region is free
         FTR(tb + 14);
-        FPH(2);
         {
             uint32_t v[32];
-            tmem_ld32(tmem + lane_off + 384 + c0, v);  // x1 + O (FFN2 accumulated onto the residual)
+            tmem_ld32(tmem + lane_off + c0, v);
             tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 32; ++j) x1[j] = __uint_as_float(v[j]) + sVec[512 + c0 + j];
+            for (int j = 0; j < 32; ++j) x1[j] = x1[j] + (__uint_as_float(v[j]) + sVec[512 + c0 + j]);
         }
 // this unit's output is written during the next unit's QKV MMA (or after the loop)
         if ((lane & 7) == 0) {
@@ -1295,19 +1223,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         pnloc = nloc;
         pend = true;
         FTR(tb + 15);
-        FPH(3);
     }
     if (pend) {  // the last unit's output
         __syncthreads();  // the row ids
         stage_out(pKV);
         __syncthreads();
         store_out(pKV, 0, 16);
-        __syncthreads();
-        FPH(3);
     }
-    if (kPhase && threadIdx.x == 0)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) atomicAdd(a.phase + k, ph_acc[k]);
     if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 64 + 49] = static_cast<unsigned long long>(clock64());
     FTRG(61);
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(a.nonfinite, 1);
@@ -1318,11 +1240,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
     FTRG(62);
 }
 
-template <int NT, int GC, bool kF64, bool kPhase>
+template <int NT, int GC, bool kF64>
 int max_pairs() {
     static int n = -1;
     if (n < 0) {
-        cudaFuncSetAttribute(k_block_fused<NT, GC, kF64, kPhase>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+        cudaFuncSetAttribute(k_block_fused<NT, GC, kF64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(2 * kNumSMs);
         cfg.blockDim = dim3(kThreads);
@@ -1335,7 +1257,7 @@ int max_pairs() {
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         int c = 0;
-        if (cudaOccupancyMaxActiveClusters(&c, k_block_fused<NT, GC, kF64, kPhase>, &cfg) != cudaSuccess || c <= 0) {
+        if (cudaOccupancyMaxActiveClusters(&c, k_block_fused<NT, GC, kF64>, &cfg) != cudaSuccess || c <= 0) {
             cudaGetLastError();
             c = kNumSMs / 2;
         }
@@ -1344,9 +1266,9 @@ int max_pairs() {
     return n;
 }
 
-template <int NT, int GC, bool kF64, bool kPhase>
+template <int NT, int GC, bool kF64>
 void launch_t(const FusedArgs& a, cudaStream_t s) {
-    const int np = max_pairs<NT, GC, kF64, kPhase>();
+    const int np = max_pairs<NT, GC, kF64>();
     const int pairs = a.n_units < np ? a.n_units : np;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs));
@@ -1358,20 +1280,13 @@ void launch_t(const FusedArgs& a, cudaStream_t s) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_block_fused<NT, GC, kF64, kPhase>, a);
+    cudaLaunchKernelEx(&cfg, k_block_fused<NT, GC, kF64>, a);
 }
 
 template <int NT, int GC>
 void launch_nt(const FusedArgs& a, bool f64, cudaStream_t s) {
-    // the phase-counting kernels (stage timing of the host API) only for the default G = 69
-    // (the counters cost ~2% when compiled in, so the plain kernels never carry them)
-    if (GC == 69 && a.phase) {
-        if (f64) launch_t<NT, GC, true, GC == 69>(a, s);
-        else launch_t<NT, GC, false, GC == 69>(a, s);
-    } else {
-        if (f64) launch_t<NT, GC, true, false>(a, s);
-        else launch_t<NT, GC, false, false>(a, s);
-    }
+    if (f64) launch_t<NT, GC, true>(a, s);
+    else launch_t<NT, GC, false>(a, s);
 }
 
 // the rows of the extended K/V region one unit touches (both ranks), for the unit
@@ -1451,10 +1366,9 @@ bool block_fused_supported(int G) { return G >= 1 && G <= 128 && choose_split(G)
 void launch_block_fused(const float* x, const double* x64, const __half* pe16, const int32_t* ridx,
                         const int32_t* sidx, float* x_out, int64_t rows, int G, const TcBlockWeights& w,
                         int* d_nonfinite, cudaStream_t s, int64_t* launches, unsigned long long* trace,
-                        unsigned long long* phase) {
+                        unsigned long long* /*phase*/) {
     if (rows <= 0) return;
     FusedArgs a{};
-    a.phase = phase;
     a.x = x; a.x64 = x64; a.pe16 = pe16; a.ridx = ridx; a.sidx = sidx; a.x_out = x_out;
     a.rows = rows; a.G = G; a.gpu = 256 / G;
     a.split = choose_split(G);
