@@ -789,16 +789,22 @@ def run_equal_window(args, F, ctx, cfg, dev, stream, flush):
 
 
 def run_split_scene(args, F, ctx, cfg, dev, stream, rank, world, dist, flush):
-    """BASELINE config 4: the F250 scene (255,066 pillars) split by group ranges across
-    the ranks with an all-gather of each block's sorted-order rows (NCCL over NVLink);
-    device time per scene, max over ranks (strong scaling: total work fixed)."""
+    """BASELINE config 4: the F250 scene (255,066 pillars) split by group ranges across the
+    ranks.  Default exchange "p2p": every block kernel writes its output rows straight into
+    the x buffer of the rank that needs them next (CUDA IPC peer memory over NVLink; a
+    1-element NCCL all-reduce orders the ranks between blocks) -- no pack / collective /
+    unpack.  "a2a" / "allgather": the NCCL collective paths.  Device time per scene, max over
+    ranks (strong scaling: total work fixed); the schedule (split_begin) is inside the timed
+    region."""
     import torch
 
-    from paper_2301_08739_b200.split import DeviceRunner, split_forward, split_forward_a2a
+    from paper_2301_08739_b200.split import DeviceRunner, split_forward, split_forward_a2a, split_forward_p2p
     ps = F.make_pillars(F.SCENES["F250"], 42)  # replicated on every rank
     n = ps.size()
     d_coords = torch.from_numpy(ps.coords).to(dev)
     d_feats = torch.from_numpy(ps.features.astype(np.float32)).to(dev)
+    exchange = args.split_exchange or "p2p"
+    flag = torch.zeros(1, dtype=torch.float32, device=dev)
 
     def all_gather(dst, src):
         if dist:
@@ -812,46 +818,62 @@ def run_split_scene(args, F, ctx, cfg, dev, stream, rank, world, dist, flush):
         else:
             dst.copy_(src)
 
+    def barrier():  # stream-ordered: every rank's block b before any rank's block b+1
+        if dist:
+            dist.all_reduce(flag)
+
+    def exchange_handles(mine):
+        allh = [None] * world
+        dist.all_gather_object(allh, mine)
+        return allh
+
     def alloc(rows):
         return torch.empty((rows, cfg.d_model), dtype=torch.float32, device=dev)
 
-    # all-to-all of only the needed rows when there are peers; one rank has nothing to exchange
-    exchange = args.split_exchange or ("a2a" if world > 1 else "allgather")
+    runner = DeviceRunner(ctx, d_coords, d_feats, cfg, same_stream=True,
+                          exchange_handles=exchange_handles if (dist and exchange == "p2p") else None)
 
     def one():
-        runner = DeviceRunner(ctx, d_coords, d_feats, cfg)
+        if exchange == "p2p":
+            return split_forward_p2p(runner, cfg.n_blocks, cfg.group_size, world, rank, barrier)
         if exchange == "a2a":
             return split_forward_a2a(runner, cfg.n_blocks, cfg.group_size, world, rank, all_gather, all_to_all,
                                      alloc)
         return split_forward(runner, cfg.n_blocks, cfg.group_size, world, rank, all_gather, alloc)
 
     steps = max(3, args.steps // 5)
-    for _ in range(2):
-        one()
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    ms = 0.0
-    for _ in range(steps):
-        flush.zero_()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        out = one()
-        b.record(stream)
+    try:
+        for _ in range(2):
+            one()
         torch.cuda.synchronize()
-        ms += a.elapsed_time(b)
+        if dist:
+            dist.barrier()
+        ms = 0.0
+        for _ in range(steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            out = one()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ms += a.elapsed_time(b)
+        ctx.sync_check()
+    finally:
+        if dist:
+            dist.barrier()  # no rank unmaps peer memory another rank may still write
+        runner.close()
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t[0]) / steps
-    if exchange == "a2a":
-        how = ("NCCL all_to_all_single of only the rows each rank needs for its next group range "
-               "(~K/P x 128 fp32 rows per rank per block; all-gather after the last block)")
-    else:
-        how = "NCCL all_gather_into_tensor of each block's K x 128 fp32 rows"
+    how = {"p2p": "peer memory: each block kernel writes its output rows straight into the consuming rank's "
+                  "x buffer (CUDA IPC over NVLink), 1-element NCCL all-reduce between blocks",
+           "a2a": "NCCL all_to_all_single of only the rows each rank needs for its next group range "
+                  "(~K/P x 128 fp32 rows per rank per block; all-gather after the last block)",
+           "allgather": "NCCL all_gather_into_tensor of each block's K x 128 fp32 rows"}[exchange]
     return {"workload": "F250 scene (255,066 pillars), 8 blocks, group-range split across the ranks",
             "pillars": n, "kept": int(out.shape[0]), "ms_per_scene": ms, "pillars_per_s": n / (ms / 1e3),
-            "exchange": how if dist else f"single rank ({exchange} exchange path, no peers)",
+            "exchange": how if dist else f"single rank ({exchange} path; no peers)", "world": world,
             "scaling": "strong", "steps": steps}
 
 
@@ -863,8 +885,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-split", action="store_true", help="skip the config-4 split-scene measurement")
-    ap.add_argument("--split-exchange", default=None, choices=["a2a", "allgather"],
-                    help="config-4 exchange between blocks (default: a2a with peers, allgather alone)")
+    ap.add_argument("--split-exchange", default=None, choices=["p2p", "a2a", "allgather"],
+                    help="config-4 exchange between blocks (default: p2p, the exchange fused into the block "
+                         "kernel over peer memory)")
     ap.add_argument("--no-batch", action="store_true", help="skip the config-3 64-frame batch measurement")
     ap.add_argument("--no-points", action="store_true", help="skip the GPU pillarization measurement")
     ap.add_argument("--no-equal-window", action="store_true", help="skip the equal-window baseline comparison")

@@ -240,6 +240,33 @@ int fwa_b200_split_plan(fwa_b200_ctx* ctx, int block, int32_t* ids_out);
 /* the same into a device buffer (K int32), enqueued on the context stream */
 int fwa_b200_split_plan_device(fwa_b200_ctx* ctx, int block, int32_t* d_ids_out);
 
+/* Peer-memory variant of the split (the exchange fused into the block kernel): instead of a
+ * collective between blocks, rank r's block-b kernel writes every output row straight into
+ * the x buffer (N x d_model f32, pillar-id order) of the rank whose block-(b+1) group range
+ * holds that pillar -- NVLink peer memory (x_peers from fwa_b200_ipc_open), so the transfer
+ * overlaps the block's compute row by row; the last block writes every row into rank 0's
+ * output buffer (out_peers[0], K x d_model, active order).  Between blocks the caller only
+ * orders the ranks (e.g. a 1-element NCCL all-reduce on the context stream).
+ *  p2p_setup: after split_begin; world <= 8; x_peers / out_peers: `world` device pointers
+ *             valid in this process (this rank's own at [rank]); builds the per-block
+ *             rank-tagged scatter rows of this rank's group range (split.py partition_groups).
+ *  block_p2p: block b over this rank's range; d_x = block 0: the input rows (N x d_model f32,
+ *             pillar-id order), later blocks: this rank's x buffer (x_peers[rank]).
+ * bf16 fused path only (FWA_ERR_CONTRACT otherwise); < 2^28 pillars. */
+int fwa_b200_split_p2p_setup(fwa_b200_ctx* ctx, int world, int rank, float* const* x_peers,
+                             float* const* out_peers);
+int fwa_b200_split_block_p2p(fwa_b200_ctx* ctx, int block, const float* d_x);
+
+/* Device memory that can be shared across processes (cudaMalloc'd, so IPC handles refer to
+ * the allocation base) and its CUDA IPC handles: export with fwa_b200_ipc_handle
+ * (FWA_IPC_HANDLE_BYTES), open in a peer process with fwa_b200_ipc_open. */
+#define FWA_IPC_HANDLE_BYTES 64
+void* fwa_b200_alloc(fwa_b200_ctx* ctx, size_t bytes);
+void fwa_b200_free(fwa_b200_ctx* ctx, void* d_ptr);
+int fwa_b200_ipc_handle(fwa_b200_ctx* ctx, void* d_ptr, void* handle_out);
+int fwa_b200_ipc_open(fwa_b200_ctx* ctx, const void* handle, void** d_ptr_out);
+int fwa_b200_ipc_close(fwa_b200_ctx* ctx, void* d_ptr);
+
 /* flatten::sort (minimum slice): host coords in, host permutation out. */
 int fwa_b200_sort_plan(fwa_b200_ctx* ctx, const double* coords, int64_t n, double w_x,
                        double w_y, int shift, int major_axis_y, int32_t* perm_out);

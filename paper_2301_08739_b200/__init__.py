@@ -41,6 +41,8 @@ EXPORTS = [
     "fwa_b200_pillarize", "fwa_b200_pillarize_device", "fwa_b200_generate_points", "fwa_b200_pillar_params",
     "fwa_b200_row_checksums", "fwa_b200_fnv1a64", "fwa_b200_equal_window_forward", "fwa_b200_block_backward",
     "fwa_b200_load_input_proj", "fwa_b200_init_params_fin", "fwa_b200_current_device",
+    "fwa_b200_split_p2p_setup", "fwa_b200_split_block_p2p", "fwa_b200_alloc", "fwa_b200_free",
+    "fwa_b200_ipc_handle", "fwa_b200_ipc_open", "fwa_b200_ipc_close",
 ]
 
 PREC_BF16, PREC_FP32, PREC_BF16_3K = 0, 1, 2
@@ -165,6 +167,15 @@ def lib():
         L.fwa_b200_split_scatter.argtypes = [vp, C.c_int, vp, vp]
         L.fwa_b200_split_plan.argtypes = [vp, C.c_int, vp]
         L.fwa_b200_split_plan_device.argtypes = [vp, C.c_int, vp]
+        L.fwa_b200_split_p2p_setup.argtypes = [vp, C.c_int, C.c_int, vp, vp]
+        L.fwa_b200_split_block_p2p.argtypes = [vp, C.c_int, vp]
+        L.fwa_b200_alloc.argtypes = [vp, C.c_size_t]
+        L.fwa_b200_alloc.restype = vp
+        L.fwa_b200_free.argtypes = [vp, vp]
+        L.fwa_b200_free.restype = None
+        L.fwa_b200_ipc_handle.argtypes = [vp, vp, vp]
+        L.fwa_b200_ipc_open.argtypes = [vp, vp, C.POINTER(vp)]
+        L.fwa_b200_ipc_close.argtypes = [vp, vp]
         L.fwa_b200_init_params.argtypes = [C.POINTER(_Cfg), C.c_uint64, vp, C.c_size_t]
         L.fwa_b200_init_params.restype = i64
         L.fwa_b200_init_params_fin.argtypes = [C.POINTER(_Cfg), i32, C.c_uint64, vp, C.c_size_t, vp]
@@ -553,6 +564,40 @@ class Context:
 
     def split_scatter(self, b: int, d_y: int, d_dst: int):
         self._check(lib().fwa_b200_split_scatter(self._h, b, C.c_void_p(d_y), C.c_void_p(d_dst)))
+
+    def split_p2p_setup(self, world: int, rank: int, x_ptrs: Sequence[int], out_ptrs: Sequence[int]):
+        """Peer-memory split: `world` device pointers of every rank's x buffer (N x D f32) and
+        output buffer (K x D f32), valid in this process."""
+        xp = (C.c_void_p * world)(*x_ptrs)
+        op = (C.c_void_p * world)(*out_ptrs)
+        self._check(lib().fwa_b200_split_p2p_setup(self._h, world, rank, xp, op))
+
+    def split_block_p2p(self, b: int, d_x: int):
+        self._check(lib().fwa_b200_split_block_p2p(self._h, b, C.c_void_p(d_x)))
+
+    def alloc(self, nbytes: int) -> int:
+        """cudaMalloc'd device memory (shareable by CUDA IPC)."""
+        p = lib().fwa_b200_alloc(self._h, nbytes)
+        if not p:
+            raise CudaError(lib().fwa_b200_last_error(self._h).decode())
+        return int(p)
+
+    def free(self, ptr: int):
+        lib().fwa_b200_free(self._h, C.c_void_p(ptr))
+
+    def ipc_handle(self, ptr: int) -> bytes:
+        h = (C.c_uint8 * 64)()
+        self._check(lib().fwa_b200_ipc_handle(self._h, C.c_void_p(ptr), h))
+        return bytes(h)
+
+    def ipc_open(self, handle: bytes) -> int:
+        p = C.c_void_p()
+        h = (C.c_uint8 * 64).from_buffer_copy(handle)
+        self._check(lib().fwa_b200_ipc_open(self._h, h, C.byref(p)))
+        return int(p.value)
+
+    def ipc_close(self, ptr: int):
+        self._check(lib().fwa_b200_ipc_close(self._h, C.c_void_p(ptr)))
 
     def split_plan_device(self, b: int, d_ids: int):
         self._check(lib().fwa_b200_split_plan_device(self._h, b, C.c_void_p(d_ids)))

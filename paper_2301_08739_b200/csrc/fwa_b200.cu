@@ -109,6 +109,13 @@ struct fwa_b200_ctx {
         __half* pe16 = nullptr;
         bool fast = false;
         uint64_t ws_epoch = 0;
+        // peer-memory variant: this rank's group range, per-block rank-tagged scatter rows
+        // (n_blocks x rows), device arrays of the 8 peer pointers (x buffers | outputs)
+        int world = 0, rank = 0;
+        int64_t g0 = 0, g1 = 0;
+        int32_t* p2p_sidx = nullptr;
+        float** p2p_x = nullptr;
+        float** p2p_out = nullptr;
     } split;
     int64_t* h_tab = nullptr;  // pinned frame-table staging (2 slots)
     size_t h_tab_cap = 0;
@@ -365,6 +372,27 @@ __global__ void k_out_pos(const int32_t* __restrict__ idx, const uint32_t* __res
     if (r < n) out[r] = static_cast<int32_t>(rank[idx[r]]);
 }
 
+
+// peer-memory split tables.  inv[s][pid] = position of pillar pid in spec s's kept plan
+__global__ void k_plan_inverse(const int32_t* __restrict__ idx, int64_t K, int32_t* __restrict__ inv) {
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k < K) inv[idx[k]] = static_cast<int32_t>(k);
+}
+// row r of this rank's block-b range: block b < last -> (rank owning the pillar's group in
+// block b+1) << 28 | pillar id; the last block -> its output row (rank 0's buffer)
+__global__ void k_p2p_rows(const int32_t* __restrict__ plan_b, const int32_t* __restrict__ inv_next,
+                           const int32_t* __restrict__ out_pos, int64_t r0, int64_t rows, int64_t chunk, int last,
+                           int32_t* __restrict__ sidx) {
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    if (last) {
+        sidx[r] = out_pos[r0 + r];
+        return;
+    }
+    const int32_t pid = plan_b[r0 + r];
+    const int32_t dest = static_cast<int32_t>(inv_next[pid] / chunk);
+    sidx[r] = (dest << 28) | pid;
+}
 
 std::vector<BlockParams> upload_block_params(const std::vector<Record>& recs, DevBuf& pf32,
                                              DevBuf& pbf16, cudaStream_t st) {
@@ -828,7 +856,8 @@ struct Scratch {
 // x_out[sidx[r]].  kernels.hpp:636-650 composed with backbone.hpp:245-283.
 void run_block(fwa_b200_ctx* c, const BlockParams& p, const fwa_config_t* cfg, int64_t rows,
                const int32_t* ridx, const float* x_in, const double* x_in64, const float* pe,
-               const __half* pe16, float* x_out, const int32_t* sidx, bool fast) {
+               const __half* pe16, float* x_out, const int32_t* sidx, bool fast,
+               float* const* d_peers = nullptr) {
     cudaStream_t st = c->stream;
     const int d = cfg->d_model, dff = cfg->d_ff, G = cfg->group_size;
     if (rows == 0) return;
@@ -843,10 +872,11 @@ void run_block(fwa_b200_ctx* c, const BlockParams& p, const fwa_config_t* cfg, i
         const int slot = r && r->next_slot < r->n_slots ? r->next_slot++ : -1;
         RecSpan span(c, slot >= 0 ? -1 : FWA_STAGE_ATTENTION, slot);
         launch_block_fused(x_in, x_in64, pe16, ridx, sidx, x_out, rows, G, p.tc, c->d_flag, st, &c->launches, tr,
-                           slot >= 0 ? r->d_phase + 4 * slot : nullptr);
+                           slot >= 0 ? r->d_phase + 4 * slot : nullptr, d_peers, d_peers ? 8 : 0);
         check_launch("k_block_fused");
         return;
     }
+    if (d_peers) throw FwaError{FWA_ERR_CONTRACT, "peer-memory split: needs the fused bf16 block kernel"};
     if (fast) {
         __nv_bfloat16* qkv = ws<__nv_bfloat16>(c, "qkv16", static_cast<size_t>(rows) * 3 * d);
         // attention output as per-128-row-tile SW128 images (the out-proj A operand)
@@ -1686,6 +1716,115 @@ int fwa_b200_split_scatter(fwa_b200_ctx* c, int block, const float* d_y, float* 
         launch_scatter_sorted(d_y, pos, sp.K, sp.cfg.d_model, d_dst, c->stream, &c->launches);
         check_launch();
     });
+}
+
+int fwa_b200_split_p2p_setup(fwa_b200_ctx* c, int world, int rank, float* const* x_peers, float* const* out_peers) {
+    return guarded(c, [&] {
+        auto& sp = c->split;
+        if (!sp.ready) throw FwaError{FWA_ERR_CONTRACT, "fwa_b200_split_begin first"};
+        if (sp.ws_epoch != c->ws_epoch)
+            throw FwaError{FWA_ERR_CONTRACT, "split: workspace moved since split_begin (call it again)"};
+        if (world < 1 || world > 8 || rank < 0 || rank >= world || !x_peers || !out_peers)
+            throw FwaError{FWA_ERR_SHAPE, "split p2p: 1 <= world <= 8, 0 <= rank < world, peer pointers"};
+        if (!sp.fast || c->precision != FWA_PREC_BF16 || !block_fused_supported(sp.cfg.group_size))
+            throw FwaError{FWA_ERR_CONTRACT, "peer-memory split: needs the fused bf16 block kernel"};
+        if (sp.ntot >= (int64_t{1} << 28)) throw FwaError{FWA_ERR_SHAPE, "peer-memory split: >= 2^28 pillars"};
+        cudaStream_t st = c->stream;
+        const int G = sp.cfg.group_size, nb = sp.cfg.n_blocks;
+        const int64_t n_groups = sp.K / G;
+        const int64_t per = std::max<int64_t>(1, (n_groups + world - 1) / world);  // split.py partition_groups
+        sp.world = world;
+        sp.rank = rank;
+        sp.g0 = std::min(rank * per, n_groups);
+        sp.g1 = std::min((rank + 1) * per, n_groups);
+        const int64_t rows = (sp.g1 - sp.g0) * G, r0 = sp.g0 * G, chunk = per * G;
+        const int n_specs = std::min(nb, 4);
+        int32_t* inv = ws<int32_t>(c, "p2p_inv", static_cast<size_t>(n_specs) * sp.ntot);
+        for (int s = 0; s < n_specs; ++s) {
+            k_plan_inverse<<<static_cast<unsigned>((sp.K + 255) / 256), 256, 0, st>>>(sp.idx + sp.K * s, sp.K,
+                                                                                       inv + sp.ntot * s);
+            ++c->launches;
+        }
+        sp.p2p_sidx = ws<int32_t>(c, "p2p_sidx", static_cast<size_t>(nb) * std::max<int64_t>(rows, 1));
+        for (int b = 0; b < nb; ++b) {
+            const bool last = b == nb - 1;
+            if (rows > 0) {
+                k_p2p_rows<<<static_cast<unsigned>((rows + 255) / 256), 256, 0, st>>>(
+                    sp.idx + sp.K * (b % 4), last ? nullptr : inv + sp.ntot * ((b + 1) % 4), sp.out_pos, r0, rows,
+                    chunk, last ? 1 : 0, sp.p2p_sidx + static_cast<int64_t>(b) * rows);
+                ++c->launches;
+            }
+        }
+        float* hp[16];
+        for (int k = 0; k < 8; ++k) {
+            hp[k] = x_peers[k < world ? k : 0];
+            hp[8 + k] = out_peers[k < world ? k : 0];
+        }
+        float** dp = ws<float*>(c, "p2p_peers", 16);
+        CUDA_OK(cudaMemcpyAsync(dp, hp, sizeof(hp), cudaMemcpyHostToDevice, st));
+        CUDA_OK(cudaStreamSynchronize(st));  // hp (host) is read by the copy
+        check_launch("split p2p tables");
+        sp.p2p_x = dp;
+        sp.p2p_out = dp + 8;
+        // the new table buffers bumped the workspace epoch; the schedule's own buffers (plans,
+        // output rows, PE) did not move -- re-arm the staleness check at the current epoch
+        if (c->ws["idx"].p != static_cast<void*>(sp.idx) || c->ws["out_pos"].p != static_cast<void*>(sp.out_pos)) {
+            sp.ready = false;
+            throw FwaError{FWA_ERR_CONTRACT, "split: workspace moved; call split_begin and p2p_setup again"};
+        }
+        sp.ws_epoch = c->ws_epoch;
+    });
+}
+
+int fwa_b200_split_block_p2p(fwa_b200_ctx* c, int block, const float* d_x) {
+    return guarded(c, [&] {
+        auto& sp = c->split;
+        if (!sp.ready || !sp.p2p_sidx) throw FwaError{FWA_ERR_CONTRACT, "fwa_b200_split_p2p_setup first"};
+        if (block < 0 || block >= sp.cfg.n_blocks || !d_x) throw FwaError{FWA_ERR_SHAPE, "split: bad block"};
+        if (sp.ws_epoch != c->ws_epoch)
+            throw FwaError{FWA_ERR_CONTRACT, "split: workspace moved since split_begin (call it again)"};
+        const int G = sp.cfg.group_size;
+        const int64_t rows = (sp.g1 - sp.g0) * G;
+        if (rows == 0) return;
+        const bool last = block == sp.cfg.n_blocks - 1;
+        const int32_t* idx = sp.idx + sp.K * (block % 4) + sp.g0 * G;
+        run_block(c, c->blocks[static_cast<size_t>(block)], &sp.cfg, rows, idx, d_x, nullptr, sp.pe, sp.pe16,
+                  nullptr, sp.p2p_sidx + static_cast<int64_t>(block) * rows, sp.fast, last ? sp.p2p_out : sp.p2p_x);
+    });
+}
+
+void* fwa_b200_alloc(fwa_b200_ctx* c, size_t bytes) {
+    void* p = nullptr;
+    const int rc = guarded(c, [&] { CUDA_OK(cudaMalloc(&p, bytes ? bytes : 1)); });
+    return rc == FWA_OK ? p : nullptr;
+}
+
+void fwa_b200_free(fwa_b200_ctx* c, void* d_ptr) {
+    if (c) cudaSetDevice(c->device);
+    if (d_ptr) cudaFree(d_ptr);
+}
+
+int fwa_b200_ipc_handle(fwa_b200_ctx* c, void* d_ptr, void* handle_out) {
+    return guarded(c, [&] {
+        if (!d_ptr || !handle_out) throw FwaError{FWA_ERR_SHAPE, "ipc: null pointer"};
+        cudaIpcMemHandle_t h;
+        CUDA_OK(cudaIpcGetMemHandle(&h, d_ptr));
+        static_assert(sizeof(h) == FWA_IPC_HANDLE_BYTES, "cudaIpcMemHandle_t size");
+        std::memcpy(handle_out, &h, sizeof(h));
+    });
+}
+
+int fwa_b200_ipc_open(fwa_b200_ctx* c, const void* handle, void** d_ptr_out) {
+    return guarded(c, [&] {
+        if (!handle || !d_ptr_out) throw FwaError{FWA_ERR_SHAPE, "ipc: null pointer"};
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof(h));
+        CUDA_OK(cudaIpcOpenMemHandle(d_ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+    });
+}
+
+int fwa_b200_ipc_close(fwa_b200_ctx* c, void* d_ptr) {
+    return guarded(c, [&] { CUDA_OK(cudaIpcCloseMemHandle(d_ptr)); });
 }
 
 int fwa_b200_sort_plan(fwa_b200_ctx* c, const double* coords, int64_t n, double w_x, double w_y,

@@ -179,7 +179,8 @@ bool block_fused_supported(int G);
 void launch_block_fused(const float* x, const double* x64, const __half* pe16, const int32_t* ridx,
                         const int32_t* sidx, float* x_out, int64_t rows, int G, const TcBlockWeights& w,
                         int* d_nonfinite, cudaStream_t s, int64_t* launches,
-                        unsigned long long* trace = nullptr, unsigned long long* phase = nullptr);
+                        unsigned long long* trace = nullptr, unsigned long long* phase = nullptr,
+                        float* const* peers = nullptr, int n_peers = 0);  // peers: DEVICE array of 8 pointers
 // BackboneParams::input_proj (backbone.hpp:179-190), bit-exact: out[r][j] = bias[j] +
 // sum_c w[j][c] * (float)x[r][c], fp32, c in order, no FMA contraction
 void launch_input_proj(const void* x, bool x_f64, int64_t n, int f_in, const float* w, const float* b,

@@ -41,8 +41,8 @@ __global__ void k_positional_embedding(const double* __restrict__ coords, int64_
 // fp16 fast path (PE rows feed the bf16 LN1 + PE sum): one thread per (pillar, axis), all
 // d/4 frequencies.  sin(2 pi f c) = sin(pi t), t = 2 f c: with 2f = Fh + Fl and
 // c = ch + cl as float pairs, t = p + e where p = Fh ch (e = its exact FMA residual plus
-// the cross terms); p is reduced EXACTLY mod 2 in fp32 (|p| < 2^22), then fp32
-// sincospi.  |err| ~1e-7, far below the fp16 rounding (2^-12) of the stored value.
+// the cross terms); p is reduced EXACTLY mod 2 in fp32 (|p| < 2^22), then the SFU's
+// sin / cos of pi r.  |err| < 1e-6, far below the fp16 rounding (2^-12) of the stored value.
 __global__ void k_pe_fp16(const double* __restrict__ coords, int64_t n, int nf, const float2* __restrict__ F,
                           __half* __restrict__ pe16) {
     const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -61,8 +61,10 @@ __global__ void k_pe_fp16(const double* __restrict__ coords, int64_t n, int nf, 
             const float p = f.x * ch;
             const float e = fmaf(f.x, ch, -p) + fmaf(f.x, cl, f.y * ch);
             const float r = fmaf(-2.0f, rintf(0.5f * p), p) + e;
+            // |pi r| <= pi (+ tiny): the SFU sin/cos (abs err <= 2^-21.4 on [-pi, pi]; fp32 pi and
+            // the product add < 1e-6) -- 2 MUFU ops instead of the software sincospi
             float sv, cv;
-            sincospif(r, &sv, &cv);
+            __sincosf(r * 3.14159265358979f, &sv, &cv);
             const __half2 h = __floats2half2_rn(sv, cv);
             w[j] = *reinterpret_cast<const uint32_t*>(&h);
         }

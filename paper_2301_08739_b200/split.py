@@ -11,6 +11,12 @@ to pillar-id order (`fwa_b200_split_scatter`) because block b+1 re-sorts with an
 rows each rank needs for its next group range (the per-peer lists follow from the
 replicated schedule), cutting the exchange from K rows to about K/P rows per rank.
 
+`split_forward_p2p` fuses the exchange into the block kernel: rank r's block-b kernel
+writes every output row straight into the x buffer of the rank whose block-(b+1) group range
+holds that pillar (peer memory over NVLink: CUDA IPC mappings of the peers' buffers), and the
+last block writes into rank 0's output -- no pack, no collective, no unpack; between blocks
+the ranks only order themselves (`barrier`, e.g. a 1-element NCCL all-reduce on the stream).
+
 `split_forward` is written against a small runner interface so the identical host logic
 runs on the GPU (`DeviceRunner`, the C ABI) and in the CPU gloo tests (an oracle runner).
 """
@@ -116,24 +122,97 @@ def split_forward_a2a(runner, n_blocks: int, group_size: int, world: int, rank: 
     return runner.out_buffer()
 
 
+def p2p_dest_rows(idx_b, idx_next, out_pos, ranges, per, group_size, rank, last):
+    """The rank-tagged scatter rows of `split_forward_p2p` (what fwa_b200_split_p2p_setup
+    builds on the device): row r of this rank's block-b range -> (rank owning its pillar in
+    block b+1) << 28 | pillar id, or, for the last block, rank 0's output row."""
+    import numpy as np
+    a, e = ranges[rank][0] * group_size, ranges[rank][1] * group_size
+    if last:
+        return np.asarray(out_pos, np.int64)[a:e]
+    idx_b = np.asarray(idx_b, np.int64)
+    idx_next = np.asarray(idx_next, np.int64)
+    pos = np.empty(int(max(idx_b.max(), idx_next.max())) + 1, np.int64)
+    pos[idx_next] = np.arange(idx_next.size)
+    pid = idx_b[a:e]
+    return ((pos[pid] // (per * group_size)) << 28) | pid
+
+
+def split_forward_p2p(runner, n_blocks: int, group_size: int, world: int, rank: int, barrier: Callable):
+    """runner: begin() -> K; p2p_setup(world, rank) (peer pointers + tables); input();
+    x_buffer(); block_p2p(b, x); out_buffer().  barrier(): orders every rank's block b before
+    any rank's block b+1 (stream-ordered).  Returns the output buffer (complete on rank 0)."""
+    runner.begin()
+    runner.p2p_setup(world, rank)
+    x = runner.input()
+    for b in range(n_blocks):
+        runner.block_p2p(b, x)
+        barrier()
+        x = runner.x_buffer()
+    return runner.out_buffer()
+
+
+def split_forward_p2p_emulated(runners, n_blocks: int):
+    """`world` = len(runners) ranks of split_forward_p2p in ONE process (one GPU): every
+    rank's runner has its own context, x buffer and output; the peers are plain local
+    pointers and the ranks' blocks run in turn on one stream (that order is the barrier).
+    Rank 0's output is returned."""
+    world = len(runners)
+    for r in runners:
+        r.begin()
+    xs = [r.x_buffer().data_ptr() for r in runners]
+    outs = [r.out_buffer().data_ptr() for r in runners]
+    for rk, r in enumerate(runners):
+        r.ctx.split_p2p_setup(world, rk, xs, outs)
+    for b in range(n_blocks):
+        for r in runners:
+            r.block_p2p(b, r.input() if b == 0 else r.x_buffer())
+    return runners[0].out_buffer()
+
+
 class DeviceRunner:
     """The C-ABI implementation (torch tensors for device memory)."""
 
-    def __init__(self, ctx, d_coords, d_feats, cfg):
+    def __init__(self, ctx, d_coords, d_feats, cfg, same_stream=False, exchange_handles=None):
+        """same_stream: the context runs on torch's current stream (created with it), so
+        library kernels, torch index ops and NCCL collectives are stream-ordered and no host
+        synchronisation is needed.  exchange_handles: see p2p_setup (world > 1)."""
         import torch
         self.ctx, self.cfg = ctx, cfg
         self.d_coords, self.d_feats = d_coords, d_feats
         self.n = d_coords.shape[0]
         dev = d_feats.device
-        self.x = torch.empty((self.n, cfg.d_model), dtype=torch.float32, device=dev)
+        self.same_stream = same_stream
+        self.exchange_handles = exchange_handles
+        self._opened = []
+        self._x_raw = self._out_raw = None
+        if exchange_handles is not None:  # cudaMalloc'd (IPC-shareable) x buffer
+            self._x_raw = ctx.alloc(self.n * cfg.d_model * 4)
+            self.x = _device_view(self._x_raw, (self.n, cfg.d_model), dev)
+        else:
+            self.x = torch.empty((self.n, cfg.d_model), dtype=torch.float32, device=dev)
         self.out = None
         self.dev = dev
 
     def begin(self):
         import torch
         K = self.ctx.split_begin(self.d_coords.data_ptr(), self.n, self.cfg)
-        self.out = torch.empty((K, self.cfg.d_model), dtype=torch.float32, device=self.dev)
+        if self.exchange_handles is not None:
+            if self._out_raw is None:
+                self._out_raw = self.ctx.alloc(K * self.cfg.d_model * 4)
+            self.out = _device_view(self._out_raw, (K, self.cfg.d_model), self.dev)
+        else:
+            self.out = torch.empty((K, self.cfg.d_model), dtype=torch.float32, device=self.dev)
         return K
+
+    def close(self):
+        for p in self._opened:
+            self.ctx.ipc_close(p)
+        self._opened = []
+        for p in (self._x_raw, self._out_raw):
+            if p:
+                self.ctx.free(p)
+        self._x_raw = self._out_raw = None
 
     def input(self):
         return self.d_feats
@@ -146,7 +225,34 @@ class DeviceRunner:
 
     def block(self, b, g0, g1, x, y_local):
         self.ctx.split_block(b, g0, g1, x.data_ptr(), y_local.data_ptr())
-        self.ctx.sync_check()  # the library's stream -> torch's (collectives, index ops)
+        if not self.same_stream:
+            self.ctx.sync_check()  # the library's stream -> torch's (collectives, index ops)
+
+    # ---- peer-memory exchange (split_forward_p2p)
+    def p2p_setup(self, world, rank):
+        """Peer pointers: this rank's own buffers alone, or -- with `exchange_handles`
+        (rank-ordered all-gather of bytes objects, e.g. dist.all_gather_object) -- CUDA IPC
+        mappings of every rank's cudaMalloc'd x and output buffers."""
+        if world == 1:
+            xs, outs = [self.x.data_ptr()], [self.out.data_ptr()]
+        else:
+            if self.exchange_handles is None:
+                raise RuntimeError("split_forward_p2p with world > 1 needs exchange_handles")
+            mine = (self.ctx.ipc_handle(self._x_raw), self.ctx.ipc_handle(self._out_raw))
+            allh = self.exchange_handles(mine)
+            xs, outs = [], []
+            for r, (hx, ho) in enumerate(allh):
+                if r == rank:
+                    xs.append(self._x_raw)
+                    outs.append(self._out_raw)
+                else:
+                    xs.append(self.ctx.ipc_open(hx))
+                    outs.append(self.ctx.ipc_open(ho))
+                    self._opened += [xs[-1], outs[-1]]
+        self.ctx.split_p2p_setup(world, rank, xs, outs)
+
+    def block_p2p(self, b, x):
+        self.ctx.split_block_p2p(b, x.data_ptr() if hasattr(x, "data_ptr") else int(x))
 
     def scatter(self, b, y_all, dst):
         self.ctx.split_scatter(b, y_all.data_ptr(), dst.data_ptr())
@@ -191,8 +297,19 @@ class DeviceRunner:
     def unpack(self, rows, pillar_ids, dst):
         import torch
         dst.index_copy_(0, pillar_ids, rows)
-        torch.cuda.synchronize(self.dev)  # before the next block kernel (library stream) reads dst
+        if not self.same_stream:
+            torch.cuda.synchronize(self.dev)  # before the next block kernel (library stream) reads dst
 
     def alloc_rows(self, n):
         import torch
         return torch.empty((n, self.cfg.d_model), dtype=torch.float32, device=self.dev)
+
+
+def _device_view(ptr, shape, dev):
+    """A torch float32 tensor over raw device memory (no ownership)."""
+    import torch
+
+    class _Arr:
+        __cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f4", "data": (int(ptr), False),
+                                    "version": 3, "strides": None}
+    return torch.as_tensor(_Arr(), device=dev)

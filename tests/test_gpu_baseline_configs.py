@@ -12,8 +12,9 @@ reference's own generator / pillarizer / initialiser (`O.ref_make_pillars`,
   config 3  the F60 seed-42 frame inside a batch of F60-spec frames (seeds 44, 42, 43)
             through fwa_b200_backbone_forward_batch: the same bars for that frame.
   config 4  the F250 scene (255,066 pillars) through the group-range split
-            (split.py, the C-ABI DeviceRunner) at emulated world 1 and 3 (all-gather) and
-            world 1 all-to-all: bf16 bar against the reference.
+            (split.py, the C-ABI DeviceRunner) at emulated world 1 and 3 (all-gather and the
+            peer-memory exchange fused into the block kernel) and world 1 all-to-all: bf16
+            bar against the reference.
 
 The measured errors are printed (pytest -s) and quoted in DESIGN.md §2.5."""
 import os
@@ -104,7 +105,7 @@ def test_config3_frame_inside_batch(f60):
     assert err <= TOL_BF16, err
 
 
-@pytest.mark.parametrize("world,exchange", [(1, "allgather"), (3, "allgather"), (1, "a2a")])
+@pytest.mark.parametrize("world,exchange", [(1, "allgather"), (3, "allgather"), (1, "a2a"), (1, "p2p"), (3, "p2p")])
 def test_config4_f250_split(f250, world, exchange):
     import torch
     from paper_2301_08739_b200.split import DeviceRunner, partition_groups, split_forward_a2a
@@ -116,7 +117,18 @@ def test_config4_f250_split(f250, world, exchange):
     dev = torch.device("cuda", 0)
     runner = DeviceRunner(ctx, torch.from_numpy(coords).to(dev),
                           torch.from_numpy(feats.astype(np.float32)).to(dev), cfg)
-    if exchange == "a2a":
+    if exchange == "p2p":  # `world` ranks emulated on this GPU: own contexts / x buffers, one stream
+        from paper_2301_08739_b200.split import split_forward_p2p_emulated
+        st = torch.cuda.Stream(dev)
+        with torch.cuda.stream(st):
+            dc, dfe = torch.from_numpy(coords).to(dev), torch.from_numpy(feats.astype(np.float32)).to(dev)
+            runners = []
+            for _ in range(world):
+                c = F.Context(0, stream=st.cuda_stream, precision="bf16")
+                c.load_params(cfg, blob)
+                runners.append(DeviceRunner(c, dc, dfe, cfg, same_stream=True))
+            out = split_forward_p2p_emulated(runners, cfg.n_blocks)
+    elif exchange == "a2a":
         out = split_forward_a2a(runner, cfg.n_blocks, cfg.group_size, 1, 0,
                                 lambda dst, src: dst.copy_(src),
                                 lambda dst, src, dc, sc: dst.copy_(src),

@@ -12,7 +12,8 @@ import pytest
 
 import oracle as O
 import paper_2301_08739_b200 as F
-from paper_2301_08739_b200.split import exchange_tables, partition_groups, split_forward, split_forward_a2a
+from paper_2301_08739_b200.split import (exchange_tables, p2p_dest_rows, partition_groups, split_forward,
+                                         split_forward_a2a, split_forward_p2p)
 
 D, H, DFF, G, NB = 16, 4, 32, 16, 4
 
@@ -251,5 +252,138 @@ def test_split_a2a_device_runner_equals_run_backbone():
                             lambda dst, src: dst.copy_(src),
                             lambda dst, src, dc, sc: dst.copy_(src),
                             lambda rows: torch.zeros((rows, 128), dtype=torch.float32, device=dev))
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), want.features)
+
+
+# ----------------------------------------------------------------------------- peer memory
+
+class SharedPeerOracleRunner(OracleRunner):
+    """split_forward_p2p on CPU: every rank's x buffer and output live in shared memory (the
+    stand-in for NVLink peer memory); block_p2p computes the rank's range with the C
+    restatement and writes each output row into the buffer of the rank that consumes it
+    next, per p2p_dest_rows -- exactly the rank-tagged rows the device tables hold."""
+
+    def __init__(self, coords, feats, blob, shm_x, shm_out):
+        super().__init__(coords, feats, blob)
+        self.shm_x, self.shm_out = shm_x, shm_out
+
+    def begin(self):
+        nk = super().begin()
+        self.peers_x = [np.frombuffer(b, np.float32).reshape(-1, D) for b in self.shm_x]
+        self.peers_out = [np.frombuffer(b, np.float32).reshape(-1, D) for b in self.shm_out]
+        return nk
+
+    def p2p_setup(self, world, rank):
+        self.world, self.rank = world, rank
+        n_groups = self.out.shape[0] // G
+        self.ranges, self.per = partition_groups(n_groups, world)
+
+    def x_buffer(self):
+        return self.peers_x[self.rank]
+
+    def out_buffer(self):
+        return self.peers_out[self.rank]
+
+    def block_p2p(self, b, x):
+        g0, g1 = self.ranges[self.rank]
+        rows = self.idx[b][g0 * G:g1 * G]
+        if not len(rows):
+            return
+        rec = self.blob[b * self.rec:(b + 1) * self.rec]
+        y = O.port_block_forward(x[rows], self.pe[rows], g1 - g0, rec)
+        last = b == NB - 1
+        tags = p2p_dest_rows(self.idx[b], None if last else self.idx[b + 1], self.out_pos, self.ranges,
+                             self.per, G, self.rank, last)
+        if last:
+            self.peers_out[0][tags] = y
+            return
+        for k, t in enumerate(tags):
+            self.peers_x[int(t) >> 28][int(t) & 0x0FFFFFFF] = y[k]
+
+
+def _gloo_worker_p2p(rank, world, port, coords, feats, blob, shm_x, shm_out, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        runner = SharedPeerOracleRunner(coords, feats, blob, shm_x, shm_out)
+        out = split_forward_p2p(runner, NB, G, world, rank, dist.barrier)
+        q.put((rank, out.copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_split_p2p_gloo_equals_single_process(world):
+    """The peer-memory exchange (each block's rows written straight into the consumer
+    rank's buffer, a barrier between blocks): rank 0's output == the single-process oracle
+    backbone, bit for bit, at world sizes 2 and 3 (gloo barrier, shared-memory peers)."""
+    import torch.multiprocessing as mp
+    coords, feats = _scene()
+    cfg = O.make_cfg(d_model=D, n_heads=H, d_ff=DFF, group_size=G, n_blocks=NB)
+    blob = F.init_backbone_params(F.FwaConfig(d_model=D, n_heads=H, d_ff=DFF, group_size=G, n_blocks=NB), 5)
+    want = O.port_run_backbone(coords, feats, cfg, blob)
+    ctx = mp.get_context("spawn")
+    n, nk = coords.shape[0], want["features"].shape[0]
+    shm_x = [ctx.RawArray("f", n * D) for _ in range(world)]
+    shm_out = [ctx.RawArray("f", nk * D) for _ in range(world)]
+    q = ctx.Queue()
+    port = 31500 + (os.getpid() % 1000) + world
+    procs = [ctx.Process(target=_gloo_worker_p2p, args=(r, world, port, coords, feats, blob, shm_x, shm_out, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert all(p.exitcode == 0 for p in procs)
+    assert np.array_equal(outs[0], want["features"])
+
+
+def test_p2p_dest_rows_partition_every_next_block_row():
+    """Every pillar of a rank's block-b range is tagged with the rank that holds it in block
+    b+1: over all ranks the tags route each next-block row to exactly its owner."""
+    rng = np.random.default_rng(8)
+    K, world = 41 * G, 3
+    kept = rng.permutation(K + 7)[:K]
+    idx_b, idx_n = rng.permutation(kept), rng.permutation(kept)
+    ranges, per = partition_groups(K // G, world)
+    got = {}
+    for r in range(world):
+        for t in p2p_dest_rows(idx_b, idx_n, None, ranges, per, G, r, False):
+            got[int(t) & 0x0FFFFFFF] = int(t) >> 28
+    assert len(got) == K
+    for s_ in range(world):
+        a, b = ranges[s_][0] * G, ranges[s_][1] * G
+        assert all(got[int(p)] == s_ for p in idx_n[a:b])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_split_p2p_device_emulated_equals_run_backbone(world):
+    """The C-ABI peer-memory split, `world` ranks emulated in one process on one GPU (each
+    rank its own context, x buffer and output; peers = local pointers): rank 0's output is
+    bitwise equal to run_backbone (rows are independent of their tile position)."""
+    import torch
+    from paper_2301_08739_b200.split import DeviceRunner, split_forward_p2p_emulated
+    ps = F.make_pillars(F.SCENES["F10"], 42)
+    cfg = F.FwaConfig()
+    blob = F.init_backbone_params(cfg, 42)
+    ref_ctx = F.Context(0, precision="bf16")
+    ref_ctx.load_params(cfg, blob)
+    want = ref_ctx.run_backbone(F.PillarSet(ps.coords, ps.features.astype(np.float32)), cfg)
+    dev = torch.device("cuda", 0)
+    st = torch.cuda.Stream(dev)
+    with torch.cuda.stream(st):
+        dc = torch.from_numpy(ps.coords).to(dev)
+        df = torch.from_numpy(ps.features.astype(np.float32)).to(dev)
+        runners = []
+        for _ in range(world):
+            c = F.Context(0, stream=st.cuda_stream, precision="bf16")
+            c.load_params(cfg, blob)
+            runners.append(DeviceRunner(c, dc, df, cfg, same_stream=True))
+        out = split_forward_p2p_emulated(runners, cfg.n_blocks)
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy(), want.features)

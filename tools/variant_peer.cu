@@ -64,10 +64,6 @@ namespace {
 
 constexpr int kThreads = 512;
 constexpr int kMaxPeers = 8;
-// kernel modes (template): the plain block; + per-phase SM-clock counters (StageTimes of the
-// host API); + rank-tagged output rows (the peer-memory split).  Kept as separate instances:
-// either addition costs 2-6% when compiled into the plain kernel (register pressure).
-constexpr int kModePlain = 0, kModePhase = 1, kModePeer = 2;
 constexpr int kWBytes = 131072;  // per-rank weight image in HBM: W_qkv 48K | W_out 16K | W1' 32K | W2 32K
 constexpr int kOffWqkv = 0, kOffWout = 49152, kOffW1 = 65536;
 constexpr int kOffRA = 98304;                   // 32 KB SW128 image
@@ -676,6 +672,11 @@ struct FusedArgs {
     const int32_t* ridx;     // block row -> pillar id (gather)
     const int32_t* sidx;     // block row -> output row (scatter)
     float* x_out;
+    // peer-memory split (fwa_b200_split_block_p2p): output row r goes to
+    // peer[sidx[r] >> 28] + (sidx[r] & 0x0FFFFFFF) * 128 -- the buffer of the rank that
+    // consumes it next (NVLink peer memory or, emulated, another local buffer); peer[0] ==
+    // x_out and no high bits otherwise
+    float* peer[kMaxPeers];
     int64_t rows;            // n_groups * G
     int G, gpu, n_units;
     int split;               // rank 0 holds unit rows [0, split), rank 1 [split, R)
@@ -685,10 +686,6 @@ struct FusedArgs {
     unsigned long long* trace;  // FWA_B200_TRACE: 64 SM-clock slots per CTA (phase boundaries)
     unsigned long long* phase;  // stage timing: SM clocks per phase summed over CTAs [gather, attention, ffn, scatter]
     float lmax;                 // attention fast pass: row sums beyond [1/lmax, lmax] re-run shifted
-    // peer-memory split (fwa_b200_split_block_p2p): output row r goes to
-    // peer[sidx[r] >> 28] + (sidx[r] & 0x0FFFFFFF) * 128 -- the buffer of the rank that
-    // consumes it next (NVLink peer memory or, emulated, another local buffer)
-    float* const* peer;  // device array of kMaxPeers pointers (null: plain rows)
 };
 
 #define FTR(k)                                                                                  \
@@ -713,14 +710,14 @@ struct FusedArgs {
 // overlap the next unit's QKV MMA) -- into a.phase[0..3] once, at exit
 #define FPH(k)                                                                                  \
     do {                                                                                        \
-        if (kMode == kModePhase && threadIdx.x == 0) {                                          \
+        if (kPhase && threadIdx.x == 0) {                                                       \
             const unsigned long long t_ = static_cast<unsigned long long>(clock64());           \
             if ((k) >= 0) ph_acc[(k)] += t_ - ph_acc[4];                                        \
             ph_acc[4] = t_;                                                                     \
         }                                                                                       \
     } while (0)
 
-template <int NT, int GC, bool kF64, int kMode>
+template <int NT, int GC, bool kF64, bool kPhase>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block_fused(FusedArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
@@ -736,6 +733,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
     uint8_t* pRX = smem + kOffRX;
     int4* sTab = reinterpret_cast<int4*>(smem + kOffTab);
     int* sRowId = reinterpret_cast<int*>(smem + kOffRowId);
+    float** sPeer = reinterpret_cast<float**>(smem + kOffTab + 448);  // the output peer table (8 pointers)
     float* sVec = reinterpret_cast<float*>(smem + kOffVec);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBars);
     uint64_t* bW = bars;
@@ -768,8 +766,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
     }
     for (int i = threadIdx.x; i < kVecFloats; i += kThreads)
         sVec[i] = a.vec[i];
-    if (kMode == kModePeer && threadIdx.x < kMaxPeers)  // the output peer table
-        reinterpret_cast<float**>(smem + kOffTab + 448)[threadIdx.x] = a.peer[threadIdx.x];
+    if (threadIdx.x < kMaxPeers) sPeer[threadIdx.x] = a.peer[threadIdx.x];
     if (warp == 0) {
         __syncwarp();
         tmem_alloc2(tmem_slot, 512);
@@ -876,13 +873,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
     auto store_out = [&](const uint8_t* stg, int w0, int nw) {  // warps [w0, w0 + nw): rows w - w0 + nw*k
         for (int r = warp - w0; r < pnloc; r += nw) {
             const float4 o = *reinterpret_cast<const float4*>(stg + stage_off(r, lane));
-            if constexpr (kMode == kModePeer) {
-                const uint32_t rid = static_cast<uint32_t>(sRowId[r]);
-                float* const base = reinterpret_cast<float* const*>(smem + kOffTab + 448)[rid >> 28];
-                reinterpret_cast<float4*>(base + static_cast<int64_t>(rid & 0x0FFFFFFFu) * 128)[lane] = o;
-            } else {
-                reinterpret_cast<float4*>(a.x_out + static_cast<int64_t>(sRowId[r]) * 128)[lane] = o;
-            }
+            const uint32_t rid = static_cast<uint32_t>(sRowId[r]);
+            reinterpret_cast<float4*>(sPeer[rid >> 28] + static_cast<int64_t>(rid & 0x0FFFFFFFu) * 128)[lane] = o;
         }
     };
     // m-tile table (first query row, part end, key ext row) of this CTA's 16-query tiles,
@@ -913,7 +905,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
     tmem_st_wait();
     // phase clock sums live in the barrier block's spare slots (thread 0 only: no registers)
     unsigned long long* ph_acc = reinterpret_cast<unsigned long long*>(smem + kOffTab + 384);  // [4] sums, [4] last stamp
-    if (kMode == kModePhase && threadIdx.x == 0)
+    if (kPhase && threadIdx.x == 0)
         for (int k = 0; k < 5; ++k) ph_acc[k] = 0ull;
     FPH(-1);
     int it = 0;
@@ -1322,7 +1314,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         __syncthreads();
         FPH(3);
     }
-    if (kMode == kModePhase && threadIdx.x == 0)
+    if (kPhase && threadIdx.x == 0)
 #pragma unroll
         for (int k = 0; k < 4; ++k) atomicAdd(a.phase + k, ph_acc[k]);
     if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 64 + 49] = static_cast<unsigned long long>(clock64());
@@ -1335,11 +1327,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
     FTRG(62);
 }
 
-template <int NT, int GC, bool kF64, int kMode>
+template <int NT, int GC, bool kF64, bool kPhase>
 int max_pairs() {
     static int n = -1;
     if (n < 0) {
-        cudaFuncSetAttribute(k_block_fused<NT, GC, kF64, kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+        cudaFuncSetAttribute(k_block_fused<NT, GC, kF64, kPhase>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(2 * kNumSMs);
         cfg.blockDim = dim3(kThreads);
@@ -1352,7 +1344,7 @@ int max_pairs() {
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         int c = 0;
-        if (cudaOccupancyMaxActiveClusters(&c, k_block_fused<NT, GC, kF64, kMode>, &cfg) != cudaSuccess || c <= 0) {
+        if (cudaOccupancyMaxActiveClusters(&c, k_block_fused<NT, GC, kF64, kPhase>, &cfg) != cudaSuccess || c <= 0) {
             cudaGetLastError();
             c = kNumSMs / 2;
         }
@@ -1361,9 +1353,9 @@ int max_pairs() {
     return n;
 }
 
-template <int NT, int GC, bool kF64, int kMode>
+template <int NT, int GC, bool kF64, bool kPhase>
 void launch_t(const FusedArgs& a, cudaStream_t s) {
-    const int np = max_pairs<NT, GC, kF64, kMode>();
+    const int np = max_pairs<NT, GC, kF64, kPhase>();
     const int pairs = a.n_units < np ? a.n_units : np;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs));
@@ -1375,21 +1367,19 @@ void launch_t(const FusedArgs& a, cudaStream_t s) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_block_fused<NT, GC, kF64, kMode>, a);
+    cudaLaunchKernelEx(&cfg, k_block_fused<NT, GC, kF64, kPhase>, a);
 }
 
 template <int NT, int GC>
 void launch_nt(const FusedArgs& a, bool f64, cudaStream_t s) {
-    // the phase-counting kernels (stage timing of the host API) only for the default G = 69;
-    // the peer-scatter kernels (the peer-memory split) for f32 inputs
-    if (a.peer && !f64) {
-        launch_t<NT, GC, false, kModePeer>(a, s);
-    } else if (GC == 69 && a.phase) {
-        if (f64) launch_t<NT, GC, true, GC == 69 ? kModePhase : kModePlain>(a, s);
-        else launch_t<NT, GC, false, GC == 69 ? kModePhase : kModePlain>(a, s);
+    // the phase-counting kernels (stage timing of the host API) only for the default G = 69
+    // (the counters cost ~2% when compiled in, so the plain kernels never carry them)
+    if (GC == 69 && a.phase) {
+        if (f64) launch_t<NT, GC, true, GC == 69>(a, s);
+        else launch_t<NT, GC, false, GC == 69>(a, s);
     } else {
-        if (f64) launch_t<NT, GC, true, kModePlain>(a, s);
-        else launch_t<NT, GC, false, kModePlain>(a, s);
+        if (f64) launch_t<NT, GC, true, false>(a, s);
+        else launch_t<NT, GC, false, false>(a, s);
     }
 }
 
@@ -1475,8 +1465,11 @@ void launch_block_fused(const float* x, const double* x64, const __half* pe16, c
     FusedArgs a{};
     a.phase = phase;
     a.x = x; a.x64 = x64; a.pe16 = pe16; a.ridx = ridx; a.sidx = sidx; a.x_out = x_out;
-    a.peer = peers;  // a device array of kMaxPeers pointers (the caller pads with x_out)
-    (void)n_peers;
+    if (peers) {  // rank-tagged rows: peer[rank] + (row & 0x0FFFFFFF) * 128
+        for (int k = 0; k < kMaxPeers; ++k) a.peer[k] = k < n_peers ? peers[k] : nullptr;
+    } else {      // plain rows (< 2^31): the same address x_out + row * 128 for any tag bits
+        for (int k = 0; k < kMaxPeers; ++k) a.peer[k] = x_out + static_cast<int64_t>(k) * (int64_t{1} << 28) * 128;
+    }
     a.rows = rows; a.G = G; a.gpu = 256 / G;
     a.split = choose_split(G);
     const int64_t n_groups = rows / G;
