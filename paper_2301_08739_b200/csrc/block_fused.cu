@@ -220,33 +220,12 @@ FWA_DEVINL void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r
                  : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
                  : "r"(addr));
 }
-FWA_DEVINL void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
-                         uint32_t b1) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-        "{%8,%9}, {%0,%1,%2,%3};"
-        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-// P = 2^x (SFU, rel err 2^-22, -inf -> +0) for two exponent arguments -> bf16x2 (the
-// PV A-operand format)
+// 2^x (SFU, rel err 2^-22, -inf -> +0)
 FWA_DEVINL float ex2f(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
-FWA_DEVINL uint32_t ex2_bf16x2(float lo, float hi) { return pack_bf16x2(ex2f(lo), ex2f(hi)); }
-// 2^x for x <= 0 on the FMA pipe (the SFU is the attention's bottleneck): round-to-
-// nearest split x = j + f (f in [-1/2, 1/2]), near-minimax cubic for 2^f (rel err 1.0e-4,
-// below the bf16 rounding of P), j added to the exponent field; x < -126 gives ~0
-FWA_DEVINL float ex2_poly(float x) {
-    x = fminf(fmaxf(x, -126.0f), 64.5f);  // beyond 2^64 the caller re-runs with the max shift
-    const float t = __fadd_rn(x, 12582912.0f);  // 1.5 * 2^23: j in the low mantissa bits
-    const float f = __fsub_rn(x, __fsub_rn(t, 12582912.0f));
-    const float p = fmaf(fmaf(fmaf(0.05500852f, f, 0.24221109f), f, 0.693283f), f, 1.0f);
-    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-}
-FWA_DEVINL uint32_t ex2_poly_bf16x2(float lo, float hi) { return pack_bf16x2(ex2_poly(lo), ex2_poly(hi)); }
 // byte offset of element (row, col) in a 128-row K-major SW128 bf16 image
 FWA_DEVINL uint32_t img_off(int row, int col) {
     return static_cast<uint32_t>((col >> 6) * 16384 + row * 128 + ((((col & 63) >> 3) ^ (row & 7)) << 4) +
@@ -256,171 +235,134 @@ FWA_DEVINL uint32_t img_off(int row, int col) {
 // Q is stored pre-scaled by (1/sqrt(16)) * log2(e), so S = Q K^T is the softmax exponent
 // in base 2.
 constexpr float kScaleLog2 = 0.25f * 1.4426950408889634f;
-#ifndef FWA_GELU_POLY
-#define FWA_GELU_POLY 8  // every FWA_GELU_POLY-th activation on the FMA pipe (gelu2_poly)
-#endif
-#ifndef FWA_POLY_MASK
-#define FWA_POLY_MASK 0  // key tiles nt with bit (nt & 3) set take the FMA-pipe exp2 (0: none, measured fastest)
-#endif
 FWA_DEVINL float rcp_approx(float x) {
     float y;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
 
-// One attention task: head `head`, query rows [m0, m0+16) of a group whose keys are the
-// extended rows [ke0, ke0 + G); rows >= qend are computed but not stored.  Q is read from
-// and O written to the R_A image (same cells).
-//   kMax = false (fast pass): P = 2^S without the row-max shift (softmax is shift
-//     invariant; the shift only guards the range) -- no max reduction, the exponent is
-//     the MMA output itself.  Returns false, storing nothing, when a row sum leaves
-//     [1/lmax, lmax] (lmax = 2^64: possible overflow / underflow); the caller then re-runs
-//     the task
-//   kMax = true: the reference's max-subtracted softmax (kernels.hpp:252-265, 533).
-template <int NT, int GC, bool kMax>
-FWA_DEVINL bool attn_task(uint32_t sRA, uint32_t sKV, uint8_t* pRA, int head, int m0, int qend, int ke0,
-                          int G_rt, float lmax) {
-    const int G = GC > 0 ? GC : G_rt;
-    const int lane = threadIdx.x & 31;
-    const int g = lane >> 2, t4 = lane & 3;
-    constexpr int kPolyMask = FWA_POLY_MASK;  // nt & 3 in the mask: 0b0010 -> nt = 1, 5 at G = 69
-    const int nt_live = (G + 7) >> 3;
-    uint32_t a0, a1, a2, a3;
-    {
-        // rows >= qend belong to another task's m-tile (same head columns, which that task
-        // overwrites with its O): read this task's first row instead -- discarded rows, no
-        // cross-warp hazard
-        int qrow = m0 + (lane & 7) + ((lane >> 3) & 1) * 8;
-        if (qrow >= qend) qrow = m0;
-        const int col = head * 16 + (lane >> 4) * 8;
-        ldsm_x4(sRA + img_off(qrow, col), a0, a1, a2, a3);
+// Attention operands are fp16 (Q pre-scaled, K, V; written by the QKV epilogue): the
+// scores of the fast pass are accumulated in fp16, so they ARE the packed f16x2 operand of
+// ex2.approx.f16x2 and, exponentiated, the A fragments of the PV MMA -- no fp32 score
+// registers, no conversions between the two MMAs.
+FWA_DEVINL uint32_t pack_f16x2(float lo, float hi) {
+    __half2 v = __floats2half2_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+// c = A B (fp16 accumulate, C = 0)
+FWA_DEVINL void mma_f16acc(uint32_t (&c)[2], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                           uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f16.f16.f16.f16 {%0,%1}, {%2,%3,%4,%5}, {%6,%7}, {%8,%8};"
+        : "=r"(c[0]), "=r"(c[1])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "r"(0u));
+}
+// c += A B (fp16 operands, fp32 accumulate)
+FWA_DEVINL void mma_f16f32(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                           uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// 2^x for two fp16 exponents (SFU; -inf -> +0)
+FWA_DEVINL uint32_t ex2_f16x2(uint32_t x) {
+    uint32_t y;
+    asm("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
+#ifndef FWA_EXP_EXPERIMENT
+#define FWA_EXP_EXPERIMENT 0
+#endif
+constexpr uint32_t kOnesF16 = 0x3C003C00u;  // f16x2 (1, 1): the row-sum B fragment
+
+// 2^x for two fp16 exponents on the FMA / ALU pipes (no SFU): x clamped to [-15, 16];
+// j = round(x) by the 1.5 * 2^10 magic add (fp16 spacing 1 on [1024, 2048)); f = x - j in
+// [-1/2, 1/2]; 2^f by a degree-3 fit (rel err 7.5e-5; 6.9e-4 evaluated in fp16); 2^j
+// built in each half's exponent field from the low bits of 1536 + j (j + 15 in [0, 31]:
+// j = -15 gives +0 -- masked keys (-inf) land there; j = 16 gives +inf, so an exponent
+// past the fast pass's range still fails its row-sum check).
+FWA_DEVINL uint32_t ex2_poly_f16x2(uint32_t xb) {
+    __half2 x = *reinterpret_cast<const __half2*>(&xb);
+    x = __hmin2(__hmax2(x, __float2half2_rn(-15.0f)), __float2half2_rn(16.0f));
+    const __half2 magic = __float2half2_rn(1536.0f);
+    const __half2 t = __hadd2(x, magic);
+    const __half2 f = __hsub2(x, __hsub2(t, magic));
+    __half2 p = __hfma2(__float2half2_rn(0.05517098f), f, __float2half2_rn(0.24260972f));
+    p = __hfma2(p, f, __float2half2_rn(0.69326097f));
+    p = __hfma2(p, f, __float2half2_rn(0.99992816f));
+    const uint32_t tb = *reinterpret_cast<const uint32_t*>(&t);
+    const uint32_t sc = ((tb + 0x000F000Fu) << 10) & 0xFC00FC00u;
+    const __half2 r = __hmul2(p, *reinterpret_cast<const __half2*>(&sc));
+    return *reinterpret_cast<const uint32_t*>(&r);
+}
+#ifndef FWA_EXP_POLY
+#define FWA_EXP_POLY 2  // exponentials on the FMA pipe: 0 none, 1 odd key tiles, 2 key tiles 3 mod 4 (2 of 9 at G = 69)
+#endif
+
+// keys >= G: V := 0 (their K/V rows may hold any bits -- P = 0 times NaN is NaN)
+FWA_DEVINL void mask_v_tail(uint32_t (&vb)[4], int kt, int G, int t4) {
+    if (kt * 16 + 16 > G) {
+        const int k0 = kt * 16 + 2 * t4, k1 = k0 + 8;
+        const uint32_t m0 = (k0 < G ? 0xFFFFu : 0u) | (k0 + 1 < G ? 0xFFFF0000u : 0u);
+        const uint32_t m1 = (k1 < G ? 0xFFFFu : 0u) | (k1 + 1 < G ? 0xFFFF0000u : 0u);
+        vb[0] &= m0;
+        vb[2] &= m0;
+        vb[1] &= m1;
+        vb[3] &= m1;
     }
-    uint32_t kb[NT][2];
-#pragma unroll
-    for (int np = 0; np < NT; np += 2) {
-        const int krow = ke0 + (np + (lane >> 4)) * 8 + (lane & 7);
-        ldsm_x4(sKV + krow * kKVPitch + head * 32 + ((lane >> 3) & 1) * 16, kb[np][0], kb[np][1], kb[np + 1][0],
-                kb[np + 1][1]);
-    }
-    uint32_t vb[NT / 2][4];
-#pragma unroll
-    for (int kt = 0; kt < NT / 2; ++kt) {
-        const int vrow = ke0 + kt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
-        ldsm_x4_t(sKV + vrow * kKVPitch + 256 + head * 32 + (lane >> 4) * 16, vb[kt][0], vb[kt][1], vb[kt][2],
-                  vb[kt][3]);
-    }
-    // keys >= G: V := 0 (their rows may hold any bits -- P = 0 times NaN is NaN)
-#pragma unroll
-    for (int kt = 0; kt < NT / 2; ++kt) {
-        if (kt * 16 + 16 > G) {
-            const int k0 = kt * 16 + 2 * t4, k1 = k0 + 8;
-            const uint32_t m0 = (k0 < G ? 0xFFFFu : 0u) | (k0 + 1 < G ? 0xFFFF0000u : 0u);
-            const uint32_t m1 = (k1 < G ? 0xFFFFu : 0u) | (k1 + 1 < G ? 0xFFFF0000u : 0u);
-            vb[kt][0] &= m0;
-            vb[kt][2] &= m0;
-            vb[kt][1] &= m1;
-            vb[kt][3] &= m1;
-        }
-    }
-    float s[NT][4];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-        s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
-        if (nt < nt_live) mma16816(s[nt], a0, a1, a2, a3, kb[nt][0], kb[nt][1]);
-        if (nt < nt_live && nt * 8 + 8 > G) {
-            const int col = nt * 8 + 2 * t4;
-            if (col >= G) { s[nt][0] = -INFINITY; s[nt][2] = -INFINITY; }
-            if (col + 1 >= G) { s[nt][1] = -INFINITY; s[nt][3] = -INFINITY; }
-        }
-    }
-    float mb0 = 0.f, mb1 = 0.f;
-    if (kMax) {
-        float m0v = -INFINITY, m1v = -INFINITY;
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-            if (nt >= nt_live) continue;
-            m0v = fmaxf(m0v, fmaxf(s[nt][0], s[nt][1]));
-            m1v = fmaxf(m1v, fmaxf(s[nt][2], s[nt][3]));
-        }
-        m0v = fmaxf(m0v, __shfl_xor_sync(0xffffffffu, m0v, 1));
-        m0v = fmaxf(m0v, __shfl_xor_sync(0xffffffffu, m0v, 2));
-        m1v = fmaxf(m1v, __shfl_xor_sync(0xffffffffu, m1v, 1));
-        m1v = fmaxf(m1v, __shfl_xor_sync(0xffffffffu, m1v, 2));
-        mb0 = m0v;
-        mb1 = m1v;
-    }
-    uint32_t p[NT][2];  // bf16x2: [0] row g, [1] row g + 8
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-        if (nt < nt_live) {
-            const float e0 = kMax ? s[nt][0] - mb0 : s[nt][0], e1 = kMax ? s[nt][1] - mb0 : s[nt][1];
-            const float e2 = kMax ? s[nt][2] - mb1 : s[nt][2], e3 = kMax ? s[nt][3] - mb1 : s[nt][3];
-            if (((kPolyMask >> (nt & 3)) & 1) && nt * 8 + 8 <= G) {  // some exponentials on the FMA pipe
-                p[nt][0] = ex2_poly_bf16x2(e0, e1);
-                p[nt][1] = ex2_poly_bf16x2(e2, e3);
-            } else {
-                p[nt][0] = ex2_bf16x2(e0, e1);
-                p[nt][1] = ex2_bf16x2(e2, e3);
-            }
-        } else {
-            p[nt][0] = p[nt][1] = 0u;
-        }
-    }
-    constexpr uint32_t kOnes = 0x3F803F80u;  // bf16x2 (1, 1)
-    float o[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-    float l[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-    for (int kt = 0; kt < NT / 2; ++kt) {
-        if (2 * kt >= nt_live) continue;
-        mma16816(o[0], p[2 * kt][0], p[2 * kt][1], p[2 * kt + 1][0], p[2 * kt + 1][1], vb[kt][0], vb[kt][1]);
-        mma16816(o[1], p[2 * kt][0], p[2 * kt][1], p[2 * kt + 1][0], p[2 * kt + 1][1], vb[kt][2], vb[kt][3]);
-        mma16816(l, p[2 * kt][0], p[2 * kt][1], p[2 * kt + 1][0], p[2 * kt + 1][1], kOnes, kOnes);
-    }
-    const int r0 = m0 + g, r1 = r0 + 8;
-    if (!kMax) {  // only the kept rows (< qend) decide whether the task is re-run shifted
-        const float lmin = rcp_approx(lmax);
-        const bool ok = (r0 >= qend || (l[0] >= lmin && l[0] <= lmax)) && (r1 >= qend || (l[2] >= lmin && l[2] <= lmax));
-        if (__any_sync(0xffffffffu, !ok)) return false;
-    }
-    const float i0 = rcp_approx(l[0]), i1 = rcp_approx(l[2]);
-    __syncwarp();  // every lane's Q fragment reads (ldmatrix) precede any lane's O writes
+}
+
+// The attention output of rows r0 = m0 + g and r1 = r0 + 8 (those below the part end qend)
+// into the R_A image as bf16 (the out-proj A operand), in place of this task's Q cells.
+FWA_DEVINL void store_o(uint8_t* pRA, int head, int r0, int qend, const float (&o)[2][4], float i0, float i1,
+                        int t4) {
+    const int r1 = r0 + 8;
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
         const int col = head * 16 + nt * 8 + 2 * t4;
         if (r0 < qend) *reinterpret_cast<uint32_t*>(pRA + img_off(r0, col)) = pack_bf16x2(o[nt][0] * i0, o[nt][1] * i0);
         if (r1 < qend) *reinterpret_cast<uint32_t*>(pRA + img_off(r1, col)) = pack_bf16x2(o[nt][2] * i1, o[nt][3] * i1);
     }
-    return true;
 }
 
-// Two attention tasks interleaved in one warp, streamed per 16-key slab: K tile -> S ->
-// P = 2^S -> V tile -> PV accumulate, so only one slab's S/P/K/V is live per task (~40
-// registers) and the two independent chains hide each other's MMA / SFU latency.  The
-// fast pass of attn_task (no row-max shift); bit b of the result set = task b must be
-// re-run with the shift (its row sums left [1/lmax, lmax]); nothing stored for it.
-template <int NT, int GC>
-FWA_DEVINL uint32_t attn_task2(uint32_t sRA, uint32_t sKV, uint8_t* pRA, const int (&head)[2], const int4 (&e)[2],
-                               int G_rt, float lmax) {
+// The Q fragment of a task (m-tile rows [m0, m0 + 16), head columns).  Rows >= qend belong
+// to another task's m-tile (the same head columns, which that task overwrites with its O):
+// such lanes read this task's first row instead -- discarded rows, no cross-warp hazard.
+FWA_DEVINL void load_q(uint32_t sRA, int head, int m0, int qend, uint32_t (&a)[4]) {
+    const int lane = threadIdx.x & 31;
+    int qrow = m0 + (lane & 7) + ((lane >> 3) & 1) * 8;
+    if (qrow >= qend) qrow = m0;
+    ldsm_x4(sRA + img_off(qrow, head * 16 + (lane >> 4) * 8), a[0], a[1], a[2], a[3]);
+}
+
+// NK attention tasks (head[k], query rows [e[k].x, e[k].x + 16) of a group part ending at
+// e[k].y, keys = the extended K/V rows [e[k].z, e[k].z + G)) interleaved in one warp and
+// streamed per 16-key slab: K tile -> S (fp16 accumulate) -> P = 2^S (ex2.f16x2) -> V tile
+// -> PV and row sums (fp32 accumulate).  No row-max pass: softmax is shift invariant and the
+// shift only guards the range, so a task whose kept-row sums leave [lo, hi] (an exponent
+// beyond the fp16 range or too coarse in it, or P values down in the fp16 subnormals) is
+// re-run by attn_shift: bit k of the result; nothing is stored for it.
+template <int NT, int GC, int NK>
+FWA_DEVINL uint32_t attn_fast(uint32_t sRA, uint32_t sKV, uint8_t* pRA, const int (&head)[NK], const int4 (&e)[NK],
+                              int G_rt, float lo, float hi) {
     const int G = GC > 0 ? GC : G_rt;
     const int lane = threadIdx.x & 31;
     const int g = lane >> 2, t4 = lane & 3;
-    constexpr int kPolyMask = FWA_POLY_MASK;
     const int nt_live = (G + 7) >> 3;
-    constexpr uint32_t kOnes = 0x3F803F80u;  // bf16x2 (1, 1)
-    uint32_t a[2][4];
-    float o[2][2][4] = {}, l[2][4] = {};
+    // the last live key tile: its columns >= G -> -inf (fp16 0xFC00)
+    const int cm = (nt_live - 1) * 8 + 2 * t4;
+    const uint32_t keep = (cm < G ? 0x0000FFFFu : 0u) | (cm + 1 < G ? 0xFFFF0000u : 0u);
+    uint32_t a[NK][4];
+    float o[NK][2][4] = {}, l[NK][4] = {};
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        int qrow = e[k].x + (lane & 7) + ((lane >> 3) & 1) * 8;
-        if (qrow >= e[k].y) qrow = e[k].x;  // rows past the part end: this task's own row (see attn_task)
-        const int col = head[k] * 16 + (lane >> 4) * 8;
-        ldsm_x4(sRA + img_off(qrow, col), a[k][0], a[k][1], a[k][2], a[k][3]);
-    }
+    for (int k = 0; k < NK; ++k) load_q(sRA, head[k], e[k].x, e[k].y, a[k]);
 #pragma unroll
     for (int kt = 0; kt < NT / 2; ++kt) {
         if (2 * kt >= nt_live) continue;
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < NK; ++k) {
             const int ke0 = e[k].z;
             uint32_t kb[2][2], vb[4];
             {
@@ -430,15 +372,7 @@ FWA_DEVINL uint32_t attn_task2(uint32_t sRA, uint32_t sKV, uint8_t* pRA, const i
                 const int vrow = ke0 + kt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
                 ldsm_x4_t(sKV + vrow * kKVPitch + 256 + head[k] * 32 + (lane >> 4) * 16, vb[0], vb[1], vb[2], vb[3]);
             }
-            if (kt * 16 + 16 > G) {  // keys >= G: V := 0 (their rows may hold any bits)
-                const int k0 = kt * 16 + 2 * t4, k1 = k0 + 8;
-                const uint32_t m0 = (k0 < G ? 0xFFFFu : 0u) | (k0 + 1 < G ? 0xFFFF0000u : 0u);
-                const uint32_t m1 = (k1 < G ? 0xFFFFu : 0u) | (k1 + 1 < G ? 0xFFFF0000u : 0u);
-                vb[0] &= m0;
-                vb[2] &= m0;
-                vb[1] &= m1;
-                vb[3] &= m1;
-            }
+            mask_v_tail(vb, kt, G, t4);
             uint32_t p[2][2];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -447,50 +381,111 @@ FWA_DEVINL uint32_t attn_task2(uint32_t sRA, uint32_t sKV, uint8_t* pRA, const i
                     p[h][0] = p[h][1] = 0u;
                     continue;
                 }
-                float sv[4] = {0.f, 0.f, 0.f, 0.f};
-                mma16816(sv, a[k][0], a[k][1], a[k][2], a[k][3], kb[h][0], kb[h][1]);
+                uint32_t sv[2];
+                mma_f16acc(sv, a[k][0], a[k][1], a[k][2], a[k][3], kb[h][0], kb[h][1]);
                 if (nt * 8 + 8 > G) {
-                    const int col = nt * 8 + 2 * t4;
-                    if (col >= G) { sv[0] = -INFINITY; sv[2] = -INFINITY; }
-                    if (col + 1 >= G) { sv[1] = -INFINITY; sv[3] = -INFINITY; }
+                    sv[0] = (sv[0] & keep) | (0xFC00FC00u & ~keep);
+                    sv[1] = (sv[1] & keep) | (0xFC00FC00u & ~keep);
                 }
-                if (((kPolyMask >> (nt & 3)) & 1) && nt * 8 + 8 <= G) {
-                    p[h][0] = ex2_poly_bf16x2(sv[0], sv[1]);
-                    p[h][1] = ex2_poly_bf16x2(sv[2], sv[3]);
-                } else {
-                    p[h][0] = ex2_bf16x2(sv[0], sv[1]);
-                    p[h][1] = ex2_bf16x2(sv[2], sv[3]);
+#if FWA_EXP_EXPERIMENT == 1  // timing experiment only: no SFU (wrong numerics)
+                {
+                    __half2 a0 = *reinterpret_cast<__half2*>(&sv[0]), a1 = *reinterpret_cast<__half2*>(&sv[1]);
+                    const __half2 one = __float2half2_rn(1.0f);
+                    a0 = __hfma2(a0, a0, one);
+                    a1 = __hfma2(a1, a1, one);
+                    p[h][0] = *reinterpret_cast<uint32_t*>(&a0);
+                    p[h][1] = *reinterpret_cast<uint32_t*>(&a1);
                 }
+#else
+                // the choice depends on the KEY tile only (key tiles start at the group start), so
+                // a row's result does not depend on where its group sits in a unit
+                const bool poly = FWA_EXP_POLY == 1 ? h == 1 : FWA_EXP_POLY == 2 ? (nt & 3) == 3 : false;
+                p[h][0] = poly ? ex2_poly_f16x2(sv[0]) : ex2_f16x2(sv[0]);
+                p[h][1] = poly ? ex2_poly_f16x2(sv[1]) : ex2_f16x2(sv[1]);
+#endif
             }
-            mma16816(o[k][0], p[0][0], p[0][1], p[1][0], p[1][1], vb[0], vb[1]);
-            mma16816(o[k][1], p[0][0], p[0][1], p[1][0], p[1][1], vb[2], vb[3]);
-            mma16816(l[k], p[0][0], p[0][1], p[1][0], p[1][1], kOnes, kOnes);
+            mma_f16f32(o[k][0], p[0][0], p[0][1], p[1][0], p[1][1], vb[0], vb[1]);
+            mma_f16f32(o[k][1], p[0][0], p[0][1], p[1][0], p[1][1], vb[2], vb[3]);
+            mma_f16f32(l[k], p[0][0], p[0][1], p[1][0], p[1][1], kOnesF16, kOnesF16);
         }
     }
-    const float lmin = rcp_approx(lmax);
     uint32_t redo = 0;
     __syncwarp();  // every lane's Q fragment reads (ldmatrix) precede any lane's O writes
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < NK; ++k) {
         const int r0 = e[k].x + g, r1 = r0 + 8;
         // only the kept rows (< part end) decide whether the task is re-run shifted
-        const bool ok = (r0 >= e[k].y || (l[k][0] >= lmin && l[k][0] <= lmax)) &&
-                        (r1 >= e[k].y || (l[k][2] >= lmin && l[k][2] <= lmax));
+        const bool ok = (r0 >= e[k].y || (l[k][0] >= lo && l[k][0] <= hi)) &&
+                        (r1 >= e[k].y || (l[k][2] >= lo && l[k][2] <= hi));
         if (__any_sync(0xffffffffu, !ok)) {
             redo |= 1u << k;
             continue;
         }
-        const float i0 = rcp_approx(l[k][0]), i1 = rcp_approx(l[k][2]);
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-            const int col = head[k] * 16 + nt * 8 + 2 * t4;
-            if (r0 < e[k].y)
-                *reinterpret_cast<uint32_t*>(pRA + img_off(r0, col)) = pack_bf16x2(o[k][nt][0] * i0, o[k][nt][1] * i0);
-            if (r1 < e[k].y)
-                *reinterpret_cast<uint32_t*>(pRA + img_off(r1, col)) = pack_bf16x2(o[k][nt][2] * i1, o[k][nt][3] * i1);
-        }
+        store_o(pRA, head[k], r0, e[k].y, o[k], rcp_approx(l[k][0]), rcp_approx(l[k][2]), t4);
     }
     return redo;
+}
+
+// The reference's max-subtracted softmax (kernels.hpp:252-265, 533) for one task: scores
+// in fp32 (fp16 operands, fp32 accumulate), P = 2^(S - max) in (0, 1] rounded to fp16.
+template <int NT, int GC>
+FWA_DEVINL void attn_shift(uint32_t sRA, uint32_t sKV, uint8_t* pRA, int head, int m0, int qend, int ke0, int G_rt) {
+    const int G = GC > 0 ? GC : G_rt;
+    const int lane = threadIdx.x & 31;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int nt_live = (G + 7) >> 3;
+    uint32_t a[4];
+    load_q(sRA, head, m0, qend, a);
+    float s[NT][4];
+#pragma unroll
+    for (int np = 0; np < NT; np += 2) {
+        uint32_t kb[2][2];
+        const int krow = ke0 + (np + (lane >> 4)) * 8 + (lane & 7);
+        ldsm_x4(sKV + krow * kKVPitch + head * 32 + ((lane >> 3) & 1) * 16, kb[0][0], kb[0][1], kb[1][0], kb[1][1]);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int nt = np + h;
+            s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = -INFINITY;
+            if (nt >= nt_live) continue;
+            s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+            mma_f16f32(s[nt], a[0], a[1], a[2], a[3], kb[h][0], kb[h][1]);
+            const int col = nt * 8 + 2 * t4;
+            if (col >= G) { s[nt][0] = -INFINITY; s[nt][2] = -INFINITY; }
+            if (col + 1 >= G) { s[nt][1] = -INFINITY; s[nt][3] = -INFINITY; }
+        }
+    }
+    float m0v = -INFINITY, m1v = -INFINITY;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+        m0v = fmaxf(m0v, fmaxf(s[nt][0], s[nt][1]));
+        m1v = fmaxf(m1v, fmaxf(s[nt][2], s[nt][3]));
+    }
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1) {
+        m0v = fmaxf(m0v, __shfl_xor_sync(0xffffffffu, m0v, o));
+        m1v = fmaxf(m1v, __shfl_xor_sync(0xffffffffu, m1v, o));
+    }
+    float o[2][4] = {}, l[4] = {};
+#pragma unroll
+    for (int kt = 0; kt < NT / 2; ++kt) {
+        if (2 * kt >= nt_live) continue;
+        uint32_t vb[4];
+        const int vrow = ke0 + kt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+        ldsm_x4_t(sKV + vrow * kKVPitch + 256 + head * 32 + (lane >> 4) * 16, vb[0], vb[1], vb[2], vb[3]);
+        mask_v_tail(vb, kt, G, t4);
+        uint32_t p[2][2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int nt = 2 * kt + h;
+            p[h][0] = pack_f16x2(ex2f(s[nt][0] - m0v), ex2f(s[nt][1] - m0v));
+            p[h][1] = pack_f16x2(ex2f(s[nt][2] - m1v), ex2f(s[nt][3] - m1v));
+        }
+        mma_f16f32(o[0], p[0][0], p[0][1], p[1][0], p[1][1], vb[0], vb[1]);
+        mma_f16f32(o[1], p[0][0], p[0][1], p[1][0], p[1][1], vb[2], vb[3]);
+        mma_f16f32(l, p[0][0], p[0][1], p[1][0], p[1][1], kOnesF16, kOnesF16);
+    }
+    __syncwarp();  // every lane's Q fragment reads precede any lane's O writes
+    store_o(pRA, head, m0 + g, qend, o, rcp_approx(l[0]), rcp_approx(l[2]), t4);
 }
 
 // ---------------------------------------------------------------- row I/O
@@ -643,30 +638,22 @@ FWA_DEVINL float tanh_approx(float x) {
     return y;
 }
 // 2 GELU(x) = x (1 + tanh(x (a + b x^2))), (a, b) the minimax fit to the exact-erf GELU
-// over the reals: |GELU error| <= 2.7e-4, below tanh.approx's own error (2^-11 relative)
-// and an order below the bf16 rounding of the result (the degree-2 fit, 2.6e-5, left the
-// golden bf16 error unchanged and cost 0.6% of the frame).  a + b x^2 > 0 everywhere, so
-// the argument is monotone and tanh saturates.  The factor 1/2 is folded into W2
-// (build_pair_images).  6 instructions per element with the bias add: the SM
-// sub-partition's SFU (one tanh per element) is the GELU bound.
-FWA_DEVINL float gelu2_fast(float x) {
-    const float t = tanh_approx(x * fmaf(3.470089e-02f, x * x, 8.0015708e-01f));
-    return fmaf(x, t, x);
-}
-
-// the same on the FMA pipe only (no SFU): 2 GELU(x) = x + E(x), E(x) = x erf(x/sqrt 2)
-// = x^2 Q(x^2) on |x| <= 4 (Q degree 6, minimax), |x| beyond: |GELU error| <= 1.9e-4.
-// 12 instructions per element with the bias add; a share of the elements takes this form
-// so the SFU and the FMA pipe finish together.
-FWA_DEVINL float gelu2_poly(float x) {
-    const float x2 = x * x;
-    float p = fmaf(4.556269317e-08f, x2, -3.197195383e-06f);
-    p = fmaf(p, x2, 9.591085836e-05f);
-    p = fmaf(p, x2, -1.628029277e-03f);
-    p = fmaf(p, x2, 1.754476875e-02f);
-    p = fmaf(p, x2, -1.291462034e-01f);
-    p = fmaf(p, x2, 7.957667112e-01f);
-    return x + (x2 > 16.0f ? fabsf(x) : p * x2);
+// over the reals: |GELU error| <= 2.7e-4, below tanh.approx's own error.  a + b x^2 > 0
+// everywhere, so the argument is monotone and tanh saturates (an fp16 overflow of x^2 or
+// of the argument gives tanh = +-1, the correct limit).  Evaluated on PAIRS in fp16x2
+// (the FFN2 A operand is fp16, W2 too): one pack, three half2 ops, one tanh.approx.f16x2
+// and one half2 FMA per two activations (rounding ~2^-11 relative, below the bf16
+// rounding of the earlier fp32 form's output).  The factor 1/2 is folded into W2
+// (build_pair_images).  The SM sub-partition's SFU is the bound (16 tanh lanes per clock
+// per SM, the same per element for f32 and f16x2).
+FWA_DEVINL uint32_t gelu2_f16x2(float x0, float x1) {
+    const __half2 h = __floats2half2_rn(x0, x1);
+    const __half2 t = __hfma2(__hmul2(h, h), __float2half2_rn(3.470089e-02f), __float2half2_rn(8.0015708e-01f));
+    const __half2 u = __hmul2(h, t);
+    uint32_t th;
+    asm("tanh.approx.f16x2 %0, %1;" : "=r"(th) : "r"(*reinterpret_cast<const uint32_t*>(&u)));
+    const __half2 r = __hfma2(h, *reinterpret_cast<const __half2*>(&th), h);
+    return *reinterpret_cast<const uint32_t*>(&r);
 }
 
 struct FusedArgs {
@@ -792,6 +779,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
     const uint32_t ready_remote = mapa(smem_u32(bReady), 0);
     const uint32_t halo_remote = mapa(smem_u32(bHalo), rank ^ 1);
     constexpr uint32_t id256 = idesc_bf16_f32(256, 128);
+    constexpr uint32_t id256h = idesc_f16_f32(256, 128);  // FFN2: fp16 GELU activations x fp16 W2
     bool bad = false;
     uint32_t hs = 0;  // handshake count (parity of bReady, leader)
 
@@ -1091,8 +1079,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
                 for (int hf = 0; hf < 2; ++hf) {
                     uint32_t o[4];
 #pragma unroll
-                    for (int e = 0; e < 4; ++e)  // the accumulators started at the bias
-                        o[e] = pack_bf16x2(__uint_as_float(kv[hh][8 * hf + 2 * e]), __uint_as_float(kv[hh][8 * hf + 2 * e + 1]));
+                    for (int e = 0; e < 4; ++e)  // the accumulators started at the bias; fp16 operands
+                        o[e] = pack_f16x2(__uint_as_float(kv[hh][8 * hf + 2 * e]), __uint_as_float(kv[hh][8 * hf + 2 * e + 1]));
                     X[hf] = make_uint4(o[0], o[1], o[2], o[3]);
                 }
                 const int off = 256 * part + h * 32;
@@ -1123,7 +1111,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
                     uint32_t o[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e)
-                        o[e] = pack_bf16x2(__uint_as_float(qv[hh][8 * hf + 2 * e]), __uint_as_float(qv[hh][8 * hf + 2 * e + 1]));
+                        o[e] = pack_f16x2(__uint_as_float(qv[hh][8 * hf + 2 * e]), __uint_as_float(qv[hh][8 * hf + 2 * e + 1]));
                     *reinterpret_cast<uint4*>(pRA + sw128_offset(row, 16 * h + 8 * hf, 128)) = make_uint4(o[0], o[1], o[2], o[3]);
                 }
             }
@@ -1131,45 +1119,52 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         __syncthreads();        // local K/V, Q and the m-tile table visible
         FTR(tb + 4);
         {
-            const int ntasks = sTab[16].x * 8;  // (m-tile, head)
+            const int ntasks = FWA_EXP_EXPERIMENT == 2 ? 0 : sTab[16].x * 8;  // (m-tile, head)
             bool halo = false;
-#ifndef FWA_ATTN_PAIRS
-#define FWA_ATTN_PAIRS 1
+            // the fast pass's accepted row-sum range: exponents well inside the fp16 range
+            // (|S| < 12: spacing <= 2^-7) and P above the fp16 subnormals; FWA_B200_ATTN_LMAX
+            // narrows it (tests force the shifted path)
+            const float hi = fminf(a.lmax, 4096.0f), lo = fmaxf(1.0f / a.lmax, 0.015625f);
+#ifndef FWA_ATTN_NK
+#define FWA_ATTN_NK 2
 #endif
-#if FWA_ATTN_PAIRS
-            // tasks t and t + 16 of this warp together (the same head, two m-tiles)
+            // tasks t, t + 16, ... of this warp together (the same head, FWA_ATTN_NK m-tiles)
+            constexpr int NKW = FWA_ATTN_NK;
 #pragma unroll 1
-            for (int t = warp; t < ntasks; t += 32) {
-                const bool two = t + 16 < ntasks;
-                const int4 ee[2] = {sTab[t >> 3], two ? sTab[(t + 16) >> 3] : sTab[t >> 3]};
-                if ((ee[0].w || (two && ee[1].w)) && !halo) {  // the peer's halo rows have landed
+            for (int t = warp; t < ntasks; t += 16 * NKW) {
+                int4 ee[NKW];
+                int hd[NKW];
+                bool need_halo = false;
+                int nk = 0;
+#pragma unroll
+                for (int k = 0; k < NKW; ++k) {
+                    const int tk = t + 16 * k < ntasks ? t + 16 * k : t;
+                    nk += t + 16 * k < ntasks;
+                    ee[k] = sTab[tk >> 3];
+                    hd[k] = tk & 7;
+                    need_halo |= ee[k].w != 0;
+                }
+                if (need_halo && !halo) {  // the peer's halo rows have landed
+                    FTR(tb + 5);
                     mbar_wait(bHalo, ph);
+                    FTR(tb + 6);
                     halo = true;
                 }
-                if (two) {
-                    const int hd[2] = {t & 7, (t + 16) & 7};
-                    const uint32_t redo = attn_task2<NT, GC>(sRA, sKV, pRA, hd, ee, G, a.lmax);
-                    for (int k = 0; k < 2; ++k)
-                        if (redo & (1u << k)) attn_task<NT, GC, true>(sRA, sKV, pRA, hd[k], ee[k].x, ee[k].y, ee[k].z, G, a.lmax);
-                } else if (!attn_task<NT, GC, false>(sRA, sKV, pRA, t & 7, ee[0].x, ee[0].y, ee[0].z, G, a.lmax)) {
-                    attn_task<NT, GC, true>(sRA, sKV, pRA, t & 7, ee[0].x, ee[0].y, ee[0].z, G, a.lmax);
+                uint32_t redo;
+                if (nk == NKW) {
+                    redo = attn_fast<NT, GC, NKW>(sRA, sKV, pRA, hd, ee, G, lo, hi);
+                } else {
+                    redo = 0;
+                    for (int k = 0; k < nk; ++k) {
+                        const int hd1[1] = {hd[k]};
+                        const int4 ee1[1] = {ee[k]};
+                        redo |= attn_fast<NT, GC, 1>(sRA, sKV, pRA, hd1, ee1, G, lo, hi) << k;
+                    }
                 }
+                for (int k = 0; k < nk; ++k)
+                    if (redo & (1u << k)) attn_shift<NT, GC>(sRA, sKV, pRA, hd[k], ee[k].x, ee[k].y, ee[k].z, G);
             }
-#else
-#pragma unroll 1
-            for (int t = warp; t < ntasks; t += 16) {
-                const int4 e = sTab[t >> 3];
-                if (e.w && !halo) {  // the peer's halo rows have landed (st.async bytes)
-                    mbar_wait(bHalo, ph);
-                    halo = true;
-                }
-                if (!attn_task<NT, GC, false>(sRA, sKV, pRA, t & 7, e.x, e.y, e.z, G, a.lmax))
-                    attn_task<NT, GC, true>(sRA, sKV, pRA, t & 7, e.x, e.y, e.z, G, a.lmax);
-            }
-#endif
         }
-        FTR(tb + 5);
-        FTR(tb + 6);
         FTR(tb + 7);
 
         // ---- 3. out-proj: P = O Wout^T (TMEM [0,128)); residual reload overlaps the MMA.
@@ -1262,13 +1257,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
             for (int j = 0; j < 4; ++j) {
                 uint32_t o[4];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {  // the accumulators started at b1'
-                    const int k = 8 * j + 2 * e;
-                    const float g1 = __uint_as_float(v[k + 1]);
-                    o[e] = pack_bf16x2(gelu2_fast(__uint_as_float(v[k])),
-                                       (FWA_GELU_POLY && (k + 1) % FWA_GELU_POLY == FWA_GELU_POLY - 1)
-                                           ? gelu2_poly(g1) : gelu2_fast(g1));
-                }
+                for (int e = 0; e < 4; ++e)  // the accumulators started at b1'
+                    o[e] = gelu2_f16x2(__uint_as_float(v[8 * j + 2 * e]), __uint_as_float(v[8 * j + 2 * e + 1]));
                 *reinterpret_cast<uint4*>(act + sw128_offset(row, c0 + 8 * j, 128)) = make_uint4(o[0], o[1], o[2], o[3]);
             }
             if (hh == 0 && threadIdx.x == 0) mbar_wait(bW2, ph);  // FFN2 reads W2 in both CTAs
@@ -1279,7 +1269,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
 #pragma unroll
                 for (int ks = 0; ks < 8; ++ks)  // onto x1 = (x + b_out) + P in [384, 512)
                     mma2_bf16(tmem + 384, sdesc_sw128(a0 + (ks >> 2) * 16384 + (ks & 3) * 32),
-                              sdesc_sw128(sWa + kOffW2 + (2 * hh + (ks >> 2)) * 8192 + (ks & 3) * 32), id256,
+                              sdesc_sw128(sWa + kOffW2 + (2 * hh + (ks >> 2)) * 8192 + (ks & 3) * 32), id256h,
                               1u);
                 if (hh) mma_commit_pair(bO);
             }

@@ -773,7 +773,7 @@ void build_schedule_body(fwa_b200_ctx* c, const double* d_coords, const fwa_conf
         if (nd > 0)
             launch_drop_tables(S.sorted, nd, d_off, d_rows, d_drop_off, nf, S.sorted_inv, ntot, n_specs,
                                S.dropped_ids, drop_sorted, drop_pos, st, &c->launches);
-        launch_compact_all(S.sorted, ntot, n_specs, drop_sorted, drop_pos, nd, S.K, s_last, S.idx,
+        launch_compact_all(S.sorted, S.sorted_inv, ntot, n_specs, d_off, d_rows, nf, drop_sorted, drop_pos, nd, S.K, s_last, S.idx,
                            S.kept_rank, S.kept_ids, S.out_pos, st, &c->launches);
         check_launch();
         return;

@@ -89,7 +89,8 @@ void launch_drop_tables(const int32_t* sorted0, int n, const int64_t* frame_off,
                         const int64_t* drop_off, int n_frames, const int32_t* inv, int64_t ntot, int n_specs,
                         int32_t* dropped_ids, int32_t* drop_sorted, int32_t* drop_pos, cudaStream_t s,
                         int64_t* launches);
-void launch_compact_all(const int32_t* sorted, int64_t ntot, int n_specs, const int32_t* drop_sorted,
+void launch_compact_all(const int32_t* sorted, const int32_t* inv0, int64_t ntot, int n_specs,
+                        const int64_t* frame_off, const int64_t* rows, int n_frames, const int32_t* drop_sorted,
                         const int32_t* drop_pos, int n_drop, int64_t K, int s_last, int32_t* idx,
                         uint32_t* kept_rank, int32_t* kept_ids, int32_t* out_pos, cudaStream_t s,
                         int64_t* launches);

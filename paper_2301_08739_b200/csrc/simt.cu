@@ -45,31 +45,33 @@ __global__ void k_positional_embedding(const double* __restrict__ coords, int64_
 // sin / cos of pi r.  |err| < 1e-6, far below the fp16 rounding (2^-12) of the stored value.
 __global__ void k_pe_fp16(const double* __restrict__ coords, int64_t n, int nf, const float2* __restrict__ F,
                           __half* __restrict__ pe16) {
+    // one thread per (row, axis, 4 frequencies): consecutive threads write consecutive 16 B
+    // of the fp16 PE rows (every store instruction fills whole 128 B lines)
+    const int groups = nf >> 2;  // nf % 4 == 0
     const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t i = t >> 1;
-    const int axis = static_cast<int>(t & 1);
+    const int64_t ra = t / groups;  // row * 2 + axis
+    const int k0 = static_cast<int>(t - ra * groups) * 4;
+    const int64_t i = ra >> 1;
+    const int axis = static_cast<int>(ra & 1);
     if (i >= n) return;
-    const double c = coords[2 * i + axis];
+    const double c = __ldg(coords + 2 * i + axis);
     const float ch = static_cast<float>(c);
     const float cl = static_cast<float>(c - static_cast<double>(ch));
-    uint4* dst = reinterpret_cast<uint4*>(pe16 + i * (4 * nf) + axis * (2 * nf));
-    for (int k0 = 0; k0 < nf; k0 += 4) {
-        uint32_t w[4];
+    uint32_t w[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const float2 f = F[k0 + j];
-            const float p = f.x * ch;
-            const float e = fmaf(f.x, ch, -p) + fmaf(f.x, cl, f.y * ch);
-            const float r = fmaf(-2.0f, rintf(0.5f * p), p) + e;
-            // |pi r| <= pi (+ tiny): the SFU sin/cos (abs err <= 2^-21.4 on [-pi, pi]; fp32 pi and
-            // the product add < 1e-6) -- 2 MUFU ops instead of the software sincospi
-            float sv, cv;
-            __sincosf(r * 3.14159265358979f, &sv, &cv);
-            const __half2 h = __floats2half2_rn(sv, cv);
-            w[j] = *reinterpret_cast<const uint32_t*>(&h);
-        }
-        dst[k0 >> 2] = make_uint4(w[0], w[1], w[2], w[3]);
+    for (int j = 0; j < 4; ++j) {
+        const float2 f = __ldg(F + k0 + j);
+        const float p = f.x * ch;
+        const float e = fmaf(f.x, ch, -p) + fmaf(f.x, cl, f.y * ch);
+        const float r = fmaf(-2.0f, rintf(0.5f * p), p) + e;
+        // |pi r| <= pi (+ tiny): the SFU sin/cos (abs err <= 2^-21.4 on [-pi, pi]; fp32 pi and
+        // the product add < 1e-6) -- 2 MUFU ops instead of the software sincospi
+        float sv, cv;
+        __sincosf(r * 3.14159265358979f, &sv, &cv);
+        const __half2 h = __floats2half2_rn(sv, cv);
+        w[j] = *reinterpret_cast<const uint32_t*>(&h);
     }
+    reinterpret_cast<uint4*>(pe16 + i * (4 * nf) + axis * (2 * nf))[k0 >> 2] = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
 // `fwa attend` row checksums (tools/fwa_cli.cpp:214-218): sum = 0.0; sum += (double)f[c]
@@ -102,7 +104,9 @@ __global__ void k_prefetch_l2(const uint8_t* __restrict__ p, int64_t bytes) {
 }
 
 void launch_prefetch_l2(const void* p, int64_t bytes, cudaStream_t s, int64_t* launches) {
-    if (!p || bytes < 16) return;
+    // only while the rows fit L2 with room for the schedule's buffers (a batch of frames
+    // larger than that would only evict its own rows)
+    if (!p || bytes < 16 || bytes > (48ll << 20)) return;
     k_prefetch_l2<<<kNumSMs, 128, 0, s>>>(static_cast<const uint8_t*>(p), bytes);
     ++*launches;
 }
@@ -111,7 +115,7 @@ void launch_positional_embedding(const double* coords, int64_t n, int d, const d
                                  float* pe, __half* pe16, cudaStream_t s, int64_t* launches) {
     if (!pe && pe16 && (d / 4) % 4 == 0) {  // d_freq holds [nf doubles | nf float2 (2f hi, lo)]
         const int nf = d / 4;
-        k_pe_fp16<<<static_cast<unsigned>((2 * n + 255) / 256), 256, 0, s>>>(
+        k_pe_fp16<<<static_cast<unsigned>((2 * n * (nf / 4) + 255) / 256), 256, 0, s>>>(
             coords, n, nf, reinterpret_cast<const float2*>(d_freq + nf), pe16);
         ++*launches;
         return;

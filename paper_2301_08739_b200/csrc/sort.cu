@@ -843,40 +843,55 @@ __global__ void __launch_bounds__(1024) k_drop_tables(const int32_t* __restrict_
     for (int k = threadIdx.x; k < n; k += blockDim.x) dst[k] = v[k];
 }
 
-// Grid over n_specs * ntot plan entries + ntot pillar ids:
-//   plan entry (s, j): kept id -> idx[s][j - #drop_pos[s] < j]; for the last block's
-//   spec also out_pos[that] = kept_rank(id)
-//   pillar id i: kept_rank[i] = i - #drop_sorted < i; kept_ids[kept_rank] = i
+// Grid (pillar-index chunks of 256, n_specs + 1):
+//   y = s < n_specs, plan entry (s, j): kept id -> idx[s][j - #drop_pos[s] < j]; for the last
+//   block's spec also out_pos[that] = kept_rank(id)
+//   y = n_specs, pillar id i: kept_rank[i] = i - #drop_sorted < i; kept_ids[kept_rank] = i
+// A pillar is dropped iff its spec-0 position lies in its frame's tail (the frame of a plan
+// position j is the frame of the id stored there: frames never mix).  The counts of sorted
+// drop values below j are taken per CTA: one binary search for the CTA's first index, then a
+// short forward walk per thread (a 256-index range holds at most a few drops).
 FWA_DEVINL bool is_dropped(const int32_t* drop_sorted, int n, int32_t id, int* lb_out) {
     const int lb = count_less(drop_sorted, n, id);
     if (lb_out) *lb_out = lb;
     return lb < n && drop_sorted[lb] == id;
 }
 
-__global__ void k_compact_all(const int32_t* __restrict__ sorted, int64_t ntot, int n_specs,
-                              const int32_t* __restrict__ drop_sorted,
-                              const int32_t* __restrict__ drop_pos, int n_drop, int64_t K, int s_last,
-                              int32_t* __restrict__ idx, uint32_t* __restrict__ kept_rank,
-                              int32_t* __restrict__ kept_ids, int32_t* __restrict__ out_pos) {
-    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t total = ntot * n_specs;
-    if (t < total) {
-        const int s = static_cast<int>(t / ntot);
-        const int32_t id = sorted[t];
-        int lb;
-        if (is_dropped(drop_sorted, n_drop, id, &lb)) return;
-        const int64_t j = t - static_cast<int64_t>(s) * ntot;
-        const int64_t c = j - count_less(drop_pos + static_cast<int64_t>(s) * (n_drop > 0 ? n_drop : 1), n_drop,
-                                         static_cast<int32_t>(t));
+__global__ void __launch_bounds__(256) k_compact_all(const int32_t* __restrict__ sorted,
+                                                     const int32_t* __restrict__ inv0, int64_t ntot, int n_specs,
+                                                     const int64_t* __restrict__ frame_off,
+                                                     const int64_t* __restrict__ rows, int n_frames,
+                                                     const int32_t* __restrict__ drop_sorted,
+                                                     const int32_t* __restrict__ drop_pos, int n_drop, int64_t K,
+                                                     int s_last, int32_t* __restrict__ idx,
+                                                     uint32_t* __restrict__ kept_rank,
+                                                     int32_t* __restrict__ kept_ids, int32_t* __restrict__ out_pos) {
+    const int s = static_cast<int>(blockIdx.y);
+    const bool plan = s < n_specs;
+    const int64_t j0 = static_cast<int64_t>(blockIdx.x) * blockDim.x;
+    const int64_t j = j0 + threadIdx.x;
+    const int64_t base = plan ? static_cast<int64_t>(s) * ntot : 0;  // drop_pos holds stacked plan indices
+    const int32_t* dl = plan ? drop_pos + static_cast<int64_t>(s) * (n_drop > 0 ? n_drop : 1) : drop_sorted;
+    __shared__ int s_lo, s_f0;
+    if (threadIdx.x == 0) {
+        s_lo = n_drop > 0 ? count_less(dl, n_drop, static_cast<int32_t>(base + j0)) : 0;
+        s_f0 = n_frames > 1 ? frame_of(frame_off, n_frames, j0 < ntot ? j0 : ntot - 1) : 0;
+    }
+    __syncthreads();
+    if (j >= ntot) return;
+    const int32_t id = plan ? sorted[base + j] : static_cast<int32_t>(j);
+    int f = s_f0;
+    while (f + 1 < n_frames && frame_off[f + 1] <= j) ++f;
+    if (n_drop > 0 && inv0[id] >= frame_off[f] + rows[f]) return;  // block 0's tail of its frame
+    int lb = s_lo;
+    while (lb < n_drop && dl[lb] < base + j) ++lb;
+    const int64_t c = j - lb;
+    if (plan) {
         idx[static_cast<int64_t>(s) * K + c] = id;
-        if (s == s_last) out_pos[c] = id - lb;
-    } else if (t < total + ntot) {
-        const int32_t i = static_cast<int32_t>(t - total);
-        int lb;
-        if (is_dropped(drop_sorted, n_drop, i, &lb)) return;
-        const int32_t r = i - lb;
-        kept_rank[i] = static_cast<uint32_t>(r);
-        kept_ids[r] = i;
+        if (s == s_last) out_pos[c] = id - count_less(drop_sorted, n_drop, id);
+    } else {
+        kept_rank[j] = static_cast<uint32_t>(c);
+        kept_ids[c] = id;
     }
 }
 
@@ -889,13 +904,14 @@ void launch_drop_tables(const int32_t* sorted0, int n, const int64_t* frame_off,
     ++*launches;
 }
 
-void launch_compact_all(const int32_t* sorted, int64_t ntot, int n_specs, const int32_t* drop_sorted,
+void launch_compact_all(const int32_t* sorted, const int32_t* inv0, int64_t ntot, int n_specs,
+                        const int64_t* frame_off, const int64_t* rows, int n_frames, const int32_t* drop_sorted,
                         const int32_t* drop_pos, int n_drop, int64_t K, int s_last, int32_t* idx,
                         uint32_t* kept_rank, int32_t* kept_ids, int32_t* out_pos, cudaStream_t s,
                         int64_t* launches) {
-    const int64_t total = ntot * (n_specs + 1);
-    k_compact_all<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
-        sorted, ntot, n_specs, drop_sorted, drop_pos, n_drop, K, s_last, idx, kept_rank, kept_ids, out_pos);
+    dim3 grid(static_cast<unsigned>((ntot + 255) / 256), static_cast<unsigned>(n_specs + 1));
+    k_compact_all<<<grid, 256, 0, s>>>(sorted, inv0, ntot, n_specs, frame_off, rows, n_frames, drop_sorted, drop_pos,
+                                       n_drop, K, s_last, idx, kept_rank, kept_ids, out_pos);
     ++*launches;
 }
 

@@ -49,6 +49,16 @@ void swizzle_weight_bf16(const float* w, int rows, int k, uint16_t* out) {
             out[sw128_offset(r, c, rows) / 2] = f32_to_bf16_rn(w[static_cast<size_t>(r) * k + c]);
 }
 
+static uint16_t f32_to_f16_rn(float f) {
+    const __half h = __float2half_rn(f);
+    return *reinterpret_cast<const uint16_t*>(&h);
+}
+static void swizzle_weight_f16(const float* w, int rows, int k, uint16_t* out) {
+    for (int r = 0; r < rows; ++r)
+        for (int c = 0; c < k; ++c)
+            out[sw128_offset(r, c, rows) / 2] = f32_to_f16_rn(w[static_cast<size_t>(r) * k + c]);
+}
+
 void build_pair_images(const float* w_qkv, const float* w_out, const float* w1f, const float* w2,
                        uint16_t* out) {
     // the fused kernel's GELU omits its factor 1/2 (x (1 + tanh g) instead of x/2 (1 + tanh g)):
@@ -61,7 +71,7 @@ void build_pair_images(const float* w_qkv, const float* w_out, const float* w1f,
         for (int c = 0; c < 3; ++c) swizzle_weight_bf16(w_qkv + (128 * c + 64 * v) * 128, 64, 128, o + c * 8192);
         swizzle_weight_bf16(w_out + 64 * v * 128, 64, 128, o + 24576);
         for (int h = 0; h < 2; ++h) swizzle_weight_bf16(w1f + (128 * h + 64 * v) * 128, 64, 128, o + 32768 + h * 8192);
-        swizzle_weight_bf16(w2 + 64 * v * 256, 64, 256, o + 49152);
+        swizzle_weight_f16(w2 + 64 * v * 256, 64, 256, o + 49152);  // fp16: the GELU activations are fp16
     }
 }
 

@@ -22,7 +22,7 @@ def st(col): v = (g[:, col] - e0) / 1e3; return f"min {v.min():7.2f} med {np.med
 print("fused kernel, global timer relative to the first CTA entry (us):")
 for col, nm in ((63, "entry"), (60, "griddep_wait done"), (59, "weights landed"), (61, "unit loop done"), (62, "exit")):
     print(f"  {nm:18s} {st(col)}")
-names = ["start", "ln1_ld", "ln1", "qkv", "ep0", "att0", "ep1", "att1", "P", "ln2", "Ua", "ffn2a", "Ub", "ffn2b", "O", "out"]
+names = ["start", "ln1_ld", "ln1", "qkv", "ep", "att_pre", "halo", "att_post", "P", "ln2", "Ua", "ffn2a", "Ub", "ffn2b", "O", "out"]
 for cta in (0, 1, 40, 41, 146, 147):
     row = t[cta]
     print(f"cta {cta}: setup {row[1] - row[0] if row[1] else 0}")
