@@ -773,7 +773,7 @@ void build_schedule_body(fwa_b200_ctx* c, const double* d_coords, const fwa_conf
         if (nd > 0)
             launch_drop_tables(S.sorted, nd, d_off, d_rows, d_drop_off, nf, S.sorted_inv, ntot, n_specs,
                                S.dropped_ids, drop_sorted, drop_pos, st, &c->launches);
-        launch_compact_all(S.sorted, S.sorted_inv, ntot, n_specs, d_off, d_rows, nf, drop_sorted, drop_pos, nd, S.K, s_last, S.idx,
+        launch_compact_all(S.sorted, ntot, n_specs, d_off, d_drop_off, nf, drop_sorted, drop_pos, nd, S.K, s_last, S.idx,
                            S.kept_rank, S.kept_ids, S.out_pos, st, &c->launches);
         check_launch();
         return;
@@ -871,8 +871,9 @@ void run_block(fwa_b200_ctx* c, const BlockParams& p, const fwa_config_t* cfg, i
         StageRec* r = c->rec;
         const int slot = r && r->next_slot < r->n_slots ? r->next_slot++ : -1;
         RecSpan span(c, slot >= 0 ? -1 : FWA_STAGE_ATTENTION, slot);
-        launch_block_fused(x_in, x_in64, pe16, ridx, sidx, x_out, rows, G, p.tc, c->d_flag, st, &c->launches, tr,
-                           slot >= 0 ? r->d_phase + 4 * slot : nullptr, d_peers, d_peers ? 8 : 0);
+        if (!launch_block_fused(x_in, x_in64, pe16, ridx, sidx, x_out, rows, G, p.tc, c->d_flag, st, &c->launches, tr,
+                                slot >= 0 ? r->d_phase + 4 * slot : nullptr, d_peers, d_peers ? 8 : 0))
+            throw FwaError{FWA_ERR_CUDA, "k_block_fused: cuTensorMapEncodeTiled (x-row tensor map) failed"};
         check_launch("k_block_fused");
         return;
     }

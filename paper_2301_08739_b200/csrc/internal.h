@@ -89,8 +89,8 @@ void launch_drop_tables(const int32_t* sorted0, int n, const int64_t* frame_off,
                         const int64_t* drop_off, int n_frames, const int32_t* inv, int64_t ntot, int n_specs,
                         int32_t* dropped_ids, int32_t* drop_sorted, int32_t* drop_pos, cudaStream_t s,
                         int64_t* launches);
-void launch_compact_all(const int32_t* sorted, const int32_t* inv0, int64_t ntot, int n_specs,
-                        const int64_t* frame_off, const int64_t* rows, int n_frames, const int32_t* drop_sorted,
+void launch_compact_all(const int32_t* sorted, int64_t ntot, int n_specs, const int64_t* frame_off,
+                        const int64_t* drop_off, int n_frames, const int32_t* drop_sorted,
                         const int32_t* drop_pos, int n_drop, int64_t K, int s_last, int32_t* idx,
                         uint32_t* kept_rank, int32_t* kept_ids, int32_t* out_pos, cudaStream_t s,
                         int64_t* launches);
@@ -177,7 +177,8 @@ void launch_outproj_ffn_tc(const __nv_bfloat16* cat, const float* x_in, const do
 // One whole block (gather .. scatter) in one persistent kernel on CTA pairs
 // (block_fused.cu); supported group sizes: see block_fused_supported.
 bool block_fused_supported(int G);
-void launch_block_fused(const float* x, const double* x64, const __half* pe16, const int32_t* ridx,
+// false: the x-row tensor map could not be encoded (nothing launched)
+bool launch_block_fused(const float* x, const double* x64, const __half* pe16, const int32_t* ridx,
                         const int32_t* sidx, float* x_out, int64_t rows, int G, const TcBlockWeights& w,
                         int* d_nonfinite, cudaStream_t s, int64_t* launches,
                         unsigned long long* trace = nullptr, unsigned long long* phase = nullptr,

@@ -847,20 +847,14 @@ __global__ void __launch_bounds__(1024) k_drop_tables(const int32_t* __restrict_
 //   y = s < n_specs, plan entry (s, j): kept id -> idx[s][j - #drop_pos[s] < j]; for the last
 //   block's spec also out_pos[that] = kept_rank(id)
 //   y = n_specs, pillar id i: kept_rank[i] = i - #drop_sorted < i; kept_ids[kept_rank] = i
-// A pillar is dropped iff its spec-0 position lies in its frame's tail (the frame of a plan
-// position j is the frame of the id stored there: frames never mix).  The counts of sorted
-// drop values below j are taken per CTA: one binary search for the CTA's first index, then a
-// short forward walk per thread (a 256-index range holds at most a few drops).
-FWA_DEVINL bool is_dropped(const int32_t* drop_sorted, int n, int32_t id, int* lb_out) {
-    const int lb = count_less(drop_sorted, n, id);
-    if (lb_out) *lb_out = lb;
-    return lb < n && drop_sorted[lb] == id;
-}
-
-__global__ void __launch_bounds__(256) k_compact_all(const int32_t* __restrict__ sorted,
-                                                     const int32_t* __restrict__ inv0, int64_t ntot, int n_specs,
+// Each CTA finds the first sorted drop value at or past its first index by one binary
+// search; every thread walks on from there to its own index (a 256-index range holds few
+// drops), so it has both its count and whether it is itself dropped -- no gathers.  The
+// kept rank of a plan entry's id (out_pos) searches only the id's frame's drops (ids of a
+// frame are contiguous, so are its entries of the sorted drop list).
+__global__ void __launch_bounds__(256) k_compact_all(const int32_t* __restrict__ sorted, int64_t ntot, int n_specs,
                                                      const int64_t* __restrict__ frame_off,
-                                                     const int64_t* __restrict__ rows, int n_frames,
+                                                     const int64_t* __restrict__ drop_off, int n_frames,
                                                      const int32_t* __restrict__ drop_sorted,
                                                      const int32_t* __restrict__ drop_pos, int n_drop, int64_t K,
                                                      int s_last, int32_t* __restrict__ idx,
@@ -875,23 +869,27 @@ __global__ void __launch_bounds__(256) k_compact_all(const int32_t* __restrict__
     __shared__ int s_lo, s_f0;
     if (threadIdx.x == 0) {
         s_lo = n_drop > 0 ? count_less(dl, n_drop, static_cast<int32_t>(base + j0)) : 0;
-        s_f0 = n_frames > 1 ? frame_of(frame_off, n_frames, j0 < ntot ? j0 : ntot - 1) : 0;
+        s_f0 = plan && s == s_last && n_frames > 1 ? frame_of(frame_off, n_frames, j0 < ntot ? j0 : ntot - 1) : 0;
     }
     __syncthreads();
     if (j >= ntot) return;
-    const int32_t id = plan ? sorted[base + j] : static_cast<int32_t>(j);
-    int f = s_f0;
-    while (f + 1 < n_frames && frame_off[f + 1] <= j) ++f;
-    if (n_drop > 0 && inv0[id] >= frame_off[f] + rows[f]) return;  // block 0's tail of its frame
     int lb = s_lo;
     while (lb < n_drop && dl[lb] < base + j) ++lb;
+    if (lb < n_drop && dl[lb] == base + j) return;  // dropped (block 0's tail of its frame)
     const int64_t c = j - lb;
     if (plan) {
+        const int32_t id = sorted[base + j];
         idx[static_cast<int64_t>(s) * K + c] = id;
-        if (s == s_last) out_pos[c] = id - count_less(drop_sorted, n_drop, id);
+        if (s == s_last) {
+            int f = s_f0;
+            while (f + 1 < n_frames && frame_off[f + 1] <= j) ++f;
+            const int d0 = n_frames > 1 ? static_cast<int>(drop_off[f]) : 0;
+            const int d1 = n_frames > 1 && f + 1 < n_frames ? static_cast<int>(drop_off[f + 1]) : n_drop;
+            out_pos[c] = id - d0 - count_less(drop_sorted + d0, d1 - d0, id);
+        }
     } else {
         kept_rank[j] = static_cast<uint32_t>(c);
-        kept_ids[c] = id;
+        kept_ids[c] = static_cast<int32_t>(j);
     }
 }
 
@@ -904,13 +902,13 @@ void launch_drop_tables(const int32_t* sorted0, int n, const int64_t* frame_off,
     ++*launches;
 }
 
-void launch_compact_all(const int32_t* sorted, const int32_t* inv0, int64_t ntot, int n_specs,
-                        const int64_t* frame_off, const int64_t* rows, int n_frames, const int32_t* drop_sorted,
+void launch_compact_all(const int32_t* sorted, int64_t ntot, int n_specs, const int64_t* frame_off,
+                        const int64_t* drop_off, int n_frames, const int32_t* drop_sorted,
                         const int32_t* drop_pos, int n_drop, int64_t K, int s_last, int32_t* idx,
                         uint32_t* kept_rank, int32_t* kept_ids, int32_t* out_pos, cudaStream_t s,
                         int64_t* launches) {
     dim3 grid(static_cast<unsigned>((ntot + 255) / 256), static_cast<unsigned>(n_specs + 1));
-    k_compact_all<<<grid, 256, 0, s>>>(sorted, inv0, ntot, n_specs, frame_off, rows, n_frames, drop_sorted, drop_pos,
+    k_compact_all<<<grid, 256, 0, s>>>(sorted, ntot, n_specs, frame_off, drop_off, n_frames, drop_sorted, drop_pos,
                                        n_drop, K, s_last, idx, kept_rank, kept_ids, out_pos);
     ++*launches;
 }

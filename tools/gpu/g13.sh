@@ -1,0 +1,4 @@
+python -m pytest tests -m gpu -q -x -k "fused or golden or config2 or zero_weights or determinism or batch or frame_stream or split" > gpurun_out/g13_pytest.txt 2>&1; tail -3 gpurun_out/g13_pytest.txt
+for r in 1 2; do for v in cpa; do FWA_B200_LIB=$PWD/paper_2301_08739_b200/libfwa_b200_p$v.so python tools/ab_time.py 40 2>&1 | tail -1; done; python tools/ab_time.py 40 2>&1 | tail -1; done
+python tools/trace_fused.py 2>&1 | grep -A2 "cta 0:\|cta 1:"
+python tools/sched_batch.py 64 2>&1 | tail -1
