@@ -394,7 +394,7 @@ def run_ours(args, rank, world, local_rank, dist):
     pk_t_kind = ("%s bf16 burst (clocks at max, no power cap while timed)" if unthrottled
                  else "%s bf16 sustained (clocks below max or power-capped while timed)") % pk_kind
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r2_ncu_traffic.json")) as f:
             ncu_traffic = json.load(f)
     except Exception:
         ncu_traffic = {}

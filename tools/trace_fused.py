@@ -31,7 +31,8 @@ for cta in (0, 1, 40, 41, 146, 147):
         b = 1 + 16 * u
         if not row[b]:
             break
-        seg = [(names[k], int(row[b + k] - row[b + k - 1])) for k in range(1, 16) if row[b + k]]
+        ks = sorted((int(row[b + k]), k) for k in range(0, 16) if row[b + k])
+        seg = [(names[k], t - tp) for (tp, _), (t, k) in zip(ks, ks[1:])]
         print("   u%d total %d: " % (u, int(row[b + 15] - row[b])) + " ".join(f"{n}={v}" for n, v in seg))
 
 clk = (t[:, 49] - t[:, 0]).astype(np.float64)
