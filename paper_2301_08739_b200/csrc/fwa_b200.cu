@@ -27,6 +27,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <optional>
 #include <string>
 #include <vector>
 
@@ -226,6 +227,10 @@ struct StageRec {
     std::vector<StageSpan> spans;
     unsigned long long* d_phase = nullptr;  // n_slots x 4, zeroed when the call starts
     int n_slots = 0, next_slot = 0;
+    // the fused blocks of a call share phase slot 0 and ONE event span (set by forward_device):
+    // no events between the block launches, whose programmatic dependent launches they
+    // would serialise
+    bool blocks_whole = false;
     std::vector<unsigned long long> h_phase;
 };
 
@@ -869,8 +874,10 @@ void run_block(fwa_b200_ctx* c, const BlockParams& p, const fwa_config_t* cfg, i
         unsigned long long* tr = trace_fused && !x_in64 ? ws<unsigned long long>(c, "trace", 2 * 148 * 64) : nullptr;
         StageEv t(c, FWA_PROF_BLOCK);
         StageRec* r = c->rec;
-        const int slot = r && r->next_slot < r->n_slots ? r->next_slot++ : -1;
-        RecSpan span(c, slot >= 0 ? -1 : FWA_STAGE_ATTENTION, slot);
+        const bool whole = r && r->blocks_whole;
+        const int slot = whole ? 0 : r && r->next_slot < r->n_slots ? r->next_slot++ : -1;
+        std::optional<RecSpan> span;
+        if (!whole) span.emplace(c, slot >= 0 ? -1 : FWA_STAGE_ATTENTION, slot);
         if (!launch_block_fused(x_in, x_in64, pe16, ridx, sidx, x_out, rows, G, p.tc, c->d_flag, st, &c->launches, tr,
                                 slot >= 0 ? r->d_phase + 4 * slot : nullptr, d_peers, d_peers ? 8 : 0))
             throw FwaError{FWA_ERR_CUDA, "k_block_fused: cuTensorMapEncodeTiled (x-row tensor map) failed"};
@@ -1031,6 +1038,14 @@ void forward_device(fwa_b200_ctx* c, const double* d_coords, const float* d_feat
     if (feats_ready) CUDA_OK(cudaStreamWaitEvent(st, feats_ready, 0));  // block 0 reads them
     float* X = ws<float>(c, "X", static_cast<size_t>(S.ntot) * d);
     static const bool skip_blocks = std::getenv("FWA_B200_DEBUG_SCHEDULE_ONLY") != nullptr;  // timing probe
+    // StageTimes of the fused blocks: one span around all of them, apportioned by their
+    // summed phase counters (slot 0)
+    std::optional<RecSpan> blocks_span;
+    if (c->rec && fast && c->precision == FWA_PREC_BF16 && block_fused_supported(cfg->group_size) &&
+        c->rec->n_slots > 0) {
+        c->rec->blocks_whole = true;
+        blocks_span.emplace(c, -1, 0);
+    }
     for (int b = 0; b < (skip_blocks ? 0 : cfg->n_blocks); ++b) {
         const int s = b % 4;
         const int32_t* idx = S.idx + S.K * s;
@@ -1040,6 +1055,8 @@ void forward_device(fwa_b200_ctx* c, const double* d_coords, const float* d_feat
         run_block(c, c->blocks[static_cast<size_t>(b)], cfg, S.K, idx, xin, xin64, pe, pe16,
                   last ? d_out : X, last ? S.out_pos : idx, fast);
     }
+    blocks_span.reset();
+    if (c->rec) c->rec->blocks_whole = false;
     if (d_kept)
         CUDA_OK(cudaMemcpyAsync(d_kept, S.kept_ids, static_cast<size_t>(S.K) * 4,
                                 cudaMemcpyDeviceToDevice, st));
