@@ -1477,22 +1477,27 @@ int mtiles(int G, int r0, int r1) {
     return n;
 }
 
-// the row split of a full unit: fewest attention task rounds (4 heads x m-tiles per
-// pass over 16 warps) on the slower CTA, then the most even split of the rows
+// the row split of a full unit, by (1) the fewest attention task rounds (2 tasks per warp per
+// round: 32 (m-tile, head) tasks of the slower CTA), (2) the fewest m-tiles in all (group
+// parts padded to 16 query rows: a split inside a group can cost a tile), (3) rank 0 -- whose
+// thread 0 also issues the pair's MMAs -- not holding more m-tiles than rank 1, (4) the most
+// even rows.  G = 69: 101 | 106 rows, 7 | 8 m-tiles (measured 0.564 ms/frame F60 vs 0.573
+// for the even 103 | 104 = 8 | 8)
 int choose_split(int G) {
     const int R = (256 / G) * G;
-    int best = -1, best_rounds = 1 << 30, best_skew = 1 << 30;
+    int best = -1;
+    long long best_key = 1LL << 62;
     for (int s = R - 128 > 1 ? R - 128 : 1; s <= 128 && s <= R; ++s) {
         if (ext_rows_needed(G, s) > kKVRows) continue;
         if (!staging_fits(G, s)) continue;
-        if (mtiles(G, 0, s) > 16 || mtiles(G, s, R) > 16) continue;  // the per-CTA m-tile table
-        const int t0 = 4 * mtiles(G, 0, s), t1 = 4 * mtiles(G, s, R);
-        const int rounds = ((t0 + 15) / 16 > (t1 + 15) / 16) ? (t0 + 15) / 16 : (t1 + 15) / 16;
+        const int m0 = mtiles(G, 0, s), m1 = mtiles(G, s, R);
+        if (m0 > 16 || m1 > 16) continue;  // the per-CTA m-tile table
+        const int rounds = ((m0 > m1 ? m0 : m1) * 8 + 31) / 32;
         const int skew = s > R - s ? s - (R - s) : (R - s) - s;
-        if (rounds < best_rounds || (rounds == best_rounds && skew < best_skew)) {
+        const long long key = ((static_cast<long long>(rounds) * 64 + (m0 + m1)) * 2 + (m0 > m1 ? 1 : 0)) * 512 + skew;
+        if (key < best_key) {
             best = s;
-            best_rounds = rounds;
-            best_skew = skew;
+            best_key = key;
         }
     }
     return best;
@@ -1546,6 +1551,13 @@ bool launch_block_fused(const float* x, const double* x64, const __half* pe16, c
     (void)n_peers;
     a.rows = rows; a.G = G; a.gpu = 256 / G;
     a.split = choose_split(G);
+    if (const char* e = std::getenv("FWA_B200_SPLIT")) {  // experiments: a forced row split (checked)
+        const int sp = std::atoi(e);
+        const int R = (256 / G) * G;
+        if (sp >= R - 128 && sp <= 128 && ext_rows_needed(G, sp) <= kKVRows && staging_fits(G, sp) &&
+            mtiles(G, 0, sp) <= 16 && mtiles(G, sp, R) <= 16)
+            a.split = sp;
+    }
     const int64_t n_groups = rows / G;
     a.n_units = static_cast<int>((n_groups + a.gpu - 1) / a.gpu);
     a.wpair = w.w_pair; a.vec = w.vec_pair; a.nonfinite = d_nonfinite;
