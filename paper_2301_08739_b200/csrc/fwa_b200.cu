@@ -601,7 +601,7 @@ int32_t* sort_specs(fwa_b200_ctx* c, const double* d_coords, int64_t ntot, int n
     const int64_t n_part = sort_keys_partials(ntot);
     long long* partials = ws<long long>(c, "key_partials", static_cast<size_t>(n_part) * 4 * n_specs);
     if (!exact) {
-        SpecBins* d_sb = ws<SpecBins>(c, "specbins", 4);
+        SpecBins* d_sb = ws<SpecBins>(c, "specbins", 4 * static_cast<size_t>(nf));
         uint32_t* d_nbins = ws<uint32_t>(c, "nbins", 4);
         unsigned* ticket = ws<unsigned>(c, "sort_ticket", 4);  // [0] key kernel, [1] bin scan
         uint32_t* large = ws<uint32_t>(c, "large_bins", static_cast<size_t>(kBinCap) + 1);
@@ -624,7 +624,14 @@ int32_t* sort_specs(fwa_b200_ctx* c, const double* d_coords, int64_t ntot, int n
         uint32_t* cursor = ws<uint32_t>(c, "cursor", static_cast<size_t>(kBinCap));
         uint32_t* tile_sums = ws<uint32_t>(c, "bin_tile_sums", 1024);
         uint32_t* bin_of = ws<uint32_t>(c, "bin_of", static_cast<size_t>(total));
-        launch_bins_hist(win, ntot, n_specs, d_off, nf, d_sb, bin_of, hist, d_nbins, st, &c->launches);
+        if (nf > 1) {
+            // a batch: every frame's own window range (frames far apart in world coordinates cost
+            // no empty bins between them); the union layout of the key kernel's setup is replaced
+            long long* mmf = ws<long long>(c, "minmax_frame", 4 * static_cast<size_t>(n_specs) * nf);
+            launch_frame_minmax(win, ntot, n_specs, d_off, nf, mmf, st, &c->launches);
+            launch_bins_setup_frames(mmf, n_specs, nf, kBinCap, d_sb, d_nbins, c->d_flag + 1, st, &c->launches);
+        }
+        launch_bins_hist(win, ntot, n_specs, d_off, nf, d_sb, bin_of, hist, d_nbins, st, &c->launches, nf > 1);
         launch_scan_bins_dev(hist, bin_start, cursor, d_nbins, kBinCap, tile_sums, ticket + 1, st, &c->launches);
         int32_t* pre = ws<int32_t>(c, "pre", static_cast<size_t>(total));
         double* pre_loc = ws<double>(c, "pre_loc", 2 * static_cast<size_t>(total));

@@ -67,6 +67,9 @@ void launch_bins_setup(const long long* partials, int64_t n_part, int n_specs, i
                        long long* mm, SpecBins* specs, uint32_t* d_nbins, int* overflow, cudaStream_t s,
                        int64_t* launches);
 void launch_zero_bins(uint32_t* hist, const uint32_t* d_nbins, cudaStream_t s, int64_t* launches);
+// per-frame dense bins of a frame batch from launch_frame_minmax's (spec, frame) ranges
+void launch_bins_setup_frames(const long long* mm, int n_specs, int nf, long long cap, SpecBins* specs,
+                              uint32_t* d_nbins, int* overflow, cudaStream_t s, int64_t* launches);
 // tile-local exclusive scan; tile_sums becomes the per-4096-bin tile offsets the
 // consumers add (tile_off below); ticket: zero-initialised, self-resetting
 void launch_scan_bins_dev(const uint32_t* hist, uint32_t* bin_start, uint32_t* cursor, const uint32_t* d_nbins,

@@ -312,9 +312,27 @@ __global__ void __launch_bounds__(256) k_frame_minmax(const long long* __restric
     if (threadIdx.x == 0) f0 = n_frames > 1 ? frame_of(frame_off, n_frames, base) : 0;
     __syncthreads();
     const int64_t i = base + threadIdx.x;
-    if (i < ntot) {
-        const longlong2 w = reinterpret_cast<const longlong2*>(win)[static_cast<int64_t>(s) * ntot + i];
-        const int f = n_frames > 1 ? frame_of(frame_off, n_frames, i) : 0;
+    const bool in = i < ntot;
+    longlong2 w = make_longlong2(0, 0);
+    int f = -1;
+    if (in) {
+        w = reinterpret_cast<const longlong2*>(win)[static_cast<int64_t>(s) * ntot + i];
+        f = n_frames > 1 ? frame_of(frame_off, n_frames, i) : 0;
+    }
+    // consecutive pillars mostly share a frame: a warp whose lanes all do reduces first and
+    // lane 0 alone updates the slot
+    const int f_lane0 = __shfl_sync(0xffffffffu, f, 0);
+    if (__all_sync(0xffffffffu, in && f == f_lane0)) {
+        const long long a0 = wmin(w.x), a1 = wmax(w.x), a2 = wmin(w.y), a3 = wmax(w.y);
+        if ((threadIdx.x & 31) == 0) {
+            const int k = f - f0;
+            long long* m = k < 8 ? sm[k] : mm + (static_cast<int64_t>(s) * n_frames + f) * 4;
+            atomicMin(m, a0);
+            atomicMax(m + 1, a1);
+            atomicMin(m + 2, a2);
+            atomicMax(m + 3, a3);
+        }
+    } else if (in) {
         const int k = f - f0;
         long long* m = k < 8 ? sm[k] : mm + (static_cast<int64_t>(s) * n_frames + f) * 4;
         atomicMin(m, w.x);
@@ -1103,6 +1121,74 @@ void launch_bins_setup(const long long* partials, int64_t n_part, int n_specs, i
                        long long* mm, SpecBins* specs, uint32_t* d_nbins, int* overflow, cudaStream_t s,
                        int64_t* launches) {
     k_bins_setup<<<1, 1024, 0, s>>>(partials, n_part, n_specs, nf, cap, mm, specs, d_nbins, overflow);
+    ++*launches;
+}
+
+// Per-frame dense bin layout of a frame batch on the device (no host round trip): one CTA
+// turns the (spec, frame) window min/max of k_frame_minmax into SpecBins[s * nf + f] (each
+// frame's own window range, bases by an exclusive scan in (spec, frame) order -- the
+// lexicographic window order of the union) and the device-side bin count; a total beyond
+// the capacity raises *overflow (the host API then re-runs with exact bins), otherwise it
+// clears it (a union range too wide for the fused setup is not an overflow here).
+__global__ void __launch_bounds__(1024) k_bins_setup_frames(const long long* __restrict__ mm, int n_specs, int nf,
+                                                            long long cap, SpecBins* __restrict__ specs,
+                                                            uint32_t* __restrict__ d_nbins, int* __restrict__ overflow) {
+    __shared__ long long carry;
+    __shared__ long long wsum[32];
+    __shared__ int bad;
+    const int n = n_specs * nf;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        carry = 0;
+        bad = 0;
+    }
+    __syncthreads();
+    for (int i0 = 0; i0 < n; i0 += blockDim.x) {
+        const int i = i0 + threadIdx.x;
+        long long sz = 0;
+        const long long* m = mm + static_cast<int64_t>(i) * 4;
+        if (i < n) {
+            const long long rM = m[1] - m[0] + 1, rm = m[3] - m[2] + 1;
+            if (rM <= 0 || rm <= 0 || rM > (1LL << 31) || rm > (1LL << 31) ||
+                static_cast<double>(rM) * static_cast<double>(rm) > static_cast<double>(cap))
+                bad = 1;
+            else
+                sz = rM * rm;
+        }
+        long long x = sz;  // inclusive warp scan
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            long long w = lane < static_cast<int>(blockDim.x >> 5) ? wsum[lane] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long y = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += y;
+            }
+            wsum[lane] = w;
+        }
+        __syncthreads();
+        const long long base = carry + x - sz + (wid ? wsum[wid - 1] : 0);
+        if (i < n) specs[i] = SpecBins{m[0], m[2], m[3] - m[2] + 1, sz, base};
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry = base + sz;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const bool over = bad || carry > cap;
+        *d_nbins = over ? 0u : static_cast<uint32_t>(carry);
+        if (overflow) *overflow = over ? 1 : 0;
+    }
+}
+
+void launch_bins_setup_frames(const long long* mm, int n_specs, int nf, long long cap, SpecBins* specs,
+                              uint32_t* d_nbins, int* overflow, cudaStream_t s, int64_t* launches) {
+    k_bins_setup_frames<<<1, 1024, 0, s>>>(mm, n_specs, nf, cap, specs, d_nbins, overflow);
     ++*launches;
 }
 

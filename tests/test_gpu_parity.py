@@ -739,6 +739,32 @@ def test_batch_frames_far_apart_per_frame_bins(ctx32):
         assert np.array_equal(res["features"][ko[i]:ko[i + 1]], r.features)
 
 
+def test_device_batch_far_apart_no_bin_overflow(ctx16):
+    """The device-resident (sync-free) forward of a batch whose frames lie kilometres apart:
+    per-frame window bins on the device, so no capacity overflow is raised (round 1 and the
+    union layout needed ~10^9 bins there) and the rows equal the host-API batch bit for bit."""
+    import torch
+    cfg = F.FwaConfig(n_blocks=2)
+    ctx16.load_params(cfg, F.init_backbone_params(cfg, 42))
+    frames = []
+    for k in range(3):
+        p = F.make_pillars(F.SCENES["F10"], 60 + k)
+        frames.append(F.PillarSet(p.coords + np.array([[k * 40000.0, -k * 25000.0]]), p.features))
+    off = np.cumsum([0] + [p.size() for p in frames])
+    coords = np.concatenate([p.coords for p in frames])
+    feats = np.concatenate([p.features for p in frames]).astype(np.float32)
+    dev = torch.device("cuda", 0)
+    dc, df = torch.from_numpy(coords).to(dev), torch.from_numpy(feats).to(dev)
+    dout = torch.empty((coords.shape[0], cfg.d_model), dtype=torch.float32, device=dev)
+    dkept = torch.empty(coords.shape[0], dtype=torch.int32, device=dev)
+    nk = ctx16.forward_device(dc.data_ptr(), df.data_ptr(), off.tolist(), cfg, dout.data_ptr(), dkept.data_ptr())
+    ctx16.sync_check()  # raised FWA_ERR_INTERNAL (bin capacity) with the union layout
+    res = ctx16.run_batch(coords, feats, off, cfg)
+    assert nk == len(res["kept"])
+    assert np.array_equal(dkept[:nk].cpu().numpy(), res["kept"])
+    assert np.array_equal(dout[:nk].cpu().numpy(), res["features"][:nk])
+
+
 def test_far_outlier_window_rank_fallback(ctx32):
     """One pillar 10^8 m away: no dense window layout fits (the round-1 code raised
     FWA_ERR_INTERNAL); the exact path rank-compresses the windows with a radix sort and the
