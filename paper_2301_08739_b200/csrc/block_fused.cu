@@ -1430,9 +1430,14 @@ void launch_nt(const FusedArgs& a, bool f64, cudaStream_t s) {
 
 // the rows of the extended K/V region one unit touches (both ranks), for the unit
 // geometry of group size G (the full unit; a partial last unit touches a subset)
+// the key-tile count a kernel instance is compiled for: the group sizes with their own
+// instances (compile-time G: the default 69 and the BASELINE config-5 sweep's 32, 48, 96,
+// 128) get exactly ceil(G / 16) * 2, any other G the next generic instance
 int kernel_nt(int G) {
     const int nt = ((G + 15) / 16) * 2;
-    return G == 69 ? 10 : nt <= 4 ? 4 : nt <= 8 ? 8 : nt <= 12 ? 12 : 16;
+    if (G == 69) return 10;
+    if (G == 48) return 6;
+    return nt <= 4 ? 4 : nt <= 8 ? 8 : nt <= 12 ? 12 : 16;
 }
 
 // rows of the extended K/V region a full unit touches (both ranks) for group size G
@@ -1574,12 +1579,19 @@ bool launch_block_fused(const float* x, const double* x64, const __half* pe16, c
         }
         a.xmap = last_map;
     }
-    switch (kernel_nt(G)) {
-        case 10: launch_nt<10, 69>(a, f64, s); break;  // FwaConfig default group size (backbone.hpp:26)
-        case 4: launch_nt<4, 0>(a, f64, s); break;
-        case 8: launch_nt<8, 0>(a, f64, s); break;
-        case 12: launch_nt<12, 0>(a, f64, s); break;
-        default: launch_nt<16, 0>(a, f64, s); break;
+    switch (G) {
+        case 69: launch_nt<10, 69>(a, f64, s); break;  // FwaConfig default group size (backbone.hpp:26)
+        case 32: launch_nt<4, 32>(a, f64, s); break;   // config-5 sweep sizes
+        case 48: launch_nt<6, 48>(a, f64, s); break;
+        case 96: launch_nt<12, 96>(a, f64, s); break;
+        case 128: launch_nt<16, 128>(a, f64, s); break;
+        default:
+            switch (kernel_nt(G)) {
+                case 4: launch_nt<4, 0>(a, f64, s); break;
+                case 8: launch_nt<8, 0>(a, f64, s); break;
+                case 12: launch_nt<12, 0>(a, f64, s); break;
+                default: launch_nt<16, 0>(a, f64, s); break;
+            }
     }
     ++*launches;
     return true;
