@@ -805,6 +805,15 @@ def run_split_scene(args, F, ctx, cfg, dev, stream, rank, world, dist, flush):
     d_feats = torch.from_numpy(ps.features.astype(np.float32)).to(dev)
     exchange = args.split_exchange or "p2p"
     flag = torch.zeros(1, dtype=torch.float32, device=dev)
+    if dist and exchange == "p2p":
+        # every rank must be able to map every peer's memory (NVLink / NVSwitch P2P); the
+        # ranks agree on the result, so all of them take the same path (NCCL all-to-all else)
+        ok = all(torch.cuda.can_device_access_peer(dev.index, j) for j in range(torch.cuda.device_count())
+                 if j != dev.index)
+        agree = torch.tensor([1.0 if ok else 0.0], device=dev)
+        dist.all_reduce(agree, op=dist.ReduceOp.MIN)
+        if agree.item() < 1.0:
+            exchange = "a2a"
 
     def all_gather(dst, src):
         if dist:
