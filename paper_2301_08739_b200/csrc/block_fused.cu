@@ -195,8 +195,25 @@ FWA_DEVINL void tmem_st8(uint32_t taddr, float4 a, float4 b) {
 }
 // this thread's TMEM row, columns [col, col + n): the broadcast bias values v[0, n) (8 at a
 // time: few live registers)
+#ifndef FWA_BIAS_X32
+#define FWA_BIAS_X32 1
+#endif
 template <int N>
 FWA_DEVINL void tmem_bias_row(uint32_t taddr, const float* v) {
+#if FWA_BIAS_X32
+    // 32 columns per tcgen05.st (fewer MIO instructions than 8-column stores)
+#pragma unroll
+    for (int j = 0; j < N; j += 32) {
+        float w[32];
+#pragma unroll
+        for (int k = 0; k < 32; k += 4) {
+            const float4 f = *reinterpret_cast<const float4*>(v + j + k);
+            w[k] = f.x; w[k + 1] = f.y; w[k + 2] = f.z; w[k + 3] = f.w;
+        }
+        tmem_st32(taddr + j, w);
+    }
+    return;
+#endif
 #pragma unroll
     for (int j = 0; j < N; j += 8)
         tmem_st8(taddr + j, *reinterpret_cast<const float4*>(v + j), *reinterpret_cast<const float4*>(v + j + 4));
@@ -439,8 +456,16 @@ FWA_DEVINL uint32_t attn_fast(uint32_t sRA, uint32_t sKV, uint8_t* pRA, const in
 
 // The reference's max-subtracted softmax (kernels.hpp:252-265, 533) for one task: scores
 // in fp32 (fp16 operands, fp32 accumulate), P = 2^(S - max) in (0, 1] rounded to fp16.
+#ifndef FWA_SHIFT_NOINLINE
+#define FWA_SHIFT_NOINLINE 0  // 1 measured 0.3% slower
+#endif
+#if FWA_SHIFT_NOINLINE
+#define FWA_SHIFT_ATTR __device__ __noinline__  // rarely run: kept out of the attention loop's code (i-cache)
+#else
+#define FWA_SHIFT_ATTR FWA_DEVINL
+#endif
 template <int NT, int GC>
-FWA_DEVINL void attn_shift(uint32_t sRA, uint32_t sKV, uint8_t* pRA, int head, int m0, int qend, int ke0, int G_rt) {
+FWA_SHIFT_ATTR void attn_shift(uint32_t sRA, uint32_t sKV, uint8_t* pRA, int head, int m0, int qend, int ke0, int G_rt) {
     const int G = GC > 0 ? GC : G_rt;
     const int lane = threadIdx.x & 31;
     const int g = lane >> 2, t4 = lane & 3;
@@ -1364,7 +1389,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
     FTRG(61);
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(a.nonfinite, 1);
     fence_before_sync();
-    cluster_sync_all();
+#ifndef FWA_EXIT_RELAXED
+#define FWA_EXIT_RELAXED 1
+#endif
+    // both CTAs done with the pair's TMEM before either deallocates: an execution barrier
+    // (relaxed: the exit needs no memory ordering between the CTAs, and a release arrive
+    // costs a MEMBAR that waits for this CTA's last row stores)
+    if (FWA_EXIT_RELAXED)
+        asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+    else
+        cluster_sync_all();
     fence_after_sync();
     if (warp == 0) tmem_dealloc2(tmem, 512);
     FTRG(62);
