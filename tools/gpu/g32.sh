@@ -1,0 +1,3 @@
+FWA_B200_LIB=$PWD/paper_2301_08739_b200/libfwa_b200_plhadd.so python -m pytest tests -m gpu -q -x -k "fused or golden or config2 or shifted or batch_many" > gpurun_out/g32_pytest.txt 2>&1; tail -2 gpurun_out/g32_pytest.txt
+FWA_B200_LIB=$PWD/paper_2301_08739_b200/libfwa_b200_plhadd.so python -m pytest tests -m gpu -q -s -k "config2" 2>&1 | grep parity
+for r in 1 2 3; do FWA_B200_LIB=$PWD/paper_2301_08739_b200/libfwa_b200_plhadd.so python tools/ab_time.py 40 2>&1 | tail -1; python tools/ab_time.py 40 2>&1 | tail -1; done
