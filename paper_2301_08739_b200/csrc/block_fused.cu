@@ -193,15 +193,10 @@ FWA_DEVINL void tmem_st8(uint32_t taddr, float4 a, float4 b) {
                  "f"(a.y), "f"(a.z), "f"(a.w), "f"(b.x), "f"(b.y), "f"(b.z), "f"(b.w)
                  : "memory");
 }
-// this thread's TMEM row, columns [col, col + n): the broadcast bias values v[0, n) (8 at a
-// time: few live registers)
-#ifndef FWA_BIAS_X32
-#define FWA_BIAS_X32 1
-#endif
+// this thread's TMEM row, columns [col, col + N): the broadcast bias values v[0, N), 32
+// columns per tcgen05.st
 template <int N>
 FWA_DEVINL void tmem_bias_row(uint32_t taddr, const float* v) {
-#if FWA_BIAS_X32
-    // 32 columns per tcgen05.st (fewer MIO instructions than 8-column stores)
 #pragma unroll
     for (int j = 0; j < N; j += 32) {
         float w[32];
@@ -212,11 +207,6 @@ FWA_DEVINL void tmem_bias_row(uint32_t taddr, const float* v) {
         }
         tmem_st32(taddr + j, w);
     }
-    return;
-#endif
-#pragma unroll
-    for (int j = 0; j < N; j += 8)
-        tmem_st8(taddr + j, *reinterpret_cast<const float4*>(v + j), *reinterpret_cast<const float4*>(v + j + 4));
 }
 FWA_DEVINL void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 FWA_DEVINL float4 tmem_ld4(uint32_t taddr) {
