@@ -95,10 +95,19 @@ struct fwa_b200_ctx {
                    params_version == o.params_version && ws_epoch == o.ws_epoch;
         }
     };
-    GraphKey g_key, g_warm;
-    cudaGraphExec_t g_exec = nullptr;
-    int64_t g_launches = 0;
-    int64_t* g_tab = nullptr;  // frame table owned by the captured graph
+    // a few captured graphs (a double-buffered frame stream alternates two keys), least
+    // recently used first out; a key is captured on its second sighting among the last few
+    struct GraphEntry {
+        GraphKey key;
+        cudaGraphExec_t exec = nullptr;
+        int64_t launches = 0;
+        int64_t* tab = nullptr;  // frame table owned by the captured graph
+        uint64_t used = 0;
+    };
+    static constexpr int kGraphs = 4;
+    std::vector<GraphEntry> graphs;
+    std::vector<GraphKey> g_seen;  // recent keys run eagerly (at most kGraphs)
+    uint64_t g_clock = 0;
     bool g_disabled = false;
     // group-range split of one scene across ranks (BASELINE config 4)
     struct Split {
@@ -121,7 +130,8 @@ struct fwa_b200_ctx {
     int64_t* h_tab = nullptr;  // pinned frame-table staging (2 slots)
     size_t h_tab_cap = 0;
     int h_tab_slot = 0;
-    cudaEvent_t ev_tab[2] = {nullptr, nullptr};
+    static constexpr int kTabSlots = 8;  // pinned frame-table staging ring (host run-ahead depth)
+    cudaEvent_t ev_tab[kTabSlots] = {};
     long long* h_minmax = nullptr;  // pinned (16)
     // stage profiling (the analogue of the reference's StageTimer, backbone.hpp:139-151)
     bool profiling = false;
@@ -739,15 +749,19 @@ const int64_t* upload_frame_table(fwa_b200_ctx* c, const Schedule& S) {
     std::vector<int64_t> tab = frame_table(S);
     // pinned staging so the copy is truly asynchronous (ring: the previous call's copy
     // may still be pending)
-    if (c->h_tab_cap < tab.size() * 2) {
+    constexpr int kSlots = fwa_b200_ctx::kTabSlots;
+    if (c->h_tab_cap < tab.size() * kSlots) {
         if (c->h_tab) cudaFreeHost(c->h_tab);
         c->h_tab = nullptr;
-        c->h_tab_cap = std::max<size_t>(tab.size() * 2, 64);
+        c->h_tab_cap = std::max<size_t>(tab.size() * kSlots, 64 * kSlots);
         CUDA_OK(cudaMallocHost(&c->h_tab, c->h_tab_cap * 8));
         c->h_tab_slot = 0;
     }
-    CUDA_OK(cudaStreamSynchronize(c->side));  // previous call's PE done (cheap; usually idle)
-    int64_t* h = c->h_tab + (c->h_tab_slot ^= 1) * (c->h_tab_cap / 2);
+    // pinned staging ring: the host only waits when it runs kSlots calls ahead of the copies
+    // (no wait on the side stream: the PE of this call is ordered after every earlier use of
+    // its buffer by the fork event below)
+    c->h_tab_slot = (c->h_tab_slot + 1) % kSlots;
+    int64_t* h = c->h_tab + c->h_tab_slot * (c->h_tab_cap / kSlots);
     CUDA_OK(cudaEventSynchronize(c->ev_tab[c->h_tab_slot]));
     std::copy(tab.begin(), tab.end(), h);
     CUDA_OK(cudaMemcpyAsync(d_tab, h, tab.size() * 8, cudaMemcpyHostToDevice, st));
@@ -1364,8 +1378,7 @@ int fwa_b200_ctx_create(int device, void* stream, fwa_b200_ctx** out) {
         CUDA_OK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
         CUDA_OK(cudaEventCreateWithFlags(&c->ev_copy, cudaEventDisableTiming));
         CUDA_OK(cudaEventCreateWithFlags(&c->ev_feats, cudaEventDisableTiming));
-        CUDA_OK(cudaEventCreateWithFlags(&c->ev_tab[0], cudaEventDisableTiming));
-        CUDA_OK(cudaEventCreateWithFlags(&c->ev_tab[1], cudaEventDisableTiming));
+        for (auto& e : c->ev_tab) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         CUDA_OK(cudaMalloc(&c->d_flag, 2 * sizeof(int)));
         CUDA_OK(cudaMallocHost(&c->h_flag, 2 * sizeof(int)));
         CUDA_OK(cudaMallocHost(&c->h_minmax, 16 * sizeof(long long)));
@@ -1405,8 +1418,10 @@ void fwa_b200_ctx_destroy(fwa_b200_ctx* c) {
     if (c->h_flag) cudaFreeHost(c->h_flag);
     if (c->h_minmax) cudaFreeHost(c->h_minmax);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
-    if (c->g_exec) cudaGraphExecDestroy(c->g_exec);
-    if (c->g_tab) cudaFree(c->g_tab);
+    for (auto& g : c->graphs) {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        if (g.tab) cudaFree(g.tab);
+    }
     if (c->side) {
         cudaStreamSynchronize(c->side);
         cudaStreamDestroy(c->side);
@@ -1598,33 +1613,54 @@ int fwa_b200_backbone_forward_device(fwa_b200_ctx* c, const double* d_coords, co
             forward_device(c, d_coords, d_feats, nullptr, cfg, S, d_out, d_kept, nullptr, nullptr, true);
             return;
         }
-        if (c->g_exec && c->g_key == key) {
-            CUDA_OK(cudaGraphLaunch(c->g_exec, c->stream));
-            c->launches += c->g_launches;
-            return;
-        }
-        if (!(c->g_warm == key)) {  // first sighting: run eagerly (sizes the workspace)
+        ++c->g_clock;
+        for (auto& g : c->graphs)
+            if (g.key == key) {
+                CUDA_OK(cudaGraphLaunch(g.exec, c->stream));
+                c->launches += g.launches;
+                g.used = c->g_clock;
+                return;
+            }
+        auto seen = std::find(c->g_seen.begin(), c->g_seen.end(), key);
+        if (seen == c->g_seen.end()) {  // first sighting: run eagerly (sizes the workspace)
             forward_device(c, d_coords, d_feats, nullptr, cfg, S, d_out, d_kept, nullptr, nullptr, true);
-            c->g_warm = key;
-            c->g_warm.ws_epoch = c->ws_epoch;
+            key.ws_epoch = c->ws_epoch;
+            c->g_seen.push_back(key);
+            if (static_cast<int>(c->g_seen.size()) > fwa_b200_ctx::kGraphs) c->g_seen.erase(c->g_seen.begin());
             return;
         }
-        // second sighting: capture
+        c->g_seen.erase(seen);
+        // second sighting: capture into a free or the least recently used slot
+        fwa_b200_ctx::GraphEntry* e = nullptr;
+        if (static_cast<int>(c->graphs.size()) < fwa_b200_ctx::kGraphs) {
+            c->graphs.emplace_back();
+            e = &c->graphs.back();
+        } else {
+            e = &*std::min_element(c->graphs.begin(), c->graphs.end(),
+                                   [](const auto& x, const auto& y) { return x.used < y.used; });
+            if (e->exec) cudaGraphExecDestroy(e->exec);
+            e->exec = nullptr;
+        }
         const std::vector<int64_t> tab = frame_table(S);
-        if (c->g_tab) cudaFree(c->g_tab);
-        c->g_tab = nullptr;
-        CUDA_OK(cudaMalloc(&c->g_tab, tab.size() * 8));
-        CUDA_OK(cudaMemcpy(c->g_tab, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice));
+        if (e->tab) cudaFree(e->tab);
+        e->tab = nullptr;
+        CUDA_OK(cudaMalloc(&e->tab, tab.size() * 8));
+        CUDA_OK(cudaMemcpy(e->tab, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice));
         CUDA_OK(cudaStreamSynchronize(c->stream));
         const int64_t l0 = c->launches;
         cudaGraph_t graph = nullptr;
+        auto drop_entry = [&] {
+            if (e->tab) cudaFree(e->tab);
+            c->graphs.erase(c->graphs.begin() + (e - c->graphs.data()));
+        };
         CUDA_OK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         try {
-            forward_device(c, d_coords, d_feats, nullptr, cfg, S, d_out, d_kept, c->g_tab, nullptr, true);
+            forward_device(c, d_coords, d_feats, nullptr, cfg, S, d_out, d_kept, e->tab, nullptr, true);
         } catch (...) {
             cudaStreamEndCapture(c->stream, &graph);
             if (graph) cudaGraphDestroy(graph);
             cudaGetLastError();
+            drop_entry();
             c->g_disabled = true;
             throw;
         }
@@ -1633,17 +1669,18 @@ int fwa_b200_backbone_forward_device(fwa_b200_ctx* c, const double* d_coords, co
         if (ec != cudaSuccess || !graph || cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
             if (graph) cudaGraphDestroy(graph);
             cudaGetLastError();
+            drop_entry();
             c->g_disabled = true;  // not capturable here: stay eager
             forward_device(c, d_coords, d_feats, nullptr, cfg, S, d_out, d_kept, nullptr, nullptr, true);
             return;
         }
         cudaGraphDestroy(graph);
-        if (c->g_exec) cudaGraphExecDestroy(c->g_exec);
-        c->g_exec = exec;
-        c->g_launches = c->launches - l0;
-        c->g_key = key;
-        c->g_key.ws_epoch = c->ws_epoch;
-        CUDA_OK(cudaGraphLaunch(c->g_exec, c->stream));
+        e->exec = exec;
+        e->launches = c->launches - l0;
+        e->key = key;
+        e->key.ws_epoch = c->ws_epoch;
+        e->used = c->g_clock;
+        CUDA_OK(cudaGraphLaunch(e->exec, c->stream));
     });
 }
 
