@@ -375,6 +375,31 @@ def test_repeated_calls_bitwise_stable(prec):
             assert np.array_equal(o.kept_indices, r0.kept_indices) and np.array_equal(o.features, r0.features)
 
 
+def test_device_graph_cache_double_buffered(ctx16):
+    """The device-resident forward with two alternating output buffers (a double-buffered
+    frame stream): both keys are captured as graphs and replayed; a third buffer set runs
+    eagerly; every output is bitwise equal to the first eager result."""
+    import torch
+    cfg = F.FwaConfig(n_blocks=4)
+    ctx16.load_params(cfg, F.init_backbone_params(cfg, 42))
+    ps = F.make_pillars(F.SCENES["F10"], 7)
+    n = ps.size()
+    dev = torch.device("cuda", 0)
+    dc = torch.from_numpy(ps.coords).to(dev)
+    df = torch.from_numpy(ps.features.astype(np.float32)).to(dev)
+    outs = [torch.zeros((n, cfg.d_model), dtype=torch.float32, device=dev) for _ in range(3)]
+    ref = None
+    for i in range(9):
+        o = outs[2] if i == 7 else outs[i % 2]
+        o.zero_()
+        nk = ctx16.forward_device(dc.data_ptr(), df.data_ptr(), [0, n], cfg, o.data_ptr())
+        ctx16.sync_check()
+        got = o[:nk].cpu().numpy()
+        if ref is None:
+            ref = got
+        assert np.array_equal(got, ref), i
+
+
 def test_errors_mirror_reference(ctx32):
     cfg = F.FwaConfig(d_model=16, n_heads=4, d_ff=32, group_size=8, n_blocks=2)
     blob = F.init_backbone_params(cfg, 1)
