@@ -63,7 +63,20 @@ using namespace tc;
 
 namespace {
 
-constexpr int kThreads = 512;
+// FWA_THREADS / 32 warps: 4 TMEM lane quarters x kColWarps column slices.  (A separate
+// MMA-issue warp or warpgroup costs the compute warps registers: 17 warps put 5 on one SM
+// sub-partition, so ptxas caps every thread at 96 registers, and it does not budget by
+// setmaxnreg -- both spill heavily; thread 0 of rank 0 issues the pair's MMAs.)
+#ifndef FWA_THREADS
+#define FWA_THREADS 512
+#endif
+constexpr int kThreads = FWA_THREADS;
+constexpr int kWarps = kThreads / 32;
+constexpr int kColWarps = kWarps / 4;     // warps per TMEM lane quarter
+constexpr int kCols = 128 / kColWarps;    // channels per thread in the row-per-lane phases
+constexpr int kRowsPass = kThreads / 8;   // rows per pass of the 8-lanes-per-row phases
+constexpr int kPasses = 128 / kRowsPass;  // 2 (512 threads) or 1 (1024)
+static_assert(kThreads == 512 || kThreads == 1024, "16 or 32 warps");
 constexpr int kMaxPeers = 8;
 // kernel modes (template): the plain block; + per-phase SM-clock counters (StageTimes of the
 // host API); + rank-tagged output rows (the peer-memory split).  Kept as separate instances:
@@ -173,6 +186,29 @@ FWA_DEVINL void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
           "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
         : "r"(taddr));
 }
+template <int N>
+FWA_DEVINL void tmem_ldN(uint32_t taddr, uint32_t (&v)[N]) {
+    if constexpr (N == 32) tmem_ld32(taddr, v);
+    else tmem_ld16(taddr, v);
+}
+// the sum of this lane's N (4 or 8) consecutive TMEM columns (row-statistics exchange), pairwise
+template <int N>
+FWA_DEVINL float tmem_sum_cols(uint32_t taddr) {
+    uint32_t v[8];
+    if constexpr (N == 4)
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                     : "r"(taddr));
+    else
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                       "=r"(v[7])
+                     : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    const float a = (__uint_as_float(v[0]) + __uint_as_float(v[1])) + (__uint_as_float(v[2]) + __uint_as_float(v[3]));
+    if constexpr (N == 4) return a;
+    else return a + ((__uint_as_float(v[4]) + __uint_as_float(v[5])) + (__uint_as_float(v[6]) + __uint_as_float(v[7])));
+}
 FWA_DEVINL void tmem_st1(uint32_t taddr, float v) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(__float_as_uint(v))
                  : "memory");
@@ -188,6 +224,20 @@ FWA_DEVINL void tmem_st32(uint32_t taddr, const float (&v)[32]) {
         "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
         : "memory");
 }
+FWA_DEVINL void tmem_st16(uint32_t taddr, const float* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]),
+        "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])
+        : "memory");
+}
+// N = 16 or 32 consecutive columns of this thread's TMEM lane
+template <int N>
+FWA_DEVINL void tmem_stN(uint32_t taddr, const float (&v)[N]) {
+    if constexpr (N == 32) tmem_st32(taddr, v);
+    else tmem_st16(taddr, v);
+}
 FWA_DEVINL void tmem_st8(uint32_t taddr, float4 a, float4 b) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "f"(a.x),
                  "f"(a.y), "f"(a.z), "f"(a.w), "f"(b.x), "f"(b.y), "f"(b.z), "f"(b.w)
@@ -198,7 +248,7 @@ FWA_DEVINL void tmem_st8(uint32_t taddr, float4 a, float4 b) {
 template <int N>
 FWA_DEVINL void tmem_bias_row(uint32_t taddr, const float* v) {
 #pragma unroll
-    for (int j = 0; j < N; j += 32) {
+    for (int j = 0; j + 32 <= N; j += 32) {
         float w[32];
 #pragma unroll
         for (int k = 0; k < 32; k += 4) {
@@ -206,6 +256,15 @@ FWA_DEVINL void tmem_bias_row(uint32_t taddr, const float* v) {
             w[k] = f.x; w[k + 1] = f.y; w[k + 2] = f.z; w[k + 3] = f.w;
         }
         tmem_st32(taddr + j, w);
+    }
+    if constexpr (N % 32 == 16) {
+        float w[16];
+#pragma unroll
+        for (int k = 0; k < 16; k += 4) {
+            const float4 f = *reinterpret_cast<const float4*>(v + N - 16 + k);
+            w[k] = f.x; w[k + 1] = f.y; w[k + 2] = f.z; w[k + 3] = f.w;
+        }
+        tmem_st16(taddr + N - 16, w);
     }
 }
 FWA_DEVINL void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
@@ -753,7 +812,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
     const int q = warp & 3, cq = warp >> 2;
     const int row = q * 32 + lane;  // local row == TMEM lane
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
-    const int c0 = cq * 32;
+    const int c0 = cq * kCols;
     uint8_t* sW = smem;
     uint8_t* pRA = smem + kOffRA;
     uint8_t* pKV = smem + kOffKV;
@@ -846,8 +905,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         const int sp = a.split < ur ? a.split : ur;
         const int r0 = rank ? sp : 0, nl = rank ? ur - sp : sp;
 #pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
-            const int r = hf * 64 + warp * 4 + (lane >> 3);
+        for (int hf = 0; hf < kPasses; ++hf) {
+            const int r = hf * kRowsPass + warp * 4 + (lane >> 3);
             if (r < nl) ids[hf] = idx ? idx[ub + r0 + r] : static_cast<int>(ub + r0 + r);
         }
     };
@@ -862,6 +921,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         if constexpr (!kF64) {
             if (u >= a.n_units) return;
 #if FWA_X_TMA
+            static_assert(kThreads == 512, "the gather4 path is written for 16 warps");
             // lanes 0, 8, 16, 24 hold the ids of rows warp*4 + 0..3 (ids[0]) and 64 + warp*4 + 0..3
             // (ids[1]); rows past the CTA's are id 0 (any valid row: never stored).  Lane
             // hf*4 + cb issues the gather4 of half hf, column block cb: 8 TMA per warp, 64 KB per CTA
@@ -884,8 +944,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
             const int nl = rank ? ur - sp : sp;
             const int sub = lane & 7;
 #pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-                const int r = hf * 64 + warp * 4 + (lane >> 3);
+            for (int hf = 0; hf < kPasses; ++hf) {
+                const int r = hf * kRowsPass + warp * 4 + (lane >> 3);
                 const float* src = a.x + static_cast<int64_t>(ids[hf]) * 128 + 4 * sub;
                 const uint32_t nb = r < nl ? 16u : 0u;
 #pragma unroll
@@ -907,13 +967,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
     // every warp stages its rows into the K/V region (free until this unit's epilogue, clear
     // of the rows the peer's halo push may be landing in), warp 0 -- which holds the MMA
     // issuer in rank 0 -- only arrives on named barrier 1, warps 1..15 store the 512 B rows.
-    float x1[32];
+    float x1[kCols];
     int pnloc = 0;
     bool pend = false;
     auto stage_out = [&](uint8_t* stg) {
         if (row < pnloc)
 #pragma unroll
-            for (int j = 0; j < 32; j += 4)
+            for (int j = 0; j < kCols; j += 4)
                 *reinterpret_cast<float4*>(stg + stage_off(row, (c0 + j) >> 2)) =
                     make_float4(x1[j], x1[j + 1], x1[j + 2], x1[j + 3]);
     };
@@ -953,7 +1013,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
             if (lane == 16) sTab[16].x = n;
         }
     };
-    tmem_bias_row<96>(tmem + lane_off + 96 * cq, sVec + 96 * cq);  // the first unit's QKV bias
+    tmem_bias_row<384 / kColWarps>(tmem + lane_off + (384 / kColWarps) * cq, sVec + (384 / kColWarps) * cq);  // the first unit's QKV bias
     tmem_st_wait();
     // phase clock sums live in the barrier block's spare slots (thread 0 only: no registers)
     unsigned long long* ph_acc = reinterpret_cast<unsigned long long*>(smem + kOffTab + 384);  // [4] sums, [4] last stamp
@@ -987,10 +1047,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         //         at a time); the out-proj MMA accumulates onto them (= the residual).
         if constexpr (!kF64) {
             const int sub = lane & 7, rl = lane >> 3;
-            uint2 pe[2][4];
+            uint2 pe[2][4];  // [kPasses] used
 #pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-                const int r = hf * 64 + warp * 4 + rl;
+            for (int hf = 0; hf < kPasses; ++hf) {
+                const int r = hf * kRowsPass + warp * 4 + rl;
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
                     pe[hf][i] = r < nloc ? __ldg(reinterpret_cast<const uint2*>(a.pe16 + static_cast<int64_t>(gid[hf]) * 128 +
@@ -1010,7 +1070,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
             cp_async_wait_all();
             __syncthreads();  // every thread's row chunks landed
 #endif
-            {
+            if constexpr (kPasses == 2) {
                 float v[2][16];
                 const int rr[2] = {warp * 4 + rl, 64 + warp * 4 + rl};
                 const bool vv[2] = {rr[0] < nloc, rr[1] < nloc};
@@ -1022,25 +1082,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
                         v[hf][4 * i] = f.x; v[hf][4 * i + 1] = f.y; v[hf][4 * i + 2] = f.z; v[hf][4 * i + 3] = f.w;
                     }
                 ln1_rows2_to_image(v, pe, vv, rr, sub, sVec + 896, pRA, bad);
-                FTR(tb + 1);
-            }
-            {  // the residual rows -> TMEM [384, 512)
-                float xr[32];
+            } else {
+                float v[16];
+                const int r = warp * 4 + rl;
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const float4 f = *reinterpret_cast<const float4*>(xs + xs_off(row, 8 * cq + j));
+                for (int i = 0; i < 4; ++i) {
+                    const float4 f = *reinterpret_cast<const float4*>(xs + xs_off(r, 8 * i + sub));
+                    v[4 * i] = f.x; v[4 * i + 1] = f.y; v[4 * i + 2] = f.z; v[4 * i + 3] = f.w;
+                }
+                ln1_row_to_image(v, pe[0], r < nloc, r, sub, sVec + 896, pRA, bad);
+            }
+            FTR(tb + 1);
+            {  // the residual rows -> TMEM [384, 512)
+                float xr[kCols];
+#pragma unroll
+                for (int j = 0; j < kCols / 4; ++j) {
+                    const float4 f = *reinterpret_cast<const float4*>(xs + xs_off(row, (c0 >> 2) + j));
                     const float4 bo = *reinterpret_cast<const float4*>(sVec + 384 + c0 + 4 * j);
                     xr[4 * j] = f.x + bo.x; xr[4 * j + 1] = f.y + bo.y; xr[4 * j + 2] = f.z + bo.z; xr[4 * j + 3] = f.w + bo.w;
                 }
-                tmem_st32(tmem + lane_off + 384 + c0, xr);  // x + b_out: the out-proj accumulates onto it
+                tmem_stN<kCols>(tmem + lane_off + 384 + c0, xr);  // x + b_out: the out-proj accumulates onto it
             }
         } else {
             const int sub = lane & 7, rl = lane >> 3;
-            float v[2][16];
-            uint2 pe[2][4];
+            float v[kPasses][16];
+            uint2 pe[kPasses][4];
 #pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-                const int r = hf * 64 + warp * 4 + rl;
+            for (int hf = 0; hf < kPasses; ++hf) {
+                const int r = hf * kRowsPass + warp * 4 + rl;
                 load_row_quads<kF64>(a.x, a.x64, a.pe16, gid[hf], sub, r < nloc, v[hf], pe[hf]);
             }
             // this unit's scatter ids (== the gather ids except in the last block), then the
@@ -1053,25 +1122,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
             }
             unit_ids(a.ridx, u + npairs, gid);
 #pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-                const int r = hf * 64 + warp * 4 + rl;
+            for (int hf = 0; hf < kPasses; ++hf) {
+                const int r = hf * kRowsPass + warp * 4 + rl;
                 ln1_row_to_image(v[hf], pe[hf], r < nloc, r, sub, sVec + 896, pRA, bad);
-                if (hf == 0) FTR(tb + 1);
+            }
+            FTR(tb + 1);
+            // the f32 rows to TMEM through a 64-row staging in R_X, one half of the rows at a time
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    *reinterpret_cast<float4*>(pRX + stage_off(r & 63, 8 * i + sub)) =
-                        make_float4(v[hf][4 * i], v[hf][4 * i + 1], v[hf][4 * i + 2], v[hf][4 * i + 3]);
+            for (int half = 0; half < 2; ++half) {
+#pragma unroll
+                for (int hf = 0; hf < kPasses; ++hf) {
+                    const int r = hf * kRowsPass + warp * 4 + rl;
+                    if ((r >> 6) == half)
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            *reinterpret_cast<float4*>(pRX + stage_off(r & 63, 8 * i + sub)) =
+                                make_float4(v[hf][4 * i], v[hf][4 * i + 1], v[hf][4 * i + 2], v[hf][4 * i + 3]);
+                }
                 __syncthreads();
-                if ((row >> 6) == hf) {
-                    float xr[32];
+                if ((row >> 6) == half) {
+                    float xr[kCols];
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const float4 f = *reinterpret_cast<const float4*>(pRX + stage_off(row & 63, 8 * cq + j));
+                    for (int j = 0; j < kCols / 4; ++j) {
+                        const float4 f = *reinterpret_cast<const float4*>(pRX + stage_off(row & 63, (c0 >> 2) + j));
                         const float4 bo = *reinterpret_cast<const float4*>(sVec + 384 + c0 + 4 * j);
                         xr[4 * j] = f.x + bo.x; xr[4 * j + 1] = f.y + bo.y; xr[4 * j + 2] = f.z + bo.z;
                         xr[4 * j + 3] = f.w + bo.w;
                     }
-                    tmem_st32(tmem + lane_off + 384 + c0, xr);  // x + b_out
+                    tmem_stN<kCols>(tmem + lane_off + 384 + c0, xr);  // x + b_out
                     tmem_st_wait();
                 }
                 __syncthreads();
@@ -1105,7 +1183,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         ++hs;
         if (pend && warp != 0) {
             bar1_sync(kThreads);
-            store_out(stg, 1, 15);
+            store_out(stg, 1, kWarps - 1);
         }
         // ---- 2. QKV epilogue (all 8 heads) + attention
         // the attention m-tile table, built while the QKV MMA runs; read after the
@@ -1127,13 +1205,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
             mbar_wait(part ? bV : bK, ph);
             fence_after_sync();
             if (part == 0) FTR(tb + 3);
-            uint32_t kv[2][16];
-            tmem_ld16(tmem + lane_off + 128 + 128 * part + 32 * cq, kv[0]);
-            tmem_ld16(tmem + lane_off + 128 + 128 * part + 32 * cq + 16, kv[1]);
+            constexpr int kHeadsT = 8 / kColWarps;  // heads per thread (2 or 1)
+            uint32_t kv[kHeadsT][16];
+#pragma unroll
+            for (int hh = 0; hh < kHeadsT; ++hh)
+                tmem_ld16(tmem + lane_off + 128 + 128 * part + 16 * (kHeadsT * cq + hh), kv[hh]);
             tmem_ld_wait();
 #pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                const int h = 2 * cq + hh;
+            for (int hh = 0; hh < kHeadsT; ++hh) {
+                const int h = kHeadsT * cq + hh;
                 uint4 X[2];
 #pragma unroll
                 for (int hf = 0; hf < 2; ++hf) {
@@ -1159,13 +1239,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         mbar_wait(bQKV, ph);
         fence_after_sync();
         {
-            uint32_t qv[2][16];
-            tmem_ld16(tmem + lane_off + 32 * cq, qv[0]);
-            tmem_ld16(tmem + lane_off + 32 * cq + 16, qv[1]);
+            constexpr int kHeadsT = 8 / kColWarps;
+            uint32_t qv[kHeadsT][16];
+#pragma unroll
+            for (int hh = 0; hh < kHeadsT; ++hh) tmem_ld16(tmem + lane_off + 16 * (kHeadsT * cq + hh), qv[hh]);
             tmem_ld_wait();
 #pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                const int h = 2 * cq + hh;
+            for (int hh = 0; hh < kHeadsT; ++hh) {
+                const int h = kHeadsT * cq + hh;
 #pragma unroll
                 for (int hf = 0; hf < 2; ++hf) {
                     uint32_t o[4];
@@ -1186,20 +1267,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
             // narrows it (tests force the shifted path)
             const float hi = fminf(a.lmax, 4096.0f), lo = fmaxf(1.0f / a.lmax, 0.015625f);
 #ifndef FWA_ATTN_NK
-#define FWA_ATTN_NK 2
+#define FWA_ATTN_NK (FWA_THREADS == 512 ? 2 : 1)
 #endif
             // tasks t, t + 16, ... of this warp together (the same head, FWA_ATTN_NK m-tiles)
             constexpr int NKW = FWA_ATTN_NK;
 #pragma unroll 1
-            for (int t = warp; t < ntasks; t += 16 * NKW) {
+            for (int t = warp; t < ntasks; t += kWarps * NKW) {
                 int4 ee[NKW];
                 int hd[NKW];
                 bool need_halo = false;
                 int nk = 0;
 #pragma unroll
                 for (int k = 0; k < NKW; ++k) {
-                    const int tk = t + 16 * k < ntasks ? t + 16 * k : t;
-                    nk += t + 16 * k < ntasks;
+                    const int tk = t + kWarps * k < ntasks ? t + kWarps * k : t;
+                    nk += t + kWarps * k < ntasks;
                     ee[k] = sTab[tk >> 3];
                     hd[k] = tk & 7;
                     need_halo |= ee[k].w != 0;
@@ -1246,39 +1327,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         ++hs;
         // while the out-proj MMAs run: the FFN1 accumulators start at b1' (LN2's beta folded
         // in) -- this row, columns [128 + 64 cq, +64), which the QKV epilogue drained
-        tmem_bias_row<64>(tmem + lane_off + 128 + 64 * cq, sVec + 640 + 64 * cq);
+        tmem_bias_row<256 / kColWarps>(tmem + lane_off + 128 + (256 / kColWarps) * cq, sVec + 640 + (256 / kColWarps) * cq);
         tmem_st_wait();
         mbar_wait(bP, ph);
         fence_after_sync();
         FTR(tb + 8);
         FPH(1);
         {
-            uint32_t v[32];
-            tmem_ld32(tmem + lane_off + 384 + c0, v);  // x + P (the MMA accumulated onto x)
+            uint32_t v[kCols];
+            tmem_ldN<kCols>(tmem + lane_off + 384 + c0, v);  // x + P (the MMA accumulated onto x)
             tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 32; ++j) x1[j] = __uint_as_float(v[j]);  // (x + b_out) + P
+            for (int j = 0; j < kCols; ++j) x1[j] = __uint_as_float(v[j]);  // (x + b_out) + P
         }
         // ---- 4. LN2 (affine folded into W1 / b1) -> R_A
         {
             float sm = 0.f;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) sm += x1[j];
+            for (int j = 0; j < kCols; ++j) sm += x1[j];
             tmem_st1(tmem + lane_off + cq, sm);
             tmem_st_wait();
             cta_sync_tc();
-            float4 ps = tmem_ld4(tmem + lane_off);
-            const float mean = ((ps.x + ps.y) + (ps.z + ps.w)) * (1.0f / 128.0f);
+            const float mean = tmem_sum_cols<kColWarps>(tmem + lane_off) * (1.0f / 128.0f);
             float v2 = 0.f;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v2 += (x1[j] - mean) * (x1[j] - mean);
-            tmem_st1(tmem + lane_off + 4 + cq, v2);
+            for (int j = 0; j < kCols; ++j) v2 += (x1[j] - mean) * (x1[j] - mean);
+            tmem_st1(tmem + lane_off + kColWarps + cq, v2);
             tmem_st_wait();
             cta_sync_tc();
-            ps = tmem_ld4(tmem + lane_off + 4);
-            const float inv = rsqrtf(((ps.x + ps.y) + (ps.z + ps.w)) * (1.0f / 128.0f) + 1e-5f);
+            const float inv = rsqrtf(tmem_sum_cols<kColWarps>(tmem + lane_off + kColWarps) * (1.0f / 128.0f) + 1e-5f);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < kCols / 8; ++j) {
                 uint32_t o[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
@@ -1310,11 +1389,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
             fence_after_sync();
             FTR(tb + 10 + 2 * hh);
             uint8_t* act = hh ? pRA : pRX;
-            uint32_t v[32];
-            tmem_ld32(tmem + lane_off + 128 + 128 * hh + c0, v);
+            uint32_t v[kCols];
+            tmem_ldN<kCols>(tmem + lane_off + 128 + 128 * hh + c0, v);
             tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < kCols / 8; ++j) {
                 uint32_t o[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e)  // the accumulators started at b1'
@@ -1339,7 +1418,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         // the NEXT unit's QKV accumulators start at the bias (b_qkv, LN1's beta folded in): this
         // thread's row, columns [96 cq, 96 cq + 96).  [0, 384) is free: the handshake above
         // retired every GELU read of U, and FFN2 accumulates onto [384, 512)
-        tmem_bias_row<96>(tmem + lane_off + 96 * cq, sVec + 96 * cq);
+        tmem_bias_row<384 / kColWarps>(tmem + lane_off + (384 / kColWarps) * cq, sVec + (384 / kColWarps) * cq);
         tmem_st_wait();
         // ---- 6. out = x1 + (O + b2) -> staged in R_A (two 64-row halves) -> row scatter
         mbar_wait(bO, ph);
@@ -1348,16 +1427,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         FTR(tb + 14);
         FPH(2);
         {
-            uint32_t v[32];
-            tmem_ld32(tmem + lane_off + 384 + c0, v);  // x1 + O (FFN2 accumulated onto the residual)
+            uint32_t v[kCols];
+            tmem_ldN<kCols>(tmem + lane_off + 384 + c0, v);  // x1 + O (FFN2 accumulated onto the residual)
             tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 32; ++j) x1[j] = __uint_as_float(v[j]) + sVec[512 + c0 + j];
+            for (int j = 0; j < kCols; ++j) x1[j] = __uint_as_float(v[j]) + sVec[512 + c0 + j];
         }
 // this unit's output is written during the next unit's QKV MMA (or after the loop)
         if ((lane & 7) == 0) {
-            sRowId[warp * 4 + (lane >> 3)] = sid[0];
-            sRowId[64 + warp * 4 + (lane >> 3)] = sid[1];
+#pragma unroll
+            for (int hf = 0; hf < kPasses; ++hf) sRowId[hf * kRowsPass + warp * 4 + (lane >> 3)] = sid[hf];
         }
         pnloc = nloc;
         pend = true;
@@ -1368,7 +1447,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
         __syncthreads();  // the row ids
         stage_out(pKV);
         __syncthreads();
-        store_out(pKV, 0, 16);
+        store_out(pKV, 0, kWarps);
         __syncthreads();
         FPH(3);
     }
