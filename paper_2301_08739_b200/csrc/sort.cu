@@ -303,42 +303,47 @@ void launch_bins_hist(const long long* win, int64_t ntot, int n_specs, const int
 // atomic per touched slot (the rare farther frame goes straight to global)
 __global__ void __launch_bounds__(256) k_frame_minmax(const long long* __restrict__ win, int64_t ntot,
                                                       const int64_t* __restrict__ frame_off, int n_frames,
-                                                      long long* __restrict__ mm) {
+                                                      long long* __restrict__ mm, int64_t chunk) {
+    // each CTA reduces a contiguous chunk of pillars (few frames) into 8 shared-memory slots
+    // (frames f0 .. f0 + 7 from its first), then one global atomic per touched slot value;
+    // a warp whose lanes share a frame reduces by shuffles first
     const int s = blockIdx.y;
     __shared__ long long sm[8][4];
     __shared__ int f0;
-    const int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x;
+    const int64_t c0 = static_cast<int64_t>(blockIdx.x) * chunk;
+    const int64_t c1 = c0 + chunk < ntot ? c0 + chunk : ntot;
     if (threadIdx.x < 32) sm[threadIdx.x >> 2][threadIdx.x & 3] = (threadIdx.x & 1) ? LLONG_MIN : LLONG_MAX;
-    if (threadIdx.x == 0) f0 = n_frames > 1 ? frame_of(frame_off, n_frames, base) : 0;
+    if (threadIdx.x == 0) f0 = n_frames > 1 && c0 < ntot ? frame_of(frame_off, n_frames, c0) : 0;
     __syncthreads();
-    const int64_t i = base + threadIdx.x;
-    const bool in = i < ntot;
-    longlong2 w = make_longlong2(0, 0);
-    int f = -1;
-    if (in) {
-        w = reinterpret_cast<const longlong2*>(win)[static_cast<int64_t>(s) * ntot + i];
-        f = n_frames > 1 ? frame_of(frame_off, n_frames, i) : 0;
-    }
-    // consecutive pillars mostly share a frame: a warp whose lanes all do reduces first and
-    // lane 0 alone updates the slot
-    const int f_lane0 = __shfl_sync(0xffffffffu, f, 0);
-    if (__all_sync(0xffffffffu, in && f == f_lane0)) {
-        const long long a0 = wmin(w.x), a1 = wmax(w.x), a2 = wmin(w.y), a3 = wmax(w.y);
-        if ((threadIdx.x & 31) == 0) {
-            const int k = f - f0;
-            long long* m = k < 8 ? sm[k] : mm + (static_cast<int64_t>(s) * n_frames + f) * 4;
-            atomicMin(m, a0);
-            atomicMax(m + 1, a1);
-            atomicMin(m + 2, a2);
-            atomicMax(m + 3, a3);
+    int f = f0;
+    for (int64_t t0 = c0; t0 < c1; t0 += blockDim.x) {
+        const int64_t i = t0 + threadIdx.x;
+        const bool in = i < c1;
+        longlong2 w = make_longlong2(0, 0);
+        if (in) {
+            w = reinterpret_cast<const longlong2*>(win)[static_cast<int64_t>(s) * ntot + i];
+            while (f + 1 < n_frames && frame_off[f + 1] <= i) ++f;
         }
-    } else if (in) {
-        const int k = f - f0;
-        long long* m = k < 8 ? sm[k] : mm + (static_cast<int64_t>(s) * n_frames + f) * 4;
-        atomicMin(m, w.x);
-        atomicMax(m + 1, w.x);
-        atomicMin(m + 2, w.y);
-        atomicMax(m + 3, w.y);
+        const int fl = in ? f : -1;
+        const int f_lane0 = __shfl_sync(0xffffffffu, fl, 0);
+        if (__all_sync(0xffffffffu, in && fl == f_lane0)) {
+            const long long a0 = wmin(w.x), a1 = wmax(w.x), a2 = wmin(w.y), a3 = wmax(w.y);
+            if ((threadIdx.x & 31) == 0) {
+                const int k = fl - f0;
+                long long* m = k < 8 ? sm[k] : mm + (static_cast<int64_t>(s) * n_frames + fl) * 4;
+                atomicMin(m, a0);
+                atomicMax(m + 1, a1);
+                atomicMin(m + 2, a2);
+                atomicMax(m + 3, a3);
+            }
+        } else if (in) {
+            const int k = fl - f0;
+            long long* m = k < 8 ? sm[k] : mm + (static_cast<int64_t>(s) * n_frames + fl) * 4;
+            atomicMin(m, w.x);
+            atomicMax(m + 1, w.x);
+            atomicMin(m + 2, w.y);
+            atomicMax(m + 3, w.y);
+        }
     }
     __syncthreads();
     if (threadIdx.x < 32) {
@@ -355,8 +360,11 @@ __global__ void __launch_bounds__(256) k_frame_minmax(const long long* __restric
 void launch_frame_minmax(const long long* win, int64_t ntot, int n_specs, const int64_t* d_frame_off, int n_frames,
                          long long* mm, cudaStream_t s, int64_t* launches) {
     k_init_minmax<<<(4 * n_specs * n_frames + 255) / 256, 256, 0, s>>>(mm, 4 * n_specs * n_frames);
-    dim3 grid(static_cast<unsigned>((ntot + 255) / 256), static_cast<unsigned>(n_specs));
-    k_frame_minmax<<<grid, 256, 0, s>>>(win, ntot, d_frame_off, n_frames, mm);
+    const int64_t tiles = (ntot + 255) / 256;
+    const int64_t ctas = tiles < 2 * kNumSMs ? tiles : 2 * kNumSMs;  // per spec
+    const int64_t chunk = ((ntot + ctas - 1) / ctas + 255) / 256 * 256;
+    dim3 grid(static_cast<unsigned>((ntot + chunk - 1) / chunk), static_cast<unsigned>(n_specs));
+    k_frame_minmax<<<grid, 256, 0, s>>>(win, ntot, d_frame_off, n_frames, mm, chunk);
     *launches += 2;
 }
 
@@ -802,6 +810,27 @@ FWA_DEVINL int count_less(const int32_t* a, int n, int32_t v) {
     return lo;
 }
 
+// the same by one warp: each round the 32 lanes probe 32 evenly spaced elements of the
+// remaining range and narrow it to one slot (3 dependent loads for n <= 32^3)
+FWA_DEVINL int warp_count_less(const int32_t* a, int n, int32_t v) {
+    const int lane = threadIdx.x & 31;
+    int lo = 0, hi = n;  // answer in [lo, hi]
+    while (hi - lo > 32) {
+        const int step = (hi - lo + 31) / 32;
+        const int idx = lo + lane * step;
+        const bool less = idx < hi && a[idx] < v;
+        const unsigned m = __ballot_sync(0xffffffffu, less);
+        const int k = 32 - __clz(m);  // probes 0..k-1 are < v (a is sorted)
+        const int nlo = k ? lo + (k - 1) * step + 1 : lo;
+        const int nhi = lo + k * step < hi ? lo + k * step : hi;
+        lo = nlo;
+        hi = nhi;
+    }
+    const int idx = lo + lane;
+    const unsigned m = __ballot_sync(0xffffffffu, idx < hi && a[idx] < v);
+    return lo + __popc(m);
+}
+
 // One CTA: sort the dropped ids, then (per spec) the positions of those ids in the
 // spec's full-set plan (inv[s][id]).  Rank sort for n <= blockDim.x, else a bitonic sort
 // in shared memory, n <= kMaxDrop.
@@ -885,9 +914,15 @@ __global__ void __launch_bounds__(256) k_compact_all(const int32_t* __restrict__
     const int64_t base = plan ? static_cast<int64_t>(s) * ntot : 0;  // drop_pos holds stacked plan indices
     const int32_t* dl = plan ? drop_pos + static_cast<int64_t>(s) * (n_drop > 0 ? n_drop : 1) : drop_sorted;
     __shared__ int s_lo, s_f0;
-    if (threadIdx.x == 0) {
-        s_lo = n_drop > 0 ? count_less(dl, n_drop, static_cast<int32_t>(base + j0)) : 0;
-        s_f0 = plan && s == s_last && n_frames > 1 ? frame_of(frame_off, n_frames, j0 < ntot ? j0 : ntot - 1) : 0;
+    if (threadIdx.x < 32) {  // warp 0: 32-way searches (a few dependent loads, not log2 n)
+        if (n_drop > 0) {
+            const int lo = warp_count_less(dl, n_drop, static_cast<int32_t>(base + j0));
+            if (threadIdx.x == 0) s_lo = lo;
+        } else if (threadIdx.x == 0) {
+            s_lo = 0;
+        }
+        if (threadIdx.x == 0)
+            s_f0 = plan && s == s_last && n_frames > 1 ? frame_of(frame_off, n_frames, j0 < ntot ? j0 : ntot - 1) : 0;
     }
     __syncthreads();
     if (j >= ntot) return;
