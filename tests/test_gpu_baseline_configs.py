@@ -152,3 +152,25 @@ def test_config4_f250_split(f250, world, exchange):
     err = O.max_rel_err(got, want["features"])
     print(f"\n[parity] config 4 F250 split world {world} {exchange} (bf16): {err:.3e}")
     assert err <= TOL_BF16, err
+
+
+@pytest.mark.parametrize("G", [32, 48, 96, 128])
+def test_config5_group_sizes_f30(G):
+    """BASELINE config 5's group-size axis at full frame size: the F30 frame (30,212 pillars),
+    8 blocks, G = 32 / 48 / 96 / 128 -- each a compile-time instance of the fused block
+    kernel -- against the compiled reference: integer schedule bit-exact, bf16 features within
+    1e-2."""
+    coords, feats = O.ref_make_pillars(_scene_dict(F.SCENES["F30"]), 42)
+    rcfg = O.make_cfg(group_size=G)
+    blob = O.ref_init_params(rcfg, 128, 42)
+    want = O.ref_run_backbone(coords, feats, rcfg, blob, n_threads=THREADS)
+    cfg = F.FwaConfig(group_size=G)
+    ctx = F.Context(0, precision="bf16")
+    assert ctx.fast_path(cfg)
+    ctx.load_params(cfg, blob)
+    r = ctx.run_backbone(F.PillarSet(coords, feats), cfg)
+    _ints(r.kept_indices, np.concatenate(r.dropped_indices), r.stats.dropped_per_block,
+          (r.stats.cache.computed, r.stats.cache.hits), want)
+    err = O.max_rel_err(r.features, want["features"])
+    print(f"\n[parity] config 5 F30 G {G} 8 blocks bf16: normwise max rel err {err:.3e}")
+    assert err <= TOL_BF16, err
