@@ -860,15 +860,30 @@ def run_split_scene(args, F, ctx, cfg, dev, stream, rank, world, dist, flush):
     runner = DeviceRunner(ctx, d_coords, d_feats, cfg, same_stream=True,
                           exchange_handles=exchange_handles if (dist and exchange == "p2p") else None)
 
+    def agree(ok):  # every rank's verdict on its peer mappings
+        if not dist:
+            return ok
+        v = torch.tensor([1.0 if ok else 0.0], device=dev)
+        dist.all_reduce(v, op=dist.ReduceOp.MIN)
+        return v.item() >= 1.0
+
     def one():
         if exchange == "p2p":
-            return split_forward_p2p(runner, cfg.n_blocks, cfg.group_size, world, rank, barrier)
+            return split_forward_p2p(runner, cfg.n_blocks, cfg.group_size, world, rank, barrier, agree)
         if exchange == "a2a":
             return split_forward_a2a(runner, cfg.n_blocks, cfg.group_size, world, rank, all_gather, all_to_all,
                                      alloc)
         return split_forward(runner, cfg.n_blocks, cfg.group_size, world, rank, all_gather, alloc)
 
     steps = max(3, args.steps // 5)
+    if exchange == "p2p" and dist:
+        try:  # the peer mappings (made once); a failure on any rank switches every rank to NCCL
+            one()
+        except RuntimeError:
+            torch.cuda.synchronize()
+            runner.close()
+            exchange = "a2a"
+            runner = DeviceRunner(ctx, d_coords, d_feats, cfg, same_stream=True)
     try:
         for _ in range(2):
             one()

@@ -23,7 +23,7 @@ runs on the GPU (`DeviceRunner`, the C ABI) and in the CPU gloo tests (an oracle
 from __future__ import annotations
 
 import math
-from typing import Callable, List, Tuple
+from typing import Callable, Optional, List, Tuple
 
 import numpy as np
 
@@ -138,12 +138,14 @@ def p2p_dest_rows(idx_b, idx_next, out_pos, ranges, per, group_size, rank, last)
     return ((pos[pid] // (per * group_size)) << 28) | pid
 
 
-def split_forward_p2p(runner, n_blocks: int, group_size: int, world: int, rank: int, barrier: Callable):
+def split_forward_p2p(runner, n_blocks: int, group_size: int, world: int, rank: int, barrier: Callable,
+                      agree: Optional[Callable] = None):
     """runner: begin() -> K; p2p_setup(world, rank) (peer pointers + tables); input();
     x_buffer(); block_p2p(b, x); out_buffer().  barrier(): orders every rank's block b before
-    any rank's block b+1 (stream-ordered).  Returns the output buffer (complete on rank 0)."""
+    any rank's block b+1 (stream-ordered).  agree: see DeviceRunner.p2p_setup.  Returns the
+    output buffer (complete on rank 0)."""
     runner.begin()
-    runner.p2p_setup(world, rank)
+    runner.p2p_setup(world, rank, agree) if agree is not None else runner.p2p_setup(world, rank)
     x = runner.input()
     for b in range(n_blocks):
         runner.block_p2p(b, x)
@@ -229,10 +231,17 @@ class DeviceRunner:
             self.ctx.sync_check()  # the library's stream -> torch's (collectives, index ops)
 
     # ---- peer-memory exchange (split_forward_p2p)
-    def p2p_setup(self, world, rank):
+    def p2p_setup(self, world, rank, agree=None):
         """Peer pointers: this rank's own buffers alone, or -- with `exchange_handles`
         (rank-ordered all-gather of bytes objects, e.g. dist.all_gather_object) -- CUDA IPC
-        mappings of every rank's cudaMalloc'd x and output buffers."""
+        mappings of every rank's cudaMalloc'd x and output buffers.  The mappings are made
+        once per runner (the buffers do not move).  agree(ok) -> bool: every rank's verdict
+        on its mappings (e.g. an all-reduce MIN), so a failure raises on ALL ranks alike
+        instead of leaving the others waiting in the first inter-block barrier."""
+        key = (world, rank, self.x.data_ptr(), self.out.data_ptr())
+        if getattr(self, "_p2p_key", None) == key:
+            self.ctx.split_p2p_setup(world, rank, self._p2p_xs, self._p2p_outs)
+            return
         if world == 1:
             xs, outs = [self.x.data_ptr()], [self.out.data_ptr()]
         else:
@@ -241,15 +250,25 @@ class DeviceRunner:
             mine = (self.ctx.ipc_handle(self._x_raw), self.ctx.ipc_handle(self._out_raw))
             allh = self.exchange_handles(mine)
             xs, outs = [], []
-            for r, (hx, ho) in enumerate(allh):
-                if r == rank:
-                    xs.append(self._x_raw)
-                    outs.append(self._out_raw)
-                else:
-                    xs.append(self.ctx.ipc_open(hx))
-                    outs.append(self.ctx.ipc_open(ho))
-                    self._opened += [xs[-1], outs[-1]]
+            ok = True
+            try:
+                for r, (hx, ho) in enumerate(allh):
+                    if r == rank:
+                        xs.append(self._x_raw)
+                        outs.append(self._out_raw)
+                    else:
+                        xs.append(self.ctx.ipc_open(hx))
+                        self._opened.append(xs[-1])
+                        outs.append(self.ctx.ipc_open(ho))
+                        self._opened.append(outs[-1])
+            except Exception:  # noqa: BLE001 -- reported through `agree`
+                ok = False
+            if agree is not None:
+                ok = agree(ok)
+            if not ok:
+                raise RuntimeError("peer-memory split: CUDA IPC mapping failed on at least one rank")
         self.ctx.split_p2p_setup(world, rank, xs, outs)
+        self._p2p_key, self._p2p_xs, self._p2p_outs = key, xs, outs
 
     def block_p2p(self, b, x):
         self.ctx.split_block_p2p(b, x.data_ptr() if hasattr(x, "data_ptr") else int(x))
