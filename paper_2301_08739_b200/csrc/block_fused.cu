@@ -98,7 +98,7 @@ FWA_DEVINL uint32_t xs_off(int r, int chunk) {  // byte offset of the 16 B chunk
     return static_cast<uint32_t>((chunk >> 3) * kXSBlock + r * 128 + (((chunk & 7) ^ (r & 7)) << 4));
 }
 #ifndef FWA_X_TMA
-#define FWA_X_TMA 0  // 1: x rows by TMA tile::gather4 (measured slower: 0.582 vs 0.570 ms/frame F60), 0: cp.async, same layout
+#define FWA_X_TMA 0  // x rows by 0: cp.async, 1: TMA tile::gather4, 2: gather4 for channels 0-63 + cp.async (same layout; measured F60 0.555 / 0.572 / 0.578 ms/frame)
 #endif
 constexpr int kRXBytes = 60928;
 constexpr int kKVPitch = 528;                   // 8 x 32 B K | 8 x 32 B V | 16 B pad
@@ -902,32 +902,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
             static_assert(kThreads == 512, "the gather4 path is written for 16 warps");
             // lanes 0, 8, 16, 24 hold the ids of rows warp*4 + 0..3 (ids[0]) and 64 + warp*4 + 0..3
             // (ids[1]); rows past the CTA's are id 0 (any valid row: never stored).  Lane
-            // hf*4 + cb issues the gather4 of half hf, column block cb: 8 TMA per warp, 64 KB per CTA
-            if (threadIdx.x == 0) mbar_arrive_expect_tx(bX, 4 * kXSBlock);
+            // hf*NB + cb issues the gather4 of half hf, column block cb (FWA_X_TMA 1: all four
+            // blocks, 64 KB per CTA; 2: blocks 0-1 by TMA, 2-3 by cp.async)
+            constexpr int NB = FWA_X_TMA == 2 ? 2 : 4;
+            if (threadIdx.x == 0) mbar_arrive_expect_tx(bX, NB * kXSBlock);
             int rid[2][4];
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf)
 #pragma unroll
                 for (int k = 0; k < 4; ++k) rid[hf][k] = __shfl_sync(0xffffffffu, ids[hf], 8 * k);
-            if (lane < 8) {
-                const int hf = lane >> 2, cb = lane & 3;
+            if (lane < 2 * NB) {
+                const int hf = lane / NB, cb = lane % NB;
                 fence_proxy_async_smem();  // earlier generic accesses to the region before the async writes
                 tma_gather4(sXS + cb * kXSBlock + (hf * 64 + warp * 4) * 128, &a.xmap, smem_u32(bX), cb * 32,
                             rid[hf][0], rid[hf][1], rid[hf][2], rid[hf][3]);
             }
-#else
+#endif
+#if FWA_X_TMA != 1
             const int64_t ub = static_cast<int64_t>(u) * R;
             const int ur = static_cast<int>(a.rows - ub < R ? a.rows - ub : R);
             const int sp = a.split < ur ? a.split : ur;
             const int nl = rank ? ur - sp : sp;
             const int sub = lane & 7;
+            constexpr int i0 = FWA_X_TMA == 2 ? 2 : 0;
 #pragma unroll
             for (int hf = 0; hf < kPasses; ++hf) {
                 const int r = hf * kRowsPass + warp * 4 + (lane >> 3);
                 const float* src = a.x + static_cast<int64_t>(ids[hf]) * 128 + 4 * sub;
                 const uint32_t nb = r < nl ? 16u : 0u;
 #pragma unroll
-                for (int i = 0; i < 4; ++i) cp_async16(sXS + xs_off(r, 8 * i + sub), src + 32 * i, nb);
+                for (int i = i0; i < 4; ++i) cp_async16(sXS + xs_off(r, 8 * i + sub), src + 32 * i, nb);
             }
             cp_async_commit();
 #endif
@@ -1044,7 +1048,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_block
             unit_ids(a.ridx, u + npairs, gid);
 #if FWA_X_TMA
             mbar_wait(bX, ph);  // this unit's rows landed (TMA bytes)
-#else
+#endif
+#if FWA_X_TMA != 1
             cp_async_wait_all();
             __syncthreads();  // every thread's row chunks landed
 #endif
@@ -1645,7 +1650,7 @@ bool launch_block_fused(const float* x, const double* x64, const __half* pe16, c
     a.lmax = 0x1p64f;
     if (const char* e = std::getenv("FWA_B200_ATTN_LMAX")) a.lmax = std::strtof(e, nullptr);  // tests
     const bool f64 = x64 != nullptr;
-    if (!f64 && FWA_X_TMA) {  // one encode per distinct row buffer (host, ~1 us)
+    if (!f64 && FWA_X_TMA != 0) {  // one encode per distinct row buffer (host, ~1 us)
         static thread_local const float* last = nullptr;
         static thread_local CUtensorMap last_map;
         if (x != last) {
