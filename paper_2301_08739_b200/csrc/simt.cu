@@ -278,16 +278,20 @@ void launch_gemm_f32(const GemmArgs& a, GemmEpi epi, cudaStream_t s, int64_t* la
 }
 
 // ------------------------------------------------------------------ attention fp32
-// One CTA per (group, head); K/V of the head staged in shared memory when they
-// fit, one thread per query row; logits recomputed in a second pass instead of
-// materialising the G x G matrix (the reference's O(G) cache-free path).
+// One CTA per (group, head); K/V of the head staged in shared memory when they fit, one
+// thread per query row with its query and output row in registers (HD = head dim as a
+// template; any other width takes the generic body with the rows in memory); the logits
+// are recomputed in a second pass instead of materialising the G x G matrix (the
+// reference's O(G) cache-free path, kernels.hpp:512-548: max-subtracted softmax, the same
+// fp32 operation order).
 
+template <int HD>
 __global__ void __launch_bounds__(128) k_attention_f32(const float* __restrict__ qkv, int G, int d,
                                                        int heads, float* __restrict__ cat,
                                                        bool stage) {
     extern __shared__ float sm[];
     const int grp = blockIdx.x, head = blockIdx.y;
-    const int hd = d / heads;
+    const int hd = HD > 0 ? HD : d / heads;
     const int64_t base = static_cast<int64_t>(grp) * G;
     const int off = head * hd;
     const float scale = 1.0f / sqrtf(static_cast<float>(hd));
@@ -302,28 +306,60 @@ __global__ void __launch_bounds__(128) k_attention_f32(const float* __restrict__
         __syncthreads();
     }
     for (int i = threadIdx.x; i < G; i += blockDim.x) {
-        const float* q = qkv + (base + i) * 3 * d + off;
-        float mx = -INFINITY;
-        for (int j = 0; j < G; ++j) {
-            const float* kj = stage ? Ks + j * hd : qkv + (base + j) * 3 * d + d + off;
-            float acc = 0.f;
-            for (int c = 0; c < hd; ++c) acc = fmaf(q[c], kj[c], acc);
-            mx = fmaxf(mx, acc * scale);
+        const float* qg = qkv + (base + i) * 3 * d + off;
+        float* og = cat + (base + i) * d + off;
+        if constexpr (HD > 0) {
+            float q[HD], o[HD];
+#pragma unroll
+            for (int c = 0; c < HD; ++c) {
+                q[c] = qg[c];
+                o[c] = 0.f;
+            }
+            float mx = -INFINITY;
+            for (int j = 0; j < G; ++j) {
+                const float* kj = stage ? Ks + j * HD : qkv + (base + j) * 3 * d + d + off;
+                float acc = 0.f;
+#pragma unroll
+                for (int c = 0; c < HD; ++c) acc = fmaf(q[c], kj[c], acc);
+                mx = fmaxf(mx, acc * scale);
+            }
+            float sum = 0.f;
+            for (int j = 0; j < G; ++j) {
+                const float* kj = stage ? Ks + j * HD : qkv + (base + j) * 3 * d + d + off;
+                const float* vj = stage ? Vs + j * HD : qkv + (base + j) * 3 * d + 2 * d + off;
+                float acc = 0.f;
+#pragma unroll
+                for (int c = 0; c < HD; ++c) acc = fmaf(q[c], kj[c], acc);
+                const float p = expf(acc * scale - mx);
+                sum += p;
+#pragma unroll
+                for (int c = 0; c < HD; ++c) o[c] = fmaf(p, vj[c], o[c]);
+            }
+            const float inv = 1.0f / sum;
+#pragma unroll
+            for (int c = 0; c < HD; ++c) og[c] = o[c] * inv;
+        } else {
+            float mx = -INFINITY;
+            for (int j = 0; j < G; ++j) {
+                const float* kj = stage ? Ks + j * hd : qkv + (base + j) * 3 * d + d + off;
+                float acc = 0.f;
+                for (int c = 0; c < hd; ++c) acc = fmaf(qg[c], kj[c], acc);
+                mx = fmaxf(mx, acc * scale);
+            }
+            float sum = 0.f;
+            for (int c = 0; c < hd; ++c) og[c] = 0.f;
+            for (int j = 0; j < G; ++j) {
+                const float* kj = stage ? Ks + j * hd : qkv + (base + j) * 3 * d + d + off;
+                const float* vj = stage ? Vs + j * hd : qkv + (base + j) * 3 * d + 2 * d + off;
+                float acc = 0.f;
+                for (int c = 0; c < hd; ++c) acc = fmaf(qg[c], kj[c], acc);
+                const float p = expf(acc * scale - mx);
+                sum += p;
+                for (int c = 0; c < hd; ++c) og[c] = fmaf(p, vj[c], og[c]);
+            }
+            const float inv = 1.0f / sum;
+            for (int c = 0; c < hd; ++c) og[c] *= inv;
         }
-        float sum = 0.f;
-        float* o = cat + (base + i) * d + off;
-        for (int c = 0; c < hd; ++c) o[c] = 0.f;
-        for (int j = 0; j < G; ++j) {
-            const float* kj = stage ? Ks + j * hd : qkv + (base + j) * 3 * d + d + off;
-            const float* vj = stage ? Vs + j * hd : qkv + (base + j) * 3 * d + 2 * d + off;
-            float acc = 0.f;
-            for (int c = 0; c < hd; ++c) acc = fmaf(q[c], kj[c], acc);
-            const float p = expf(acc * scale - mx);
-            sum += p;
-            for (int c = 0; c < hd; ++c) o[c] = fmaf(p, vj[c], o[c]);
-        }
-        const float inv = 1.0f / sum;
-        for (int c = 0; c < hd; ++c) o[c] *= inv;
     }
 }
 
@@ -335,7 +371,14 @@ void launch_attention_f32(const float* qkv, int64_t rows, int G, int d, int head
     const size_t smem = 2ull * G * hd * sizeof(float);
     const bool stage = smem <= 48 * 1024;
     dim3 grid(static_cast<unsigned>(n_groups), static_cast<unsigned>(heads));
-    k_attention_f32<<<grid, 128, stage ? smem : 0, s>>>(qkv, G, d, heads, cat, stage);
+    const size_t sb = stage ? smem : 0;
+    switch (hd) {
+        case 4: k_attention_f32<4><<<grid, 128, sb, s>>>(qkv, G, d, heads, cat, stage); break;
+        case 8: k_attention_f32<8><<<grid, 128, sb, s>>>(qkv, G, d, heads, cat, stage); break;
+        case 16: k_attention_f32<16><<<grid, 128, sb, s>>>(qkv, G, d, heads, cat, stage); break;
+        case 32: k_attention_f32<32><<<grid, 128, sb, s>>>(qkv, G, d, heads, cat, stage); break;
+        default: k_attention_f32<0><<<grid, 128, sb, s>>>(qkv, G, d, heads, cat, stage); break;
+    }
     ++*launches;
 }
 
