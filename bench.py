@@ -179,6 +179,19 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
+def summarize_protocol(samples, runs, warmup):
+    """The reference's summary (bench.hpp:85-143) through the package's restatement, which
+    tests/test_host.py pins bit-identical to the compiled reference: samples outside
+    [q1 - 3 IQR, q3 + 3 IQR] dropped, mean / p50 / p95 of the rest."""
+    from paper_2301_08739_b200 import benchcli
+    r = benchcli.summarize("backbone_forward", 0, "", list(samples), runs, warmup)
+    w = r["wall_time_ms"]
+    return {"runs": runs, "warmup": warmup, "outliers_excluded": r["outliers_excluded"],
+            "mean_ms": w["mean"], "p50_ms": w["p50"], "p95_ms": w["p95"], "min_ms": min(samples),
+            "rule": "bench.hpp:85-143 (3 x IQR exclusion, linear-interpolation percentiles); device time "
+                    "of one forward per run (CUDA events), L2 flushed before each"}
+
+
 def _cpu_model():
     try:
         for l in open("/proc/cpuinfo"):
@@ -300,6 +313,20 @@ def run_ours(args, rank, world, local_rank, dist):
         eager_ev[i][1].record(stream)
     torch.cuda.synchronize()
     eager_ms = sum(a.elapsed_time(b) for a, b in eager_ev) / args.steps
+    # the reference's own timing protocol (bench.hpp:85-143: 50 runs after 10 warm-up runs,
+    # samples beyond 3 x IQR excluded, mean / p50 / p95 of the rest), per run the device time
+    # of one forward (CUDA events, inputs resident, L2 flushed before each run)
+    proto_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(50)]
+    for _ in range(10):
+        flush.zero_()
+        step()
+    for a, b in proto_ev:
+        flush.zero_()
+        a.record(stream)
+        step()
+        b.record(stream)
+    torch.cuda.synchronize()
+    protocol = summarize_protocol([a.elapsed_time(b) for a, b in proto_ev], 50, 10)
     # ---------------------------------------------------------------- e2e via the host API
     pin = dict(pin_memory=True)
     h_coords = torch.from_numpy(ps.coords).pin_memory()
@@ -482,6 +509,7 @@ def run_ours(args, rank, world, local_rank, dist):
         "clocks": clk,
         "kernels": kernels,
         "stage_timed_ms_per_step": prof_ms / args.steps,
+        "protocol": protocol,
         "eager": {"ms_per_frame": eager_ms, "pillars_per_s": n / (eager_ms / 1e3),
                   "note": "fwa_b200_backbone_forward_device enqueued eagerly every call (six rotating "
                           "output buffers defeat the CUDA-graph cache), device time, L2 flushed"},
