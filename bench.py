@@ -406,6 +406,9 @@ def run_ours(args, rank, world, local_rank, dist):
     f250 = None
     if world == 1 and not args.no_sweep:
         f250 = secondary(run_f250_frame, args, F, ctx, cfg, dev, stream, flush)
+    check = None
+    if world == 1 and not args.no_sweep:
+        check = secondary(run_check_mode, F, cfg, blob, d_coords, d_feats, n, dev, stream, flush)
 
     # ---------------------------------------------------------------- reduce over ranks
     t_dev = torch.tensor([dev_ms, e2e_stream_s, float(n), float(nk), e2e_s], dtype=torch.float64, device=dev)
@@ -523,6 +526,7 @@ def run_ours(args, rank, world, local_rank, dist):
         "config4_split": split,
         "config5_sweep": sweep,
         "f250_frame": f250,
+        "check_mode": check,
     }
     print(json.dumps(line), flush=True)
 
@@ -654,6 +658,30 @@ def run_f250_frame(args, F, ctx, cfg, dev, stream, flush):
     return {"workload": "F250 scene (255,066 pillars) as one frame, 8 blocks", "pillars": n, "ms_per_frame": ms,
             "pillars_per_s": n / (ms / 1e3), "schedule": schedule_object(prof["schedule"], n),
             "block_kernel_ms": prof["block_fused"] / cfg.n_blocks}
+
+
+def run_check_mode(F, cfg, blob, d_coords, d_feats, n, dev, stream, flush):
+    """The fp32 check mode (FWA_PREC_FP32: SIMT fp32 kernels, parity <= 1e-4) on the
+    headline F60 frame: device-resident forward, L2 flushed, median of 5."""
+    import torch
+    ctx32 = F.Context(dev.index, stream=stream.cuda_stream, precision="fp32")
+    ctx32.load_params(cfg, blob)
+    d_out = torch.empty((n, cfg.d_model), dtype=torch.float32, device=dev)
+    fn = lambda: ctx32.forward_device(d_coords.data_ptr(), d_feats.data_ptr(), [0, n], cfg, d_out.data_ptr())
+    flush.zero_()
+    fn()
+    ts = []
+    for _ in range(5):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ms = float(np.median(ts))
+    return {"workload": "F60 frame, 8 blocks, fp32 check mode (SIMT fp32, tolerance 1e-4)", "ms_per_frame": ms,
+            "pillars_per_s": n / (ms / 1e3), "dtype": "f32"}
 
 
 def run_batch_frames(args, F, ctx, cfg, dev, stream, rank, world, dist, flush):
