@@ -593,7 +593,8 @@ FWA_DEVINL void ln1_row_to_image(const float (&v)[16], const uint2 (&ph)[4], boo
     sm += __shfl_xor_sync(0xffffffffu, sm, 4);
     // a non-finite input makes the row sum non-finite; only then look at the values (a
     // finite row whose sum overflows is not an error, as in the reference)
-    if (!isfinite(sm)) {
+    // (a warp-uniform branch: predicated, the 16 checks would cost every row)
+    if (__any_sync(0xffffffffu, !isfinite(sm))) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) bad |= !isfinite(v[j]);
     }
@@ -642,12 +643,14 @@ FWA_DEVINL void ln1_rows2_to_image(const float (&v)[2][16], const uint2 (&ph)[2]
         sm[0] += t0;
         sm[1] += t1;
     }
+    // a non-finite input makes the row sum non-finite; only then look at the values (a
+    // warp-uniform branch: predicated, the 32 checks would cost every row)
+    if (__any_sync(0xffffffffu, !isfinite(sm[0]) || !isfinite(sm[1]))) {
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
-        if (!isfinite(sm[h])) {  // a non-finite input makes the row sum non-finite
+        for (int h = 0; h < 2; ++h)
 #pragma unroll
-            for (int j = 0; j < 16; ++j) bad |= !isfinite(v[h][j]);
-        }
+            for (int j = 0; j < 16; ++j) bad |= !isfinite(sm[h]) && !isfinite(v[h][j]);
+    }
     const float mean[2] = {sm[0] * (1.0f / 128.0f), sm[1] * (1.0f / 128.0f)};
     float sq[2] = {0.f, 0.f};
 #pragma unroll
