@@ -43,13 +43,16 @@ __global__ void k_positional_embedding(const double* __restrict__ coords, int64_
 // c = ch + cl as float pairs, t = p + e where p = Fh ch (e = its exact FMA residual plus
 // the cross terms); p is reduced EXACTLY mod 2 in fp32 (|p| < 2^22), then the SFU's
 // sin / cos of pi r.  |err| < 1e-6, far below the fp16 rounding (2^-12) of the stored value.
+template <int GR>
 __global__ void k_pe_fp16(const double* __restrict__ coords, int64_t n, int nf, const float2* __restrict__ F,
                           __half* __restrict__ pe16) {
     // one thread per (row, axis, 4 frequencies): consecutive threads write consecutive 16 B
-    // of the fp16 PE rows (every store instruction fills whole 128 B lines)
-    const int groups = nf >> 2;  // nf % 4 == 0
+    // of the fp16 PE rows (every store instruction fills whole 128 B lines).  GR: the
+    // frequency groups per axis at compile time (8 for D = 128: the index split is a shift;
+    // a runtime 64-bit division would cost more than the row's arithmetic)
+    const int groups = GR > 0 ? GR : nf >> 2;  // nf % 4 == 0
     const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t ra = t / groups;  // row * 2 + axis
+    const int64_t ra = GR > 0 ? t / GR : t / groups;  // row * 2 + axis
     const int k0 = static_cast<int>(t - ra * groups) * 4;
     const int64_t i = ra >> 1;
     const int axis = static_cast<int>(ra & 1);
@@ -115,7 +118,11 @@ void launch_positional_embedding(const double* coords, int64_t n, int d, const d
                                  float* pe, __half* pe16, cudaStream_t s, int64_t* launches) {
     if (!pe && pe16 && (d / 4) % 4 == 0) {  // d_freq holds [nf doubles | nf float2 (2f hi, lo)]
         const int nf = d / 4;
-        k_pe_fp16<<<static_cast<unsigned>((2 * n * (nf / 4) + 255) / 256), 256, 0, s>>>(
+        if (nf == 32)
+            k_pe_fp16<8><<<static_cast<unsigned>((2 * n * (nf / 4) + 255) / 256), 256, 0, s>>>(
+            coords, n, nf, reinterpret_cast<const float2*>(d_freq + nf), pe16);
+        else
+            k_pe_fp16<0><<<static_cast<unsigned>((2 * n * (nf / 4) + 255) / 256), 256, 0, s>>>(
             coords, n, nf, reinterpret_cast<const float2*>(d_freq + nf), pe16);
         ++*launches;
         return;
