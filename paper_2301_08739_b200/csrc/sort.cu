@@ -315,36 +315,50 @@ __global__ void __launch_bounds__(256) k_frame_minmax(const long long* __restric
     if (threadIdx.x < 32) sm[threadIdx.x >> 2][threadIdx.x & 3] = (threadIdx.x & 1) ? LLONG_MIN : LLONG_MAX;
     if (threadIdx.x == 0) f0 = n_frames > 1 && c0 < ntot ? frame_of(frame_off, n_frames, c0) : 0;
     __syncthreads();
+    // per-thread running extremes of the current frame in registers (a CTA's chunk spans one
+    // or two frames at batch scale), flushed into the slots only when the frame changes;
+    // four rows' loads in flight per thread
     int f = f0;
-    for (int64_t t0 = c0; t0 < c1; t0 += blockDim.x) {
-        const int64_t i = t0 + threadIdx.x;
-        const bool in = i < c1;
-        longlong2 w = make_longlong2(0, 0);
-        if (in) {
-            w = reinterpret_cast<const longlong2*>(win)[static_cast<int64_t>(s) * ntot + i];
-            while (f + 1 < n_frames && frame_off[f + 1] <= i) ++f;
+    int64_t next_b = f + 1 < n_frames ? frame_off[f + 1] : INT64_MAX;
+    int fc = -1;
+    long long a0 = LLONG_MAX, a1 = LLONG_MIN, a2 = LLONG_MAX, a3 = LLONG_MIN;
+    auto flush = [&]() {
+        if (fc < 0) return;
+        const int k = fc - f0;
+        long long* m = k < 8 ? sm[k] : mm + (static_cast<int64_t>(s) * n_frames + fc) * 4;
+        atomicMin(m, a0);
+        atomicMax(m + 1, a1);
+        atomicMin(m + 2, a2);
+        atomicMax(m + 3, a3);
+        a0 = LLONG_MAX, a1 = LLONG_MIN, a2 = LLONG_MAX, a3 = LLONG_MIN;
+    };
+    const longlong2* ws = reinterpret_cast<const longlong2*>(win) + static_cast<int64_t>(s) * ntot;
+    for (int64_t t0 = c0 + threadIdx.x; t0 < c1; t0 += 4 * blockDim.x) {
+        longlong2 w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t i = t0 + u * blockDim.x;
+            w[u] = i < c1 ? ws[i] : make_longlong2(0, 0);
         }
-        const int fl = in ? f : -1;
-        const int f_lane0 = __shfl_sync(0xffffffffu, fl, 0);
-        if (__all_sync(0xffffffffu, in && fl == f_lane0)) {
-            const long long a0 = wmin(w.x), a1 = wmax(w.x), a2 = wmin(w.y), a3 = wmax(w.y);
-            if ((threadIdx.x & 31) == 0) {
-                const int k = fl - f0;
-                long long* m = k < 8 ? sm[k] : mm + (static_cast<int64_t>(s) * n_frames + fl) * 4;
-                atomicMin(m, a0);
-                atomicMax(m + 1, a1);
-                atomicMin(m + 2, a2);
-                atomicMax(m + 3, a3);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t i = t0 + u * blockDim.x;
+            if (i >= c1) break;
+            while (next_b <= i) {
+                ++f;
+                next_b = f + 1 < n_frames ? frame_off[f + 1] : INT64_MAX;
             }
-        } else if (in) {
-            const int k = fl - f0;
-            long long* m = k < 8 ? sm[k] : mm + (static_cast<int64_t>(s) * n_frames + fl) * 4;
-            atomicMin(m, w.x);
-            atomicMax(m + 1, w.x);
-            atomicMin(m + 2, w.y);
-            atomicMax(m + 3, w.y);
+            if (f != fc) {
+                flush();
+                fc = f;
+            }
+            a0 = w[u].x < a0 ? w[u].x : a0;
+            a1 = w[u].x > a1 ? w[u].x : a1;
+            a2 = w[u].y < a2 ? w[u].y : a2;
+            a3 = w[u].y > a3 ? w[u].y : a3;
         }
     }
+    flush();
     __syncthreads();
     if (threadIdx.x < 32) {
         const int k = threadIdx.x >> 2, q = threadIdx.x & 3;
