@@ -1,0 +1,5 @@
+# bound: out-proj MMAs removed (op0) or halved (op4) -- wrong numerics, timing only
+for r in 1 2 3; do
+  for v in op0 op4; do echo -n "$v "; FWA_B200_LIB=$PWD/paper_2301_08739_b200/libfwa_b200_p$v.so python tools/ab_time.py 40 2>&1 | tail -1; done
+  echo -n "base "; python tools/ab_time.py 40 2>&1 | tail -1
+done
