@@ -72,7 +72,7 @@ struct fwa_b200_ctx {
     cudaStream_t copy = nullptr;             // host API: feature H2D overlaps the schedule
     cudaEvent_t ev_copy = nullptr, ev_feats = nullptr;
     cudaStream_t d2h = nullptr;              // pipelined frames: outputs back while the next computes
-    cudaEvent_t fr_ev[8] = {};
+    cudaEvent_t fr_ev[10] = {};
     int* h_fr_flags = nullptr;               // pinned, 2 ints per frame
     size_t h_fr_cap = 0;
     int* d_flag = nullptr;     // [0] non-finite input, [1] window-bin capacity overflow
@@ -1256,12 +1256,13 @@ void forward_frames(fwa_b200_ctx* c, int F, const double* const* coords, const v
     unsigned long long* d_phase = ws<unsigned long long>(c, "phase_acc", 4 * static_cast<size_t>(F) * cfg->n_blocks);
     if (!c->d2h) CUDA_OK(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
     for (auto* e : {&c->fr_ev[0], &c->fr_ev[1], &c->fr_ev[2], &c->fr_ev[3], &c->fr_ev[4], &c->fr_ev[5],
-                    &c->fr_ev[6], &c->fr_ev[7]})
+                    &c->fr_ev[6], &c->fr_ev[7], &c->fr_ev[8], &c->fr_ev[9]})
         if (!*e) CUDA_OK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     cudaEvent_t* ev_inc = c->fr_ev;      // [2] coordinates landed
     cudaEvent_t* ev_inf = c->fr_ev + 2;  // [2] features landed
     cudaEvent_t* ev_done = c->fr_ev + 4; // [2] frame computed (inputs free, outputs ready)
     cudaEvent_t* ev_out = c->fr_ev + 6;  // [2] outputs copied back (slot free)
+    cudaEvent_t* ev_in_free = c->fr_ev + 8;  // [2] the frame's kernels enqueued past their inputs
     if (c->h_fr_cap < static_cast<size_t>(F)) {
         if (c->h_fr_flags) CUDA_OK(cudaFreeHost(c->h_fr_flags));
         c->h_fr_flags = nullptr;
@@ -1283,7 +1284,9 @@ void forward_frames(fwa_b200_ctx* c, int F, const double* const* coords, const v
     for (int f = 0; f < F; ++f) {
         const int s = f & 1;
         const size_t nf = static_cast<size_t>(n[f]);
-        if (f >= 2) CUDA_OK(cudaStreamWaitEvent(c->copy, ev_done[s], 0));
+        // the slot's inputs are free once the frame's kernels are done with them -- not after
+        // its small device-to-host copies, which queue behind the previous frame's output copy
+        if (f >= 2) CUDA_OK(cudaStreamWaitEvent(c->copy, ev_in_free[s], 0));
         CUDA_OK(cudaMemcpyAsync(in_c[s], coords[f], nf * 16, cudaMemcpyHostToDevice, c->copy));
         CUDA_OK(cudaEventRecord(ev_inc[s], c->copy));
         CUDA_OK(cudaMemcpyAsync(in_f[s], feats[f], nf * fin * esz, cudaMemcpyHostToDevice, c->copy));
@@ -1301,6 +1304,7 @@ void forward_frames(fwa_b200_ctx* c, int F, const double* const* coords, const v
         const float* x32 = c->proj_in > 0 ? in_p[s] : (f64 ? nullptr : static_cast<const float*>(in_f[s]));
         const double* x64 = c->proj_in > 0 || !f64 ? nullptr : static_cast<const double*>(in_f[s]);
         forward_device(c, in_c[s], x32, x64, cfg, S, o_f[s], nullptr, nullptr, ev_inf[s]);
+        CUDA_OK(cudaEventRecord(ev_in_free[s], st));
         c->rec = nullptr;
         K[f] = S.K;
         nd[f] = S.n_drop;
