@@ -817,6 +817,7 @@ void launch_spec_compact(const int32_t* sorted, int64_t total, const uint8_t* dr
 //   kept_rank(id)        = id - #{dropped ids < id}
 //   compact position(j)  = j  - #{dropped positions < j}   (per spec)
 
+constexpr int kSmemDrops = 1024;  // k_compact_all: drop tables staged in shared memory up to this
 FWA_DEVINL int count_less(const int32_t* a, int n, int32_t v) {
     int lo = 0, hi = n;
     while (lo < hi) {
@@ -931,31 +932,47 @@ __global__ void __launch_bounds__(256) k_compact_all(const int32_t* __restrict__
     const int64_t base = plan ? static_cast<int64_t>(s) * ntot : 0;  // drop_pos holds stacked plan indices
     const int32_t* dl = plan ? drop_pos + static_cast<int64_t>(s) * (n_drop > 0 ? n_drop : 1) : drop_sorted;
     __shared__ int s_lo, s_f0;
-    if (threadIdx.x < 32) {  // warp 0: 32-way searches (a few dependent loads, not log2 n)
-        if (n_drop > 0) {
-            const int lo = warp_count_less(dl, n_drop, static_cast<int32_t>(base + j0));
-            if (threadIdx.x == 0) s_lo = lo;
-        } else if (threadIdx.x == 0) {
-            s_lo = 0;
+    // up to kSmemDrops drops (single frames: < G): this table, and for out_pos the sorted drop
+    // ids, are staged in shared memory and every thread binary-searches there (no dependent
+    // L2 loads); larger tables (frame batches) use the warp search + walk in global memory
+    __shared__ int32_t s_dl[kSmemDrops], s_ds[kSmemDrops];
+    const bool staged = n_drop <= kSmemDrops;
+    const bool need_out = plan && s == s_last;
+    if (staged) {
+        for (int i = threadIdx.x; i < n_drop; i += blockDim.x) {
+            s_dl[i] = dl[i];
+            if (need_out) s_ds[i] = drop_sorted[i];
         }
         if (threadIdx.x == 0)
-            s_f0 = plan && s == s_last && n_frames > 1 ? frame_of(frame_off, n_frames, j0 < ntot ? j0 : ntot - 1) : 0;
+            s_f0 = need_out && n_frames > 1 ? frame_of(frame_off, n_frames, j0 < ntot ? j0 : ntot - 1) : 0;
+    } else if (threadIdx.x < 32) {  // warp 0: 32-way searches (a few dependent loads, not log2 n)
+        const int lo = warp_count_less(dl, n_drop, static_cast<int32_t>(base + j0));
+        if (threadIdx.x == 0) {
+            s_lo = lo;
+            s_f0 = need_out && n_frames > 1 ? frame_of(frame_off, n_frames, j0 < ntot ? j0 : ntot - 1) : 0;
+        }
     }
     __syncthreads();
     if (j >= ntot) return;
-    int lb = s_lo;
-    while (lb < n_drop && dl[lb] < base + j) ++lb;
-    if (lb < n_drop && dl[lb] == base + j) return;  // dropped (block 0's tail of its frame)
+    int lb;
+    if (staged) {
+        lb = count_less(s_dl, n_drop, static_cast<int32_t>(base + j));
+        if (lb < n_drop && s_dl[lb] == base + j) return;  // dropped (block 0's tail of its frame)
+    } else {
+        lb = s_lo;
+        while (lb < n_drop && dl[lb] < base + j) ++lb;
+        if (lb < n_drop && dl[lb] == base + j) return;
+    }
     const int64_t c = j - lb;
     if (plan) {
         const int32_t id = sorted[base + j];
         idx[static_cast<int64_t>(s) * K + c] = id;
-        if (s == s_last) {
+        if (need_out) {
             int f = s_f0;
             while (f + 1 < n_frames && frame_off[f + 1] <= j) ++f;
             const int d0 = n_frames > 1 ? static_cast<int>(drop_off[f]) : 0;
             const int d1 = n_frames > 1 && f + 1 < n_frames ? static_cast<int>(drop_off[f + 1]) : n_drop;
-            out_pos[c] = id - d0 - count_less(drop_sorted + d0, d1 - d0, id);
+            out_pos[c] = id - d0 - count_less((staged ? s_ds : drop_sorted) + d0, d1 - d0, id);
         }
     } else {
         kept_rank[j] = static_cast<uint32_t>(c);
