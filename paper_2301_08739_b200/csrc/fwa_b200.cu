@@ -796,11 +796,14 @@ void build_schedule_body(fwa_b200_ctx* c, const double* d_coords, const fwa_conf
         const int nd = static_cast<int>(S.n_drop);
         int32_t* drop_sorted = ws<int32_t>(c, "drop_sorted", static_cast<size_t>(nd) + 1);
         int32_t* drop_pos = ws<int32_t>(c, "drop_pos", static_cast<size_t>(nd + 1) * n_specs);
-        if (nd > 0)
+        // one frame with few drops: compaction builds the tables itself (one launch fewer)
+        const bool fuse = nf == 1 && nd <= kFuseDrops;
+        if (nd > 0 && !fuse)
             launch_drop_tables(S.sorted, nd, d_off, d_rows, d_drop_off, nf, S.sorted_inv, ntot, n_specs,
                                S.dropped_ids, drop_sorted, drop_pos, st, &c->launches);
         launch_compact_all(S.sorted, ntot, n_specs, d_off, d_drop_off, nf, drop_sorted, drop_pos, nd, S.K, s_last, S.idx,
-                           S.kept_rank, S.kept_ids, S.out_pos, st, &c->launches);
+                           S.kept_rank, S.kept_ids, S.out_pos, st, &c->launches, fuse ? S.sorted_inv : nullptr,
+                           fuse ? S.dropped_ids : nullptr);
         check_launch();
         return;
     }

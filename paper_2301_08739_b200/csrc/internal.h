@@ -96,7 +96,8 @@ void launch_compact_all(const int32_t* sorted, int64_t ntot, int n_specs, const 
                         const int64_t* drop_off, int n_frames, const int32_t* drop_sorted,
                         const int32_t* drop_pos, int n_drop, int64_t K, int s_last, int32_t* idx,
                         uint32_t* kept_rank, int32_t* kept_ids, int32_t* out_pos, cudaStream_t s,
-                        int64_t* launches);
+                        int64_t* launches, const int32_t* fuse_inv = nullptr, int32_t* fuse_dropped_ids = nullptr);
+constexpr int kFuseDrops = 256;  // one frame with at most this many drops: the drop tables inside compaction
 
 // ------------------------------------------------------------------ schedule (backbone.hpp:236-316)
 void launch_drop_mark(const int32_t* sorted0, int64_t ntot, const int64_t* d_frame_off,

@@ -924,7 +924,9 @@ __global__ void __launch_bounds__(256) k_compact_all(const int32_t* __restrict__
                                                      const int32_t* __restrict__ drop_pos, int n_drop, int64_t K,
                                                      int s_last, int32_t* __restrict__ idx,
                                                      uint32_t* __restrict__ kept_rank,
-                                                     int32_t* __restrict__ kept_ids, int32_t* __restrict__ out_pos) {
+                                                     int32_t* __restrict__ kept_ids, int32_t* __restrict__ out_pos,
+                                                     const int32_t* __restrict__ fuse_inv,
+                                                     int32_t* __restrict__ fuse_dropped_ids) {
     const int s = static_cast<int>(blockIdx.y);
     const bool plan = s < n_specs;
     const int64_t j0 = static_cast<int64_t>(blockIdx.x) * blockDim.x;
@@ -938,7 +940,32 @@ __global__ void __launch_bounds__(256) k_compact_all(const int32_t* __restrict__
     __shared__ int32_t s_dl[kSmemDrops], s_ds[kSmemDrops];
     const bool staged = n_drop <= kSmemDrops;
     const bool need_out = plan && s == s_last;
-    if (staged) {
+    if (fuse_inv) {
+        // one frame, n_drop <= kFuseDrops: this CTA builds its own tables (no k_drop_tables
+        // launch) -- the dropped ids are spec 0's plan tail sorted[K, K + n_drop) (block 0
+        // drops its tail, flatten.hpp:134-146), the table of plan s their positions in it
+        // (inverse permutation), ranked by counting (distinct values)
+        __shared__ int32_t s_v[kFuseDrops], s_id[kFuseDrops];
+        int32_t v = 0, id = 0;
+        if (static_cast<int>(threadIdx.x) < n_drop) {
+            id = sorted[K + threadIdx.x];
+            if (!plan && blockIdx.x == 0 && fuse_dropped_ids) fuse_dropped_ids[threadIdx.x] = id;  // tail order
+            v = plan ? fuse_inv[static_cast<int64_t>(s) * ntot + id] : id;
+            s_v[threadIdx.x] = v;
+            s_id[threadIdx.x] = id;
+        }
+        __syncthreads();
+        if (static_cast<int>(threadIdx.x) < n_drop) {
+            int r = 0, ri = 0;
+            for (int k = 0; k < n_drop; ++k) {
+                r += s_v[k] < v;
+                ri += s_id[k] < id;
+            }
+            s_dl[r] = v;
+            if (need_out) s_ds[ri] = id;
+        }
+        if (threadIdx.x == 0) s_f0 = 0;
+    } else if (staged) {
         for (int i = threadIdx.x; i < n_drop; i += blockDim.x) {
             s_dl[i] = dl[i];
             if (need_out) s_ds[i] = drop_sorted[i];
@@ -993,10 +1020,13 @@ void launch_compact_all(const int32_t* sorted, int64_t ntot, int n_specs, const 
                         const int64_t* drop_off, int n_frames, const int32_t* drop_sorted,
                         const int32_t* drop_pos, int n_drop, int64_t K, int s_last, int32_t* idx,
                         uint32_t* kept_rank, int32_t* kept_ids, int32_t* out_pos, cudaStream_t s,
-                        int64_t* launches) {
+                        int64_t* launches, const int32_t* fuse_inv, int32_t* fuse_dropped_ids) {
+    static_assert(kFuseDrops <= 256 && kFuseDrops <= kSmemDrops, "one value per thread of a 256-thread CTA");
+    if (fuse_inv && (n_frames != 1 || n_drop > kFuseDrops)) fuse_inv = nullptr;
     dim3 grid(static_cast<unsigned>((ntot + 255) / 256), static_cast<unsigned>(n_specs + 1));
     k_compact_all<<<grid, 256, 0, s>>>(sorted, ntot, n_specs, frame_off, drop_off, n_frames, drop_sorted, drop_pos,
-                                       n_drop, K, s_last, idx, kept_rank, kept_ids, out_pos);
+                                       n_drop, K, s_last, idx, kept_rank, kept_ids, out_pos, fuse_inv,
+                                       fuse_dropped_ids);
     ++*launches;
 }
 
