@@ -22,7 +22,7 @@ for r in rows:
     launches.append((d['Kernel Name'].split('(')[0][:70], v))
 if frame is not None:
     # a forward's first launch is its positional embedding (side stream, before the keys)
-    starts = [i for i, (k, _) in enumerate(launches) if k.startswith('k_pe_fp16')]
+    starts = [i for i, (k, _) in enumerate(launches) if 'k_pe_fp16' in k]
     bounds = list(zip(starts, starts[1:] + [len(launches)]))
     if frame < 0 and len(bounds) > 1:
         bounds = bounds[:-1]  # the last COMPLETE frame
